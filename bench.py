@@ -1,0 +1,357 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 hot path of the N-D Bartels–Stewart solver (BASELINE.json).
+
+One step = one full solve of the workload's Sylvester equation on the GPU: forward transform
+(N mode products with U_j^H), blocked triangular solve, inverse transform (N mode products
+with U_j). The host Schur factorisations are setup, computed once and timed separately
+(BASELINE.md 2). Metric: unknowns/s = P / step time (P = prod n_j).
+
+  value   device-resident: B already in HBM, K steps timed with CUDA events (max over ranks);
+  e2e     through the C-ABI host-buffer call nds_solve_schur (the reference-facing drop-in for
+          ndsylv::solve after its Schur step) from pinned host memory: plan creation + singular
+          check + H2D(B) + solve + D2H(X) inside the timed region every step;
+  roofline  dominant kernel (complex-FP64 DMMA mode-product GEMM), algorithmic FLOPs per launch
+          (8 P n_j, one CMAC = 8 real flops) over its CUDA-event launch time, against the FP64
+          DMMA peak measured on this pool (profiles/fp64_peaks_r01.json);
+  cpu_baseline  the reference CPU solver (oracle/_ref, built from /root/reference sources) on a
+          bounded slab sample of the same workload, rank 0 at N=1 only.
+
+--impl reference runs the reference's own CPU solver (oracle/_ref) the same way.
+Multi-GPU (torchrun): independent replicas of the workload, one per rank (weak scaling).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "unknowns/s (prod n_j/s), complex128"
+DEFAULT_CONFIG = "c1"  # configs[1] of BASELINE.json: N=3, n=256, 16.8M unknowns (fits one GPU)
+CPU_SAMPLE_DIMS = {"c0": (32, 32, 32), "c1": (256, 256, 32), "c2": (96, 96, 96, 8), "c3": (128, 128, 128, 4),
+                   "c4": (2,) * 21}
+
+
+def fp64_peak():
+    path = os.path.join(ROOT, "profiles", "fp64_peaks_r01.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["dmma_tflops_sustained"]), "measured on this pool: DMMA m8n8k4 microbenchmark (" + \
+            os.path.relpath(path, ROOT) + ")"
+    except Exception:
+        return 37.2, "nominal 148 SM x 64 FMA/clk x 2 x 1.965 GHz (no measured file)"
+
+
+def ncu_traffic(config):
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(config)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, device):
+        self.device = device
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.samples.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[4 + i].lower() == "active"})
+        pw = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "power_w_max": max(pw) if pw else None, "samples": len(self.samples)}
+
+
+def dist_init():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl" if os.environ.get("NDS_BENCH_BACKEND", "nccl") == "nccl" else "gloo")
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(world, value, device=None):
+    if world == 1:
+        return value
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def cpu_reference_sample(config, seed, threads):
+    """The reference CPU solver (oracle/_ref) on a bounded slab of the workload."""
+    import oracle
+    from paper_2412_15840_b200 import configs
+    ref = oracle.Ref()
+    ref.set_threads(threads)
+    dims = CPU_SAMPLE_DIMS[config]
+    a, b = configs.make_problem(config, seed=seed, dims=dims)
+    x, rep = ref.solve(a, b)
+    secs = rep["transform_seconds"] + rep["backsub_seconds"] + rep["inverse_seconds"]
+    p = int(np.prod(dims))
+    return p / secs, {"dims": list(dims), "P": p, "seconds_excl_schur": secs,
+                      "stage_seconds": {k: rep[k] for k in ("schur_seconds", "transform_seconds", "backsub_seconds",
+                                                            "inverse_seconds")}}
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    samples = []
+    info = None
+    for i in range(args.warmup + args.steps):
+        v, info = cpu_reference_sample(args.config, args.seed, threads)
+        if i >= args.warmup:
+            samples.append(v)
+    value = statistics.mean(samples)
+    dims = CPU_SAMPLE_DIMS[args.config]
+    sample = (f"reference ndsylv::solve (oracle/_ref, -O3 -fopenmp, no -march) on the {'x'.join(map(str, dims))} "
+              f"slab of {args.config} (P={info['P']}); rate = P / (transform+backsub+inverse s), Schur excluded")
+    line = {"metric": METRIC, "value": value, "unit": "unknowns/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": info["P"] / value * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic (generator v1)",
+            "impl": "reference",
+            "config": {"workload": args.config, "dims": list(dims), "sample_of": args.config},
+            "cpu_baseline": {"value": value, "unit": "unknowns/s", "cores": threads, "kind": "reference",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "unknowns/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "stage_seconds": info["stage_seconds"]}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=["c0", "c1", "c2", "c3", "c4"])
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--verify", action="store_true", help="device residual check after timing")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+
+    world, rank, local = dist_init()
+    if args.impl == "reference":
+        return run_reference(args, world, rank)
+
+    import torch
+    import paper_2412_15840_b200 as nds
+    from paper_2412_15840_b200 import configs
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    ctx = nds.Context(local)
+    stream = torch.cuda.current_stream(dev)
+    ctx.set_stream(stream.cuda_stream)
+
+    # --- inputs (host, generator v1) and host Schur setup -------------------------------------
+    a_list, b_host = configs.make_problem(args.config, seed=args.seed + rank)
+    dims = tuple(b_host.shape)
+    P = int(np.prod(dims))
+    t0 = time.perf_counter()
+    factors = [ctx.schur(a) for a in a_list]
+    schur_s = time.perf_counter() - t0
+    us = [f[0] for f in factors]
+    ts = [f[1] for f in factors]
+    plan = ctx.plan(us, ts)
+
+    flat = np.ascontiguousarray(b_host.ravel(order="F"))
+    pinned_b = torch.from_numpy(flat).pin_memory()
+    pinned_x = torch.empty_like(pinned_b).pin_memory()
+    d_b = pinned_b.to(dev, non_blocking=True)
+    d_x = torch.empty_like(d_b)
+    d_w = torch.empty_like(d_b)
+    torch.cuda.synchronize(dev)
+
+    # --- device-resident timing ----------------------------------------------------------------
+    for _ in range(args.warmup):
+        plan.execute(d_b.data_ptr(), d_x.data_ptr(), d_w.data_ptr())
+    torch.cuda.synchronize(dev)
+    launches_per_step = plan.launches()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    barrier(world)
+    torch.cuda.synchronize(dev)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            plan.execute(d_b.data_ptr(), d_x.data_ptr(), d_w.data_ptr())
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+    barrier(world)
+    ms_total = e0.elapsed_time(e1)
+    ms_total = max_over_ranks(world, ms_total, dev)
+    ms_step = ms_total / args.steps
+    value = world * P / (ms_step * 1e-3)
+
+    # --- per-launch profile of the same workload (separate pass, CUDA events per launch) -----
+    plan.profile_begin(launches_per_step * args.steps + 8)
+    for _ in range(args.steps):
+        plan.execute(d_b.data_ptr(), d_x.data_ptr(), d_w.data_ptr())
+    recs = plan.profile_end()
+    by_kind = {}
+    for kind, mode, ms in recs:
+        by_kind.setdefault(kind, []).append((mode, ms))
+    gemm = by_kind.get("transform_gemm", [])
+    peak_tf, peak_src = fp64_peak()
+    roofline = None
+    if gemm:
+        flops = [8.0 * P * dims[abs(m) - 1] for m, _ in gemm]
+        avg_ms = sum(ms for _, ms in gemm) / len(gemm)
+        achieved = sum(flops) / sum(ms for _, ms in gemm) / 1e9  # TFLOP/s (flop/ms / 1e9)
+        traffic = ncu_traffic(args.config)
+        roofline = {"bound": "tensor", "pipe": "FP64 DMMA (mma.sync.m8n8k4.f64)", "kernel": "zgemm_dmma_kernel",
+                    "achieved": round(achieved, 3), "peak": peak_tf, "unit": "TFLOP/s",
+                    "frac": round(achieved / peak_tf, 4), "traffic": traffic,
+                    "flops_per_launch": flops[0], "avg_launch_ms": avg_ms,
+                    "peak_source": peak_src,
+                    "algorithmic": "8 P n_j real flops per mode pass (1 CMAC = 8 flops)"}
+    step_ms_prof = sum(ms for _, _, ms in recs) / args.steps
+    stage_ms = {k: sum(ms for _, ms in v) / args.steps for k, v in by_kind.items()}
+    solve_flops = 8.0 * P * (sum(dims) - len(dims)) / 2 + 8.0 * P
+    solve_ms = stage_ms.get("solve_level", 0.0) + stage_ms.get("solve_persistent", 0.0)
+    kernels = {
+        "transform_gemm_share": stage_ms.get("transform_gemm", 0.0) / step_ms_prof if step_ms_prof else None,
+        "stage_ms_per_step": {k: round(v, 4) for k, v in stage_ms.items()},
+        "solve_tflops": solve_flops / (solve_ms * 1e-3) / 1e12 if solve_ms else None,
+        "solve_frac_fp64": (solve_flops / (solve_ms * 1e-3) / 1e12) / peak_tf if solve_ms else None,
+    }
+
+    # --- end to end through the C-ABI host-buffer call -----------------------------------------
+    e2e = None
+    if not args.no_e2e:
+        import ctypes as C
+        lib = ctx.lib
+        up, ku = nds._ptr_array(us)
+        tp, kt = nds._ptr_array(ts)
+        dims_c = nds._dims(dims)
+        rep = nds._Report()
+        sing = nds._Singular()
+        hb, hx = pinned_b.data_ptr(), pinned_x.data_ptr()
+
+        def e2e_call():
+            rc = lib.nds_solve_schur(ctx.h, len(dims), dims_c, up, tp, hb, hx, 0.0, nds.ALLOW_FAST_PATH,
+                                     C.byref(rep), C.byref(sing))
+            if rc:
+                raise RuntimeError(ctx.last_error())
+
+        for _ in range(2):
+            e2e_call()
+        barrier(world)
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            e2e_call()
+        e2e_s = (time.perf_counter() - t0) / args.e2e_steps
+        e2e_s = max_over_ranks(world, e2e_s, dev)
+        e2e = {"value": world * P / e2e_s, "unit": "unknowns/s", "h2d_bytes_per_step": 16 * P,
+               "d2h_bytes_per_step": 16 * P, "ms_per_step": e2e_s * 1e3, "steps": args.e2e_steps,
+               "api": "nds_solve_schur (host buffers, pinned)",
+               "h2d_ms": rep.h2d_seconds * 1e3, "d2h_ms": rep.d2h_seconds * 1e3,
+               "device_ms": (rep.transform_seconds + rep.backsub_seconds + rep.inverse_seconds) * 1e3}
+
+    verify = None
+    if args.verify:
+        verify = ctx.dev_residual(a_list, dims, d_x.data_ptr(), d_b.data_ptr())
+
+    # --- CPU baseline (rank 0, N=1) -------------------------------------------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        try:
+            v, info = cpu_reference_sample(args.config, args.seed, threads)
+            d = CPU_SAMPLE_DIMS[args.config]
+            cpu = {"value": v, "unit": "unknowns/s", "cores": threads, "kind": "reference",
+                   "sample": f"reference ndsylv::solve (oracle/_ref) on the {'x'.join(map(str, d))} slab of "
+                             f"{args.config}, P={info['P']}, rate = P/(transform+backsub+inverse s), Schur excluded",
+                   "stage_seconds": info["stage_seconds"]}
+        except Exception as e:  # the reference build travels with the repo; report if absent
+            cpu = {"value": None, "unit": "unknowns/s", "cores": threads, "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "unknowns/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "c128 (fp64 DMMA)", "data": "synthetic (generator v1, seeded Gaussian)",
+            "config": {"workload": args.config, "dims": list(dims), "P": P, "description": configs.DESCRIPTIONS[args.config],
+                       "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                       "l2": "inputs larger than L2 (256 MiB per tensor vs 126 MB L2); no flush",
+                       "schur_seconds_host": schur_s},
+            "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches_per_step * args.steps, "launches_per_step": launches_per_step,
+            "clocks": clk.summary(), "verify": verify,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,191 @@
+/*
+ * ndsylv_b200 — B200-native (sm_100a) hot path of the non-recursive N-D Bartels–Stewart
+ * solver for  sum_j A_j x_j X = B  (arXiv 2412.15840), behind a plain C ABI.
+ *
+ * Drop-in boundary. Each entry point below replaces one function of the reference C++ API
+ * (/root/reference/proj/include/ndsylv/*.hpp) and keeps its argument meaning, layout and
+ * error behaviour; INTEGRATION.md shows the adapter a maintainer adds on the reference side.
+ *
+ *   Layout: tensors are column-major (first index fastest) arrays of complex128 — the exact
+ *   storage of ndsylv::NDTensor::data (tensor.hpp:23-39); matrices are column-major n x n
+ *   (ndsylv::Matrix, matrix.hpp:11-30). nds_z is layout-identical to std::complex<double>.
+ *   Modes are 1-based where a mode number is passed (kernels.hpp:10-12).
+ *
+ *   Errors: every call returns an nds_status. The codes mirror the reference's exception
+ *   types and the CLI's exit-code mapping (tools/ndsylv_main.cpp:366-381):
+ *     SingularOperatorError (types.hpp:31-47) -> NDS_ERR_SINGULAR (=2) + nds_singular filled
+ *     std::bad_alloc / device out of memory   -> NDS_ERR_NOMEM (=4)
+ *     std::invalid_argument                   -> NDS_ERR_INVALID
+ *     ConvergenceError (Schur, schur.cpp:146) -> NDS_ERR_CONVERGENCE
+ *     std::overflow_error (tensor.cpp:13)     -> NDS_ERR_OVERFLOW
+ *   The message of the last failure on a context is returned by nds_last_error().
+ *
+ *   Threading: one context per host thread; a context owns one CUDA device, one stream and
+ *   the workspaces. Host-buffer calls are synchronous (like the reference); the nds_plan_*
+ *   device-pointer calls are asynchronous on the context stream. There is no CPU fallback:
+ *   without a usable sm_100 device every compute call returns NDS_ERR_CUDA.
+ */
+#ifndef NDSYLV_B200_H
+#define NDSYLV_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NDS_MAX_MODES 64 /* NDT1 order limit, README.md "Tensor files" */
+
+typedef struct {
+  double re, im;
+} nds_z;
+
+typedef enum {
+  NDS_OK = 0,
+  NDS_ERR_OTHER = 1,
+  NDS_ERR_SINGULAR = 2,
+  NDS_ERR_FILE = 3,
+  NDS_ERR_NOMEM = 4,
+  NDS_ERR_INVALID = 5,
+  NDS_ERR_CONVERGENCE = 6,
+  NDS_ERR_OVERFLOW = 7,
+  NDS_ERR_CUDA = 8
+} nds_status;
+
+/* SolveOptions (sylvester.hpp:19-28): allow_fast_path defaults to true in the reference. */
+enum { NDS_ALLOW_FAST_PATH = 1u, NDS_REAL_OUTPUT = 2u };
+
+/* SolveReport (sylvester.hpp:30-42) plus device-side timings. */
+typedef struct {
+  double min_abs_denominator;
+  int32_t used_normal_fast_path;
+  int64_t flop_estimate;
+  int64_t schur_flop_estimate;
+  int64_t backsub_entries;
+  int64_t backsub_multiplies;
+  double schur_seconds;     /* host Schur setup (nds_solve only) */
+  double transform_seconds; /* forward transform, device time */
+  double backsub_seconds;   /* triangular solve (or fast-path divide), device time */
+  double inverse_seconds;   /* inverse transform, device time */
+  double total_seconds;     /* wall time of the call */
+  double h2d_seconds;       /* host->device copy of B (host-buffer calls) */
+  double d2h_seconds;       /* device->host copy of X (host-buffer calls) */
+  int32_t kernel_launches;  /* device kernels launched by the call */
+} nds_report;
+
+/* SingularOperatorError payload: 1-based multi-index of the FIRST offender in the reference's
+ * descending visiting order (sylvester.cpp:88-103) and its denominator. */
+typedef struct {
+  int32_t n_modes;
+  int64_t multi_index[NDS_MAX_MODES];
+  double den_re, den_im;
+} nds_singular;
+
+/* BackSubstituteStats (sylvester.hpp:69-73) */
+typedef struct {
+  int64_t entries;
+  int64_t multiplies;
+  double min_abs_denominator;
+} nds_backsub_stats;
+
+typedef struct nds_ctx nds_ctx;
+typedef struct nds_plan nds_plan;
+
+const char* nds_version(void);
+
+/* ---- context ------------------------------------------------------------------------- */
+int nds_ctx_create(nds_ctx** out, int device);
+void nds_ctx_destroy(nds_ctx* ctx);
+/* Use an external cudaStream_t (e.g. torch's current stream); NULL restores the own stream. */
+int nds_ctx_set_stream(nds_ctx* ctx, void* cuda_stream);
+void* nds_ctx_stream(nds_ctx* ctx);
+const char* nds_last_error(const nds_ctx* ctx);
+/* Release cached device workspaces. */
+void nds_ctx_trim(nds_ctx* ctx);
+
+/* ---- reference API, host buffers ----------------------------------------------------- */
+
+/* ndsylv::solve (sylvester.hpp:79, sylvester.cpp:167-227): Schur on the host (timed into
+ * rep->schur_seconds), transforms + triangular solve on the GPU. x may alias b. */
+int nds_solve(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z* const* a, const nds_z* b, nds_z* x,
+              double singular_tol, unsigned flags, nds_report* rep, nds_singular* sing);
+
+/* The same path when the caller already holds the Schur factors A_j = U_j T_j U_j^H
+ * (SchurFactors, schur.hpp:9-14) — what ndsylv::solve does after its schur() calls. */
+int nds_solve_schur(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z* const* u, const nds_z* const* t,
+                    const nds_z* b, nds_z* x, double singular_tol, unsigned flags, nds_report* rep,
+                    nds_singular* sing);
+
+/* ndsylv::schur (schur.hpp:19) — host complex Schur (Householder Hessenberg + shifted QR). */
+int nds_schur(nds_ctx* ctx, int n, const nds_z* a, nds_z* u, nds_z* t);
+
+/* ndsylv::forward_transform (sylvester.hpp:64): c = U_N^H x_N ( ... U_1^H x_1 b ). c may alias b. */
+int nds_forward_transform(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z* const* u, const nds_z* b,
+                          nds_z* c);
+/* ndsylv::inverse_transform (sylvester.hpp:67): x = U_N x_N ( ... U_1 x_1 y ). x may alias y. */
+int nds_inverse_transform(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z* const* u, const nds_z* y,
+                          nds_z* x);
+/* ndsylv::back_substitute (sylvester.hpp:77): overwrites c with y in place. */
+int nds_back_substitute(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z* const* t, nds_z* c,
+                        double singular_tol, nds_backsub_stats* stats, nds_singular* sing);
+/* ndsylv::mode_product (kernels.hpp:12): r = m x_mode x (mode 1-based). r must not alias x. */
+int nds_mode_product(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z* m, int mode, const nds_z* x,
+                     nds_z* r);
+/* ndsylv::apply_operator (sylvester.hpp:61): r = sum_j A_j x_j x. */
+int nds_apply_operator(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z* const* a, const nds_z* x,
+                       nds_z* r);
+/* ndsylv::flop_estimate / schur_flop_estimate (sylvester.hpp:86-90); -1 on invalid/overflow. */
+int64_t nds_flop_estimate(int n_modes, const int64_t* dims);
+int64_t nds_schur_flop_estimate(int n_modes, const int64_t* dims);
+
+/* ---- plans: device-resident, reusable (B200-native extension) ------------------------- */
+
+/* Uploads the factors, runs the singular check (NDS_ERR_SINGULAR + sing on failure) and
+ * decides the route (fast path or triangular solve), like sylvester.cpp:180-213. */
+int nds_plan_create(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z* const* u, const nds_z* const* t,
+                    double singular_tol, unsigned flags, nds_plan** out, nds_singular* sing);
+void nds_plan_destroy(nds_plan* plan);
+/* Fills the static report fields (min |den|, route, estimates, counts). */
+int nds_plan_report(const nds_plan* plan, nds_report* rep);
+int64_t nds_plan_total(const nds_plan* plan);
+
+/* Device pointers, async on the context stream. d_b is not modified; d_x may equal d_b.
+ * d_work: NULL (use the context workspace) or a device buffer of plan_total entries. */
+int nds_plan_execute(nds_plan* plan, const nds_z* d_b, nds_z* d_x, nds_z* d_work);
+/* Stages, device pointers, async. forward/inverse: out may equal in. backsub is in place. */
+int nds_plan_forward(nds_plan* plan, const nds_z* d_in, nds_z* d_out, nds_z* d_work);
+int nds_plan_backsub(nds_plan* plan, nds_z* d_c);
+int nds_plan_inverse(nds_plan* plan, const nds_z* d_in, nds_z* d_out, nds_z* d_work);
+/* Host buffers, synchronous: H2D(b), execute, D2H(x); stage device times into rep. */
+int nds_plan_execute_host(nds_plan* plan, const nds_z* h_b, nds_z* h_x, nds_report* rep);
+/* Kernel launches one nds_plan_execute issues. */
+int nds_plan_launches(const nds_plan* plan);
+/* Per-launch device timing: after _begin, every launch of execute/forward/backsub/inverse records
+ * a CUDA event on the context stream (up to max_launches). _end synchronises and returns the
+ * number of launches written: kind (0 transform GEMM, 1 transform direct, 2 solve level,
+ * 3 elementwise, 4 persistent solve), mode (+j inverse / -j forward, or solve level) and ms. */
+int nds_plan_profile_begin(nds_plan* plan, int max_launches);
+int nds_plan_profile_end(nds_plan* plan, int cap, int* kinds, int* modes, float* ms);
+
+/* ---- device-pointer kernels (test / residual surfaces) -------------------------------- */
+
+/* r = op(m) x_mode x (+ r if accumulate); op = m or m^H (conj_transpose). m is a DEVICE n x n
+ * column-major matrix. Async on the context stream. r must not alias x. */
+int nds_dev_mode_product(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z* d_m, int mode,
+                         int conj_transpose, const nds_z* d_x, nds_z* d_r, int accumulate);
+/* Device residual: returns max_i |sum_j A_j x_j X - B|_i and the 2-norm, plus |B| norms.
+ * a[] are HOST matrices (uploaded), d_x and d_b device tensors. Synchronous. */
+int nds_dev_residual(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z* const* a, const nds_z* d_x,
+                     const nds_z* d_b, double* res_max, double* res_2, double* b_max, double* b_2);
+
+/* ---- harness utility ------------------------------------------------------------------ */
+/* Seeded standard normals (Box–Muller over splitmix64 counters, stream-separated), host
+ * side, OpenMP-parallel and order-independent: out[i] for i in [0, count). */
+void nds_randn(uint64_t seed, uint64_t stream, int64_t count, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* NDSYLV_B200_H */

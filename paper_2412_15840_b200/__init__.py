@@ -1,0 +1,463 @@
+"""ndsylv_b200 — B200-native (sm_100a) hot path of the N-D Bartels–Stewart Sylvester solver.
+
+Python mirror of the reference C++ API (``/root/reference/proj/include/ndsylv``) over the C ABI
+of ``libndsylv_b200.so`` (``include/ndsylv_b200.h``). Names, argument meaning and error
+behaviour follow the reference:
+
+========================  =====================================================
+reference (C++)           here
+========================  =====================================================
+``solve`` (sylvester.hpp:79)           :meth:`Context.solve`
+``schur`` (schur.hpp:19)               :meth:`Context.schur`
+``forward_transform`` (:64)            :meth:`Context.forward_transform`
+``inverse_transform`` (:67)            :meth:`Context.inverse_transform`
+``back_substitute`` (:77)              :meth:`Context.back_substitute`
+``mode_product`` (kernels.hpp:12)      :meth:`Context.mode_product`
+``apply_operator`` (:61)               :meth:`Context.apply_operator`
+``flop_estimate`` / ``schur_flop_estimate`` (:86-90)
+``SingularOperatorError`` (types.hpp:31-47)   :class:`SingularOperatorError`
+``std::invalid_argument``               ``ValueError``
+``std::overflow_error``                 ``OverflowError``
+``ConvergenceError``                    :class:`ConvergenceError`
+========================  =====================================================
+
+Tensors are numpy ``complex128`` arrays of shape ``dims`` interpreted in column-major
+(Fortran) order, exactly the reference ``NDTensor`` storage; matrices are ``(n, n)``.
+There is no CPU fallback: without the built library or an sm_100 GPU the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libndsylv_b200.so")
+
+NDS_MAX_MODES = 64
+ALLOW_FAST_PATH = 1
+REAL_OUTPUT = 2
+
+OK, ERR_OTHER, ERR_SINGULAR, ERR_FILE, ERR_NOMEM, ERR_INVALID, ERR_CONVERGENCE, ERR_OVERFLOW, ERR_CUDA = range(9)
+
+# Symbols include/ndsylv_b200.h declares (checked by tests/test_abi.py).
+EXPORTED = [
+    "nds_version", "nds_ctx_create", "nds_ctx_destroy", "nds_ctx_set_stream", "nds_ctx_stream", "nds_last_error",
+    "nds_ctx_trim", "nds_solve", "nds_solve_schur", "nds_schur", "nds_forward_transform", "nds_inverse_transform",
+    "nds_back_substitute", "nds_mode_product", "nds_apply_operator", "nds_flop_estimate", "nds_schur_flop_estimate",
+    "nds_plan_create", "nds_plan_destroy", "nds_plan_report", "nds_plan_total", "nds_plan_execute",
+    "nds_plan_forward", "nds_plan_backsub", "nds_plan_inverse", "nds_plan_execute_host", "nds_plan_launches",
+    "nds_plan_profile_begin", "nds_plan_profile_end",
+    "nds_dev_mode_product", "nds_dev_residual", "nds_randn",
+]
+
+
+class NdsError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(msg)
+        self.code = code
+
+
+class SingularOperatorError(NdsError):
+    """types.hpp:31-47: 1-based multi-index of the first offender and its denominator."""
+
+    def __init__(self, msg, multi_index, denominator):
+        super().__init__(ERR_SINGULAR, msg)
+        self.multi_index = list(multi_index)
+        self.denominator = denominator
+
+
+class ConvergenceError(NdsError):
+    pass
+
+
+class DeviceError(NdsError):
+    pass
+
+
+class _Report(C.Structure):
+    _fields_ = [
+        ("min_abs_denominator", C.c_double),
+        ("used_normal_fast_path", C.c_int32),
+        ("flop_estimate", C.c_int64),
+        ("schur_flop_estimate", C.c_int64),
+        ("backsub_entries", C.c_int64),
+        ("backsub_multiplies", C.c_int64),
+        ("schur_seconds", C.c_double),
+        ("transform_seconds", C.c_double),
+        ("backsub_seconds", C.c_double),
+        ("inverse_seconds", C.c_double),
+        ("total_seconds", C.c_double),
+        ("h2d_seconds", C.c_double),
+        ("d2h_seconds", C.c_double),
+        ("kernel_launches", C.c_int32),
+    ]
+
+
+class _Singular(C.Structure):
+    _fields_ = [("n_modes", C.c_int32), ("multi_index", C.c_int64 * NDS_MAX_MODES), ("den_re", C.c_double),
+                ("den_im", C.c_double)]
+
+
+class _Stats(C.Structure):
+    _fields_ = [("entries", C.c_int64), ("multiplies", C.c_int64), ("min_abs_denominator", C.c_double)]
+
+
+_vp = C.c_void_p
+_i64p = C.POINTER(C.c_int64)
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libndsylv_b200.so. Raises (loudly) when it has not been built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} is missing: build it with `python -m paper_2412_15840_b200.build` "
+                          "(there is no CPU fallback)")
+    L = C.CDLL(path)
+    L.nds_version.restype = C.c_char_p
+    L.nds_last_error.restype = C.c_char_p
+    L.nds_last_error.argtypes = [_vp]
+    L.nds_ctx_create.argtypes = [C.POINTER(_vp), C.c_int]
+    L.nds_ctx_destroy.argtypes = [_vp]
+    L.nds_ctx_set_stream.argtypes = [_vp, _vp]
+    L.nds_ctx_stream.argtypes = [_vp]
+    L.nds_ctx_stream.restype = _vp
+    L.nds_ctx_trim.argtypes = [_vp]
+    L.nds_solve.argtypes = [_vp, C.c_int, _i64p, _vp, _vp, _vp, C.c_double, C.c_uint, C.POINTER(_Report),
+                            C.POINTER(_Singular)]
+    L.nds_solve_schur.argtypes = [_vp, C.c_int, _i64p, _vp, _vp, _vp, _vp, C.c_double, C.c_uint,
+                                  C.POINTER(_Report), C.POINTER(_Singular)]
+    L.nds_schur.argtypes = [_vp, C.c_int, _vp, _vp, _vp]
+    L.nds_forward_transform.argtypes = [_vp, C.c_int, _i64p, _vp, _vp, _vp]
+    L.nds_inverse_transform.argtypes = [_vp, C.c_int, _i64p, _vp, _vp, _vp]
+    L.nds_back_substitute.argtypes = [_vp, C.c_int, _i64p, _vp, _vp, C.c_double, C.POINTER(_Stats),
+                                      C.POINTER(_Singular)]
+    L.nds_mode_product.argtypes = [_vp, C.c_int, _i64p, _vp, C.c_int, _vp, _vp]
+    L.nds_apply_operator.argtypes = [_vp, C.c_int, _i64p, _vp, _vp, _vp]
+    L.nds_flop_estimate.argtypes = [C.c_int, _i64p]
+    L.nds_flop_estimate.restype = C.c_int64
+    L.nds_schur_flop_estimate.argtypes = [C.c_int, _i64p]
+    L.nds_schur_flop_estimate.restype = C.c_int64
+    L.nds_plan_create.argtypes = [_vp, C.c_int, _i64p, _vp, _vp, C.c_double, C.c_uint, C.POINTER(_vp),
+                                  C.POINTER(_Singular)]
+    L.nds_plan_destroy.argtypes = [_vp]
+    L.nds_plan_report.argtypes = [_vp, C.POINTER(_Report)]
+    L.nds_plan_total.argtypes = [_vp]
+    L.nds_plan_total.restype = C.c_int64
+    L.nds_plan_execute.argtypes = [_vp, _vp, _vp, _vp]
+    L.nds_plan_forward.argtypes = [_vp, _vp, _vp, _vp]
+    L.nds_plan_backsub.argtypes = [_vp, _vp]
+    L.nds_plan_inverse.argtypes = [_vp, _vp, _vp, _vp]
+    L.nds_plan_execute_host.argtypes = [_vp, _vp, _vp, C.POINTER(_Report)]
+    L.nds_plan_launches.argtypes = [_vp]
+    L.nds_plan_profile_begin.argtypes = [_vp, C.c_int]
+    L.nds_plan_profile_end.argtypes = [_vp, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                       C.POINTER(C.c_float)]
+    L.nds_dev_mode_product.argtypes = [_vp, C.c_int, _i64p, _vp, C.c_int, C.c_int, _vp, _vp, C.c_int]
+    L.nds_dev_residual.argtypes = [_vp, C.c_int, _i64p, _vp, _vp, _vp, C.POINTER(C.c_double),
+                                   C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double)]
+    L.nds_randn.argtypes = [C.c_uint64, C.c_uint64, C.c_int64, _vp]
+    _lib = L
+    return L
+
+
+def version() -> str:
+    return load_library().nds_version().decode()
+
+
+# ---- marshalling -----------------------------------------------------------------------------
+
+def _f(x):
+    return np.asfortranarray(np.asarray(x, dtype=np.complex128))
+
+
+def _dims(shape):
+    return (C.c_int64 * len(shape))(*[int(v) for v in shape])
+
+
+def _ptr_array(mats):
+    keep = [_f(m) for m in mats]
+    arr = (_vp * len(keep))(*[m.ctypes.data for m in keep])
+    return arr, keep
+
+
+def _dict(s):
+    return {k: getattr(s, k) for k, _ in s._fields_}
+
+
+def _raise(code, msg, sing=None):
+    if code == ERR_SINGULAR:
+        mi = [sing.multi_index[j] for j in range(sing.n_modes)] if sing is not None else []
+        den = complex(sing.den_re, sing.den_im) if sing is not None else complex("nan")
+        raise SingularOperatorError(msg, mi, den)
+    if code == ERR_INVALID:
+        raise ValueError(msg)
+    if code == ERR_OVERFLOW:
+        raise OverflowError(msg)
+    if code == ERR_NOMEM:
+        raise MemoryError(msg)
+    if code == ERR_CONVERGENCE:
+        raise ConvergenceError(code, msg)
+    if code == ERR_CUDA:
+        raise DeviceError(code, msg)
+    raise NdsError(code, msg)
+
+
+def flop_estimate(dims) -> int:
+    v = load_library().nds_flop_estimate(len(dims), _dims(dims))
+    if v < 0:
+        raise OverflowError("flop estimate overflows int64")
+    return v
+
+
+def schur_flop_estimate(dims) -> int:
+    v = load_library().nds_schur_flop_estimate(len(dims), _dims(dims))
+    if v < 0:
+        raise OverflowError("flop estimate overflows int64")
+    return v
+
+
+def randn(seed: int, stream: int, count: int) -> np.ndarray:
+    """Seeded standard normals (harness generator v1)."""
+    out = np.empty(int(count), dtype=np.float64)
+    load_library().nds_randn(seed & (2**64 - 1), stream & (2**64 - 1), int(count), out.ctypes.data)
+    return out
+
+
+@dataclass
+class SolveResult:
+    """SolveResult (sylvester.hpp:44-47)."""
+    x: np.ndarray
+    report: dict = field(default_factory=dict)
+
+
+class Plan:
+    """Device-resident solver for one coefficient set (factors uploaded once)."""
+
+    def __init__(self, ctx: "Context", us, ts, singular_tol=0.0, allow_fast_path=True, real_output=False):
+        self.ctx = ctx
+        self.dims = tuple(int(u.shape[0]) for u in us)
+        up, self._ku = _ptr_array(us)
+        tp, self._kt = _ptr_array(ts)
+        flags = (ALLOW_FAST_PATH if allow_fast_path else 0) | (REAL_OUTPUT if real_output else 0)
+        h = _vp()
+        sing = _Singular()
+        rc = ctx.lib.nds_plan_create(ctx.h, len(us), _dims(self.dims), up, tp, float(singular_tol), flags,
+                                     C.byref(h), C.byref(sing))
+        if rc:
+            _raise(rc, ctx.last_error(), sing)
+        self.h = h
+        self.total = int(np.prod(self.dims))
+
+    def report(self) -> dict:
+        r = _Report()
+        self.ctx.lib.nds_plan_report(self.h, C.byref(r))
+        return _dict(r)
+
+    def _check(self, rc):
+        if rc:
+            _raise(rc, self.ctx.last_error())
+
+    def execute(self, d_b: int, d_x: int, d_work: int = 0):
+        """Device pointers (ints), async on the context stream."""
+        self._check(self.ctx.lib.nds_plan_execute(self.h, d_b, d_x, d_work or None))
+
+    def forward(self, d_in: int, d_out: int, d_work: int):
+        self._check(self.ctx.lib.nds_plan_forward(self.h, d_in, d_out, d_work))
+
+    def backsub(self, d_c: int):
+        self._check(self.ctx.lib.nds_plan_backsub(self.h, d_c))
+
+    def inverse(self, d_in: int, d_out: int, d_work: int):
+        self._check(self.ctx.lib.nds_plan_inverse(self.h, d_in, d_out, d_work))
+
+    def execute_host(self, b: np.ndarray, x: np.ndarray | None = None):
+        """Host buffers (b, x column-major complex128 of shape dims; may be pinned)."""
+        b = _f(b)
+        if x is None:
+            x = np.empty_like(b, order="F")
+        rep = _Report()
+        self._check(self.ctx.lib.nds_plan_execute_host(self.h, b.ctypes.data, x.ctypes.data, C.byref(rep)))
+        return SolveResult(x, _dict(rep))
+
+    def execute_host_ptr(self, h_b: int, h_x: int) -> dict:
+        rep = _Report()
+        self._check(self.ctx.lib.nds_plan_execute_host(self.h, h_b, h_x, C.byref(rep)))
+        return _dict(rep)
+
+    def launches(self) -> int:
+        return self.ctx.lib.nds_plan_launches(self.h)
+
+    def profile_begin(self, max_launches: int):
+        self._check(self.ctx.lib.nds_plan_profile_begin(self.h, int(max_launches)))
+
+    KINDS = {0: "transform_gemm", 1: "transform_direct", 2: "solve_level", 3: "elementwise", 4: "solve_persistent"}
+
+    def profile_end(self, cap: int = 1 << 16):
+        """[(kind, mode, ms)] for every launch recorded since profile_begin."""
+        kinds = (C.c_int * cap)()
+        modes = (C.c_int * cap)()
+        ms = (C.c_float * cap)()
+        n = self.ctx.lib.nds_plan_profile_end(self.h, cap, kinds, modes, ms)
+        if n < 0:
+            _raise(-n, self.ctx.last_error())
+        return [(self.KINDS.get(kinds[i], str(kinds[i])), modes[i], ms[i]) for i in range(n)]
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.ctx.lib.nds_plan_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Context:
+    """One CUDA device + stream + workspaces (nds_ctx)."""
+
+    def __init__(self, device: int = 0):
+        self.lib = load_library()
+        h = _vp()
+        rc = self.lib.nds_ctx_create(C.byref(h), int(device))
+        if rc:
+            _raise(rc, self.lib.nds_last_error(None).decode())
+        self.h = h
+
+    def last_error(self) -> str:
+        return self.lib.nds_last_error(self.h).decode()
+
+    def _check(self, rc, sing=None):
+        if rc:
+            _raise(rc, self.last_error(), sing)
+
+    def set_stream(self, stream_handle: int | None):
+        self._check(self.lib.nds_ctx_set_stream(self.h, stream_handle or None))
+
+    def stream(self) -> int:
+        return self.lib.nds_ctx_stream(self.h) or 0
+
+    def trim(self):
+        self.lib.nds_ctx_trim(self.h)
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.nds_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- reference API ------------------------------------------------------------------
+    @staticmethod
+    def _flags(allow_fast_path, real_output):
+        return (ALLOW_FAST_PATH if allow_fast_path else 0) | (REAL_OUTPUT if real_output else 0)
+
+    def solve(self, coefficients, rhs, singular_tol=0.0, allow_fast_path=True, real_output=False) -> SolveResult:
+        """ndsylv::solve (sylvester.cpp:167-227): host Schur + GPU transforms and solve."""
+        b = _f(rhs)
+        if len(coefficients) != b.ndim:
+            raise ValueError("coefficient count does not match tensor order")
+        for j, a in enumerate(coefficients):
+            a = np.asarray(a)
+            if a.ndim != 2 or a.shape[0] != a.shape[1] or a.shape[0] != b.shape[j]:
+                raise ValueError(f"coefficient {j + 1} does not match mode extent")
+        ap, keep = _ptr_array(coefficients)
+        x = np.empty_like(b, order="F")
+        rep = _Report()
+        sing = _Singular()
+        rc = self.lib.nds_solve(self.h, b.ndim, _dims(b.shape), ap, b.ctypes.data, x.ctypes.data,
+                                float(singular_tol), self._flags(allow_fast_path, real_output), C.byref(rep),
+                                C.byref(sing))
+        self._check(rc, sing)
+        return SolveResult(x, _dict(rep))
+
+    def solve_schur(self, us, ts, rhs, singular_tol=0.0, allow_fast_path=True, real_output=False) -> SolveResult:
+        b = _f(rhs)
+        up, k1 = _ptr_array(us)
+        tp, k2 = _ptr_array(ts)
+        x = np.empty_like(b, order="F")
+        rep = _Report()
+        sing = _Singular()
+        rc = self.lib.nds_solve_schur(self.h, b.ndim, _dims(b.shape), up, tp, b.ctypes.data, x.ctypes.data,
+                                      float(singular_tol), self._flags(allow_fast_path, real_output), C.byref(rep),
+                                      C.byref(sing))
+        self._check(rc, sing)
+        return SolveResult(x, _dict(rep))
+
+    def schur(self, a):
+        a = _f(a)
+        if a.ndim != 2 or a.shape[0] != a.shape[1]:
+            raise ValueError("schur requires a non-empty square matrix")
+        n = a.shape[0]
+        u = np.empty((n, n), dtype=np.complex128, order="F")
+        t = np.empty((n, n), dtype=np.complex128, order="F")
+        self._check(self.lib.nds_schur(self.h, n, a.ctypes.data, u.ctypes.data, t.ctypes.data))
+        return u, t
+
+    def forward_transform(self, us, b):
+        b = _f(b)
+        up, keep = _ptr_array(us)
+        c = np.empty_like(b, order="F")
+        self._check(self.lib.nds_forward_transform(self.h, b.ndim, _dims(b.shape), up, b.ctypes.data, c.ctypes.data))
+        return c
+
+    def inverse_transform(self, us, y):
+        y = _f(y)
+        up, keep = _ptr_array(us)
+        x = np.empty_like(y, order="F")
+        self._check(self.lib.nds_inverse_transform(self.h, y.ndim, _dims(y.shape), up, y.ctypes.data, x.ctypes.data))
+        return x
+
+    def back_substitute(self, ts, c, singular_tol=0.0):
+        """Returns (y, stats). The reference overwrites c in place; here c is copied."""
+        y = _f(c).copy(order="F")
+        tp, keep = _ptr_array(ts)
+        st = _Stats()
+        sing = _Singular()
+        rc = self.lib.nds_back_substitute(self.h, y.ndim, _dims(y.shape), tp, y.ctypes.data, float(singular_tol),
+                                          C.byref(st), C.byref(sing))
+        self._check(rc, sing)
+        return y, _dict(st)
+
+    def mode_product(self, m, mode, x):
+        x = _f(x)
+        m = _f(m)
+        r = np.empty_like(x, order="F")
+        self._check(self.lib.nds_mode_product(self.h, x.ndim, _dims(x.shape), m.ctypes.data, int(mode),
+                                              x.ctypes.data, r.ctypes.data))
+        return r
+
+    def apply_operator(self, coefficients, x):
+        x = _f(x)
+        ap, keep = _ptr_array(coefficients)
+        r = np.empty_like(x, order="F")
+        self._check(self.lib.nds_apply_operator(self.h, x.ndim, _dims(x.shape), ap, x.ctypes.data, r.ctypes.data))
+        return r
+
+    # ---- device surfaces ------------------------------------------------------------------
+    def plan(self, us, ts, singular_tol=0.0, allow_fast_path=True, real_output=False) -> Plan:
+        return Plan(self, us, ts, singular_tol, allow_fast_path, real_output)
+
+    def dev_mode_product(self, dims, d_m: int, mode: int, d_x: int, d_r: int, conj_transpose=False,
+                         accumulate=False):
+        self._check(self.lib.nds_dev_mode_product(self.h, len(dims), _dims(dims), d_m, int(mode),
+                                                  1 if conj_transpose else 0, d_x, d_r, 1 if accumulate else 0))
+
+    def dev_residual(self, coefficients, dims, d_x: int, d_b: int) -> dict:
+        ap, keep = _ptr_array(coefficients)
+        vals = [C.c_double() for _ in range(4)]
+        self._check(self.lib.nds_dev_residual(self.h, len(dims), _dims(dims), ap, d_x, d_b, *[C.byref(v) for v in vals]))
+        rm, r2, bm, b2 = (v.value for v in vals)
+        return {"res_max": rm, "res_2": r2, "b_max": bm, "b_2": b2,
+                "rel_res_max": rm / bm if bm else float("inf"), "rel_res_2": r2 / b2 if b2 else float("inf")}

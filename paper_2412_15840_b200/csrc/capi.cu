@@ -1,0 +1,879 @@
+// C-ABI of ndsylv_b200 (include/ndsylv_b200.h): validation, contexts, plans, the solve
+// orchestration of sylvester.cpp:167-227 on the device, and error mapping.
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "schur.h"
+
+using nds::Error;
+
+struct nds_ctx {
+  int device = 0;
+  cudaStream_t own = nullptr;
+  cudaStream_t stream = nullptr;
+  std::string last_error;
+  double2* ws[2] = {nullptr, nullptr};  // two tensor-sized workspaces
+  size_t ws_bytes = 0;
+  void* scratch = nullptr;  // small device scratch (reductions)
+  cudaEvent_t ev[8] = {};
+};
+
+struct nds_plan {
+  nds_ctx* ctx = nullptr;
+  int n_modes = 0;
+  int64_t dims[NDS_MAX_MODES] = {};
+  int64_t total = 0;
+  unsigned flags = 0;
+  double tol = 0.0;
+  bool fast_path = false;
+  double min_abs_den = 0.0;
+  nds::FactorSet f;
+  nds::SolvePlan sp;
+  bool have_solve_plan = false;
+  int launches = 0;
+  // per-launch CUDA-event profile (nds_plan_profile_begin / _end)
+  bool profiling = false;
+  std::vector<cudaEvent_t> pev;
+  std::vector<int> pkind, pmode;
+  nds::Recorder rec;
+};
+
+namespace {
+
+using Clock = std::chrono::steady_clock;
+double secs(Clock::time_point t0) { return std::chrono::duration<double>(Clock::now() - t0).count(); }
+
+thread_local std::string g_noctx_error;
+
+template <class F>
+int guarded(nds_ctx* ctx, F&& f) {
+  std::string* err = ctx ? &ctx->last_error : &g_noctx_error;
+  try {
+    f();
+    return NDS_OK;
+  } catch (const Error& e) {
+    *err = e.what();
+    return e.code;
+  } catch (const std::bad_alloc& e) {
+    *err = e.what();
+    return NDS_ERR_NOMEM;
+  } catch (const std::exception& e) {
+    *err = e.what();
+    return NDS_ERR_OTHER;
+  }
+}
+
+// tensor.cpp:8-16 (checked_total) + sylvester.cpp:17-27 (order >= 2 for the solve).
+int64_t checked_total(int n_modes, const int64_t* dims, int min_modes) {
+  if (n_modes < min_modes)
+    throw Error(NDS_ERR_INVALID, min_modes >= 2 ? "problem order must be at least 2" : "tensor order must be at least 1");
+  if (n_modes > NDS_MAX_MODES) throw Error(NDS_ERR_INVALID, "tensor order exceeds NDS_MAX_MODES");
+  if (!dims) throw Error(NDS_ERR_INVALID, "dims is null");
+  int64_t total = 1;
+  for (int j = 0; j < n_modes; ++j) {
+    if (dims[j] < 1) throw Error(NDS_ERR_INVALID, "tensor dimensions must be at least 1");
+    if (__builtin_mul_overflow(total, dims[j], &total)) throw Error(NDS_ERR_OVERFLOW, "tensor size overflows int64");
+  }
+  if (total > std::numeric_limits<int64_t>::max() / 16) throw Error(NDS_ERR_OVERFLOW, "tensor byte size overflows");
+  return total;
+}
+
+void require_ptrs(int n_modes, const nds_z* const* m, const char* what) {
+  if (!m) throw Error(NDS_ERR_INVALID, std::string(what) + " is null");
+  for (int j = 0; j < n_modes; ++j)
+    if (!m[j]) throw Error(NDS_ERR_INVALID, std::string(what) + "[" + std::to_string(j) + "] is null");
+}
+
+void ensure_device(nds_ctx* ctx) { NDS_CUDA(cudaSetDevice(ctx->device)); }
+
+void ensure_ws(nds_ctx* ctx, int64_t total) {
+  const size_t bytes = (size_t)total * sizeof(double2);
+  if (ctx->ws_bytes >= bytes) return;
+  for (auto& w : ctx->ws)
+    if (w) {
+      cudaFree(w);
+      w = nullptr;
+    }
+  ctx->ws_bytes = 0;
+  NDS_CUDA(cudaMalloc(&ctx->ws[0], bytes));
+  NDS_CUDA(cudaMalloc(&ctx->ws[1], bytes));
+  ctx->ws_bytes = bytes;
+}
+
+// Build the device factor set: U_j in four layouts, T_j, diag(T_j). u may be null (t-only) or
+// t may be null (u-only, transforms).
+void upload_factors(nds_ctx* ctx, nds::FactorSet& f, int n_modes, const int64_t* dims, const nds_z* const* u,
+                    const nds_z* const* t) {
+  f.n_modes = n_modes;
+  int64_t sq = 0, diag = 0;
+  for (int j = 0; j < n_modes; ++j) {
+    f.dims[j] = dims[j];
+    sq += dims[j] * dims[j];
+    diag += dims[j];
+  }
+  const int64_t n_u = u ? 4 * sq : 0;
+  const int64_t n_t = t ? sq : 0;
+  const int64_t n_d = t ? diag : 0;
+  std::vector<double2> host((size_t)(n_u + n_t + n_d) + 1);
+  NDS_CUDA(cudaMalloc(&f.pool, host.size() * sizeof(double2)));
+  int64_t off = 0;
+  nds::Geom& g = f.geom;
+  g.n_modes = n_modes;
+  g.total = 1;
+  int64_t toff = 0, doff = 0;
+  for (int j = 0; j < n_modes; ++j) {
+    const int64_t n = dims[j];
+    g.dims[j] = n;
+    g.strides[j] = g.total;
+    g.total *= n;
+    if (u) {
+      double2* ur = host.data() + off;
+      double2* uc = ur + n * n;
+      double2* hr = uc + n * n;
+      double2* hc = hr + n * n;
+      for (int64_t k = 0; k < n; ++k)
+        for (int64_t i = 0; i < n; ++i) {
+          const nds_z z = u[j][i + k * n];  // U(i, k), column-major
+          uc[i + k * n] = make_double2(z.re, z.im);
+          ur[i * n + k] = make_double2(z.re, z.im);
+          // U^H(k, i) = conj(U(i, k))
+          hc[k + i * n] = make_double2(z.re, -z.im);
+          hr[k * n + i] = make_double2(z.re, -z.im);
+        }
+      f.u_row[j] = f.pool + off;
+      f.u_col[j] = f.pool + off + n * n;
+      f.uh_row[j] = f.pool + off + 2 * n * n;
+      f.uh_col[j] = f.pool + off + 3 * n * n;
+      off += 4 * n * n;
+    }
+  }
+  if (t) {
+    f.t_pool = f.pool + off;
+    for (int j = 0; j < n_modes; ++j) {
+      const int64_t n = dims[j];
+      g.toff[j] = toff;
+      for (int64_t i = 0; i < n * n; ++i) host[off + toff + i] = make_double2(t[j][i].re, t[j][i].im);
+      toff += n * n;
+    }
+    off += toff;
+    f.diag_pool = f.pool + off;
+    for (int j = 0; j < n_modes; ++j) {
+      const int64_t n = dims[j];
+      g.doff[j] = doff;
+      for (int64_t i = 0; i < n; ++i) host[off + doff + i] = make_double2(t[j][i + i * n].re, t[j][i + i * n].im);
+      doff += n;
+    }
+    off += doff;
+  }
+  NDS_CUDA(cudaMemcpyAsync(f.pool, host.data(), (size_t)off * sizeof(double2), cudaMemcpyHostToDevice, ctx->stream));
+  NDS_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+void free_factors(nds::FactorSet& f) {
+  if (f.pool) cudaFree(f.pool);
+  f.pool = nullptr;
+}
+
+// sylvester.cpp:29-33 — eps * sum_j ||T_j||_F (std::norm = re^2 + im^2, matrix.cpp:99-103).
+double default_tol(int n_modes, const int64_t* dims, const nds_z* const* t) {
+  double s = 0.0;
+  for (int j = 0; j < n_modes; ++j) {
+    double f2 = 0.0;
+    for (int64_t i = 0; i < dims[j] * dims[j]; ++i) f2 += t[j][i].re * t[j][i].re + t[j][i].im * t[j][i].im;
+    s += std::sqrt(f2);
+  }
+  return std::numeric_limits<double>::epsilon() * s;
+}
+
+// sylvester.cpp:35-40
+bool numerically_diagonal(int64_t n, const nds_z* t) {
+  double off2 = 0.0, all2 = 0.0;
+  for (int64_t c = 0; c < n; ++c)
+    for (int64_t r = 0; r < n; ++r) {
+      const nds_z z = t[r + c * n];
+      const double v = z.re * z.re + z.im * z.im;
+      all2 += v;
+      if (r < c) off2 += v;
+    }
+  return std::sqrt(off2) <= 1e-12 * (1.0 + std::sqrt(all2));
+}
+
+void fill_singular(nds_singular* sing, int n_modes, const int64_t* dims, int64_t flat, const nds_z* const* t) {
+  if (!sing) return;
+  sing->n_modes = n_modes;
+  double re = 0.0, im = 0.0;
+  for (int j = 0; j < n_modes; ++j) {
+    const int64_t ij = flat % dims[j];
+    flat /= dims[j];
+    sing->multi_index[j] = ij + 1;
+    re += t[j][ij + ij * dims[j]].re;
+    im += t[j][ij + ij * dims[j]].im;
+  }
+  sing->den_re = re;
+  sing->den_im = im;
+}
+
+std::string format_singular(const nds_singular& s) {
+  std::string m = "singular operator: denominator " + std::to_string(s.den_re) + (s.den_im < 0 ? "" : "+") +
+                  std::to_string(s.den_im) + "i at multi-index (";
+  for (int j = 0; j < s.n_modes; ++j) m += (j ? ", " : "") + std::to_string(s.multi_index[j]);
+  return m + ")";
+}
+
+// N mode-product passes in -> out (modes 1..N, op = U_j^H if adjoint else U_j). `in` is never
+// written; out may equal in. Destinations alternate out/work so the last lands in out.
+int transform_chain(nds_plan* p, bool adjoint, const double2* in, double2* out, double2* work) {
+  const int N = p->n_modes;
+  nds::Recorder* rec = p->profiling ? &p->rec : nullptr;
+  int launches = 0;
+  const bool in_place = in == out;
+  const double2* src = in;
+  for (int j = 1; j <= N; ++j) {
+    // Out of place: last pass lands in out. In place: first pass must leave `in`, so start in
+    // work (odd N then ends in work and is copied back).
+    double2* dst = in_place ? ((j % 2 == 1) ? work : out) : (((N - j) % 2 == 0) ? out : work);
+    const int kind = nds::mode_product_launch(p->f, j, adjoint, nds::mode_view(N, p->dims, j), src, dst, false,
+                                              p->ctx->stream);
+    if (rec) rec->mark(p->ctx->stream, kind, adjoint ? -j : j);
+    ++launches;
+    src = dst;
+  }
+  if (src != out) {
+    NDS_CUDA(cudaMemcpyAsync(out, src, (size_t)p->total * sizeof(double2), cudaMemcpyDeviceToDevice, p->ctx->stream));
+  }
+  return launches;
+}
+
+int backsub_run(nds_plan* p, double2* c) {
+  nds::Recorder* rec = p->profiling ? &p->rec : nullptr;
+  if (p->fast_path) {
+    nds::fast_divide_launch(p->f.geom, p->f.diag_pool, c, p->ctx->stream);
+    if (rec) rec->mark(p->ctx->stream, nds::kElementwise, 0);
+    return 1;
+  }
+  return nds::backsub_launch(p->sp, p->f.t_pool, c, p->ctx->stream, rec);
+}
+
+// Full path on device buffers: b -> (fwd) -> C -> (solve, in place) -> Y -> (inv) -> x.
+// Destinations alternate W/X from the first pass so the 2N-th pass lands in x and b is only read.
+int execute(nds_plan* p, const double2* b, double2* x, double2* work, cudaEvent_t* ev) {
+  const int N = p->n_modes;
+  cudaStream_t s = p->ctx->stream;
+  nds::Recorder* rec = p->profiling ? &p->rec : nullptr;
+  int launches = 0;
+  const double2* src = b;
+  auto dst_of = [&](int pass) { return (pass % 2 == 1) ? work : x; };  // pass 1..2N
+  if (ev) NDS_CUDA(cudaEventRecord(ev[0], s));
+  if (rec) rec->mark(s, -1, 0);
+  for (int j = 1; j <= N; ++j) {
+    double2* dst = dst_of(j);
+    const int kind = nds::mode_product_launch(p->f, j, true, nds::mode_view(N, p->dims, j), src, dst, false, s);
+    if (rec) rec->mark(s, kind, -j);
+    ++launches;
+    src = dst;
+  }
+  double2* c = dst_of(N);
+  if (ev) NDS_CUDA(cudaEventRecord(ev[1], s));
+  launches += backsub_run(p, c);
+  if (ev) NDS_CUDA(cudaEventRecord(ev[2], s));
+  src = c;
+  for (int j = 1; j <= N; ++j) {
+    double2* dst = dst_of(N + j);
+    const int kind = nds::mode_product_launch(p->f, j, false, nds::mode_view(N, p->dims, j), src, dst, false, s);
+    if (rec) rec->mark(s, kind, j);
+    ++launches;
+    src = dst;
+  }
+  if (p->flags & NDS_REAL_OUTPUT) {
+    launches += nds::real_part_launch(x, p->total, s);
+    if (rec) rec->mark(s, nds::kElementwise, 0);
+  }
+  if (ev) NDS_CUDA(cudaEventRecord(ev[3], s));
+  return launches;
+}
+
+void plan_create_impl(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z* const* u, const nds_z* const* t,
+                      double singular_tol, unsigned flags, nds_plan** out, nds_singular* sing) {
+  if (!out) throw Error(NDS_ERR_INVALID, "out is null");
+  *out = nullptr;
+  const int64_t total = checked_total(n_modes, dims, 2);
+  require_ptrs(n_modes, u, "u");
+  require_ptrs(n_modes, t, "t");
+  ensure_device(ctx);
+  std::unique_ptr<nds_plan> p(new nds_plan);
+  p->ctx = ctx;
+  p->n_modes = n_modes;
+  std::memcpy(p->dims, dims, n_modes * sizeof(int64_t));
+  p->total = total;
+  p->flags = flags;
+  p->tol = singular_tol > 0.0 ? singular_tol : default_tol(n_modes, dims, t);
+  bool diag_route = (flags & NDS_ALLOW_FAST_PATH) != 0;
+  for (int j = 0; diag_route && j < n_modes; ++j) diag_route = numerically_diagonal(dims[j], t[j]);
+  p->fast_path = diag_route;
+  upload_factors(ctx, p->f, n_modes, dims, u, t);
+  // Singular check over all entries (sylvester.cpp:101-103 / :137): the first offender in the
+  // reference's descending visiting order is the one with the largest flat index.
+  int64_t bad = -1;
+  nds::den_scan(p->f.geom, p->f.diag_pool, p->tol, &p->min_abs_den, &bad, ctx->stream, ctx->scratch);
+  if (bad >= 0) {
+    nds_singular tmp{};
+    fill_singular(&tmp, n_modes, dims, bad, t);
+    if (sing) *sing = tmp;
+    free_factors(p->f);
+    throw Error(NDS_ERR_SINGULAR, format_singular(tmp));
+  }
+  if (!p->fast_path) {
+    int64_t toff[NDS_MAX_MODES];
+    for (int j = 0; j < n_modes; ++j) toff[j] = p->f.geom.toff[j];
+    nds::solve_plan_build(p->sp, n_modes, dims, toff);
+    p->have_solve_plan = true;
+  }
+  *out = p.release();
+}
+
+void plan_destroy_impl(nds_plan* p) {
+  if (!p) return;
+  cudaSetDevice(p->ctx->device);
+  for (auto e : p->pev) cudaEventDestroy(e);
+  free_factors(p->f);
+  if (p->have_solve_plan) nds::solve_plan_free(p->sp);
+  delete p;
+}
+
+void report_static(const nds_plan* p, nds_report* rep) {
+  std::memset(rep, 0, sizeof(*rep));
+  rep->min_abs_denominator = p->min_abs_den;
+  rep->used_normal_fast_path = p->fast_path ? 1 : 0;
+  rep->flop_estimate = nds_flop_estimate(p->n_modes, p->dims);
+  rep->schur_flop_estimate = nds_schur_flop_estimate(p->n_modes, p->dims);
+  if (!p->fast_path) {
+    rep->backsub_entries = p->total;
+    int64_t mult = 0;  // sum over entries of sum_j (n_j - i_j) = sum_j (P / n_j) n_j (n_j - 1) / 2
+    for (int j = 0; j < p->n_modes; ++j) mult += (p->total / p->dims[j]) * (p->dims[j] * (p->dims[j] - 1) / 2);
+    rep->backsub_multiplies = mult;
+  }
+}
+
+float ev_ms(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0.f;
+  NDS_CUDA(cudaEventElapsedTime(&ms, a, b));
+  return ms;
+}
+
+void execute_host_impl(nds_plan* p, const nds_z* hb, nds_z* hx, nds_report* rep) {
+  if (!hb || !hx) throw Error(NDS_ERR_INVALID, "null tensor pointer");
+  nds_ctx* ctx = p->ctx;
+  ensure_device(ctx);
+  ensure_ws(ctx, p->total);
+  cudaStream_t s = ctx->stream;
+  const size_t bytes = (size_t)p->total * sizeof(double2);
+  double2* X = ctx->ws[0];
+  double2* W = ctx->ws[1];
+  NDS_CUDA(cudaEventRecord(ctx->ev[4], s));
+  NDS_CUDA(cudaMemcpyAsync(X, hb, bytes, cudaMemcpyHostToDevice, s));
+  const int launches = execute(p, X, X, W, ctx->ev);
+  NDS_CUDA(cudaMemcpyAsync(hx, X, bytes, cudaMemcpyDeviceToHost, s));
+  NDS_CUDA(cudaEventRecord(ctx->ev[5], s));
+  NDS_CUDA(cudaStreamSynchronize(s));
+  if (rep) {
+    report_static(p, rep);
+    rep->h2d_seconds = ev_ms(ctx->ev[4], ctx->ev[0]) * 1e-3;
+    rep->transform_seconds = ev_ms(ctx->ev[0], ctx->ev[1]) * 1e-3;
+    rep->backsub_seconds = ev_ms(ctx->ev[1], ctx->ev[2]) * 1e-3;
+    rep->inverse_seconds = ev_ms(ctx->ev[2], ctx->ev[3]) * 1e-3;
+    rep->d2h_seconds = ev_ms(ctx->ev[3], ctx->ev[5]) * 1e-3;
+    rep->kernel_launches = launches;
+  }
+}
+
+// Host-buffer transform (forward_transform / inverse_transform).
+void transform_host(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z* const* u, const nds_z* in, nds_z* out,
+                    bool adjoint) {
+  const int64_t total = checked_total(n_modes, dims, 1);
+  require_ptrs(n_modes, u, "u");
+  if (!in || !out) throw Error(NDS_ERR_INVALID, "null tensor pointer");
+  ensure_device(ctx);
+  ensure_ws(ctx, total);
+  nds_plan p;
+  p.ctx = ctx;
+  p.n_modes = n_modes;
+  std::memcpy(p.dims, dims, n_modes * sizeof(int64_t));
+  p.total = total;
+  upload_factors(ctx, p.f, n_modes, dims, u, nullptr);
+  const size_t bytes = (size_t)total * sizeof(double2);
+  try {
+    NDS_CUDA(cudaMemcpyAsync(ctx->ws[0], in, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    transform_chain(&p, adjoint, ctx->ws[0], ctx->ws[0], ctx->ws[1]);
+    NDS_CUDA(cudaMemcpyAsync(out, ctx->ws[0], bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    NDS_CUDA(cudaStreamSynchronize(ctx->stream));
+  } catch (...) {
+    free_factors(p.f);
+    throw;
+  }
+  free_factors(p.f);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* nds_version(void) { return "ndsylv_b200 0.1 (sm_100a)"; }
+
+int nds_ctx_create(nds_ctx** out, int device) {
+  if (!out) return NDS_ERR_INVALID;
+  *out = nullptr;
+  return guarded(nullptr, [&] {
+    int count = 0;
+    NDS_CUDA(cudaGetDeviceCount(&count));
+    if (device < 0 || device >= count) throw Error(NDS_ERR_CUDA, "no such CUDA device");
+    cudaDeviceProp prop;
+    NDS_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) throw Error(NDS_ERR_CUDA, std::string("ndsylv_b200 needs an sm_100 device, found ") + prop.name);
+    std::unique_ptr<nds_ctx> c(new nds_ctx);
+    c->device = device;
+    NDS_CUDA(cudaSetDevice(device));
+    NDS_CUDA(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
+    c->stream = c->own;
+    NDS_CUDA(cudaMalloc(&c->scratch, 256));
+    for (auto& e : c->ev) NDS_CUDA(cudaEventCreate(&e));
+    *out = c.release();
+  });
+}
+
+void nds_ctx_destroy(nds_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  nds_ctx_trim(ctx);
+  if (ctx->scratch) cudaFree(ctx->scratch);
+  for (auto& e : ctx->ev)
+    if (e) cudaEventDestroy(e);
+  if (ctx->own) cudaStreamDestroy(ctx->own);
+  delete ctx;
+}
+
+int nds_ctx_set_stream(nds_ctx* ctx, void* cuda_stream) {
+  if (!ctx) return NDS_ERR_INVALID;
+  ctx->stream = cuda_stream ? (cudaStream_t)cuda_stream : ctx->own;
+  return NDS_OK;
+}
+
+void* nds_ctx_stream(nds_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+
+const char* nds_last_error(const nds_ctx* ctx) { return ctx ? ctx->last_error.c_str() : g_noctx_error.c_str(); }
+
+void nds_ctx_trim(nds_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  for (auto& w : ctx->ws)
+    if (w) {
+      cudaFree(w);
+      w = nullptr;
+    }
+  ctx->ws_bytes = 0;
+}
+
+int nds_schur(nds_ctx* ctx, int n, const nds_z* a, nds_z* u, nds_z* t) {
+  return guarded(ctx, [&] {
+    if (!a || !u || !t) throw Error(NDS_ERR_INVALID, "null matrix pointer");
+    nds::schur_host(n, a, u, t);
+  });
+}
+
+int nds_plan_create(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z* const* u, const nds_z* const* t,
+                    double singular_tol, unsigned flags, nds_plan** out, nds_singular* sing) {
+  if (!ctx) return NDS_ERR_INVALID;
+  return guarded(ctx, [&] { plan_create_impl(ctx, n_modes, dims, u, t, singular_tol, flags, out, sing); });
+}
+
+void nds_plan_destroy(nds_plan* plan) { plan_destroy_impl(plan); }
+
+int nds_plan_report(const nds_plan* plan, nds_report* rep) {
+  if (!plan || !rep) return NDS_ERR_INVALID;
+  report_static(plan, rep);
+  return NDS_OK;
+}
+
+int64_t nds_plan_total(const nds_plan* plan) { return plan ? plan->total : -1; }
+
+int nds_plan_execute(nds_plan* plan, const nds_z* d_b, nds_z* d_x, nds_z* d_work) {
+  if (!plan) return NDS_ERR_INVALID;
+  return guarded(plan->ctx, [&] {
+    if (!d_b || !d_x) throw Error(NDS_ERR_INVALID, "null device tensor pointer");
+    ensure_device(plan->ctx);
+    double2* w = (double2*)d_work;
+    if (!w) {
+      ensure_ws(plan->ctx, plan->total);
+      w = plan->ctx->ws[1];
+    }
+    if (w == (double2*)d_x || w == (const double2*)d_b) throw Error(NDS_ERR_INVALID, "work must not alias b or x");
+    plan->launches = execute(plan, (const double2*)d_b, (double2*)d_x, w, nullptr);
+  });
+}
+
+int nds_plan_forward(nds_plan* plan, const nds_z* d_in, nds_z* d_out, nds_z* d_work) {
+  if (!plan) return NDS_ERR_INVALID;
+  return guarded(plan->ctx, [&] {
+    if (!d_in || !d_out || !d_work) throw Error(NDS_ERR_INVALID, "null device tensor pointer");
+    transform_chain(plan, true, (const double2*)d_in, (double2*)d_out, (double2*)d_work);
+  });
+}
+
+int nds_plan_backsub(nds_plan* plan, nds_z* d_c) {
+  if (!plan) return NDS_ERR_INVALID;
+  return guarded(plan->ctx, [&] {
+    if (!d_c) throw Error(NDS_ERR_INVALID, "null device tensor pointer");
+    backsub_run(plan, (double2*)d_c);
+  });
+}
+
+int nds_plan_inverse(nds_plan* plan, const nds_z* d_in, nds_z* d_out, nds_z* d_work) {
+  if (!plan) return NDS_ERR_INVALID;
+  return guarded(plan->ctx, [&] {
+    if (!d_in || !d_out || !d_work) throw Error(NDS_ERR_INVALID, "null device tensor pointer");
+    transform_chain(plan, false, (const double2*)d_in, (double2*)d_out, (double2*)d_work);
+    if (plan->flags & NDS_REAL_OUTPUT) nds::real_part_launch((double2*)d_out, plan->total, plan->ctx->stream);
+  });
+}
+
+int nds_plan_execute_host(nds_plan* plan, const nds_z* h_b, nds_z* h_x, nds_report* rep) {
+  if (!plan) return NDS_ERR_INVALID;
+  return guarded(plan->ctx, [&] { execute_host_impl(plan, h_b, h_x, rep); });
+}
+
+int nds_plan_launches(const nds_plan* plan) { return plan ? plan->launches : -1; }
+
+int nds_plan_profile_begin(nds_plan* plan, int max_launches) {
+  if (!plan || max_launches < 2) return NDS_ERR_INVALID;
+  return guarded(plan->ctx, [&] {
+    ensure_device(plan->ctx);
+    while ((int)plan->pev.size() < max_launches) {
+      cudaEvent_t e;
+      NDS_CUDA(cudaEventCreate(&e));
+      plan->pev.push_back(e);
+    }
+    plan->pkind.assign(max_launches, 0);
+    plan->pmode.assign(max_launches, 0);
+    plan->rec = nds::Recorder{plan->pev.data(), plan->pkind.data(), plan->pmode.data(), max_launches, 0};
+    plan->profiling = true;
+  });
+}
+
+int nds_plan_profile_end(nds_plan* plan, int cap, int* kinds, int* modes, float* ms) {
+  if (!plan || !plan->profiling) return -NDS_ERR_INVALID;
+  int count = 0;
+  const int rc = guarded(plan->ctx, [&] {
+    NDS_CUDA(cudaStreamSynchronize(plan->ctx->stream));
+    const nds::Recorder& r = plan->rec;
+    for (int i = 1; i < r.n && count < cap; ++i) {
+      if (r.kind[i] < 0) continue;  // step start marker
+      float t = 0.f;
+      NDS_CUDA(cudaEventElapsedTime(&t, r.ev[i - 1], r.ev[i]));
+      if (kinds) kinds[count] = r.kind[i];
+      if (modes) modes[count] = r.mode[i];
+      if (ms) ms[count] = t;
+      ++count;
+    }
+    plan->profiling = false;
+  });
+  return rc ? -rc : count;
+}
+
+int nds_solve_schur(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z* const* u, const nds_z* const* t,
+                    const nds_z* b, nds_z* x, double singular_tol, unsigned flags, nds_report* rep,
+                    nds_singular* sing) {
+  if (!ctx) return NDS_ERR_INVALID;
+  return guarded(ctx, [&] {
+    const auto t0 = Clock::now();
+    nds_plan* p = nullptr;
+    plan_create_impl(ctx, n_modes, dims, u, t, singular_tol, flags, &p, sing);
+    try {
+      execute_host_impl(p, b, x, rep);
+    } catch (...) {
+      plan_destroy_impl(p);
+      throw;
+    }
+    plan_destroy_impl(p);
+    if (rep) rep->total_seconds = secs(t0);
+  });
+}
+
+int nds_solve(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z* const* a, const nds_z* b, nds_z* x,
+              double singular_tol, unsigned flags, nds_report* rep, nds_singular* sing) {
+  if (!ctx) return NDS_ERR_INVALID;
+  return guarded(ctx, [&] {
+    const auto t0 = Clock::now();
+    checked_total(n_modes, dims, 2);
+    require_ptrs(n_modes, a, "a");
+    std::vector<std::vector<nds_z>> us(n_modes), ts(n_modes);
+    std::vector<const nds_z*> up(n_modes), tp(n_modes);
+    for (int j = 0; j < n_modes; ++j) {
+      us[j].resize(dims[j] * dims[j]);
+      ts[j].resize(dims[j] * dims[j]);
+      nds::schur_host((int)dims[j], a[j], us[j].data(), ts[j].data());
+      up[j] = us[j].data();
+      tp[j] = ts[j].data();
+    }
+    const double schur_s = secs(t0);
+    nds_plan* p = nullptr;
+    plan_create_impl(ctx, n_modes, dims, up.data(), tp.data(), singular_tol, flags, &p, sing);
+    try {
+      execute_host_impl(p, b, x, rep);
+    } catch (...) {
+      plan_destroy_impl(p);
+      throw;
+    }
+    plan_destroy_impl(p);
+    if (rep) {
+      rep->schur_seconds = schur_s;
+      rep->total_seconds = secs(t0);
+    }
+  });
+}
+
+int nds_forward_transform(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z* const* u, const nds_z* b,
+                          nds_z* c) {
+  if (!ctx) return NDS_ERR_INVALID;
+  return guarded(ctx, [&] { transform_host(ctx, n_modes, dims, u, b, c, true); });
+}
+
+int nds_inverse_transform(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z* const* u, const nds_z* y,
+                          nds_z* x) {
+  if (!ctx) return NDS_ERR_INVALID;
+  return guarded(ctx, [&] { transform_host(ctx, n_modes, dims, u, y, x, false); });
+}
+
+int nds_back_substitute(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z* const* t, nds_z* c,
+                        double singular_tol, nds_backsub_stats* stats, nds_singular* sing) {
+  if (!ctx) return NDS_ERR_INVALID;
+  return guarded(ctx, [&] {
+    // back_substitute validates order >= 1 (sylvester.cpp:71-78); the plan needs >= 1 too.
+    const int64_t total = checked_total(n_modes, dims, 1);
+    require_ptrs(n_modes, t, "t");
+    if (!c) throw Error(NDS_ERR_INVALID, "null tensor pointer");
+    ensure_device(ctx);
+    ensure_ws(ctx, total);
+    std::unique_ptr<nds_plan> p(new nds_plan);
+    p->ctx = ctx;
+    p->n_modes = n_modes;
+    std::memcpy(p->dims, dims, n_modes * sizeof(int64_t));
+    p->total = total;
+    p->tol = singular_tol;  // back_substitute takes the tolerance verbatim (no default)
+    upload_factors(ctx, p->f, n_modes, dims, nullptr, t);
+    try {
+      int64_t bad = -1;
+      nds::den_scan(p->f.geom, p->f.diag_pool, p->tol, &p->min_abs_den, &bad, ctx->stream, ctx->scratch);
+      if (bad >= 0) {
+        nds_singular tmp{};
+        fill_singular(&tmp, n_modes, dims, bad, t);
+        if (sing) *sing = tmp;
+        throw Error(NDS_ERR_SINGULAR, format_singular(tmp));
+      }
+      int64_t toff[NDS_MAX_MODES];
+      for (int j = 0; j < n_modes; ++j) toff[j] = p->f.geom.toff[j];
+      nds::solve_plan_build(p->sp, n_modes, dims, toff);
+      p->have_solve_plan = true;
+      const size_t bytes = (size_t)total * sizeof(double2);
+      NDS_CUDA(cudaMemcpyAsync(ctx->ws[0], c, bytes, cudaMemcpyHostToDevice, ctx->stream));
+      nds::backsub_launch(p->sp, p->f.t_pool, ctx->ws[0], ctx->stream);
+      NDS_CUDA(cudaMemcpyAsync(c, ctx->ws[0], bytes, cudaMemcpyDeviceToHost, ctx->stream));
+      NDS_CUDA(cudaStreamSynchronize(ctx->stream));
+      if (stats) {
+        nds_report r;
+        report_static(p.get(), &r);
+        stats->entries = r.backsub_entries;
+        stats->multiplies = r.backsub_multiplies;
+        stats->min_abs_denominator = p->min_abs_den;
+      }
+    } catch (...) {
+      plan_destroy_impl(p.release());
+      throw;
+    }
+    plan_destroy_impl(p.release());
+  });
+}
+
+int nds_mode_product(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z* m, int mode, const nds_z* x,
+                     nds_z* r) {
+  if (!ctx) return NDS_ERR_INVALID;
+  return guarded(ctx, [&] {
+    const int64_t total = checked_total(n_modes, dims, 1);
+    if (mode < 1 || mode > n_modes) throw Error(NDS_ERR_INVALID, "mode out of range");
+    if (!m || !x || !r) throw Error(NDS_ERR_INVALID, "null pointer");
+    ensure_device(ctx);
+    ensure_ws(ctx, total);
+    const int64_t n = dims[mode - 1];
+    std::vector<double2> mm(2 * n * n);
+    for (int64_t k = 0; k < n; ++k)
+      for (int64_t i = 0; i < n; ++i) {
+        const nds_z z = m[i + k * n];
+        mm[i * n + k] = make_double2(z.re, z.im);      // row-major
+        mm[n * n + i + k * n] = make_double2(z.re, z.im);  // column-major
+      }
+    double2* dm = nullptr;
+    NDS_CUDA(cudaMalloc(&dm, mm.size() * sizeof(double2)));
+    try {
+      const size_t bytes = (size_t)total * sizeof(double2);
+      NDS_CUDA(cudaMemcpyAsync(dm, mm.data(), mm.size() * sizeof(double2), cudaMemcpyHostToDevice, ctx->stream));
+      NDS_CUDA(cudaMemcpyAsync(ctx->ws[0], x, bytes, cudaMemcpyHostToDevice, ctx->stream));
+      nds::mode_product_matrix_launch(dm, dm + n * n, nds::mode_view(n_modes, dims, mode), ctx->ws[0], ctx->ws[1],
+                                      false, ctx->stream);
+      NDS_CUDA(cudaMemcpyAsync(r, ctx->ws[1], bytes, cudaMemcpyDeviceToHost, ctx->stream));
+      NDS_CUDA(cudaStreamSynchronize(ctx->stream));
+    } catch (...) {
+      cudaFree(dm);
+      throw;
+    }
+    cudaFree(dm);
+  });
+}
+
+// Upload A_j in both layouts and compute r = sum_j A_j x_j x on the device.
+static void apply_operator_dev(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z* const* a, const double2* x,
+                               double2* r) {
+  int64_t sq = 0;
+  for (int j = 0; j < n_modes; ++j) sq += dims[j] * dims[j];
+  std::vector<double2> mm(2 * sq);
+  std::vector<int64_t> off(n_modes);
+  int64_t o = 0;
+  for (int j = 0; j < n_modes; ++j) {
+    const int64_t n = dims[j];
+    off[j] = o;
+    for (int64_t k = 0; k < n; ++k)
+      for (int64_t i = 0; i < n; ++i) {
+        const nds_z z = a[j][i + k * n];
+        mm[o + i * n + k] = make_double2(z.re, z.im);
+        mm[o + n * n + i + k * n] = make_double2(z.re, z.im);
+      }
+    o += 2 * n * n;
+  }
+  double2* dm = nullptr;
+  NDS_CUDA(cudaMalloc(&dm, mm.size() * sizeof(double2)));
+  try {
+    NDS_CUDA(cudaMemcpyAsync(dm, mm.data(), mm.size() * sizeof(double2), cudaMemcpyHostToDevice, ctx->stream));
+    for (int j = 1; j <= n_modes; ++j) {
+      const int64_t n = dims[j - 1];
+      nds::mode_product_matrix_launch(dm + off[j - 1], dm + off[j - 1] + n * n, nds::mode_view(n_modes, dims, j), x, r,
+                                      j > 1, ctx->stream);
+    }
+    NDS_CUDA(cudaStreamSynchronize(ctx->stream));
+  } catch (...) {
+    cudaFree(dm);
+    throw;
+  }
+  cudaFree(dm);
+}
+
+int nds_apply_operator(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z* const* a, const nds_z* x,
+                       nds_z* r) {
+  if (!ctx) return NDS_ERR_INVALID;
+  return guarded(ctx, [&] {
+    const int64_t total = checked_total(n_modes, dims, 1);
+    require_ptrs(n_modes, a, "a");
+    if (!x || !r) throw Error(NDS_ERR_INVALID, "null pointer");
+    ensure_device(ctx);
+    ensure_ws(ctx, total);
+    const size_t bytes = (size_t)total * sizeof(double2);
+    NDS_CUDA(cudaMemcpyAsync(ctx->ws[0], x, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    apply_operator_dev(ctx, n_modes, dims, a, ctx->ws[0], ctx->ws[1]);
+    NDS_CUDA(cudaMemcpyAsync(r, ctx->ws[1], bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    NDS_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int nds_dev_mode_product(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z* d_m, int mode,
+                         int conj_transpose, const nds_z* d_x, nds_z* d_r, int accumulate) {
+  if (!ctx) return NDS_ERR_INVALID;
+  return guarded(ctx, [&] {
+    checked_total(n_modes, dims, 1);
+    if (mode < 1 || mode > n_modes) throw Error(NDS_ERR_INVALID, "mode out of range");
+    if (!d_m || !d_x || !d_r) throw Error(NDS_ERR_INVALID, "null pointer");
+    ensure_device(ctx);
+    const int64_t n = dims[mode - 1];
+    std::vector<nds_z> hm(n * n);
+    NDS_CUDA(cudaMemcpyAsync(hm.data(), d_m, n * n * sizeof(nds_z), cudaMemcpyDeviceToHost, ctx->stream));
+    NDS_CUDA(cudaStreamSynchronize(ctx->stream));
+    std::vector<double2> mm(2 * n * n);
+    for (int64_t k = 0; k < n; ++k)
+      for (int64_t i = 0; i < n; ++i) {
+        nds_z z = conj_transpose ? hm[k + i * n] : hm[i + k * n];  // op(M)(i, k)
+        if (conj_transpose) z.im = -z.im;
+        mm[i * n + k] = make_double2(z.re, z.im);
+        mm[n * n + i + k * n] = make_double2(z.re, z.im);
+      }
+    double2* dm = nullptr;
+    NDS_CUDA(cudaMalloc(&dm, mm.size() * sizeof(double2)));
+    NDS_CUDA(cudaMemcpyAsync(dm, mm.data(), mm.size() * sizeof(double2), cudaMemcpyHostToDevice, ctx->stream));
+    nds::mode_product_matrix_launch(dm, dm + n * n, nds::mode_view(n_modes, dims, mode), (const double2*)d_x,
+                                    (double2*)d_r, accumulate != 0, ctx->stream);
+    NDS_CUDA(cudaStreamSynchronize(ctx->stream));
+    cudaFree(dm);
+  });
+}
+
+int nds_dev_residual(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z* const* a, const nds_z* d_x,
+                     const nds_z* d_b, double* res_max, double* res_2, double* b_max, double* b_2) {
+  if (!ctx) return NDS_ERR_INVALID;
+  return guarded(ctx, [&] {
+    const int64_t total = checked_total(n_modes, dims, 1);
+    require_ptrs(n_modes, a, "a");
+    if (!d_x || !d_b) throw Error(NDS_ERR_INVALID, "null pointer");
+    ensure_device(ctx);
+    double2* r = nullptr;
+    NDS_CUDA(cudaMalloc(&r, (size_t)total * sizeof(double2)));
+    try {
+      apply_operator_dev(ctx, n_modes, dims, a, (const double2*)d_x, r);
+      double rm, r2, bm, b2;
+      nds::residual_norms(r, (const double2*)d_b, total, &rm, &r2, &bm, &b2, ctx->stream);
+      if (res_max) *res_max = rm;
+      if (res_2) *res_2 = r2;
+      if (b_max) *b_max = bm;
+      if (b_2) *b_2 = b2;
+    } catch (...) {
+      cudaFree(r);
+      throw;
+    }
+    cudaFree(r);
+  });
+}
+
+// sylvester.cpp:229-241
+int64_t nds_flop_estimate(int n_modes, const int64_t* dims) {
+  if (n_modes < 1 || !dims) return -1;
+  int64_t total = 1, sum = 0, factor = 0, flops = 0;
+  for (int j = 0; j < n_modes; ++j) {
+    if (dims[j] < 1) return -1;
+    if (__builtin_mul_overflow(total, dims[j], &total) || __builtin_add_overflow(sum, dims[j], &sum)) return -1;
+  }
+  if (__builtin_mul_overflow(sum, (int64_t)5, &factor) ||
+      __builtin_add_overflow(factor, (int64_t)1 - (int64_t)n_modes, &factor) ||
+      __builtin_mul_overflow(total, factor, &flops))
+    return -1;
+  return flops;
+}
+
+// sylvester.cpp:243-257
+int64_t nds_schur_flop_estimate(int n_modes, const int64_t* dims) {
+  if (n_modes < 1 || !dims) return -1;
+  int64_t total = 1, sum_cubes = 0, flops = 0;
+  for (int j = 0; j < n_modes; ++j) {
+    int64_t sq = 0, cube = 0;
+    if (dims[j] < 1 || __builtin_mul_overflow(total, dims[j], &total)) return -1;
+    if (__builtin_mul_overflow(dims[j], dims[j], &sq) || __builtin_mul_overflow(sq, dims[j], &cube) ||
+        __builtin_add_overflow(sum_cubes, cube, &sum_cubes))
+      return -1;
+  }
+  if (__builtin_mul_overflow(sum_cubes, (int64_t)25, &flops)) return -1;
+  return flops;
+}
+
+void nds_randn(uint64_t seed, uint64_t stream, int64_t count, double* out) { nds::randn_host(seed, stream, count, out); }
+
+}  // extern "C"

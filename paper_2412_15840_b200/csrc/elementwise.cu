@@ -1,0 +1,151 @@
+// Entry-wise kernels of the solve path.
+//   den_scan      — singular check + min |den| (sylvester.cpp:101-103, :119-141): den(i) =
+//                   sum_j T_j(i_j, i_j) accumulated j = 1..N from 0, |den| = hypot.
+//   fast_divide   — normal-coefficient route, c /= den (sylvester.cpp:190-204).
+//   real_part     — SolveOptions::real_output (sylvester.cpp:223-224).
+//   residual_norms — verification of sum_j A_j x_j X = B on the device (apply_operator,
+//                   sylvester.cpp:44-53, is the mode-product kernel with accumulate).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace nds {
+
+constexpr int kEwThreads = 256;
+
+__device__ __forceinline__ double2 den_at(const Geom& g, const double2* __restrict__ diag, int64_t idx) {
+  double2 den = make_double2(0.0, 0.0);
+  for (int j = 0; j < g.n_modes; ++j) {
+    const int64_t ij = idx % g.dims[j];
+    idx /= g.dims[j];
+    den = cadd(den, __ldg(diag + g.doff[j] + ij));
+  }
+  return den;
+}
+
+__global__ void den_scan_kernel(const Geom g, const double2* __restrict__ diag, double tol,
+                                unsigned long long* __restrict__ min_bits, long long* __restrict__ max_bad) {
+  double local_min = INFINITY;
+  long long local_bad = -1;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < g.total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const double2 den = den_at(g, diag, idx);
+    const double a = hypot(den.x, den.y);
+    local_min = fmin(local_min, a);
+    if (a <= tol) local_bad = max(local_bad, (long long)idx);  // sylvester.cpp:103 (NaN passes)
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    local_min = fmin(local_min, __shfl_xor_sync(0xffffffffu, local_min, o));
+    local_bad = max(local_bad, __shfl_xor_sync(0xffffffffu, local_bad, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(min_bits, (unsigned long long)__double_as_longlong(local_min));  // non-negative: int order
+    if (local_bad >= 0) atomicMax(max_bad, local_bad);
+  }
+}
+
+void den_scan(const Geom& g, const double2* diag, double tol, double* min_abs, int64_t* max_bad, cudaStream_t stream,
+              void* scratch) {
+  unsigned long long* d_min = (unsigned long long*)scratch;
+  long long* d_bad = (long long*)((char*)scratch + 8);
+  const unsigned long long init_min = (unsigned long long)0x7ff0000000000000ull;  // +inf
+  const long long init_bad = -1;
+  NDS_CUDA(cudaMemcpyAsync(d_min, &init_min, 8, cudaMemcpyHostToDevice, stream));
+  NDS_CUDA(cudaMemcpyAsync(d_bad, &init_bad, 8, cudaMemcpyHostToDevice, stream));
+  const int64_t blocks = std::min<int64_t>((g.total + kEwThreads - 1) / kEwThreads, 148 * 32);
+  den_scan_kernel<<<(unsigned)blocks, kEwThreads, 0, stream>>>(g, diag, tol, d_min, d_bad);
+  NDS_LAUNCH_CHECK();
+  unsigned long long h_min;
+  long long h_bad;
+  NDS_CUDA(cudaMemcpyAsync(&h_min, d_min, 8, cudaMemcpyDeviceToHost, stream));
+  NDS_CUDA(cudaMemcpyAsync(&h_bad, d_bad, 8, cudaMemcpyDeviceToHost, stream));
+  NDS_CUDA(cudaStreamSynchronize(stream));
+  long long bits = (long long)h_min;
+  double m;
+  memcpy(&m, &bits, 8);
+  *min_abs = m;
+  *max_bad = h_bad;
+}
+
+__global__ void fast_divide_kernel(const Geom g, const double2* __restrict__ diag, double2* __restrict__ c) {
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < g.total;
+       idx += (int64_t)gridDim.x * blockDim.x)
+    c[idx] = cdiv(c[idx], den_at(g, diag, idx));
+}
+
+int fast_divide_launch(const Geom& g, const double2* diag, double2* c, cudaStream_t stream) {
+  const int64_t blocks = std::min<int64_t>((g.total + kEwThreads - 1) / kEwThreads, 148 * 32);
+  fast_divide_kernel<<<(unsigned)blocks, kEwThreads, 0, stream>>>(g, diag, c);
+  NDS_LAUNCH_CHECK();
+  return 1;
+}
+
+__global__ void real_part_kernel(double2* __restrict__ x, int64_t total) {
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x)
+    x[idx].y = 0.0;
+}
+
+int real_part_launch(double2* x, int64_t total, cudaStream_t stream) {
+  const int64_t blocks = std::min<int64_t>((total + kEwThreads - 1) / kEwThreads, 148 * 32);
+  real_part_kernel<<<(unsigned)blocks, kEwThreads, 0, stream>>>(x, total);
+  NDS_LAUNCH_CHECK();
+  return 1;
+}
+
+constexpr int kResBlocks = 148 * 8;
+
+__global__ void residual_kernel(const double2* __restrict__ r, const double2* __restrict__ b, int64_t total,
+                                double* __restrict__ part) {
+  double rmax = 0.0, r2 = 0.0, bmax = 0.0, b2 = 0.0;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const double2 bv = b[idx];
+    const double2 d = csub(r[idx], bv);
+    const double ad = hypot(d.x, d.y), ab = hypot(bv.x, bv.y);
+    rmax = fmax(rmax, ad);
+    bmax = fmax(bmax, ab);
+    r2 += ad * ad;
+    b2 += ab * ab;
+  }
+  __shared__ double sh[4][kEwThreads];
+  sh[0][threadIdx.x] = rmax;
+  sh[1][threadIdx.x] = r2;
+  sh[2][threadIdx.x] = bmax;
+  sh[3][threadIdx.x] = b2;
+  __syncthreads();
+  for (int s = kEwThreads / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) {
+      sh[0][threadIdx.x] = fmax(sh[0][threadIdx.x], sh[0][threadIdx.x + s]);
+      sh[1][threadIdx.x] += sh[1][threadIdx.x + s];
+      sh[2][threadIdx.x] = fmax(sh[2][threadIdx.x], sh[2][threadIdx.x + s]);
+      sh[3][threadIdx.x] += sh[3][threadIdx.x + s];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x < 4) part[blockIdx.x * 4 + threadIdx.x] = sh[threadIdx.x][0];
+}
+
+void residual_norms(const double2* r, const double2* b, int64_t total, double* res_max, double* res_2, double* b_max,
+                    double* b_2, cudaStream_t stream) {
+  double* d_part;
+  NDS_CUDA(cudaMallocAsync(&d_part, kResBlocks * 4 * sizeof(double), stream));
+  residual_kernel<<<kResBlocks, kEwThreads, 0, stream>>>(r, b, total, d_part);
+  NDS_LAUNCH_CHECK();
+  std::vector<double> part(kResBlocks * 4);
+  NDS_CUDA(cudaMemcpyAsync(part.data(), d_part, part.size() * sizeof(double), cudaMemcpyDeviceToHost, stream));
+  NDS_CUDA(cudaFreeAsync(d_part, stream));
+  NDS_CUDA(cudaStreamSynchronize(stream));
+  double rm = 0, rs = 0, bm = 0, bs = 0;
+  for (int i = 0; i < kResBlocks; ++i) {
+    rm = std::max(rm, part[i * 4 + 0]);
+    rs += part[i * 4 + 1];
+    bm = std::max(bm, part[i * 4 + 2]);
+    bs += part[i * 4 + 3];
+  }
+  *res_max = rm;
+  *res_2 = std::sqrt(rs);
+  *b_max = bm;
+  *b_2 = std::sqrt(bs);
+}
+
+}  // namespace nds

@@ -1,0 +1,96 @@
+// Internal launch interface between the C-ABI layer (capi.cu) and the kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <vector>
+
+#include "common.cuh"
+
+namespace nds {
+
+// Device copies of the Schur factors of one problem. Every U_j is kept in the four layouts the
+// transform kernels read without a permutation pass: M row-major / column-major for M = U_j
+// (inverse transform) and M = U_j^H (forward transform).
+struct FactorSet {
+  int n_modes = 0;
+  int64_t dims[NDS_MAX_MODES] = {};
+  double2* u_row[NDS_MAX_MODES] = {};
+  double2* u_col[NDS_MAX_MODES] = {};
+  double2* uh_row[NDS_MAX_MODES] = {};
+  double2* uh_col[NDS_MAX_MODES] = {};
+  double2* pool = nullptr;  // one allocation backing all of the above + T + diag
+  double2* t_pool = nullptr;     // T_j column-major, concatenated (offsets in geom.toff)
+  double2* diag_pool = nullptr;  // diag(T_j), concatenated (offsets in geom.doff)
+  Geom geom{};
+};
+
+// Launch classes (for the per-launch profile read back by bench.py).
+enum LaunchKind { kXformGemm = 0, kXformDirect = 1, kBacksubLevel = 2, kElementwise = 3, kBacksubPersistent = 4 };
+
+// Optional CUDA-event recorder: one event after every launch (ev[0] is the start marker).
+struct Recorder {
+  cudaEvent_t* ev = nullptr;
+  int* kind = nullptr;
+  int* mode = nullptr;
+  int cap = 0;
+  int n = 0;
+  void mark(cudaStream_t s, int k, int m) {
+    if (ev && n < cap) {
+      cudaEventRecord(ev[n], s);
+      kind[n] = k;
+      mode[n] = m;
+      ++n;
+    }
+  }
+};
+
+// r = M x_mode x (+ r), M = U_mode or U_mode^H. One launch; returns its LaunchKind.
+int mode_product_launch(const FactorSet& f, int mode, bool adjoint, const ModeView& v, const double2* x, double2* r,
+                        bool accumulate, cudaStream_t stream);
+
+// Plain matrix variant (apply_operator / residual): m_row, m_col are the two layouts of M.
+int mode_product_matrix_launch(const double2* m_row, const double2* m_col, const ModeView& v, const double2* x,
+                               double2* r, bool accumulate, cudaStream_t stream);
+
+// ---- triangular solve --------------------------------------------------------------------
+struct TileGeom {
+  int n_modes;
+  int tile_entries;  // prod b_j
+  int64_t dims[NDS_MAX_MODES];
+  int64_t strides[NDS_MAX_MODES];
+  int64_t nb[NDS_MAX_MODES];  // blocks per mode
+  int64_t toff[NDS_MAX_MODES];
+  int b[NDS_MAX_MODES];       // tile extent per mode
+  int bstride[NDS_MAX_MODES]; // strides inside a full tile
+};
+
+struct SolvePlan {
+  TileGeom geom{};
+  int levels = 0;                 // tile hyperplanes: sum_j (nb_j - 1) + 1
+  std::vector<int64_t> level_off; // host copy, size levels + 1
+  int64_t* d_tiles = nullptr;     // tile ids sorted by descending level
+  int wf_levels = 0;              // hyperplanes inside a full tile
+  int* d_wf = nullptr;            // local entries sorted by descending local level
+  int* d_wf_off = nullptr;
+  void* pool = nullptr;
+};
+
+void solve_plan_build(SolvePlan& sp, int n_modes, const int64_t* dims, const int64_t* toff);
+void solve_plan_free(SolvePlan& sp);
+// In-place Y over C. Returns kernels launched.
+int backsub_launch(const SolvePlan& sp, const double2* t_pool, double2* c, cudaStream_t stream,
+                   Recorder* rec = nullptr);
+
+// ---- elementwise / reductions ------------------------------------------------------------
+// min |den| over all entries and the largest flat index with |den| <= tol (-1 if none).
+void den_scan(const Geom& g, const double2* diag, double tol, double* min_abs, int64_t* max_bad, cudaStream_t stream,
+              void* scratch /* >= 16 bytes device */);
+int fast_divide_launch(const Geom& g, const double2* diag, double2* c, cudaStream_t stream);
+int real_part_launch(double2* x, int64_t total, cudaStream_t stream);
+// Max-abs and sum-of-squares of (r - b) and of b, deterministic (per-block partials).
+void residual_norms(const double2* r, const double2* b, int64_t total, double* res_max, double* res_2, double* b_max,
+                    double* b_2, cudaStream_t stream);
+
+}  // namespace nds

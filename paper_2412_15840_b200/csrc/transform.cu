@@ -1,0 +1,303 @@
+// Mode-j tensor-times-matrix (TTM) kernels for the forward / inverse transforms
+// (reference: kernels.cpp:24-44 mode_product_impl, driven by sylvester.cpp:55-69).
+//
+// On the column-major (inner, n, outer) view of mode j (kernels.cpp:9-21) the product
+//   R[a, i, b] = sum_k M[i, k] X[a, k, b]
+// is a strided-batched complex GEMM with no permutation pass:
+//   * inner >= 8  ("ROWM"): C(i, c) = M(i, :) . X(:, c), columns c = (a, b) read straight from the
+//     tensor's native strides, a contiguous;
+//   * inner == 1  ("COLM", mode 1): C(b, i) = X(b, :) . M^T(:, i), rows of X contiguous in k;
+//   * otherwise (tiny inner, e.g. n_1 < 8): a direct kernel.
+// The GEMM runs on the FP64 tensor pipe (DMMA, mma.sync.m8n8k4.f64): measured 37.1 TF on B200
+// vs 34.1 TF for DFMA (tools/microbench/fp64_peaks.cu, profiles/). Complex products use four
+// real DMMAs per 8x8x4 block (re.re, -im.im, re.im, im.re) accumulated in registers; tiles are
+// staged global->shared with a multi-stage cp.async pipeline into bank-conflict-free padded
+// layouts (row strides = 4 resp. 2 mod 8 complex for the DMMA fragment pattern).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace nds {
+
+// ------------------------------------------------------------------------------------------
+// Direct kernel: one output entry per thread. Used for 1 < inner < 8 or tiny n.
+// ------------------------------------------------------------------------------------------
+__global__ void mode_product_direct_kernel(const double2* __restrict__ mcol, int64_t inner, int n, int64_t outer,
+                                           const double2* __restrict__ x, double2* __restrict__ r, int accumulate) {
+  const int64_t total = inner * n * outer;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a = idx % inner;
+    const int64_t t = idx / inner;
+    const int i = (int)(t % n);
+    const int64_t b = t / n;
+    const double2* xp = x + b * n * inner + a;
+    double2 s = make_double2(0.0, 0.0);
+    for (int k = 0; k < n; ++k) s = cfma(s, __ldg(mcol + i + (int64_t)k * n), __ldg(xp + (int64_t)k * inner));
+    if (accumulate) s = cadd(r[idx], s);
+    r[idx] = s;
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// DMMA complex GEMM
+// ------------------------------------------------------------------------------------------
+struct GemmArgs {
+  const double2* A;  // A(r, k) = A[r * lda + k]
+  int64_t lda;
+  int64_t rows;      // rows of A and C
+  const double2* B;  // B(k, a, b) = B[k * ldbk + a + b * ldbb]
+  int64_t ldbk, ldbb;
+  double2* C;        // C(r, a, b) = C[r * ldcr + a + b * ldcb]
+  int64_t ldcr, ldcb;
+  int K;
+  int wshift;        // tile column c = a' + (b' << wshift)
+  int64_t alim, blim;
+  int64_t ntile_rows, ntile_a;
+  int accumulate;
+};
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+
+template <int BM, int BN, int BK, int WM, int WN, int STAGES>
+struct GemmCfg {
+  static constexpr int kThreads = WM * WN * 32;
+  static constexpr int kLdA = BK + 4;  // complex; = 4 mod 8 -> conflict-free A fragments
+  static constexpr int kLdB = BN + 2;  // complex; = 2 mod 8 -> conflict-free B fragments
+  static constexpr int kStageA = BM * kLdA;
+  static constexpr int kStageB = BK * kLdB;
+  static constexpr size_t kSmem = (size_t)STAGES * (kStageA + kStageB) * sizeof(double2);
+  static constexpr int MI = BM / WM / 8;
+  static constexpr int NI = BN / WN / 8;
+};
+
+template <int BM, int BN, int BK, int WM, int WN, int STAGES>
+__global__ void __launch_bounds__(WM* WN * 32, 1) zgemm_dmma_kernel(const GemmArgs g) {
+  using Cfg = GemmCfg<BM, BN, BK, WM, WN, STAGES>;
+  constexpr int NT = Cfg::kThreads;
+  constexpr int MI = Cfg::MI, NI = Cfg::NI;
+  extern __shared__ __align__(16) double2 smem[];
+  double2* sA = smem;
+  double2* sB = smem + STAGES * Cfg::kStageA;
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int wy = warp / WN, wx = warp % WN;
+
+  const int64_t tile = blockIdx.x;
+  const int64_t row_tile = tile % g.ntile_rows;
+  const int64_t col_tile = tile / g.ntile_rows;
+  const int64_t row0 = row_tile * BM;
+  const int64_t a0 = (col_tile % g.ntile_a) << g.wshift;
+  const int64_t b0 = (col_tile / g.ntile_a) * (BN >> g.wshift);
+  const int wmask = (1 << g.wshift) - 1;
+
+  auto load_stage = [&](int stage, int k0) {
+    double2* dA = sA + stage * Cfg::kStageA;
+    double2* dB = sB + stage * Cfg::kStageB;
+#pragma unroll
+    for (int e = tid; e < BM * BK; e += NT) {
+      const int r = e / BK, k = e % BK;
+      const int64_t gr = row0 + r;
+      const int gk = k0 + k;
+      const bool ok = gr < g.rows && gk < g.K;
+      const double2* src = ok ? g.A + gr * g.lda + gk : g.A;
+      cp_async16(dA + r * Cfg::kLdA + k, src, ok ? 16 : 0);
+    }
+#pragma unroll
+    for (int e = tid; e < BK * BN; e += NT) {
+      const int c = e % BN, k = e / BN;
+      const int64_t ga = a0 + (c & wmask);
+      const int64_t gb = b0 + (c >> g.wshift);
+      const int gk = k0 + k;
+      const bool ok = gk < g.K && ga < g.alim && gb < g.blim;
+      const double2* src = ok ? g.B + (int64_t)gk * g.ldbk + ga + gb * g.ldbb : g.B;
+      cp_async16(dB + k * Cfg::kLdB + c, src, ok ? 16 : 0);
+    }
+  };
+
+  double cre[MI][NI][2], cim[MI][NI][2];
+#pragma unroll
+  for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < NI; ++ni) cre[mi][ni][0] = cre[mi][ni][1] = cim[mi][ni][0] = cim[mi][ni][1] = 0.0;
+
+  const int nk = (g.K + BK - 1) / BK;
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < nk) load_stage(s, s * BK);
+    cp_async_commit();
+  }
+
+  const int arow = wy * (BM / WM) + (lane >> 2);
+  const int bcol = wx * (BN / WN) + (lane >> 2);
+  const int kq = lane & 3;
+
+  for (int kt = 0; kt < nk; ++kt) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    {
+      const int nxt = kt + STAGES - 1;
+      if (nxt < nk) load_stage(nxt % STAGES, nxt * BK);
+      cp_async_commit();
+    }
+    const double2* cA = sA + (kt % STAGES) * Cfg::kStageA;
+    const double2* cB = sB + (kt % STAGES) * Cfg::kStageB;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double ar[MI], ai[MI], an[MI], br[NI], bi[NI];
+#pragma unroll
+      for (int mi = 0; mi < MI; ++mi) {
+        const double2 v = cA[(arow + mi * 8) * Cfg::kLdA + kk + kq];
+        ar[mi] = v.x;
+        ai[mi] = v.y;
+        an[mi] = -v.y;
+      }
+#pragma unroll
+      for (int ni = 0; ni < NI; ++ni) {
+        const double2 v = cB[(kk + kq) * Cfg::kLdB + bcol + ni * 8];
+        br[ni] = v.x;
+        bi[ni] = v.y;
+      }
+#pragma unroll
+      for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < NI; ++ni) {
+          dmma(cre[mi][ni][0], cre[mi][ni][1], ar[mi], br[ni]);
+          dmma(cim[mi][ni][0], cim[mi][ni][1], ar[mi], bi[ni]);
+          dmma(cre[mi][ni][0], cre[mi][ni][1], an[mi], bi[ni]);
+          dmma(cim[mi][ni][0], cim[mi][ni][1], ai[mi], br[ni]);
+        }
+    }
+  }
+  cp_async_wait<0>();
+
+  // Epilogue: lane holds C[r][2q], C[r][2q+1] of each 8x8 fragment.
+#pragma unroll
+  for (int mi = 0; mi < MI; ++mi) {
+    const int64_t r = row0 + wy * (BM / WM) + mi * 8 + (lane >> 2);
+    if (r >= g.rows) continue;
+#pragma unroll
+    for (int ni = 0; ni < NI; ++ni) {
+      const int c = wx * (BN / WN) + ni * 8 + 2 * kq;
+      const int64_t ga = a0 + (c & wmask);
+      const int64_t gb = b0 + (c >> g.wshift);
+      if (gb >= g.blim) continue;
+      double2* dst = g.C + r * g.ldcr + ga + gb * g.ldcb;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (ga + h < g.alim) {
+          double2 v = make_double2(cre[mi][ni][h], cim[mi][ni][h]);
+          if (g.accumulate) v = cadd(dst[h], v);
+          dst[h] = v;
+        }
+      }
+    }
+  }
+}
+
+// Tile configuration: 64 x 128 complex per CTA, 8 warps of 32 x 32, BK = 16,
+// 3-stage pipeline (160 KB smem, 1 CTA / SM).
+constexpr int kBM = 64, kBN = 128, kBK = 16, kWM = 2, kWN = 4, kStages = 3;
+using MainCfg = GemmCfg<kBM, kBN, kBK, kWM, kWN, kStages>;
+
+static void launch_gemm(GemmArgs g, cudaStream_t stream) {
+  static bool attr_set = false;
+  auto kern = zgemm_dmma_kernel<kBM, kBN, kBK, kWM, kWN, kStages>;
+  if (!attr_set) {
+    NDS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)MainCfg::kSmem));
+    attr_set = true;
+  }
+  g.ntile_rows = (g.rows + kBM - 1) / kBM;
+  const int64_t W = 1ll << g.wshift;
+  g.ntile_a = (g.alim + W - 1) / W;
+  const int64_t bb = kBN / W;
+  const int64_t ntile_b = (g.blim + bb - 1) / bb;
+  const int64_t tiles = g.ntile_rows * g.ntile_a * ntile_b;
+  kern<<<(unsigned)tiles, MainCfg::kThreads, MainCfg::kSmem, stream>>>(g);
+  NDS_LAUNCH_CHECK();
+}
+
+// Column split for ROWM: power of two W in [8, kBN] minimising padded columns (ties -> wider).
+static int pick_wshift(int64_t inner) {
+  int best = 3;
+  double best_waste = 1e30;
+  for (int s = 3; (1 << s) <= kBN; ++s) {
+    const int64_t w = 1ll << s;
+    const double waste = (double)(((inner + w - 1) / w) * w) / (double)inner;
+    if (waste <= best_waste + 1e-12) {
+      best_waste = waste;
+      best = s;
+    }
+  }
+  return best;
+}
+
+int mode_product_launch(const FactorSet& f, int mode, bool adjoint, const ModeView& v, const double2* x, double2* r,
+                        bool accumulate, cudaStream_t stream) {
+  const double2* mrow = adjoint ? f.uh_row[mode - 1] : f.u_row[mode - 1];
+  const double2* mcol = adjoint ? f.uh_col[mode - 1] : f.u_col[mode - 1];
+  return mode_product_matrix_launch(mrow, mcol, v, x, r, accumulate, stream);
+}
+
+int mode_product_matrix_launch(const double2* mrow, const double2* mcol, const ModeView& v, const double2* x,
+                               double2* r, bool accumulate, cudaStream_t stream) {
+  const int n = (int)v.n;
+  const bool gemm = n >= 16 && (v.inner == 1 || v.inner >= 8);
+  if (!gemm) {
+    const int64_t total = v.inner * v.n * v.outer;
+    const int threads = 256;
+    const int64_t blocks = std::min<int64_t>((total + threads - 1) / threads, 148 * 16);
+    mode_product_direct_kernel<<<(unsigned)blocks, threads, 0, stream>>>(mcol, v.inner, n, v.outer, x, r,
+                                                                        accumulate ? 1 : 0);
+    NDS_LAUNCH_CHECK();
+    return kXformDirect;
+  }
+  GemmArgs g{};
+  g.K = n;
+  g.accumulate = accumulate ? 1 : 0;
+  if (v.inner == 1) {  // COLM: C(b, i) = X(b, :) . M^T(:, i)
+    g.A = x;
+    g.lda = n;
+    g.rows = v.outer;
+    g.B = mcol;  // B(k, i) = M[i][k] = mcol[i + k n]
+    g.ldbk = n;
+    g.ldbb = 0;
+    g.wshift = 7;  // one column slice of width kBN
+    g.alim = n;
+    g.blim = 1;
+    g.C = r;
+    g.ldcr = n;
+    g.ldcb = 0;
+  } else {  // ROWM: C(i, (a, b)) = M(i, :) . X(:, (a, b))
+    g.A = mrow;  // A(i, k) = M[i][k] = mrow[i n + k]
+    g.lda = n;
+    g.rows = n;
+    g.B = x;
+    g.ldbk = v.inner;
+    g.ldbb = v.inner * n;
+    g.wshift = pick_wshift(v.inner);
+    g.alim = v.inner;
+    g.blim = v.outer;
+    g.C = r;
+    g.ldcr = v.inner;
+    g.ldcb = v.inner * n;
+  }
+  launch_gemm(g, stream);
+  return kXformGemm;
+}
+
+}  // namespace nds
