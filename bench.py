@@ -206,7 +206,10 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     ctx = nds.Context(local)
-    stream = torch.cuda.current_stream(dev)
+    # A dedicated stream: torch's legacy default stream has handle 0, which the C ABI reads as
+    # "use the context's own stream". Kernels and the timing events share this stream.
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
 
     # --- inputs (host, generator v1) and host Schur setup -------------------------------------

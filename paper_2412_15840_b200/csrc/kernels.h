@@ -74,7 +74,16 @@ struct SolvePlan {
   int wf_levels = 0;              // hyperplanes inside a full tile
   int* d_wf = nullptr;            // local entries sorted by descending local level
   int* d_wf_off = nullptr;
+  int* d_wf_group = nullptr;      // lanes per entry for each local hyperplane (v2)
   void* pool = nullptr;
+  // v2 (GEMM regime: every b_j a power of two >= 8 dividing n_j): per level, DMMA update work
+  // items (tile, mode, k-range) writing partials, then one diagonal-tile kernel.
+  bool v2 = false;
+  std::vector<int64_t> item_off;  // per level, into d_items (host copy), size levels + 1
+  int4* d_items = nullptr;        // {tile slot (global), mode, k_begin, k_end}
+  int2* d_tile_items = nullptr;   // per tile slot: {first item (global), count}
+  double2* d_partial = nullptr;   // max items per level x tile_entries
+  int64_t max_level_items = 0;
 };
 
 void solve_plan_build(SolvePlan& sp, int n_modes, const int64_t* dims, const int64_t* toff);
