@@ -1,0 +1,389 @@
+// v2 of the blocked triangular solve — GEMM regime: cubic tiles of B^N = 4096 entries with B a
+// in {8, 16} dividing every n_j (c0, c1: N=3 B=16; c2, c3: N=4 B=8).
+// Included by backsub.cu.
+
+constexpr int kUpdThreads = 256;
+constexpr int kALd = 12;  // A stage row stride (complex): = 4 mod 8 -> conflict-free fragments
+
+
+__device__ __forceinline__ void cp_async16_bs(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_commit_bs() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_wait1_bs() { asm volatile("cp.async.wait_group 1;\n" ::); }
+__device__ __forceinline__ void cp_wait0_bs() { asm volatile("cp.async.wait_group 0;\n" ::); }
+
+__device__ __forceinline__ void dmma_bs(double& c0, double& c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+
+// Off-tile coupling of one work item (tile I, mode j, rows [kb, ke) along mode j) as a small
+// complex GEMM on the FP64 tensor pipe:
+//   partial(l_j, c) = sum_{k in [kb, ke)} T_j(o_j + l_j, k) * Y(k along mode j, c),
+// rows l_j (b_j = 8 RB), columns c = the other local coordinates of the tile (cols = 4096 / b_j),
+// K streamed from global through a 3-stage cp.async ring of BK = 2048 / cols rows (32 KB).
+// Every thread owns 8 fixed (k, c) slots of each stage; their global / shared offsets are
+// computed once. Each warp owns RB x CB fragments (8x8) and reuses its A/B fragments across
+// them. The partial is written in tile-local column-major order for the diagonal kernel.
+template <int RB, int CB>
+__global__ void __launch_bounds__(kUpdThreads, 2)
+    tile_update_kernel(const TileGeom g, const double2* __restrict__ T, const int64_t* __restrict__ tiles,
+                       const int4* __restrict__ items, double2* __restrict__ partial, const double2* __restrict__ Y) {
+  constexpr int BJ = 8 * RB;
+  constexpr int COLS = 4096 / BJ;
+  constexpr int BK = 2048 / COLS;
+  constexpr int LDB = COLS + 2;  // = 2 mod 8 -> conflict-free B fragments
+  static_assert(RB * CB == 8 && BK % 4 == 0, "tile shape");
+  extern __shared__ __align__(16) double2 sm[];
+  __shared__ int64_t so[NDS_MAX_MODES];
+  __shared__ int64_t s_base;
+  const int4 it = items[blockIdx.x];
+  const int j = it.y, kb = it.z, ke = it.w;
+  const int N = g.n_modes;
+  int64_t* colg = (int64_t*)sm;  // global offset of column c
+  int* coll = (int*)(colg + COLS);
+  double2* sA = (double2*)(coll + COLS);  // [3][BJ][kALd]
+  double2* sB = sA + 3 * BJ * kALd;       // [3][BK][LDB]
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    int64_t t = tiles[it.x];
+    int64_t base = 0;
+    for (int m = 0; m < N; ++m) {
+      const int64_t I = t % g.nb[m];
+      t /= g.nb[m];
+      so[m] = I * g.b[m];
+      if (m != j) base += so[m] * g.strides[m];
+    }
+    s_base = base;
+  }
+  for (int c = tid; c < COLS; c += kUpdThreads) {  // c: local coords of modes != j, earliest fastest
+    int rem = c;
+    int64_t og = 0;
+    int ol = 0;
+    for (int m = 0; m < N; ++m) {
+      if (m == j) continue;
+      const int lm = rem % BJ;
+      rem /= BJ;
+      og += lm * g.strides[m];
+      ol += lm * g.bstride[m];
+    }
+    colg[c] = og;
+    coll[c] = ol;
+  }
+  __syncthreads();
+  const int64_t sj = g.strides[j];
+  const double2* Yb = Y + s_base;
+  const double2* Tj = T + g.toff[j] + so[j];
+  const int64_t nj = g.dims[j];
+
+  // fixed per-thread load slots
+  int64_t gofs[8];
+  int sofs[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int e = tid + i * kUpdThreads;
+    int k, c;
+    if (j == 0) {  // mode 1 is contiguous along k: k fastest
+      k = e % BK;
+      c = e / BK;
+    } else {
+      c = e % COLS;
+      k = e / COLS;
+    }
+    gofs[i] = (int64_t)k * sj + colg[c];
+    sofs[i] = k * LDB + c;
+  }
+  const bool a_loader = tid < BJ * BK;
+  const int a_r = tid / BK, a_k = tid % BK;
+
+  auto load_stage = [&](int stage, int k0) {
+    double2* dB = sB + stage * BK * LDB;
+    const double2* src = Yb + (int64_t)k0 * sj;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) cp_async16_bs(dB + sofs[i], src + gofs[i]);
+    if (a_loader) cp_async16_bs(sA + stage * BJ * kALd + a_r * kALd + a_k, Tj + a_r + (int64_t)(k0 + a_k) * nj);
+  };
+
+  const int lane = tid & 31, warp = tid >> 5;
+  double cre[RB][CB][2], cim[RB][CB][2];
+#pragma unroll
+  for (int r = 0; r < RB; ++r)
+#pragma unroll
+    for (int q = 0; q < CB; ++q) cre[r][q][0] = cre[r][q][1] = cim[r][q][0] = cim[r][q][1] = 0.0;
+
+  const int nk = (ke - kb) / BK;  // host guarantees BK | (ke - kb)
+  load_stage(0, kb);
+  cp_commit_bs();
+  if (nk > 1) load_stage(1, kb + BK);
+  cp_commit_bs();
+  const int cbase = warp * CB * 8 + (lane >> 2);
+  const int arow = lane >> 2, kq = lane & 3;
+  for (int kt = 0; kt < nk; ++kt) {
+    cp_wait1_bs();
+    __syncthreads();
+    if (kt + 2 < nk) load_stage((kt + 2) % 3, kb + (kt + 2) * BK);
+    cp_commit_bs();
+    const double2* cA = sA + (kt % 3) * BJ * kALd;
+    const double2* cB = sB + (kt % 3) * BK * LDB;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double ar[RB], ai[RB], an[RB], br[CB], bi[CB];
+#pragma unroll
+      for (int r = 0; r < RB; ++r) {
+        const double2 a = cA[(r * 8 + arow) * kALd + kk + kq];
+        ar[r] = a.x;
+        ai[r] = a.y;
+        an[r] = -a.y;
+      }
+#pragma unroll
+      for (int q = 0; q < CB; ++q) {
+        const double2 b = cB[(kk + kq) * LDB + cbase + q * 8];
+        br[q] = b.x;
+        bi[q] = b.y;
+      }
+#pragma unroll
+      for (int r = 0; r < RB; ++r)
+#pragma unroll
+        for (int q = 0; q < CB; ++q) {
+          dmma_bs(cre[r][q][0], cre[r][q][1], ar[r], br[q]);
+          dmma_bs(cim[r][q][0], cim[r][q][1], ar[r], bi[q]);
+          dmma_bs(cre[r][q][0], cre[r][q][1], an[r], bi[q]);
+          dmma_bs(cim[r][q][0], cim[r][q][1], ai[r], br[q]);
+        }
+    }
+  }
+  cp_wait0_bs();
+  double2* out = partial + (int64_t)blockIdx.x * 4096;
+  const int bsj = g.bstride[j];
+#pragma unroll
+  for (int r = 0; r < RB; ++r)
+#pragma unroll
+    for (int q = 0; q < CB; ++q) {
+      const int row = r * 8 + (lane >> 2);
+      const int c = warp * CB * 8 + q * 8 + 2 * kq;
+      out[row * bsj + coll[c]] = make_double2(cre[r][q][0], cim[r][q][0]);
+      out[row * bsj + coll[c + 1]] = make_double2(cre[r][q][1], cim[r][q][1]);
+    }
+}
+
+// n terms tp[i grp] * sp[i ss], i < n, into four independent accumulators (loads batched).
+__device__ __forceinline__ void dot_run(const double2* tp, const double2* sp, int n, int grp, int ss,
+                                        double2 (&acc)[4]) {
+  int i = 0;
+  for (; i + 4 <= n; i += 4) {
+    const double2 t0 = tp[0], t1 = tp[grp], t2 = tp[2 * grp], t3 = tp[3 * grp];
+    const double2 s0 = sp[0], s1 = sp[ss], s2 = sp[2 * ss], s3 = sp[3 * ss];
+    acc[0] = cfma(acc[0], t0, s0);
+    acc[1] = cfma(acc[1], t1, s1);
+    acc[2] = cfma(acc[2], t2, s2);
+    acc[3] = cfma(acc[3], t3, s3);
+    tp += 4 * grp;
+    sp += 4 * ss;
+  }
+  for (; i < n; ++i) {
+    acc[0] = cfma(acc[0], tp[0], sp[0]);
+    tp += grp;
+    sp += ss;
+  }
+}
+
+// Padded local strides of the diagonal tile in shared memory, chosen so that the entries of a
+// local hyperplane (sorted by leading coordinates) fall into distinct 16-byte bank groups:
+// N=3, B=16: (1, 17, 274) -> address mod 8 = l1 + l2 + 2 l3; N=4, B=8: (1, 9, 74, 595).
+template <int N, int B>
+struct PadStrides {
+  static constexpr int s1 = B + 1;
+  static constexpr int s2 = N >= 3 ? s1 * B + 2 : 0;
+  static constexpr int s3 = N >= 4 ? s2 * B + 3 : 0;
+  __device__ static constexpr int at(int m) { return m == 0 ? 1 : m == 1 ? s1 : m == 2 ? s2 : s3; }
+  static constexpr int extent = 1 + (B - 1) * (1 + s1 + s2 + s3);
+  __device__ static int pad(int l) {
+    int a = 0;
+#pragma unroll
+    for (int m = 0; m < N; ++m) a += ((l >> ((B == 16 ? 4 : 3) * m)) & (B - 1)) * at(m);
+    return a;
+  }
+};
+
+
+// Diagonal tile (cubic, B^N = 4096 entries): S = C_I - sum(partials) (fixed order ->
+// deterministic), then the local anti-diagonal wavefront over sum_j l_j = t, highest first.
+// Hyperplane step lv (t = N (B - 1) - lv) is described by a host-built table: lvl[lv] =
+// lanes-per-entry grp | (busy warps << 8), and thr[lv][tid] = the local entry this thread works
+// on (0xffff: none); entries of a hyperplane are sorted by leading coordinates so lanes share
+// loop trip counts. An entry's grp lanes split its sum_j sum_{k > l_j} T_j(i_j, k) y(...) terms,
+// combine them with warp shuffles, and the leader scales by 1 / sum_j T_j(i_j, i_j). S uses
+// padded strides (PadStrides) so a hyperplane's entries sit in distinct shared-memory banks.
+template <int N, int B, int NT>
+__global__ void __launch_bounds__(NT, 2)
+    tile_diag_kernel(const TileGeom g, const double2* __restrict__ T, const int64_t* __restrict__ tiles,
+                     const int4* __restrict__ tile_ranges, const double2* __restrict__ far_partial,
+                     const double2* __restrict__ near_partial, const uint16_t* __restrict__ thr_g,
+                     const int* __restrict__ lvl_g, int wf_levels, double2* __restrict__ Y) {
+  constexpr int E = 4096;
+  constexpr int LB = B == 16 ? 4 : 3;
+  constexpr int WL = N * (B - 1) + 1;  // hyperplanes in a tile
+  static_assert((1 << (LB * N)) == E, "cubic 4096-entry tile");
+  using PS = PadStrides<N, B>;
+  extern __shared__ __align__(16) double2 sm[];
+  __shared__ int64_t so[N];
+  __shared__ int64_t st[N];
+  __shared__ int lvl[WL];
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    int64_t t = tiles[blockIdx.x];
+    for (int m = 0; m < N; ++m) {
+      const int64_t I = t % g.nb[m];
+      t /= g.nb[m];
+      so[m] = I * B;
+      st[m] = g.strides[m];
+    }
+  }
+  double2* S = sm;
+  double2* Td = S + PS::extent + (PS::extent & 1);  // [N][B][B] row-major: T_m(o_m + row, o_m + col)
+  uint16_t* thr = (uint16_t*)(Td + N * B * B);      // [WL][NT]
+  {
+    const uint4* src = (const uint4*)thr_g;
+    uint4* dst = (uint4*)thr;
+    for (int i = tid; i < WL * NT / 8; i += NT) dst[i] = src[i];
+  }
+  for (int i = tid; i < WL; i += NT) lvl[i] = lvl_g[i];
+  __syncthreads();
+#pragma unroll
+  for (int m = 0; m < N; ++m) {
+    const double2* Tm = T + g.toff[m];
+    const int64_t nm = g.dims[m];
+    for (int e = tid; e < B * B; e += NT) {
+      const int r = e / B, c = e % B;
+      Td[(m * B + r) * B + c] = Tm[(so[m] + r) + (so[m] + c) * nm];
+    }
+  }
+  const int4 tr = tile_ranges[blockIdx.x];  // {far first, far count, near first, near count}
+  {
+    constexpr int PER = E / NT;  // entries per thread, loads issued together
+    double2 v[PER];
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const int l = tid + i * NT;
+      int64_t gidx = 0;
+#pragma unroll
+      for (int m = 0; m < N; ++m) gidx += (so[m] + ((l >> (LB * m)) & (B - 1))) * st[m];
+      v[i] = Y[gidx];
+    }
+    for (int p = 0; p < tr.y; ++p) {
+      const double2* pp = far_partial + (int64_t)(tr.x + p) * E + tid;
+#pragma unroll
+      for (int i = 0; i < PER; ++i) v[i] = csub(v[i], pp[i * NT]);
+    }
+    for (int p = 0; p < tr.w; ++p) {
+      const double2* pp = near_partial + (int64_t)(tr.z + p) * E + tid;
+#pragma unroll
+      for (int i = 0; i < PER; ++i) v[i] = csub(v[i], pp[i * NT]);
+    }
+#pragma unroll
+    for (int i = 0; i < PER; ++i) S[PS::pad(tid + i * NT)] = v[i];
+  }
+  __syncthreads();
+
+  const int warp = tid >> 5;
+#ifdef NDS_DIAG_CLOCK
+  if (tid == 0 && blockIdx.x == 0) nds_diag_clock_start = clock64();
+#endif
+#pragma unroll 1
+  for (int lv = 0; lv < wf_levels; ++lv) {
+    const int info = lvl[lv];
+    if (warp < (info >> 8)) {  // warp-uniform: this warp holds entries on hyperplane lv
+      const int grp = info & 0xff;
+      const int lraw = thr[lv * NT + tid];
+      const bool act = lraw != 0xffff;
+      const int l = act ? lraw : 0;
+      const int sub = tid & (grp - 1);
+      int lm[N];
+      int pl = 0;
+#pragma unroll
+      for (int m = 0; m < N; ++m) {
+        lm[m] = (l >> (LB * m)) & (B - 1);
+        pl += lm[m] * PS::at(m);
+      }
+      // denominator first: independent of S, its latency hides under the dot products
+      double2 den = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int m = 0; m < N; ++m) den = cadd(den, Td[m * B * B + lm[m] * (B + 1)]);
+      double2 a0 = make_double2(0.0, 0.0), a1 = make_double2(0.0, 0.0);
+      if (act) {
+#pragma unroll
+        for (int m = 0; m < N; ++m) {
+          const double2* tp = Td + m * B * B + lm[m] * (B + 1) + 1 + sub;
+          const double2* sp = S + pl + (1 + sub) * PS::at(m);
+          const int ss = grp * PS::at(m);
+          int q = B - 1 - lm[m] - sub;
+#pragma unroll 1
+          for (; q > grp; q -= 2 * grp) {
+            const double2 t0 = tp[0], t1 = tp[grp], s0 = sp[0], s1 = sp[ss];
+            a0 = cfma(a0, t0, s0);
+            a1 = cfma(a1, t1, s1);
+            tp += 2 * grp;
+            sp += 2 * ss;
+          }
+          if (q > 0) a0 = cfma(a0, tp[0], sp[0]);
+        }
+      }
+      double2 acc = cadd(a0, a1);
+      for (int o = 1; o < grp; o <<= 1) {
+        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+      }
+      if (act && sub == 0) S[pl] = cmul(csub(S[pl], acc), crecip(den));
+    }
+    __syncthreads();
+#ifdef NDS_DIAG_CLOCK
+    if (tid == 0 && blockIdx.x == 0) nds_diag_clock[lv] = clock64();
+#endif
+  }
+  {
+    constexpr int PER = E / NT;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const int l = tid + i * NT;
+      int64_t gidx = 0;
+#pragma unroll
+      for (int m = 0; m < N; ++m) gidx += (so[m] + ((l >> (LB * m)) & (B - 1))) * st[m];
+      Y[gidx] = S[PS::pad(l)];
+    }
+  }
+}
+
+using UpdateKernel = void (*)(const TileGeom, const double2*, const int64_t*, const int4*, double2*, const double2*);
+using DiagKernel = void (*)(const TileGeom, const double2*, const int64_t*, const int4*, const double2*,
+                            const double2*, const uint16_t*, const int*, int, double2*);
+
+static UpdateKernel update_kernel_for(int b) {
+  switch (b) {
+    case 8: return tile_update_kernel<1, 8>;
+    case 16: return tile_update_kernel<2, 4>;
+    default: return nullptr;
+  }
+}
+
+// Threads per diagonal-tile CTA: at least the widest local hyperplane (192 for 16^3, 480 for 8^4).
+static int diag_threads_for(int n_modes) { return n_modes == 3 ? 256 : 512; }
+
+static DiagKernel diag_kernel_for(int n_modes, int b) {
+  if (n_modes == 3 && b == 16) return tile_diag_kernel<3, 16, 256>;
+  if (n_modes == 4 && b == 8) return tile_diag_kernel<4, 8, 512>;
+  return nullptr;
+}
+
+static size_t update_smem_bytes(int b) {
+  const int cols = 4096 / b, bk = 2048 / cols;
+  return (size_t)cols * (8 + 4) + (size_t)3 * b * kALd * 16 + (size_t)3 * bk * (cols + 2) * 16;
+}
+
+static size_t diag_smem_bytes(int n_modes, int b, int wf_levels) {
+  const int ext = n_modes == 3 ? PadStrides<3, 16>::extent : PadStrides<4, 8>::extent;
+  return (size_t)(ext + (ext & 1)) * 16 + (size_t)n_modes * b * b * 16 +
+         (size_t)wf_levels * diag_threads_for(n_modes) * sizeof(uint16_t);
+}

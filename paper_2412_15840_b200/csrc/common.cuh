@@ -133,6 +133,17 @@ __device__ __forceinline__ double2 cdiv(double2 num, double2 den) {
   return make_double2(x, y);
 }
 
+// 1 / d = conj(d) / |d|^2 with an exact power-of-two prescale, so |d|^2 neither overflows
+// nor underflows for any finite non-zero d.
+__device__ __forceinline__ double2 crecip(double2 d) {
+  const double m = fmax(fabs(d.x), fabs(d.y));
+  const int e = ((__double2hiint(m) >> 20) & 0x7ff) - 1023;  // exponent field (normal range)
+  const double s = __hiloint2double((1023 - e) << 20, 0);   // exactly 2^-e
+  const double xr = d.x * s, xi = d.y * s;
+  const double inv = 1.0 / (xr * xr + xi * xi);
+  return make_double2(xr * inv * s, -xi * inv * s);
+}
+
 inline int ceil_div_i(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
 
 }  // namespace nds

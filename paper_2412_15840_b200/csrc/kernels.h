@@ -75,15 +75,23 @@ struct SolvePlan {
   int* d_wf = nullptr;            // local entries sorted by descending local level
   int* d_wf_off = nullptr;
   int* d_wf_group = nullptr;      // lanes per entry for each local hyperplane (v2)
+  uint16_t* d_thr = nullptr;      // v2: [wf_levels][diag threads] local entry per thread (0xffff none)
+  int* d_lvl = nullptr;           // v2: per local hyperplane: grp | (busy warps << 8)
   void* pool = nullptr;
   // v2 (GEMM regime: every b_j a power of two >= 8 dividing n_j): per level, DMMA update work
   // items (tile, mode, k-range) writing partials, then one diagonal-tile kernel.
   bool v2 = false;
-  std::vector<int64_t> item_off;  // per level, into d_items (host copy), size levels + 1
-  int4* d_items = nullptr;        // {tile slot (global), mode, k_begin, k_end}
-  int2* d_tile_items = nullptr;   // per tile slot: {first item (global), count}
-  double2* d_partial = nullptr;   // max items per level x tile_entries
-  int64_t max_level_items = 0;
+  // Items {tile slot (global), mode, k_begin, k_end}; far = neighbours >= 2 blocks away (ready
+  // one level early, low-priority stream), near = adjacent block (critical stream).
+  std::vector<int64_t> far_off, near_off;  // per level into the item lists, size levels + 1
+  int4* d_far_items = nullptr;
+  int4* d_near_items = nullptr;
+  int4* d_tile_ranges = nullptr;  // per tile slot: {far first, far count, near first, near count} (level-relative)
+  double2* d_far_partial[2] = {nullptr, nullptr};  // double-buffered by level parity
+  double2* d_near_partial = nullptr;
+  int64_t max_far = 0, max_near = 0;
+  cudaStream_t s_crit = nullptr, s_far = nullptr;
+  std::vector<cudaEvent_t> ev;  // diag(lv), far(lv), start, end
 };
 
 void solve_plan_build(SolvePlan& sp, int n_modes, const int64_t* dims, const int64_t* toff);
