@@ -1,0 +1,186 @@
+// Fused mode-product passes for runs of binary modes (n_j = 2), the tiny-mode regime of
+// BASELINE config c4 (N = 29, n_j = 2): reference kernels.cpp:24-44 applied to one mode at a
+// time costs a full read+write of the tensor per mode (29 passes per transform); here k
+// consecutive binary modes are applied in ONE pass.
+//
+// A pass covers modes [a, a+k) of the column-major tensor viewed as (inner I, 2^k, outer O).
+// Each CTA owns a 4096-entry tile: a run of R consecutive inner positions (R >= 8 entries =
+// 128 B when I > 1, so global access stays coalesced) x all 2^k group positions, at one outer
+// index; tile bit b < log2 R is a run bit, bit log2 R + q is group mode q. The tile is staged in
+// shared memory (XOR-swizzled in 8-entry groups), then processed in rounds of up to 4 group
+// modes: each thread gathers the 2^4 entries spanning the round's modes into registers, applies
+// the 2x2 matrices as butterflies, and scatters back. Modes commute (test_kernels.cpp:91-99), so
+// the grouping changes rounding only.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace nds {
+
+constexpr int kBinThreads = 256;
+
+struct BinPass {
+  int64_t I;       // inner extent (product of modes before the group)
+  int64_t O;       // outer extent
+  int64_t n_runs;  // I / R
+  int logR, k;     // run bits, group bits (logR + k = 12)
+  int rounds;
+  int nrb[3];      // group bits per round (<= 4)
+  int rb[3][4];    // tile bit of each round bit
+  int tb[3][12];   // tile bits carried by the thread index (and slot index) in each round
+  const double2* M[12];  // 2x2 column-major op(U_j) per group mode
+};
+
+__device__ __forceinline__ int swz(int p) { return p ^ (((p >> 3) ^ (p >> 6) ^ (p >> 9)) & 7); }
+
+// One round: each thread slot gathers the 2^NB entries spanning the round's NB group modes,
+// applies the NB 2x2 matrices as butterflies in registers, and scatters them back.
+template <int NB>
+__device__ __forceinline__ void bin_round(const BinPass& bp, int rd, double2* S, const double2 (*Mq)[4], int tid) {
+  constexpr int V = 1 << NB;
+  int rbit[NB];
+#pragma unroll
+  for (int q = 0; q < NB; ++q) rbit[q] = bp.rb[rd][q];
+  for (int s = tid; s < (4096 >> NB); s += kBinThreads) {
+    int p0 = 0;
+#pragma unroll
+    for (int i = 0; i < 12 - NB; ++i) p0 |= ((s >> i) & 1) << bp.tb[rd][i];
+    int addr[V];
+    double2 v[V];
+#pragma unroll
+    for (int e = 0; e < V; ++e) {
+      int p = p0;
+#pragma unroll
+      for (int q = 0; q < NB; ++q) p |= ((e >> q) & 1) << rbit[q];
+      addr[e] = swz(p);
+      v[e] = S[addr[e]];
+    }
+#pragma unroll
+    for (int q = 0; q < NB; ++q) {
+      const int mode = rbit[q] - bp.logR;
+      const double2 m00 = Mq[mode][0], m10 = Mq[mode][1], m01 = Mq[mode][2], m11 = Mq[mode][3];
+#pragma unroll
+      for (int e = 0; e < V; ++e) {
+        if (!((e >> q) & 1)) {
+          const double2 a = v[e], b = v[e | (1 << q)];
+          v[e] = cfma(cmul(m00, a), m01, b);
+          v[e | (1 << q)] = cfma(cmul(m10, a), m11, b);
+        }
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < V; ++e) S[addr[e]] = v[e];
+  }
+}
+
+__global__ void __launch_bounds__(kBinThreads, 2) binary_pass_kernel(const BinPass bp, const double2* __restrict__ x,
+                                                                  double2* __restrict__ r) {
+  extern __shared__ __align__(16) double2 S[];  // 4096 entries (64 KB, dynamic)
+  __shared__ double2 Mq[12][4];
+  const int tid = threadIdx.x;
+  if (tid < 4 * bp.k) Mq[tid >> 2][tid & 3] = bp.M[tid >> 2][tid & 3];
+  const int64_t tile = blockIdx.x;
+  const int64_t run = tile % bp.n_runs;
+  const int64_t o = tile / bp.n_runs;
+  const int R = 1 << bp.logR;
+  const int64_t base = run * R + bp.I * ((int64_t)1 << bp.k) * o;
+  // global -> shared (coalesced along runs of R entries)
+#pragma unroll 4
+  for (int p = tid; p < 4096; p += kBinThreads) S[swz(p)] = x[base + (p & (R - 1)) + bp.I * (p >> bp.logR)];
+  __syncthreads();
+  for (int rd = 0; rd < bp.rounds; ++rd) {
+    switch (bp.nrb[rd]) {
+      case 4: bin_round<4>(bp, rd, S, Mq, tid); break;
+      case 3: bin_round<3>(bp, rd, S, Mq, tid); break;
+      case 2: bin_round<2>(bp, rd, S, Mq, tid); break;
+      default: bin_round<1>(bp, rd, S, Mq, tid); break;
+    }
+    __syncthreads();
+  }
+#pragma unroll 4
+  for (int p = tid; p < 4096; p += kBinThreads) r[base + (p & (R - 1)) + bp.I * (p >> bp.logR)] = S[swz(p)];
+}
+
+// Plan the passes over [mode0, mode1) (1-based, all n_j = 2): greedily take as many binary modes
+// as fit a 4096-entry tile with runs of min(I, 8..4096) entries.
+std::vector<BinGroup> plan_binary_groups(int n_modes, const int64_t* dims) {
+  std::vector<BinGroup> out;
+  int64_t inner = 1;
+  int j = 0;
+  while (j < n_modes) {
+    int avail = 0;
+    while (j + avail < n_modes && dims[j + avail] == 2) ++avail;
+    if (avail == 0) {
+      inner *= dims[j];
+      ++j;
+      continue;
+    }
+    // runs of R = 2^logR inner entries: at least min(I, 8) (128 B), the rest of the 12 tile bits
+    // go to group modes
+    int logI = 0;
+    while (((int64_t)1 << logI) < inner) ++logI;
+    const int k = std::min(avail, 12 - std::min(logI, 3));
+    const int logR = 12 - k;
+    int64_t outer = 1;
+    for (int m = j + k; m < n_modes; ++m) outer *= dims[m];
+    if (logR <= logI && inner % ((int64_t)1 << logR) == 0) {
+      BinGroup gr;
+      gr.first = j + 1;
+      gr.count = k;
+      gr.inner = inner;
+      gr.outer = outer;
+      gr.logR = logR;
+      out.push_back(gr);
+    }
+    for (int m = 0; m < k; ++m) inner *= 2;
+    j += k;
+  }
+  return out;
+}
+
+int binary_pass_launch(const FactorSet& f, const BinGroup& gr, bool adjoint, const double2* x, double2* r,
+                       cudaStream_t stream) {
+  BinPass bp{};
+  bp.I = gr.inner;
+  bp.O = gr.outer;
+  bp.logR = gr.logR;
+  bp.k = gr.count;
+  bp.n_runs = gr.inner >> gr.logR;
+  for (int q = 0; q < gr.count; ++q) bp.M[q] = adjoint ? f.uh_col[gr.first - 1 + q] : f.u_col[gr.first - 1 + q];
+  // rounds of <= 4 group bits; thread bits: the remaining tile bits, first three with distinct
+  // residues mod 3 where possible (conflict-free shared-memory phases under swz)
+  bp.rounds = (gr.count + 3) / 4;
+  for (int rd = 0; rd < bp.rounds; ++rd) {
+    const int nb = std::min(4, gr.count - 4 * rd);
+    bp.nrb[rd] = nb;
+    bool used[12] = {};
+    for (int q = 0; q < nb; ++q) {
+      bp.rb[rd][q] = gr.logR + 4 * rd + q;
+      used[bp.rb[rd][q]] = true;
+    }
+    std::vector<int> rest;
+    for (int b = 0; b < 12; ++b)
+      if (!used[b]) rest.push_back(b);
+    std::vector<int> order;
+    for (int want = 0; want < 3; ++want)
+      for (size_t i = 0; i < rest.size(); ++i)
+        if (rest[i] >= 0 && rest[i] % 3 == want) {
+          order.push_back(rest[i]);
+          rest[i] = -1;
+          break;
+        }
+    for (int b : rest)
+      if (b >= 0) order.push_back(b);
+    for (size_t i = 0; i < order.size(); ++i) bp.tb[rd][i] = order[i];
+  }
+  static bool attr_set = false;
+  if (!attr_set) {
+    NDS_CUDA(cudaFuncSetAttribute(binary_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 4096 * 16));
+    attr_set = true;
+  }
+  const int64_t tiles = bp.n_runs * bp.O;
+  binary_pass_kernel<<<(unsigned)tiles, kBinThreads, 4096 * 16, stream>>>(bp, x, r);
+  NDS_LAUNCH_CHECK();
+  return kXformDirect;
+}
+
+}  // namespace nds

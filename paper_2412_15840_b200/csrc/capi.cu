@@ -35,8 +35,11 @@ struct nds_plan {
   bool fast_path = false;
   double min_abs_den = 0.0;
   nds::FactorSet f;
+  std::vector<nds::BinGroup> groups;  // fused passes over runs of binary modes
   nds::SolvePlan sp;
   bool have_solve_plan = false;
+  bool binary = false;  // all n_j = 2: binary_solve.cu regime
+  nds::BinarySolvePlan bsp;
   int launches = 0;
   // per-launch CUDA-event profile (nds_plan_profile_begin / _end)
   bool profiling = false;
@@ -229,19 +232,47 @@ std::string format_singular(const nds_singular& s) {
 
 // N mode-product passes in -> out (modes 1..N, op = U_j^H if adjoint else U_j). `in` is never
 // written; out may equal in. Destinations alternate out/work so the last lands in out.
+// One pass of a transform: a single mode (GEMM / direct kernel) or a fused run of binary modes.
+struct XPass {
+  int mode;   // first mode (1-based)
+  int group;  // index into nds_plan::groups, or -1
+};
+
+std::vector<XPass> transform_passes(const nds_plan* p) {
+  std::vector<XPass> out;
+  size_t gi = 0;
+  for (int j = 1; j <= p->n_modes;) {
+    if (gi < p->groups.size() && p->groups[gi].first == j) {
+      out.push_back({j, (int)gi});
+      j += p->groups[gi].count;
+      ++gi;
+    } else {
+      out.push_back({j, -1});
+      ++j;
+    }
+  }
+  return out;
+}
+
+int launch_pass(nds_plan* p, const XPass& ps, bool adjoint, const double2* src, double2* dst) {
+  if (ps.group >= 0) return nds::binary_pass_launch(p->f, p->groups[ps.group], adjoint, src, dst, p->ctx->stream);
+  return nds::mode_product_launch(p->f, ps.mode, adjoint, nds::mode_view(p->n_modes, p->dims, ps.mode), src, dst,
+                                  false, p->ctx->stream);
+}
+
 int transform_chain(nds_plan* p, bool adjoint, const double2* in, double2* out, double2* work) {
-  const int N = p->n_modes;
+  const std::vector<XPass> passes = transform_passes(p);
+  const int N = (int)passes.size();
   nds::Recorder* rec = p->profiling ? &p->rec : nullptr;
   int launches = 0;
   const bool in_place = in == out;
   const double2* src = in;
   for (int j = 1; j <= N; ++j) {
     // Out of place: last pass lands in out. In place: first pass must leave `in`, so start in
-    // work (odd N then ends in work and is copied back).
+    // work (an odd pass count then ends in work and is copied back).
     double2* dst = in_place ? ((j % 2 == 1) ? work : out) : (((N - j) % 2 == 0) ? out : work);
-    const int kind = nds::mode_product_launch(p->f, j, adjoint, nds::mode_view(N, p->dims, j), src, dst, false,
-                                              p->ctx->stream);
-    if (rec) rec->mark(p->ctx->stream, kind, adjoint ? -j : j);
+    const int kind = launch_pass(p, passes[j - 1], adjoint, src, dst);
+    if (rec) rec->mark(p->ctx->stream, kind, adjoint ? -passes[j - 1].mode : passes[j - 1].mode);
     ++launches;
     src = dst;
   }
@@ -251,6 +282,26 @@ int transform_chain(nds_plan* p, bool adjoint, const double2* in, double2* out, 
   return launches;
 }
 
+// Solver for the plan's regime: all-binary tiles, or the general tiled solve (v1 / v2).
+void build_solver(nds_plan* p) {
+  bool binary = true;
+  for (int j = 0; j < p->n_modes; ++j) binary = binary && p->dims[j] == 2;
+  if (binary) {
+    nds::binary_solve_plan_build(p->bsp, p->n_modes, p->f.t_pool);
+  } else {
+    int64_t toff[NDS_MAX_MODES];
+    for (int j = 0; j < p->n_modes; ++j) toff[j] = p->f.geom.toff[j];
+    nds::solve_plan_build(p->sp, p->n_modes, p->dims, toff);
+  }
+  p->binary = binary;
+  p->have_solve_plan = true;
+}
+
+int launch_solver(nds_plan* p, double2* c, cudaStream_t s, nds::Recorder* rec) {
+  if (p->binary) return nds::binary_solve_launch(p->bsp, c, s, rec);
+  return nds::backsub_launch(p->sp, p->f.t_pool, c, s, rec);
+}
+
 int backsub_run(nds_plan* p, double2* c) {
   nds::Recorder* rec = p->profiling ? &p->rec : nullptr;
   if (p->fast_path) {
@@ -258,13 +309,14 @@ int backsub_run(nds_plan* p, double2* c) {
     if (rec) rec->mark(p->ctx->stream, nds::kElementwise, 0);
     return 1;
   }
-  return nds::backsub_launch(p->sp, p->f.t_pool, c, p->ctx->stream, rec);
+  return launch_solver(p, c, p->ctx->stream, rec);
 }
 
 // Full path on device buffers: b -> (fwd) -> C -> (solve, in place) -> Y -> (inv) -> x.
 // Destinations alternate W/X from the first pass so the 2N-th pass lands in x and b is only read.
 int execute(nds_plan* p, const double2* b, double2* x, double2* work, cudaEvent_t* ev) {
-  const int N = p->n_modes;
+  const std::vector<XPass> passes = transform_passes(p);
+  const int N = (int)passes.size();
   cudaStream_t s = p->ctx->stream;
   nds::Recorder* rec = p->profiling ? &p->rec : nullptr;
   int launches = 0;
@@ -274,8 +326,8 @@ int execute(nds_plan* p, const double2* b, double2* x, double2* work, cudaEvent_
   if (rec) rec->mark(s, -1, 0);
   for (int j = 1; j <= N; ++j) {
     double2* dst = dst_of(j);
-    const int kind = nds::mode_product_launch(p->f, j, true, nds::mode_view(N, p->dims, j), src, dst, false, s);
-    if (rec) rec->mark(s, kind, -j);
+    const int kind = launch_pass(p, passes[j - 1], true, src, dst);
+    if (rec) rec->mark(s, kind, -passes[j - 1].mode);
     ++launches;
     src = dst;
   }
@@ -286,8 +338,8 @@ int execute(nds_plan* p, const double2* b, double2* x, double2* work, cudaEvent_
   src = c;
   for (int j = 1; j <= N; ++j) {
     double2* dst = dst_of(N + j);
-    const int kind = nds::mode_product_launch(p->f, j, false, nds::mode_view(N, p->dims, j), src, dst, false, s);
-    if (rec) rec->mark(s, kind, j);
+    const int kind = launch_pass(p, passes[j - 1], false, src, dst);
+    if (rec) rec->mark(s, kind, passes[j - 1].mode);
     ++launches;
     src = dst;
   }
@@ -318,6 +370,7 @@ void plan_create_impl(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_
   for (int j = 0; diag_route && j < n_modes; ++j) diag_route = numerically_diagonal(dims[j], t[j]);
   p->fast_path = diag_route;
   upload_factors(ctx, p->f, n_modes, dims, u, t);
+  p->groups = nds::plan_binary_groups(n_modes, dims);
   // Singular check over all entries (sylvester.cpp:101-103 / :137): the first offender in the
   // reference's descending visiting order is the one with the largest flat index.
   int64_t bad = -1;
@@ -329,12 +382,7 @@ void plan_create_impl(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_
     free_factors(p->f);
     throw Error(NDS_ERR_SINGULAR, format_singular(tmp));
   }
-  if (!p->fast_path) {
-    int64_t toff[NDS_MAX_MODES];
-    for (int j = 0; j < n_modes; ++j) toff[j] = p->f.geom.toff[j];
-    nds::solve_plan_build(p->sp, n_modes, dims, toff);
-    p->have_solve_plan = true;
-  }
+  if (!p->fast_path) build_solver(p.get());
   *out = p.release();
 }
 
@@ -343,7 +391,12 @@ void plan_destroy_impl(nds_plan* p) {
   cudaSetDevice(p->ctx->device);
   for (auto e : p->pev) cudaEventDestroy(e);
   free_factors(p->f);
-  if (p->have_solve_plan) nds::solve_plan_free(p->sp);
+  if (p->have_solve_plan) {
+    if (p->binary)
+      nds::binary_solve_plan_free(p->bsp);
+    else
+      nds::solve_plan_free(p->sp);
+  }
   delete p;
 }
 
@@ -407,6 +460,7 @@ void transform_host(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z*
   std::memcpy(p.dims, dims, n_modes * sizeof(int64_t));
   p.total = total;
   upload_factors(ctx, p.f, n_modes, dims, u, nullptr);
+  p.groups = nds::plan_binary_groups(n_modes, dims);
   const size_t bytes = (size_t)total * sizeof(double2);
   try {
     NDS_CUDA(cudaMemcpyAsync(ctx->ws[0], in, bytes, cudaMemcpyHostToDevice, ctx->stream));
@@ -676,13 +730,10 @@ int nds_back_substitute(nds_ctx* ctx, int n_modes, const int64_t* dims, const nd
         if (sing) *sing = tmp;
         throw Error(NDS_ERR_SINGULAR, format_singular(tmp));
       }
-      int64_t toff[NDS_MAX_MODES];
-      for (int j = 0; j < n_modes; ++j) toff[j] = p->f.geom.toff[j];
-      nds::solve_plan_build(p->sp, n_modes, dims, toff);
-      p->have_solve_plan = true;
+      build_solver(p.get());
       const size_t bytes = (size_t)total * sizeof(double2);
       NDS_CUDA(cudaMemcpyAsync(ctx->ws[0], c, bytes, cudaMemcpyHostToDevice, ctx->stream));
-      nds::backsub_launch(p->sp, p->f.t_pool, ctx->ws[0], ctx->stream);
+      launch_solver(p.get(), ctx->ws[0], ctx->stream, nullptr);
       NDS_CUDA(cudaMemcpyAsync(c, ctx->ws[0], bytes, cudaMemcpyDeviceToHost, ctx->stream));
       NDS_CUDA(cudaStreamSynchronize(ctx->stream));
       if (stats) {

@@ -50,6 +50,16 @@ struct Recorder {
 int mode_product_launch(const FactorSet& f, int mode, bool adjoint, const ModeView& v, const double2* x, double2* r,
                         bool accumulate, cudaStream_t stream);
 
+// A run of `count` binary modes starting at mode `first` (1-based) applied in one fused pass on
+// the (inner, 2^count, outer) view, with runs of 2^logR inner entries per tile.
+struct BinGroup {
+  int first = 0, count = 0, logR = 0;
+  int64_t inner = 1, outer = 1;
+};
+std::vector<BinGroup> plan_binary_groups(int n_modes, const int64_t* dims);
+int binary_pass_launch(const FactorSet& f, const BinGroup& gr, bool adjoint, const double2* x, double2* r,
+                       cudaStream_t stream);
+
 // Plain matrix variant (apply_operator / residual): m_row, m_col are the two layouts of M.
 int mode_product_matrix_launch(const double2* m_row, const double2* m_col, const ModeView& v, const double2* x,
                                double2* r, bool accumulate, cudaStream_t stream);
@@ -93,6 +103,21 @@ struct SolvePlan {
   cudaStream_t s_crit = nullptr, s_far = nullptr;
   std::vector<cudaEvent_t> ev;  // diag(lv), far(lv), start, end
 };
+
+// All-binary regime (every n_j = 2, config c4): contiguous 2^min(N,12)-entry tiles, binary outer
+// modes, one launch per outer popcount level (binary_solve.cu).
+struct BinarySolvePlan {
+  int m = 0, n_outer = 0, levels = 0;
+  const double2* t = nullptr;  // T pool (T_j at t + 4 j)
+  std::vector<int64_t> level_off;
+  int64_t* d_tiles = nullptr;
+  int* d_wf = nullptr;
+  int* d_wf_off = nullptr;
+  void* pool = nullptr;
+};
+void binary_solve_plan_build(BinarySolvePlan& bp, int n_modes, const double2* t_pool_dev);
+void binary_solve_plan_free(BinarySolvePlan& bp);
+int binary_solve_launch(const BinarySolvePlan& bp, double2* c, cudaStream_t stream, Recorder* rec = nullptr);
 
 void solve_plan_build(SolvePlan& sp, int n_modes, const int64_t* dims, const int64_t* toff);
 void solve_plan_free(SolvePlan& sp);
