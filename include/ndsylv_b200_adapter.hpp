@@ -1,0 +1,75 @@
+// ndsylv_b200_adapter.hpp — B200 back end for ndsylv::solve with the reference's own types and
+// exceptions (include together with the reference headers, link libndsylv_b200.so).
+#pragma once
+#include <chrono>
+#include <memory>
+#include <stdexcept>
+#include "ndsylv/sylvester.hpp"
+#include "ndsylv_b200.h"
+
+namespace ndsylv::gpu {
+
+inline nds_ctx* context() {  // one context per host thread (sylvester.hpp: solve is reentrant)
+  thread_local std::unique_ptr<nds_ctx, void (*)(nds_ctx*)> c{nullptr, nds_ctx_destroy};
+  if (!c) {
+    nds_ctx* raw = nullptr;
+    if (nds_ctx_create(&raw, 0) != NDS_OK) throw std::runtime_error(nds_last_error(nullptr));
+    c.reset(raw);
+  }
+  return c.get();
+}
+
+inline void rethrow(int rc, const nds_singular& s) {
+  const char* msg = nds_last_error(context());
+  switch (rc) {
+    case NDS_OK: return;
+    case NDS_ERR_SINGULAR:
+      throw SingularOperatorError(std::vector<std::int64_t>(s.multi_index, s.multi_index + s.n_modes),
+                                  cxd(s.den_re, s.den_im));
+    case NDS_ERR_INVALID: throw std::invalid_argument(msg);
+    case NDS_ERR_OVERFLOW: throw std::overflow_error(msg);
+    case NDS_ERR_CONVERGENCE: throw ConvergenceError(msg);
+    case NDS_ERR_NOMEM: throw std::bad_alloc();
+    default: throw std::runtime_error(msg);
+  }
+}
+
+// Same contract as ndsylv::solve (sylvester.cpp:167-227): Schur on the host with the
+// reference's own ndsylv::schur, transforms + triangular solve on the GPU.
+inline SolveResult solve(const SylvesterProblem& p, const SolveOptions& o = {}) {
+  const int n = p.rhs.order();
+  std::vector<SchurFactors> f;
+  SolveResult r;
+  auto t0 = std::chrono::steady_clock::now();
+  for (const Matrix& a : p.coefficients) f.push_back(schur(a));
+  const double schur_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  std::vector<const nds_z*> u, t;
+  for (auto& s : f) {
+    u.push_back(reinterpret_cast<const nds_z*>(s.u.data()));
+    t.push_back(reinterpret_cast<const nds_z*>(s.t.data()));
+  }
+  r.x = NDTensor::zeros(p.rhs.dims);
+  nds_report rep{};
+  nds_singular sing{};
+  const unsigned flags = (o.allow_fast_path ? NDS_ALLOW_FAST_PATH : 0u) | (o.real_output ? NDS_REAL_OUTPUT : 0u);
+  rethrow(nds_solve_schur(context(), n, p.rhs.dims.data(), u.data(), t.data(),
+                          reinterpret_cast<const nds_z*>(p.rhs.data.data()),
+                          reinterpret_cast<nds_z*>(r.x.data.data()), o.singular_tol, flags, &rep, &sing),
+          sing);
+  r.report.min_abs_denominator = rep.min_abs_denominator;
+  r.report.used_normal_fast_path = rep.used_normal_fast_path != 0;
+  r.report.flop_estimate = rep.flop_estimate;
+  r.report.schur_flop_estimate = rep.schur_flop_estimate;
+  r.report.backsub_entries = rep.backsub_entries;
+  r.report.backsub_multiplies = rep.backsub_multiplies;
+  r.report.schur_seconds = schur_s;
+  r.report.transform_seconds = rep.transform_seconds;
+  r.report.backsub_seconds = rep.backsub_seconds;
+  r.report.inverse_seconds = rep.inverse_seconds;
+  r.report.total_seconds = schur_s + rep.total_seconds;
+  return r;
+}
+
+// Stage functions (sylvester.hpp:64-77) map 1:1: nds_forward_transform, nds_inverse_transform,
+// nds_back_substitute (in place, like the reference), nds_mode_product, nds_apply_operator.
+}  // namespace ndsylv::gpu
