@@ -174,6 +174,15 @@ int nds_plan_profile_end(nds_plan* plan, int cap, int* kinds, int* modes, float*
  * column-major matrix. Async on the context stream. r must not alias x. */
 int nds_dev_mode_product(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z* d_m, int mode,
                          int conj_transpose, const nds_z* d_x, nds_z* d_r, int accumulate);
+/* Rectangular update along one mode, device tensors (multi-GPU slab coupling):
+ *   r += M x_mode x,  x of extents dims_x, r of the same extents except rows_out along `mode`,
+ *   M a HOST rows_out x dims_x[mode-1] column-major matrix (negate it to subtract). Async. */
+int nds_dev_mode_update(nds_ctx* ctx, int n_modes, const int64_t* dims_x, int mode, int64_t rows_out,
+                        const nds_z* m, const nds_z* d_x, nds_z* d_r);
+/* In-place triangular solve of a device tensor (back_substitute on device memory): T_j HOST
+ * upper-triangular matrices. Synchronous; singular check and stats as nds_back_substitute. */
+int nds_dev_back_substitute(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z* const* t, nds_z* d_c,
+                            double singular_tol, nds_backsub_stats* stats, nds_singular* sing);
 /* Device residual: returns max_i |sum_j A_j x_j X - B|_i and the 2-norm, plus |B| norms.
  * a[] are HOST matrices (uploaded), d_x and d_b device tensors. Synchronous. */
 int nds_dev_residual(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z* const* a, const nds_z* d_x,

@@ -50,7 +50,7 @@ EXPORTED = [
     "nds_plan_create", "nds_plan_destroy", "nds_plan_report", "nds_plan_total", "nds_plan_execute",
     "nds_plan_forward", "nds_plan_backsub", "nds_plan_inverse", "nds_plan_execute_host", "nds_plan_launches",
     "nds_plan_profile_begin", "nds_plan_profile_end",
-    "nds_dev_mode_product", "nds_dev_residual", "nds_randn",
+    "nds_dev_mode_product", "nds_dev_mode_update", "nds_dev_back_substitute", "nds_dev_residual", "nds_randn",
 ]
 
 
@@ -159,6 +159,9 @@ def load_library(path: str = LIB_PATH):
     L.nds_plan_profile_end.argtypes = [_vp, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int),
                                        C.POINTER(C.c_float)]
     L.nds_dev_mode_product.argtypes = [_vp, C.c_int, _i64p, _vp, C.c_int, C.c_int, _vp, _vp, C.c_int]
+    L.nds_dev_mode_update.argtypes = [_vp, C.c_int, _i64p, C.c_int, C.c_int64, _vp, _vp, _vp]
+    L.nds_dev_back_substitute.argtypes = [_vp, C.c_int, _i64p, _vp, _vp, C.c_double, C.POINTER(_Stats),
+                                          C.POINTER(_Singular)]
     L.nds_dev_residual.argtypes = [_vp, C.c_int, _i64p, _vp, _vp, _vp, C.POINTER(C.c_double),
                                    C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double)]
     L.nds_randn.argtypes = [C.c_uint64, C.c_uint64, C.c_int64, _vp]
@@ -453,6 +456,22 @@ class Context:
                          accumulate=False):
         self._check(self.lib.nds_dev_mode_product(self.h, len(dims), _dims(dims), d_m, int(mode),
                                                   1 if conj_transpose else 0, d_x, d_r, 1 if accumulate else 0))
+
+    def dev_mode_update(self, dims_x, mode: int, m, d_x: int, d_r: int):
+        """r += m x_mode x on device tensors; m is a host (rows_out, n_mode) matrix."""
+        m = _f(m)
+        self._check(self.lib.nds_dev_mode_update(self.h, len(dims_x), _dims(dims_x), int(mode), int(m.shape[0]),
+                                                 m.ctypes.data, d_x, d_r))
+
+    def dev_back_substitute(self, ts, dims, d_c: int, singular_tol=0.0) -> dict:
+        """In-place triangular solve of a device tensor (back_substitute on device memory)."""
+        tp, keep = _ptr_array(ts)
+        st = _Stats()
+        sing = _Singular()
+        rc = self.lib.nds_dev_back_substitute(self.h, len(dims), _dims(dims), tp, d_c, float(singular_tol),
+                                              C.byref(st), C.byref(sing))
+        self._check(rc, sing)
+        return _dict(st)
 
     def dev_residual(self, coefficients, dims, d_x: int, d_b: int) -> dict:
         ap, keep = _ptr_array(coefficients)

@@ -869,6 +869,75 @@ int nds_dev_mode_product(nds_ctx* ctx, int n_modes, const int64_t* dims, const n
   });
 }
 
+int nds_dev_mode_update(nds_ctx* ctx, int n_modes, const int64_t* dims_x, int mode, int64_t rows_out,
+                        const nds_z* m, const nds_z* d_x, nds_z* d_r) {
+  if (!ctx) return NDS_ERR_INVALID;
+  return guarded(ctx, [&] {
+    checked_total(n_modes, dims_x, 1);
+    if (mode < 1 || mode > n_modes) throw Error(NDS_ERR_INVALID, "mode out of range");
+    if (rows_out < 1) throw Error(NDS_ERR_INVALID, "rows_out must be positive");
+    if (!m || !d_x || !d_r) throw Error(NDS_ERR_INVALID, "null pointer");
+    ensure_device(ctx);
+    const int64_t n = dims_x[mode - 1];
+    std::vector<double2> mm(2 * rows_out * n);
+    for (int64_t k = 0; k < n; ++k)
+      for (int64_t i = 0; i < rows_out; ++i) {
+        const nds_z z = m[i + k * rows_out];
+        mm[i * n + k] = make_double2(z.re, z.im);                   // row-major (rows_out x n)
+        mm[rows_out * n + i + k * rows_out] = make_double2(z.re, z.im);  // column-major
+      }
+    double2* dm = nullptr;
+    NDS_CUDA(cudaMallocAsync(&dm, mm.size() * sizeof(double2), ctx->stream));
+    NDS_CUDA(cudaMemcpyAsync(dm, mm.data(), mm.size() * sizeof(double2), cudaMemcpyHostToDevice, ctx->stream));
+    nds::mode_product_matrix_launch(dm, dm + rows_out * n, nds::mode_view(n_modes, dims_x, mode), (const double2*)d_x,
+                                    (double2*)d_r, true, ctx->stream, rows_out);
+    NDS_CUDA(cudaFreeAsync(dm, ctx->stream));
+    NDS_CUDA(cudaStreamSynchronize(ctx->stream));  // mm must outlive the async copy
+  });
+}
+
+int nds_dev_back_substitute(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z* const* t, nds_z* d_c,
+                            double singular_tol, nds_backsub_stats* stats, nds_singular* sing) {
+  if (!ctx) return NDS_ERR_INVALID;
+  return guarded(ctx, [&] {
+    const int64_t total = checked_total(n_modes, dims, 1);
+    require_ptrs(n_modes, t, "t");
+    if (!d_c) throw Error(NDS_ERR_INVALID, "null device tensor pointer");
+    ensure_device(ctx);
+    std::unique_ptr<nds_plan> p(new nds_plan);
+    p->ctx = ctx;
+    p->n_modes = n_modes;
+    std::memcpy(p->dims, dims, n_modes * sizeof(int64_t));
+    p->total = total;
+    p->tol = singular_tol;
+    upload_factors(ctx, p->f, n_modes, dims, nullptr, t);
+    try {
+      int64_t bad = -1;
+      nds::den_scan(p->f.geom, p->f.diag_pool, p->tol, &p->min_abs_den, &bad, ctx->stream, ctx->scratch);
+      if (bad >= 0) {
+        nds_singular tmp{};
+        fill_singular(&tmp, n_modes, dims, bad, t);
+        if (sing) *sing = tmp;
+        throw Error(NDS_ERR_SINGULAR, format_singular(tmp));
+      }
+      build_solver(p.get());
+      launch_solver(p.get(), (double2*)d_c, ctx->stream, nullptr);
+      NDS_CUDA(cudaStreamSynchronize(ctx->stream));
+      if (stats) {
+        nds_report r;
+        report_static(p.get(), &r);
+        stats->entries = r.backsub_entries;
+        stats->multiplies = r.backsub_multiplies;
+        stats->min_abs_denominator = p->min_abs_den;
+      }
+    } catch (...) {
+      plan_destroy_impl(p.release());
+      throw;
+    }
+    plan_destroy_impl(p.release());
+  });
+}
+
 int nds_dev_residual(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z* const* a, const nds_z* d_x,
                      const nds_z* d_b, double* res_max, double* res_2, double* b_max, double* b_2) {
   if (!ctx) return NDS_ERR_INVALID;

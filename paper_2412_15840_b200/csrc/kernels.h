@@ -61,8 +61,9 @@ int binary_pass_launch(const FactorSet& f, const BinGroup& gr, bool adjoint, con
                        cudaStream_t stream);
 
 // Plain matrix variant (apply_operator / residual): m_row, m_col are the two layouts of M.
+// rows_out > 0: rectangular M (rows_out x n), r has extent rows_out along the mode.
 int mode_product_matrix_launch(const double2* m_row, const double2* m_col, const ModeView& v, const double2* x,
-                               double2* r, bool accumulate, cudaStream_t stream);
+                               double2* r, bool accumulate, cudaStream_t stream, int64_t rows_out = -1);
 
 // ---- triangular solve --------------------------------------------------------------------
 struct TileGeom {

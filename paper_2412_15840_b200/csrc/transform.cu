@@ -21,18 +21,20 @@ namespace nds {
 // ------------------------------------------------------------------------------------------
 // Direct kernel: one output entry per thread. Used for 1 < inner < 8 or tiny n.
 // ------------------------------------------------------------------------------------------
-__global__ void mode_product_direct_kernel(const double2* __restrict__ mcol, int64_t inner, int n, int64_t outer,
-                                           const double2* __restrict__ x, double2* __restrict__ r, int accumulate) {
-  const int64_t total = inner * n * outer;
+// r (extent m along the mode) = M (m x n, column-major) x_mode x (extent n).
+__global__ void mode_product_direct_kernel(const double2* __restrict__ mcol, int64_t inner, int n, int m,
+                                           int64_t outer, const double2* __restrict__ x, double2* __restrict__ r,
+                                           int accumulate) {
+  const int64_t total = inner * m * outer;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
     const int64_t a = idx % inner;
     const int64_t t = idx / inner;
-    const int i = (int)(t % n);
-    const int64_t b = t / n;
+    const int i = (int)(t % m);
+    const int64_t b = t / m;
     const double2* xp = x + b * n * inner + a;
     double2 s = make_double2(0.0, 0.0);
-    for (int k = 0; k < n; ++k) s = cfma(s, __ldg(mcol + i + (int64_t)k * n), __ldg(xp + (int64_t)k * inner));
+    for (int k = 0; k < n; ++k) s = cfma(s, __ldg(mcol + i + (int64_t)k * m), __ldg(xp + (int64_t)k * inner));
     if (accumulate) s = cadd(r[idx], s);
     r[idx] = s;
   }
@@ -254,14 +256,15 @@ int mode_product_launch(const FactorSet& f, int mode, bool adjoint, const ModeVi
 }
 
 int mode_product_matrix_launch(const double2* mrow, const double2* mcol, const ModeView& v, const double2* x,
-                               double2* r, bool accumulate, cudaStream_t stream) {
+                               double2* r, bool accumulate, cudaStream_t stream, int64_t rows_out) {
   const int n = (int)v.n;
+  const int64_t m = rows_out > 0 ? rows_out : v.n;  // rows of M (output extent along the mode)
   const bool gemm = n >= 16 && (v.inner == 1 || v.inner >= 8);
   if (!gemm) {
-    const int64_t total = v.inner * v.n * v.outer;
+    const int64_t total = v.inner * m * v.outer;
     const int threads = 256;
     const int64_t blocks = std::min<int64_t>((total + threads - 1) / threads, 148 * 16);
-    mode_product_direct_kernel<<<(unsigned)blocks, threads, 0, stream>>>(mcol, v.inner, n, v.outer, x, r,
+    mode_product_direct_kernel<<<(unsigned)blocks, threads, 0, stream>>>(mcol, v.inner, n, (int)m, v.outer, x, r,
                                                                         accumulate ? 1 : 0);
     NDS_LAUNCH_CHECK();
     return kXformDirect;
@@ -273,19 +276,19 @@ int mode_product_matrix_launch(const double2* mrow, const double2* mcol, const M
     g.A = x;
     g.lda = n;
     g.rows = v.outer;
-    g.B = mcol;  // B(k, i) = M[i][k] = mcol[i + k n]
-    g.ldbk = n;
+    g.B = mcol;  // B(k, i) = M[i][k] = mcol[i + k m]
+    g.ldbk = m;
     g.ldbb = 0;
     g.wshift = 7;  // one column slice of width kBN
-    g.alim = n;
+    g.alim = m;
     g.blim = 1;
     g.C = r;
-    g.ldcr = n;
+    g.ldcr = m;
     g.ldcb = 0;
   } else {  // ROWM: C(i, (a, b)) = M(i, :) . X(:, (a, b))
     g.A = mrow;  // A(i, k) = M[i][k] = mrow[i n + k]
     g.lda = n;
-    g.rows = n;
+    g.rows = m;
     g.B = x;
     g.ldbk = v.inner;
     g.ldbb = v.inner * n;
@@ -294,7 +297,7 @@ int mode_product_matrix_launch(const double2* mrow, const double2* mcol, const M
     g.blim = v.outer;
     g.C = r;
     g.ldcr = v.inner;
-    g.ldcb = v.inner * n;
+    g.ldcb = v.inner * m;
   }
   launch_gemm(g, stream);
   return kXformGemm;

@@ -1,0 +1,180 @@
+"""Multi-GPU solve: one process per GPU, torch.distributed (NCCL over NVLink) for the exchanges.
+
+SURVEY.md 8(e). The transforms shard naturally; the triangular solve does not.
+
+Layouts (every local tensor is column-major complex128, flattened):
+  L_N: rank r owns the slab of mode N  [sN_r, sN_r + mN_r)   -> local dims (n_1, ..., n_{N-1}, mN_r)
+  L_1: rank q owns the slab of mode 1  [s1_q, s1_q + m1_q)   -> local dims (m1_q, n_2, ..., n_N)
+
+solve(B in L_N):
+  1. forward, modes 1..N-1: local (each mode product is independent across mode-N slabs);
+  2. all-to-all re-shard L_N -> L_1 (the only exchange of the transform);
+  3. forward, mode N: local in L_1;
+  4. triangular solve, slab-pipelined along mode 1: the rank holding the highest mode-1 slab
+     solves its slab (T_1 restricted to its diagonal block), broadcasts Y, every lower rank
+     applies  C_p -= T_1[p rows, q cols] x_1 Y_q  (rectangular mode-1 update), then the next
+     slab solves — T_1 is dense upper triangular, so rank p needs every q > p;
+  5. inverse, modes 2..N: local in L_1;
+  6. all-to-all re-shard L_1 -> L_N;
+  7. inverse, mode 1: local in L_N.  X is returned in the input layout L_N.
+
+The per-rank compute goes through `LocalOps`; `CudaLocalOps` calls the C ABI kernels on the
+rank's GPU. Tests substitute a CPU implementation to exercise the orchestration with gloo.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+
+def block_partition(n: int, parts: int):
+    """Contiguous block split of range(n): (starts, sizes), earlier parts one larger."""
+    base, extra = divmod(n, parts)
+    sizes = [base + (1 if r < extra else 0) for r in range(parts)]
+    starts = [sum(sizes[:r]) for r in range(parts)]
+    return starts, sizes
+
+
+class CudaLocalOps:
+    """Local compute on this rank's GPU through the ndsylv_b200 C ABI (device pointers)."""
+
+    def __init__(self, ctx):
+        self.ctx = ctx
+
+    def zeros(self, count, like):
+        return torch.zeros(count, dtype=torch.complex128, device=like.device)
+
+    def mode_product(self, dims, m, mode, x):
+        out = self.zeros(int(np.prod(dims)), x)
+        self.ctx.dev_mode_update(dims, mode, m, x.data_ptr(), out.data_ptr())
+        return out
+
+    def mode_update(self, dims_x, mode, m, x, acc):
+        """acc += m x_mode x (m rectangular, host)."""
+        self.ctx.dev_mode_update(dims_x, mode, m, x.data_ptr(), acc.data_ptr())
+
+    def back_substitute(self, ts, dims, c, tol):
+        self.ctx.dev_back_substitute(ts, dims, c.data_ptr(), tol)
+
+    def synchronize(self):
+        torch.cuda.synchronize()
+
+
+def _exchange(send_blocks, recv_sizes, group):
+    """Uneven all-to-all of complex128 blocks (sent as float64 pairs)."""
+    send = torch.cat([b.reshape(-1) for b in send_blocks]) if send_blocks else torch.empty(0, dtype=torch.complex128)
+    send_r = torch.view_as_real(send.contiguous()).reshape(-1)
+    recv_r = torch.empty(2 * sum(recv_sizes), dtype=torch.float64, device=send_r.device)
+    dist.all_to_all_single(recv_r, send_r, [2 * s for s in recv_sizes], [2 * b.numel() for b in send_blocks],
+                           group=group)
+    recv = torch.view_as_complex(recv_r.reshape(-1, 2))
+    out, off = [], 0
+    for s in recv_sizes:
+        out.append(recv[off:off + s])
+        off += s
+    return out
+
+
+class ShardedSolver:
+    """Distributed solve of sum_j A_j x_j X = B from host Schur factors (same on every rank)."""
+
+    def __init__(self, dims, us, ts, ops, group=None, singular_tol=0.0):
+        self.dims = tuple(int(d) for d in dims)
+        self.N = len(self.dims)
+        if self.N < 2:
+            raise ValueError("problem order must be at least 2")
+        self.us = [np.asfortranarray(u, dtype=np.complex128) for u in us]
+        self.ts = [np.asfortranarray(t, dtype=np.complex128) for t in ts]
+        self.uhs = [np.asfortranarray(u.conj().T) for u in self.us]
+        self.ops = ops
+        self.group = group
+        self.P = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        n1, nN = self.dims[0], self.dims[-1]
+        if n1 < self.P or nN < self.P:
+            raise ValueError("n_1 and n_N must be >= the number of ranks")
+        self.s1, self.m1 = block_partition(n1, self.P)
+        self.sN, self.mN = block_partition(nN, self.P)
+        # sylvester.cpp:29-33 — the tolerance of the WHOLE operator, not of a slab
+        self.tol = singular_tol if singular_tol > 0 else np.finfo(float).eps * sum(np.linalg.norm(t) for t in self.ts)
+
+    # local dims
+    def dims_LN(self, r):
+        return self.dims[:-1] + (self.mN[r],)
+
+    def dims_L1(self, q):
+        return (self.m1[q],) + self.dims[1:]
+
+    def reshard_N_to_1(self, x):
+        """x: this rank's L_N slab -> this rank's L_1 slab."""
+        r, n1 = self.rank, self.dims[0]
+        rows = x.reshape(-1, n1)  # column-major: mode 1 fastest
+        send = [rows[:, self.s1[q]:self.s1[q] + self.m1[q]].contiguous() for q in range(self.P)]
+        rest = int(np.prod(self.dims[1:-1]))
+        recv_sizes = [self.m1[r] * rest * self.mN[src] for src in range(self.P)]
+        blocks = _exchange(send, recv_sizes, self.group)
+        return torch.cat(blocks)  # mode N is the slowest index: source slabs concatenate in order
+
+    def reshard_1_to_N(self, y):
+        """y: this rank's L_1 slab -> this rank's L_N slab."""
+        r, nN = self.rank, self.dims[-1]
+        planes = y.reshape(nN, -1)  # column-major: mode N slowest
+        send = [planes[self.sN[q]:self.sN[q] + self.mN[q]].contiguous() for q in range(self.P)]
+        rest = int(np.prod(self.dims[1:-1]))
+        recv_sizes = [self.m1[src] * rest * self.mN[r] for src in range(self.P)]
+        blocks = _exchange(send, recv_sizes, self.group)
+        n1 = self.dims[0]
+        out = torch.empty(n1 * rest * self.mN[r], dtype=y.dtype, device=y.device)
+        o_rows = out.reshape(-1, n1)
+        for src, blk in enumerate(blocks):
+            o_rows[:, self.s1[src]:self.s1[src] + self.m1[src]] = blk.reshape(-1, self.m1[src])
+        return out
+
+    def solve(self, b_local):
+        """b_local: this rank's L_N slab of B. Returns this rank's L_N slab of X."""
+        ops, r, N = self.ops, self.rank, self.N
+        # 1. forward, modes 1..N-1 (local in L_N)
+        x = b_local
+        for j in range(1, N):
+            x = ops.mode_product(self.dims_LN(r), self.uhs[j - 1], j, x)
+        # 2. re-shard, 3. mode N (local in L_1)
+        c = self.reshard_N_to_1(x)
+        c = ops.mode_product(self.dims_L1(r), self.uhs[N - 1], N, c)
+        # 4. slab-pipelined triangular solve along mode 1
+        t1 = self.ts[0]
+        for q in reversed(range(self.P)):
+            sq, mq = self.s1[q], self.m1[q]
+            if r == q:
+                ts_local = [np.asfortranarray(t1[sq:sq + mq, sq:sq + mq])] + self.ts[1:]
+                ops.back_substitute(ts_local, self.dims_L1(q), c, self.tol)
+                yq = c
+            else:
+                yq = torch.empty(mq * int(np.prod(self.dims[1:])), dtype=c.dtype, device=c.device)
+            if q > 0:
+                yr = torch.view_as_real(yq)
+                dist.broadcast(yr, src=q, group=self.group)
+                yq = torch.view_as_complex(yr)
+                if r < q:
+                    sr, mr = self.s1[r], self.m1[r]
+                    block = -np.asfortranarray(t1[sr:sr + mr, sq:sq + mq])
+                    ops.mode_update(self.dims_L1(q), 1, block, yq, c)
+        # 5. inverse, modes 2..N (local in L_1), 6. re-shard, 7. mode 1 (local in L_N)
+        y = c
+        for j in range(2, N + 1):
+            y = ops.mode_product(self.dims_L1(r), self.us[j - 1], j, y)
+        x = self.reshard_1_to_N(y)
+        return ops.mode_product(self.dims_LN(r), self.us[0], 1, x)
+
+
+def scatter_LN(b, P):
+    """Split a full column-major tensor (numpy, shape dims) into the L_N slabs (host helper)."""
+    nN = b.shape[-1]
+    s, m = block_partition(nN, P)
+    flat = np.asfortranarray(b).reshape(-1, order="F")
+    plane = int(np.prod(b.shape[:-1]))
+    return [flat[s[r] * plane:(s[r] + m[r]) * plane].copy() for r in range(P)]
+
+
+def gather_LN(slabs, dims):
+    return np.concatenate([np.asarray(s) for s in slabs]).reshape(dims, order="F")
