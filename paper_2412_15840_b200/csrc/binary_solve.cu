@@ -82,11 +82,10 @@ __global__ void __launch_bounds__(kBinSolveThreads) binary_tile_solve_kernel(con
   for (int l = tid; l < E; l += blockDim.x) Y[base + l] = S[l];
 }
 
-void binary_solve_plan_build(BinarySolvePlan& bp, int n_modes, const double2* t_pool_dev) {
+void binary_solve_plan_build(BinarySolvePlan& bp, int n_modes) {
   const int m = std::min(n_modes, 12);
   bp.m = m;
   bp.n_outer = n_modes - m;
-  bp.t = t_pool_dev;
   const int64_t ntiles = (int64_t)1 << bp.n_outer;
   bp.levels = bp.n_outer + 1;
   // tiles by outer popcount, highest first
@@ -123,13 +122,14 @@ void binary_solve_plan_free(BinarySolvePlan& bp) {
   bp.pool = nullptr;
 }
 
-int binary_solve_launch(const BinarySolvePlan& bp, double2* c, cudaStream_t stream, Recorder* rec) {
+int binary_solve_launch(const BinarySolvePlan& bp, const double2* t_pool, double2* c, cudaStream_t stream,
+                        Recorder* rec) {
   static bool attr_set = false;
   if (!attr_set) {
     NDS_CUDA(cudaFuncSetAttribute(binary_tile_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 4096 * 16));
     attr_set = true;
   }
-  BinSolveGeom g{bp.m, bp.n_outer, bp.m + 1, bp.t};
+  BinSolveGeom g{bp.m, bp.n_outer, bp.m + 1, t_pool};
   const size_t smem = ((size_t)1 << bp.m) * sizeof(double2);
   int launches = 0;
   for (int lv = 0; lv < bp.levels; ++lv) {
@@ -143,4 +143,13 @@ int binary_solve_launch(const BinarySolvePlan& bp, double2* c, cudaStream_t stre
   return launches;
 }
 
+}  // namespace nds
+
+namespace nds {
+SolverCache::~SolverCache() {
+  if (binary)
+    binary_solve_plan_free(bsp);
+  else
+    solve_plan_free(sp);
+}
 }  // namespace nds

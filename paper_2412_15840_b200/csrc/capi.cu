@@ -4,6 +4,7 @@
 #include <cmath>
 #include <cstring>
 #include <limits>
+#include <map>
 #include <memory>
 #include <string>
 #include <vector>
@@ -13,6 +14,7 @@
 #include "schur.h"
 
 using nds::Error;
+using nds::ModeView;
 
 struct nds_ctx {
   int device = 0;
@@ -23,6 +25,11 @@ struct nds_ctx {
   size_t ws_bytes = 0;
   void* scratch = nullptr;  // small device scratch (reductions)
   cudaEvent_t ev[8] = {};
+  cudaStream_t copy = nullptr;  // host<->device chunk copies overlapped with compute
+  void* stage = nullptr;        // pinned staging for factor uploads
+  size_t stage_bytes = 0;
+  cudaEvent_t cev[16] = {};
+  std::map<std::vector<int64_t>, std::shared_ptr<nds::SolverCache>> solvers;  // by extents
 };
 
 struct nds_plan {
@@ -36,10 +43,7 @@ struct nds_plan {
   double min_abs_den = 0.0;
   nds::FactorSet f;
   std::vector<nds::BinGroup> groups;  // fused passes over runs of binary modes
-  nds::SolvePlan sp;
-  bool have_solve_plan = false;
-  bool binary = false;  // all n_j = 2: binary_solve.cu regime
-  nds::BinarySolvePlan bsp;
+  std::shared_ptr<nds::SolverCache> solver;  // dims-only structures, shared via the context
   int launches = 0;
   // per-launch CUDA-event profile (nds_plan_profile_begin / _end)
   bool profiling = false;
@@ -121,66 +125,70 @@ void upload_factors(nds_ctx* ctx, nds::FactorSet& f, int n_modes, const int64_t*
     sq += dims[j] * dims[j];
     diag += dims[j];
   }
+  // device pool: [U layouts: 4 sq][T: sq][diag][raw U: sq]; host staging (pinned, per context):
+  // [raw U: sq][T: sq][diag] — one fast H2D, the four U layouts are built on the device.
   const int64_t n_u = u ? 4 * sq : 0;
   const int64_t n_t = t ? sq : 0;
   const int64_t n_d = t ? diag : 0;
-  std::vector<double2> host((size_t)(n_u + n_t + n_d) + 1);
-  NDS_CUDA(cudaMalloc(&f.pool, host.size() * sizeof(double2)));
-  int64_t off = 0;
+  const int64_t n_raw = u ? sq : 0;
+  const size_t stage_bytes = (size_t)(n_raw + n_t + n_d) * sizeof(double2);
+  NDS_CUDA(cudaStreamSynchronize(ctx->stream));  // the staging buffer may still feed a previous copy
+  if (ctx->stage_bytes < stage_bytes) {
+    if (ctx->stage) cudaFreeHost(ctx->stage);
+    ctx->stage = nullptr;
+    ctx->stage_bytes = 0;
+    NDS_CUDA(cudaHostAlloc(&ctx->stage, stage_bytes, cudaHostAllocDefault));
+    ctx->stage_bytes = stage_bytes;
+  }
+  NDS_CUDA(cudaMallocAsync(&f.pool, (size_t)(n_u + n_t + n_d + n_raw + 1) * sizeof(double2), ctx->stream));
+  f.stream = ctx->stream;
+  double2* stage = (double2*)ctx->stage;
   nds::Geom& g = f.geom;
   g.n_modes = n_modes;
   g.total = 1;
-  int64_t toff = 0, doff = 0;
+  int64_t off = 0, soff = 0, toff = 0, doff = 0;
   for (int j = 0; j < n_modes; ++j) {
     const int64_t n = dims[j];
     g.dims[j] = n;
     g.strides[j] = g.total;
     g.total *= n;
     if (u) {
-      double2* ur = host.data() + off;
-      double2* uc = ur + n * n;
-      double2* hr = uc + n * n;
-      double2* hc = hr + n * n;
-      for (int64_t k = 0; k < n; ++k)
-        for (int64_t i = 0; i < n; ++i) {
-          const nds_z z = u[j][i + k * n];  // U(i, k), column-major
-          uc[i + k * n] = make_double2(z.re, z.im);
-          ur[i * n + k] = make_double2(z.re, z.im);
-          // U^H(k, i) = conj(U(i, k))
-          hc[k + i * n] = make_double2(z.re, -z.im);
-          hr[k * n + i] = make_double2(z.re, -z.im);
-        }
+      std::memcpy(stage + soff, u[j], (size_t)(n * n) * sizeof(double2));
       f.u_row[j] = f.pool + off;
       f.u_col[j] = f.pool + off + n * n;
       f.uh_row[j] = f.pool + off + 2 * n * n;
       f.uh_col[j] = f.pool + off + 3 * n * n;
       off += 4 * n * n;
+      soff += n * n;
     }
   }
+  double2* raw = f.pool + n_u + n_t + n_d;
   if (t) {
     f.t_pool = f.pool + off;
     for (int j = 0; j < n_modes; ++j) {
       const int64_t n = dims[j];
       g.toff[j] = toff;
-      for (int64_t i = 0; i < n * n; ++i) host[off + toff + i] = make_double2(t[j][i].re, t[j][i].im);
+      std::memcpy(stage + soff + toff, t[j], (size_t)(n * n) * sizeof(double2));
       toff += n * n;
     }
-    off += toff;
-    f.diag_pool = f.pool + off;
+    f.diag_pool = f.pool + off + toff;
     for (int j = 0; j < n_modes; ++j) {
       const int64_t n = dims[j];
       g.doff[j] = doff;
-      for (int64_t i = 0; i < n; ++i) host[off + doff + i] = make_double2(t[j][i + i * n].re, t[j][i + i * n].im);
+      for (int64_t i = 0; i < n; ++i) stage[soff + toff + doff + i] = make_double2(t[j][i + i * n].re, t[j][i + i * n].im);
       doff += n;
     }
-    off += doff;
+    NDS_CUDA(cudaMemcpyAsync(f.t_pool, stage + soff, (size_t)(toff + doff) * sizeof(double2), cudaMemcpyHostToDevice,
+                             ctx->stream));
   }
-  NDS_CUDA(cudaMemcpyAsync(f.pool, host.data(), (size_t)off * sizeof(double2), cudaMemcpyHostToDevice, ctx->stream));
-  NDS_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (u) {
+    NDS_CUDA(cudaMemcpyAsync(raw, stage, (size_t)sq * sizeof(double2), cudaMemcpyHostToDevice, ctx->stream));
+    nds::factor_layouts_launch(f, raw, ctx->stream);
+  }
 }
 
 void free_factors(nds::FactorSet& f) {
-  if (f.pool) cudaFree(f.pool);
+  if (f.pool) cudaFreeAsync(f.pool, f.stream);
   f.pool = nullptr;
 }
 
@@ -260,6 +268,19 @@ int launch_pass(nds_plan* p, const XPass& ps, bool adjoint, const double2* src, 
                                   false, p->ctx->stream);
 }
 
+// The same pass restricted to one of K contiguous chunks of the slowest modes (those of the last
+// pass): its outer extent shrinks by K; src / dst point at the chunk.
+int launch_pass_chunk(nds_plan* p, const XPass& ps, bool adjoint, const double2* src, double2* dst, int K) {
+  if (ps.group >= 0) {
+    nds::BinGroup g = p->groups[ps.group];
+    g.outer /= K;
+    return nds::binary_pass_launch(p->f, g, adjoint, src, dst, p->ctx->stream);
+  }
+  ModeView v = nds::mode_view(p->n_modes, p->dims, ps.mode);
+  v.outer /= K;
+  return nds::mode_product_launch(p->f, ps.mode, adjoint, v, src, dst, false, p->ctx->stream);
+}
+
 int transform_chain(nds_plan* p, bool adjoint, const double2* in, double2* out, double2* work) {
   const std::vector<XPass> passes = transform_passes(p);
   const int N = (int)passes.size();
@@ -284,22 +305,28 @@ int transform_chain(nds_plan* p, bool adjoint, const double2* in, double2* out, 
 
 // Solver for the plan's regime: all-binary tiles, or the general tiled solve (v1 / v2).
 void build_solver(nds_plan* p) {
-  bool binary = true;
-  for (int j = 0; j < p->n_modes; ++j) binary = binary && p->dims[j] == 2;
-  if (binary) {
-    nds::binary_solve_plan_build(p->bsp, p->n_modes, p->f.t_pool);
-  } else {
-    int64_t toff[NDS_MAX_MODES];
-    for (int j = 0; j < p->n_modes; ++j) toff[j] = p->f.geom.toff[j];
-    nds::solve_plan_build(p->sp, p->n_modes, p->dims, toff);
+  const std::vector<int64_t> key(p->dims, p->dims + p->n_modes);
+  auto& slot = p->ctx->solvers[key];
+  if (!slot) {
+    auto sc = std::make_shared<nds::SolverCache>();
+    bool binary = true;
+    for (int j = 0; j < p->n_modes; ++j) binary = binary && p->dims[j] == 2;
+    sc->binary = binary;
+    if (binary) {
+      nds::binary_solve_plan_build(sc->bsp, p->n_modes);
+    } else {
+      int64_t toff[NDS_MAX_MODES];
+      for (int j = 0; j < p->n_modes; ++j) toff[j] = p->f.geom.toff[j];  // depends on dims only
+      nds::solve_plan_build(sc->sp, p->n_modes, p->dims, toff);
+    }
+    slot = sc;
   }
-  p->binary = binary;
-  p->have_solve_plan = true;
+  p->solver = slot;
 }
 
 int launch_solver(nds_plan* p, double2* c, cudaStream_t s, nds::Recorder* rec) {
-  if (p->binary) return nds::binary_solve_launch(p->bsp, c, s, rec);
-  return nds::backsub_launch(p->sp, p->f.t_pool, c, s, rec);
+  if (p->solver->binary) return nds::binary_solve_launch(p->solver->bsp, p->f.t_pool, c, s, rec);
+  return nds::backsub_launch(p->solver->sp, p->f.t_pool, c, s, rec);
 }
 
 int backsub_run(nds_plan* p, double2* c) {
@@ -391,13 +418,7 @@ void plan_destroy_impl(nds_plan* p) {
   cudaSetDevice(p->ctx->device);
   for (auto e : p->pev) cudaEventDestroy(e);
   free_factors(p->f);
-  if (p->have_solve_plan) {
-    if (p->binary)
-      nds::binary_solve_plan_free(p->bsp);
-    else
-      nds::solve_plan_free(p->sp);
-  }
-  delete p;
+  delete p;  // the shared solver structures stay cached in the context
 }
 
 void report_static(const nds_plan* p, nds_report* rep) {
@@ -429,13 +450,86 @@ void execute_host_impl(nds_plan* p, const nds_z* hb, nds_z* hx, nds_report* rep)
   const size_t bytes = (size_t)p->total * sizeof(double2);
   double2* X = ctx->ws[0];
   double2* W = ctx->ws[1];
-  NDS_CUDA(cudaEventRecord(ctx->ev[4], s));
-  NDS_CUDA(cudaMemcpyAsync(X, hb, bytes, cudaMemcpyHostToDevice, s));
-  const int launches = execute(p, X, X, W, ctx->ev);
-  NDS_CUDA(cudaMemcpyAsync(hx, X, bytes, cudaMemcpyDeviceToHost, s));
-  NDS_CUDA(cudaEventRecord(ctx->ev[5], s));
+  const std::vector<XPass> passes = transform_passes(p);
+  const int np = (int)passes.size();
+  // Copy/compute overlap: the passes before the last one act independently on contiguous chunks
+  // of the slowest modes (those of the last pass), so B streams in chunk by chunk under them and
+  // X streams out under the inverse (whose last-pass-first order keeps the per-chunk passes last).
+  int K = 1;
+  if (np >= 2) {
+    const ModeView lastv = nds::mode_view(p->n_modes, p->dims, passes.back().mode);
+    const int64_t outer_last = p->total / lastv.inner;  // product of the last pass's modes and beyond
+    for (int k : {8, 4, 2})
+      if (outer_last % k == 0 && p->total / k >= (1 << 16)) {
+        K = k;
+        break;
+      }
+  }
+  int launches = 0;
+  if (K == 1) {
+    NDS_CUDA(cudaEventRecord(ctx->ev[4], s));
+    NDS_CUDA(cudaMemcpyAsync(X, hb, bytes, cudaMemcpyHostToDevice, s));
+    launches = execute(p, X, X, W, ctx->ev);
+    NDS_CUDA(cudaMemcpyAsync(hx, X, bytes, cudaMemcpyDeviceToHost, s));
+    NDS_CUDA(cudaEventRecord(ctx->ev[5], s));
+  } else {
+    cudaStream_t cs = ctx->copy;
+    const int64_t chunk = p->total / K;
+    const size_t cbytes = (size_t)chunk * sizeof(double2);
+    auto dst_of = [&](int pass) { return (pass % 2 == 1) ? W : X; };  // pass 1..2 np; input in X
+    NDS_CUDA(cudaEventRecord(ctx->ev[4], s));
+    NDS_CUDA(cudaStreamWaitEvent(cs, ctx->ev[4], 0));
+    for (int k = 0; k < K; ++k) {
+      NDS_CUDA(cudaMemcpyAsync(X + k * chunk, hb + k * chunk, cbytes, cudaMemcpyHostToDevice, cs));
+      NDS_CUDA(cudaEventRecord(ctx->cev[k], cs));
+    }
+    NDS_CUDA(cudaEventRecord(ctx->ev[6], cs));
+    for (int k = 0; k < K; ++k) {  // forward: passes 1 .. np-1 per chunk as it lands
+      NDS_CUDA(cudaStreamWaitEvent(s, ctx->cev[k], 0));
+      const double2* src = X + k * chunk;
+      for (int j = 1; j < np; ++j) {
+        double2* dst = dst_of(j) + k * chunk;
+        launch_pass_chunk(p, passes[j - 1], true, src, dst, K);
+        ++launches;
+        src = dst;
+      }
+    }
+    NDS_CUDA(cudaEventRecord(ctx->ev[0], s));
+    launch_pass(p, passes.back(), true, dst_of(np - 1), dst_of(np));  // forward last pass, whole tensor
+    ++launches;
+    double2* c = dst_of(np);
+    NDS_CUDA(cudaEventRecord(ctx->ev[1], s));
+    launches += backsub_run(p, c);
+    NDS_CUDA(cudaEventRecord(ctx->ev[2], s));
+    launch_pass(p, passes.back(), false, c, dst_of(np + 1));  // inverse: last pass first
+    ++launches;
+    for (int k = 0; k < K; ++k) {
+      const double2* src = dst_of(np + 1) + k * chunk;
+      for (int j = 1; j < np; ++j) {
+        double2* dst = dst_of(np + 1 + j) + k * chunk;
+        launch_pass_chunk(p, passes[j - 1], false, src, dst, K);
+        ++launches;
+        src = dst;
+      }
+      if (p->flags & NDS_REAL_OUTPUT) launches += nds::real_part_launch(X + k * chunk, chunk, s);
+      NDS_CUDA(cudaEventRecord(ctx->cev[8 + k], s));
+      NDS_CUDA(cudaStreamWaitEvent(cs, ctx->cev[8 + k], 0));
+      NDS_CUDA(cudaMemcpyAsync(hx + k * chunk, X + k * chunk, cbytes, cudaMemcpyDeviceToHost, cs));
+    }
+    NDS_CUDA(cudaEventRecord(ctx->ev[3], s));
+    NDS_CUDA(cudaEventRecord(ctx->ev[5], cs));
+    NDS_CUDA(cudaStreamWaitEvent(s, ctx->ev[5], 0));
+  }
   NDS_CUDA(cudaStreamSynchronize(s));
-  if (rep) {
+  if (rep && K > 1) {  // overlapped: the forward stage includes the streamed H2D of B
+    report_static(p, rep);
+    rep->h2d_seconds = ev_ms(ctx->ev[4], ctx->ev[6]) * 1e-3;
+    rep->transform_seconds = ev_ms(ctx->ev[4], ctx->ev[1]) * 1e-3;
+    rep->backsub_seconds = ev_ms(ctx->ev[1], ctx->ev[2]) * 1e-3;
+    rep->inverse_seconds = ev_ms(ctx->ev[2], ctx->ev[3]) * 1e-3;
+    rep->d2h_seconds = ev_ms(ctx->ev[3], ctx->ev[5]) * 1e-3;
+    rep->kernel_launches = launches;
+  } else if (rep) {
     report_static(p, rep);
     rep->h2d_seconds = ev_ms(ctx->ev[4], ctx->ev[0]) * 1e-3;
     rep->transform_seconds = ev_ms(ctx->ev[0], ctx->ev[1]) * 1e-3;
@@ -497,6 +591,13 @@ int nds_ctx_create(nds_ctx** out, int device) {
     c->stream = c->own;
     NDS_CUDA(cudaMalloc(&c->scratch, 256));
     for (auto& e : c->ev) NDS_CUDA(cudaEventCreate(&e));
+    NDS_CUDA(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
+    // keep stream-ordered allocations (factor pools) cached instead of returning them at syncs
+    cudaMemPool_t pool;
+    NDS_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t keep = UINT64_MAX;
+    NDS_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    for (auto& e : c->cev) NDS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     *out = c.release();
   });
 }
@@ -509,6 +610,10 @@ void nds_ctx_destroy(nds_ctx* ctx) {
   if (ctx->scratch) cudaFree(ctx->scratch);
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
+  for (auto& e : ctx->cev)
+    if (e) cudaEventDestroy(e);
+  if (ctx->copy) cudaStreamDestroy(ctx->copy);
+  if (ctx->stage) cudaFreeHost(ctx->stage);
   if (ctx->own) cudaStreamDestroy(ctx->own);
   delete ctx;
 }
@@ -532,6 +637,8 @@ void nds_ctx_trim(nds_ctx* ctx) {
       w = nullptr;
     }
   ctx->ws_bytes = 0;
+  cudaStreamSynchronize(ctx->stream);
+  ctx->solvers.clear();  // plans still alive keep their shared solver structures
 }
 
 int nds_schur(nds_ctx* ctx, int n, const nds_z* a, nds_z* u, nds_z* t) {

@@ -22,16 +22,64 @@ __device__ __forceinline__ double2 den_at(const Geom& g, const double2* __restri
   return den;
 }
 
-__global__ void den_scan_kernel(const Geom g, const double2* __restrict__ diag, double tol,
+// Eigenvalue sums without per-entry integer division: the leading modes A (product sizeA <= 1024)
+// get a shared table dA[a] = sum_{j in A} T_j(i_j, i_j); each row (one index b of the remaining
+// modes) adds dB(b) = sum_{j not in A} T_j(i_j, i_j), decoded once per row. den = dA + dB (the
+// reference sums j = 1..N left to right; the grouping only changes the last bit).
+struct DenSplit {
+  int nA;         // leading modes in A
+  int sizeA;      // prod of their extents
+  int64_t rows;   // total / sizeA
+};
+
+static DenSplit den_split(const Geom& g) {
+  DenSplit s{0, 1, 0};
+  while (s.nA < g.n_modes && s.sizeA * g.dims[s.nA] <= 1024) s.sizeA *= (int)g.dims[s.nA++];
+  s.rows = g.total / s.sizeA;
+  return s;
+}
+
+__device__ __forceinline__ void den_tables(const Geom& g, const DenSplit& s, const double2* __restrict__ diag,
+                                           double2* dA) {
+  for (int a = threadIdx.x; a < s.sizeA; a += blockDim.x) {
+    int rem = a;
+    double2 d = make_double2(0.0, 0.0);
+    for (int j = 0; j < s.nA; ++j) {
+      d = cadd(d, __ldg(diag + g.doff[j] + rem % g.dims[j]));
+      rem /= (int)g.dims[j];
+    }
+    dA[a] = d;
+  }
+}
+
+__device__ __forceinline__ double2 den_row(const Geom& g, const DenSplit& s, const double2* __restrict__ diag,
+                                           int64_t row) {
+  double2 d = make_double2(0.0, 0.0);
+  for (int j = s.nA; j < g.n_modes; ++j) {
+    d = cadd(d, __ldg(diag + g.doff[j] + row % g.dims[j]));
+    row /= g.dims[j];
+  }
+  return d;
+}
+
+__global__ void den_scan_kernel(const Geom g, const DenSplit s, const double2* __restrict__ diag, double tol,
                                 unsigned long long* __restrict__ min_bits, long long* __restrict__ max_bad) {
+  __shared__ double2 dA[1024];
+  __shared__ double2 dB;
+  den_tables(g, s, diag, dA);
   double local_min = INFINITY;
   long long local_bad = -1;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < g.total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const double2 den = den_at(g, diag, idx);
-    const double a = hypot(den.x, den.y);
-    local_min = fmin(local_min, a);
-    if (a <= tol) local_bad = max(local_bad, (long long)idx);  // sylvester.cpp:103 (NaN passes)
+  for (int64_t row = blockIdx.x; row < s.rows; row += gridDim.x) {
+    __syncthreads();
+    if (threadIdx.x == 0) dB = den_row(g, s, diag, row);
+    __syncthreads();
+    const double2 db = dB;
+    for (int a = threadIdx.x; a < s.sizeA; a += blockDim.x) {
+      const double2 den = cadd(dA[a], db);
+      const double v = hypot(den.x, den.y);
+      local_min = fmin(local_min, v);
+      if (v <= tol) local_bad = max(local_bad, (long long)(row * s.sizeA + a));  // sylvester.cpp:103
+    }
   }
   for (int o = 16; o > 0; o >>= 1) {
     local_min = fmin(local_min, __shfl_xor_sync(0xffffffffu, local_min, o));
@@ -51,8 +99,9 @@ void den_scan(const Geom& g, const double2* diag, double tol, double* min_abs, i
   const long long init_bad = -1;
   NDS_CUDA(cudaMemcpyAsync(d_min, &init_min, 8, cudaMemcpyHostToDevice, stream));
   NDS_CUDA(cudaMemcpyAsync(d_bad, &init_bad, 8, cudaMemcpyHostToDevice, stream));
-  const int64_t blocks = std::min<int64_t>((g.total + kEwThreads - 1) / kEwThreads, 148 * 32);
-  den_scan_kernel<<<(unsigned)blocks, kEwThreads, 0, stream>>>(g, diag, tol, d_min, d_bad);
+  const DenSplit s = den_split(g);
+  const int64_t blocks = std::min<int64_t>(s.rows, 148 * 16);
+  den_scan_kernel<<<(unsigned)blocks, kEwThreads, 0, stream>>>(g, s, diag, tol, d_min, d_bad);
   NDS_LAUNCH_CHECK();
   unsigned long long h_min;
   long long h_bad;
@@ -66,17 +115,69 @@ void den_scan(const Geom& g, const double2* diag, double tol, double* min_abs, i
   *max_bad = h_bad;
 }
 
-__global__ void fast_divide_kernel(const Geom g, const double2* __restrict__ diag, double2* __restrict__ c) {
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < g.total;
-       idx += (int64_t)gridDim.x * blockDim.x)
-    c[idx] = cdiv(c[idx], den_at(g, diag, idx));
+__global__ void fast_divide_kernel(const Geom g, const DenSplit s, const double2* __restrict__ diag,
+                                   double2* __restrict__ c) {
+  __shared__ double2 dA[1024];
+  __shared__ double2 dB;
+  den_tables(g, s, diag, dA);
+  for (int64_t row = blockIdx.x; row < s.rows; row += gridDim.x) {
+    __syncthreads();
+    if (threadIdx.x == 0) dB = den_row(g, s, diag, row);
+    __syncthreads();
+    const double2 db = dB;
+    double2* cr = c + row * s.sizeA;
+    for (int a = threadIdx.x; a < s.sizeA; a += blockDim.x) cr[a] = cdiv(cr[a], cadd(dA[a], db));
+  }
 }
 
 int fast_divide_launch(const Geom& g, const double2* diag, double2* c, cudaStream_t stream) {
-  const int64_t blocks = std::min<int64_t>((g.total + kEwThreads - 1) / kEwThreads, 148 * 32);
-  fast_divide_kernel<<<(unsigned)blocks, kEwThreads, 0, stream>>>(g, diag, c);
+  const DenSplit s = den_split(g);
+  const int64_t blocks = std::min<int64_t>(s.rows, 148 * 16);
+  fast_divide_kernel<<<(unsigned)blocks, kEwThreads, 0, stream>>>(g, s, diag, c);
   NDS_LAUNCH_CHECK();
   return 1;
+}
+
+struct LayoutArgs {
+  int n_modes;
+  int n[NDS_MAX_MODES];
+  int64_t raw_off[NDS_MAX_MODES];
+  double2* ur[NDS_MAX_MODES];
+  double2* uc[NDS_MAX_MODES];
+  double2* hr[NDS_MAX_MODES];
+  double2* hc[NDS_MAX_MODES];
+};
+
+__global__ void factor_layouts_kernel(const LayoutArgs a, const double2* __restrict__ raw) {
+  const int j = blockIdx.y;
+  const int n = a.n[j];
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n * n; e += gridDim.x * blockDim.x) {
+    const int i = e % n, k = e / n;
+    const double2 z = raw[a.raw_off[j] + e];  // U(i, k)
+    a.uc[j][i + k * n] = z;
+    a.ur[j][i * n + k] = z;
+    a.hc[j][k + i * n] = conj2(z);  // U^H(k, i) = conj(U(i, k))
+    a.hr[j][k * n + i] = conj2(z);
+  }
+}
+
+void factor_layouts_launch(const FactorSet& f, const double2* raw, cudaStream_t stream) {
+  LayoutArgs a{};
+  a.n_modes = f.n_modes;
+  int64_t off = 0, maxsq = 1;
+  for (int j = 0; j < f.n_modes; ++j) {
+    a.n[j] = (int)f.dims[j];
+    a.raw_off[j] = off;
+    off += f.dims[j] * f.dims[j];
+    maxsq = std::max<int64_t>(maxsq, f.dims[j] * f.dims[j]);
+    a.ur[j] = f.u_row[j];
+    a.uc[j] = f.u_col[j];
+    a.hr[j] = f.uh_row[j];
+    a.hc[j] = f.uh_col[j];
+  }
+  const dim3 grid((unsigned)std::min<int64_t>((maxsq + 255) / 256, 1024), (unsigned)f.n_modes);
+  factor_layouts_kernel<<<grid, 256, 0, stream>>>(a, raw);
+  NDS_LAUNCH_CHECK();
 }
 
 __global__ void real_part_kernel(double2* __restrict__ x, int64_t total) {

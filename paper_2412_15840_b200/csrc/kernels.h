@@ -21,6 +21,7 @@ struct FactorSet {
   double2* uh_row[NDS_MAX_MODES] = {};
   double2* uh_col[NDS_MAX_MODES] = {};
   double2* pool = nullptr;  // one allocation backing all of the above + T + diag
+  cudaStream_t stream = nullptr;  // stream the pool was allocated on (stream-ordered free)
   double2* t_pool = nullptr;     // T_j column-major, concatenated (offsets in geom.toff)
   double2* diag_pool = nullptr;  // diag(T_j), concatenated (offsets in geom.doff)
   Geom geom{};
@@ -109,16 +110,26 @@ struct SolvePlan {
 // modes, one launch per outer popcount level (binary_solve.cu).
 struct BinarySolvePlan {
   int m = 0, n_outer = 0, levels = 0;
-  const double2* t = nullptr;  // T pool (T_j at t + 4 j)
   std::vector<int64_t> level_off;
   int64_t* d_tiles = nullptr;
   int* d_wf = nullptr;
   int* d_wf_off = nullptr;
   void* pool = nullptr;
 };
-void binary_solve_plan_build(BinarySolvePlan& bp, int n_modes, const double2* t_pool_dev);
+void binary_solve_plan_build(BinarySolvePlan& bp, int n_modes);
 void binary_solve_plan_free(BinarySolvePlan& bp);
-int binary_solve_launch(const BinarySolvePlan& bp, double2* c, cudaStream_t stream, Recorder* rec = nullptr);
+// t_pool: T_j (2x2 column-major) at t_pool + 4 j.
+int binary_solve_launch(const BinarySolvePlan& bp, const double2* t_pool, double2* c, cudaStream_t stream,
+                        Recorder* rec = nullptr);
+
+// Dims-only solver structures (tile lists, work items, partial buffers, internal streams), cached
+// per context and shared by every plan with the same extents.
+struct SolverCache {
+  bool binary = false;
+  BinarySolvePlan bsp;
+  SolvePlan sp;
+  ~SolverCache();
+};
 
 void solve_plan_build(SolvePlan& sp, int n_modes, const int64_t* dims, const int64_t* toff);
 void solve_plan_free(SolvePlan& sp);
@@ -127,6 +138,8 @@ int backsub_launch(const SolvePlan& sp, const double2* t_pool, double2* c, cudaS
                    Recorder* rec = nullptr);
 
 // ---- elementwise / reductions ------------------------------------------------------------
+// Build u_row / u_col / uh_row / uh_col of every mode from the raw column-major U_j (concatenated).
+void factor_layouts_launch(const FactorSet& f, const double2* raw, cudaStream_t stream);
 // min |den| over all entries and the largest flat index with |den| <= tol (-1 if none).
 void den_scan(const Geom& g, const double2* diag, double tol, double* min_abs, int64_t* max_bad, cudaStream_t stream,
               void* scratch /* >= 16 bytes device */);
