@@ -2,6 +2,13 @@
 // in {8, 16} dividing every n_j (c0, c1: N=3 B=16; c2, c3: N=4 B=8).
 // Included by backsub.cu.
 
+#ifdef NDS_DIAG_CLOCK  // timing probes for tools/microbench/diag_bench.cu only
+#define NDS_PROBE(k, v) \
+  if (tid == 0 && blockIdx.x == 0) nds_diag_probe[lv * 4 + (k)] = clock64() + (long long)((v) * 0)
+#else
+#define NDS_PROBE(k, v)
+#endif
+
 constexpr int kUpdThreads = 256;
 constexpr int kALd = 12;  // A stage row stride (complex): = 4 mod 8 -> conflict-free fragments
 
@@ -298,6 +305,7 @@ __global__ void __launch_bounds__(NT, 2)
     if (warp < (info >> 8)) {  // warp-uniform: this warp holds entries on hyperplane lv
       const int grp = info & 0xff;
       const int lraw = thr[lv * NT + tid];
+      NDS_PROBE(0, lraw);
       const bool act = lraw != 0xffff;
       const int l = act ? lraw : 0;
       const int sub = tid & (grp - 1);
@@ -312,31 +320,47 @@ __global__ void __launch_bounds__(NT, 2)
       double2 den = make_double2(0.0, 0.0);
 #pragma unroll
       for (int m = 0; m < N; ++m) den = cadd(den, Td[m * B * B + lm[m] * (B + 1)]);
+      const double2 rden = crecip_fast(den);  // issued before the dot products, off their chain
+      NDS_PROBE(1, rden.x);
       double2 a0 = make_double2(0.0, 0.0), a1 = make_double2(0.0, 0.0);
+      double2 a2 = make_double2(0.0, 0.0), a3 = make_double2(0.0, 0.0);
       if (act) {
 #pragma unroll
         for (int m = 0; m < N; ++m) {
           const double2* tp = Td + m * B * B + lm[m] * (B + 1) + 1 + sub;
           const double2* sp = S + pl + (1 + sub) * PS::at(m);
           const int ss = grp * PS::at(m);
-          int q = B - 1 - lm[m] - sub;
+          int q = B - 1 - lm[m] - sub;  // this lane's terms: ceil(q / grp)
 #pragma unroll 1
-          for (; q > grp; q -= 2 * grp) {
+          for (; q > 3 * grp; q -= 4 * grp) {  // 4 terms in flight
+            const double2 t0 = tp[0], t1 = tp[grp], t2 = tp[2 * grp], t3 = tp[3 * grp];
+            const double2 s0 = sp[0], s1 = sp[ss], s2 = sp[2 * ss], s3 = sp[3 * ss];
+            a0 = cfma(a0, t0, s0);
+            a1 = cfma(a1, t1, s1);
+            a2 = cfma(a2, t2, s2);
+            a3 = cfma(a3, t3, s3);
+            tp += 4 * grp;
+            sp += 4 * ss;
+          }
+          if (q > grp) {
             const double2 t0 = tp[0], t1 = tp[grp], s0 = sp[0], s1 = sp[ss];
             a0 = cfma(a0, t0, s0);
             a1 = cfma(a1, t1, s1);
             tp += 2 * grp;
             sp += 2 * ss;
+            q -= 2 * grp;
           }
-          if (q > 0) a0 = cfma(a0, tp[0], sp[0]);
+          if (q > 0) a2 = cfma(a2, tp[0], sp[0]);
         }
       }
-      double2 acc = cadd(a0, a1);
+      double2 acc = cadd(cadd(a0, a1), cadd(a2, a3));
+      NDS_PROBE(2, acc.x);
       for (int o = 1; o < grp; o <<= 1) {
         acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
         acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
       }
-      if (act && sub == 0) S[pl] = cmul(csub(S[pl], acc), crecip(den));
+      if (act && sub == 0) S[pl] = cmul(csub(S[pl], acc), rden);
+      NDS_PROBE(3, S[pl].x);
     }
     __syncthreads();
 #ifdef NDS_DIAG_CLOCK

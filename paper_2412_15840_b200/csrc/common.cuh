@@ -144,6 +144,26 @@ __device__ __forceinline__ double2 crecip(double2 d) {
   return make_double2(xr * inv * s, -xi * inv * s);
 }
 
+// 1 / x for a normal positive double: MUFU reciprocal seed + two Newton steps (<= 1 ulp).
+__device__ __forceinline__ double drcp_fast(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
+// crecip without the IEEE division subroutine (prescaled as crecip, so |d|^2 is normal).
+__device__ __forceinline__ double2 crecip_fast(double2 d) {
+  const double m = fmax(fabs(d.x), fabs(d.y));
+  const int e = ((__double2hiint(m) >> 20) & 0x7ff) - 1023;
+  const double s = __hiloint2double((1023 - e) << 20, 0);
+  const double xr = d.x * s, xi = d.y * s;
+  const double inv = drcp_fast(fma(xr, xr, xi * xi));
+  return make_double2(xr * inv * s, -xi * inv * s);
+}
+
 inline int ceil_div_i(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
 
 }  // namespace nds

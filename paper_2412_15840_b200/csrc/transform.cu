@@ -13,6 +13,8 @@
 // real DMMAs per 8x8x4 block (re.re, -im.im, re.im, im.re) accumulated in registers; tiles are
 // staged global->shared with a multi-stage cp.async pipeline into bank-conflict-free padded
 // layouts (row strides = 4 resp. 2 mod 8 complex for the DMMA fragment pattern).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -86,7 +88,7 @@ struct GemmCfg {
   static constexpr int NI = BN / WN / 8;
 };
 
-template <int BM, int BN, int BK, int WM, int WN, int STAGES>
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool M3>
 __global__ void __launch_bounds__(WM* WN * 32, 1) zgemm_dmma_kernel(const GemmArgs g) {
   using Cfg = GemmCfg<BM, BN, BK, WM, WN, STAGES>;
   constexpr int NT = Cfg::kThreads;
@@ -131,11 +133,19 @@ __global__ void __launch_bounds__(WM* WN * 32, 1) zgemm_dmma_kernel(const GemmAr
     }
   };
 
-  double cre[MI][NI][2], cim[MI][NI][2];
+  // 4M: cre, cim. 3M (Karatsuba): cre = Ar Br, cim = Ai Bi, c3 = (Ar + Ai)(Br + Bi);
+  // Re = cre - cim, Im = c3 - cre - cim (3 real DMMAs per complex 8x8x4 block instead of 4).
+  double cre[MI][NI][2], cim[MI][NI][2], c3[M3 ? MI : 1][M3 ? NI : 1][2];
 #pragma unroll
   for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
     for (int ni = 0; ni < NI; ++ni) cre[mi][ni][0] = cre[mi][ni][1] = cim[mi][ni][0] = cim[mi][ni][1] = 0.0;
+  if constexpr (M3) {
+#pragma unroll
+    for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < NI; ++ni) c3[mi][ni][0] = c3[mi][ni][1] = 0.0;
+  }
 
   const int nk = (g.K + BK - 1) / BK;
 #pragma unroll
@@ -166,7 +176,7 @@ __global__ void __launch_bounds__(WM* WN * 32, 1) zgemm_dmma_kernel(const GemmAr
         const double2 v = cA[(arow + mi * 8) * Cfg::kLdA + kk + kq];
         ar[mi] = v.x;
         ai[mi] = v.y;
-        an[mi] = -v.y;
+        an[mi] = M3 ? v.x + v.y : -v.y;  // 3M: Ar + Ai; 4M: -Ai
       }
 #pragma unroll
       for (int ni = 0; ni < NI; ++ni) {
@@ -174,15 +184,29 @@ __global__ void __launch_bounds__(WM* WN * 32, 1) zgemm_dmma_kernel(const GemmAr
         br[ni] = v.x;
         bi[ni] = v.y;
       }
+      if constexpr (M3) {
+        double bs[NI];
 #pragma unroll
-      for (int mi = 0; mi < MI; ++mi)
+        for (int ni = 0; ni < NI; ++ni) bs[ni] = br[ni] + bi[ni];
 #pragma unroll
-        for (int ni = 0; ni < NI; ++ni) {
-          dmma(cre[mi][ni][0], cre[mi][ni][1], ar[mi], br[ni]);
-          dmma(cim[mi][ni][0], cim[mi][ni][1], ar[mi], bi[ni]);
-          dmma(cre[mi][ni][0], cre[mi][ni][1], an[mi], bi[ni]);
-          dmma(cim[mi][ni][0], cim[mi][ni][1], ai[mi], br[ni]);
-        }
+        for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < NI; ++ni) {
+            dmma(cre[mi][ni][0], cre[mi][ni][1], ar[mi], br[ni]);
+            dmma(cim[mi][ni][0], cim[mi][ni][1], ai[mi], bi[ni]);
+            dmma(c3[mi][ni][0], c3[mi][ni][1], an[mi], bs[ni]);
+          }
+      } else {
+#pragma unroll
+        for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < NI; ++ni) {
+            dmma(cre[mi][ni][0], cre[mi][ni][1], ar[mi], br[ni]);
+            dmma(cim[mi][ni][0], cim[mi][ni][1], ar[mi], bi[ni]);
+            dmma(cre[mi][ni][0], cre[mi][ni][1], an[mi], bi[ni]);
+            dmma(cim[mi][ni][0], cim[mi][ni][1], ai[mi], br[ni]);
+          }
+      }
     }
   }
   cp_async_wait<0>();
@@ -202,7 +226,11 @@ __global__ void __launch_bounds__(WM* WN * 32, 1) zgemm_dmma_kernel(const GemmAr
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         if (ga + h < g.alim) {
-          double2 v = make_double2(cre[mi][ni][h], cim[mi][ni][h]);
+          double2 v;
+          if constexpr (M3)
+            v = make_double2(cre[mi][ni][h] - cim[mi][ni][h], c3[mi][ni][h] - cre[mi][ni][h] - cim[mi][ni][h]);
+          else
+            v = make_double2(cre[mi][ni][h], cim[mi][ni][h]);
           if (g.accumulate) v = cadd(dst[h], v);
           dst[h] = v;
         }
@@ -211,33 +239,48 @@ __global__ void __launch_bounds__(WM* WN * 32, 1) zgemm_dmma_kernel(const GemmAr
   }
 }
 
-// Tile configuration: 64 x 128 complex per CTA, 8 warps of 32 x 32, BK = 16,
-// 3-stage pipeline (160 KB smem, 1 CTA / SM).
-constexpr int kBM = 64, kBN = 128, kBK = 16, kWM = 2, kWN = 4, kStages = 3;
-using MainCfg = GemmCfg<kBM, kBN, kBK, kWM, kWN, kStages>;
-
-static void launch_gemm(GemmArgs g, cudaStream_t stream) {
+// Tile configurations:
+//   4M: 64 x 128 complex per CTA, 8 warps of 32 x 32, BK = 16, 3 stages (160 KB smem, 1 CTA/SM);
+//   3M: 64 x 64 per CTA, 8 warps of 32 x 16 (three accumulators), BK = 16, 4 stages.
+template <int BM, int BN, int BK, int WM, int WN, int ST, bool M3>
+static void launch_gemm_t(GemmArgs g, cudaStream_t stream) {
+  using Cfg = GemmCfg<BM, BN, BK, WM, WN, ST>;
   static bool attr_set = false;
-  auto kern = zgemm_dmma_kernel<kBM, kBN, kBK, kWM, kWN, kStages>;
+  auto kern = zgemm_dmma_kernel<BM, BN, BK, WM, WN, ST, M3>;
   if (!attr_set) {
-    NDS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)MainCfg::kSmem));
+    NDS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem));
     attr_set = true;
   }
-  g.ntile_rows = (g.rows + kBM - 1) / kBM;
+  g.ntile_rows = (g.rows + BM - 1) / BM;
   const int64_t W = 1ll << g.wshift;
   g.ntile_a = (g.alim + W - 1) / W;
-  const int64_t bb = kBN / W;
+  const int64_t bb = BN / W;
   const int64_t ntile_b = (g.blim + bb - 1) / bb;
   const int64_t tiles = g.ntile_rows * g.ntile_a * ntile_b;
-  kern<<<(unsigned)tiles, MainCfg::kThreads, MainCfg::kSmem, stream>>>(g);
+  kern<<<(unsigned)tiles, Cfg::kThreads, Cfg::kSmem, stream>>>(g);
   NDS_LAUNCH_CHECK();
 }
 
-// Column split for ROWM: power of two W in [8, kBN] minimising padded columns (ties -> wider).
+// NDS_GEMM=4m selects the 4-real-product kernel; default 3M (algorithmic flops are still
+// counted as 8 per complex MAC in every roofline figure).
+static bool use_3m() {
+  static const bool v = !(getenv("NDS_GEMM") && std::string(getenv("NDS_GEMM")) == "4m");
+  return v;
+}
+static int gemm_bn() { return use_3m() ? 64 : 128; }
+
+static void launch_gemm(GemmArgs g, cudaStream_t stream) {
+  if (use_3m())
+    launch_gemm_t<64, 64, 16, 2, 4, 4, true>(g, stream);
+  else
+    launch_gemm_t<64, 128, 16, 2, 4, 3, false>(g, stream);
+}
+
+// Column split for ROWM: power of two W in [8, BN] minimising padded columns (ties -> wider).
 static int pick_wshift(int64_t inner) {
   int best = 3;
   double best_waste = 1e30;
-  for (int s = 3; (1 << s) <= kBN; ++s) {
+  for (int s = 3; (1 << s) <= gemm_bn(); ++s) {
     const int64_t w = 1ll << s;
     const double waste = (double)(((inner + w - 1) / w) * w) / (double)inner;
     if (waste <= best_waste + 1e-12) {
@@ -279,7 +322,7 @@ int mode_product_matrix_launch(const double2* mrow, const double2* mcol, const M
     g.B = mcol;  // B(k, i) = M[i][k] = mcol[i + k m]
     g.ldbk = m;
     g.ldbb = 0;
-    g.wshift = 7;  // one column slice of width kBN
+    g.wshift = gemm_bn() == 128 ? 7 : 6;  // one column slice of width BN
     g.alim = m;
     g.blim = 1;
     g.C = r;

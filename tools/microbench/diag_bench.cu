@@ -69,7 +69,8 @@ int main() {
   cudaMemcpyFromSymbol(probe, nds_diag_probe, sizeof(probe));
   long long prev = c0;
   for (int lv = 0; lv < sp.wf_levels; ++lv) {
-    printf("lv %2d cnt %3d grp %2d cycles %6lld\n", lv, off[lv + 1] - off[lv], grp[lv], clk[lv] - prev);
+    printf("lv %2d cnt %3d grp %2d cycles %6lld  [thr %lld rden %lld dot %lld upd %lld bar %lld]\n", lv, off[lv + 1] - off[lv], grp[lv], clk[lv] - prev,
+           probe[lv*4] - prev, probe[lv*4+1] - probe[lv*4], probe[lv*4+2] - probe[lv*4+1], probe[lv*4+3] - probe[lv*4+2], clk[lv] - probe[lv*4+3]);
     prev = clk[lv];
   }
   return 0;
