@@ -14,6 +14,8 @@
 //      divided by sum_j T_j(i_j, i_j) (same summation order as sylvester.cpp:92-96),
 //   3. write Y_I back.
 #include <algorithm>
+#include <cstdio>
+#include <string>
 #include <numeric>
 
 #include "common.cuh"
@@ -304,8 +306,28 @@ void solve_plan_build(SolvePlan& sp, int n_modes, const int64_t* dims, const int
     lvl[lv] = grp | (((cnt * grp + 31) / 32) << 8);
   }
 
+  // v2 lines kernel: thread -> mode-1 line, ordered by d = sum_{m>=2} l_m, then by l_2, l_3, ...
+  std::vector<uint16_t> line;
+  if (sp.v2) {
+    const int b = g.b[0], nl = g.tile_entries / b;
+    int lb = 0;
+    while ((1 << lb) < b) ++lb;
+    std::vector<std::pair<int, int>> key(nl);
+    for (int c = 0; c < nl; ++c) {
+      int d = 0, k = 0;
+      for (int m = 1; m < n_modes; ++m) {
+        const int lmv = (c >> (lb * (m - 1))) & (b - 1);
+        d += lmv;
+        k = k * b + lmv;
+      }
+      key[c] = {d * 65536 + k, c};
+    }
+    std::sort(key.begin(), key.end());
+    for (auto& kv : key) line.push_back((uint16_t)kv.second);
+  }
+
   size_t bytes = ntiles * sizeof(int64_t) + (g.tile_entries + 3 * wf_levels + 2) * sizeof(int) +
-                 thr.size() * sizeof(uint16_t) + 64;
+                 (thr.size() + line.size() + 8) * sizeof(uint16_t) + 64;
   bytes = (bytes + 15) / 16 * 16;
   const size_t items_off = bytes;
   bytes += (far_items.size() + near_items.size() + ntiles) * sizeof(int4);
@@ -321,6 +343,7 @@ void solve_plan_build(SolvePlan& sp, int n_modes, const int64_t* dims, const int
   sp.d_wf_group = sp.d_wf_off + wf_levels + 1;
   sp.d_lvl = sp.d_wf_group + wf_levels;
   sp.d_thr = (uint16_t*)(((uintptr_t)(sp.d_lvl + wf_levels) + 15) & ~(uintptr_t)15);
+  sp.d_line = sp.d_thr + thr.size();
   sp.d_far_items = (int4*)(base + items_off);
   sp.d_near_items = sp.d_far_items + far_items.size();
   sp.d_tile_ranges = sp.d_near_items + near_items.size();
@@ -334,6 +357,8 @@ void solve_plan_build(SolvePlan& sp, int n_modes, const int64_t* dims, const int
   NDS_CUDA(cudaMemcpy(sp.d_lvl, lvl.data(), wf_levels * sizeof(int), cudaMemcpyHostToDevice));
   if (!thr.empty())
     NDS_CUDA(cudaMemcpy(sp.d_thr, thr.data(), thr.size() * sizeof(uint16_t), cudaMemcpyHostToDevice));
+  if (!line.empty())
+    NDS_CUDA(cudaMemcpy(sp.d_line, line.data(), line.size() * sizeof(uint16_t), cudaMemcpyHostToDevice));
   if (sp.v2) {
     if (!far_items.empty())
       NDS_CUDA(cudaMemcpy(sp.d_far_items, far_items.data(), far_items.size() * sizeof(int4), cudaMemcpyHostToDevice));
@@ -369,6 +394,8 @@ int backsub_launch(const SolvePlan& sp, const double2* t_pool, double2* c, cudaS
       NDS_CUDA(cudaFuncSetAttribute(update_kernel_for(b), cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024));
     NDS_CUDA(cudaFuncSetAttribute(diag_kernel_for(3, 16), cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024));
     NDS_CUDA(cudaFuncSetAttribute(diag_kernel_for(4, 8), cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024));
+    NDS_CUDA(cudaFuncSetAttribute(lines_kernel_for(3, 16), cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024));
+    NDS_CUDA(cudaFuncSetAttribute(lines_kernel_for(4, 8), cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024));
     attr_set = true;
   }
   const TileGeom& g = sp.geom;
@@ -391,10 +418,27 @@ int backsub_launch(const SolvePlan& sp, const double2* t_pool, double2* c, cudaS
   const DiagKernel diag = diag_kernel_for(g.n_modes, b);
   const size_t upd_smem = update_smem_bytes(b);
   const size_t diag_smem = diag_smem_bytes(g.n_modes, b, sp.wf_levels);
+  // NDS_DIAG=wave selects the per-hyperplane entry kernel (A/B experiments); default lines
+  static const bool use_lines = !(getenv("NDS_DIAG") && std::string(getenv("NDS_DIAG")) == "wave");
+  const LinesKernel lines = lines_kernel_for(g.n_modes, b);
+  const size_t lines_smem = lines_smem_bytes(g.n_modes, b);
   static const int dbg_levels = getenv("NDS_DEBUG_WF_LEVELS") ? atoi(getenv("NDS_DEBUG_WF_LEVELS")) : -1;
   const int wfl = dbg_levels >= 0 ? std::min(dbg_levels, sp.wf_levels) : sp.wf_levels;  // timing experiments only
   const int L = sp.levels;
   cudaEvent_t ev_start = sp.ev[2 * L], ev_end = sp.ev[2 * L + 1];
+  // NDS_SOLVE_TRACE=1: per-level start/end events of every launch, printed to stderr (timeline
+  // experiments only; adds event records to the streams).
+  static const bool trace = getenv("NDS_SOLVE_TRACE") != nullptr;
+  std::vector<cudaEvent_t> tev;
+  auto tmark = [&](cudaStream_t s, int lv, int k) {
+    if (!trace) return;
+    NDS_CUDA(cudaEventRecord(tev[(size_t)lv * 6 + k], s));
+  };
+  if (trace) {
+    tev.resize((size_t)L * 6 + 1);
+    for (auto& e : tev) NDS_CUDA(cudaEventCreate(&e));
+    NDS_CUDA(cudaEventRecord(tev.back(), stream));
+  }
   auto ev_diag = [&](int lv) { return sp.ev[lv]; };
   auto ev_far = [&](int lv) { return sp.ev[L + lv]; };
   // fork: both internal streams start after everything already queued on the caller's stream
@@ -409,24 +453,35 @@ int backsub_launch(const SolvePlan& sp, const double2* t_pool, double2* c, cudaS
     if (nf > 0) {
       // far(lv) needs levels <= lv - 2; it overlaps diag(lv - 1) on the critical stream
       if (lv >= 2) NDS_CUDA(cudaStreamWaitEvent(sp.s_far, ev_diag(lv - 2), 0));
+      tmark(sp.s_far, lv, 0);
       upd<<<(unsigned)nf, kUpdThreads, upd_smem, sp.s_far>>>(g, t_pool, sp.d_tiles, sp.d_far_items + sp.far_off[lv],
                                                              far_buf, c);
       NDS_LAUNCH_CHECK();
+      tmark(sp.s_far, lv, 1);
       NDS_CUDA(cudaEventRecord(ev_far(lv), sp.s_far));
       ++launches;
     }
     if (nn > 0) {
+      tmark(sp.s_crit, lv, 2);
       upd<<<(unsigned)nn, kUpdThreads, upd_smem, sp.s_crit>>>(g, t_pool, sp.d_tiles, sp.d_near_items + sp.near_off[lv],
                                                               sp.d_near_partial, c);
       NDS_LAUNCH_CHECK();
+      tmark(sp.s_crit, lv, 3);
       ++launches;
     }
     if (nf > 0) NDS_CUDA(cudaStreamWaitEvent(sp.s_crit, ev_far(lv), 0));
     const int64_t nt = sp.level_off[lv + 1] - sp.level_off[lv];
-    diag<<<(unsigned)nt, diag_threads_for(g.n_modes), diag_smem, sp.s_crit>>>(
-        g, t_pool, sp.d_tiles + sp.level_off[lv], sp.d_tile_ranges + sp.level_off[lv], far_buf, sp.d_near_partial,
-        sp.d_thr, sp.d_lvl, wfl, c);
+    tmark(sp.s_crit, lv, 4);
+    if (use_lines)
+      lines<<<(unsigned)nt, diag_threads_for(g.n_modes), lines_smem, sp.s_crit>>>(
+          g, t_pool, sp.d_tiles + sp.level_off[lv], sp.d_tile_ranges + sp.level_off[lv], far_buf, sp.d_near_partial,
+          sp.d_line, c);
+    else
+      diag<<<(unsigned)nt, diag_threads_for(g.n_modes), diag_smem, sp.s_crit>>>(
+          g, t_pool, sp.d_tiles + sp.level_off[lv], sp.d_tile_ranges + sp.level_off[lv], far_buf, sp.d_near_partial,
+          sp.d_thr, sp.d_lvl, wfl, c);
     NDS_LAUNCH_CHECK();
+    tmark(sp.s_crit, lv, 5);
     NDS_CUDA(cudaEventRecord(ev_diag(lv), sp.s_crit));
     ++launches;
   }
@@ -434,6 +489,22 @@ int backsub_launch(const SolvePlan& sp, const double2* t_pool, double2* c, cudaS
   NDS_CUDA(cudaEventRecord(ev_end, sp.s_crit));
   NDS_CUDA(cudaStreamWaitEvent(stream, ev_end, 0));
   if (rec) rec->mark(stream, kBacksubPersistent, L);
+  if (trace) {
+    NDS_CUDA(cudaStreamSynchronize(stream));
+    for (int lv = 0; lv < L; ++lv) {
+      const int64_t nf = sp.far_off[lv + 1] - sp.far_off[lv];
+      const int64_t nn = sp.near_off[lv + 1] - sp.near_off[lv];
+      float t[6] = {-1, -1, -1, -1, -1, -1};
+      for (int k = 0; k < 6; ++k) {
+        if ((k < 2 && nf == 0) || ((k == 2 || k == 3) && nn == 0)) continue;
+        NDS_CUDA(cudaEventElapsedTime(&t[k], tev.back(), tev[(size_t)lv * 6 + k]));
+      }
+      fprintf(stderr, "TRACE %d %lld %lld %lld %.1f %.1f %.1f %.1f %.1f %.1f\n", lv,
+              (long long)(sp.level_off[lv + 1] - sp.level_off[lv]), (long long)nf, (long long)nn, t[0] * 1e3,
+              t[1] * 1e3, t[2] * 1e3, t[3] * 1e3, t[4] * 1e3, t[5] * 1e3);
+    }
+    for (auto e : tev) cudaEventDestroy(e);
+  }
   return launches;
 }
 

@@ -2,7 +2,7 @@
 // in {8, 16} dividing every n_j (c0, c1: N=3 B=16; c2, c3: N=4 B=8).
 // Included by backsub.cu.
 
-#ifdef NDS_DIAG_CLOCK  // timing probes for tools/microbench/diag_bench.cu only
+#ifdef NDS_DIAG_PROBES  // timing probes for tools/microbench/diag_bench.cu only
 #define NDS_PROBE(k, v) \
   if (tid == 0 && blockIdx.x == 0) nds_diag_probe[lv * 4 + (k)] = clock64() + (long long)((v) * 0)
 #else
@@ -324,6 +324,10 @@ __global__ void __launch_bounds__(NT, 2)
       NDS_PROBE(1, rden.x);
       double2 a0 = make_double2(0.0, 0.0), a1 = make_double2(0.0, 0.0);
       double2 a2 = make_double2(0.0, 0.0), a3 = make_double2(0.0, 0.0);
+      // Flattened term loop: every entry of hyperplane lv has exactly lv terms (cubic tile), so
+      // the trip count is warp-uniform; term t maps to mode m (t >= qc[m]) and position k = t -
+      // qc[m] along it. Offsets are affine in t within a mode: S: sb[m] + t a_m, T: tb[m] + t.
+#if !defined(NDS_DIAG_FLAT) && !defined(NDS_DIAG_NODOT)
       if (act) {
 #pragma unroll
         for (int m = 0; m < N; ++m) {
@@ -353,6 +357,41 @@ __global__ void __launch_bounds__(NT, 2)
           if (q > 0) a2 = cfma(a2, tp[0], sp[0]);
         }
       }
+#elif !defined(NDS_DIAG_NODOT)
+      if (act) {
+        int qc[N], sb[N], tb[N];
+        int q = 0;
+#pragma unroll
+        for (int m = 0; m < N; ++m) {
+          qc[m] = q;
+          sb[m] = pl + (1 - q) * PS::at(m);
+          tb[m] = m * B * B + lm[m] * (B + 1) + 1 - q;
+          q += B - 1 - lm[m];
+        }
+        auto term = [&](int t, double2& a) {
+          int so = sb[0], sa = PS::at(0), to = tb[0];
+#pragma unroll
+          for (int m = 1; m < N; ++m)
+            if (t >= qc[m]) {
+              so = sb[m];
+              sa = PS::at(m);
+              to = tb[m];
+            }
+          a = cfma(a, Td[to + t], S[so + t * sa]);
+        };
+        int t = sub;
+#pragma unroll 1
+        for (; t + 3 * grp < lv; t += 4 * grp) {
+          term(t, a0);
+          term(t + grp, a1);
+          term(t + 2 * grp, a2);
+          term(t + 3 * grp, a3);
+        }
+        if (t < lv) term(t, a0);
+        if (t + grp < lv) term(t + grp, a1);
+        if (t + 2 * grp < lv) term(t + 2 * grp, a2);
+      }
+#endif
       double2 acc = cadd(cadd(a0, a1), cadd(a2, a3));
       NDS_PROBE(2, acc.x);
       for (int o = 1; o < grp; o <<= 1) {
@@ -378,6 +417,181 @@ __global__ void __launch_bounds__(NT, 2)
       Y[gidx] = S[PS::pad(l)];
     }
   }
+}
+
+// Padded shared-memory strides of the line-owner kernel: thread t owns the mode-1 line
+// (l_2, l_3, ...) = digits of t, so a warp's lanes differ in l_2 (fastest) and a hyperplane puts
+// them at l_1 = s - l_2 - ...; a_2 - 1 odd spreads those lanes over all eight 16-byte bank groups.
+template <int N, int B>
+struct LinePad {
+  static constexpr int a1 = B + 2;
+  static constexpr int a2 = a1 * B + 1;
+  static constexpr int a3 = N >= 4 ? a2 * B + 1 : 0;
+  __host__ __device__ static constexpr int at(int m) { return m == 0 ? 1 : m == 1 ? a1 : m == 2 ? a2 : a3; }
+  static constexpr int extent = 1 + (B - 1) * (1 + a1 + a2 + a3);
+  __device__ static int pad(int l) {
+    int a = 0;
+#pragma unroll
+    for (int m = 0; m < N; ++m) a += ((l >> ((B == 16 ? 4 : 3) * m)) & (B - 1)) * at(m);
+    return a;
+  }
+};
+
+// Diagonal tile, line-owner formulation. Thread t owns the mode-1 line with fixed local
+// coordinates (l_2, .., l_N) = base-B digits of t and walks it from row B-1 down to 0, one row
+// per local hyperplane: row r is solved at step lv = (N-1)(B-1) - d + (B-1-r), d = sum_{m>=2} l_m.
+// Eq. (9)'s sum splits as
+//   mode 1:   sum_{k>r} T_1(r, k) y(k, l_2, ..)  — the thread's own history, kept as pending sums
+//             q[j] = sum_{k solved} T_1(r-1-j, k) y_k in registers that shift by one row per step
+//             (static register indices); T_1's superdiagonals are stored diagonal-major so the
+//             lanes' different rows r read consecutive words;
+//   mode 2:   T_2(l_2, l_2 + 1 + k) is fixed per thread — held in registers;
+//   modes 3+: T_m(l_m, ..) is shared by the lanes of a (half-)warp — a shared-memory broadcast;
+// so per term only the neighbour y is read from shared memory, at a compile-time offset from the
+// entry. Same partial-subtraction prologue and epilogue as tile_diag_kernel.
+template <int N, int B, int NT>
+__global__ void __launch_bounds__(NT, 1)
+    tile_diag_lines_kernel(const TileGeom g, const double2* __restrict__ T, const int64_t* __restrict__ tiles,
+                           const int4* __restrict__ tile_ranges, const double2* __restrict__ far_partial,
+                           const double2* __restrict__ near_partial, const uint16_t* __restrict__ /*unused*/,
+                           double2* __restrict__ Y) {
+  constexpr int E = 4096;
+  constexpr int LB = B == 16 ? 4 : 3;
+  constexpr int WL = N * (B - 1) + 1;
+  static_assert((1 << (LB * N)) == E && E / B == NT, "one thread per mode-1 line of a cubic 4096-entry tile");
+  using PS = LinePad<N, B>;
+  extern __shared__ __align__(16) double2 sm[];
+  __shared__ int64_t so[N];
+  __shared__ int64_t st[N];
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    int64_t t = tiles[blockIdx.x];
+    for (int m = 0; m < N; ++m) {
+      const int64_t I = t % g.nb[m];
+      t /= g.nb[m];
+      so[m] = I * B;
+      st[m] = g.strides[m];
+    }
+  }
+  double2* S = sm;
+  double2* Td = S + PS::extent + (PS::extent & 1);  // [N][B][B] row-major: T_m(o_m + row, o_m + col)
+  double2* Dq = Td + N * B * B;                     // [B][B]: Dq[j][r] = T_1(r - 1 - j, r)
+  __syncthreads();
+#pragma unroll
+  for (int m = 0; m < N; ++m) {
+    const double2* Tm = T + g.toff[m];
+    const int64_t nm = g.dims[m];
+    for (int e = tid; e < B * B; e += NT) {
+      const int r = e / B, c = e % B;
+      Td[(m * B + r) * B + c] = Tm[(so[m] + r) + (so[m] + c) * nm];
+      if (m == 0) {  // e = j B + r'
+        const int j = e / B, rr = e % B;
+        Dq[e] = rr >= j + 1 ? Tm[(so[0] + rr - 1 - j) + (so[0] + rr) * nm] : make_double2(0.0, 0.0);
+      }
+    }
+  }
+  const int4 tr = tile_ranges[blockIdx.x];  // {far first, far count, near first, near count}
+  {
+    constexpr int PER = E / NT;
+    double2 v[PER];
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const int l = tid + i * NT;
+      int64_t gidx = 0;
+#pragma unroll
+      for (int m = 0; m < N; ++m) gidx += (so[m] + ((l >> (LB * m)) & (B - 1))) * st[m];
+      v[i] = Y[gidx];
+    }
+    for (int p = 0; p < tr.y; ++p) {
+      const double2* pp = far_partial + (int64_t)(tr.x + p) * E + tid;
+#pragma unroll
+      for (int i = 0; i < PER; ++i) v[i] = csub(v[i], pp[i * NT]);
+    }
+    for (int p = 0; p < tr.w; ++p) {
+      const double2* pp = near_partial + (int64_t)(tr.z + p) * E + tid;
+#pragma unroll
+      for (int i = 0; i < PER; ++i) v[i] = csub(v[i], pp[i * NT]);
+    }
+#pragma unroll
+    for (int i = 0; i < PER; ++i) S[PS::pad(tid + i * NT)] = v[i];
+  }
+  __syncthreads();
+
+  int lm[N];
+  int d = 0, pb = 0;
+  lm[0] = 0;
+#pragma unroll
+  for (int m = 1; m < N; ++m) {
+    lm[m] = (tid >> (LB * (m - 1))) & (B - 1);
+    d += lm[m];
+    pb += lm[m] * PS::at(m);
+  }
+  double2 t2r[B - 1];  // T_2(l_2, l_2 + 1 + k)
+#pragma unroll
+  for (int k = 0; k < B - 1; ++k)
+    t2r[k] = k < B - 1 - lm[1] ? Td[(B + lm[1]) * B + lm[1] + 1 + k] : make_double2(0.0, 0.0);
+  double2 dsum = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int m = 1; m < N; ++m) dsum = cadd(dsum, Td[(m * B + lm[m]) * B + lm[m]]);
+  const int lv0 = (N - 1) * (B - 1) - d;  // step of row B-1
+  double2 q[B - 1];
+#pragma unroll
+  for (int j = 0; j < B - 1; ++j) q[j] = make_double2(0.0, 0.0);
+
+#pragma unroll 1
+  for (int lv = 0; lv < WL; ++lv) {
+    const int r = B - 1 - (lv - lv0);
+    if (lv >= lv0 && r >= 0) {
+      const double2* e = S + r + pb;  // this step's entry
+      const double2 rden = crecip_fast(cadd(Td[r * (B + 1)], dsum));
+      double2 a[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = make_double2(0.0, 0.0);
+      const int q2 = B - 1 - lm[1];
+#pragma unroll
+      for (int k = 0; k < B - 1; ++k)
+        if (k < q2) a[k & 3] = cfma(a[k & 3], t2r[k], e[(1 + k) * PS::a1]);
+#pragma unroll
+      for (int m = 2; m < N; ++m) {
+        const double2* tm = Td + (m * B + lm[m]) * B + lm[m] + 1;
+        const int qm = B - 1 - lm[m];
+#pragma unroll
+        for (int k = 0; k < B - 1; ++k)
+          if (k < qm) a[(k + 2) & 3] = cfma(a[(k + 2) & 3], tm[k], e[(1 + k) * PS::at(m)]);
+      }
+      const double2 acc = cadd(cadd(a[0], a[1]), cadd(a[2], cadd(a[3], q[0])));
+      const double2 y = cmul(csub(e[0], acc), rden);
+      S[r + pb] = y;
+      // mode-1 history: q[j] <- q[j+1] + T_1(r-1-j, r) y for the rows r-1-j >= 0 still ahead
+#pragma unroll
+      for (int j = 0; j < B - 1; ++j)
+        if (j < r) q[j] = cfma(j + 1 < B - 1 ? q[j + 1] : make_double2(0.0, 0.0), Dq[j * B + r], y);
+    }
+    __syncthreads();
+  }
+  {
+    constexpr int PER = E / NT;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const int l = tid + i * NT;
+      int64_t gidx = 0;
+#pragma unroll
+      for (int m = 0; m < N; ++m) gidx += (so[m] + ((l >> (LB * m)) & (B - 1))) * st[m];
+      Y[gidx] = S[PS::pad(l)];
+    }
+  }
+}
+
+using LinesKernel = void (*)(const TileGeom, const double2*, const int64_t*, const int4*, const double2*,
+                             const double2*, const uint16_t*, double2*);
+static LinesKernel lines_kernel_for(int n_modes, int b) {
+  if (n_modes == 3 && b == 16) return tile_diag_lines_kernel<3, 16, 256>;
+  if (n_modes == 4 && b == 8) return tile_diag_lines_kernel<4, 8, 512>;
+  return nullptr;
+}
+static size_t lines_smem_bytes(int n_modes, int b) {
+  const int ext = n_modes == 3 ? LinePad<3, 16>::extent : LinePad<4, 8>::extent;
+  return (size_t)(ext + (ext & 1)) * 16 + (size_t)(n_modes + 1) * b * b * 16;
 }
 
 using UpdateKernel = void (*)(const TileGeom, const double2*, const int64_t*, const int4*, double2*, const double2*);

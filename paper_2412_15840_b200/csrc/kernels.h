@@ -89,6 +89,7 @@ struct SolvePlan {
   int* d_wf_group = nullptr;      // lanes per entry for each local hyperplane (v2)
   uint16_t* d_thr = nullptr;      // v2: [wf_levels][diag threads] local entry per thread (0xffff none)
   int* d_lvl = nullptr;           // v2: per local hyperplane: grp | (busy warps << 8)
+  uint16_t* d_line = nullptr;     // v2 lines kernel: per thread its mode-1 line (l_2..l_N packed), sorted by sum
   void* pool = nullptr;
   // v2 (GEMM regime: every b_j a power of two >= 8 dividing n_j): per level, DMMA update work
   // items (tile, mode, k-range) writing partials, then one diagonal-tile kernel.

@@ -261,19 +261,37 @@ static void launch_gemm_t(GemmArgs g, cudaStream_t stream) {
   NDS_LAUNCH_CHECK();
 }
 
-// NDS_GEMM=4m selects the 4-real-product kernel; default 3M (algorithmic flops are still
-// counted as 8 per complex MAC in every roofline figure).
-static bool use_3m() {
-  static const bool v = !(getenv("NDS_GEMM") && std::string(getenv("NDS_GEMM")) == "4m");
+// NDS_GEMM selects the kernel variant (A/B experiments); default 3M 64x64 BK16 4-stage.
+// Algorithmic flops are counted as 8 per complex MAC in every roofline figure regardless.
+static int gemm_variant() {
+  static const int v = [] {
+    const char* e = getenv("NDS_GEMM");
+    if (!e) return 0;
+    const std::string s(e);
+    if (s == "4m") return 1;
+    if (s == "3m_bk32") return 2;
+    if (s == "3m_128x32") return 3;
+    if (s == "3m_s3") return 4;
+    return 0;
+  }();
   return v;
 }
-static int gemm_bn() { return use_3m() ? 64 : 128; }
+static int gemm_bn() {
+  switch (gemm_variant()) {
+    case 1: return 128;
+    case 3: return 32;
+    default: return 64;
+  }
+}
 
 static void launch_gemm(GemmArgs g, cudaStream_t stream) {
-  if (use_3m())
-    launch_gemm_t<64, 64, 16, 2, 4, 4, true>(g, stream);
-  else
-    launch_gemm_t<64, 128, 16, 2, 4, 3, false>(g, stream);
+  switch (gemm_variant()) {
+    case 1: launch_gemm_t<64, 128, 16, 2, 4, 3, false>(g, stream); break;
+    case 2: launch_gemm_t<64, 64, 32, 2, 4, 3, true>(g, stream); break;
+    case 3: launch_gemm_t<128, 32, 16, 4, 2, 4, true>(g, stream); break;
+    case 4: launch_gemm_t<64, 64, 16, 2, 4, 3, true>(g, stream); break;
+    default: launch_gemm_t<64, 64, 16, 2, 4, 4, true>(g, stream); break;
+  }
 }
 
 // Column split for ROWM: power of two W in [8, BN] minimising padded columns (ties -> wider).
@@ -322,7 +340,7 @@ int mode_product_matrix_launch(const double2* mrow, const double2* mcol, const M
     g.B = mcol;  // B(k, i) = M[i][k] = mcol[i + k m]
     g.ldbk = m;
     g.ldbb = 0;
-    g.wshift = gemm_bn() == 128 ? 7 : 6;  // one column slice of width BN
+    g.wshift = __builtin_ctz(gemm_bn());  // one column slice of width BN
     g.alim = m;
     g.blim = 1;
     g.C = r;

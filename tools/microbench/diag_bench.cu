@@ -56,6 +56,24 @@ int main() {
       printf("grid %3d levels %2d : %8.2f us/launch  err=%s\n", grid, L, ms * 1000 / reps, cudaGetErrorString(cudaGetLastError()));
     }
   }
+  {
+    auto kl = lines_kernel_for(3, 16);
+    const size_t lsmem = lines_smem_bytes(3, 16);
+    cudaFuncSetAttribute(kl, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
+    for (int grid : {1, 148, 296}) {
+      for (int w = 0; w < 3; ++w)
+        kl<<<grid, kDiagThreads, lsmem>>>(sp.geom, dT, dtiles, (const int4*)ditems, nullptr, nullptr, sp.d_line, dY);
+      cudaEventRecord(e0);
+      const int reps = 20;
+      for (int r = 0; r < reps; ++r)
+        kl<<<grid, kDiagThreads, lsmem>>>(sp.geom, dT, dtiles, (const int4*)ditems, nullptr, nullptr, sp.d_line, dY);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      printf("lines grid %3d : %8.2f us/launch  err=%s\n", grid, ms * 1000 / reps, cudaGetErrorString(cudaGetLastError()));
+    }
+  }
   // per-level cycles of CTA 0 for a full single-tile run
   k<<<1, kDiagThreads, smem>>>(sp.geom, dT, dtiles, (const int4*)ditems, nullptr, nullptr, sp.d_thr, sp.d_lvl, sp.wf_levels, dY);
   cudaDeviceSynchronize();
