@@ -88,8 +88,8 @@ struct GemmCfg {
   static constexpr int NI = BN / WN / 8;
 };
 
-template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool M3>
-__global__ void __launch_bounds__(WM* WN * 32, 1) zgemm_dmma_kernel(const GemmArgs g) {
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool M3, int MINB = 1>
+__global__ void __launch_bounds__(WM* WN * 32, MINB) zgemm_dmma_kernel(const GemmArgs g) {
   using Cfg = GemmCfg<BM, BN, BK, WM, WN, STAGES>;
   constexpr int NT = Cfg::kThreads;
   constexpr int MI = Cfg::MI, NI = Cfg::NI;
@@ -239,14 +239,16 @@ __global__ void __launch_bounds__(WM* WN * 32, 1) zgemm_dmma_kernel(const GemmAr
   }
 }
 
-// Tile configurations:
-//   4M: 64 x 128 complex per CTA, 8 warps of 32 x 32, BK = 16, 3 stages (160 KB smem, 1 CTA/SM);
-//   3M: 64 x 64 per CTA, 8 warps of 32 x 16 (three accumulators), BK = 16, 4 stages.
-template <int BM, int BN, int BK, int WM, int WN, int ST, bool M3>
+// Tile configurations. 3M kernels, 2 CTAs / SM, 8 warps, BK = 16, 3 stages:
+//   kWide: 64 x 32 per CTA (warps of 32 x 8);  kTall: 32 x 64 per CTA (warps of 32 x 8).
+// The shape with the least padded output is chosen per GEMM (ties: kWide). NDS_GEMM=4m|3m64
+// force the 4-multiply 64 x 128 kernel / the 1-CTA 64 x 64 3M kernel (A/B experiments).
+// Algorithmic flops are counted as 8 per complex MAC in every roofline figure regardless.
+template <int BM, int BN, int BK, int WM, int WN, int ST, bool M3, int MINB = 1>
 static void launch_gemm_t(GemmArgs g, cudaStream_t stream) {
   using Cfg = GemmCfg<BM, BN, BK, WM, WN, ST>;
   static bool attr_set = false;
-  auto kern = zgemm_dmma_kernel<BM, BN, BK, WM, WN, ST, M3>;
+  auto kern = zgemm_dmma_kernel<BM, BN, BK, WM, WN, ST, M3, MINB>;
   if (!attr_set) {
     NDS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem));
     attr_set = true;
@@ -261,44 +263,46 @@ static void launch_gemm_t(GemmArgs g, cudaStream_t stream) {
   NDS_LAUNCH_CHECK();
 }
 
-// NDS_GEMM selects the kernel variant (A/B experiments); default 3M 64x64 BK16 4-stage.
-// Algorithmic flops are counted as 8 per complex MAC in every roofline figure regardless.
-static int gemm_variant() {
+enum GemmShape { kWide = 0, kTall = 1, kForce4M = 2, kForce3M64 = 3 };
+struct ShapeDims {
+  int bm, bn;
+};
+static ShapeDims shape_dims(GemmShape s) {
+  switch (s) {
+    case kTall: return {32, 64};
+    case kForce4M: return {64, 128};
+    case kForce3M64: return {64, 64};
+    default: return {64, 32};
+  }
+}
+static int forced_shape() {
   static const int v = [] {
     const char* e = getenv("NDS_GEMM");
-    if (!e) return 0;
+    if (!e) return -1;
     const std::string s(e);
-    if (s == "4m") return 1;
-    if (s == "3m_bk32") return 2;
-    if (s == "3m_128x32") return 3;
-    if (s == "3m_s3") return 4;
-    return 0;
+    if (s == "4m") return (int)kForce4M;
+    if (s == "3m64") return (int)kForce3M64;
+    if (s == "wide") return (int)kWide;
+    if (s == "tall") return (int)kTall;
+    return -1;
   }();
   return v;
 }
-static int gemm_bn() {
-  switch (gemm_variant()) {
-    case 1: return 128;
-    case 3: return 32;
-    default: return 64;
+
+static void launch_gemm(GemmShape shape, GemmArgs g, cudaStream_t stream) {
+  switch (shape) {
+    case kTall: launch_gemm_t<32, 64, 16, 1, 8, 3, true, 2>(g, stream); break;
+    case kForce4M: launch_gemm_t<64, 128, 16, 2, 4, 3, false>(g, stream); break;
+    case kForce3M64: launch_gemm_t<64, 64, 16, 2, 4, 4, true>(g, stream); break;
+    default: launch_gemm_t<64, 32, 16, 2, 4, 3, true, 2>(g, stream); break;
   }
 }
 
-static void launch_gemm(GemmArgs g, cudaStream_t stream) {
-  switch (gemm_variant()) {
-    case 1: launch_gemm_t<64, 128, 16, 2, 4, 3, false>(g, stream); break;
-    case 2: launch_gemm_t<64, 64, 32, 2, 4, 3, true>(g, stream); break;
-    case 3: launch_gemm_t<128, 32, 16, 4, 2, 4, true>(g, stream); break;
-    case 4: launch_gemm_t<64, 64, 16, 2, 4, 3, true>(g, stream); break;
-    default: launch_gemm_t<64, 64, 16, 2, 4, 4, true>(g, stream); break;
-  }
-}
-
-// Column split for ROWM: power of two W in [8, BN] minimising padded columns (ties -> wider).
-static int pick_wshift(int64_t inner) {
+// Column split for ROWM: power of two W in [8, bn] minimising padded columns (ties -> wider).
+static int pick_wshift(int64_t inner, int bn) {
   int best = 3;
   double best_waste = 1e30;
-  for (int s = 3; (1 << s) <= gemm_bn(); ++s) {
+  for (int s = 3; (1 << s) <= bn; ++s) {
     const int64_t w = 1ll << s;
     const double waste = (double)(((inner + w - 1) / w) * w) / (double)inner;
     if (waste <= best_waste + 1e-12) {
@@ -307,6 +311,31 @@ static int pick_wshift(int64_t inner) {
     }
   }
   return best;
+}
+
+// Fill the shape-dependent fields (wshift) and return the padded output volume of the grid.
+static double shape_cost(GemmArgs& g, bool colm, int64_t inner, GemmShape s) {
+  const ShapeDims sd = shape_dims(s);
+  g.wshift = colm ? __builtin_ctz(sd.bn) : pick_wshift(inner, sd.bn);
+  const int64_t W = 1ll << g.wshift, bb = sd.bn / W;
+  const double rows = (double)((g.rows + sd.bm - 1) / sd.bm) * sd.bm;
+  const double cols = (double)((g.alim + W - 1) / W) * W * (double)((g.blim + bb - 1) / bb) * bb;
+  return rows * cols;
+}
+
+static void launch_gemm_auto(GemmArgs g, bool colm, int64_t inner, cudaStream_t stream) {
+  GemmShape best;
+  const int f = forced_shape();
+  if (f >= 0) {
+    best = (GemmShape)f;
+  } else {
+    GemmArgs gt = g;
+    const double cw = shape_cost(gt, colm, inner, kWide);
+    const double ct = shape_cost(gt, colm, inner, kTall);
+    best = ct < cw * (1.0 - 1e-9) ? kTall : kWide;
+  }
+  shape_cost(g, colm, inner, best);
+  launch_gemm(best, g, stream);
 }
 
 int mode_product_launch(const FactorSet& f, int mode, bool adjoint, const ModeView& v, const double2* x, double2* r,
@@ -340,7 +369,6 @@ int mode_product_matrix_launch(const double2* mrow, const double2* mcol, const M
     g.B = mcol;  // B(k, i) = M[i][k] = mcol[i + k m]
     g.ldbk = m;
     g.ldbb = 0;
-    g.wshift = __builtin_ctz(gemm_bn());  // one column slice of width BN
     g.alim = m;
     g.blim = 1;
     g.C = r;
@@ -353,14 +381,13 @@ int mode_product_matrix_launch(const double2* mrow, const double2* mcol, const M
     g.B = x;
     g.ldbk = v.inner;
     g.ldbb = v.inner * n;
-    g.wshift = pick_wshift(v.inner);
     g.alim = v.inner;
     g.blim = v.outer;
     g.C = r;
     g.ldcr = v.inner;
     g.ldcb = v.inner * m;
   }
-  launch_gemm(g, stream);
+  launch_gemm_auto(g, v.inner == 1, v.inner, stream);
   return kXformGemm;
 }
 
