@@ -449,8 +449,8 @@ struct LinePad {
 //   modes 3+: T_m(l_m, ..) is shared by the lanes of a (half-)warp — a shared-memory broadcast;
 // so per term only the neighbour y is read from shared memory, at a compile-time offset from the
 // entry. Same partial-subtraction prologue and epilogue as tile_diag_kernel.
-template <int N, int B, int NT>
-__global__ void __launch_bounds__(NT, 1)
+template <int N, int B, int NT, bool T2REG>
+__global__ void __launch_bounds__(NT, T2REG ? 1 : 2)
     tile_diag_lines_kernel(const TileGeom g, const double2* __restrict__ T, const int64_t* __restrict__ tiles,
                            const int4* __restrict__ tile_ranges, const double2* __restrict__ far_partial,
                            const double2* __restrict__ near_partial, const uint16_t* __restrict__ /*unused*/,
@@ -526,10 +526,12 @@ __global__ void __launch_bounds__(NT, 1)
     d += lm[m];
     pb += lm[m] * PS::at(m);
   }
-  double2 t2r[B - 1];  // T_2(l_2, l_2 + 1 + k)
+  double2 t2r[T2REG ? B - 1 : 1];  // T_2(l_2, l_2 + 1 + k) (registers, or read from Td per term)
+  const double2* t2s = Td + (B + lm[1]) * B + lm[1] + 1;
+  if constexpr (T2REG) {
 #pragma unroll
-  for (int k = 0; k < B - 1; ++k)
-    t2r[k] = k < B - 1 - lm[1] ? Td[(B + lm[1]) * B + lm[1] + 1 + k] : make_double2(0.0, 0.0);
+    for (int k = 0; k < B - 1; ++k) t2r[k] = k < B - 1 - lm[1] ? t2s[k] : make_double2(0.0, 0.0);
+  }
   double2 dsum = make_double2(0.0, 0.0);
 #pragma unroll
   for (int m = 1; m < N; ++m) dsum = cadd(dsum, Td[(m * B + lm[m]) * B + lm[m]]);
@@ -550,7 +552,7 @@ __global__ void __launch_bounds__(NT, 1)
       const int q2 = B - 1 - lm[1];
 #pragma unroll
       for (int k = 0; k < B - 1; ++k)
-        if (k < q2) a[k & 3] = cfma(a[k & 3], t2r[k], e[(1 + k) * PS::a1]);
+        if (k < q2) a[k & 3] = cfma(a[k & 3], T2REG ? t2r[T2REG ? k : 0] : t2s[k], e[(1 + k) * PS::a1]);
 #pragma unroll
       for (int m = 2; m < N; ++m) {
         const double2* tm = Td + (m * B + lm[m]) * B + lm[m] + 1;
@@ -585,8 +587,9 @@ __global__ void __launch_bounds__(NT, 1)
 using LinesKernel = void (*)(const TileGeom, const double2*, const int64_t*, const int4*, const double2*,
                              const double2*, const uint16_t*, double2*);
 static LinesKernel lines_kernel_for(int n_modes, int b) {
-  if (n_modes == 3 && b == 16) return tile_diag_lines_kernel<3, 16, 256>;
-  if (n_modes == 4 && b == 8) return tile_diag_lines_kernel<4, 8, 512>;
+  static const bool t2reg = getenv("NDS_DIAG_T2SMEM") == nullptr;  // A/B: T_2 rows from smem, 2 CTAs/SM
+  if (n_modes == 3 && b == 16) return t2reg ? tile_diag_lines_kernel<3, 16, 256, true> : tile_diag_lines_kernel<3, 16, 256, false>;
+  if (n_modes == 4 && b == 8) return tile_diag_lines_kernel<4, 8, 512, true>;
   return nullptr;
 }
 static size_t lines_smem_bytes(int n_modes, int b) {
