@@ -86,25 +86,30 @@ __global__ void __launch_bounds__(kUpdThreads, 2)
   const double2* Tj = T + g.toff[j] + so[j];
   const int64_t nj = g.dims[j];
 
-  // fixed per-thread load slots
-  int64_t gofs[8];
+  // fixed per-thread load slots. Mode 1 (j == 0) is contiguous along k in global memory, so
+  // its lanes run along k and the stage is stored k-fastest ([c][8] with the k index XOR-swizzled
+  // by bit 0 of c: conflict-free for both the cp.async writes and the fragment reads); other
+  // modes run along c into the [k][LDB] layout.
+  const bool kfast = j == 0;
+  int gofs[8];
   int sofs[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     const int e = tid + i * kUpdThreads;
     int k, c;
-    if (j == 0) {  // mode 1 is contiguous along k: k fastest
+    if (kfast) {
       k = e % BK;
       c = e / BK;
+      sofs[i] = c * BK + (k ^ (BK >= 8 ? (c & 1) << 2 : 0));
     } else {
       c = e % COLS;
       k = e / COLS;
+      sofs[i] = k * LDB + c;
     }
-    gofs[i] = (int64_t)k * sj + colg[c];
-    sofs[i] = k * LDB + c;
+    gofs[i] = (int)((int64_t)k * sj + colg[c]);
   }
   const bool a_loader = tid < BJ * BK;
-  const int a_r = tid / BK, a_k = tid % BK;
+  const int a_r = tid % BJ, a_k = tid / BJ;  // rows fastest: coalesced along T_j's columns
 
   auto load_stage = [&](int stage, int k0) {
     double2* dB = sB + stage * BK * LDB;
@@ -147,7 +152,8 @@ __global__ void __launch_bounds__(kUpdThreads, 2)
       }
 #pragma unroll
       for (int q = 0; q < CB; ++q) {
-        const double2 b = cB[(kk + kq) * LDB + cbase + q * 8];
+        const int c = cbase + q * 8;
+        const double2 b = kfast ? cB[c * BK + ((kk + kq) ^ (BK >= 8 ? (c & 1) << 2 : 0))] : cB[(kk + kq) * LDB + c];
         br[q] = b.x;
         bi[q] = b.y;
       }
