@@ -35,8 +35,8 @@ __device__ __forceinline__ void dmma_bs(double& c0, double& c1, double a, double
 // Every thread owns 8 fixed (k, c) slots of each stage; their global / shared offsets are
 // computed once. Each warp owns RB x CB fragments (8x8) and reuses its A/B fragments across
 // them. The partial is written in tile-local column-major order for the diagonal kernel.
-template <int RB, int CB>
-__global__ void __launch_bounds__(kUpdThreads, 2)
+template <int RB, int CB, bool M3>
+__global__ void __launch_bounds__(kUpdThreads, M3 ? 1 : 2)
     tile_update_kernel(const TileGeom g, const double2* __restrict__ T, const int64_t* __restrict__ tiles,
                        const int4* __restrict__ items, double2* __restrict__ partial, const double2* __restrict__ Y) {
   constexpr int BJ = 8 * RB;
@@ -120,11 +120,15 @@ __global__ void __launch_bounds__(kUpdThreads, 2)
   };
 
   const int lane = tid & 31, warp = tid >> 5;
-  double cre[RB][CB][2], cim[RB][CB][2];
+  // 4M: cre, cim; 3M: cre = Ar Br, cim = Ai Bi, c3 = (Ar + Ai)(Br + Bi) (see zgemm_dmma_kernel)
+  double cre[RB][CB][2], cim[RB][CB][2], c3[M3 ? RB : 1][M3 ? CB : 1][2];
 #pragma unroll
   for (int r = 0; r < RB; ++r)
 #pragma unroll
-    for (int q = 0; q < CB; ++q) cre[r][q][0] = cre[r][q][1] = cim[r][q][0] = cim[r][q][1] = 0.0;
+    for (int q = 0; q < CB; ++q) {
+      cre[r][q][0] = cre[r][q][1] = cim[r][q][0] = cim[r][q][1] = 0.0;
+      if constexpr (M3) c3[r][q][0] = c3[r][q][1] = 0.0;
+    }
 
   const int nk = (ke - kb) / BK;  // host guarantees BK | (ke - kb)
   load_stage(0, kb);
@@ -148,7 +152,7 @@ __global__ void __launch_bounds__(kUpdThreads, 2)
         const double2 a = cA[(r * 8 + arow) * kALd + kk + kq];
         ar[r] = a.x;
         ai[r] = a.y;
-        an[r] = -a.y;
+        an[r] = M3 ? a.x + a.y : -a.y;
       }
 #pragma unroll
       for (int q = 0; q < CB; ++q) {
@@ -157,15 +161,29 @@ __global__ void __launch_bounds__(kUpdThreads, 2)
         br[q] = b.x;
         bi[q] = b.y;
       }
+      if constexpr (M3) {
+        double bs[CB];
 #pragma unroll
-      for (int r = 0; r < RB; ++r)
+        for (int q = 0; q < CB; ++q) bs[q] = br[q] + bi[q];
 #pragma unroll
-        for (int q = 0; q < CB; ++q) {
-          dmma_bs(cre[r][q][0], cre[r][q][1], ar[r], br[q]);
-          dmma_bs(cim[r][q][0], cim[r][q][1], ar[r], bi[q]);
-          dmma_bs(cre[r][q][0], cre[r][q][1], an[r], bi[q]);
-          dmma_bs(cim[r][q][0], cim[r][q][1], ai[r], br[q]);
-        }
+        for (int r = 0; r < RB; ++r)
+#pragma unroll
+          for (int q = 0; q < CB; ++q) {
+            dmma_bs(cre[r][q][0], cre[r][q][1], ar[r], br[q]);
+            dmma_bs(cim[r][q][0], cim[r][q][1], ai[r], bi[q]);
+            dmma_bs(c3[r][q][0], c3[r][q][1], an[r], bs[q]);
+          }
+      } else {
+#pragma unroll
+        for (int r = 0; r < RB; ++r)
+#pragma unroll
+          for (int q = 0; q < CB; ++q) {
+            dmma_bs(cre[r][q][0], cre[r][q][1], ar[r], br[q]);
+            dmma_bs(cim[r][q][0], cim[r][q][1], ar[r], bi[q]);
+            dmma_bs(cre[r][q][0], cre[r][q][1], an[r], bi[q]);
+            dmma_bs(cim[r][q][0], cim[r][q][1], ai[r], br[q]);
+          }
+      }
     }
   }
   cp_wait0_bs();
@@ -177,8 +195,15 @@ __global__ void __launch_bounds__(kUpdThreads, 2)
     for (int q = 0; q < CB; ++q) {
       const int row = r * 8 + (lane >> 2);
       const int c = warp * CB * 8 + q * 8 + 2 * kq;
-      out[row * bsj + coll[c]] = make_double2(cre[r][q][0], cim[r][q][0]);
-      out[row * bsj + coll[c + 1]] = make_double2(cre[r][q][1], cim[r][q][1]);
+      if constexpr (M3) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          out[row * bsj + coll[c + h]] =
+              make_double2(cre[r][q][h] - cim[r][q][h], c3[r][q][h] - cre[r][q][h] - cim[r][q][h]);
+      } else {
+        out[row * bsj + coll[c]] = make_double2(cre[r][q][0], cim[r][q][0]);
+        out[row * bsj + coll[c + 1]] = make_double2(cre[r][q][1], cim[r][q][1]);
+      }
     }
 }
 
@@ -607,10 +632,20 @@ using UpdateKernel = void (*)(const TileGeom, const double2*, const int64_t*, co
 using DiagKernel = void (*)(const TileGeom, const double2*, const int64_t*, const int4*, const double2*,
                             const double2*, const uint16_t*, const int*, int, double2*);
 
+// 3M (1 CTA / SM) for b = 16, 4M (2 CTAs / SM) for b = 8 — measured; NDS_UPD=3m|4m overrides.
+static int update_override() {
+  static const int v = [] {
+    const char* e = getenv("NDS_UPD");
+    if (!e) return -1;
+    return std::string(e) == "3m" ? 1 : 0;
+  }();
+  return v;
+}
 static UpdateKernel update_kernel_for(int b) {
+  const int o = update_override();
   switch (b) {
-    case 8: return tile_update_kernel<1, 8>;
-    case 16: return tile_update_kernel<2, 4>;
+    case 8: return o == 1 ? tile_update_kernel<1, 8, true> : tile_update_kernel<1, 8, false>;
+    case 16: return o == 0 ? tile_update_kernel<2, 4, false> : tile_update_kernel<2, 4, true>;
     default: return nullptr;
   }
 }
