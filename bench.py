@@ -315,7 +315,12 @@ def main():
                "d2h_bytes_per_step": 16 * P, "ms_per_step": e2e_s * 1e3, "steps": args.e2e_steps,
                "api": "nds_solve_schur (host buffers, pinned)",
                "h2d_ms": rep.h2d_seconds * 1e3, "d2h_ms": rep.d2h_seconds * 1e3,
-               "device_ms": (rep.transform_seconds + rep.backsub_seconds + rep.inverse_seconds) * 1e3}
+               "device_ms": (rep.transform_seconds + rep.backsub_seconds + rep.inverse_seconds) * 1e3,
+               "stages_ms": {"h2d_stream": rep.h2d_seconds * 1e3,
+                             "forward_incl_h2d": rep.transform_seconds * 1e3,
+                             "solve": rep.backsub_seconds * 1e3,
+                             "inverse": rep.inverse_seconds * 1e3,
+                             "d2h_tail": rep.d2h_seconds * 1e3}}
 
     verify = None
     if args.verify:

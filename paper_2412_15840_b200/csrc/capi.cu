@@ -21,8 +21,8 @@ struct nds_ctx {
   cudaStream_t own = nullptr;
   cudaStream_t stream = nullptr;
   std::string last_error;
-  double2* ws[2] = {nullptr, nullptr};  // two tensor-sized workspaces
-  size_t ws_bytes = 0;
+  double2* ws[3] = {nullptr, nullptr, nullptr};  // tensor-sized workspaces (ws[2]: chunked e2e only)
+  size_t ws_bytes = 0, ws3_bytes = 0;
   void* scratch = nullptr;  // small device scratch (reductions)
   cudaEvent_t ev[8] = {};
   cudaStream_t copy = nullptr;  // host<->device chunk copies overlapped with compute
@@ -103,15 +103,25 @@ void ensure_device(nds_ctx* ctx) { NDS_CUDA(cudaSetDevice(ctx->device)); }
 void ensure_ws(nds_ctx* ctx, int64_t total) {
   const size_t bytes = (size_t)total * sizeof(double2);
   if (ctx->ws_bytes >= bytes) return;
-  for (auto& w : ctx->ws)
-    if (w) {
-      cudaFree(w);
-      w = nullptr;
+  for (int i = 0; i < 2; ++i)
+    if (ctx->ws[i]) {
+      cudaFree(ctx->ws[i]);
+      ctx->ws[i] = nullptr;
     }
   ctx->ws_bytes = 0;
   NDS_CUDA(cudaMalloc(&ctx->ws[0], bytes));
   NDS_CUDA(cudaMalloc(&ctx->ws[1], bytes));
   ctx->ws_bytes = bytes;
+}
+
+void ensure_ws3(nds_ctx* ctx, int64_t total) {
+  const size_t bytes = (size_t)total * sizeof(double2);
+  if (ctx->ws3_bytes >= bytes) return;
+  if (ctx->ws[2]) cudaFree(ctx->ws[2]);
+  ctx->ws[2] = nullptr;
+  ctx->ws3_bytes = 0;
+  NDS_CUDA(cudaMalloc(&ctx->ws[2], bytes));
+  ctx->ws3_bytes = bytes;
 }
 
 // Build the device factor set: U_j in four layouts, T_j, diag(T_j). u may be null (t-only) or
@@ -476,7 +486,6 @@ void execute_host_impl(nds_plan* p, const nds_z* hb, nds_z* hx, nds_report* rep)
     cudaStream_t cs = ctx->copy;
     const int64_t chunk = p->total / K;
     const size_t cbytes = (size_t)chunk * sizeof(double2);
-    auto dst_of = [&](int pass) { return (pass % 2 == 1) ? W : X; };  // pass 1..2 np; input in X
     NDS_CUDA(cudaEventRecord(ctx->ev[4], s));
     NDS_CUDA(cudaStreamWaitEvent(cs, ctx->ev[4], 0));
     for (int k = 0; k < K; ++k) {
@@ -484,37 +493,91 @@ void execute_host_impl(nds_plan* p, const nds_z* hb, nds_z* hx, nds_report* rep)
       NDS_CUDA(cudaEventRecord(ctx->cev[k], cs));
     }
     NDS_CUDA(cudaEventRecord(ctx->ev[6], cs));
-    for (int k = 0; k < K; ++k) {  // forward: passes 1 .. np-1 per chunk as it lands
-      NDS_CUDA(cudaStreamWaitEvent(s, ctx->cev[k], 0));
-      const double2* src = X + k * chunk;
-      for (int j = 1; j < np; ++j) {
-        double2* dst = dst_of(j) + k * chunk;
-        launch_pass_chunk(p, passes[j - 1], true, src, dst, K);
+    // Last pass per chunk too when it is a row-major GEMM whose chunk slab is >= 16 wide:
+    // forward as C += U^H[:, slab_k] x_N X_k (K-split, chunks accumulate in order into a third
+    // buffer), inverse as X_k = U[slab_k, :] x_N Y (row block). Then only one chunk's worth of
+    // work separates the last H2D from the solve and the solve from the first D2H.
+    const XPass& lp = passes.back();
+    const ModeView lv = nds::mode_view(p->n_modes, p->dims, lp.mode);
+    const int64_t slab = lv.n / K;
+    const bool split_last = lp.group < 0 && lv.outer == 1 && lv.n % K == 0 &&
+                            nds::gemm_rowm_ok(ModeView{lv.inner, slab, 1});
+    if (split_last) {
+      ensure_ws3(ctx, p->total);
+      double2* S3 = ctx->ws[2];
+      const int n = (int)lv.n;
+      auto chunk_buf = [&](int pass) { return (pass % 2 == 1) ? S3 : X; };  // per-chunk ping-pong
+      for (int k = 0; k < K; ++k) {  // forward: passes 1 .. np-1, then the slab's share of pass np
+        NDS_CUDA(cudaStreamWaitEvent(s, ctx->cev[k], 0));
+        const double2* src = X + k * chunk;
+        for (int j = 1; j < np; ++j) {
+          double2* dst = chunk_buf(j) + k * chunk;
+          launch_pass_chunk(p, passes[j - 1], true, src, dst, K);
+          ++launches;
+          src = dst;
+        }
+        nds::mode_product_matrix_launch(p->f.uh_row[lp.mode - 1] + k * slab, nullptr, ModeView{lv.inner, slab, 1}, src,
+                                        W, k > 0, s, n, n);
         ++launches;
-        src = dst;
       }
-    }
-    NDS_CUDA(cudaEventRecord(ctx->ev[0], s));
-    launch_pass(p, passes.back(), true, dst_of(np - 1), dst_of(np));  // forward last pass, whole tensor
-    ++launches;
-    double2* c = dst_of(np);
-    NDS_CUDA(cudaEventRecord(ctx->ev[1], s));
-    launches += backsub_run(p, c);
-    NDS_CUDA(cudaEventRecord(ctx->ev[2], s));
-    launch_pass(p, passes.back(), false, c, dst_of(np + 1));  // inverse: last pass first
-    ++launches;
-    for (int k = 0; k < K; ++k) {
-      const double2* src = dst_of(np + 1) + k * chunk;
-      for (int j = 1; j < np; ++j) {
-        double2* dst = dst_of(np + 1 + j) + k * chunk;
-        launch_pass_chunk(p, passes[j - 1], false, src, dst, K);
+      NDS_CUDA(cudaEventRecord(ctx->ev[0], s));
+      double2* c = W;
+      NDS_CUDA(cudaEventRecord(ctx->ev[1], s));
+      launches += backsub_run(p, c);
+      NDS_CUDA(cudaEventRecord(ctx->ev[2], s));
+      // inverse per chunk: row block of the last pass, then passes 1 .. np-1; inverse pass i of
+      // np writes X when np - i is even, so the chunk ends in X
+      auto inv_buf = [&](int i) { return ((np - i) % 2 == 0) ? X : S3; };
+      for (int k = 0; k < K; ++k) {
+        double2* dst0 = inv_buf(1) + k * chunk;
+        nds::mode_product_matrix_launch(p->f.u_row[lp.mode - 1] + k * slab * n, nullptr, lv, c, dst0, false, s, slab);
         ++launches;
-        src = dst;
+        const double2* src = dst0;
+        for (int j = 1; j < np; ++j) {
+          double2* dst = inv_buf(1 + j) + k * chunk;
+          launch_pass_chunk(p, passes[j - 1], false, src, dst, K);
+          ++launches;
+          src = dst;
+        }
+        if (p->flags & NDS_REAL_OUTPUT) launches += nds::real_part_launch(X + k * chunk, chunk, s);
+        NDS_CUDA(cudaEventRecord(ctx->cev[8 + k], s));
+        NDS_CUDA(cudaStreamWaitEvent(cs, ctx->cev[8 + k], 0));
+        NDS_CUDA(cudaMemcpyAsync(hx + k * chunk, X + k * chunk, cbytes, cudaMemcpyDeviceToHost, cs));
       }
-      if (p->flags & NDS_REAL_OUTPUT) launches += nds::real_part_launch(X + k * chunk, chunk, s);
-      NDS_CUDA(cudaEventRecord(ctx->cev[8 + k], s));
-      NDS_CUDA(cudaStreamWaitEvent(cs, ctx->cev[8 + k], 0));
-      NDS_CUDA(cudaMemcpyAsync(hx + k * chunk, X + k * chunk, cbytes, cudaMemcpyDeviceToHost, cs));
+    } else {
+      auto dst_of = [&](int pass) { return (pass % 2 == 1) ? W : X; };  // pass 1..2 np; input in X
+      for (int k = 0; k < K; ++k) {  // forward: passes 1 .. np-1 per chunk as it lands
+        NDS_CUDA(cudaStreamWaitEvent(s, ctx->cev[k], 0));
+        const double2* src = X + k * chunk;
+        for (int j = 1; j < np; ++j) {
+          double2* dst = dst_of(j) + k * chunk;
+          launch_pass_chunk(p, passes[j - 1], true, src, dst, K);
+          ++launches;
+          src = dst;
+        }
+      }
+      NDS_CUDA(cudaEventRecord(ctx->ev[0], s));
+      launch_pass(p, passes.back(), true, dst_of(np - 1), dst_of(np));  // forward last pass, whole tensor
+      ++launches;
+      double2* c = dst_of(np);
+      NDS_CUDA(cudaEventRecord(ctx->ev[1], s));
+      launches += backsub_run(p, c);
+      NDS_CUDA(cudaEventRecord(ctx->ev[2], s));
+      launch_pass(p, passes.back(), false, c, dst_of(np + 1));  // inverse: last pass first
+      ++launches;
+      for (int k = 0; k < K; ++k) {
+        const double2* src = dst_of(np + 1) + k * chunk;
+        for (int j = 1; j < np; ++j) {
+          double2* dst = dst_of(np + 1 + j) + k * chunk;
+          launch_pass_chunk(p, passes[j - 1], false, src, dst, K);
+          ++launches;
+          src = dst;
+        }
+        if (p->flags & NDS_REAL_OUTPUT) launches += nds::real_part_launch(X + k * chunk, chunk, s);
+        NDS_CUDA(cudaEventRecord(ctx->cev[8 + k], s));
+        NDS_CUDA(cudaStreamWaitEvent(cs, ctx->cev[8 + k], 0));
+        NDS_CUDA(cudaMemcpyAsync(hx + k * chunk, X + k * chunk, cbytes, cudaMemcpyDeviceToHost, cs));
+      }
     }
     NDS_CUDA(cudaEventRecord(ctx->ev[3], s));
     NDS_CUDA(cudaEventRecord(ctx->ev[5], cs));
@@ -636,7 +699,7 @@ void nds_ctx_trim(nds_ctx* ctx) {
       cudaFree(w);
       w = nullptr;
     }
-  ctx->ws_bytes = 0;
+  ctx->ws_bytes = ctx->ws3_bytes = 0;
   cudaStreamSynchronize(ctx->stream);
   ctx->solvers.clear();  // plans still alive keep their shared solver structures
 }

@@ -63,8 +63,12 @@ int binary_pass_launch(const FactorSet& f, const BinGroup& gr, bool adjoint, con
 
 // Plain matrix variant (apply_operator / residual): m_row, m_col are the two layouts of M.
 // rows_out > 0: rectangular M (rows_out x n), r has extent rows_out along the mode.
+// lda_row > 0: m_row is a column block of a wider row-major matrix (row stride lda_row); only
+// valid on the GEMM path with inner >= 8 (the caller checks gemm_rowm_ok).
 int mode_product_matrix_launch(const double2* m_row, const double2* m_col, const ModeView& v, const double2* x,
-                               double2* r, bool accumulate, cudaStream_t stream, int64_t rows_out = -1);
+                               double2* r, bool accumulate, cudaStream_t stream, int64_t rows_out = -1,
+                               int64_t lda_row = -1);
+inline bool gemm_rowm_ok(const ModeView& v) { return v.n >= 16 && v.inner >= 8; }
 
 // ---- triangular solve --------------------------------------------------------------------
 struct TileGeom {

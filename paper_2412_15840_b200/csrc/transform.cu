@@ -346,7 +346,7 @@ int mode_product_launch(const FactorSet& f, int mode, bool adjoint, const ModeVi
 }
 
 int mode_product_matrix_launch(const double2* mrow, const double2* mcol, const ModeView& v, const double2* x,
-                               double2* r, bool accumulate, cudaStream_t stream, int64_t rows_out) {
+                               double2* r, bool accumulate, cudaStream_t stream, int64_t rows_out, int64_t lda_row) {
   const int n = (int)v.n;
   const int64_t m = rows_out > 0 ? rows_out : v.n;  // rows of M (output extent along the mode)
   const bool gemm = n >= 16 && (v.inner == 1 || v.inner >= 8);
@@ -375,8 +375,8 @@ int mode_product_matrix_launch(const double2* mrow, const double2* mcol, const M
     g.ldcr = m;
     g.ldcb = 0;
   } else {  // ROWM: C(i, (a, b)) = M(i, :) . X(:, (a, b))
-    g.A = mrow;  // A(i, k) = M[i][k] = mrow[i n + k]
-    g.lda = n;
+    g.A = mrow;  // A(i, k) = M[i][k] = mrow[i lda + k] (lda = n unless M is a column block)
+    g.lda = lda_row > 0 ? lda_row : n;
     g.rows = m;
     g.B = x;
     g.ldbk = v.inner;

@@ -197,11 +197,14 @@ def test_configs_reduced_against_reference(ctx, ref, name, dims):
     assert rel_max(r.x, x_ref) <= 1e-9
 
 
-@pytest.mark.parametrize("dims", [(2,) * 20, (48, 40, 64), (16, 16, 16, 32), (40, 3, 1024)],
-                         ids=["bin20", "48x40x64", "16x16x16x32", "40x3x1024"])
+@pytest.mark.parametrize("dims", [(2,) * 20, (48, 40, 64), (16, 16, 16, 32), (40, 3, 1024), (24, 20, 256),
+                                  (8, 12, 10, 128)],
+                         ids=["bin20", "48x40x64", "16x16x16x32", "40x3x1024", "24x20x256", "8x12x10x128"])
 def test_host_path_with_copy_overlap(ctx, port, dims):
     """nds_solve_schur streams B in / X out in chunks of the slowest modes overlapped with the
-    per-chunk transform passes; results must equal the unchunked oracle path."""
+    per-chunk transform passes; results must equal the unchunked oracle path. The last three
+    shapes also split the last pass per chunk (K-split forward accumulation into a third buffer,
+    row-block inverse)."""
     rng = np.random.default_rng(17)
     us, ts = rand_factors(rng, dims)
     b = rand_c(rng, dims)
