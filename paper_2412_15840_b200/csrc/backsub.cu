@@ -267,7 +267,8 @@ void solve_plan_build(SolvePlan& sp, int n_modes, const int64_t* dims, const int
         }
       }
       int64_t kc = INT64_MAX;
-      if (natural > 0 && natural < 2 * 148) kc = std::max<int64_t>(32, ((rows + 295) / 296 + 7) / 8 * 8);
+      const int64_t kq = std::max(8, update_bk(g.b[0]));  // item k-ranges are multiples of the stage depth
+      if (natural > 0 && natural < 2 * 148) kc = std::max<int64_t>(32, ((rows + 295) / 296 + kq - 1) / kq * kq);
       for (int64_t s = sp.level_off[lv]; s < sp.level_off[lv + 1]; ++s) {
         int64_t r = tiles[s];
         const int f0 = (int)far_items.size(), n0 = (int)near_items.size();
@@ -391,7 +392,8 @@ int backsub_launch(const SolvePlan& sp, const double2* t_pool, double2* c, cudaS
     NDS_CUDA(cudaFuncSetAttribute(tile_level_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)(kMaxTile * sizeof(double2))));
     for (int b : {8, 16})
-      NDS_CUDA(cudaFuncSetAttribute(update_kernel_for(b), cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024));
+      NDS_CUDA(cudaFuncSetAttribute(update_kernel_for(b), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)update_smem_bytes(b)));
     NDS_CUDA(cudaFuncSetAttribute(diag_kernel_for(3, 16), cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024));
     NDS_CUDA(cudaFuncSetAttribute(diag_kernel_for(4, 8), cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024));
     NDS_CUDA(cudaFuncSetAttribute(lines_kernel_for(3, 16), cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024));
@@ -417,6 +419,7 @@ int backsub_launch(const SolvePlan& sp, const double2* t_pool, double2* c, cudaS
   const UpdateKernel upd = update_kernel_for(b);
   const DiagKernel diag = diag_kernel_for(g.n_modes, b);
   const size_t upd_smem = update_smem_bytes(b);
+  const int uh = update_h(b);  // CTAs per update item (column halves)
   const size_t diag_smem = diag_smem_bytes(g.n_modes, b, sp.wf_levels);
   // NDS_DIAG=wave selects the per-hyperplane entry kernel (A/B experiments); default lines
   static const bool use_lines = !(getenv("NDS_DIAG") && std::string(getenv("NDS_DIAG")) == "wave");
@@ -454,7 +457,7 @@ int backsub_launch(const SolvePlan& sp, const double2* t_pool, double2* c, cudaS
       // far(lv) needs levels <= lv - 2; it overlaps diag(lv - 1) on the critical stream
       if (lv >= 2) NDS_CUDA(cudaStreamWaitEvent(sp.s_far, ev_diag(lv - 2), 0));
       tmark(sp.s_far, lv, 0);
-      upd<<<(unsigned)nf, kUpdThreads, upd_smem, sp.s_far>>>(g, t_pool, sp.d_tiles, sp.d_far_items + sp.far_off[lv],
+      upd<<<(unsigned)(nf * uh), kUpdThreads, upd_smem, sp.s_far>>>(g, t_pool, sp.d_tiles, sp.d_far_items + sp.far_off[lv],
                                                              far_buf, c);
       NDS_LAUNCH_CHECK();
       tmark(sp.s_far, lv, 1);
@@ -463,7 +466,7 @@ int backsub_launch(const SolvePlan& sp, const double2* t_pool, double2* c, cudaS
     }
     if (nn > 0) {
       tmark(sp.s_crit, lv, 2);
-      upd<<<(unsigned)nn, kUpdThreads, upd_smem, sp.s_crit>>>(g, t_pool, sp.d_tiles, sp.d_near_items + sp.near_off[lv],
+      upd<<<(unsigned)(nn * uh), kUpdThreads, upd_smem, sp.s_crit>>>(g, t_pool, sp.d_tiles, sp.d_near_items + sp.near_off[lv],
                                                               sp.d_near_partial, c);
       NDS_LAUNCH_CHECK();
       tmark(sp.s_crit, lv, 3);

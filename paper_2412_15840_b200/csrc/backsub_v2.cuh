@@ -10,7 +10,6 @@
 #endif
 
 constexpr int kUpdThreads = 256;
-constexpr int kALd = 12;  // A stage row stride (complex): = 4 mod 8 -> conflict-free fragments
 
 
 __device__ __forceinline__ void cp_async16_bs(void* smem, const void* gmem) {
@@ -31,29 +30,33 @@ __device__ __forceinline__ void dmma_bs(double& c0, double& c1, double a, double
 // complex GEMM on the FP64 tensor pipe:
 //   partial(l_j, c) = sum_{k in [kb, ke)} T_j(o_j + l_j, k) * Y(k along mode j, c),
 // rows l_j (b_j = 8 RB), columns c = the other local coordinates of the tile (cols = 4096 / b_j),
-// K streamed from global through a 3-stage cp.async ring of BK = 2048 / cols rows (32 KB).
-// Every thread owns 8 fixed (k, c) slots of each stage; their global / shared offsets are
+// K streamed from global through an ST-stage cp.async ring of BK = KM 2048 / cols rows (KM 32 KB).
+// Every thread owns 8 KM fixed (k, c) slots of each stage; their global / shared offsets are
 // computed once. Each warp owns RB x CB fragments (8x8) and reuses its A/B fragments across
 // them. The partial is written in tile-local column-major order for the diagonal kernel.
-template <int RB, int CB, bool M3>
-__global__ void __launch_bounds__(kUpdThreads, M3 ? 1 : 2)
+template <int RB, int CB, bool M3, int KM, int ST, int H>
+__global__ void __launch_bounds__(kUpdThreads, (M3 && H == 1) ? 1 : 2)
     tile_update_kernel(const TileGeom g, const double2* __restrict__ T, const int64_t* __restrict__ tiles,
                        const int4* __restrict__ items, double2* __restrict__ partial, const double2* __restrict__ Y) {
   constexpr int BJ = 8 * RB;
-  constexpr int COLS = 4096 / BJ;
-  constexpr int BK = 2048 / COLS;
-  constexpr int LDB = COLS + 2;  // = 2 mod 8 -> conflict-free B fragments
-  static_assert(RB * CB == 8 && BK % 4 == 0, "tile shape");
+  constexpr int TCOLS = 4096 / BJ;       // columns of the tile
+  constexpr int COLS = TCOLS / H;        // columns of this CTA (H CTAs per item)
+  constexpr int BK = KM * 2048 / TCOLS;
+  constexpr int LDB = COLS + 2;          // = 2 mod 8 -> conflict-free B fragments
+  constexpr int ALD = BK <= 8 ? 12 : BK + 4;  // = 4 mod 8 -> conflict-free A fragments
+  constexpr int SL = 8 * KM / H;         // load slots per thread and stage
+  static_assert(CB * 8 * (kUpdThreads / 32) == COLS && BK % 4 == 0 && BJ * BK <= kUpdThreads, "tile shape");
   extern __shared__ __align__(16) double2 sm[];
   __shared__ int64_t so[NDS_MAX_MODES];
   __shared__ int64_t s_base;
-  const int4 it = items[blockIdx.x];
+  const int4 it = items[blockIdx.x / H];
+  const int half = blockIdx.x % H;
   const int j = it.y, kb = it.z, ke = it.w;
   const int N = g.n_modes;
   int64_t* colg = (int64_t*)sm;  // global offset of column c
   int* coll = (int*)(colg + COLS);
-  double2* sA = (double2*)(coll + COLS);  // [3][BJ][kALd]
-  double2* sB = sA + 3 * BJ * kALd;       // [3][BK][LDB]
+  double2* sA = (double2*)(coll + COLS);  // [ST][BJ][ALD]
+  double2* sB = sA + ST * BJ * ALD;       // [ST][BK][LDB]
   const int tid = threadIdx.x;
   if (tid == 0) {
     int64_t t = tiles[it.x];
@@ -67,7 +70,7 @@ __global__ void __launch_bounds__(kUpdThreads, M3 ? 1 : 2)
     s_base = base;
   }
   for (int c = tid; c < COLS; c += kUpdThreads) {  // c: local coords of modes != j, earliest fastest
-    int rem = c;
+    int rem = c + half * COLS;
     int64_t og = 0;
     int ol = 0;
     for (int m = 0; m < N; ++m) {
@@ -91,10 +94,10 @@ __global__ void __launch_bounds__(kUpdThreads, M3 ? 1 : 2)
   // by bit 0 of c: conflict-free for both the cp.async writes and the fragment reads); other
   // modes run along c into the [k][LDB] layout.
   const bool kfast = j == 0;
-  int gofs[8];
-  int sofs[8];
+  int gofs[SL];
+  int sofs[SL];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
+  for (int i = 0; i < SL; ++i) {
     const int e = tid + i * kUpdThreads;
     int k, c;
     if (kfast) {
@@ -115,8 +118,8 @@ __global__ void __launch_bounds__(kUpdThreads, M3 ? 1 : 2)
     double2* dB = sB + stage * BK * LDB;
     const double2* src = Yb + (int64_t)k0 * sj;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) cp_async16_bs(dB + sofs[i], src + gofs[i]);
-    if (a_loader) cp_async16_bs(sA + stage * BJ * kALd + a_r * kALd + a_k, Tj + a_r + (int64_t)(k0 + a_k) * nj);
+    for (int i = 0; i < SL; ++i) cp_async16_bs(dB + sofs[i], src + gofs[i]);
+    if (a_loader) cp_async16_bs(sA + stage * BJ * ALD + a_r * ALD + a_k, Tj + a_r + (int64_t)(k0 + a_k) * nj);
   };
 
   const int lane = tid & 31, warp = tid >> 5;
@@ -131,25 +134,26 @@ __global__ void __launch_bounds__(kUpdThreads, M3 ? 1 : 2)
     }
 
   const int nk = (ke - kb) / BK;  // host guarantees BK | (ke - kb)
-  load_stage(0, kb);
-  cp_commit_bs();
-  if (nk > 1) load_stage(1, kb + BK);
-  cp_commit_bs();
+#pragma unroll
+  for (int st = 0; st < ST - 1; ++st) {
+    if (st < nk) load_stage(st, kb + st * BK);
+    cp_commit_bs();
+  }
   const int cbase = warp * CB * 8 + (lane >> 2);
   const int arow = lane >> 2, kq = lane & 3;
   for (int kt = 0; kt < nk; ++kt) {
-    cp_wait1_bs();
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(ST - 2));
     __syncthreads();
-    if (kt + 2 < nk) load_stage((kt + 2) % 3, kb + (kt + 2) * BK);
+    if (kt + ST - 1 < nk) load_stage((kt + ST - 1) % ST, kb + (kt + ST - 1) * BK);
     cp_commit_bs();
-    const double2* cA = sA + (kt % 3) * BJ * kALd;
-    const double2* cB = sB + (kt % 3) * BK * LDB;
+    const double2* cA = sA + (kt % ST) * BJ * ALD;
+    const double2* cB = sB + (kt % ST) * BK * LDB;
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
       double ar[RB], ai[RB], an[RB], br[CB], bi[CB];
 #pragma unroll
       for (int r = 0; r < RB; ++r) {
-        const double2 a = cA[(r * 8 + arow) * kALd + kk + kq];
+        const double2 a = cA[(r * 8 + arow) * ALD + kk + kq];
         ar[r] = a.x;
         ai[r] = a.y;
         an[r] = M3 ? a.x + a.y : -a.y;
@@ -187,7 +191,7 @@ __global__ void __launch_bounds__(kUpdThreads, M3 ? 1 : 2)
     }
   }
   cp_wait0_bs();
-  double2* out = partial + (int64_t)blockIdx.x * 4096;
+  double2* out = partial + (int64_t)(blockIdx.x / H) * 4096;
   const int bsj = g.bstride[j];
 #pragma unroll
   for (int r = 0; r < RB; ++r)
@@ -632,23 +636,43 @@ using UpdateKernel = void (*)(const TileGeom, const double2*, const int64_t*, co
 using DiagKernel = void (*)(const TileGeom, const double2*, const int64_t*, const int4*, const double2*,
                             const double2*, const uint16_t*, const int*, int, double2*);
 
-// 3M (1 CTA / SM) for b = 16, 4M (2 CTAs / SM) for b = 8 — measured; NDS_UPD=3m|4m overrides.
+// Update-kernel configurations (measured). b = 16: 3M, BK = 8, 3 stages, two CTAs per item
+// (128 columns each, 2 CTAs / SM): c1 solve 4.94 -> 4.36 ms vs one 256-column CTA (1 / SM).
+// b = 8: 4M, BK = 4, 3 stages, one CTA per item (2 / SM). NDS_UPD=3m|4m|k16|s4|h1|h2|h4 override
+// for A/B experiments.
+struct UpdCfg {
+  UpdateKernel kern;
+  int bk, stages, h;
+};
 static int update_override() {
   static const int v = [] {
     const char* e = getenv("NDS_UPD");
     if (!e) return -1;
-    return std::string(e) == "3m" ? 1 : 0;
+    const std::string s(e);
+    return s == "3m" ? 1 : s == "4m" ? 0 : s == "k16" ? 2 : s == "s4" ? 3 : s == "h2" ? 4 : s == "h1" ? 5
+         : s == "h4" ? 6 : -1;
   }();
   return v;
 }
-static UpdateKernel update_kernel_for(int b) {
+static UpdCfg update_cfg_for(int b) {
   const int o = update_override();
-  switch (b) {
-    case 8: return o == 1 ? tile_update_kernel<1, 8, true> : tile_update_kernel<1, 8, false>;
-    case 16: return o == 0 ? tile_update_kernel<2, 4, false> : tile_update_kernel<2, 4, true>;
-    default: return nullptr;
+  if (b == 8) {
+    if (o == 1) return {tile_update_kernel<1, 8, true, 1, 3, 1>, 4, 3, 1};
+    if (o == 4) return {tile_update_kernel<1, 4, true, 1, 3, 2>, 4, 3, 2};
+    if (o == 6) return {tile_update_kernel<1, 2, true, 1, 3, 4>, 4, 3, 4};
+    return {tile_update_kernel<1, 8, false, 1, 3, 1>, 4, 3, 1};
   }
+  if (b == 16) {
+    if (o == 0) return {tile_update_kernel<2, 4, false, 1, 3, 1>, 8, 3, 1};
+    if (o == 2) return {tile_update_kernel<2, 4, true, 2, 3, 1>, 16, 3, 1};
+    if (o == 3) return {tile_update_kernel<2, 4, true, 1, 4, 1>, 8, 4, 1};
+    if (o == 5) return {tile_update_kernel<2, 4, true, 1, 3, 1>, 8, 3, 1};
+    if (o == 6) return {tile_update_kernel<2, 1, true, 1, 3, 4>, 8, 3, 4};
+    return {tile_update_kernel<2, 2, true, 1, 3, 2>, 8, 3, 2};
+  }
+  return {nullptr, 0, 0, 0};
 }
+static UpdateKernel update_kernel_for(int b) { return update_cfg_for(b).kern; }
 
 // Threads per diagonal-tile CTA: at least the widest local hyperplane (192 for 16^3, 480 for 8^4).
 static int diag_threads_for(int n_modes) { return n_modes == 3 ? 256 : 512; }
@@ -658,10 +682,13 @@ static DiagKernel diag_kernel_for(int n_modes, int b) {
   if (n_modes == 4 && b == 8) return tile_diag_kernel<4, 8, 512>;
   return nullptr;
 }
+static int update_bk(int b) { return update_cfg_for(b).bk; }
+static int update_h(int b) { return update_cfg_for(b).h; }
 
 static size_t update_smem_bytes(int b) {
-  const int cols = 4096 / b, bk = 2048 / cols;
-  return (size_t)cols * (8 + 4) + (size_t)3 * b * kALd * 16 + (size_t)3 * bk * (cols + 2) * 16;
+  const UpdCfg c = update_cfg_for(b);
+  const int cols = 4096 / b / c.h, ald = c.bk <= 8 ? 12 : c.bk + 4;
+  return (size_t)cols * (8 + 4) + (size_t)c.stages * b * ald * 16 + (size_t)c.stages * c.bk * (cols + 2) * 16;
 }
 
 static size_t diag_smem_bytes(int n_modes, int b, int wf_levels) {
