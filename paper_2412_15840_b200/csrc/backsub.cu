@@ -307,35 +307,35 @@ void solve_plan_build(SolvePlan& sp, int n_modes, const int64_t* dims, const int
     lvl[lv] = grp | (((cnt * grp + 31) / 32) << 8);
   }
 
-  // v2 lines kernel: thread -> mode-1 line, ordered by d = sum_{m>=2} l_m, then by l_2, l_3, ...
-  std::vector<uint16_t> line;
+  // v2 lines kernel, push mode: for each tile slot J and mode j, the index (relative to its
+  // level) of the near item of tile J - e_j that J's diagonal CTA computes, or -1.
+  std::vector<int> near_target;
   if (sp.v2) {
-    const int b = g.b[0], nl = g.tile_entries / b;
-    int lb = 0;
-    while ((1 << lb) < b) ++lb;
-    std::vector<std::pair<int, int>> key(nl);
-    for (int c = 0; c < nl; ++c) {
-      int d = 0, k = 0;
-      for (int m = 1; m < n_modes; ++m) {
-        const int lmv = (c >> (lb * (m - 1))) & (b - 1);
-        d += lmv;
-        k = k * b + lmv;
+    near_target.assign((size_t)ntiles * n_modes, -1);
+    std::vector<int64_t> slot_of(ntiles);
+    for (int64_t s2 = 0; s2 < ntiles; ++s2) slot_of[tiles[s2]] = s2;
+    std::vector<int64_t> tstride(n_modes, 1);
+    for (int j = 1; j < n_modes; ++j) tstride[j] = tstride[j - 1] * g.nb[j - 1];
+    for (int lv = 0; lv < levels; ++lv)
+      for (int64_t n = sp.near_off[lv]; n < sp.near_off[lv + 1]; ++n) {
+        const int4 it = near_items[n];
+        const int64_t sJ = slot_of[tiles[it.x] + tstride[it.y]];
+        near_target[(size_t)sJ * n_modes + it.y] = (int)(n - sp.near_off[lv]);
       }
-      key[c] = {d * 65536 + k, c};
-    }
-    std::sort(key.begin(), key.end());
-    for (auto& kv : key) line.push_back((uint16_t)kv.second);
   }
 
   size_t bytes = ntiles * sizeof(int64_t) + (g.tile_entries + 3 * wf_levels + 2) * sizeof(int) +
-                 (thr.size() + line.size() + 8) * sizeof(uint16_t) + 64;
+                 (thr.size() + 8) * sizeof(uint16_t) + 64;
+  bytes = (bytes + 15) / 16 * 16;
+  const size_t nt_off = bytes;
+  bytes += near_target.size() * sizeof(int);
   bytes = (bytes + 15) / 16 * 16;
   const size_t items_off = bytes;
   bytes += (far_items.size() + near_items.size() + ntiles) * sizeof(int4);
   bytes = (bytes + 255) / 256 * 256;
   const size_t partial_off = bytes;
   const size_t tile_bytes = (size_t)g.tile_entries * sizeof(double2);
-  bytes += (2 * (size_t)sp.max_far + (size_t)sp.max_near) * tile_bytes + 256;
+  bytes += (2 * (size_t)sp.max_far + 2 * (size_t)sp.max_near) * tile_bytes + 256;
   NDS_CUDA(cudaMalloc(&sp.pool, bytes));
   char* base = (char*)sp.pool;
   sp.d_tiles = (int64_t*)base;
@@ -344,13 +344,14 @@ void solve_plan_build(SolvePlan& sp, int n_modes, const int64_t* dims, const int
   sp.d_wf_group = sp.d_wf_off + wf_levels + 1;
   sp.d_lvl = sp.d_wf_group + wf_levels;
   sp.d_thr = (uint16_t*)(((uintptr_t)(sp.d_lvl + wf_levels) + 15) & ~(uintptr_t)15);
-  sp.d_line = sp.d_thr + thr.size();
+  sp.d_near_target = (int*)(base + nt_off);
   sp.d_far_items = (int4*)(base + items_off);
   sp.d_near_items = sp.d_far_items + far_items.size();
   sp.d_tile_ranges = sp.d_near_items + near_items.size();
   sp.d_far_partial[0] = (double2*)(base + partial_off);
   sp.d_far_partial[1] = sp.d_far_partial[0] + (size_t)sp.max_far * g.tile_entries;
   sp.d_near_partial = sp.d_far_partial[1] + (size_t)sp.max_far * g.tile_entries;
+  sp.d_near_partial2 = sp.d_near_partial + (size_t)sp.max_near * g.tile_entries;
   NDS_CUDA(cudaMemcpy(sp.d_tiles, tiles.data(), ntiles * sizeof(int64_t), cudaMemcpyHostToDevice));
   NDS_CUDA(cudaMemcpy(sp.d_wf, wf.data(), g.tile_entries * sizeof(int), cudaMemcpyHostToDevice));
   NDS_CUDA(cudaMemcpy(sp.d_wf_off, wf_off.data(), (wf_levels + 1) * sizeof(int), cudaMemcpyHostToDevice));
@@ -358,8 +359,8 @@ void solve_plan_build(SolvePlan& sp, int n_modes, const int64_t* dims, const int
   NDS_CUDA(cudaMemcpy(sp.d_lvl, lvl.data(), wf_levels * sizeof(int), cudaMemcpyHostToDevice));
   if (!thr.empty())
     NDS_CUDA(cudaMemcpy(sp.d_thr, thr.data(), thr.size() * sizeof(uint16_t), cudaMemcpyHostToDevice));
-  if (!line.empty())
-    NDS_CUDA(cudaMemcpy(sp.d_line, line.data(), line.size() * sizeof(uint16_t), cudaMemcpyHostToDevice));
+  if (!near_target.empty())
+    NDS_CUDA(cudaMemcpy(sp.d_near_target, near_target.data(), near_target.size() * sizeof(int), cudaMemcpyHostToDevice));
   if (sp.v2) {
     if (!far_items.empty())
       NDS_CUDA(cudaMemcpy(sp.d_far_items, far_items.data(), far_items.size() * sizeof(int4), cudaMemcpyHostToDevice));
@@ -396,8 +397,10 @@ int backsub_launch(const SolvePlan& sp, const double2* t_pool, double2* c, cudaS
                                     (int)update_smem_bytes(b)));
     NDS_CUDA(cudaFuncSetAttribute(diag_kernel_for(3, 16), cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024));
     NDS_CUDA(cudaFuncSetAttribute(diag_kernel_for(4, 8), cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024));
-    NDS_CUDA(cudaFuncSetAttribute(lines_kernel_for(3, 16), cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024));
-    NDS_CUDA(cudaFuncSetAttribute(lines_kernel_for(4, 8), cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024));
+    for (bool push : {false, true}) {
+      NDS_CUDA(cudaFuncSetAttribute(lines_kernel_for(3, 16, push), cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024));
+      NDS_CUDA(cudaFuncSetAttribute(lines_kernel_for(4, 8, push), cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024));
+    }
     attr_set = true;
   }
   const TileGeom& g = sp.geom;
@@ -423,7 +426,9 @@ int backsub_launch(const SolvePlan& sp, const double2* t_pool, double2* c, cudaS
   const size_t diag_smem = diag_smem_bytes(g.n_modes, b, sp.wf_levels);
   // NDS_DIAG=wave selects the per-hyperplane entry kernel (A/B experiments); default lines
   static const bool use_lines = !(getenv("NDS_DIAG") && std::string(getenv("NDS_DIAG")) == "wave");
-  const LinesKernel lines = lines_kernel_for(g.n_modes, b);
+  // NDS_NEAR=kernel: separate near-update launches instead of the diagonal CTAs pushing them
+  static const bool push = use_lines && !(getenv("NDS_NEAR") && std::string(getenv("NDS_NEAR")) == "kernel");
+  const LinesKernel lines = lines_kernel_for(g.n_modes, b, push);
   const size_t lines_smem = lines_smem_bytes(g.n_modes, b);
   static const int dbg_levels = getenv("NDS_DEBUG_WF_LEVELS") ? atoi(getenv("NDS_DEBUG_WF_LEVELS")) : -1;
   const int wfl = dbg_levels >= 0 ? std::min(dbg_levels, sp.wf_levels) : sp.wf_levels;  // timing experiments only
@@ -464,7 +469,9 @@ int backsub_launch(const SolvePlan& sp, const double2* t_pool, double2* c, cudaS
       NDS_CUDA(cudaEventRecord(ev_far(lv), sp.s_far));
       ++launches;
     }
-    if (nn > 0) {
+    double2* near_in = push ? (lv & 1 ? sp.d_near_partial2 : sp.d_near_partial) : sp.d_near_partial;
+    double2* near_out = (lv & 1) ? sp.d_near_partial : sp.d_near_partial2;  // level lv + 1's buffer
+    if (nn > 0 && !push) {
       tmark(sp.s_crit, lv, 2);
       upd<<<(unsigned)(nn * uh), kUpdThreads, upd_smem, sp.s_crit>>>(g, t_pool, sp.d_tiles, sp.d_near_items + sp.near_off[lv],
                                                               sp.d_near_partial, c);
@@ -477,8 +484,8 @@ int backsub_launch(const SolvePlan& sp, const double2* t_pool, double2* c, cudaS
     tmark(sp.s_crit, lv, 4);
     if (use_lines)
       lines<<<(unsigned)nt, diag_threads_for(g.n_modes), lines_smem, sp.s_crit>>>(
-          g, t_pool, sp.d_tiles + sp.level_off[lv], sp.d_tile_ranges + sp.level_off[lv], far_buf, sp.d_near_partial,
-          sp.d_line, c);
+          g, t_pool, sp.d_tiles + sp.level_off[lv], sp.d_tile_ranges + sp.level_off[lv], far_buf, near_in,
+          sp.d_near_target + sp.level_off[lv] * g.n_modes, near_out, c);
     else
       diag<<<(unsigned)nt, diag_threads_for(g.n_modes), diag_smem, sp.s_crit>>>(
           g, t_pool, sp.d_tiles + sp.level_off[lv], sp.d_tile_ranges + sp.level_off[lv], far_buf, sp.d_near_partial,
@@ -496,7 +503,7 @@ int backsub_launch(const SolvePlan& sp, const double2* t_pool, double2* c, cudaS
     NDS_CUDA(cudaStreamSynchronize(stream));
     for (int lv = 0; lv < L; ++lv) {
       const int64_t nf = sp.far_off[lv + 1] - sp.far_off[lv];
-      const int64_t nn = sp.near_off[lv + 1] - sp.near_off[lv];
+      const int64_t nn = push ? 0 : sp.near_off[lv + 1] - sp.near_off[lv];
       float t[6] = {-1, -1, -1, -1, -1, -1};
       for (int k = 0; k < 6; ++k) {
         if ((k < 2 && nf == 0) || ((k == 2 || k == 3) && nn == 0)) continue;

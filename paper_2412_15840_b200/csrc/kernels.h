@@ -93,7 +93,7 @@ struct SolvePlan {
   int* d_wf_group = nullptr;      // lanes per entry for each local hyperplane (v2)
   uint16_t* d_thr = nullptr;      // v2: [wf_levels][diag threads] local entry per thread (0xffff none)
   int* d_lvl = nullptr;           // v2: per local hyperplane: grp | (busy warps << 8)
-  uint16_t* d_line = nullptr;     // v2 lines kernel: per thread its mode-1 line (l_2..l_N packed), sorted by sum
+  int* d_near_target = nullptr;   // v2 lines kernel (push): [tile slot][mode] near item of slot - e_mode at the next level
   void* pool = nullptr;
   // v2 (GEMM regime: every b_j a power of two >= 8 dividing n_j): per level, DMMA update work
   // items (tile, mode, k-range) writing partials, then one diagonal-tile kernel.
@@ -106,6 +106,7 @@ struct SolvePlan {
   int4* d_tile_ranges = nullptr;  // per tile slot: {far first, far count, near first, near count} (level-relative)
   double2* d_far_partial[2] = {nullptr, nullptr};  // double-buffered by level parity
   double2* d_near_partial = nullptr;
+  double2* d_near_partial2 = nullptr;  // push mode: near partials double-buffered by level parity
   int64_t max_far = 0, max_near = 0;
   cudaStream_t s_crit = nullptr, s_far = nullptr;
   std::vector<cudaEvent_t> ev;  // diag(lv), far(lv), start, end

@@ -57,16 +57,16 @@ int main() {
     }
   }
   {
-    auto kl = lines_kernel_for(3, 16);
+    auto kl = lines_kernel_for(3, 16, false);
     const size_t lsmem = lines_smem_bytes(3, 16);
     cudaFuncSetAttribute(kl, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
     for (int grid : {1, 148, 296}) {
       for (int w = 0; w < 3; ++w)
-        kl<<<grid, kDiagThreads, lsmem>>>(sp.geom, dT, dtiles, (const int4*)ditems, nullptr, nullptr, sp.d_line, dY);
+        kl<<<grid, kDiagThreads, lsmem>>>(sp.geom, dT, dtiles, (const int4*)ditems, nullptr, nullptr, nullptr, nullptr, dY);
       cudaEventRecord(e0);
       const int reps = 20;
       for (int r = 0; r < reps; ++r)
-        kl<<<grid, kDiagThreads, lsmem>>>(sp.geom, dT, dtiles, (const int4*)ditems, nullptr, nullptr, sp.d_line, dY);
+        kl<<<grid, kDiagThreads, lsmem>>>(sp.geom, dT, dtiles, (const int4*)ditems, nullptr, nullptr, nullptr, nullptr, dY);
       cudaEventRecord(e1);
       cudaEventSynchronize(e1);
       float ms;
