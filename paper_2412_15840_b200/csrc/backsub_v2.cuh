@@ -489,8 +489,8 @@ struct LinePad {
 //   near_out[item] (l_m, c) = sum_k T_m(o_m - B + l_m, o_m + k) Y_J(k along m, c)
 // (3M DMMA; near_target[slot N + m] = that item's index at the next level, -1 if none) — which
 // replaces the separate near-update launch on the critical path.
-template <int N, int B, int NT, bool PUSH>
-__global__ void __launch_bounds__(NT, 1)
+template <int N, int B, int NT, bool PUSH, bool T2REG>
+__global__ void __launch_bounds__(NT, T2REG ? 1 : 2)
     tile_diag_lines_kernel(const TileGeom g, const double2* __restrict__ T, const int64_t* __restrict__ tiles,
                            const int4* __restrict__ tile_ranges, const double2* __restrict__ far_partial,
                            const double2* __restrict__ near_partial, const int* __restrict__ near_target,
@@ -566,9 +566,11 @@ __global__ void __launch_bounds__(NT, 1)
     d += lm[m];
     pb += lm[m] * PS::at(m);
   }
-  double2 t2r[B - 1];  // T_2(l_2, l_2 + 1 + k)
-  {
-    const double2* t2s = Td + (B + lm[1]) * B + lm[1] + 1;
+  // T_2(l_2, l_2 + 1 + k): registers (1 CTA / SM), or read per term from Td (128 registers, so a
+  // diagonal CTA can share its SM with an update CTA)
+  double2 t2r[T2REG ? B - 1 : 1];
+  const double2* t2s = Td + (B + lm[1]) * B + lm[1] + 1;
+  if constexpr (T2REG) {
 #pragma unroll
     for (int k = 0; k < B - 1; ++k) t2r[k] = k < B - 1 - lm[1] ? t2s[k] : make_double2(0.0, 0.0);
   }
@@ -592,7 +594,7 @@ __global__ void __launch_bounds__(NT, 1)
       const int q2 = B - 1 - lm[1];
 #pragma unroll
       for (int k = 0; k < B - 1; ++k)
-        if (k < q2) a[k & 3] = cfma(a[k & 3], t2r[k], e[(1 + k) * PS::a1]);
+        if (k < q2) a[k & 3] = cfma(a[k & 3], T2REG ? t2r[T2REG ? k : 0] : t2s[k], e[(1 + k) * PS::a1]);
 #pragma unroll
       for (int m = 2; m < N; ++m) {
         const double2* tm = Td + (m * B + lm[m]) * B + lm[m] + 1;
@@ -647,59 +649,44 @@ __global__ void __launch_bounds__(NT, 1)
       if (tgt < 0) continue;  // CTA-uniform
       const double2* Tm = T + g.toff[m];
       const int64_t nm = g.dims[m], oj = so[m];
-      double2 afr[B / 4][RB];  // A(r, k) = T_m(o_m - B + r, o_m + k)
-#pragma unroll
-      for (int kk = 0; kk < B / 4; ++kk)
-#pragma unroll
-        for (int ri = 0; ri < RB; ++ri) afr[kk][ri] = Tm[(oj - B + ri * 8 + ar) + (oj + kk * 4 + kq) * nm];
       int sb[4];
 #pragma unroll
       for (int qf = 0; qf < 4; ++qf) {
         int lo;
         col_offsets(warp * 32 + qf * 8 + ar, m, sb[qf], lo);
       }
-      double cre[RB][4][2], cim[RB][4][2], c3[RB][4][2];
+      double2* out = near_out + (int64_t)tgt * E;
+#pragma unroll 1
+      for (int ri = 0; ri < RB; ++ri) {  // one 8-row fragment row at a time (register budget)
+        double2 afr[B / 4];  // A(r, k) = T_m(o_m - B + r, o_m + k)
 #pragma unroll
-      for (int ri = 0; ri < RB; ++ri)
+        for (int kk = 0; kk < B / 4; ++kk) afr[kk] = Tm[(oj - B + ri * 8 + ar) + (oj + kk * 4 + kq) * nm];
+        double cre[4][2], cim[4][2], c3[4][2];
 #pragma unroll
         for (int qf = 0; qf < 4; ++qf)
 #pragma unroll
-          for (int h = 0; h < 2; ++h) cre[ri][qf][h] = cim[ri][qf][h] = c3[ri][qf][h] = 0.0;
+          for (int h = 0; h < 2; ++h) cre[qf][h] = cim[qf][h] = c3[qf][h] = 0.0;
 #pragma unroll
-      for (int kk = 0; kk < B / 4; ++kk) {
-        double br[4], bi[4], bs[4];
-#pragma unroll
-        for (int qf = 0; qf < 4; ++qf) {
-          const double2 v = S[(kk * 4 + kq) * PS::at(m) + sb[qf]];
-          br[qf] = v.x;
-          bi[qf] = v.y;
-          bs[qf] = v.x + v.y;
-        }
-#pragma unroll
-        for (int ri = 0; ri < RB; ++ri) {
-          const double a_r = afr[kk][ri].x, a_i = afr[kk][ri].y, a_s = a_r + a_i;
+        for (int kk = 0; kk < B / 4; ++kk) {
+          const double a_r = afr[kk].x, a_i = afr[kk].y, a_s = a_r + a_i;
 #pragma unroll
           for (int qf = 0; qf < 4; ++qf) {
-            dmma_bs(cre[ri][qf][0], cre[ri][qf][1], a_r, br[qf]);
-            dmma_bs(cim[ri][qf][0], cim[ri][qf][1], a_i, bi[qf]);
-            dmma_bs(c3[ri][qf][0], c3[ri][qf][1], a_s, bs[qf]);
+            const double2 v = S[(kk * 4 + kq) * PS::at(m) + sb[qf]];
+            dmma_bs(cre[qf][0], cre[qf][1], a_r, v.x);
+            dmma_bs(cim[qf][0], cim[qf][1], a_i, v.y);
+            dmma_bs(c3[qf][0], c3[qf][1], a_s, v.x + v.y);
           }
         }
+        const int row = ri * 8 + ar;
+#pragma unroll
+        for (int qf = 0; qf < 4; ++qf)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            int so_, lo;
+            col_offsets(warp * 32 + qf * 8 + 2 * kq + h, m, so_, lo);
+            out[(row << (LB * m)) + lo] = make_double2(cre[qf][h] - cim[qf][h], c3[qf][h] - cre[qf][h] - cim[qf][h]);
+          }
       }
-      double2* out = near_out + (int64_t)tgt * E;
-#pragma unroll
-      for (int qf = 0; qf < 4; ++qf)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          int so_, lo;
-          col_offsets(warp * 32 + qf * 8 + 2 * kq + h, m, so_, lo);
-#pragma unroll
-          for (int ri = 0; ri < RB; ++ri) {
-            const int row = ri * 8 + ar;
-            out[(row << (LB * m)) + lo] =
-                make_double2(cre[ri][qf][h] - cim[ri][qf][h], c3[ri][qf][h] - cre[ri][qf][h] - cim[ri][qf][h]);
-          }
-        }
     }
   }
 }
@@ -707,8 +694,13 @@ __global__ void __launch_bounds__(NT, 1)
 using LinesKernel = void (*)(const TileGeom, const double2*, const int64_t*, const int4*, const double2*,
                              const double2*, const int*, double2*, double2*);
 static LinesKernel lines_kernel_for(int n_modes, int b, bool push) {
-  if (n_modes == 3 && b == 16) return push ? tile_diag_lines_kernel<3, 16, 256, true> : tile_diag_lines_kernel<3, 16, 256, false>;
-  if (n_modes == 4 && b == 8) return push ? tile_diag_lines_kernel<4, 8, 512, true> : tile_diag_lines_kernel<4, 8, 512, false>;
+  static const bool t2smem = getenv("NDS_DIAG_T2SMEM") != nullptr;  // A/B experiments
+  if (n_modes == 3 && b == 16) {
+    if (t2smem) return push ? tile_diag_lines_kernel<3, 16, 256, true, false> : tile_diag_lines_kernel<3, 16, 256, false, false>;
+    return push ? tile_diag_lines_kernel<3, 16, 256, true, true> : tile_diag_lines_kernel<3, 16, 256, false, true>;
+  }
+  if (n_modes == 4 && b == 8)
+    return push ? tile_diag_lines_kernel<4, 8, 512, true, true> : tile_diag_lines_kernel<4, 8, 512, false, true>;
   return nullptr;
 }
 static size_t lines_smem_bytes(int n_modes, int b) {
