@@ -387,7 +387,8 @@ void solve_plan_free(SolvePlan& sp) {
   sp.s_crit = sp.s_far = nullptr;
 }
 
-int backsub_launch(const SolvePlan& sp, const double2* t_pool, double2* c, cudaStream_t stream, Recorder* rec) {
+int backsub_launch(const SolvePlan& sp, const double2* t_pool, double2* c, cudaStream_t stream, Recorder* rec,
+                   const HeadSync* head) {
   static bool attr_set = false;
   if (!attr_set) {
     NDS_CUDA(cudaFuncSetAttribute(tile_level_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -454,6 +455,7 @@ int backsub_launch(const SolvePlan& sp, const double2* t_pool, double2* c, cudaS
   NDS_CUDA(cudaStreamWaitEvent(sp.s_crit, ev_start, 0));
   NDS_CUDA(cudaStreamWaitEvent(sp.s_far, ev_start, 0));
   if (rec) rec->mark(stream, -1, 0);
+  int head_waited = -1;
   for (int lv = 0; lv < L; ++lv) {
     const int64_t nf = sp.far_off[lv + 1] - sp.far_off[lv];
     const int64_t nn = sp.near_off[lv + 1] - sp.near_off[lv];
@@ -480,6 +482,18 @@ int backsub_launch(const SolvePlan& sp, const double2* t_pool, double2* c, cudaS
       ++launches;
     }
     if (nf > 0) NDS_CUDA(cudaStreamWaitEvent(sp.s_crit, ev_far(lv), 0));
+    if (head && head->per > 0) {  // C rows of the lowest mode-N block on this level must be ready
+      const int N = g.n_modes;
+      int64_t rest = 0;
+      for (int m = 0; m < N - 1; ++m) rest += g.nb[m] - 1;
+      const int64_t sum = (int64_t)(L - 1) - lv;
+      const int64_t bmin = std::max<int64_t>(0, sum - rest);
+      const int grp = (int)((g.nb[N - 1] - 1 - bmin) / head->per);
+      if (grp > head_waited) {
+        for (int q = head_waited + 1; q <= grp; ++q) NDS_CUDA(cudaStreamWaitEvent(sp.s_crit, head->ev[q], 0));
+        head_waited = grp;
+      }
+    }
     const int64_t nt = sp.level_off[lv + 1] - sp.level_off[lv];
     tmark(sp.s_crit, lv, 4);
     if (use_lines)

@@ -29,6 +29,8 @@ struct nds_ctx {
   void* stage = nullptr;        // pinned staging for factor uploads
   size_t stage_bytes = 0;
   cudaEvent_t cev[16] = {};
+  cudaStream_t side = nullptr;  // head overlap: row groups of the last forward pass
+  cudaEvent_t hev[33] = {};
   std::map<std::vector<int64_t>, std::shared_ptr<nds::SolverCache>> solvers;  // by extents
 };
 
@@ -361,7 +363,19 @@ int execute(nds_plan* p, const double2* b, double2* x, double2* work, cudaEvent_
   auto dst_of = [&](int pass) { return (pass % 2 == 1) ? work : x; };  // pass 1..2N
   if (ev) NDS_CUDA(cudaEventRecord(ev[0], s));
   if (rec) rec->mark(s, -1, 0);
-  for (int j = 1; j <= N; ++j) {
+  // Head overlap (cubic-tile solve, last pass a row-major GEMM): the last forward pass runs on a
+  // side stream in row groups of mode-N tile blocks, highest first, while the solve's first levels
+  // (which need only the highest blocks) start; NDS_HEAD=0 disables. N = 3 only: there a group
+  // of two blocks (1/8 of the pass for c1) takes about as long as the two nearly empty levels
+  // that wait for it (c1: -0.27 ms); with N = 4 the hyperplanes fill within a few levels and the
+  // groups fall behind (c2: +2.2 ms), so it stays off.
+  const ModeView lastv = nds::mode_view(p->n_modes, p->dims, passes.back().mode);
+  static const bool head_env = !(getenv("NDS_HEAD") && std::string(getenv("NDS_HEAD")) == "0");
+  const bool head = head_env && !p->fast_path && p->solver && !p->solver->binary && p->solver->sp.v2 &&
+                    p->n_modes == 3 && passes.back().group < 0 && passes.back().mode == p->n_modes &&
+                    lastv.outer == 1 && nds::gemm_rowm_ok(lastv);
+  const int last_fwd = head ? N - 1 : N;
+  for (int j = 1; j <= last_fwd; ++j) {
     double2* dst = dst_of(j);
     const int kind = launch_pass(p, passes[j - 1], true, src, dst);
     if (rec) rec->mark(s, kind, -passes[j - 1].mode);
@@ -370,7 +384,28 @@ int execute(nds_plan* p, const double2* b, double2* x, double2* work, cudaEvent_
   }
   double2* c = dst_of(N);
   if (ev) NDS_CUDA(cudaEventRecord(ev[1], s));
-  launches += backsub_run(p, c);
+  if (head) {
+    const nds::TileGeom& tg = p->solver->sp.geom;
+    const int64_t b = tg.b[p->n_modes - 1], nbN = tg.nb[p->n_modes - 1], n = lastv.n;
+    int per = 2;
+    while ((nbN + per - 1) / per > 32) per *= 2;
+    const int groups = (int)((nbN + per - 1) / per);
+    NDS_CUDA(cudaEventRecord(p->ctx->hev[32], s));
+    NDS_CUDA(cudaStreamWaitEvent(p->ctx->side, p->ctx->hev[32], 0));
+    for (int gq = 0; gq < groups; ++gq) {
+      const int64_t hi = nbN - (int64_t)gq * per, lo = std::max<int64_t>(0, hi - per);
+      nds::mode_product_matrix_launch(p->f.uh_row[p->n_modes - 1] + lo * b * n, nullptr, lastv, src,
+                                      c + lo * b * lastv.inner, false, p->ctx->side, (hi - lo) * b);
+      NDS_CUDA(cudaEventRecord(p->ctx->hev[gq], p->ctx->side));
+      ++launches;
+    }
+    nds::HeadSync hs;
+    hs.per = per;
+    hs.ev = p->ctx->hev;
+    launches += nds::backsub_launch(p->solver->sp, p->f.t_pool, c, s, rec, &hs);
+  } else {
+    launches += backsub_run(p, c);
+  }
   if (ev) NDS_CUDA(cudaEventRecord(ev[2], s));
   src = c;
   for (int j = 1; j <= N; ++j) {
@@ -655,6 +690,8 @@ int nds_ctx_create(nds_ctx** out, int device) {
     NDS_CUDA(cudaMalloc(&c->scratch, 256));
     for (auto& e : c->ev) NDS_CUDA(cudaEventCreate(&e));
     NDS_CUDA(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
+    NDS_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+    for (auto& e : c->hev) NDS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     // keep stream-ordered allocations (factor pools) cached instead of returning them at syncs
     cudaMemPool_t pool;
     NDS_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
@@ -675,7 +712,10 @@ void nds_ctx_destroy(nds_ctx* ctx) {
     if (e) cudaEventDestroy(e);
   for (auto& e : ctx->cev)
     if (e) cudaEventDestroy(e);
+  for (auto& e : ctx->hev)
+    if (e) cudaEventDestroy(e);
   if (ctx->copy) cudaStreamDestroy(ctx->copy);
+  if (ctx->side) cudaStreamDestroy(ctx->side);
   if (ctx->stage) cudaFreeHost(ctx->stage);
   if (ctx->own) cudaStreamDestroy(ctx->own);
   delete ctx;

@@ -139,9 +139,16 @@ struct SolverCache {
 
 void solve_plan_build(SolvePlan& sp, int n_modes, const int64_t* dims, const int64_t* toff);
 void solve_plan_free(SolvePlan& sp);
+// Head overlap: the last forward pass (mode N) produced in row groups of `per` mode-N tile blocks,
+// highest first, group g signalled by ev[g]; the diagonal tiles of a level wait only for the
+// groups holding their blocks.
+struct HeadSync {
+  int per = 0;
+  const cudaEvent_t* ev = nullptr;
+};
 // In-place Y over C. Returns kernels launched.
 int backsub_launch(const SolvePlan& sp, const double2* t_pool, double2* c, cudaStream_t stream,
-                   Recorder* rec = nullptr);
+                   Recorder* rec = nullptr, const HeadSync* head = nullptr);
 
 // ---- elementwise / reductions ------------------------------------------------------------
 // Build u_row / u_col / uh_row / uh_col of every mode from the raw column-major U_j (concatenated).
