@@ -18,6 +18,7 @@
  *     std::invalid_argument                   -> NDS_ERR_INVALID
  *     ConvergenceError (Schur, schur.cpp:146) -> NDS_ERR_CONVERGENCE
  *     std::overflow_error (tensor.cpp:13)     -> NDS_ERR_OVERFLOW
+ *     NonFiniteStateError (types.hpp:62-66)   -> NDS_ERR_NONFINITE
  *   The message of the last failure on a context is returned by nds_last_error().
  *
  *   Threading: one context per host thread; a context owns one CUDA device, one stream and
@@ -50,7 +51,8 @@ typedef enum {
   NDS_ERR_INVALID = 5,
   NDS_ERR_CONVERGENCE = 6,
   NDS_ERR_OVERFLOW = 7,
-  NDS_ERR_CUDA = 8
+  NDS_ERR_CUDA = 8,
+  NDS_ERR_NONFINITE = 9
 } nds_status;
 
 /* SolveOptions (sylvester.hpp:19-28): allow_fast_path defaults to true in the reference. */
@@ -91,6 +93,7 @@ typedef struct {
 
 typedef struct nds_ctx nds_ctx;
 typedef struct nds_plan nds_plan;
+typedef struct nds_ode nds_ode;
 
 const char* nds_version(void);
 
@@ -187,6 +190,38 @@ int nds_dev_back_substitute(nds_ctx* ctx, int n_modes, const int64_t* dims, cons
  * a[] are HOST matrices (uploaded), d_x and d_b device tensors. Synchronous. */
 int nds_dev_residual(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z* const* a, const nds_z* d_x,
                      const nds_z* d_b, double* res_max, double* res_2, double* b_max, double* b_2);
+
+/* ---- ODE  dX/dt = sum_j A_j x_j X + B,  X(0) = X0  (reference ode.hpp) ------ */
+
+/* ndsylv::triangular_exp (schur.hpp:24, schur.cpp:203-228): f = exp(t T), T upper triangular
+ * n x n column-major (Parlett recurrence, [6/6] Pade when the diagonal is not well separated).
+ * Host, like nds_schur. NDS_ERR_INVALID when T has a nonzero strict lower part. */
+int nds_triangular_exp(nds_ctx* ctx, int n, const nds_z* t_mat, double t, nds_z* f);
+
+/* ndsylv::OdePropagator (ode.hpp:18-36, ode.cpp:32-57) from the Schur factors A_j = U_j T_j U_j^H:
+ * uploads U_j, T_j, then keeps C = forward(B) and G0 = sum_j T_j x_j forward(X0) + C on the
+ * device. Like the reference constructor it does not fail on a singular operator; at() does. */
+int nds_ode_create(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z* const* u, const nds_z* const* t,
+                   const nds_z* forcing, const nds_z* initial, double singular_tol, unsigned flags, nds_ode** out);
+void nds_ode_destroy(nds_ode* ode);
+/* OdePropagator::at (ode.cpp:59-87): x = X(time), host buffer, synchronous. On the GPU:
+ * G = exp(time T_N) x_N ... exp(time T_1) x_1 G0 - C (the exponentials on the host), one
+ * triangular solve, the inverse transform. NDS_ERR_INVALID for a non-finite time;
+ * NDS_ERR_SINGULAR + sing as nds_solve. rep: stage device times (transform = exp passes). */
+int nds_ode_at(nds_ode* ode, double time, nds_z* x, nds_report* rep, nds_singular* sing);
+/* The same into a device tensor, asynchronous on the context stream. */
+int nds_ode_at_dev(nds_ode* ode, double time, nds_z* d_x);
+/* ndsylv::propagate (ode.hpp:39, ode.cpp:89-91): host Schur of each A_j + create + at. */
+int nds_propagate(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z* const* a, const nds_z* forcing,
+                  const nds_z* initial, double time, double singular_tol, unsigned flags, nds_z* x, nds_report* rep,
+                  nds_singular* sing);
+/* ndsylv::rk4_reference (ode.hpp:41-44, ode.cpp:93-129) on the device: classical RK4 with step
+ * dt, the last step shortened to land on time; each right-hand side is N mode-product GEMMs
+ * plus B; the fixed-size steps are replayed as a CUDA graph. NDS_ERR_INVALID when more than
+ * max_steps steps would be needed or dt is not positive and finite; NDS_ERR_NONFINITE when the
+ * state leaves finite range. x: host buffer. */
+int nds_rk4(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z* const* a, const nds_z* forcing,
+            const nds_z* initial, double time, double dt, int64_t max_steps, nds_z* x);
 
 /* ---- harness utility ------------------------------------------------------------------ */
 /* Seeded standard normals (Box–Muller over splitmix64 counters, stream-separated), host

@@ -120,6 +120,10 @@ class Port:
         L.orc_schur_flop_estimate.restype = C.c_int64
         L.orc_xoshiro_uniform.argtypes = [C.c_uint64, C.c_int64, _dp]
         L.orc_numerically_diagonal.argtypes = [C.c_int, _dp]
+        L.orc_triangular_exp.argtypes = [C.c_int, _dp, C.c_double, _dp]
+        L.orc_ode_at_schur.argtypes = [C.c_int, _i64p, _dpp, _dpp, _dp, _dp, C.c_double, C.c_double, C.c_uint, _dp,
+                                       _i64p, _dp]
+        L.orc_rk4.argtypes = [C.c_int, _i64p, _dpp, _dp, _dp, C.c_double, C.c_double, C.c_int64, _dp]
 
     def mode_product(self, m, mode, x):
         x = fortran(x)
@@ -194,6 +198,38 @@ class Port:
         t = fortran(t)
         return bool(self.lib.orc_numerically_diagonal(t.shape[0], _ptr(t)))
 
+    def triangular_exp(self, t_mat, t):
+        tm = fortran(t_mat)
+        f = np.empty_like(tm, order="F")
+        rc = self.lib.orc_triangular_exp(tm.shape[0], _ptr(tm), float(t), _ptr(f))
+        if rc:
+            raise OracleError(rc)
+        return f
+
+    def ode_at_schur(self, us, ts, forcing, initial, t, tol=0.0, real_output=False):
+        """OdePropagator(system).at(t) (ode.cpp:32-87) given the Schur factors."""
+        f, x0 = fortran(forcing), fortran(initial)
+        up, k1 = _ptrs(us)
+        tp, k2 = _ptrs(ts)
+        x = np.empty_like(f, order="F")
+        bad = (C.c_int64 * f.ndim)()
+        den = (C.c_double * 2)()
+        rc = self.lib.orc_ode_at_schur(f.ndim, _dims(f.shape), up, tp, _ptr(f), _ptr(x0), float(t), tol,
+                                       REAL_OUTPUT if real_output else 0, _ptr(x), bad, den)
+        if rc:
+            raise OracleError(rc, "singular" if rc == 2 else "", list(bad), complex(den[0], den[1]))
+        return x
+
+    def rk4(self, a_list, forcing, initial, t, dt, max_steps=50_000_000):
+        f, x0 = fortran(forcing), fortran(initial)
+        ap, keep = _ptrs(a_list)
+        x = np.empty_like(f, order="F")
+        rc = self.lib.orc_rk4(f.ndim, _dims(f.shape), ap, _ptr(f), _ptr(x0), float(t), float(dt), int(max_steps),
+                              _ptr(x))
+        if rc:
+            raise OracleError(rc)
+        return x
+
 
 class Ref:
     """The reference library itself (oracle/_ref), OpenMP-parallel where the reference is."""
@@ -220,6 +256,9 @@ class Ref:
         L.ref_schur_flop_estimate.argtypes = [C.c_int, _i64p]
         L.ref_schur_flop_estimate.restype = C.c_int64
         L.ref_xoshiro_uniform.argtypes = [C.c_uint64, C.c_int64, _dp]
+        L.ref_triangular_exp.argtypes = [C.c_int, _dp, C.c_double, _dp]
+        L.ref_propagate.argtypes = [C.c_int, _i64p, _dpp, _dp, _dp, C.c_double, C.c_int, _dp, _i64p, _dp]
+        L.ref_rk4.argtypes = [C.c_int, _i64p, _dpp, _dp, _dp, C.c_double, C.c_double, C.c_int64, _dp]
 
     def _check(self, rc, bad=None, den=None):
         if rc:
@@ -310,3 +349,29 @@ class Ref:
         out = np.empty(count, dtype=np.float64)
         self.lib.ref_xoshiro_uniform(seed, count, _ptr(out))
         return out
+
+    def triangular_exp(self, t_mat, t):
+        tm = fortran(t_mat)
+        f = np.empty_like(tm, order="F")
+        self._check(self.lib.ref_triangular_exp(tm.shape[0], _ptr(tm), float(t), _ptr(f)))
+        return f
+
+    def propagate(self, a_list, forcing, initial, t, real_output=False):
+        """ndsylv::propagate (ode.hpp:39): Schur + OdePropagator::at inside the reference."""
+        f, x0 = fortran(forcing), fortran(initial)
+        ap, keep = _ptrs(a_list)
+        x = np.empty_like(f, order="F")
+        bad = (C.c_int64 * f.ndim)()
+        den = (C.c_double * 2)()
+        rc = self.lib.ref_propagate(f.ndim, _dims(f.shape), ap, _ptr(f), _ptr(x0), float(t), 1 if real_output else 0,
+                                    _ptr(x), bad, den)
+        self._check(rc, bad, den)
+        return x
+
+    def rk4(self, a_list, forcing, initial, t, dt, max_steps=50_000_000):
+        f, x0 = fortran(forcing), fortran(initial)
+        ap, keep = _ptrs(a_list)
+        x = np.empty_like(f, order="F")
+        self._check(self.lib.ref_rk4(f.ndim, _dims(f.shape), ap, _ptr(f), _ptr(x0), float(t), float(dt),
+                                     int(max_steps), _ptr(x)))
+        return x

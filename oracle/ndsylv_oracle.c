@@ -376,3 +376,323 @@ void orc_xoshiro_uniform(uint64_t seed, int64_t count, double* out) {
     out[i] = (double)(result >> 11) * 0x1.0p-53;
   }
 }
+
+/* ---- ODE propagator and RK4 (ode.cpp) ------------------------------------ */
+
+/* matrix.cpp:48-58: r = a b, loops j, k (skipping zero b(k, j)), i. n x n column-major. */
+static void mat_mul(int n, const cxd* a, const cxd* b, cxd* r) {
+  memset(r, 0, (size_t)n * n * sizeof(cxd));
+  for (int j = 0; j < n; ++j)
+    for (int k = 0; k < n; ++k) {
+      const cxd bk = b[k + (size_t)j * n];
+      if (bk == 0.0) continue;
+      for (int i = 0; i < n; ++i) r[i + (size_t)j * n] += a[i + (size_t)k * n] * bk;
+    }
+}
+
+/* matrix.cpp:105-113 */
+static double mat_norm_inf(int n, const cxd* a) {
+  double best = 0.0;
+  for (int i = 0; i < n; ++i) {
+    double s = 0.0;
+    for (int j = 0; j < n; ++j) s += cabs(a[i + (size_t)j * n]);
+    if (s > best) best = s;
+  }
+  return best;
+}
+
+/* matrix.cpp:143-201: PartialPivLU(lu).solve(rhs), rhs overwritten column by column. */
+static int lu_solve(int n, cxd* lu, cxd* rhs) {
+  const double tol = DBL_EPSILON * mat_norm_inf(n, lu);
+  int* perm = (int*)malloc((size_t)n * sizeof(int));
+  cxd* col = (cxd*)malloc((size_t)n * sizeof(cxd));
+  if (!perm || !col) {
+    free(perm);
+    free(col);
+    return ORC_ERR_OTHER;
+  }
+  for (int k = 0; k < n; ++k) {
+    int piv = k;
+    double best = cabs(lu[k + (size_t)k * n]);
+    for (int i = k + 1; i < n; ++i) {
+      const double cand = cabs(lu[i + (size_t)k * n]);
+      if (cand > best) {
+        best = cand;
+        piv = i;
+      }
+    }
+    if (best <= tol) {
+      free(perm);
+      free(col);
+      return ORC_ERR_OTHER;
+    }
+    perm[k] = piv;
+    if (piv != k)
+      for (int j = 0; j < n; ++j) {
+        const cxd tmp = lu[k + (size_t)j * n];
+        lu[k + (size_t)j * n] = lu[piv + (size_t)j * n];
+        lu[piv + (size_t)j * n] = tmp;
+      }
+    const cxd inv_piv = 1.0 / lu[k + (size_t)k * n];
+    for (int i = k + 1; i < n; ++i) {
+      const cxd f = lu[i + (size_t)k * n] * inv_piv;
+      lu[i + (size_t)k * n] = f;
+      if (f == 0.0) continue;
+      for (int j = k + 1; j < n; ++j) lu[i + (size_t)j * n] -= f * lu[k + (size_t)j * n];
+    }
+  }
+  for (int j = 0; j < n; ++j) {
+    for (int i = 0; i < n; ++i) col[i] = rhs[i + (size_t)j * n];
+    for (int k = 0; k < n; ++k)
+      if (perm[k] != k) {
+        const cxd tmp = col[k];
+        col[k] = col[perm[k]];
+        col[perm[k]] = tmp;
+      }
+    for (int k = 0; k < n; ++k)
+      for (int i = k + 1; i < n; ++i) col[i] -= lu[i + (size_t)k * n] * col[k];
+    for (int i = n - 1; i >= 0; --i) {
+      cxd acc = col[i];
+      for (int k = i + 1; k < n; ++k) acc -= lu[i + (size_t)k * n] * col[k];
+      col[i] = acc / lu[i + (size_t)i * n];
+    }
+    for (int i = 0; i < n; ++i) rhs[i + (size_t)j * n] = col[i];
+  }
+  free(perm);
+  free(col);
+  return ORC_OK;
+}
+
+/* schur.cpp:230-255: [6/6] Pade with scaling and squaring; a is overwritten, result in f. */
+static int pade_exp(int n, cxd* a1, cxd* f) {
+  const size_t nn = (size_t)n * n;
+  const double norm = mat_norm_inf(n, a1);
+  int squarings = 0;
+  if (norm > 0.5) {
+    squarings = (int)ceil(log2(norm)) + 1;
+    const cxd sc = ldexp(1.0, -squarings);
+    for (size_t i = 0; i < nn; ++i) a1[i] *= sc;
+  }
+  enum { Q = 6 };
+  double coeff[Q + 1];
+  coeff[0] = 1.0;
+  for (int k = 1; k <= Q; ++k) coeff[k] = coeff[k - 1] * (double)(Q - k + 1) / (k * (2.0 * Q - k + 1));
+  cxd* a2 = (cxd*)malloc(nn * sizeof(cxd));
+  cxd* even = (cxd*)calloc(nn, sizeof(cxd));
+  cxd* odd_inner = (cxd*)calloc(nn, sizeof(cxd));
+  cxd* power = (cxd*)malloc(nn * sizeof(cxd));
+  cxd* tmp = (cxd*)malloc(nn * sizeof(cxd));
+  cxd* num = (cxd*)malloc(nn * sizeof(cxd));
+  if (!a2 || !even || !odd_inner || !power || !tmp || !num) {
+    free(a2), free(even), free(odd_inner), free(power), free(tmp), free(num);
+    return ORC_ERR_OTHER;
+  }
+  mat_mul(n, a1, a1, a2);
+  for (int i = 0; i < n; ++i) {  /* coeff * identity: every entry multiplied (zeros included) */
+    even[i + (size_t)i * n] = 1.0;
+    odd_inner[i + (size_t)i * n] = 1.0;
+  }
+  {
+    const cxd c0 = coeff[0], c1 = coeff[1];
+    for (size_t i = 0; i < nn; ++i) {
+      even[i] *= c0;
+      odd_inner[i] *= c1;
+    }
+  }
+  memcpy(power, a2, nn * sizeof(cxd));
+  for (int k = 2; k <= Q; k += 2) {
+    const cxd ck = coeff[k];
+    for (size_t i = 0; i < nn; ++i) even[i] += ck * power[i];
+    if (k + 1 <= Q) {
+      const cxd ck1 = coeff[k + 1];
+      for (size_t i = 0; i < nn; ++i) odd_inner[i] += ck1 * power[i];
+    }
+    if (k + 2 <= Q) {
+      mat_mul(n, power, a2, tmp);
+      memcpy(power, tmp, nn * sizeof(cxd));
+    }
+  }
+  mat_mul(n, a1, odd_inner, tmp); /* odd */
+  for (size_t i = 0; i < nn; ++i) {
+    num[i] = even[i] + tmp[i];
+    even[i] = even[i] - tmp[i]; /* den */
+  }
+  int rc = lu_solve(n, even, num);
+  if (rc == ORC_OK) {
+    memcpy(f, num, nn * sizeof(cxd));
+    for (int i = 0; i < squarings; ++i) {
+      mat_mul(n, f, f, tmp);
+      memcpy(f, tmp, nn * sizeof(cxd));
+    }
+  }
+  free(a2), free(even), free(odd_inner), free(power), free(tmp), free(num);
+  return rc;
+}
+
+int orc_triangular_exp(int n, const double* t_raw, double t, double* f_raw) {
+  const cxd* tm = (const cxd*)t_raw;
+  cxd* f = (cxd*)f_raw;
+  const size_t nn = (size_t)n * n;
+  for (int j = 0; j < n; ++j)
+    for (int i = j + 1; i < n; ++i)
+      if (tm[i + (size_t)j * n] != 0.0) return ORC_ERR_INVALID;
+  memset(f, 0, nn * sizeof(cxd));
+  if (t == 0.0) {
+    for (int i = 0; i < n; ++i) f[i + (size_t)i * n] = 1.0;
+    return ORC_OK;
+  }
+  /* schur.cpp:164-174 diagonal_well_separated */
+  double dmax = 0.0;
+  for (int i = 0; i < n; ++i) dmax = fmax(dmax, cabs(tm[i + (size_t)i * n]));
+  const double threshold = 1e-8 * (1.0 + dmax);
+  int separated = 1;
+  for (int i = 0; i < n && separated; ++i)
+    for (int k = i + 1; k < n; ++k)
+      if (cabs(tm[i + (size_t)i * n] - tm[k + (size_t)k * n]) < threshold) {
+        separated = 0;
+        break;
+      }
+  cxd* s = (cxd*)malloc(nn * sizeof(cxd));
+  if (!s) return ORC_ERR_OTHER;
+  const cxd ct = t; /* cxd(t, 0.0) * t_mat */
+  for (size_t i = 0; i < nn; ++i) s[i] = tm[i] * ct;
+  int rc = ORC_OK;
+  if (!separated) {
+    rc = pade_exp(n, s, f);
+    for (int j = 0; j < n; ++j)
+      for (int i = j + 1; i < n; ++i) f[i + (size_t)j * n] = 0.0;
+  } else {
+    for (int i = 0; i < n; ++i) f[i + (size_t)i * n] = cexp(s[i + (size_t)i * n]);
+    for (int p = 1; p < n; ++p)
+      for (int i = 0; i + p < n; ++i) {
+        const int j = i + p;
+#define S_(a, b) s[(a) + (size_t)(b) * n]
+#define F_(a, b) f[(a) + (size_t)(b) * n]
+        cxd num = S_(i, j) * (F_(j, j) - F_(i, i));
+        for (int k = i + 1; k < j; ++k) num += S_(i, k) * F_(k, j) - F_(i, k) * S_(k, j);
+        F_(i, j) = num / (S_(j, j) - S_(i, i));
+#undef S_
+#undef F_
+      }
+  }
+  free(s);
+  return rc;
+}
+
+/* kernels.cpp:81-88 add_scaled: y += alpha x */
+static void add_scaled(int64_t total, cxd* y, cxd alpha, const cxd* x) {
+  for (int64_t i = 0; i < total; ++i) y[i] += alpha * x[i];
+}
+
+int orc_ode_at_schur(int n_modes, const int64_t* dims, const double* const* u, const double* const* t,
+                     const double* forcing, const double* initial, double time, double singular_tol, unsigned flags,
+                     double* x, int64_t* bad_index, double* bad_den) {
+  if (n_modes < 2) return ORC_ERR_INVALID;
+  if (!isfinite(time)) return ORC_ERR_INVALID;
+  const int64_t total = orc_checked_total(n_modes, dims);
+  if (total < 0) return total == -2 ? ORC_ERR_OVERFLOW : ORC_ERR_INVALID;
+  const double tol = singular_tol > 0.0 ? singular_tol : orc_default_singular_tol(n_modes, dims, t);
+  cxd* c = (cxd*)malloc((size_t)total * sizeof(cxd));
+  cxd* y0 = (cxd*)malloc((size_t)total * sizeof(cxd));
+  cxd* g = (cxd*)malloc((size_t)total * sizeof(cxd));
+  cxd* h = (cxd*)malloc((size_t)total * sizeof(cxd));
+  int64_t fmax_n = 0;
+  for (int j = 0; j < n_modes; ++j) fmax_n = dims[j] > fmax_n ? dims[j] : fmax_n;
+  cxd* fe = (cxd*)malloc((size_t)(fmax_n * fmax_n) * sizeof(cxd));
+  int rc = ORC_OK;
+  if (!c || !y0 || !g || !h || !fe) rc = ORC_ERR_OTHER;
+  if (rc == ORC_OK) {
+    /* constructor (ode.cpp:53-56): C, Y0, operator image G0 = sum_j T_j x_j Y0 + C */
+    orc_forward_transform(n_modes, dims, u, forcing, (double*)c);
+    orc_forward_transform(n_modes, dims, u, initial, (double*)y0);
+    orc_apply_operator(n_modes, dims, t, (const double*)y0, (double*)g);
+    add_scaled(total, g, 1.0, c);
+    /* at() (ode.cpp:71-73) */
+    for (int j = 1; j <= n_modes && rc == ORC_OK; ++j) {
+      rc = orc_triangular_exp((int)dims[j - 1], t[j - 1], time, (double*)fe);
+      if (rc != ORC_OK) break;
+      orc_mode_product(n_modes, dims, (const double*)fe, j, (const double*)g, (double*)h);
+      cxd* sw = g;
+      g = h;
+      h = sw;
+    }
+  }
+  if (rc == ORC_OK) {
+    add_scaled(total, g, -1.0, c);
+    orc_backsub_stats st;
+    rc = orc_back_substitute(n_modes, dims, t, (double*)g, tol, &st, bad_index, bad_den);
+  }
+  if (rc == ORC_OK) {
+    orc_inverse_transform(n_modes, dims, u, (const double*)g, x);
+    if (flags & 2u) {
+      cxd* xc = (cxd*)x;
+      for (int64_t i = 0; i < total; ++i) xc[i] = creal(xc[i]);
+    }
+  }
+  free(c), free(y0), free(g), free(h), free(fe);
+  return rc;
+}
+
+int orc_rk4(int n_modes, const int64_t* dims, const double* const* a, const double* forcing, const double* initial,
+            double time, double dt, int64_t max_steps, double* x_raw) {
+  if (n_modes < 2) return ORC_ERR_INVALID;
+  const int64_t total = orc_checked_total(n_modes, dims);
+  if (total < 0) return total == -2 ? ORC_ERR_OVERFLOW : ORC_ERR_INVALID;
+  if (!isfinite(time)) return ORC_ERR_INVALID;
+  if (!(dt > 0.0) || !isfinite(dt)) return ORC_ERR_INVALID;
+  cxd* x = (cxd*)x_raw;
+  memcpy(x, initial, (size_t)total * sizeof(cxd));
+  if (time == 0.0) return ORC_OK;
+  const double direction = time > 0.0 ? 1.0 : -1.0;
+  const double span = fabs(time);
+  const int64_t full_steps = (int64_t)floor(span / dt);
+  if (full_steps + 1 > max_steps) return ORC_ERR_INVALID;
+  const cxd* b = (const cxd*)forcing;
+  cxd* k[4];
+  cxd* stage = (cxd*)malloc((size_t)total * sizeof(cxd));
+  int rc = stage ? ORC_OK : ORC_ERR_OTHER;
+  for (int i = 0; i < 4; ++i) {
+    k[i] = (cxd*)malloc((size_t)total * sizeof(cxd));
+    if (!k[i]) rc = ORC_ERR_OTHER;
+  }
+  /* rhs(state) = apply_operator(A, state) + B (ode.cpp:101-105) */
+#define RHS(state, out)                                                         \
+  do {                                                                          \
+    orc_apply_operator(n_modes, dims, a, (const double*)(state), (double*)(out)); \
+    add_scaled(total, (out), 1.0, b);                                           \
+  } while (0)
+  for (int64_t step = 0; rc == ORC_OK && step <= full_steps; ++step) {
+    double hh;
+    if (step < full_steps) {
+      hh = direction * dt;
+    } else {
+      const double remainder = span - (double)full_steps * dt;
+      if (!(remainder > 0.0)) break;
+      hh = direction * remainder;
+    }
+    const cxd ch = hh; /* advance (ode.cpp:107-123) */
+    RHS(x, k[0]);
+    memcpy(stage, x, (size_t)total * sizeof(cxd));
+    add_scaled(total, stage, 0.5 * ch, k[0]);
+    RHS(stage, k[1]);
+    memcpy(stage, x, (size_t)total * sizeof(cxd));
+    add_scaled(total, stage, 0.5 * ch, k[1]);
+    RHS(stage, k[2]);
+    memcpy(stage, x, (size_t)total * sizeof(cxd));
+    add_scaled(total, stage, ch, k[2]);
+    RHS(stage, k[3]);
+    add_scaled(total, x, ch / 6.0, k[0]);
+    add_scaled(total, x, ch / 3.0, k[1]);
+    add_scaled(total, x, ch / 3.0, k[2]);
+    add_scaled(total, x, ch / 6.0, k[3]);
+    for (int64_t i = 0; i < total; ++i)
+      if (!isfinite(creal(x[i])) || !isfinite(cimag(x[i]))) {
+        rc = ORC_ERR_NONFINITE;
+        break;
+      }
+  }
+#undef RHS
+  free(stage);
+  for (int i = 0; i < 4; ++i) free(k[i]);
+  return rc;
+}

@@ -30,6 +30,7 @@ enum {
   ORC_ERR_SINGULAR = 2,
   ORC_ERR_INVALID = 5,
   ORC_ERR_OVERFLOW = 7,
+  ORC_ERR_NONFINITE = 9,
 };
 
 typedef struct {
@@ -85,6 +86,23 @@ int orc_solve_schur(int n_modes, const int64_t* dims, const double* const* u, co
 /* sylvester.cpp:229-257 */
 int64_t orc_flop_estimate(int n_modes, const int64_t* dims);
 int64_t orc_schur_flop_estimate(int n_modes, const int64_t* dims);
+
+/* schur.cpp:203-228 (+ pade_exp :230-255, matrix.cpp:48-58 product, :105-113 norm_inf,
+ * :143-201 PartialPivLU) — exp(t T) for an upper triangular n x n T. ORC_ERR_INVALID when T has
+ * a nonzero strict lower part, ORC_ERR_OTHER when the Pade LU hits a tiny pivot. */
+int orc_triangular_exp(int n, const double* t_mat, double t, double* f);
+
+/* ode.cpp:32-87 — OdePropagator(system).at(time) given the Schur factors the constructor would
+ * compute (A_j = U_j T_j U_j^H): G = exp(t T_N) x_N ... exp(t T_1) x_1 (sum_j T_j x_j Y0 + C) - C,
+ * back_substitute, inverse_transform; flags bit 2 = real_output. Singular as orc_solve_schur. */
+int orc_ode_at_schur(int n_modes, const int64_t* dims, const double* const* u, const double* const* t,
+                     const double* forcing, const double* initial, double time, double singular_tol, unsigned flags,
+                     double* x, int64_t* bad_index, double* bad_den);
+
+/* ode.cpp:93-129 — classical RK4, last step shortened; ORC_ERR_INVALID on a bad step size or
+ * step budget, ORC_ERR_NONFINITE when the state leaves finite range. */
+int orc_rk4(int n_modes, const int64_t* dims, const double* const* a, const double* forcing, const double* initial,
+            double time, double dt, int64_t max_steps, double* x);
 
 /* rng.hpp:12-49 — xoshiro256++ seeded through splitmix64; uniforms from the top 53 bits. */
 void orc_xoshiro_uniform(uint64_t seed, int64_t count, double* out);

@@ -17,6 +17,8 @@
 #include <vector>
 
 #include "ndsylv/kron.hpp"
+#include "ndsylv/ode.hpp"
+#include "ndsylv/schur.hpp"
 #include "ndsylv/rng.hpp"
 #include "ndsylv/sylvester.hpp"
 
@@ -78,6 +80,9 @@ int guarded(F&& f, std::int64_t* bad_index = nullptr, double* bad_den = nullptr)
   } catch (const std::overflow_error& e) {
     g_err = e.what();
     return 7;
+  } catch (const NonFiniteStateError& e) {
+    g_err = e.what();
+    return 9;
   } catch (const std::exception& e) {
     g_err = e.what();
     return 1;
@@ -242,6 +247,42 @@ std::int64_t ref_schur_flop_estimate(int n_modes, const std::int64_t* dims) {
   std::int64_t v = -1;
   guarded([&] { v = schur_flop_estimate(dims_of(n_modes, dims)); });
   return v;
+}
+
+// ndsylv::triangular_exp (schur.hpp:24)
+int ref_triangular_exp(int n, const double* t_mat, double t, double* f) {
+  return guarded([&] { matrix_to(triangular_exp(matrix_from(n, t_mat), t), f); });
+}
+
+OdeSystem system_from(int n_modes, const std::int64_t* dims, const double* const* a, const double* forcing,
+                      const double* initial) {
+  OdeSystem sys;
+  for (int j = 0; j < n_modes; ++j) sys.coefficients.push_back(matrix_from(static_cast<int>(dims[j]), a[j]));
+  sys.forcing = tensor_from(n_modes, dims, forcing);
+  sys.initial = tensor_from(n_modes, dims, initial);
+  return sys;
+}
+
+// ndsylv::propagate (ode.hpp:39): Schur inside the OdePropagator constructor.
+int ref_propagate(int n_modes, const std::int64_t* dims, const double* const* a, const double* forcing,
+                  const double* initial, double time, int real_output, double* x, std::int64_t* bad_index,
+                  double* bad_den) {
+  return guarded(
+      [&] {
+        SolveOptions opt;
+        opt.real_output = real_output != 0;
+        const SolveResult r = propagate(system_from(n_modes, dims, a, forcing, initial), time, opt);
+        tensor_to(r.x, x);
+      },
+      bad_index, bad_den);
+}
+
+// ndsylv::rk4_reference (ode.hpp:44)
+int ref_rk4(int n_modes, const std::int64_t* dims, const double* const* a, const double* forcing,
+            const double* initial, double time, double dt, std::int64_t max_steps, double* x) {
+  return guarded([&] {
+    tensor_to(rk4_reference(system_from(n_modes, dims, a, forcing, initial), time, dt, max_steps), x);
+  });
 }
 
 void ref_xoshiro_uniform(std::uint64_t seed, std::int64_t count, double* out) {

@@ -40,7 +40,8 @@ NDS_MAX_MODES = 64
 ALLOW_FAST_PATH = 1
 REAL_OUTPUT = 2
 
-OK, ERR_OTHER, ERR_SINGULAR, ERR_FILE, ERR_NOMEM, ERR_INVALID, ERR_CONVERGENCE, ERR_OVERFLOW, ERR_CUDA = range(9)
+(OK, ERR_OTHER, ERR_SINGULAR, ERR_FILE, ERR_NOMEM, ERR_INVALID, ERR_CONVERGENCE, ERR_OVERFLOW, ERR_CUDA,
+ ERR_NONFINITE) = range(10)
 
 # Symbols include/ndsylv_b200.h declares (checked by tests/test_abi.py).
 EXPORTED = [
@@ -50,7 +51,9 @@ EXPORTED = [
     "nds_plan_create", "nds_plan_destroy", "nds_plan_report", "nds_plan_total", "nds_plan_execute",
     "nds_plan_forward", "nds_plan_backsub", "nds_plan_inverse", "nds_plan_execute_host", "nds_plan_launches",
     "nds_plan_profile_begin", "nds_plan_profile_end",
-    "nds_dev_mode_product", "nds_dev_mode_update", "nds_dev_back_substitute", "nds_dev_residual", "nds_randn",
+    "nds_dev_mode_product", "nds_dev_mode_update", "nds_dev_back_substitute", "nds_dev_residual",
+    "nds_triangular_exp", "nds_ode_create", "nds_ode_destroy", "nds_ode_at", "nds_ode_at_dev", "nds_propagate",
+    "nds_rk4", "nds_randn",
 ]
 
 
@@ -71,6 +74,10 @@ class SingularOperatorError(NdsError):
 
 class ConvergenceError(NdsError):
     pass
+
+
+class NonFiniteStateError(NdsError):
+    """NonFiniteStateError (types.hpp:62-66): an integration left finite range."""
 
 
 class DeviceError(NdsError):
@@ -164,6 +171,14 @@ def load_library(path: str = LIB_PATH):
                                           C.POINTER(_Singular)]
     L.nds_dev_residual.argtypes = [_vp, C.c_int, _i64p, _vp, _vp, _vp, C.POINTER(C.c_double),
                                    C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double)]
+    L.nds_triangular_exp.argtypes = [_vp, C.c_int, _vp, C.c_double, _vp]
+    L.nds_ode_create.argtypes = [_vp, C.c_int, _i64p, _vp, _vp, _vp, _vp, C.c_double, C.c_uint, C.POINTER(_vp)]
+    L.nds_ode_destroy.argtypes = [_vp]
+    L.nds_ode_at.argtypes = [_vp, C.c_double, _vp, C.POINTER(_Report), C.POINTER(_Singular)]
+    L.nds_ode_at_dev.argtypes = [_vp, C.c_double, _vp]
+    L.nds_propagate.argtypes = [_vp, C.c_int, _i64p, _vp, _vp, _vp, C.c_double, C.c_double, C.c_uint, _vp,
+                                C.POINTER(_Report), C.POINTER(_Singular)]
+    L.nds_rk4.argtypes = [_vp, C.c_int, _i64p, _vp, _vp, _vp, C.c_double, C.c_double, C.c_int64, _vp]
     L.nds_randn.argtypes = [C.c_uint64, C.c_uint64, C.c_int64, _vp]
     _lib = L
     return L
@@ -208,6 +223,8 @@ def _raise(code, msg, sing=None):
         raise ConvergenceError(code, msg)
     if code == ERR_CUDA:
         raise DeviceError(code, msg)
+    if code == ERR_NONFINITE:
+        raise NonFiniteStateError(code, msg)
     raise NdsError(code, msg)
 
 
@@ -237,6 +254,53 @@ class SolveResult:
     """SolveResult (sylvester.hpp:44-47)."""
     x: np.ndarray
     report: dict = field(default_factory=dict)
+
+
+class OdePropagator:
+    """ndsylv::OdePropagator (ode.hpp:18-36) from Schur factors: C and G0 stay on the device;
+    at(t) runs the exp(t T_j) mode passes, one triangular solve and the inverse transform."""
+
+    def __init__(self, ctx: "Context", us, ts, forcing, initial, singular_tol=0.0, real_output=False):
+        self.ctx = ctx
+        f, x0 = _f(forcing), _f(initial)
+        self.dims = tuple(int(v) for v in f.shape)
+        if len(us) != f.ndim or len(ts) != f.ndim:
+            raise ValueError("coefficient count does not match tensor order")
+        if x0.shape != f.shape:
+            raise ValueError("initial state shape mismatch")
+        up, self._ku = _ptr_array(us)
+        tp, self._kt = _ptr_array(ts)
+        h = _vp()
+        rc = ctx.lib.nds_ode_create(ctx.h, f.ndim, _dims(self.dims), up, tp, f.ctypes.data, x0.ctypes.data,
+                                    float(singular_tol), REAL_OUTPUT if real_output else 0, C.byref(h))
+        if rc:
+            _raise(rc, ctx.last_error())
+        self.h = h
+
+    def at(self, t: float) -> SolveResult:
+        x = np.empty(self.dims, dtype=np.complex128, order="F")
+        rep = _Report()
+        sing = _Singular()
+        rc = self.ctx.lib.nds_ode_at(self.h, float(t), x.ctypes.data, C.byref(rep), C.byref(sing))
+        if rc:
+            _raise(rc, self.ctx.last_error(), sing)
+        return SolveResult(x, _dict(rep))
+
+    def at_dev(self, t: float, d_x: int):
+        rc = self.ctx.lib.nds_ode_at_dev(self.h, float(t), d_x)
+        if rc:
+            _raise(rc, self.ctx.last_error())
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.ctx.lib.nds_ode_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 class Plan:
@@ -447,6 +511,41 @@ class Context:
         r = np.empty_like(x, order="F")
         self._check(self.lib.nds_apply_operator(self.h, x.ndim, _dims(x.shape), ap, x.ctypes.data, r.ctypes.data))
         return r
+
+    # ---- ODE (ode.hpp) ------------------------------------------------------------------------
+    def triangular_exp(self, t_mat, t: float):
+        """ndsylv::triangular_exp (schur.cpp:203-228), host."""
+        tm = _f(t_mat)
+        if tm.ndim != 2 or tm.shape[0] != tm.shape[1]:
+            raise ValueError("triangular_exp requires a square matrix")
+        f = np.empty_like(tm, order="F")
+        self._check(self.lib.nds_triangular_exp(self.h, tm.shape[0], tm.ctypes.data, float(t), f.ctypes.data))
+        return f
+
+    def ode(self, us, ts, forcing, initial, singular_tol=0.0, real_output=False) -> OdePropagator:
+        return OdePropagator(self, us, ts, forcing, initial, singular_tol, real_output)
+
+    def propagate(self, coefficients, forcing, initial, t: float, singular_tol=0.0, real_output=False) -> SolveResult:
+        """ndsylv::propagate (ode.cpp:89-91): host Schur + OdePropagator(...).at(t)."""
+        f, x0 = _f(forcing), _f(initial)
+        ap, keep = _ptr_array(coefficients)
+        x = np.empty_like(f, order="F")
+        rep = _Report()
+        sing = _Singular()
+        rc = self.lib.nds_propagate(self.h, f.ndim, _dims(f.shape), ap, f.ctypes.data, x0.ctypes.data, float(t),
+                                    float(singular_tol), REAL_OUTPUT if real_output else 0, x.ctypes.data,
+                                    C.byref(rep), C.byref(sing))
+        self._check(rc, sing)
+        return SolveResult(x, _dict(rep))
+
+    def rk4(self, coefficients, forcing, initial, t: float, dt: float, max_steps: int = 50_000_000):
+        """ndsylv::rk4_reference (ode.cpp:93-129) on the device."""
+        f, x0 = _f(forcing), _f(initial)
+        ap, keep = _ptr_array(coefficients)
+        x = np.empty_like(f, order="F")
+        self._check(self.lib.nds_rk4(self.h, f.ndim, _dims(f.shape), ap, f.ctypes.data, x0.ctypes.data, float(t),
+                                     float(dt), int(max_steps), x.ctypes.data))
+        return x
 
     # ---- device surfaces ------------------------------------------------------------------
     def plan(self, us, ts, singular_tol=0.0, allow_fast_path=True, real_output=False) -> Plan:

@@ -46,6 +46,8 @@ struct nds_plan {
   nds::FactorSet f;
   std::vector<nds::BinGroup> groups;  // fused passes over runs of binary modes
   std::shared_ptr<nds::SolverCache> solver;  // dims-only structures, shared via the context
+  bool singular = false;                     // deferred singular check (ODE propagator)
+  nds_singular sing_info{};
   int launches = 0;
   // per-launch CUDA-event profile (nds_plan_profile_begin / _end)
   bool profiling = false;
@@ -424,7 +426,8 @@ int execute(nds_plan* p, const double2* b, double2* x, double2* work, cudaEvent_
 }
 
 void plan_create_impl(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z* const* u, const nds_z* const* t,
-                      double singular_tol, unsigned flags, nds_plan** out, nds_singular* sing) {
+                      double singular_tol, unsigned flags, nds_plan** out, nds_singular* sing,
+                      bool defer_singular = false) {
   if (!out) throw Error(NDS_ERR_INVALID, "out is null");
   *out = nullptr;
   const int64_t total = checked_total(n_modes, dims, 2);
@@ -450,9 +453,14 @@ void plan_create_impl(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_
   if (bad >= 0) {
     nds_singular tmp{};
     fill_singular(&tmp, n_modes, dims, bad, t);
-    if (sing) *sing = tmp;
-    free_factors(p->f);
-    throw Error(NDS_ERR_SINGULAR, format_singular(tmp));
+    if (defer_singular) {  // OdePropagator: the constructor succeeds, at() throws
+      p->singular = true;
+      p->sing_info = tmp;
+    } else {
+      if (sing) *sing = tmp;
+      free_factors(p->f);
+      throw Error(NDS_ERR_SINGULAR, format_singular(tmp));
+    }
   }
   if (!p->fast_path) build_solver(p.get());
   *out = p.release();
@@ -664,6 +672,256 @@ void transform_host(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z*
     throw;
   }
   free_factors(p.f);
+}
+
+// ---- ODE propagator / RK4 (reference ode.cpp) -----------------------------
+
+// Host [row-major | column-major] copies of square matrices, as mode_product_matrix_launch reads.
+void pack_layouts(int64_t n, const nds_z* m, nds_z* out) {
+  for (int64_t k = 0; k < n; ++k)
+    for (int64_t i = 0; i < n; ++i) {
+      out[i * n + k] = m[i + k * n];
+      out[n * n + i + k * n] = m[i + k * n];
+    }
+}
+
+}  // namespace
+
+struct nds_ode {
+  nds_plan* plan = nullptr;        // U_j, T_j on the device, solver structures, singular info
+  double2* d_c = nullptr;          // C = forward(B)
+  double2* d_g0 = nullptr;         // G0 = sum_j T_j x_j forward(X0) + C
+  double2* d_f = nullptr;          // per mode [row | col] layouts of exp(t T_j) (also T_j at create)
+  nds_z* h_f = nullptr;            // pinned staging of the same
+  cudaEvent_t staged = nullptr;    // H2D of h_f done (h_f may be rewritten)
+  std::vector<int64_t> foff;       // per-mode offsets into d_f / h_f
+  std::vector<std::vector<nds_z>> t_host;  // T_j (column-major) for the host exponentials
+  int64_t fsize = 0;
+};
+
+namespace {
+
+void ode_destroy_impl(nds_ode* o) {
+  if (!o) return;
+  if (o->plan) cudaSetDevice(o->plan->ctx->device);
+  if (o->plan) cudaStreamSynchronize(o->plan->ctx->stream);
+  if (o->d_c) cudaFree(o->d_c);
+  if (o->d_g0) cudaFree(o->d_g0);
+  if (o->d_f) cudaFree(o->d_f);
+  if (o->h_f) cudaFreeHost(o->h_f);
+  if (o->staged) cudaEventDestroy(o->staged);
+  plan_destroy_impl(o->plan);
+  delete o;
+}
+
+// Upload per-mode [row | col] layouts from the host staging (after the previous upload finished).
+void ode_upload_f(nds_ode* o) {
+  cudaStream_t s = o->plan->ctx->stream;
+  NDS_CUDA(cudaMemcpyAsync(o->d_f, o->h_f, (size_t)o->fsize * sizeof(nds_z), cudaMemcpyHostToDevice, s));
+  NDS_CUDA(cudaEventRecord(o->staged, s));
+}
+
+void ode_create_impl(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z* const* u, const nds_z* const* t,
+                     const nds_z* forcing, const nds_z* initial, double singular_tol, unsigned flags, nds_ode** out) {
+  if (!out) throw Error(NDS_ERR_INVALID, "out is null");
+  *out = nullptr;
+  if (!forcing || !initial) throw Error(NDS_ERR_INVALID, "null tensor pointer");
+  std::unique_ptr<nds_ode, void (*)(nds_ode*)> o(new nds_ode, ode_destroy_impl);
+  // the propagator always back-substitutes (ode.cpp:74), never the fast path
+  plan_create_impl(ctx, n_modes, dims, u, t, singular_tol, flags & ~(unsigned)NDS_ALLOW_FAST_PATH, &o->plan, nullptr,
+                   true);
+  nds_plan* p = o->plan;
+  const int64_t total = p->total;
+  const size_t bytes = (size_t)total * sizeof(double2);
+  cudaStream_t s = ctx->stream;
+  o->foff.resize(n_modes);
+  for (int j = 0; j < n_modes; ++j) {
+    o->foff[j] = o->fsize;
+    o->fsize += 2 * dims[j] * dims[j];
+    o->t_host.emplace_back(t[j], t[j] + dims[j] * dims[j]);
+  }
+  NDS_CUDA(cudaMalloc(&o->d_c, bytes));
+  NDS_CUDA(cudaMalloc(&o->d_g0, bytes));
+  NDS_CUDA(cudaMalloc(&o->d_f, (size_t)o->fsize * sizeof(double2)));
+  NDS_CUDA(cudaMallocHost(&o->h_f, (size_t)o->fsize * sizeof(nds_z)));
+  NDS_CUDA(cudaEventCreateWithFlags(&o->staged, cudaEventDisableTiming));
+  ensure_ws(ctx, total);
+  // C = forward(B); Y0 = forward(X0) (ode.cpp:53-54)
+  NDS_CUDA(cudaMemcpyAsync(ctx->ws[0], forcing, bytes, cudaMemcpyHostToDevice, s));
+  transform_chain(p, true, ctx->ws[0], o->d_c, ctx->ws[1]);
+  NDS_CUDA(cudaMemcpyAsync(ctx->ws[0], initial, bytes, cudaMemcpyHostToDevice, s));
+  transform_chain(p, true, ctx->ws[0], ctx->ws[0], ctx->ws[1]);
+  // G0 = sum_j T_j x_j Y0 + C (ode.cpp:55-56: apply_operator then add_scaled(., 1, C))
+  for (int j = 0; j < n_modes; ++j) pack_layouts(dims[j], t[j], o->h_f + o->foff[j]);
+  ode_upload_f(o.get());
+  for (int j = 1; j <= n_modes; ++j) {
+    const double2* fj = (const double2*)o->d_f + o->foff[j - 1];
+    nds::mode_product_matrix_launch(fj, fj + dims[j - 1] * dims[j - 1], nds::mode_view(n_modes, dims, j), ctx->ws[0],
+                                    o->d_g0, j > 1, s);
+  }
+  nds::axpy_launch(o->d_g0, o->d_g0, make_double2(1.0, 0.0), o->d_c, total, s);
+  NDS_CUDA(cudaStreamSynchronize(s));
+  *out = o.release();
+}
+
+// X(time) into d_x (device), async on the context stream. ev (optional): stage events 0..3.
+int ode_at_dev_impl(nds_ode* o, double time, double2* d_x, cudaEvent_t* ev) {
+  if (!std::isfinite(time)) throw Error(NDS_ERR_INVALID, "time must be finite");
+  nds_plan* p = o->plan;
+  if (p->singular) throw Error(NDS_ERR_SINGULAR, format_singular(p->sing_info));
+  nds_ctx* ctx = p->ctx;
+  cudaStream_t s = ctx->stream;
+  const int N = p->n_modes;
+  ensure_ws(ctx, p->total);
+  // exp(time T_j) on the host (schur.cpp:203-228), staged once the previous upload has drained
+  NDS_CUDA(cudaEventSynchronize(o->staged));
+  std::vector<nds_z> fj;
+  for (int j = 0; j < N; ++j) {
+    const int64_t n = p->dims[j];
+    fj.resize(n * n);
+    nds::triangular_exp_host((int)n, o->t_host[j].data(), time, fj.data());
+    pack_layouts(n, fj.data(), o->h_f + o->foff[j]);
+  }
+  if (ev) NDS_CUDA(cudaEventRecord(ev[0], s));
+  ode_upload_f(o);
+  int launches = 0;
+  // G = exp(t T_N) x_N ... exp(t T_1) x_1 G0 - C  (ode.cpp:71-73)
+  const double2* src = o->d_g0;
+  double2* g = nullptr;
+  for (int j = 1; j <= N; ++j) {
+    double2* dst = ctx->ws[(j - 1) % 2];
+    const double2* f = (const double2*)o->d_f + o->foff[j - 1];
+    nds::mode_product_matrix_launch(f, f + p->dims[j - 1] * p->dims[j - 1], nds::mode_view(N, p->dims, j), src, dst,
+                                    false, s);
+    ++launches;
+    src = g = dst;
+  }
+  launches += nds::axpy_launch(g, g, make_double2(-1.0, 0.0), o->d_c, p->total, s);
+  if (ev) NDS_CUDA(cudaEventRecord(ev[1], s));
+  launches += launch_solver(p, g, s, nullptr);  // back_substitute (ode.cpp:76)
+  if (ev) NDS_CUDA(cudaEventRecord(ev[2], s));
+  double2* other = (g == ctx->ws[0]) ? ctx->ws[1] : ctx->ws[0];
+  launches += transform_chain(p, false, g, d_x, other);  // inverse_transform (ode.cpp:82)
+  if (p->flags & NDS_REAL_OUTPUT) launches += nds::real_part_launch(d_x, p->total, s);
+  if (ev) NDS_CUDA(cudaEventRecord(ev[3], s));
+  return launches;
+}
+
+void ode_at_impl(nds_ode* o, double time, nds_z* x, nds_report* rep) {
+  if (!x) throw Error(NDS_ERR_INVALID, "null tensor pointer");
+  const auto t0 = Clock::now();
+  nds_plan* p = o->plan;
+  nds_ctx* ctx = p->ctx;
+  ensure_device(ctx);
+  ensure_ws3(ctx, p->total);
+  const int launches = ode_at_dev_impl(o, time, ctx->ws[2], ctx->ev);
+  NDS_CUDA(cudaMemcpyAsync(x, ctx->ws[2], (size_t)p->total * sizeof(double2), cudaMemcpyDeviceToHost, ctx->stream));
+  NDS_CUDA(cudaEventRecord(ctx->ev[5], ctx->stream));
+  NDS_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (rep) {
+    report_static(p, rep);
+    rep->transform_seconds = ev_ms(ctx->ev[0], ctx->ev[1]) * 1e-3;
+    rep->backsub_seconds = ev_ms(ctx->ev[1], ctx->ev[2]) * 1e-3;
+    rep->inverse_seconds = ev_ms(ctx->ev[2], ctx->ev[3]) * 1e-3;
+    rep->d2h_seconds = ev_ms(ctx->ev[3], ctx->ev[5]) * 1e-3;
+    rep->kernel_launches = launches;
+    rep->total_seconds = secs(t0);
+  }
+}
+
+// rk4_reference (ode.cpp:93-129) on the device.
+void rk4_impl(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z* const* a, const nds_z* forcing,
+              const nds_z* initial, double time, double dt, int64_t max_steps, nds_z* x) {
+  const int64_t total = checked_total(n_modes, dims, 2);
+  require_ptrs(n_modes, a, "a");
+  if (!forcing || !initial || !x) throw Error(NDS_ERR_INVALID, "null tensor pointer");
+  if (!std::isfinite(time)) throw Error(NDS_ERR_INVALID, "time must be finite");
+  if (!(dt > 0.0) || !std::isfinite(dt)) throw Error(NDS_ERR_INVALID, "step size must be positive and finite");
+  const size_t bytes = (size_t)total * sizeof(double2);
+  if (time == 0.0) {
+    std::memmove(x, initial, bytes);
+    return;
+  }
+  const double direction = time > 0.0 ? 1.0 : -1.0;
+  const double span = std::fabs(time);
+  const int64_t full_steps = (int64_t)std::floor(span / dt);
+  if (full_steps + 1 > max_steps) throw Error(NDS_ERR_INVALID, "step budget exceeded");
+  ensure_device(ctx);
+  cudaStream_t s = ctx->stream;
+  // device state: X, K1..K4, stage, B, the A_j layouts, a flag
+  int64_t asz = 0;
+  std::vector<int64_t> aoff(n_modes);
+  for (int j = 0; j < n_modes; ++j) {
+    aoff[j] = asz;
+    asz += 2 * dims[j] * dims[j];
+  }
+  std::vector<nds_z> ha(asz);
+  for (int j = 0; j < n_modes; ++j) pack_layouts(dims[j], a[j], ha.data() + aoff[j]);
+  double2* pool = nullptr;
+  const size_t pool_bytes = 7 * bytes + (size_t)asz * sizeof(double2) + 256;
+  NDS_CUDA(cudaMalloc(&pool, pool_bytes));
+  cudaGraphExec_t exec = nullptr;
+  cudaGraph_t graph = nullptr;
+  auto cleanup = [&] {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+    cudaFree(pool);
+  };
+  try {
+    double2 *X = pool, *K1 = X + total, *K2 = K1 + total, *K3 = K2 + total, *K4 = K3 + total, *ST = K4 + total,
+            *B = ST + total, *dA = B + total;
+    int* flag = (int*)(dA + asz);
+    NDS_CUDA(cudaMemcpyAsync(X, initial, bytes, cudaMemcpyHostToDevice, s));
+    NDS_CUDA(cudaMemcpyAsync(B, forcing, bytes, cudaMemcpyHostToDevice, s));
+    NDS_CUDA(cudaMemcpyAsync(dA, ha.data(), (size_t)asz * sizeof(double2), cudaMemcpyHostToDevice, s));
+    NDS_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), s));
+    auto rhs = [&](const double2* state, double2* k) {  // apply_operator + forcing (ode.cpp:101-105)
+      for (int j = 1; j <= n_modes; ++j) {
+        const double2* m = dA + aoff[j - 1];
+        nds::mode_product_matrix_launch(m, m + dims[j - 1] * dims[j - 1], nds::mode_view(n_modes, dims, j), state, k,
+                                        j > 1, s);
+      }
+      nds::axpy_launch(k, k, make_double2(1.0, 0.0), B, total, s);
+    };
+    auto step = [&](double h) {  // advance (ode.cpp:107-123)
+      rhs(X, K1);
+      nds::axpy_launch(ST, X, make_double2(0.5 * h, 0.0), K1, total, s);
+      rhs(ST, K2);
+      nds::axpy_launch(ST, X, make_double2(0.5 * h, 0.0), K2, total, s);
+      rhs(ST, K3);
+      nds::axpy_launch(ST, X, make_double2(h, 0.0), K3, total, s);
+      rhs(ST, K4);
+      nds::rk4_combine_launch(X, make_double2(h / 6.0, 0.0), make_double2(h / 3.0, 0.0), K1, K2, K3, K4, total, s);
+    };
+    const double h = direction * dt;
+    int64_t done = 0;
+    if (full_steps > 0) {  // first step eagerly (sets kernel attributes), the rest as graph replays
+      step(h);
+      ++done;
+    }
+    constexpr int64_t kPerGraph = 8;
+    if (full_steps - done >= kPerGraph) {
+      NDS_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+      for (int i = 0; i < kPerGraph; ++i) step(h);
+      NDS_CUDA(cudaStreamEndCapture(s, &graph));
+      NDS_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+      for (; full_steps - done >= kPerGraph; done += kPerGraph) NDS_CUDA(cudaGraphLaunch(exec, s));
+    }
+    for (; done < full_steps; ++done) step(h);
+    const double remainder = span - (double)full_steps * dt;
+    if (remainder > 0.0) step(direction * remainder);
+    nds::nonfinite_launch(X, total, flag, s);
+    int hflag = 0;
+    NDS_CUDA(cudaMemcpyAsync(&hflag, flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+    NDS_CUDA(cudaMemcpyAsync(x, X, bytes, cudaMemcpyDeviceToHost, s));
+    NDS_CUDA(cudaStreamSynchronize(s));
+    if (hflag) throw Error(NDS_ERR_NONFINITE, "integration state is no longer finite");
+  } catch (...) {
+    cudaStreamSynchronize(s);
+    cleanup();
+    throw;
+  }
+  cleanup();
 }
 
 }  // namespace
@@ -1202,6 +1460,78 @@ int64_t nds_schur_flop_estimate(int n_modes, const int64_t* dims) {
   }
   if (__builtin_mul_overflow(sum_cubes, (int64_t)25, &flops)) return -1;
   return flops;
+}
+
+// ---- ODE (ode.hpp) ----------------------------------------------------------
+
+int nds_triangular_exp(nds_ctx* ctx, int n, const nds_z* t_mat, double t, nds_z* f) {
+  if (!ctx) return NDS_ERR_INVALID;
+  return guarded(ctx, [&] {
+    if (n < 1 || !t_mat || !f) throw Error(NDS_ERR_INVALID, "triangular_exp requires a square matrix");
+    nds::triangular_exp_host(n, t_mat, t, f);
+  });
+}
+
+int nds_ode_create(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z* const* u, const nds_z* const* t,
+                   const nds_z* forcing, const nds_z* initial, double singular_tol, unsigned flags, nds_ode** out) {
+  if (!ctx) return NDS_ERR_INVALID;
+  return guarded(ctx,
+                 [&] { ode_create_impl(ctx, n_modes, dims, u, t, forcing, initial, singular_tol, flags, out); });
+}
+
+void nds_ode_destroy(nds_ode* ode) { ode_destroy_impl(ode); }
+
+int nds_ode_at(nds_ode* ode, double time, nds_z* x, nds_report* rep, nds_singular* sing) {
+  if (!ode) return NDS_ERR_INVALID;
+  const int rc = guarded(ode->plan->ctx, [&] { ode_at_impl(ode, time, x, rep); });
+  if (rc == NDS_ERR_SINGULAR && sing) *sing = ode->plan->sing_info;
+  return rc;
+}
+
+int nds_ode_at_dev(nds_ode* ode, double time, nds_z* d_x) {
+  if (!ode) return NDS_ERR_INVALID;
+  return guarded(ode->plan->ctx, [&] {
+    if (!d_x) throw Error(NDS_ERR_INVALID, "null tensor pointer");
+    ensure_device(ode->plan->ctx);
+    ode_at_dev_impl(ode, time, (double2*)d_x, nullptr);
+  });
+}
+
+int nds_propagate(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z* const* a, const nds_z* forcing,
+                  const nds_z* initial, double time, double singular_tol, unsigned flags, nds_z* x, nds_report* rep,
+                  nds_singular* sing) {
+  if (!ctx) return NDS_ERR_INVALID;
+  nds_ode* o = nullptr;
+  const int rc = guarded(ctx, [&] {
+    const auto t0 = Clock::now();
+    checked_total(n_modes, dims, 2);
+    require_ptrs(n_modes, a, "a");
+    std::vector<std::vector<nds_z>> us(n_modes), ts(n_modes);
+    std::vector<const nds_z*> up(n_modes), tp(n_modes);
+    for (int j = 0; j < n_modes; ++j) {
+      us[j].resize(dims[j] * dims[j]);
+      ts[j].resize(dims[j] * dims[j]);
+      nds::schur_host((int)dims[j], a[j], us[j].data(), ts[j].data());
+      up[j] = us[j].data();
+      tp[j] = ts[j].data();
+    }
+    const double schur_s = secs(t0);
+    ode_create_impl(ctx, n_modes, dims, up.data(), tp.data(), forcing, initial, singular_tol, flags, &o);
+    ode_at_impl(o, time, x, rep);
+    if (rep) {
+      rep->schur_seconds = schur_s;
+      rep->total_seconds = secs(t0);
+    }
+  });
+  if (rc == NDS_ERR_SINGULAR && sing && o) *sing = o->plan->sing_info;
+  ode_destroy_impl(o);
+  return rc;
+}
+
+int nds_rk4(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z* const* a, const nds_z* forcing,
+            const nds_z* initial, double time, double dt, int64_t max_steps, nds_z* x) {
+  if (!ctx) return NDS_ERR_INVALID;
+  return guarded(ctx, [&] { rk4_impl(ctx, n_modes, dims, a, forcing, initial, time, dt, max_steps, x); });
 }
 
 void nds_randn(uint64_t seed, uint64_t stream, int64_t count, double* out) { nds::randn_host(seed, stream, count, out); }

@@ -195,6 +195,62 @@ int real_part_launch(double2* x, int64_t total, cudaStream_t stream) {
 
 constexpr int kResBlocks = 148 * 8;
 
+// ---- ODE helpers (reference kernels.cpp:81-88 add_scaled, ode.cpp:98-124 RK4 stages) -------
+// Complex scalars multiply as (a.x b.x - a.y b.y, a.x b.y + a.y b.x), the finite-value branch of
+// the libgcc product the reference's std::complex uses.
+__global__ void axpy_kernel(double2* __restrict__ z, const double2* __restrict__ x, double2 alpha,
+                            const double2* __restrict__ y, int64_t total) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x)
+    z[i] = cadd(x[i], cmul(alpha, y[i]));
+}
+
+int axpy_launch(double2* z, const double2* x, double2 alpha, const double2* y, int64_t total, cudaStream_t stream) {
+  const int64_t blocks = std::min<int64_t>((total + kEwThreads - 1) / kEwThreads, 148 * 32);
+  axpy_kernel<<<(unsigned)blocks, kEwThreads, 0, stream>>>(z, x, alpha, y, total);
+  NDS_LAUNCH_CHECK();
+  return 1;
+}
+
+// x += a1 k1; x += a2 k2; x += a2 k3; x += a1 k4 — the reference's four add_scaled calls fused,
+// same per-entry operation order (ode.cpp:118-121).
+__global__ void rk4_combine_kernel(double2* __restrict__ x, double2 a1, double2 a2, const double2* __restrict__ k1,
+                                   const double2* __restrict__ k2, const double2* __restrict__ k3,
+                                   const double2* __restrict__ k4, int64_t total) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    double2 v = x[i];
+    v = cadd(v, cmul(a1, k1[i]));
+    v = cadd(v, cmul(a2, k2[i]));
+    v = cadd(v, cmul(a2, k3[i]));
+    v = cadd(v, cmul(a1, k4[i]));
+    x[i] = v;
+  }
+}
+
+int rk4_combine_launch(double2* x, double2 a1, double2 a2, const double2* k1, const double2* k2, const double2* k3,
+                       const double2* k4, int64_t total, cudaStream_t stream) {
+  const int64_t blocks = std::min<int64_t>((total + kEwThreads - 1) / kEwThreads, 148 * 32);
+  rk4_combine_kernel<<<(unsigned)blocks, kEwThreads, 0, stream>>>(x, a1, a2, k1, k2, k3, k4, total);
+  NDS_LAUNCH_CHECK();
+  return 1;
+}
+
+// *flag |= 1 if any entry is Inf or NaN (NDTensor::all_finite).
+__global__ void nonfinite_kernel(const double2* __restrict__ x, int64_t total, int* __restrict__ flag) {
+  bool bad = false;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const double2 v = x[i];
+    bad |= !isfinite(v.x) || !isfinite(v.y);
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
+}
+
+int nonfinite_launch(const double2* x, int64_t total, int* flag, cudaStream_t stream) {
+  const int64_t blocks = std::min<int64_t>((total + kEwThreads - 1) / kEwThreads, 148 * 8);
+  nonfinite_kernel<<<(unsigned)blocks, kEwThreads, 0, stream>>>(x, total, flag);
+  NDS_LAUNCH_CHECK();
+  return 1;
+}
+
 __global__ void residual_kernel(const double2* __restrict__ r, const double2* __restrict__ b, int64_t total,
                                 double* __restrict__ part) {
   double rmax = 0.0, r2 = 0.0, bmax = 0.0, b2 = 0.0;

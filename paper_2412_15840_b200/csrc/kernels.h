@@ -158,6 +158,13 @@ void den_scan(const Geom& g, const double2* diag, double tol, double* min_abs, i
               void* scratch /* >= 16 bytes device */);
 int fast_divide_launch(const Geom& g, const double2* diag, double2* c, cudaStream_t stream);
 int real_part_launch(double2* x, int64_t total, cudaStream_t stream);
+// z = x + alpha y (z may alias x or y).
+int axpy_launch(double2* z, const double2* x, double2 alpha, const double2* y, int64_t total, cudaStream_t stream);
+// x += a1 k1 + a2 k2 + a2 k3 + a1 k4 (RK4 update, reference order).
+int rk4_combine_launch(double2* x, double2 a1, double2 a2, const double2* k1, const double2* k2, const double2* k3,
+                       const double2* k4, int64_t total, cudaStream_t stream);
+// *flag |= 1 when x has an Inf or NaN entry.
+int nonfinite_launch(const double2* x, int64_t total, int* flag, cudaStream_t stream);
 // Max-abs and sum-of-squares of (r - b) and of b, deterministic (per-block partials).
 void residual_norms(const double2* r, const double2* b, int64_t total, double* res_max, double* res_2, double* b_max,
                     double* b_2, cudaStream_t stream);
