@@ -286,6 +286,15 @@ class OdePropagator:
             _raise(rc, self.ctx.last_error(), sing)
         return SolveResult(x, _dict(rep))
 
+    def at_ptr(self, t: float, h_x: int) -> dict:
+        """at(t) into a caller-owned host buffer (e.g. pinned) of prod(dims) complex128."""
+        rep = _Report()
+        sing = _Singular()
+        rc = self.ctx.lib.nds_ode_at(self.h, float(t), h_x, C.byref(rep), C.byref(sing))
+        if rc:
+            _raise(rc, self.ctx.last_error(), sing)
+        return _dict(rep)
+
     def at_dev(self, t: float, d_x: int):
         rc = self.ctx.lib.nds_ode_at_dev(self.h, float(t), d_x)
         if rc:

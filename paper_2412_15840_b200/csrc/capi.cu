@@ -1,5 +1,6 @@
 // C-ABI of ndsylv_b200 (include/ndsylv_b200.h): validation, contexts, plans, the solve
 // orchestration of sylvester.cpp:167-227 on the device, and error mapping.
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -692,10 +693,12 @@ struct nds_ode {
   double2* d_c = nullptr;          // C = forward(B)
   double2* d_g0 = nullptr;         // G0 = sum_j T_j x_j forward(X0) + C
   double2* d_f = nullptr;          // per mode [row | col] layouts of exp(t T_j) (also T_j at create)
+  double2* d_trow = nullptr;       // row-major T_j at foff[j] / 2 (device Parlett)
   nds_z* h_f = nullptr;            // pinned staging of the same
   cudaEvent_t staged = nullptr;    // H2D of h_f done (h_f may be rewritten)
   std::vector<int64_t> foff;       // per-mode offsets into d_f / h_f
   std::vector<std::vector<nds_z>> t_host;  // T_j (column-major) for the host exponentials
+  std::vector<char> parlett;               // mode has a well-separated diagonal: exp on the device
   int64_t fsize = 0;
 };
 
@@ -708,6 +711,7 @@ void ode_destroy_impl(nds_ode* o) {
   if (o->d_c) cudaFree(o->d_c);
   if (o->d_g0) cudaFree(o->d_g0);
   if (o->d_f) cudaFree(o->d_f);
+  if (o->d_trow) cudaFree(o->d_trow);
   if (o->h_f) cudaFreeHost(o->h_f);
   if (o->staged) cudaEventDestroy(o->staged);
   plan_destroy_impl(o->plan);
@@ -739,6 +743,20 @@ void ode_create_impl(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z
     o->foff[j] = o->fsize;
     o->fsize += 2 * dims[j] * dims[j];
     o->t_host.emplace_back(t[j], t[j] + dims[j] * dims[j]);
+    // schur.cpp:164-174 diagonal_well_separated -> Parlett (device); otherwise Pade (host)
+    const int64_t n = dims[j];
+    double dmax = 0.0;
+    for (int64_t i = 0; i < n; ++i) dmax = std::max(dmax, std::hypot(t[j][i * (n + 1)].re, t[j][i * (n + 1)].im));
+    const double threshold = 1e-8 * (1.0 + dmax);
+    bool sep = true;
+    for (int64_t i = 0; i < n && sep; ++i)
+      for (int64_t k = i + 1; k < n; ++k)
+        if (std::hypot(t[j][i * (n + 1)].re - t[j][k * (n + 1)].re, t[j][i * (n + 1)].im - t[j][k * (n + 1)].im) <
+            threshold) {
+          sep = false;
+          break;
+        }
+    o->parlett.push_back(sep ? 1 : 0);
   }
   NDS_CUDA(cudaMalloc(&o->d_c, bytes));
   NDS_CUDA(cudaMalloc(&o->d_g0, bytes));
@@ -754,6 +772,10 @@ void ode_create_impl(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z
   // G0 = sum_j T_j x_j Y0 + C (ode.cpp:55-56: apply_operator then add_scaled(., 1, C))
   for (int j = 0; j < n_modes; ++j) pack_layouts(dims[j], t[j], o->h_f + o->foff[j]);
   ode_upload_f(o.get());
+  NDS_CUDA(cudaMalloc(&o->d_trow, (size_t)(o->fsize / 2) * sizeof(double2)));
+  for (int j = 0; j < n_modes; ++j)  // the row-major halves of the T layouts just uploaded
+    NDS_CUDA(cudaMemcpyAsync(o->d_trow + o->foff[j] / 2, o->d_f + o->foff[j],
+                             (size_t)dims[j] * dims[j] * sizeof(double2), cudaMemcpyDeviceToDevice, s));
   for (int j = 1; j <= n_modes; ++j) {
     const double2* fj = (const double2*)o->d_f + o->foff[j - 1];
     nds::mode_product_matrix_launch(fj, fj + dims[j - 1] * dims[j - 1], nds::mode_view(n_modes, dims, j), ctx->ws[0],
@@ -773,18 +795,35 @@ int ode_at_dev_impl(nds_ode* o, double time, double2* d_x, cudaEvent_t* ev) {
   cudaStream_t s = ctx->stream;
   const int N = p->n_modes;
   ensure_ws(ctx, p->total);
-  // exp(time T_j) on the host (schur.cpp:203-228), staged once the previous upload has drained
-  NDS_CUDA(cudaEventSynchronize(o->staged));
-  std::vector<nds_z> fj;
-  for (int j = 0; j < N; ++j) {
-    const int64_t n = p->dims[j];
-    fj.resize(n * n);
-    nds::triangular_exp_host((int)n, o->t_host[j].data(), time, fj.data());
-    pack_layouts(n, fj.data(), o->h_f + o->foff[j]);
-  }
+  // exp(time T_j) (schur.cpp:203-228): the Parlett recurrence on the device for modes with a
+  // well-separated diagonal; Pade on the host (staged once the previous upload drained) otherwise
   if (ev) NDS_CUDA(cudaEventRecord(ev[0], s));
-  ode_upload_f(o);
   int launches = 0;
+  nds::ExpArgs ea{};
+  ea.t_pool = p->f.t_pool;
+  ea.t_row = o->d_trow;
+  ea.f = (double2*)o->d_f;
+  ea.t = time;
+  int ndev = 0;
+  bool host_any = false;
+  for (int j = 0; j < N; ++j) {
+    ea.toff[j] = p->f.geom.toff[j];
+    ea.foff[j] = o->foff[j];
+    if (time != 0.0 && o->parlett[j]) {
+      ea.mode[ndev] = j;
+      ea.n[ndev] = p->dims[j];
+      ++ndev;
+    } else {
+      if (!host_any) NDS_CUDA(cudaEventSynchronize(o->staged));
+      host_any = true;
+      const int64_t n = p->dims[j];
+      std::vector<nds_z> fj(n * n);
+      nds::triangular_exp_host((int)n, o->t_host[j].data(), time, fj.data());
+      pack_layouts(n, fj.data(), o->h_f + o->foff[j]);
+    }
+  }
+  if (host_any) ode_upload_f(o);  // (modes computed on the device are overwritten below)
+  launches += nds::parlett_launch(ea, ndev, s);
   // G = exp(t T_N) x_N ... exp(t T_1) x_1 G0 - C  (ode.cpp:71-73)
   const double2* src = o->d_g0;
   double2* g = nullptr;

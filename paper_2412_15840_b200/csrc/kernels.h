@@ -150,6 +150,21 @@ struct HeadSync {
 int backsub_launch(const SolvePlan& sp, const double2* t_pool, double2* c, cudaStream_t stream,
                    Recorder* rec = nullptr, const HeadSync* head = nullptr);
 
+// ---- matrix functions (ODE propagator) -----------------------------------------------------
+// exp(t T_m) by the Parlett recurrence, one CTA per listed mode: T_m at t_pool + toff[m]
+// (column-major), result at f + foff[m] as [row-major | column-major] n x n.
+struct ExpArgs {
+  const double2* t_pool;
+  const double2* t_row;        // row-major T_m at t_row + foff[m] / 2
+  double2* f;
+  double t;
+  int mode[NDS_MAX_MODES];     // modes handled (0-based), count given at launch
+  int64_t n[NDS_MAX_MODES];    // extent of the listed mode (same index as mode[])
+  int64_t toff[NDS_MAX_MODES]; // by mode
+  int64_t foff[NDS_MAX_MODES]; // by mode
+};
+int parlett_launch(const ExpArgs& a, int count, cudaStream_t stream);
+
 // ---- elementwise / reductions ------------------------------------------------------------
 // Build u_row / u_col / uh_row / uh_col of every mode from the raw column-major U_j (concatenated).
 void factor_layouts_launch(const FactorSet& f, const double2* raw, cudaStream_t stream);

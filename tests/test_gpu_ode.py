@@ -68,6 +68,15 @@ def test_propagator_semigroup_and_device_output(ctx):
     ode.close()
 
 
+def test_propagator_scaled_identities(ctx):
+    # test_ode.cpp:24-36 (repeated eigenvalues: the host Pade branch) on the GPU path
+    rng = np.random.default_rng(41)
+    a = [-0.5 * np.eye(2, dtype=complex), (-1.0 + 0.3j) * np.eye(3, dtype=complex)]
+    x0 = rng.standard_normal((2, 3)) + 1j * rng.standard_normal((2, 3))
+    x = ctx.propagate(a, np.zeros((2, 3), complex), x0, 0.7).x
+    assert np.max(np.abs(x - np.exp((-1.5 + 0.3j) * 0.7) * x0)) <= 1e-12
+
+
 def test_propagator_errors(ctx):
     # test_ode.cpp:110-117 (singular at at(), not at construction), :124 (non-finite time), :136-141
     ts = [np.diag([1.0, -1.0]).astype(complex), np.diag([-1.0, 1.0]).astype(complex)]
