@@ -4,6 +4,7 @@
 #include <chrono>
 #include <memory>
 #include <stdexcept>
+#include "ndsylv/ode.hpp"
 #include "ndsylv/sylvester.hpp"
 #include "ndsylv_b200.h"
 
@@ -30,6 +31,7 @@ inline void rethrow(int rc, const nds_singular& s) {
     case NDS_ERR_OVERFLOW: throw std::overflow_error(msg);
     case NDS_ERR_CONVERGENCE: throw ConvergenceError(msg);
     case NDS_ERR_NOMEM: throw std::bad_alloc();
+    case NDS_ERR_NONFINITE: throw NonFiniteStateError(msg);
     default: throw std::runtime_error(msg);
   }
 }
@@ -72,4 +74,78 @@ inline SolveResult solve(const SylvesterProblem& p, const SolveOptions& o = {}) 
 
 // Stage functions (sylvester.hpp:64-77) map 1:1: nds_forward_transform, nds_inverse_transform,
 // nds_back_substitute (in place, like the reference), nds_mode_product, nds_apply_operator.
+
+// ---- ODE (ode.hpp): same contracts as ndsylv::OdePropagator / propagate / rk4_reference -----
+class OdePropagator {
+ public:
+  explicit OdePropagator(OdeSystem system, SolveOptions options = {})
+      : system_(std::move(system)), options_(options) {
+    const int n = system_.forcing.order();
+    if (n < 2) throw std::invalid_argument("system order must be at least 2");
+    if (static_cast<int>(system_.coefficients.size()) != n)
+      throw std::invalid_argument("coefficient count does not match tensor order");
+    if (system_.initial.dims != system_.forcing.dims) throw std::invalid_argument("initial state shape mismatch");
+    const auto t0 = std::chrono::steady_clock::now();
+    for (const Matrix& a : system_.coefficients) factors_.push_back(schur(a));
+    schur_seconds_ = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    std::vector<const nds_z*> u, t;
+    for (auto& f : factors_) {
+      u.push_back(reinterpret_cast<const nds_z*>(f.u.data()));
+      t.push_back(reinterpret_cast<const nds_z*>(f.t.data()));
+    }
+    nds_ode* raw = nullptr;
+    rethrow(nds_ode_create(context(), n, system_.forcing.dims.data(), u.data(), t.data(),
+                           reinterpret_cast<const nds_z*>(system_.forcing.data.data()),
+                           reinterpret_cast<const nds_z*>(system_.initial.data.data()), options_.singular_tol,
+                           options_.real_output ? NDS_REAL_OUTPUT : 0u, &raw),
+            nds_singular{});
+    ode_.reset(raw);
+  }
+
+  SolveResult at(double t) const {
+    SolveResult r;
+    r.x = NDTensor::zeros(system_.forcing.dims);
+    nds_report rep{};
+    nds_singular sing{};
+    rethrow(nds_ode_at(ode_.get(), t, reinterpret_cast<nds_z*>(r.x.data.data()), &rep, &sing), sing);
+    r.report.min_abs_denominator = rep.min_abs_denominator;
+    r.report.flop_estimate = rep.flop_estimate;
+    r.report.schur_flop_estimate = rep.schur_flop_estimate;
+    r.report.backsub_entries = rep.backsub_entries;
+    r.report.backsub_multiplies = rep.backsub_multiplies;
+    r.report.schur_seconds = schur_seconds_;
+    r.report.transform_seconds = rep.transform_seconds;
+    r.report.backsub_seconds = rep.backsub_seconds;
+    r.report.inverse_seconds = rep.inverse_seconds;
+    r.report.total_seconds = schur_seconds_ + rep.total_seconds;
+    return r;
+  }
+
+  const OdeSystem& system() const noexcept { return system_; }
+
+ private:
+  OdeSystem system_;
+  SolveOptions options_;
+  std::vector<SchurFactors> factors_;
+  double schur_seconds_ = 0.0;
+  std::unique_ptr<nds_ode, void (*)(nds_ode*)> ode_{nullptr, nds_ode_destroy};
+};
+
+inline SolveResult propagate(const OdeSystem& system, double t, const SolveOptions& options = {}) {
+  return OdePropagator(system, options).at(t);
+}
+
+inline NDTensor rk4_reference(const OdeSystem& system, double t, double dt, std::int64_t max_steps = 50'000'000) {
+  const int n = system.forcing.order();
+  if (system.initial.dims != system.forcing.dims) throw std::invalid_argument("initial state shape mismatch");
+  std::vector<const nds_z*> a;
+  for (const Matrix& m : system.coefficients) a.push_back(reinterpret_cast<const nds_z*>(m.data()));
+  NDTensor x = NDTensor::zeros(system.forcing.dims);
+  rethrow(nds_rk4(context(), n, system.forcing.dims.data(), a.data(),
+                  reinterpret_cast<const nds_z*>(system.forcing.data.data()),
+                  reinterpret_cast<const nds_z*>(system.initial.data.data()), t, dt, max_steps,
+                  reinterpret_cast<nds_z*>(x.data.data())),
+          nds_singular{});
+  return x;
+}
 }  // namespace ndsylv::gpu

@@ -17,3 +17,4 @@ def test_reference_program_with_gpu_backend():
     r = subprocess.run([BIN], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "singular_ok 1" in r.stdout
+    assert "nonfinite_ok 1" in r.stdout
