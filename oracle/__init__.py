@@ -257,7 +257,8 @@ class Ref:
         L.ref_schur_flop_estimate.restype = C.c_int64
         L.ref_xoshiro_uniform.argtypes = [C.c_uint64, C.c_int64, _dp]
         L.ref_triangular_exp.argtypes = [C.c_int, _dp, C.c_double, _dp]
-        L.ref_propagate.argtypes = [C.c_int, _i64p, _dpp, _dp, _dp, C.c_double, C.c_int, _dp, _i64p, _dp]
+        L.ref_propagate.argtypes = [C.c_int, _i64p, _dpp, _dp, _dp, C.c_double, C.c_int, _dp, C.POINTER(_ReportRef),
+                                    _i64p, _dp]
         L.ref_rk4.argtypes = [C.c_int, _i64p, _dpp, _dp, _dp, C.c_double, C.c_double, C.c_int64, _dp]
 
     def _check(self, rc, bad=None, den=None):
@@ -356,17 +357,18 @@ class Ref:
         self._check(self.lib.ref_triangular_exp(tm.shape[0], _ptr(tm), float(t), _ptr(f)))
         return f
 
-    def propagate(self, a_list, forcing, initial, t, real_output=False):
+    def propagate(self, a_list, forcing, initial, t, real_output=False, report=False):
         """ndsylv::propagate (ode.hpp:39): Schur + OdePropagator::at inside the reference."""
         f, x0 = fortran(forcing), fortran(initial)
         ap, keep = _ptrs(a_list)
         x = np.empty_like(f, order="F")
+        rep = _ReportRef()
         bad = (C.c_int64 * f.ndim)()
         den = (C.c_double * 2)()
         rc = self.lib.ref_propagate(f.ndim, _dims(f.shape), ap, _ptr(f), _ptr(x0), float(t), 1 if real_output else 0,
-                                    _ptr(x), bad, den)
+                                    _ptr(x), C.byref(rep), bad, den)
         self._check(rc, bad, den)
-        return x
+        return (x, _as_dict(rep)) if report else x
 
     def rk4(self, a_list, forcing, initial, t, dt, max_steps=50_000_000):
         f, x0 = fortran(forcing), fortran(initial)

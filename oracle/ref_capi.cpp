@@ -265,14 +265,27 @@ OdeSystem system_from(int n_modes, const std::int64_t* dims, const double* const
 
 // ndsylv::propagate (ode.hpp:39): Schur inside the OdePropagator constructor.
 int ref_propagate(int n_modes, const std::int64_t* dims, const double* const* a, const double* forcing,
-                  const double* initial, double time, int real_output, double* x, std::int64_t* bad_index,
-                  double* bad_den) {
+                  const double* initial, double time, int real_output, double* x, ref_report* rep,
+                  std::int64_t* bad_index, double* bad_den) {
   return guarded(
       [&] {
         SolveOptions opt;
         opt.real_output = real_output != 0;
         const SolveResult r = propagate(system_from(n_modes, dims, a, forcing, initial), time, opt);
         tensor_to(r.x, x);
+        if (rep) {
+          rep->min_abs_denominator = r.report.min_abs_denominator;
+          rep->used_normal_fast_path = r.report.used_normal_fast_path ? 1 : 0;
+          rep->flop_estimate = r.report.flop_estimate;
+          rep->schur_flop_estimate = r.report.schur_flop_estimate;
+          rep->backsub_entries = r.report.backsub_entries;
+          rep->backsub_multiplies = r.report.backsub_multiplies;
+          rep->schur_seconds = r.report.schur_seconds;
+          rep->transform_seconds = r.report.transform_seconds;
+          rep->backsub_seconds = r.report.backsub_seconds;
+          rep->inverse_seconds = r.report.inverse_seconds;
+          rep->total_seconds = r.report.total_seconds;
+        }
       },
       bad_index, bad_den);
 }

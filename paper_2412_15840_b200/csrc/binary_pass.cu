@@ -83,9 +83,18 @@ __global__ void __launch_bounds__(kBinThreads, 2) binary_pass_kernel(const BinPa
   const int64_t o = tile / bp.n_runs;
   const int R = 1 << bp.logR;
   const int64_t base = run * R + bp.I * ((int64_t)1 << bp.k) * o;
-  // global -> shared (coalesced along runs of R entries)
-#pragma unroll 4
-  for (int p = tid; p < 4096; p += kBinThreads) S[swz(p)] = x[base + (p & (R - 1)) + bp.I * (p >> bp.logR)];
+  // global -> shared (coalesced along runs of R entries): 8 loads of a thread in flight at a time
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    double2 v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int p = tid + (h * 8 + i) * kBinThreads;
+      v[i] = x[base + (p & (R - 1)) + bp.I * (p >> bp.logR)];
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) S[swz(tid + (h * 8 + i) * kBinThreads)] = v[i];
+  }
   __syncthreads();
   for (int rd = 0; rd < bp.rounds; ++rd) {
     switch (bp.nrb[rd]) {
@@ -96,8 +105,11 @@ __global__ void __launch_bounds__(kBinThreads, 2) binary_pass_kernel(const BinPa
     }
     __syncthreads();
   }
-#pragma unroll 4
-  for (int p = tid; p < 4096; p += kBinThreads) r[base + (p & (R - 1)) + bp.I * (p >> bp.logR)] = S[swz(p)];
+#pragma unroll
+  for (int i = 0; i < 4096 / kBinThreads; ++i) {
+    const int p = tid + i * kBinThreads;
+    r[base + (p & (R - 1)) + bp.I * (p >> bp.logR)] = S[swz(p)];
+  }
 }
 
 // Plan the passes over [mode0, mode1) (1-based, all n_j = 2): greedily take as many binary modes

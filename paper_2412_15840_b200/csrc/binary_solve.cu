@@ -25,7 +25,7 @@ struct BinSolveGeom {
   const double2* t;   // per mode j: T_j (2x2 column-major) at t + 4 j
 };
 
-__global__ void __launch_bounds__(kBinSolveThreads) binary_tile_solve_kernel(const BinSolveGeom g,
+__global__ void __launch_bounds__(kBinSolveThreads, 3) binary_tile_solve_kernel(const BinSolveGeom g,
                                                                               const int64_t* __restrict__ tiles,
                                                                               const int* __restrict__ wf,
                                                                               const int* __restrict__ wf_off,
@@ -49,12 +49,32 @@ __global__ void __launch_bounds__(kBinSolveThreads) binary_tile_solve_kernel(con
     dout = d;
   }
   const int64_t base = I << g.m;
-  // 1. load + pull from neighbour slabs (outer modes with bit 0)
-  for (int l = tid; l < E; l += blockDim.x) {
-    double2 acc = Y[base + l];
-    for (int q = 0; q < g.n_outer; ++q)
-      if (!((I >> q) & 1)) acc = cfms(acc, t01[g.m + q], Y[base + ((int64_t)1 << (g.m + q)) + l]);
-    S[l] = acc;
+  // 1. load + pull from neighbour slabs (outer modes with bit 0), one slab at a time with all of
+  //    a thread's loads of that slab in flight (same per-entry order: own value, then q ascending)
+  constexpr int PER = 4096 / kBinSolveThreads;
+  double2 acc[PER];
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    const int l = tid + i * kBinSolveThreads;
+    acc[i] = l < E ? Y[base + l] : make_double2(0.0, 0.0);
+  }
+  for (int q = 0; q < g.n_outer; ++q) {
+    if ((I >> q) & 1) continue;  // CTA-uniform
+    const double2 c = t01[g.m + q];
+    const double2* nb = Y + base + ((int64_t)1 << (g.m + q));
+    double2 v[PER];
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const int l = tid + i * kBinSolveThreads;
+      v[i] = l < E ? nb[l] : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int i = 0; i < PER; ++i) acc[i] = cfms(acc[i], c, v[i]);
+  }
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    const int l = tid + i * kBinSolveThreads;
+    if (l < E) S[l] = acc[i];
   }
   __syncthreads();
   const double2 dO = dout;
@@ -79,7 +99,11 @@ __global__ void __launch_bounds__(kBinSolveThreads) binary_tile_solve_kernel(con
     __syncthreads();
   }
   // 3. store
-  for (int l = tid; l < E; l += blockDim.x) Y[base + l] = S[l];
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    const int l = tid + i * kBinSolveThreads;
+    if (l < E) Y[base + l] = S[l];
+  }
 }
 
 void binary_solve_plan_build(BinarySolvePlan& bp, int n_modes) {
