@@ -122,6 +122,7 @@ __global__ void __launch_bounds__(kSolveThreads) tile_level_kernel(const TileGeo
 
 
 #include "backsub_v2.cuh"
+#include "backsub_persist.cuh"
 
 // Tile shape: grow the smallest extents first (earlier modes win ties, keeping tiles contiguous
 // along mode 1) while prod b_j <= kMaxTile.
@@ -324,6 +325,46 @@ void solve_plan_build(SolvePlan& sp, int n_modes, const int64_t* dims, const int
       }
   }
 
+  // dataflow (persistent) solve tables: N = 3 cubic tiles
+  sp.persist = sp.v2 && n_modes == 3 && !far_items.empty();
+  std::vector<int> p_level_of, p_level_count, p_far_rel, p_far_dep, p_far_expected, p_push_slot, p_queue;
+  if (sp.persist) {
+    std::vector<int64_t> slot_of(ntiles);
+    for (int64_t s2 = 0; s2 < ntiles; ++s2) slot_of[tiles[s2]] = s2;
+    std::vector<int64_t> tstride(n_modes, 1);
+    for (int j = 1; j < n_modes; ++j) tstride[j] = tstride[j - 1] * g.nb[j - 1];
+    const int H = update_h(g.b[0]);
+    p_level_of.resize(ntiles);
+    p_level_count.resize(levels);
+    p_far_expected.assign(ntiles, 0);
+    p_push_slot.assign((size_t)ntiles * n_modes, -1);
+    for (int lv = 0; lv < levels; ++lv) {
+      p_level_count[lv] = (int)(sp.level_off[lv + 1] - sp.level_off[lv]);
+      for (int64_t s2 = sp.level_off[lv]; s2 < sp.level_off[lv + 1]; ++s2) p_level_of[s2] = lv;
+      for (int64_t f = sp.far_off[lv]; f < sp.far_off[lv + 1]; ++f) {
+        const int4 it = far_items[f];
+        p_far_rel.push_back((int)(f - sp.far_off[lv]));
+        p_far_dep.push_back((int)slot_of[tiles[it.x] + 2 * tstride[it.y]]);
+        p_far_expected[it.x] += H;
+      }
+    }
+    for (int64_t s2 = 0; s2 < ntiles; ++s2) {
+      int64_t r = tiles[s2];
+      for (int j = 0; j < n_modes; ++j) {
+        const int64_t I = r % g.nb[j];
+        r /= g.nb[j];
+        if (I > 0) p_push_slot[(size_t)s2 * n_modes + j] = (int)slot_of[tiles[s2] - tstride[j]];
+      }
+    }
+    // merged queue: far(lv + 1) CTA-items, then the diagonal tiles of hyperplane lv
+    for (int lv = 0; lv < levels; ++lv) {
+      if (lv + 1 < levels)
+        for (int64_t f = sp.far_off[lv + 1]; f < sp.far_off[lv + 2]; ++f)
+          for (int h = 0; h < H; ++h) p_queue.push_back(-(int)(f * H + h) - 1);
+      for (int64_t s2 = sp.level_off[lv]; s2 < sp.level_off[lv + 1]; ++s2) p_queue.push_back((int)s2);
+    }
+  }
+
   size_t bytes = ntiles * sizeof(int64_t) + (g.tile_entries + 3 * wf_levels + 2) * sizeof(int) +
                  (thr.size() + 8) * sizeof(uint16_t) + 64;
   bytes = (bytes + 15) / 16 * 16;
@@ -336,6 +377,10 @@ void solve_plan_build(SolvePlan& sp, int n_modes, const int64_t* dims, const int
   const size_t partial_off = bytes;
   const size_t tile_bytes = (size_t)g.tile_entries * sizeof(double2);
   bytes += (2 * (size_t)sp.max_far + 2 * (size_t)sp.max_near) * tile_bytes + 256;
+  bytes = (bytes + 15) / 16 * 16;
+  const size_t persist_off = bytes;
+  bytes += (p_level_of.size() + p_level_count.size() + p_far_rel.size() + p_far_dep.size() + p_far_expected.size() +
+            p_push_slot.size() + p_queue.size()) * sizeof(int) + 64;
   NDS_CUDA(cudaMalloc(&sp.pool, bytes));
   char* base = (char*)sp.pool;
   sp.d_tiles = (int64_t*)base;
@@ -361,6 +406,32 @@ void solve_plan_build(SolvePlan& sp, int n_modes, const int64_t* dims, const int
     NDS_CUDA(cudaMemcpy(sp.d_thr, thr.data(), thr.size() * sizeof(uint16_t), cudaMemcpyHostToDevice));
   if (!near_target.empty())
     NDS_CUDA(cudaMemcpy(sp.d_near_target, near_target.data(), near_target.size() * sizeof(int), cudaMemcpyHostToDevice));
+  if (sp.persist) {
+    int* q = (int*)(base + persist_off);
+    auto put = [&](const std::vector<int>& v, int*& dst) {
+      dst = q;
+      if (!v.empty()) NDS_CUDA(cudaMemcpy(q, v.data(), v.size() * sizeof(int), cudaMemcpyHostToDevice));
+      q += v.size();
+    };
+    put(p_level_of, sp.d_level_of);
+    put(p_level_count, sp.d_level_count);
+    put(p_far_rel, sp.d_far_rel);
+    put(p_far_dep, sp.d_far_dep);
+    put(p_far_expected, sp.d_far_expected);
+    put(p_push_slot, sp.d_push_slot);
+    put(p_queue, sp.d_queue);
+    sp.n_queue = (int64_t)p_queue.size();
+    sp.n_far_items = (int64_t)far_items.size();
+    const PersistCtr pc = PersistCtr::of(ntiles, levels);
+    sp.ctr_count = pc.total;
+    const size_t ring = (size_t)kRing * (sp.max_far + sp.max_near) * tile_bytes;
+    NDS_CUDA(cudaMalloc(&sp.persist_pool, ring + (size_t)pc.total * sizeof(int) + 256));
+    sp.d_far_ring = (double2*)sp.persist_pool;
+    sp.d_near_ring = sp.d_far_ring + (size_t)kRing * sp.max_far * g.tile_entries;
+    sp.d_ctr = (int*)(sp.d_near_ring + (size_t)kRing * sp.max_near * g.tile_entries);
+    NDS_CUDA(cudaMallocHost(&sp.h_err, sizeof(int)));
+    *sp.h_err = 0;
+  }
   if (sp.v2) {
     if (!far_items.empty())
       NDS_CUDA(cudaMemcpy(sp.d_far_items, far_items.data(), far_items.size() * sizeof(int4), cudaMemcpyHostToDevice));
@@ -380,11 +451,104 @@ void solve_plan_build(SolvePlan& sp, int n_modes, const int64_t* dims, const int
 void solve_plan_free(SolvePlan& sp) {
   if (sp.pool) cudaFree(sp.pool);
   sp.pool = nullptr;
+  if (sp.persist_pool) cudaFree(sp.persist_pool);
+  sp.persist_pool = nullptr;
+  if (sp.h_err) cudaFreeHost(sp.h_err);
+  sp.h_err = nullptr;
   for (auto e : sp.ev) cudaEventDestroy(e);
   sp.ev.clear();
   if (sp.s_crit) cudaStreamDestroy(sp.s_crit);
   if (sp.s_far) cudaStreamDestroy(sp.s_far);
   sp.s_crit = sp.s_far = nullptr;
+}
+
+// NDS_SOLVE=split|unified selects the dataflow (persistent-kernel) solve, an experimental A/B
+// path: measured on c1 it is not faster than the level-synchronous launches plus the head
+// overlap (split 4.40 ms solve vs 4.30; unified two-queue polling 37 ms), so it is off by default.
+bool persist_enabled() {
+  static const bool v = getenv("NDS_SOLVE") && (std::string(getenv("NDS_SOLVE")) == "split" ||
+                                                std::string(getenv("NDS_SOLVE")) == "unified");
+  return v;
+}
+
+bool backsub_is_dataflow(const SolvePlan& sp) { return sp.persist && persist_enabled(); }
+
+static int persist_launch(const SolvePlan& sp, const double2* t_pool, double2* c, cudaStream_t stream, Recorder* rec) {
+  if (*sp.h_err) throw Error(NDS_ERR_CUDA, "dataflow solve watchdog fired on a previous call (dependency wait timed out)");
+  const TileGeom& g = sp.geom;
+  const int b = g.b[0];
+  const UpdCfg uc = update_cfg_for(b);
+  using FarK = void (*)(const PersistArgs);
+  const FarK fark = far_persist_kernel<2, 2, true, 1, 3, 2>;
+  const FarK diagk = diag_persist_kernel<3, 16, 256>;
+  static bool attr = false;
+  if (!attr) {
+    NDS_CUDA(cudaFuncSetAttribute(fark, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)update_smem_bytes(b)));
+    NDS_CUDA(cudaFuncSetAttribute(diagk, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024));
+    attr = true;
+  }
+  if (uc.h != 2 || uc.bk != 8 || b != 16) throw Error(NDS_ERR_OTHER, "dataflow solve needs the 16-row 3M update");
+  PersistArgs a{};
+  a.g = g;
+  a.T = t_pool;
+  a.Y = c;
+  a.tiles = sp.d_tiles;
+  a.level_of = sp.d_level_of;
+  a.level_count = sp.d_level_count;
+  a.tile_ranges = sp.d_tile_ranges;
+  a.near_target = sp.d_near_target;
+  a.push_slot = sp.d_push_slot;
+  a.far_items = sp.d_far_items;
+  a.far_rel = sp.d_far_rel;
+  a.far_dep = sp.d_far_dep;
+  a.far_expected = sp.d_far_expected;
+  a.n_tiles = sp.level_off.back();
+  a.H = uc.h;
+  a.n_far_ctas = sp.n_far_items * uc.h;
+  a.max_far = sp.max_far;
+  a.max_near = sp.max_near;
+  a.far_ring = sp.d_far_ring;
+  a.near_ring = sp.d_near_ring;
+  a.ctr = sp.d_ctr;
+  const int L = sp.levels;
+  cudaEvent_t ev_start = sp.ev[2 * L], ev_end = sp.ev[2 * L + 1], ev_far_end = sp.ev[0];
+  NDS_CUDA(cudaMemsetAsync(sp.d_ctr, 0, (size_t)sp.ctr_count * sizeof(int), stream));
+  NDS_CUDA(cudaEventRecord(ev_start, stream));
+  NDS_CUDA(cudaStreamWaitEvent(sp.s_crit, ev_start, 0));
+  NDS_CUDA(cudaStreamWaitEvent(sp.s_far, ev_start, 0));
+  if (rec) rec->mark(stream, -1, 0);
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  a.queue = sp.d_queue;
+  a.n_queue = sp.n_queue;
+  static const bool split = std::string(getenv("NDS_SOLVE")) == "split";
+  if (split) {
+    // at most one CTA of each kind per SM: both always keep resident CTAs (no deadlock)
+    const int gd = (int)std::min<int64_t>(sms, a.n_tiles);
+    const int gf = (int)std::min<int64_t>(sms, a.n_far_ctas);
+    diagk<<<gd, 256, lines_smem_bytes(3, 16), sp.s_crit>>>(a);
+    NDS_LAUNCH_CHECK();
+    fark<<<gf, kUpdThreads, update_smem_bytes(b), sp.s_far>>>(a);
+    NDS_LAUNCH_CHECK();
+    NDS_CUDA(cudaEventRecord(ev_far_end, sp.s_far));
+    NDS_CUDA(cudaStreamWaitEvent(sp.s_crit, ev_far_end, 0));
+  } else {
+    const FarK solvek = solve_persist_kernel<3, 16, 256>;
+    static bool attr2 = false;
+    if (!attr2) {
+      NDS_CUDA(cudaFuncSetAttribute(solvek, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024));
+      attr2 = true;
+    }
+    const size_t smem = std::max(lines_smem_bytes(3, 16), update_smem_bytes(b));
+    const int grid = (int)std::min<int64_t>(2 * sms, a.n_queue);
+    solvek<<<grid, 256, smem, sp.s_crit>>>(a);
+    NDS_LAUNCH_CHECK();
+  }
+  NDS_CUDA(cudaMemcpyAsync(sp.h_err, sp.d_ctr + 2, sizeof(int), cudaMemcpyDeviceToHost, sp.s_crit));
+  NDS_CUDA(cudaEventRecord(ev_end, sp.s_crit));
+  NDS_CUDA(cudaStreamWaitEvent(stream, ev_end, 0));
+  if (rec) rec->mark(stream, kBacksubPersistent, L);
+  return 2;
 }
 
 int backsub_launch(const SolvePlan& sp, const double2* t_pool, double2* c, cudaStream_t stream, Recorder* rec,
@@ -406,6 +570,7 @@ int backsub_launch(const SolvePlan& sp, const double2* t_pool, double2* c, cudaS
   }
   const TileGeom& g = sp.geom;
   int launches = 0;
+  if (sp.persist && persist_enabled()) return persist_launch(sp, t_pool, c, stream, rec);
   if (!sp.v2) {
     const size_t smem = (size_t)g.tile_entries * sizeof(double2);
     for (int lv = 0; lv < sp.levels; ++lv) {

@@ -35,9 +35,10 @@ __device__ __forceinline__ void dmma_bs(double& c0, double& c1, double a, double
 // computed once. Each warp owns RB x CB fragments (8x8) and reuses its A/B fragments across
 // them. The partial is written in tile-local column-major order for the diagonal kernel.
 template <int RB, int CB, bool M3, int KM, int ST, int H>
-__global__ void __launch_bounds__(kUpdThreads, (M3 && H == 1) ? 1 : 2)
-    tile_update_kernel(const TileGeom g, const double2* __restrict__ T, const int64_t* __restrict__ tiles,
-                       const int4* __restrict__ items, double2* __restrict__ partial, const double2* __restrict__ Y) {
+__device__ __forceinline__ void update_body(const TileGeom& g, const double2* __restrict__ T,
+                                            const int64_t* __restrict__ tiles, const int4 it, const int half,
+                                            double2* __restrict__ out, const double2* __restrict__ Y,
+                                            double2* __restrict__ sm) {
   constexpr int BJ = 8 * RB;
   constexpr int TCOLS = 4096 / BJ;       // columns of the tile
   constexpr int COLS = TCOLS / H;        // columns of this CTA (H CTAs per item)
@@ -46,11 +47,8 @@ __global__ void __launch_bounds__(kUpdThreads, (M3 && H == 1) ? 1 : 2)
   constexpr int ALD = BK <= 8 ? 12 : BK + 4;  // = 4 mod 8 -> conflict-free A fragments
   constexpr int SL = 8 * KM / H;         // load slots per thread and stage
   static_assert(CB * 8 * (kUpdThreads / 32) == COLS && BK % 4 == 0 && BJ * BK <= kUpdThreads, "tile shape");
-  extern __shared__ __align__(16) double2 sm[];
   __shared__ int64_t so[NDS_MAX_MODES];
   __shared__ int64_t s_base;
-  const int4 it = items[blockIdx.x / H];
-  const int half = blockIdx.x % H;
   const int j = it.y, kb = it.z, ke = it.w;
   const int N = g.n_modes;
   int64_t* colg = (int64_t*)sm;  // global offset of column c
@@ -191,7 +189,6 @@ __global__ void __launch_bounds__(kUpdThreads, (M3 && H == 1) ? 1 : 2)
     }
   }
   cp_wait0_bs();
-  double2* out = partial + (int64_t)(blockIdx.x / H) * 4096;
   const int bsj = g.bstride[j];
 #pragma unroll
   for (int r = 0; r < RB; ++r)
@@ -209,6 +206,15 @@ __global__ void __launch_bounds__(kUpdThreads, (M3 && H == 1) ? 1 : 2)
         out[row * bsj + coll[c + 1]] = make_double2(cre[r][q][1], cim[r][q][1]);
       }
     }
+}
+
+template <int RB, int CB, bool M3, int KM, int ST, int H>
+__global__ void __launch_bounds__(kUpdThreads, (M3 && H == 1) ? 1 : 2)
+    tile_update_kernel(const TileGeom g, const double2* __restrict__ T, const int64_t* __restrict__ tiles,
+                       const int4* __restrict__ items, double2* __restrict__ partial, const double2* __restrict__ Y) {
+  extern __shared__ __align__(16) double2 sm[];
+  update_body<RB, CB, M3, KM, ST, H>(g, T, tiles, items[blockIdx.x / H], (int)(blockIdx.x % H),
+                                     partial + (int64_t)(blockIdx.x / H) * 4096, Y, sm);
 }
 
 // n terms tp[i grp] * sp[i ss], i < n, into four independent accumulators (loads batched).
@@ -490,22 +496,21 @@ struct LinePad {
 // (3M DMMA; near_target[slot N + m] = that item's index at the next level, -1 if none) — which
 // replaces the separate near-update launch on the critical path.
 template <int N, int B, int NT, bool PUSH, bool T2REG>
-__global__ void __launch_bounds__(NT, T2REG ? 1 : 2)
-    tile_diag_lines_kernel(const TileGeom g, const double2* __restrict__ T, const int64_t* __restrict__ tiles,
-                           const int4* __restrict__ tile_ranges, const double2* __restrict__ far_partial,
-                           const double2* __restrict__ near_partial, const int* __restrict__ near_target,
-                           double2* __restrict__ near_out, double2* __restrict__ Y) {
+__device__ __forceinline__ void diag_lines_body(const TileGeom& g, const double2* __restrict__ T, const int64_t tile,
+                                                const int4 tr, const double2* __restrict__ far_partial,
+                                                const double2* __restrict__ near_partial,
+                                                const int* __restrict__ near_target, double2* __restrict__ near_out,
+                                                double2* __restrict__ Y, double2* __restrict__ sm) {
   constexpr int E = 4096;
   constexpr int LB = B == 16 ? 4 : 3;
   constexpr int WL = N * (B - 1) + 1;
   static_assert((1 << (LB * N)) == E && E / B == NT, "one thread per mode-1 line of a cubic 4096-entry tile");
   using PS = LinePad<N, B>;
-  extern __shared__ __align__(16) double2 sm[];
   __shared__ int64_t so[N];
   __shared__ int64_t st[N];
   const int tid = threadIdx.x;
   if (tid == 0) {
-    int64_t t = tiles[blockIdx.x];
+    int64_t t = tile;
     for (int m = 0; m < N; ++m) {
       const int64_t I = t % g.nb[m];
       t /= g.nb[m];
@@ -530,7 +535,7 @@ __global__ void __launch_bounds__(NT, T2REG ? 1 : 2)
       }
     }
   }
-  const int4 tr = tile_ranges[blockIdx.x];  // {far first, far count, near first, near count}
+  // tr = {far first, far count, near first, near count}
   {
     constexpr int PER = E / NT;
     double2 v[PER];
@@ -545,12 +550,12 @@ __global__ void __launch_bounds__(NT, T2REG ? 1 : 2)
     for (int p = 0; p < tr.y; ++p) {
       const double2* pp = far_partial + (int64_t)(tr.x + p) * E + tid;
 #pragma unroll
-      for (int i = 0; i < PER; ++i) v[i] = csub(v[i], pp[i * NT]);
+      for (int i = 0; i < PER; ++i) v[i] = csub(v[i], __ldcg(pp + i * NT));
     }
     for (int p = 0; p < tr.w; ++p) {
       const double2* pp = near_partial + (int64_t)(tr.z + p) * E + tid;
 #pragma unroll
-      for (int i = 0; i < PER; ++i) v[i] = csub(v[i], pp[i * NT]);
+      for (int i = 0; i < PER; ++i) v[i] = csub(v[i], __ldcg(pp + i * NT));
     }
 #pragma unroll
     for (int i = 0; i < PER; ++i) S[PS::pad(tid + i * NT)] = v[i];
@@ -645,7 +650,7 @@ __global__ void __launch_bounds__(NT, T2REG ? 1 : 2)
     };
 #pragma unroll 1
     for (int m = 0; m < N; ++m) {
-      const int tgt = near_target[(int64_t)blockIdx.x * N + m];
+      const int tgt = near_target[m];
       if (tgt < 0) continue;  // CTA-uniform
       const double2* Tm = T + g.toff[m];
       const int64_t nm = g.dims[m], oj = so[m];
@@ -689,6 +694,18 @@ __global__ void __launch_bounds__(NT, T2REG ? 1 : 2)
       }
     }
   }
+}
+
+template <int N, int B, int NT, bool PUSH, bool T2REG>
+__global__ void __launch_bounds__(NT, T2REG ? 1 : 2)
+    tile_diag_lines_kernel(const TileGeom g, const double2* __restrict__ T, const int64_t* __restrict__ tiles,
+                           const int4* __restrict__ tile_ranges, const double2* __restrict__ far_partial,
+                           const double2* __restrict__ near_partial, const int* __restrict__ near_target,
+                           double2* __restrict__ near_out, double2* __restrict__ Y) {
+  extern __shared__ __align__(16) double2 sm[];
+  diag_lines_body<N, B, NT, PUSH, T2REG>(g, T, tiles[blockIdx.x], tile_ranges[blockIdx.x], far_partial, near_partial,
+                                         near_target ? near_target + (int64_t)blockIdx.x * N : nullptr, near_out, Y,
+                                         sm);
 }
 
 using LinesKernel = void (*)(const TileGeom, const double2*, const int64_t*, const int4*, const double2*,

@@ -375,6 +375,7 @@ int execute(nds_plan* p, const double2* b, double2* x, double2* work, cudaEvent_
   const ModeView lastv = nds::mode_view(p->n_modes, p->dims, passes.back().mode);
   static const bool head_env = !(getenv("NDS_HEAD") && std::string(getenv("NDS_HEAD")) == "0");
   const bool head = head_env && !p->fast_path && p->solver && !p->solver->binary && p->solver->sp.v2 &&
+                    !nds::backsub_is_dataflow(p->solver->sp) &&
                     p->n_modes == 3 && passes.back().group < 0 && passes.back().mode == p->n_modes &&
                     lastv.outer == 1 && nds::gemm_rowm_ok(lastv);
   const int last_fwd = head ? N - 1 : N;

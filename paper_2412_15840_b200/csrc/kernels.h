@@ -109,6 +109,21 @@ struct SolvePlan {
   double2* d_near_partial2 = nullptr;  // push mode: near partials double-buffered by level parity
   int64_t max_far = 0, max_near = 0;
   cudaStream_t s_crit = nullptr, s_far = nullptr;
+  // dataflow (persistent-kernel) solve, N = 3: per-slot / per-item tables, partial rings, counters
+  bool persist = false;
+  int* d_level_of = nullptr;
+  int* d_level_count = nullptr;
+  int* d_far_rel = nullptr;
+  int* d_far_dep = nullptr;
+  int* d_far_expected = nullptr;
+  int* d_push_slot = nullptr;
+  int* d_queue = nullptr;  // merged dataflow work order
+  int64_t n_far_items = 0, ctr_count = 0, n_queue = 0;
+  void* persist_pool = nullptr;
+  double2* d_far_ring = nullptr;
+  double2* d_near_ring = nullptr;
+  int* d_ctr = nullptr;
+  int* h_err = nullptr;  // pinned: watchdog flag of the last dataflow solve
   std::vector<cudaEvent_t> ev;  // diag(lv), far(lv), start, end
 };
 
@@ -149,6 +164,9 @@ struct HeadSync {
 // In-place Y over C. Returns kernels launched.
 int backsub_launch(const SolvePlan& sp, const double2* t_pool, double2* c, cudaStream_t stream,
                    Recorder* rec = nullptr, const HeadSync* head = nullptr);
+// True when backsub_launch runs the dataflow (persistent-kernel) solve for this plan, which does
+// not honour HeadSync.
+bool backsub_is_dataflow(const SolvePlan& sp);
 
 // ---- matrix functions (ODE propagator) -----------------------------------------------------
 // exp(t T_m) by the Parlett recurrence, one CTA per listed mode: T_m at t_pool + toff[m]
