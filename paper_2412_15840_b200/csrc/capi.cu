@@ -161,6 +161,18 @@ void upload_factors(nds_ctx* ctx, nds::FactorSet& f, int n_modes, const int64_t*
   nds::Geom& g = f.geom;
   g.n_modes = n_modes;
   g.total = 1;
+  // host -> pinned staging copies, gathered and run OpenMP-parallel in 256 KB pieces
+  struct Piece {
+    void* dst;
+    const void* src;
+    size_t bytes;
+  };
+  std::vector<Piece> pieces;
+  auto add_copy = [&](void* dst, const void* src, size_t bytes) {
+    constexpr size_t kPiece = 256 * 1024;
+    for (size_t o = 0; o < bytes; o += kPiece)
+      pieces.push_back({(char*)dst + o, (const char*)src + o, std::min(kPiece, bytes - o)});
+  };
   int64_t off = 0, soff = 0, toff = 0, doff = 0;
   for (int j = 0; j < n_modes; ++j) {
     const int64_t n = dims[j];
@@ -168,7 +180,7 @@ void upload_factors(nds_ctx* ctx, nds::FactorSet& f, int n_modes, const int64_t*
     g.strides[j] = g.total;
     g.total *= n;
     if (u) {
-      std::memcpy(stage + soff, u[j], (size_t)(n * n) * sizeof(double2));
+      add_copy(stage + soff, u[j], (size_t)(n * n) * sizeof(double2));
       f.u_row[j] = f.pool + off;
       f.u_col[j] = f.pool + off + n * n;
       f.uh_row[j] = f.pool + off + 2 * n * n;
@@ -177,15 +189,18 @@ void upload_factors(nds_ctx* ctx, nds::FactorSet& f, int n_modes, const int64_t*
       soff += n * n;
     }
   }
-  double2* raw = f.pool + n_u + n_t + n_d;
-  if (t) {
-    f.t_pool = f.pool + off;
+  if (t)
     for (int j = 0; j < n_modes; ++j) {
       const int64_t n = dims[j];
       g.toff[j] = toff;
-      std::memcpy(stage + soff + toff, t[j], (size_t)(n * n) * sizeof(double2));
+      add_copy(stage + soff + toff, t[j], (size_t)(n * n) * sizeof(double2));
       toff += n * n;
     }
+#pragma omp parallel for schedule(dynamic, 1) if (pieces.size() > 4)
+  for (size_t i = 0; i < pieces.size(); ++i) std::memcpy(pieces[i].dst, pieces[i].src, pieces[i].bytes);
+  double2* raw = f.pool + n_u + n_t + n_d;
+  if (t) {
+    f.t_pool = f.pool + off;
     f.diag_pool = f.pool + off + toff;
     for (int j = 0; j < n_modes; ++j) {
       const int64_t n = dims[j];
@@ -496,7 +511,34 @@ float ev_ms(cudaEvent_t a, cudaEvent_t b) {
   return ms;
 }
 
-void execute_host_impl(nds_plan* p, const nds_z* hb, nds_z* hx, nds_report* rep) {
+// Copy/compute overlap: the passes before the last one act independently on contiguous chunks
+// of the slowest modes (those of the last pass), so B streams in chunk by chunk under them and
+// X streams out under the inverse (whose last-pass-first order keeps the per-chunk passes last).
+int chunk_count(const nds_plan* p) {
+  const std::vector<XPass> passes = transform_passes(p);
+  if (passes.size() < 2) return 1;
+  const ModeView lastv = nds::mode_view(p->n_modes, p->dims, passes.back().mode);
+  const int64_t outer_last = p->total / lastv.inner;  // product of the last pass's modes and beyond
+  for (int k : {8, 4, 2})
+    if (outer_last % k == 0 && p->total / k >= (1 << 16)) return k;
+  return 1;
+}
+
+// Start the H2D of the first `count` chunks of B (ev[4] = start) before the plan exists, so the
+// host-side plan setup overlaps the link; the rest is issued after the factor upload.
+void prefetch_chunks(nds_ctx* ctx, const nds_z* hb, int64_t total, int K, int count) {
+  ensure_ws(ctx, total);
+  const int64_t chunk = total / K;
+  NDS_CUDA(cudaEventRecord(ctx->ev[4], ctx->stream));
+  NDS_CUDA(cudaStreamWaitEvent(ctx->copy, ctx->ev[4], 0));
+  for (int k = 0; k < count; ++k) {
+    NDS_CUDA(cudaMemcpyAsync(ctx->ws[0] + k * chunk, hb + k * chunk, (size_t)chunk * sizeof(double2),
+                             cudaMemcpyHostToDevice, ctx->copy));
+    NDS_CUDA(cudaEventRecord(ctx->cev[k], ctx->copy));
+  }
+}
+
+void execute_host_impl(nds_plan* p, const nds_z* hb, nds_z* hx, nds_report* rep, int prefetched = 0) {
   if (!hb || !hx) throw Error(NDS_ERR_INVALID, "null tensor pointer");
   nds_ctx* ctx = p->ctx;
   ensure_device(ctx);
@@ -507,19 +549,7 @@ void execute_host_impl(nds_plan* p, const nds_z* hb, nds_z* hx, nds_report* rep)
   double2* W = ctx->ws[1];
   const std::vector<XPass> passes = transform_passes(p);
   const int np = (int)passes.size();
-  // Copy/compute overlap: the passes before the last one act independently on contiguous chunks
-  // of the slowest modes (those of the last pass), so B streams in chunk by chunk under them and
-  // X streams out under the inverse (whose last-pass-first order keeps the per-chunk passes last).
-  int K = 1;
-  if (np >= 2) {
-    const ModeView lastv = nds::mode_view(p->n_modes, p->dims, passes.back().mode);
-    const int64_t outer_last = p->total / lastv.inner;  // product of the last pass's modes and beyond
-    for (int k : {8, 4, 2})
-      if (outer_last % k == 0 && p->total / k >= (1 << 16)) {
-        K = k;
-        break;
-      }
-  }
+  const int K = chunk_count(p);
   int launches = 0;
   if (K == 1) {
     NDS_CUDA(cudaEventRecord(ctx->ev[4], s));
@@ -531,9 +561,11 @@ void execute_host_impl(nds_plan* p, const nds_z* hb, nds_z* hx, nds_report* rep)
     cudaStream_t cs = ctx->copy;
     const int64_t chunk = p->total / K;
     const size_t cbytes = (size_t)chunk * sizeof(double2);
-    NDS_CUDA(cudaEventRecord(ctx->ev[4], s));
-    NDS_CUDA(cudaStreamWaitEvent(cs, ctx->ev[4], 0));
-    for (int k = 0; k < K; ++k) {
+    if (prefetched == 0) {
+      NDS_CUDA(cudaEventRecord(ctx->ev[4], s));
+      NDS_CUDA(cudaStreamWaitEvent(cs, ctx->ev[4], 0));
+    }
+    for (int k = prefetched; k < K; ++k) {
       NDS_CUDA(cudaMemcpyAsync(X + k * chunk, hb + k * chunk, cbytes, cudaMemcpyHostToDevice, cs));
       NDS_CUDA(cudaEventRecord(ctx->cev[k], cs));
     }
@@ -1154,10 +1186,28 @@ int nds_solve_schur(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z*
   if (!ctx) return NDS_ERR_INVALID;
   return guarded(ctx, [&] {
     const auto t0 = Clock::now();
+    const int64_t total = checked_total(n_modes, dims, 2);
+    if (!b || !x) throw Error(NDS_ERR_INVALID, "null tensor pointer");
+    ensure_device(ctx);
+    // chunks of B start streaming in while the host sets the plan up (factor staging, singular
+    // scan); only the first one, so the factor upload does not queue behind the whole tensor
+    nds_plan probe;
+    probe.n_modes = n_modes;
+    std::memcpy(probe.dims, dims, n_modes * sizeof(int64_t));
+    probe.total = total;
+    probe.groups = nds::plan_binary_groups(n_modes, dims);
+    const int K = chunk_count(&probe);
+    const int pre = K > 1 && (const void*)b != (const void*)x ? 1 : 0;
+    if (pre) prefetch_chunks(ctx, b, total, K, pre);
     nds_plan* p = nullptr;
-    plan_create_impl(ctx, n_modes, dims, u, t, singular_tol, flags, &p, sing);
     try {
-      execute_host_impl(p, b, x, rep);
+      plan_create_impl(ctx, n_modes, dims, u, t, singular_tol, flags, &p, sing);
+    } catch (...) {
+      if (pre) cudaStreamSynchronize(ctx->copy);  // b must not be read after we return
+      throw;
+    }
+    try {
+      execute_host_impl(p, b, x, rep, pre);
     } catch (...) {
       plan_destroy_impl(p);
       throw;
