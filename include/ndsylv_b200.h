@@ -223,6 +223,29 @@ int nds_propagate(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z* c
 int nds_rk4(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z* const* a, const nds_z* forcing,
             const nds_z* initial, double time, double dt, int64_t max_steps, nds_z* x);
 
+/* ---- NDT1 tensor files and the seeded generator -------------------------- */
+
+/* Header of an NDT1 file (tensor_file.hpp:9-15): order and extents (dims has room for 64).
+ * NDS_ERR_FILE on I/O failure, bad magic, unsupported version, invalid or overflowing extents. */
+int nds_tensor_file_info(const char* path, int* n_modes, int64_t* dims);
+/* ndsylv::read_tensor (tensor_file.cpp:67-96) into a host buffer of the file's extents (which
+ * must equal n_modes / dims); a short or over-long payload is NDS_ERR_FILE. */
+int nds_read_tensor(const char* path, int n_modes, const int64_t* dims, nds_z* out);
+/* ndsylv::write_tensor (tensor_file.cpp:48-65). */
+int nds_write_tensor(const char* path, int n_modes, const int64_t* dims, const nds_z* data);
+/* The same between a file and DEVICE memory, streamed through double-buffered pinned chunks so
+ * disk reads overlap the host->device copies (and device->host copies overlap disk writes);
+ * for multi-GiB tensors. Synchronous. */
+int nds_read_tensor_dev(nds_ctx* ctx, const char* path, int n_modes, const int64_t* dims, nds_z* d_out);
+int nds_write_tensor_dev(nds_ctx* ctx, const char* path, int n_modes, const int64_t* dims, const nds_z* d_in);
+/* ndsylv::random_problem (rng.hpp:67, rng.cpp:18-25): A_1..A_N then X_true from one xoshiro256++
+ * stream (uniform [0,1) + i[0,1)), B = sum_j A_j x_j X_true (computed on the GPU). */
+int nds_random_problem(nds_ctx* ctx, int n_modes, const int64_t* dims, uint64_t seed, nds_z* const* a,
+                       nds_z* x_true, nds_z* b);
+/* ndsylv::random_ode_system (rng.hpp:70, rng.cpp:27-33): A_1..A_N, forcing, initial state. Host. */
+int nds_random_ode_system(int n_modes, const int64_t* dims, uint64_t seed, nds_z* const* a, nds_z* forcing,
+                          nds_z* initial);
+
 /* ---- harness utility ------------------------------------------------------------------ */
 /* Seeded standard normals (Box–Muller over splitmix64 counters, stream-separated), host
  * side, OpenMP-parallel and order-independent: out[i] for i in [0, count). */

@@ -260,6 +260,9 @@ class Ref:
         L.ref_propagate.argtypes = [C.c_int, _i64p, _dpp, _dp, _dp, C.c_double, C.c_int, _dp, C.POINTER(_ReportRef),
                                     _i64p, _dp]
         L.ref_rk4.argtypes = [C.c_int, _i64p, _dpp, _dp, _dp, C.c_double, C.c_double, C.c_int64, _dp]
+        L.ref_write_tensor.argtypes = [C.c_char_p, C.c_int, _i64p, _dp]
+        L.ref_read_tensor.argtypes = [C.c_char_p, C.POINTER(C.c_int), _i64p, _dp, C.c_int64]
+        L.ref_random_ode_system.argtypes = [C.c_int, _i64p, C.c_uint64, _dpp, _dp, _dp]
 
     def _check(self, rc, bad=None, den=None):
         if rc:
@@ -377,3 +380,24 @@ class Ref:
         self._check(self.lib.ref_rk4(f.ndim, _dims(f.shape), ap, _ptr(f), _ptr(x0), float(t), float(dt),
                                      int(max_steps), _ptr(x)))
         return x
+
+    def write_tensor(self, path, x):
+        x = fortran(x)
+        self._check(self.lib.ref_write_tensor(path.encode(), x.ndim, _dims(x.shape), _ptr(x)))
+
+    def read_tensor(self, path):
+        n = C.c_int()
+        dims = (C.c_int64 * 64)()
+        self._check(self.lib.ref_read_tensor(path.encode(), C.byref(n), dims, None, 0))
+        shape = tuple(dims[j] for j in range(n.value))
+        out = np.empty(shape, dtype=np.complex128, order="F")
+        self._check(self.lib.ref_read_tensor(path.encode(), C.byref(n), dims, _ptr(out), out.size))
+        return out
+
+    def random_ode_system(self, dims, seed):
+        a = [np.empty((n, n), dtype=np.complex128, order="F") for n in dims]
+        ap = (_dp * len(a))(*[_ptr(m) for m in a])
+        f = np.empty(tuple(dims), dtype=np.complex128, order="F")
+        x0 = np.empty_like(f, order="F")
+        self._check(self.lib.ref_random_ode_system(len(dims), _dims(dims), int(seed), ap, _ptr(f), _ptr(x0)))
+        return a, f, x0

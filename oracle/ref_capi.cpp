@@ -19,6 +19,7 @@
 #include "ndsylv/kron.hpp"
 #include "ndsylv/ode.hpp"
 #include "ndsylv/schur.hpp"
+#include "ndsylv/tensor_file.hpp"
 #include "ndsylv/rng.hpp"
 #include "ndsylv/sylvester.hpp"
 
@@ -295,6 +296,30 @@ int ref_rk4(int n_modes, const std::int64_t* dims, const double* const* a, const
             const double* initial, double time, double dt, std::int64_t max_steps, double* x) {
   return guarded([&] {
     tensor_to(rk4_reference(system_from(n_modes, dims, a, forcing, initial), time, dt, max_steps), x);
+  });
+}
+
+// ndsylv::write_tensor / read_tensor (tensor_file.hpp)
+int ref_write_tensor(const char* path, int n_modes, const std::int64_t* dims, const double* data) {
+  return guarded([&] { write_tensor(path, tensor_from(n_modes, dims, data)); });
+}
+int ref_read_tensor(const char* path, int* n_modes, std::int64_t* dims, double* out, std::int64_t cap) {
+  return guarded([&] {
+    const NDTensor t = read_tensor(path);
+    *n_modes = t.order();
+    for (int j = 0; j < t.order(); ++j) dims[j] = t.dims[j];
+    if (out && t.size() <= cap) tensor_to(t, out);
+  });
+}
+
+// ndsylv::random_ode_system (rng.hpp:70)
+int ref_random_ode_system(int n_modes, const std::int64_t* dims, std::uint64_t seed, double* const* a, double* forcing,
+                          double* initial) {
+  return guarded([&] {
+    const OdeSystem s = random_ode_system(dims_of(n_modes, dims), seed);
+    for (int j = 0; j < n_modes; ++j) matrix_to(s.coefficients[j], a[j]);
+    tensor_to(s.forcing, forcing);
+    tensor_to(s.initial, initial);
   });
 }
 

@@ -53,7 +53,8 @@ EXPORTED = [
     "nds_plan_profile_begin", "nds_plan_profile_end",
     "nds_dev_mode_product", "nds_dev_mode_update", "nds_dev_back_substitute", "nds_dev_residual",
     "nds_triangular_exp", "nds_ode_create", "nds_ode_destroy", "nds_ode_at", "nds_ode_at_dev", "nds_propagate",
-    "nds_rk4", "nds_randn",
+    "nds_rk4", "nds_tensor_file_info", "nds_read_tensor", "nds_write_tensor", "nds_read_tensor_dev",
+    "nds_write_tensor_dev", "nds_random_problem", "nds_random_ode_system", "nds_randn",
 ]
 
 
@@ -74,6 +75,10 @@ class SingularOperatorError(NdsError):
 
 class ConvergenceError(NdsError):
     pass
+
+
+class TensorFileError(NdsError):
+    """TensorFileError (types.hpp): NDT1 I/O or format error."""
 
 
 class NonFiniteStateError(NdsError):
@@ -179,6 +184,13 @@ def load_library(path: str = LIB_PATH):
     L.nds_propagate.argtypes = [_vp, C.c_int, _i64p, _vp, _vp, _vp, C.c_double, C.c_double, C.c_uint, _vp,
                                 C.POINTER(_Report), C.POINTER(_Singular)]
     L.nds_rk4.argtypes = [_vp, C.c_int, _i64p, _vp, _vp, _vp, C.c_double, C.c_double, C.c_int64, _vp]
+    L.nds_tensor_file_info.argtypes = [C.c_char_p, C.POINTER(C.c_int), _i64p]
+    L.nds_read_tensor.argtypes = [C.c_char_p, C.c_int, _i64p, _vp]
+    L.nds_write_tensor.argtypes = [C.c_char_p, C.c_int, _i64p, _vp]
+    L.nds_read_tensor_dev.argtypes = [_vp, C.c_char_p, C.c_int, _i64p, _vp]
+    L.nds_write_tensor_dev.argtypes = [_vp, C.c_char_p, C.c_int, _i64p, _vp]
+    L.nds_random_problem.argtypes = [_vp, C.c_int, _i64p, C.c_uint64, _vp, _vp, _vp]
+    L.nds_random_ode_system.argtypes = [C.c_int, _i64p, C.c_uint64, _vp, _vp, _vp]
     L.nds_randn.argtypes = [C.c_uint64, C.c_uint64, C.c_int64, _vp]
     _lib = L
     return L
@@ -225,6 +237,8 @@ def _raise(code, msg, sing=None):
         raise DeviceError(code, msg)
     if code == ERR_NONFINITE:
         raise NonFiniteStateError(code, msg)
+    if code == ERR_FILE:
+        raise TensorFileError(code, msg)
     raise NdsError(code, msg)
 
 
@@ -240,6 +254,47 @@ def schur_flop_estimate(dims) -> int:
     if v < 0:
         raise OverflowError("flop estimate overflows int64")
     return v
+
+
+# ---- NDT1 files and the reference generator (tensor_file.hpp, rng.hpp) ------------------------
+
+def _noctx_check(rc):
+    if rc:
+        _raise(rc, load_library().nds_last_error(None).decode())
+
+
+def tensor_file_info(path: str):
+    """Extents of an NDT1 file."""
+    n = C.c_int()
+    dims = (C.c_int64 * 64)()
+    _noctx_check(load_library().nds_tensor_file_info(path.encode(), C.byref(n), dims))
+    return tuple(dims[j] for j in range(n.value))
+
+
+def read_tensor(path: str) -> np.ndarray:
+    """ndsylv::read_tensor (tensor_file.cpp:67-96)."""
+    dims = tensor_file_info(path)
+    out = np.empty(dims, dtype=np.complex128, order="F")
+    _noctx_check(load_library().nds_read_tensor(path.encode(), len(dims), _dims(dims), out.ctypes.data))
+    return out
+
+
+def write_tensor(path: str, x) -> None:
+    """ndsylv::write_tensor (tensor_file.cpp:48-65)."""
+    x = _f(x)
+    _noctx_check(load_library().nds_write_tensor(path.encode(), x.ndim, _dims(x.shape), x.ctypes.data))
+
+
+def random_ode_system(dims, seed: int):
+    """ndsylv::random_ode_system (rng.cpp:27-33): (A_list, forcing, initial)."""
+    dims = tuple(int(d) for d in dims)
+    a = [np.empty((n, n), dtype=np.complex128, order="F") for n in dims]
+    f = np.empty(dims, dtype=np.complex128, order="F")
+    x0 = np.empty_like(f, order="F")
+    ap = (_vp * len(a))(*[m.ctypes.data for m in a])
+    _noctx_check(load_library().nds_random_ode_system(len(dims), _dims(dims), int(seed), ap, f.ctypes.data,
+                                                      x0.ctypes.data))
+    return a, f, x0
 
 
 def randn(seed: int, stream: int, count: int) -> np.ndarray:
@@ -555,6 +610,23 @@ class Context:
         self._check(self.lib.nds_rk4(self.h, f.ndim, _dims(f.shape), ap, f.ctypes.data, x0.ctypes.data, float(t),
                                      float(dt), int(max_steps), x.ctypes.data))
         return x
+
+    def random_problem(self, dims, seed: int):
+        """ndsylv::random_problem (rng.cpp:18-25): (A_list, x_true, b), b computed on the GPU."""
+        dims = tuple(int(d) for d in dims)
+        a = [np.empty((n, n), dtype=np.complex128, order="F") for n in dims]
+        x = np.empty(dims, dtype=np.complex128, order="F")
+        b = np.empty_like(x, order="F")
+        ap = (_vp * len(a))(*[m.ctypes.data for m in a])
+        self._check(self.lib.nds_random_problem(self.h, len(dims), _dims(dims), int(seed), ap, x.ctypes.data,
+                                                b.ctypes.data))
+        return a, x, b
+
+    def read_tensor_dev(self, path: str, dims, d_out: int):
+        self._check(self.lib.nds_read_tensor_dev(self.h, path.encode(), len(dims), _dims(dims), d_out))
+
+    def write_tensor_dev(self, path: str, dims, d_in: int):
+        self._check(self.lib.nds_write_tensor_dev(self.h, path.encode(), len(dims), _dims(dims), d_in))
 
     # ---- device surfaces ------------------------------------------------------------------
     def plan(self, us, ts, singular_tol=0.0, allow_fast_path=True, real_output=False) -> Plan:

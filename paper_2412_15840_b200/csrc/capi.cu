@@ -12,6 +12,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "ndt1.h"
 #include "schur.h"
 
 using nds::Error;
@@ -31,6 +32,9 @@ struct nds_ctx {
   size_t stage_bytes = 0;
   cudaEvent_t cev[16] = {};
   cudaStream_t side = nullptr;  // head overlap: row groups of the last forward pass
+  void* io_stage = nullptr;     // pinned double buffer for NDT1 streaming
+  size_t io_stage_bytes = 0;
+  cudaEvent_t io_ev[2] = {};
   cudaEvent_t hev[33] = {};
   std::map<std::vector<int64_t>, std::shared_ptr<nds::SolverCache>> solvers;  // by extents
 };
@@ -1047,6 +1051,9 @@ void nds_ctx_destroy(nds_ctx* ctx) {
   if (ctx->copy) cudaStreamDestroy(ctx->copy);
   if (ctx->side) cudaStreamDestroy(ctx->side);
   if (ctx->stage) cudaFreeHost(ctx->stage);
+  if (ctx->io_stage) cudaFreeHost(ctx->io_stage);
+  for (auto& e : ctx->io_ev)
+    if (e) cudaEventDestroy(e);
   if (ctx->own) cudaStreamDestroy(ctx->own);
   delete ctx;
 }
@@ -1622,6 +1629,154 @@ int nds_rk4(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z* const* 
             const nds_z* initial, double time, double dt, int64_t max_steps, nds_z* x) {
   if (!ctx) return NDS_ERR_INVALID;
   return guarded(ctx, [&] { rk4_impl(ctx, n_modes, dims, a, forcing, initial, time, dt, max_steps, x); });
+}
+
+// ---- NDT1 files and the generator (tensor_file.cpp, rng.cpp) -----------------
+
+namespace {
+
+void check_file_dims(const nds::Ndt1Reader& r, int n_modes, const int64_t* dims) {
+  bool same = r.n_modes == n_modes && dims;
+  for (int j = 0; same && j < n_modes; ++j) same = r.dims[j] == dims[j];
+  if (!same) throw Error(NDS_ERR_INVALID, "'" + r.path + "': extents differ from the caller's");
+}
+
+constexpr int64_t kIoChunk = 4 << 20;  // entries per pinned chunk (64 MB)
+
+void ensure_io_stage(nds_ctx* ctx) {
+  const size_t need = 2 * (size_t)kIoChunk * sizeof(nds_z);
+  if (ctx->io_stage_bytes >= need) return;
+  NDS_CUDA(cudaHostAlloc(&ctx->io_stage, need, cudaHostAllocDefault));
+  ctx->io_stage_bytes = need;
+  for (auto& e : ctx->io_ev)
+    if (!e) NDS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+}
+
+}  // namespace
+
+int nds_tensor_file_info(const char* path, int* n_modes, int64_t* dims) {
+  return guarded(nullptr, [&] {
+    if (!n_modes || !dims) throw Error(NDS_ERR_INVALID, "null output pointer");
+    nds::Ndt1Reader r;
+    nds::ndt1_open(r, path);
+    *n_modes = r.n_modes;
+    for (int j = 0; j < r.n_modes; ++j) dims[j] = r.dims[j];
+  });
+}
+
+int nds_read_tensor(const char* path, int n_modes, const int64_t* dims, nds_z* out) {
+  return guarded(nullptr, [&] {
+    if (!out) throw Error(NDS_ERR_INVALID, "null output pointer");
+    nds::Ndt1Reader r;
+    nds::ndt1_open(r, path);
+    check_file_dims(r, n_modes, dims);
+    nds::ndt1_read(r, r.total, out);
+  });
+}
+
+int nds_write_tensor(const char* path, int n_modes, const int64_t* dims, const nds_z* data) {
+  return guarded(nullptr, [&] {
+    if (!data || !dims) throw Error(NDS_ERR_INVALID, "null pointer");
+    nds::Ndt1Writer w;
+    nds::ndt1_create(w, path, n_modes, dims);
+    int64_t total = 1;
+    for (int j = 0; j < n_modes; ++j) total *= dims[j];
+    nds::ndt1_write(w, total, data);
+    nds::ndt1_close(w);
+  });
+}
+
+int nds_read_tensor_dev(nds_ctx* ctx, const char* path, int n_modes, const int64_t* dims, nds_z* d_out) {
+  if (!ctx) return NDS_ERR_INVALID;
+  return guarded(ctx, [&] {
+    if (!d_out) throw Error(NDS_ERR_INVALID, "null output pointer");
+    ensure_device(ctx);
+    nds::Ndt1Reader r;
+    nds::ndt1_open(r, path);
+    check_file_dims(r, n_modes, dims);
+    ensure_io_stage(ctx);
+    nds_z* buf[2] = {(nds_z*)ctx->io_stage, (nds_z*)ctx->io_stage + kIoChunk};
+    cudaStream_t cs = ctx->copy;
+    try {
+      int k = 0;
+      for (int64_t off = 0; off < r.total; off += kIoChunk, k ^= 1) {
+        const int64_t cnt = std::min(kIoChunk, r.total - off);
+        NDS_CUDA(cudaEventSynchronize(ctx->io_ev[k]));  // the copy that last read this half is done
+        nds::ndt1_read(r, cnt, buf[k]);                  // disk read overlaps the other half's copy
+        NDS_CUDA(cudaMemcpyAsync(d_out + off, buf[k], (size_t)cnt * sizeof(nds_z), cudaMemcpyHostToDevice, cs));
+        NDS_CUDA(cudaEventRecord(ctx->io_ev[k], cs));
+      }
+    } catch (...) {
+      cudaStreamSynchronize(cs);
+      throw;
+    }
+    NDS_CUDA(cudaStreamSynchronize(cs));
+  });
+}
+
+int nds_write_tensor_dev(nds_ctx* ctx, const char* path, int n_modes, const int64_t* dims, const nds_z* d_in) {
+  if (!ctx) return NDS_ERR_INVALID;
+  return guarded(ctx, [&] {
+    if (!d_in) throw Error(NDS_ERR_INVALID, "null input pointer");
+    ensure_device(ctx);
+    nds::Ndt1Writer w;
+    nds::ndt1_create(w, path, n_modes, dims);
+    int64_t total = 1;
+    for (int j = 0; j < n_modes; ++j) total *= dims[j];
+    ensure_io_stage(ctx);
+    nds_z* buf[2] = {(nds_z*)ctx->io_stage, (nds_z*)ctx->io_stage + kIoChunk};
+    cudaStream_t cs = ctx->copy;
+    auto issue = [&](int64_t off, int k) {
+      const int64_t cnt = std::min(kIoChunk, total - off);
+      NDS_CUDA(cudaMemcpyAsync(buf[k], d_in + off, (size_t)cnt * sizeof(nds_z), cudaMemcpyDeviceToHost, cs));
+      NDS_CUDA(cudaEventRecord(ctx->io_ev[k], cs));
+    };
+    try {
+      issue(0, 0);
+      int k = 0;
+      for (int64_t off = 0; off < total; off += kIoChunk, k ^= 1) {
+        if (off + kIoChunk < total) issue(off + kIoChunk, k ^ 1);  // next copy overlaps this write
+        NDS_CUDA(cudaEventSynchronize(ctx->io_ev[k]));
+        nds::ndt1_write(w, std::min(kIoChunk, total - off), buf[k]);
+      }
+    } catch (...) {
+      cudaStreamSynchronize(cs);
+      throw;
+    }
+    nds::ndt1_close(w);
+  });
+}
+
+int nds_random_problem(nds_ctx* ctx, int n_modes, const int64_t* dims, uint64_t seed, nds_z* const* a,
+                       nds_z* x_true, nds_z* b) {
+  if (!ctx) return NDS_ERR_INVALID;
+  return guarded(ctx, [&] {
+    const int64_t total = checked_total(n_modes, dims, 1);
+    if (!a || !x_true || !b) throw Error(NDS_ERR_INVALID, "null pointer");
+    for (int j = 0; j < n_modes; ++j)
+      if (!a[j]) throw Error(NDS_ERR_INVALID, "null matrix pointer");
+    nds_z* const tens[1] = {x_true};
+    nds::random_draw(seed, n_modes, dims, a, 1, tens);
+    ensure_device(ctx);
+    ensure_ws(ctx, total);
+    const size_t bytes = (size_t)total * sizeof(double2);
+    NDS_CUDA(cudaMemcpyAsync(ctx->ws[0], x_true, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    apply_operator_dev(ctx, n_modes, dims, a, ctx->ws[0], ctx->ws[1]);
+    NDS_CUDA(cudaMemcpyAsync(b, ctx->ws[1], bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    NDS_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int nds_random_ode_system(int n_modes, const int64_t* dims, uint64_t seed, nds_z* const* a, nds_z* forcing,
+                          nds_z* initial) {
+  return guarded(nullptr, [&] {
+    checked_total(n_modes, dims, 1);
+    if (!a || !forcing || !initial) throw Error(NDS_ERR_INVALID, "null pointer");
+    for (int j = 0; j < n_modes; ++j)
+      if (!a[j]) throw Error(NDS_ERR_INVALID, "null matrix pointer");
+    nds_z* const tens[2] = {forcing, initial};
+    nds::random_draw(seed, n_modes, dims, a, 2, tens);
+  });
 }
 
 void nds_randn(uint64_t seed, uint64_t stream, int64_t count, double* out) { nds::randn_host(seed, stream, count, out); }
