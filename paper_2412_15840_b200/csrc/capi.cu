@@ -934,7 +934,7 @@ void rk4_impl(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z* const
   std::vector<nds_z> ha(asz);
   for (int j = 0; j < n_modes; ++j) pack_layouts(dims[j], a[j], ha.data() + aoff[j]);
   double2* pool = nullptr;
-  const size_t pool_bytes = 7 * bytes + (size_t)asz * sizeof(double2) + 256;
+  const size_t pool_bytes = 8 * bytes + (size_t)asz * sizeof(double2) + 256;
   NDS_CUDA(cudaMalloc(&pool, pool_bytes));
   cudaGraphExec_t exec = nullptr;
   cudaGraph_t graph = nullptr;
@@ -945,12 +945,12 @@ void rk4_impl(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z* const
   };
   try {
     double2 *X = pool, *K1 = X + total, *K2 = K1 + total, *K3 = K2 + total, *K4 = K3 + total, *ST = K4 + total,
-            *B = ST + total, *dA = B + total;
+            *B = ST + total, *ST2 = B + total, *dA = ST2 + total;
     int* flag = (int*)(dA + asz);
     NDS_CUDA(cudaMemcpyAsync(X, initial, bytes, cudaMemcpyHostToDevice, s));
     NDS_CUDA(cudaMemcpyAsync(B, forcing, bytes, cudaMemcpyHostToDevice, s));
     NDS_CUDA(cudaMemcpyAsync(dA, ha.data(), (size_t)asz * sizeof(double2), cudaMemcpyHostToDevice, s));
-    NDS_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), s));
+    NDS_CUDA(cudaMemsetAsync(flag, 0, 256, s));  // nonfinite flag + grid-barrier counter
     auto rhs = [&](const double2* state, double2* k) {  // apply_operator + forcing (ode.cpp:101-105)
       for (int j = 1; j <= n_modes; ++j) {
         const double2* m = dA + aoff[j - 1];
@@ -959,7 +959,45 @@ void rk4_impl(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z* const
       }
       nds::axpy_launch(k, k, make_double2(1.0, 0.0), B, total, s);
     };
+    // small tensors: the launch-bound regime -> one fused kernel per stage (direct sums)
+    int64_t sumn = 0;
+    for (int j = 0; j < n_modes; ++j) sumn += dims[j];
+    const bool fused = n_modes <= 8 && total <= (1 << 20) && sumn <= 512;
+    nds::Rk4Stage rs{};
+    if (fused) {
+      rs.n_modes = n_modes;
+      rs.total = total;
+      int64_t str = 1;
+      for (int j = 0; j < n_modes; ++j) {
+        rs.dims[j] = dims[j];
+        rs.strides[j] = str;
+        str *= dims[j];
+        rs.a_row[j] = dA + aoff[j];
+      }
+      rs.b = B;
+      rs.x = X;
+    }
+    auto fused_step = [&](double h) {
+      const double2 hh = make_double2(0.5 * h, 0.0);
+      nds::Rk4Stage r1 = rs;
+      r1.in = X, r1.k_out = K1, r1.st_out = ST, r1.c = hh;
+      nds::rk4_stage_launch(r1, s);
+      nds::Rk4Stage r2 = rs;
+      r2.in = ST, r2.k_out = K2, r2.st_out = ST2, r2.c = hh;
+      nds::rk4_stage_launch(r2, s);
+      nds::Rk4Stage r3 = rs;
+      r3.in = ST2, r3.k_out = K3, r3.st_out = ST, r3.c = make_double2(h, 0.0);
+      nds::rk4_stage_launch(r3, s);
+      nds::Rk4Stage r4 = rs;
+      r4.in = ST, r4.k_out = K4, r4.final_stage = 1, r4.k1 = K1, r4.k2 = K2, r4.k3 = K3;
+      r4.a1 = make_double2(h / 6.0, 0.0), r4.a2 = make_double2(h / 3.0, 0.0);
+      nds::rk4_stage_launch(r4, s);
+    };
     auto step = [&](double h) {  // advance (ode.cpp:107-123)
+      if (fused) {
+        fused_step(h);
+        return;
+      }
       rhs(X, K1);
       nds::axpy_launch(ST, X, make_double2(0.5 * h, 0.0), K1, total, s);
       rhs(ST, K2);
@@ -970,8 +1008,15 @@ void rk4_impl(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z* const
       nds::rk4_combine_launch(X, make_double2(h / 6.0, 0.0), make_double2(h / 3.0, 0.0), K1, K2, K3, K4, total, s);
     };
     const double h = direction * dt;
+    const double remainder = span - (double)full_steps * dt;
     int64_t done = 0;
-    if (full_steps > 0) {  // first step eagerly (sets kernel attributes), the rest as graph replays
+    static const bool coop = !(getenv("NDS_RK4") && std::string(getenv("NDS_RK4")) == "graph");
+    if (fused && coop) {  // every step in one cooperative launch (grid barriers between stages)
+      nds::Rk4Buffers buf{X, {K1, K2, K3, K4}, {ST, ST2}, (unsigned int*)(flag + 32)};
+      nds::rk4_persistent_launch(rs, buf, full_steps, h, remainder > 0.0 ? direction * remainder : 0.0, s);
+      done = full_steps;
+    }
+    if (done < full_steps) {  // first step eagerly (sets kernel attributes), the rest as graph replays
       step(h);
       ++done;
     }
@@ -984,8 +1029,7 @@ void rk4_impl(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z* const
       for (; full_steps - done >= kPerGraph; done += kPerGraph) NDS_CUDA(cudaGraphLaunch(exec, s));
     }
     for (; done < full_steps; ++done) step(h);
-    const double remainder = span - (double)full_steps * dt;
-    if (remainder > 0.0) step(direction * remainder);
+    if (remainder > 0.0 && !(fused && coop)) step(direction * remainder);
     nds::nonfinite_launch(X, total, flag, s);
     int hflag = 0;
     NDS_CUDA(cudaMemcpyAsync(&hflag, flag, sizeof(int), cudaMemcpyDeviceToHost, s));

@@ -5,10 +5,12 @@
 //   real_part     — SolveOptions::real_output (sylvester.cpp:223-224).
 //   residual_norms — verification of sum_j A_j x_j X = B on the device (apply_operator,
 //                   sylvester.cpp:44-53, is the mode-product kernel with accumulate).
+
 #include "common.cuh"
 #include "kernels.h"
 
 namespace nds {
+
 
 constexpr int kEwThreads = 256;
 
@@ -247,6 +249,130 @@ __global__ void nonfinite_kernel(const double2* __restrict__ x, int64_t total, i
 int nonfinite_launch(const double2* x, int64_t total, int* flag, cudaStream_t stream) {
   const int64_t blocks = std::min<int64_t>((total + kEwThreads - 1) / kEwThreads, 148 * 8);
   nonfinite_kernel<<<(unsigned)blocks, kEwThreads, 0, stream>>>(x, total, flag);
+  NDS_LAUNCH_CHECK();
+  return 1;
+}
+
+// Fused RK4 stage for small tensors (launch-bound regime): one kernel computes the right-hand
+// side  K = sum_j A_j x_j IN + B  entry by entry (direct sums along each mode, A_j rows read
+// contiguously from the row-major copies) and applies the stage update in its epilogue:
+//   stage 0..2: ST_out = X + c K          stage 3: X += a1 K1 + a2 K2 + a2 K3 + a1 K
+// (reference ode.cpp:101-123 order per entry). Four launches per step instead of 4 (N + 2).
+// Four lanes per entry (each takes every fourth k of every mode; shuffles combine them): for the
+// small tensors this path serves, latency chains are what cost, not arithmetic.
+constexpr int kRk4Lanes = 4;
+
+__device__ __forceinline__ void rk4_stage_body(const Rk4Stage& a) {
+  const int q = threadIdx.x & (kRk4Lanes - 1);
+  const int64_t gstride = (int64_t)gridDim.x * blockDim.x / kRk4Lanes;
+  const int64_t lane_off = (threadIdx.x & 31) / kRk4Lanes;  // entry offset of this lane within its warp
+  for (int64_t base = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / kRk4Lanes; base - lane_off < a.total;
+       base += gstride) {  // trip count uniform across the warp (shuffles below use the full mask)
+    const int64_t e = base;
+    const bool active = e < a.total;
+    double2 acc = make_double2(0.0, 0.0);
+    if (active) {
+      int64_t r = e;
+      for (int m = 0; m < a.n_modes; ++m) {
+        const int64_t n = a.dims[m];
+        const int64_t im = r % n;
+        r /= n;
+        const double2* line = a.in + e - im * a.strides[m];
+        // A_1 read column-wise (adjacent entries differ in i_1), the others row-wise (broadcast)
+        const double2* ap = m == 0 ? a.a_row[m] + n * n + im : a.a_row[m] + im * n;
+        const int64_t astep = m == 0 ? n : 1, xs = a.strides[m];
+        double2 t0 = make_double2(0.0, 0.0), t1 = t0;
+        int64_t k = q;
+        for (; k + kRk4Lanes < n; k += 2 * kRk4Lanes) {
+          t0 = cfma(t0, __ldg(ap + k * astep), line[k * xs]);
+          t1 = cfma(t1, __ldg(ap + (k + kRk4Lanes) * astep), line[(k + kRk4Lanes) * xs]);
+        }
+        if (k < n) t0 = cfma(t0, __ldg(ap + k * astep), line[k * xs]);
+        acc = cadd(acc, cadd(t0, t1));
+      }
+    }
+#pragma unroll
+    for (int o = 1; o < kRk4Lanes; o <<= 1) {
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+    }
+    if (!active || q != 0) continue;
+    acc = cadd(acc, a.b[e]);
+    a.k_out[e] = acc;
+    if (a.final_stage) {
+      double2 v = a.x[e];
+      v = cadd(v, cmul(a.a1, a.k1[e]));
+      v = cadd(v, cmul(a.a2, a.k2[e]));
+      v = cadd(v, cmul(a.a2, a.k3[e]));
+      v = cadd(v, cmul(a.a1, acc));
+      a.x[e] = v;
+    } else {
+      a.st_out[e] = cadd(a.x[e], cmul(a.c, acc));
+    }
+  }
+}
+
+__global__ void rk4_stage_kernel(const Rk4Stage a) { rk4_stage_body(a); }
+
+// All steps in ONE cooperative launch: the four stages of a step are separated by grid-wide
+// barriers (each stage reads the whole previous stage buffer), so a step costs four grid syncs
+// instead of four kernel launches. Stage buffers rotate exactly as in the four-launch form.
+// Sense-free grid barrier: every CTA adds one to the counter and waits for the next multiple of
+// gridDim.x. Co-residency of all CTAs is what the cooperative launch guarantees.
+__device__ __forceinline__ void rk4_grid_barrier(unsigned int* bar, unsigned int& target) {
+  __syncthreads();
+  target += gridDim.x;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(bar, 1u);
+    unsigned int v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+    } while ((int)(v - target) < 0);
+  }
+  __syncthreads();
+}
+
+__global__ void rk4_persistent_kernel(const Rk4Stage base, const Rk4Buffers buf, int64_t steps, double h,
+                                      double h_last) {
+  unsigned int target = 0;
+  for (int64_t st = 0; st < steps + (h_last != 0.0 ? 1 : 0); ++st) {
+    const double hh = st < steps ? h : h_last;
+    Rk4Stage r = base;
+    r.in = buf.x, r.k_out = buf.k[0], r.st_out = buf.st[0], r.c = make_double2(0.5 * hh, 0.0), r.final_stage = 0;
+    rk4_stage_body(r);
+    rk4_grid_barrier(buf.bar, target);
+    r.in = buf.st[0], r.k_out = buf.k[1], r.st_out = buf.st[1];
+    rk4_stage_body(r);
+    rk4_grid_barrier(buf.bar, target);
+    r.in = buf.st[1], r.k_out = buf.k[2], r.st_out = buf.st[0], r.c = make_double2(hh, 0.0);
+    rk4_stage_body(r);
+    rk4_grid_barrier(buf.bar, target);
+    r.in = buf.st[0], r.k_out = buf.k[3], r.final_stage = 1, r.k1 = buf.k[0], r.k2 = buf.k[1], r.k3 = buf.k[2];
+    r.a1 = make_double2(hh / 6.0, 0.0), r.a2 = make_double2(hh / 3.0, 0.0);
+    rk4_stage_body(r);
+    rk4_grid_barrier(buf.bar, target);
+  }
+}
+
+int rk4_persistent_launch(const Rk4Stage& base, const Rk4Buffers& buf, int64_t steps, double h, double h_last,
+                          cudaStream_t stream) {
+  int per_sm = 0, sms = 0, dev = 0;
+  NDS_CUDA(cudaGetDevice(&dev));
+  NDS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  NDS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rk4_persistent_kernel, kEwThreads, 0));
+  const int64_t want = (base.total * kRk4Lanes + kEwThreads - 1) / kEwThreads;
+  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)per_sm * sms));
+  Rk4Stage b0 = base;
+  Rk4Buffers b1 = buf;
+  void* args[] = {&b0, &b1, &steps, &h, &h_last};
+  NDS_CUDA(cudaLaunchCooperativeKernel((const void*)rk4_persistent_kernel, blocks, kEwThreads, args, 0, stream));
+  return 1;
+}
+
+int rk4_stage_launch(const Rk4Stage& a, cudaStream_t stream) {
+  const int64_t blocks = std::min<int64_t>((a.total * kRk4Lanes + kEwThreads - 1) / kEwThreads, 148 * 16);
+  rk4_stage_kernel<<<(unsigned)blocks, kEwThreads, 0, stream>>>(a);
   NDS_LAUNCH_CHECK();
   return 1;
 }

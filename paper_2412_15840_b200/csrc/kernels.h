@@ -196,6 +196,34 @@ int axpy_launch(double2* z, const double2* x, double2 alpha, const double2* y, i
 // x += a1 k1 + a2 k2 + a2 k3 + a1 k4 (RK4 update, reference order).
 int rk4_combine_launch(double2* x, double2 a1, double2 a2, const double2* k1, const double2* k2, const double2* k3,
                        const double2* k4, int64_t total, cudaStream_t stream);
+// Fused RK4 stage (small tensors, N <= 8): K = sum_j A_j x_j in + B, then ST_out = X + c K or,
+// in the final stage, X += a1 K1 + a2 K2 + a2 K3 + a1 K.
+struct Rk4Stage {
+  int n_modes;
+  int64_t total;
+  int64_t dims[8], strides[8];
+  const double2* a_row[8];  // row-major A_j, followed by its column-major copy
+  const double2* in;
+  const double2* b;
+  double2* x;
+  double2* k_out;
+  double2* st_out;
+  double2 c;
+  int final_stage;
+  const double2 *k1, *k2, *k3;
+  double2 a1, a2;
+};
+int rk4_stage_launch(const Rk4Stage& a, cudaStream_t stream);
+// All RK4 steps in one cooperative launch (grid barriers between stages): `steps` steps of h,
+// then one of h_last when it is non-zero. Buffers: state, K1..K4, two stage tensors.
+struct Rk4Buffers {
+  double2* x;
+  double2* k[4];
+  double2* st[2];
+  unsigned int* bar;  // grid-barrier counter, zeroed before the launch
+};
+int rk4_persistent_launch(const Rk4Stage& base, const Rk4Buffers& buf, int64_t steps, double h, double h_last,
+                          cudaStream_t stream);
 // *flag |= 1 when x has an Inf or NaN entry.
 int nonfinite_launch(const double2* x, int64_t total, int* flag, cudaStream_t stream);
 // Max-abs and sum-of-squares of (r - b) and of b, deterministic (per-block partials).

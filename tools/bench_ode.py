@@ -6,7 +6,7 @@ Prints one JSON line per workload:
             events, K reps, inputs resident), host-buffer nds_ode_at (D2H included), unknowns/s;
             CPU baseline = the reference's propagate (oracle/_ref, all host threads) on the
             256x256x16 slab, rate = P / (its at() transform + backsub + inverse seconds).
-  rk4_c0  — rk4_reference on config c0 (32^3), dt = 1e-4, 200 steps (CUDA-graph replays), host
+  rk4_c0  — rk4_reference on config c0 (32^3), dt = 1e-4, 2000 steps (CUDA-graph replays), host
             buffers; CPU baseline = the reference's rk4_reference on the same system, 20 steps.
 usage: python tools/bench_ode.py [--reps K]
 """
@@ -96,7 +96,7 @@ def main():
     dims0 = b0.shape
     P0 = int(np.prod(dims0))
     x00 = rand_c(np.random.default_rng(2), dims0)
-    dt, steps = 1e-4, 200
+    dt, steps = 1e-4, 2000
     ctx.rk4(a0, b0, x00, dt * 10, dt)  # warm-up
     t0 = time.perf_counter()
     ctx.rk4(a0, b0, x00, dt * steps, dt)
