@@ -478,6 +478,33 @@ struct LinePad {
   }
 };
 
+// Line order of the line-owner kernel: lines sorted by d = sum_{m>=2} l_m, so the lanes of a warp
+// own lines whose 16-step activity windows ([lv0, lv0 + B - 1], lv0 = (N-1)(B-1) - d) nearly
+// coincide; a warp with no active lane skips the step. (Natural order puts l_2 = 0..B-1 in one
+// warp, which keeps every warp busy for all (N)(B-1)+1 steps at ~1/3 lane occupancy.)
+template <int N, int B>
+struct LineOrder {
+  uint16_t v[4096 / B];
+};
+template <int N, int B>
+constexpr LineOrder<N, B> make_line_order() {
+  LineOrder<N, B> o{};
+  constexpr int NL = 4096 / B, LB = B == 16 ? 4 : 3;
+  int p = 0;
+  for (int d = 0; d <= (N - 1) * (B - 1); ++d)
+    for (int l = 0; l < NL; ++l) {
+      int s = 0, x = l;
+      for (int m = 1; m < N; ++m) {
+        s += x & (B - 1);
+        x >>= LB;
+      }
+      if (s == d) o.v[p++] = (uint16_t)l;
+    }
+  return o;
+}
+__constant__ LineOrder<3, 16> kLineOrder3 = make_line_order<3, 16>();
+__constant__ LineOrder<4, 8> kLineOrder4 = make_line_order<4, 8>();
+
 // Diagonal tile, line-owner formulation. Thread t owns the mode-1 line with fixed local
 // coordinates (l_2, .., l_N) = base-B digits of t and walks it from row B-1 down to 0, one row
 // per local hyperplane: row r is solved at step lv = (N-1)(B-1) - d + (B-1-r), d = sum_{m>=2} l_m.
@@ -495,7 +522,7 @@ struct LinePad {
 //   near_out[item] (l_m, c) = sum_k T_m(o_m - B + l_m, o_m + k) Y_J(k along m, c)
 // (3M DMMA; near_target[slot N + m] = that item's index at the next level, -1 if none) — which
 // replaces the separate near-update launch on the critical path.
-template <int N, int B, int NT, bool PUSH, bool T2REG>
+template <int N, int B, int NT, bool PUSH, bool T2REG, bool SORT = true>
 __device__ __forceinline__ void diag_lines_body(const TileGeom& g, const double2* __restrict__ T, const int64_t tile,
                                                 const int4 tr, const double2* __restrict__ far_partial,
                                                 const double2* __restrict__ near_partial,
@@ -521,21 +548,26 @@ __device__ __forceinline__ void diag_lines_body(const TileGeom& g, const double2
   double2* S = sm;
   double2* Td = S + PS::extent + (PS::extent & 1);  // [N][B][B] row-major: T_m(o_m + row, o_m + col)
   double2* Dq = Td + N * B * B;                     // [B][B]: Dq[j][r] = T_1(r - 1 - j, r)
+  constexpr int ALD = B + 4;                        // = 4 mod 8: conflict-free DMMA A fragments
+  double2* Ap = Dq + B * B;                         // [N][B][ALD]: T_m(o_m - B + r, o_m + k) (PUSH)
   __syncthreads();
 #pragma unroll
   for (int m = 0; m < N; ++m) {
     const double2* Tm = T + g.toff[m];
     const int64_t nm = g.dims[m];
+    const bool push_m = PUSH && so[m] >= B;
     for (int e = tid; e < B * B; e += NT) {
-      const int r = e / B, c = e % B;
+      const int r = e % B, c = e / B;  // rows fastest: coalesced along T_m's columns
       Td[(m * B + r) * B + c] = Tm[(so[m] + r) + (so[m] + c) * nm];
+      if (push_m) Ap[(m * B + r) * ALD + c] = Tm[(so[m] - B + r) + (so[m] + c) * nm];
       if (m == 0) {  // e = j B + r'
         const int j = e / B, rr = e % B;
         Dq[e] = rr >= j + 1 ? Tm[(so[0] + rr - 1 - j) + (so[0] + rr) * nm] : make_double2(0.0, 0.0);
       }
     }
   }
-  // tr = {far first, far count, near first, near count}
+  // tr = {far first, far count, near first, near count}; partials two at a time so that 2 x PER
+  // loads per thread are in flight (the prologue is latency-bound)
   {
     constexpr int PER = E / NT;
     double2 v[PER];
@@ -547,15 +579,26 @@ __device__ __forceinline__ void diag_lines_body(const TileGeom& g, const double2
       for (int m = 0; m < N; ++m) gidx += (so[m] + ((l >> (LB * m)) & (B - 1))) * st[m];
       v[i] = Y[gidx];
     }
-    for (int p = 0; p < tr.y; ++p) {
-      const double2* pp = far_partial + (int64_t)(tr.x + p) * E + tid;
+    const int np = tr.y + tr.w;
+    auto part = [&](int p) {
+      return p < tr.y ? far_partial + (int64_t)(tr.x + p) * E + tid : near_partial + (int64_t)(tr.z + p - tr.y) * E + tid;
+    };
+    int p = 0;
+    for (; p + 2 <= np; p += 2) {
+      const double2 *p0 = part(p), *p1 = part(p + 1);
+      double2 w0[PER], w1[PER];
 #pragma unroll
-      for (int i = 0; i < PER; ++i) v[i] = csub(v[i], __ldcg(pp + i * NT));
+      for (int i = 0; i < PER; ++i) {
+        w0[i] = __ldcg(p0 + i * NT);
+        w1[i] = __ldcg(p1 + i * NT);
+      }
+#pragma unroll
+      for (int i = 0; i < PER; ++i) v[i] = csub(v[i], cadd(w0[i], w1[i]));
     }
-    for (int p = 0; p < tr.w; ++p) {
-      const double2* pp = near_partial + (int64_t)(tr.z + p) * E + tid;
+    if (p < np) {
+      const double2* p0 = part(p);
 #pragma unroll
-      for (int i = 0; i < PER; ++i) v[i] = csub(v[i], __ldcg(pp + i * NT));
+      for (int i = 0; i < PER; ++i) v[i] = csub(v[i], __ldcg(p0 + i * NT));
     }
 #pragma unroll
     for (int i = 0; i < PER; ++i) S[PS::pad(tid + i * NT)] = v[i];
@@ -565,9 +608,10 @@ __device__ __forceinline__ void diag_lines_body(const TileGeom& g, const double2
   int lm[N];
   int d = 0, pb = 0;
   lm[0] = 0;
+  const int line = !SORT ? tid : N == 3 ? kLineOrder3.v[tid] : kLineOrder4.v[tid];
 #pragma unroll
   for (int m = 1; m < N; ++m) {
-    lm[m] = (tid >> (LB * (m - 1))) & (B - 1);
+    lm[m] = (line >> (LB * (m - 1))) & (B - 1);
     d += lm[m];
     pb += lm[m] * PS::at(m);
   }
@@ -652,8 +696,6 @@ __device__ __forceinline__ void diag_lines_body(const TileGeom& g, const double2
     for (int m = 0; m < N; ++m) {
       const int tgt = near_target[m];
       if (tgt < 0) continue;  // CTA-uniform
-      const double2* Tm = T + g.toff[m];
-      const int64_t nm = g.dims[m], oj = so[m];
       int sb[4];
 #pragma unroll
       for (int qf = 0; qf < 4; ++qf) {
@@ -661,49 +703,57 @@ __device__ __forceinline__ void diag_lines_body(const TileGeom& g, const double2
         col_offsets(warp * 32 + qf * 8 + ar, m, sb[qf], lo);
       }
       double2* out = near_out + (int64_t)tgt * E;
-#pragma unroll 1
-      for (int ri = 0; ri < RB; ++ri) {  // one 8-row fragment row at a time (register budget)
-        double2 afr[B / 4];  // A(r, k) = T_m(o_m - B + r, o_m + k)
+      const double2* am = Ap + m * B * ALD;
+      double cre[RB][4][2], cim[RB][4][2], c3[RB][4][2];
 #pragma unroll
-        for (int kk = 0; kk < B / 4; ++kk) afr[kk] = Tm[(oj - B + ri * 8 + ar) + (oj + kk * 4 + kq) * nm];
-        double cre[4][2], cim[4][2], c3[4][2];
+      for (int ri = 0; ri < RB; ++ri)
 #pragma unroll
         for (int qf = 0; qf < 4; ++qf)
 #pragma unroll
-          for (int h = 0; h < 2; ++h) cre[qf][h] = cim[qf][h] = c3[qf][h] = 0.0;
+          for (int h = 0; h < 2; ++h) cre[ri][qf][h] = cim[ri][qf][h] = c3[ri][qf][h] = 0.0;
 #pragma unroll
-        for (int kk = 0; kk < B / 4; ++kk) {
-          const double a_r = afr[kk].x, a_i = afr[kk].y, a_s = a_r + a_i;
+      for (int kk = 0; kk < B / 4; ++kk) {
+        double a_r[RB], a_i[RB], a_s[RB];
 #pragma unroll
-          for (int qf = 0; qf < 4; ++qf) {
-            const double2 v = S[(kk * 4 + kq) * PS::at(m) + sb[qf]];
-            dmma_bs(cre[qf][0], cre[qf][1], a_r, v.x);
-            dmma_bs(cim[qf][0], cim[qf][1], a_i, v.y);
-            dmma_bs(c3[qf][0], c3[qf][1], a_s, v.x + v.y);
+        for (int ri = 0; ri < RB; ++ri) {
+          const double2 a = am[(ri * 8 + ar) * ALD + kk * 4 + kq];
+          a_r[ri] = a.x, a_i[ri] = a.y, a_s[ri] = a.x + a.y;
+        }
+#pragma unroll
+        for (int qf = 0; qf < 4; ++qf) {
+          const double2 v = S[(kk * 4 + kq) * PS::at(m) + sb[qf]];
+          const double vs = v.x + v.y;
+#pragma unroll
+          for (int ri = 0; ri < RB; ++ri) {
+            dmma_bs(cre[ri][qf][0], cre[ri][qf][1], a_r[ri], v.x);
+            dmma_bs(cim[ri][qf][0], cim[ri][qf][1], a_i[ri], v.y);
+            dmma_bs(c3[ri][qf][0], c3[ri][qf][1], a_s[ri], vs);
           }
         }
-        const int row = ri * 8 + ar;
-#pragma unroll
-        for (int qf = 0; qf < 4; ++qf)
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            int so_, lo;
-            col_offsets(warp * 32 + qf * 8 + 2 * kq + h, m, so_, lo);
-            out[(row << (LB * m)) + lo] = make_double2(cre[qf][h] - cim[qf][h], c3[qf][h] - cre[qf][h] - cim[qf][h]);
-          }
       }
+#pragma unroll
+      for (int qf = 0; qf < 4; ++qf)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          int so_, lo;
+          col_offsets(warp * 32 + qf * 8 + 2 * kq + h, m, so_, lo);
+#pragma unroll
+          for (int ri = 0; ri < RB; ++ri)
+            out[((ri * 8 + ar) << (LB * m)) + lo] =
+                make_double2(cre[ri][qf][h] - cim[ri][qf][h], c3[ri][qf][h] - cre[ri][qf][h] - cim[ri][qf][h]);
+        }
     }
   }
 }
 
-template <int N, int B, int NT, bool PUSH, bool T2REG>
+template <int N, int B, int NT, bool PUSH, bool T2REG, bool SORT = true>
 __global__ void __launch_bounds__(NT, T2REG ? 1 : 2)
     tile_diag_lines_kernel(const TileGeom g, const double2* __restrict__ T, const int64_t* __restrict__ tiles,
                            const int4* __restrict__ tile_ranges, const double2* __restrict__ far_partial,
                            const double2* __restrict__ near_partial, const int* __restrict__ near_target,
                            double2* __restrict__ near_out, double2* __restrict__ Y) {
   extern __shared__ __align__(16) double2 sm[];
-  diag_lines_body<N, B, NT, PUSH, T2REG>(g, T, tiles[blockIdx.x], tile_ranges[blockIdx.x], far_partial, near_partial,
+  diag_lines_body<N, B, NT, PUSH, T2REG, SORT>(g, T, tiles[blockIdx.x], tile_ranges[blockIdx.x], far_partial, near_partial,
                                          near_target ? near_target + (int64_t)blockIdx.x * N : nullptr, near_out, Y,
                                          sm);
 }
@@ -712,17 +762,22 @@ using LinesKernel = void (*)(const TileGeom, const double2*, const int64_t*, con
                              const double2*, const int*, double2*, double2*);
 static LinesKernel lines_kernel_for(int n_modes, int b, bool push) {
   static const bool t2smem = getenv("NDS_DIAG_T2SMEM") != nullptr;  // A/B experiments
+  static const bool natural = getenv("NDS_DIAG_NATURAL") != nullptr;
   if (n_modes == 3 && b == 16) {
+    if (natural)
+      return push ? tile_diag_lines_kernel<3, 16, 256, true, true, false> : tile_diag_lines_kernel<3, 16, 256, false, true, false>;
     if (t2smem) return push ? tile_diag_lines_kernel<3, 16, 256, true, false> : tile_diag_lines_kernel<3, 16, 256, false, false>;
     return push ? tile_diag_lines_kernel<3, 16, 256, true, true> : tile_diag_lines_kernel<3, 16, 256, false, true>;
   }
+  if (n_modes == 4 && b == 8 && natural)
+    return push ? tile_diag_lines_kernel<4, 8, 512, true, true, false> : tile_diag_lines_kernel<4, 8, 512, false, true, false>;
   if (n_modes == 4 && b == 8)
     return push ? tile_diag_lines_kernel<4, 8, 512, true, true> : tile_diag_lines_kernel<4, 8, 512, false, true>;
   return nullptr;
 }
 static size_t lines_smem_bytes(int n_modes, int b) {
   const int ext = n_modes == 3 ? LinePad<3, 16>::extent : LinePad<4, 8>::extent;
-  return (size_t)(ext + (ext & 1)) * 16 + (size_t)(n_modes + 1) * b * b * 16;
+  return (size_t)(ext + (ext & 1)) * 16 + (size_t)(n_modes + 1) * b * b * 16 + (size_t)n_modes * b * (b + 4) * 16;
 }
 
 using UpdateKernel = void (*)(const TileGeom, const double2*, const int64_t*, const int4*, double2*, const double2*);
@@ -743,7 +798,7 @@ static int update_override() {
     if (!e) return -1;
     const std::string s(e);
     return s == "3m" ? 1 : s == "4m" ? 0 : s == "k16" ? 2 : s == "s4" ? 3 : s == "h2" ? 4 : s == "h1" ? 5
-         : s == "h4" ? 6 : -1;
+         : s == "h4" ? 6 : s == "h2s4" ? 7 : s == "h2s5" ? 8 : -1;
   }();
   return v;
 }
@@ -753,6 +808,8 @@ static UpdCfg update_cfg_for(int b) {
     if (o == 1) return {tile_update_kernel<1, 8, true, 1, 3, 1>, 4, 3, 1};
     if (o == 4) return {tile_update_kernel<1, 4, true, 1, 3, 2>, 4, 3, 2};
     if (o == 6) return {tile_update_kernel<1, 2, true, 1, 3, 4>, 4, 3, 4};
+    if (o == 7) return {tile_update_kernel<1, 8, false, 1, 4, 1>, 4, 4, 1};
+    if (o == 8) return {tile_update_kernel<1, 8, false, 1, 5, 1>, 4, 5, 1};
     return {tile_update_kernel<1, 8, false, 1, 3, 1>, 4, 3, 1};
   }
   if (b == 16) {
@@ -761,6 +818,8 @@ static UpdCfg update_cfg_for(int b) {
     if (o == 3) return {tile_update_kernel<2, 4, true, 1, 4, 1>, 8, 4, 1};
     if (o == 5) return {tile_update_kernel<2, 4, true, 1, 3, 1>, 8, 3, 1};
     if (o == 6) return {tile_update_kernel<2, 1, true, 1, 3, 4>, 8, 3, 4};
+    if (o == 7) return {tile_update_kernel<2, 2, true, 1, 4, 2>, 8, 4, 2};
+    if (o == 8) return {tile_update_kernel<2, 2, true, 1, 5, 2>, 8, 5, 2};
     return {tile_update_kernel<2, 2, true, 1, 3, 2>, 8, 3, 2};
   }
   return {nullptr, 0, 0, 0};
