@@ -10,10 +10,15 @@ solve(B in L_N):
   1. forward, modes 1..N-1: local (each mode product is independent across mode-N slabs);
   2. all-to-all re-shard L_N -> L_1 (the only exchange of the transform);
   3. forward, mode N: local in L_1;
-  4. triangular solve, slab-pipelined along mode 1: the rank holding the highest mode-1 slab
-     solves its slab (T_1 restricted to its diagonal block), broadcasts Y, every lower rank
-     applies  C_p -= T_1[p rows, q cols] x_1 Y_q  (rectangular mode-1 update), then the next
-     slab solves — T_1 is dense upper triangular, so rank p needs every q > p;
+  4. triangular solve, pipelined over (rank, sub-block): each rank's L_1 slab is cut into K
+     contiguous sub-blocks along mode N (the slowest index). Block (q, k) needs
+       - the mode-1 couplings  C_q[k] -= T_1[q rows, q' cols] x_1 Y_q'[k]  from every q' > q
+         (T_1 is dense upper triangular, so rank q needs every higher rank, not only q + 1),
+         received point-to-point as soon as rank q' has solved its block k;
+       - the mode-N couplings from its own blocks k' > k, applied by rank q right after solving
+         k':  C_q[:s_k'] -= T_N[:s_k', k' cols] x_N Y_q[k']  (one rectangular update);
+     then the local solve with T_1 and T_N restricted to their diagonal blocks. Blocks form a
+     wavefront over (P-1-q) + (K-1-k): P + K - 1 waves instead of P serial slab solves;
   5. inverse, modes 2..N: local in L_1;
   6. all-to-all re-shard L_1 -> L_N;
   7. inverse, mode 1: local in L_N.  X is returned in the input layout L_N.
@@ -41,6 +46,8 @@ class CudaLocalOps:
 
     def __init__(self, ctx):
         self.ctx = ctx
+        # one stream for the C ABI kernels and torch/NCCL: received blocks are read in stream order
+        ctx.set_stream(torch.cuda.current_stream().cuda_stream)
 
     def zeros(self, count, like):
         return torch.zeros(count, dtype=torch.complex128, device=like.device)
@@ -79,7 +86,7 @@ def _exchange(send_blocks, recv_sizes, group):
 class ShardedSolver:
     """Distributed solve of sum_j A_j x_j X = B from host Schur factors (same on every rank)."""
 
-    def __init__(self, dims, us, ts, ops, group=None, singular_tol=0.0):
+    def __init__(self, dims, us, ts, ops, group=None, singular_tol=0.0, sub_blocks=None):
         self.dims = tuple(int(d) for d in dims)
         self.N = len(self.dims)
         if self.N < 2:
@@ -96,6 +103,9 @@ class ShardedSolver:
             raise ValueError("n_1 and n_N must be >= the number of ranks")
         self.s1, self.m1 = block_partition(n1, self.P)
         self.sN, self.mN = block_partition(nN, self.P)
+        # pipeline depth along mode N (K sub-blocks per rank)
+        k = sub_blocks if sub_blocks is not None else 4 * self.P if self.P > 1 else 1
+        self.sK, self.mK = block_partition(nN, max(1, min(int(k), nN)))
         # sylvester.cpp:29-33 — the tolerance of the WHOLE operator, not of a slab
         self.tol = singular_tol if singular_tol > 0 else np.finfo(float).eps * sum(np.linalg.norm(t) for t in self.ts)
 
@@ -141,30 +151,52 @@ class ShardedSolver:
         # 2. re-shard, 3. mode N (local in L_1)
         c = self.reshard_N_to_1(x)
         c = ops.mode_product(self.dims_L1(r), self.uhs[N - 1], N, c)
-        # 4. slab-pipelined triangular solve along mode 1
-        t1 = self.ts[0]
-        for q in reversed(range(self.P)):
-            sq, mq = self.s1[q], self.m1[q]
-            if r == q:
-                ts_local = [np.asfortranarray(t1[sq:sq + mq, sq:sq + mq])] + self.ts[1:]
-                ops.back_substitute(ts_local, self.dims_L1(q), c, self.tol)
-                yq = c
-            else:
-                yq = torch.empty(mq * int(np.prod(self.dims[1:])), dtype=c.dtype, device=c.device)
-            if q > 0:
-                yr = torch.view_as_real(yq)
-                dist.broadcast(yr, src=q, group=self.group)
-                yq = torch.view_as_complex(yr)
-                if r < q:
-                    sr, mr = self.s1[r], self.m1[r]
-                    block = -np.asfortranarray(t1[sr:sr + mr, sq:sq + mq])
-                    ops.mode_update(self.dims_L1(q), 1, block, yq, c)
+        # 4. triangular solve pipelined over (rank, mode-N sub-block)
+        self.pipelined_backsub(c)
         # 5. inverse, modes 2..N (local in L_1), 6. re-shard, 7. mode 1 (local in L_N)
         y = c
         for j in range(2, N + 1):
             y = ops.mode_product(self.dims_L1(r), self.us[j - 1], j, y)
         x = self.reshard_1_to_N(y)
         return ops.mode_product(self.dims_LN(r), self.us[0], 1, x)
+
+    def _global(self, q):
+        return q if self.group is None else dist.get_global_rank(self.group, q)
+
+    def pipelined_backsub(self, c):
+        """Step 4 in place on this rank's L_1 slab c (see the module docstring)."""
+        ops, r, N, P = self.ops, self.rank, self.N, self.P
+        t1, tN = self.ts[0], self.ts[-1]
+        s1, m1 = self.s1[r], self.m1[r]
+        mid = int(np.prod(self.dims[1:-1]))
+        plane = m1 * mid  # entries per mode-N index in this rank's slab
+        pending = []  # (work, tensor): sends stay alive until the end
+        for k in reversed(range(len(self.mK))):
+            sk, mk = self.sK[k], self.mK[k]
+            blk = c[sk * plane:(sk + mk) * plane]
+            # mode-1 couplings from every higher rank's block k
+            for q in range(P - 1, r, -1):
+                yq = torch.empty(self.m1[q] * mid * mk, dtype=c.dtype, device=c.device)
+                yr = torch.view_as_real(yq)
+                dist.recv(yr, src=self._global(q), group=self.group)
+                m = -np.asfortranarray(t1[s1:s1 + m1, self.s1[q]:self.s1[q] + self.m1[q]])
+                ops.mode_update((self.m1[q],) + self.dims[1:-1] + (mk,), 1, m, yq, blk)
+            # local solve: T_1 and T_N restricted to their diagonal blocks
+            ts_local = [np.asfortranarray(t1[s1:s1 + m1, s1:s1 + m1])] + self.ts[1:-1] + \
+                       [np.asfortranarray(tN[sk:sk + mk, sk:sk + mk])]
+            ops.back_substitute(ts_local, (m1,) + self.dims[1:-1] + (mk,), blk, self.tol)
+            # forward the solved block to every lower rank (point-to-point, non-blocking)
+            if r > 0:
+                ops.synchronize()
+                br = torch.view_as_real(blk)
+                for q in range(r - 1, -1, -1):
+                    pending.append((dist.isend(br, dst=self._global(q), group=self.group), br))
+            # mode-N couplings of this block into the lower sub-blocks of this rank
+            if sk > 0:
+                m = -np.asfortranarray(tN[:sk, sk:sk + mk])
+                ops.mode_update((m1,) + self.dims[1:-1] + (mk,), N, m, blk, c[:sk * plane])
+        for w, _ in pending:
+            w.wait()
 
 
 def scatter_LN(b, P):

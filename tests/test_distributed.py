@@ -38,6 +38,9 @@ class CpuOps:
         y, _ = self.port.back_substitute(ts, c.numpy().reshape(dims, order="F"), tol)
         c.copy_(torch.from_numpy(y.reshape(-1, order="F").copy()))
 
+    def synchronize(self):
+        pass
+
 
 def _free_port():
     s = socket.socket()
@@ -47,7 +50,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, dims, seed, out_dir):
+def _worker(rank, world, port, dims, seed, out_dir, sub_blocks=None):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -61,7 +64,7 @@ def _worker(rank, world, port, dims, seed, out_dir):
         ts.append(t)
     b = rng.standard_normal(dims) + 1j * rng.standard_normal(dims)
     slabs = scatter_LN(b, world)
-    solver = ShardedSolver(dims, us, ts, CpuOps())
+    solver = ShardedSolver(dims, us, ts, CpuOps(), sub_blocks=sub_blocks)
     x_local = solver.solve(torch.from_numpy(slabs[rank]))
     np.save(os.path.join(out_dir, f"x{rank}.npy"), x_local.numpy())
     if rank == 0:
@@ -70,10 +73,14 @@ def _worker(rank, world, port, dims, seed, out_dir):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,dims", [(2, (6, 5, 8)), (3, (7, 4, 5)), (2, (4, 3, 2, 5)), (3, (5, 6))])
-def test_sharded_solve_matches_oracle(tmp_path, world, dims):
+@pytest.mark.parametrize("world,dims,sub_blocks", [(2, (6, 5, 8), None), (3, (7, 4, 5), None), (2, (4, 3, 2, 5), None),
+                                                  (3, (5, 6), None), (2, (6, 5, 8), 1), (3, (7, 4, 9), 9),
+                                                  (2, (5, 3, 7), 3)])
+def test_sharded_solve_matches_oracle(tmp_path, world, dims, sub_blocks):
+    # sub_blocks: pipeline depth along mode N (None = 4 per rank, 1 = serial slabs, n_N = one
+    # mode-N index per block)
     port = _free_port()
-    mp.spawn(_worker, args=(world, port, dims, 123, str(tmp_path)), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, port, dims, 123, str(tmp_path), sub_blocks), nprocs=world, join=True)
     z = np.load(tmp_path / "problem.npz")
     n = len(dims)
     us = [z[f"u{j}"] for j in range(n)]
@@ -108,10 +115,11 @@ def test_cuda_local_ops_single_rank(ctx):
         us.append(np.asfortranarray(q))
         ts.append(np.asfortranarray(t))
     b = rng.standard_normal(dims) + 1j * rng.standard_normal(dims)
-    solver = ShardedSolver(dims, us, ts, CudaLocalOps(ctx))
-    x = solver.solve(torch.from_numpy(scatter_LN(b, 1)[0]).cuda()).cpu().numpy().reshape(dims, order="F")
     x_ref, _ = oracle.Port().solve_schur(us, ts, b, flags=0)
-    assert np.max(np.abs(x - x_ref)) / np.max(np.abs(x_ref)) <= 1e-12
+    for k in (1, 5):  # whole slab, and 5 mode-N sub-blocks (device mode-N coupling updates)
+        solver = ShardedSolver(dims, us, ts, CudaLocalOps(ctx), sub_blocks=k)
+        x = solver.solve(torch.from_numpy(scatter_LN(b, 1)[0]).cuda()).cpu().numpy().reshape(dims, order="F")
+        assert np.max(np.abs(x - x_ref)) / np.max(np.abs(x_ref)) <= 1e-12
     # rectangular update kernel (GEMM and direct variants) against numpy
     for shape, mode, rows in [((40, 20, 3), 1, 7), ((6, 40, 5), 2, 33), ((3, 5, 64), 3, 17), ((2, 3, 4), 2, 2)]:
         x0 = rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
