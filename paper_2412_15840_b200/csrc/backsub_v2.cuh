@@ -798,7 +798,7 @@ static int update_override() {
     if (!e) return -1;
     const std::string s(e);
     return s == "3m" ? 1 : s == "4m" ? 0 : s == "k16" ? 2 : s == "s4" ? 3 : s == "h2" ? 4 : s == "h1" ? 5
-         : s == "h4" ? 6 : s == "h2s4" ? 7 : s == "h2s5" ? 8 : -1;
+         : s == "h4" ? 6 : s == "h2s4" ? 7 : s == "h2s5" ? 8 : s == "h2k16s2" ? 9 : s == "h4k16" ? 10 : -1;
   }();
   return v;
 }
@@ -820,6 +820,8 @@ static UpdCfg update_cfg_for(int b) {
     if (o == 6) return {tile_update_kernel<2, 1, true, 1, 3, 4>, 8, 3, 4};
     if (o == 7) return {tile_update_kernel<2, 2, true, 1, 4, 2>, 8, 4, 2};
     if (o == 8) return {tile_update_kernel<2, 2, true, 1, 5, 2>, 8, 5, 2};
+    if (o == 9) return {tile_update_kernel<2, 2, true, 2, 2, 2>, 16, 2, 2};
+    if (o == 10) return {tile_update_kernel<2, 1, true, 2, 3, 4>, 16, 3, 4};
     return {tile_update_kernel<2, 2, true, 1, 3, 2>, 8, 3, 2};
   }
   return {nullptr, 0, 0, 0};

@@ -32,10 +32,12 @@ __global__ void __launch_bounds__(kBinSolveThreads, 3) binary_tile_solve_kernel(
                                                                               double2* __restrict__ Y) {
   extern __shared__ __align__(16) double2 S[];  // 2^m entries
   __shared__ double2 t01[64], t00[64], t11[64];
+  __shared__ double2 dlo[64], dhi[64];  // den(l) = dlo[l & 63] + dhi[l >> 6] (outer part in dhi)
   __shared__ double2 dout;
   const int tid = threadIdx.x;
   const int N = g.m + g.n_outer;
   const int E = 1 << g.m;
+  const int mlo = g.m < 6 ? g.m : 6, mhi = g.m - mlo;
   const int64_t I = tiles[blockIdx.x];  // outer index (bit q = outer mode m + q)
   for (int j = tid; j < N; j += blockDim.x) {
     t00[j] = g.t[4 * j + 0];
@@ -47,6 +49,17 @@ __global__ void __launch_bounds__(kBinSolveThreads, 3) binary_tile_solve_kernel(
     double2 d = make_double2(0.0, 0.0);
     for (int q = 0; q < g.n_outer; ++q) d = cadd(d, ((I >> q) & 1) ? t11[g.m + q] : t00[g.m + q]);
     dout = d;
+  }
+  __syncthreads();
+  if (tid < 64) {  // inner modes 0..mlo-1
+    double2 d = make_double2(0.0, 0.0);
+    for (int j = 0; j < mlo; ++j) d = cadd(d, ((tid >> j) & 1) ? t11[j] : t00[j]);
+    dlo[tid] = d;
+  } else if (tid < 128) {  // inner modes mlo..m-1, then the outer modes
+    const int x = tid - 64;
+    double2 d = make_double2(0.0, 0.0);
+    for (int j = 0; j < mhi; ++j) d = cadd(d, ((x >> j) & 1) ? t11[mlo + j] : t00[mlo + j]);
+    dhi[x] = cadd(d, dout);
   }
   const int64_t base = I << g.m;
   // 1. load + pull from neighbour slabs (outer modes with bit 0), one slab at a time with all of
@@ -77,24 +90,17 @@ __global__ void __launch_bounds__(kBinSolveThreads, 3) binary_tile_solve_kernel(
     if (l < E) S[l] = acc[i];
   }
   __syncthreads();
-  const double2 dO = dout;
-  // 2. local popcount wavefront
+  // 2. local popcount wavefront, highest level first; inner-mode terms in mode order (loop fully
+  //    unrolled so the neighbour loads issue early; den from the two half tables)
   for (int lv = 0; lv < g.wf_levels; ++lv) {
     const int p1 = wf_off[lv + 1];
     for (int p = wf_off[lv] + tid; p < p1; p += blockDim.x) {
       const int l = wf[p];
       double2 num = S[l];
-      double2 den = make_double2(0.0, 0.0);
-      for (int j = 0; j < g.m; ++j) {
-        if ((l >> j) & 1) {
-          den = cadd(den, t11[j]);
-        } else {
-          den = cadd(den, t00[j]);
-          num = cfms(num, t01[j], S[l | (1 << j)]);
-        }
-      }
-      den = cadd(den, dO);
-      S[l] = cdiv(num, den);
+#pragma unroll
+      for (int j = 0; j < 12; ++j)
+        if (j < g.m && !((l >> j) & 1)) num = cfms(num, t01[j], S[l | (1 << j)]);
+      S[l] = cmul(num, crecip_fast(cadd(dlo[l & 63], dhi[l >> mlo])));
     }
     __syncthreads();
   }
