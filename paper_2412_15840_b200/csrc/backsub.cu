@@ -293,6 +293,139 @@ void solve_plan_build(SolvePlan& sp, int n_modes, const int64_t* dims, const int
     }
   }
 
+  // Grouped far updates (fgroup = G > 1): along every mode-j line the far targets (blocks
+  // t <= nb_j - 3) form groups of G consecutive blocks from the top, t0, t0 - 1, .., t0 - G' + 1.
+  // At the level of t0 one item (k-split like the plain items) covers all of them with the
+  // sources every member needs, rows >= (t0 + 2) b; member t0 - q then still needs the q blocks
+  // [t0 - q + 2, t0 + 2), added by a remainder item at its own level (sources two or more levels
+  // old, so ready). Partials live in a ring of fg_ring level regions (an item writes regions of
+  // up to G - 1 later levels), one slot per (target, mode, chunk): the diagonal kernel reads
+  // exactly the slots listed in tile_ranges, as with plain items.
+  std::vector<FarGroupItem> fg_items;
+  sp.fgroup = 0;
+  if (sp.v2) {
+    const int want = far_group_for(g.b[0]);
+    bool ok = want >= 1;
+    for (int j = 0; j < n_modes && ok; ++j)
+      if (g.b[j] != g.b[0] || (g.nb[j] >= 3 && want * g.b[j] > g.dims[j])) ok = false;
+    if (ok) sp.fgroup = want;
+  }
+  if (sp.fgroup >= 1) {
+    const int G = sp.fgroup;
+    std::vector<int64_t> slot_of(ntiles);
+    for (int64_t s2 = 0; s2 < ntiles; ++s2) slot_of[tiles[s2]] = s2;
+    std::vector<int64_t> tstride(n_modes, 1);
+    for (int j = 1; j < n_modes; ++j) tstride[j] = tstride[j - 1] * g.nb[j - 1];
+    // per (slot, mode): chunk items of the group item covering it, row block within it, remainder
+    std::vector<std::vector<int>> chunks((size_t)ntiles * n_modes);
+    std::vector<int> rowblk((size_t)ntiles * n_modes, -1), remainder((size_t)ntiles * n_modes, -1);
+    std::vector<std::vector<FarGroupItem>> per_level(levels);
+    const int64_t kq = std::max(8, far_group_bk(g.b[0]));
+    for (int lv = 0; lv < levels; ++lv) {
+      int64_t natural = 0, rows = 0;
+      auto top_of = [&](int64_t nbj, int64_t t) { return nbj - 3 - ((nbj - 3 - t) / G) * G; };
+      for (int64_t s2 = sp.level_off[lv]; s2 < sp.level_off[lv + 1]; ++s2) {
+        int64_t r = tiles[s2];
+        for (int j = 0; j < n_modes; ++j) {
+          const int64_t t = r % g.nb[j];
+          r /= g.nb[j];
+          if (t > g.nb[j] - 3) continue;
+          const int64_t t0 = top_of(g.nb[j], t);
+          ++natural;
+          rows += t == t0 ? g.dims[j] - (t0 + 2) * g.b[j] : (t0 - t) * g.b[j];
+        }
+      }
+      int64_t kc = INT64_MAX;
+      if (natural > 0 && natural < 2 * 148) kc = std::max<int64_t>(32, ((rows + 295) / 296 + kq - 1) / kq * kq);
+      for (int64_t s2 = sp.level_off[lv]; s2 < sp.level_off[lv + 1]; ++s2) {
+        int64_t r = tiles[s2];
+        for (int j = 0; j < n_modes; ++j) {
+          const int64_t t = r % g.nb[j];
+          r /= g.nb[j];
+          if (t > g.nb[j] - 3) continue;
+          const int64_t t0 = top_of(g.nb[j], t), b = g.b[j];
+          if (t == t0) {
+            const int gp = (int)std::min<int64_t>(G, t0 + 1);
+            const int64_t rb0 = t0 - gp + 1;
+            std::vector<int> ids;
+            for (int64_t kb = (t0 + 2) * b; kb < g.dims[j]; kb += (kc == INT64_MAX ? g.dims[j] : kc)) {
+              const int64_t ke = kc == INT64_MAX ? g.dims[j] : std::min<int64_t>(g.dims[j], kb + kc);
+              FarGroupItem it{};
+              it.tile = (int)s2;
+              it.j = j;
+              it.kb = (int)kb;
+              it.ke = (int)ke;
+              it.rb0 = (int)(gp < G ? 0 : rb0);  // a truncated group starts at block 0
+              it.nrb = (int)(gp < G ? t0 + 1 : gp);
+              it.acc = 0;
+              for (int q = 0; q < 4; ++q) it.out[q] = -1;
+              ids.push_back((int)per_level[lv].size() | (lv << 20));
+              per_level[lv].push_back(it);
+            }
+            for (int q = 0; q < gp; ++q) {  // members t0 - q
+              const int64_t ms = slot_of[tiles[s2] - q * tstride[j]];
+              chunks[(size_t)ms * n_modes + j] = ids;
+              rowblk[(size_t)ms * n_modes + j] = (int)(t0 - q - (gp < G ? 0 : rb0));
+            }
+          } else {
+            FarGroupItem it{};
+            it.tile = (int)s2;
+            it.j = j;
+            it.kb = (int)((t + 2) * b);
+            it.ke = (int)((t0 + 2) * b);
+            it.rb0 = (int)t;
+            it.nrb = 1;
+            it.acc = 1;
+            for (int q = 0; q < 4; ++q) it.out[q] = -1;
+            remainder[(size_t)s2 * n_modes + j] = (int)per_level[lv].size() | (lv << 20);
+            per_level[lv].push_back(it);
+          }
+        }
+      }
+    }
+    // slots: per target level, per tile, per mode, per chunk (tile_ranges order)
+    int64_t max_slots = 1;
+    std::vector<int> slot_idx((size_t)ntiles * n_modes, -1);
+    for (int lv = 0; lv < levels; ++lv) {
+      int idx = 0;
+      for (int64_t s2 = sp.level_off[lv]; s2 < sp.level_off[lv + 1]; ++s2) {
+        const int first = idx;
+        for (int j = 0; j < n_modes; ++j) {
+          const auto& ids = chunks[(size_t)s2 * n_modes + j];
+          if (ids.empty()) continue;
+          slot_idx[(size_t)s2 * n_modes + j] = idx;
+          idx += (int)ids.size();
+        }
+        tile_ranges[s2].x = first;
+        tile_ranges[s2].y = idx - first;
+      }
+      max_slots = std::max<int64_t>(max_slots, idx);
+    }
+    sp.fg_ring = G + 2;
+    sp.fg_slots = max_slots;
+    for (int lv = 0; lv < levels; ++lv)
+      for (int64_t s2 = sp.level_off[lv]; s2 < sp.level_off[lv + 1]; ++s2)
+        for (int j = 0; j < n_modes; ++j) {
+          const auto& ids = chunks[(size_t)s2 * n_modes + j];
+          if (ids.empty()) continue;
+          const int64_t base = (int64_t)(lv % sp.fg_ring) * max_slots + slot_idx[(size_t)s2 * n_modes + j];
+          const int q = rowblk[(size_t)s2 * n_modes + j];
+          for (size_t c2 = 0; c2 < ids.size(); ++c2)
+            per_level[ids[c2] >> 20][ids[c2] & 0xfffff].out[q] = (int)(base + (int64_t)c2);
+          const int rm = remainder[(size_t)s2 * n_modes + j];
+          if (rm >= 0) per_level[rm >> 20][rm & 0xfffff].out[0] = (int)base;
+        }
+    sp.fg_off.assign(levels + 1, 0);
+    for (int lv = 0; lv < levels; ++lv) {
+      // longest first (LPT): the short remainder items fill the launch's tail
+      std::stable_sort(per_level[lv].begin(), per_level[lv].end(), [](const FarGroupItem& a, const FarGroupItem& b2) {
+        return (int64_t)(a.ke - a.kb) * (a.acc ? 1 : 2) > (int64_t)(b2.ke - b2.kb) * (b2.acc ? 1 : 2);
+      });
+      for (const auto& it : per_level[lv]) fg_items.push_back(it);
+      sp.fg_off[lv + 1] = (int64_t)fg_items.size();
+    }
+  }
+
   // v2 per-thread step tables for the diagonal kernel
   const int dthreads = sp.v2 ? diag_threads_for(n_modes) : 0;
   std::vector<uint16_t> thr((size_t)wf_levels * dthreads, 0xffff);
@@ -326,7 +459,7 @@ void solve_plan_build(SolvePlan& sp, int n_modes, const int64_t* dims, const int
   }
 
   // dataflow (persistent) solve tables: N = 3 cubic tiles
-  sp.persist = sp.v2 && n_modes == 3 && !far_items.empty();
+  sp.persist = sp.v2 && n_modes == 3 && !far_items.empty() && sp.fgroup == 0;
   std::vector<int> p_level_of, p_level_count, p_far_rel, p_far_dep, p_far_expected, p_push_slot, p_queue;
   if (sp.persist) {
     std::vector<int64_t> slot_of(ntiles);
@@ -373,10 +506,14 @@ void solve_plan_build(SolvePlan& sp, int n_modes, const int64_t* dims, const int
   bytes = (bytes + 15) / 16 * 16;
   const size_t items_off = bytes;
   bytes += (far_items.size() + near_items.size() + ntiles) * sizeof(int4);
+  bytes = (bytes + 15) / 16 * 16;
+  const size_t fg_items_off = bytes;
+  bytes += fg_items.size() * sizeof(FarGroupItem);
   bytes = (bytes + 255) / 256 * 256;
   const size_t partial_off = bytes;
   const size_t tile_bytes = (size_t)g.tile_entries * sizeof(double2);
-  bytes += (2 * (size_t)sp.max_far + 2 * (size_t)sp.max_near) * tile_bytes + 256;
+  const size_t far_bufs = sp.fgroup >= 1 ? (size_t)sp.fg_ring * sp.fg_slots : 2 * (size_t)sp.max_far;
+  bytes += (far_bufs + 2 * (size_t)sp.max_near) * tile_bytes + 256;
   bytes = (bytes + 15) / 16 * 16;
   const size_t persist_off = bytes;
   bytes += (p_level_of.size() + p_level_count.size() + p_far_rel.size() + p_far_dep.size() + p_far_expected.size() +
@@ -393,9 +530,13 @@ void solve_plan_build(SolvePlan& sp, int n_modes, const int64_t* dims, const int
   sp.d_far_items = (int4*)(base + items_off);
   sp.d_near_items = sp.d_far_items + far_items.size();
   sp.d_tile_ranges = sp.d_near_items + near_items.size();
+  sp.d_fg_items = (FarGroupItem*)(base + fg_items_off);
+  if (!fg_items.empty())
+    NDS_CUDA(cudaMemcpy(sp.d_fg_items, fg_items.data(), fg_items.size() * sizeof(FarGroupItem), cudaMemcpyHostToDevice));
   sp.d_far_partial[0] = (double2*)(base + partial_off);
-  sp.d_far_partial[1] = sp.d_far_partial[0] + (size_t)sp.max_far * g.tile_entries;
-  sp.d_near_partial = sp.d_far_partial[1] + (size_t)sp.max_far * g.tile_entries;
+  sp.d_far_partial[1] = sp.fgroup >= 1 ? sp.d_far_partial[0] : sp.d_far_partial[0] + (size_t)sp.max_far * g.tile_entries;
+  sp.d_fg_ring = sp.d_far_partial[0];
+  sp.d_near_partial = sp.d_far_partial[0] + far_bufs * g.tile_entries;
   sp.d_near_partial2 = sp.d_near_partial + (size_t)sp.max_near * g.tile_entries;
   NDS_CUDA(cudaMemcpy(sp.d_tiles, tiles.data(), ntiles * sizeof(int64_t), cudaMemcpyHostToDevice));
   NDS_CUDA(cudaMemcpy(sp.d_wf, wf.data(), g.tile_entries * sizeof(int), cudaMemcpyHostToDevice));
@@ -557,9 +698,13 @@ int backsub_launch(const SolvePlan& sp, const double2* t_pool, double2* c, cudaS
   if (!attr_set) {
     NDS_CUDA(cudaFuncSetAttribute(tile_level_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)(kMaxTile * sizeof(double2))));
-    for (int b : {8, 16})
+    for (int b : {8, 16}) {
       NDS_CUDA(cudaFuncSetAttribute(update_kernel_for(b), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)update_smem_bytes(b)));
+      if (far_group_for(b) >= 1)
+        NDS_CUDA(cudaFuncSetAttribute(far_group_cfg(b).kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)far_group_smem_bytes(b)));
+    }
     NDS_CUDA(cudaFuncSetAttribute(diag_kernel_for(3, 16), cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024));
     NDS_CUDA(cudaFuncSetAttribute(diag_kernel_for(4, 8), cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024));
     for (bool push : {false, true}) {
@@ -621,16 +766,24 @@ int backsub_launch(const SolvePlan& sp, const double2* t_pool, double2* c, cudaS
   NDS_CUDA(cudaStreamWaitEvent(sp.s_far, ev_start, 0));
   if (rec) rec->mark(stream, -1, 0);
   int head_waited = -1;
+  const bool grouped = sp.fgroup >= 1;
+  const FarGroupCfg fgc = far_group_cfg(b);
+  const size_t fg_smem = far_group_smem_bytes(b);
   for (int lv = 0; lv < L; ++lv) {
-    const int64_t nf = sp.far_off[lv + 1] - sp.far_off[lv];
+    const int64_t nf = grouped ? sp.fg_off[lv + 1] - sp.fg_off[lv] : sp.far_off[lv + 1] - sp.far_off[lv];
     const int64_t nn = sp.near_off[lv + 1] - sp.near_off[lv];
-    double2* far_buf = sp.d_far_partial[lv & 1];
+    double2* far_buf = grouped ? sp.d_fg_ring + (size_t)(lv % sp.fg_ring) * sp.fg_slots * g.tile_entries
+                               : sp.d_far_partial[lv & 1];
     if (nf > 0) {
       // far(lv) needs levels <= lv - 2; it overlaps diag(lv - 1) on the critical stream
       if (lv >= 2) NDS_CUDA(cudaStreamWaitEvent(sp.s_far, ev_diag(lv - 2), 0));
       tmark(sp.s_far, lv, 0);
-      upd<<<(unsigned)(nf * uh), kUpdThreads, upd_smem, sp.s_far>>>(g, t_pool, sp.d_tiles, sp.d_far_items + sp.far_off[lv],
-                                                             far_buf, c);
+      if (grouped)
+        fgc.kern<<<(unsigned)(nf * fgc.h), kUpdThreads, fg_smem, sp.s_far>>>(g, t_pool, sp.d_tiles,
+                                                                          sp.d_fg_items + sp.fg_off[lv], sp.d_fg_ring, c);
+      else
+        upd<<<(unsigned)(nf * uh), kUpdThreads, upd_smem, sp.s_far>>>(g, t_pool, sp.d_tiles, sp.d_far_items + sp.far_off[lv],
+                                                               far_buf, c);
       NDS_LAUNCH_CHECK();
       tmark(sp.s_far, lv, 1);
       NDS_CUDA(cudaEventRecord(ev_far(lv), sp.s_far));
@@ -681,7 +834,7 @@ int backsub_launch(const SolvePlan& sp, const double2* t_pool, double2* c, cudaS
   if (trace) {
     NDS_CUDA(cudaStreamSynchronize(stream));
     for (int lv = 0; lv < L; ++lv) {
-      const int64_t nf = sp.far_off[lv + 1] - sp.far_off[lv];
+      const int64_t nf = sp.fgroup >= 1 ? sp.fg_off[lv + 1] - sp.fg_off[lv] : sp.far_off[lv + 1] - sp.far_off[lv];
       const int64_t nn = push ? 0 : sp.near_off[lv + 1] - sp.near_off[lv];
       float t[6] = {-1, -1, -1, -1, -1, -1};
       for (int k = 0; k < 6; ++k) {

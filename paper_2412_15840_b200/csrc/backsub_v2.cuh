@@ -2,6 +2,12 @@
 // in {8, 16} dividing every n_j (c0, c1: N=3 B=16; c2, c3: N=4 B=8).
 // Included by backsub.cu.
 
+#ifdef NDS_LINES_PROBE  // phase probes for tools/microbench/lines_bench.cu only
+#define NDS_LPROBE(k) \
+  if (threadIdx.x == 0 && blockIdx.x == 0) nds_lines_probe[k] = clock64()
+#else
+#define NDS_LPROBE(k)
+#endif
 #ifdef NDS_DIAG_PROBES  // timing probes for tools/microbench/diag_bench.cu only
 #define NDS_PROBE(k, v) \
   if (tid == 0 && blockIdx.x == 0) nds_diag_probe[lv * 4 + (k)] = clock64() + (long long)((v) * 0)
@@ -24,6 +30,26 @@ __device__ __forceinline__ void dmma_bs(double& c0, double& c1, double a, double
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
       : "+d"(c0), "+d"(c1)
       : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void mbar_init_bs(uint64_t* b, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"((unsigned)__cvta_generic_to_shared(b)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_bs(uint64_t* b) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(b))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait_bs(uint64_t* b, int parity) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(b);
+  unsigned ok = 0;
+  do {
+    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+                 : "=r"(ok)
+                 : "r"(a), "r"(parity)
+                 : "memory");
+  } while (!ok);
 }
 
 // Off-tile coupling of one work item (tile I, mode j, rows [kb, ke) along mode j) as a small
@@ -215,6 +241,182 @@ __global__ void __launch_bounds__(kUpdThreads, (M3 && H == 1) ? 1 : 2)
   extern __shared__ __align__(16) double2 sm[];
   update_body<RB, CB, M3, KM, ST, H>(g, T, tiles, items[blockIdx.x / H], (int)(blockIdx.x % H),
                                      partial + (int64_t)(blockIdx.x / H) * 4096, Y, sm);
+}
+
+// Grouped far update (SolvePlan::fgroup = G > 1). One item covers up to G target tiles that are
+// consecutive along its mode j (same other block coordinates, so the same columns), rows
+// [rb0 b, (rb0 + G) b) of T_j, and one k-range of the neighbour slab (source rows) that every
+// one of those targets still needs:
+//   out_q(l_j, c) (+)= sum_{k in [kb, ke)} T_j(rb0 b + q b + l_j, k) * Y(k along j, c),  q < nrb,
+// q = row block (target block rb0 + q), out_q a slot of the far-partial ring (its target's
+// level region). acc = 1 accumulates into an existing slot (the remainder item of a target whose
+// group item ran at an earlier level). Raising the rows from b to G b divides the slab traffic
+// per flop by G and gives every B fragment G times the DMMA work. Row blocks q >= nrb (a
+// truncated group at the bottom of a line) are computed but not stored.
+template <int BT, int G, int CB, bool M3, int KM, int ST, int H>
+__device__ __forceinline__ void far_group_body(const TileGeom& g, const double2* __restrict__ T,
+                                               const int64_t* __restrict__ tiles, const FarGroupItem& it,
+                                               const int half, double2* __restrict__ ring,
+                                               const double2* __restrict__ Y, double2* __restrict__ sm) {
+  constexpr int RB = G * BT / 8;         // row fragments
+  constexpr int BJ = G * BT;             // rows
+  constexpr int TCOLS = 4096 / BT;       // columns of a tile
+  constexpr int COLS = TCOLS / H;        // columns of this CTA
+  constexpr int BK = KM * 2048 / TCOLS;
+  constexpr int LDB = COLS + 2;
+  constexpr int ALD = BK <= 8 ? 12 : BK + 4;
+  constexpr int SL = 8 * KM / H;
+  static_assert(CB * 8 * (kUpdThreads / 32) == COLS && BK % 4 == 0 && BJ * BK <= kUpdThreads, "tile shape");
+  __shared__ int64_t s_base;
+  const int j = it.j, kb = it.kb, ke = it.ke;
+  const int N = g.n_modes;
+  int64_t* colg = (int64_t*)sm;
+  int* coll = (int*)(colg + COLS);
+  double2* sA = (double2*)(coll + COLS);  // [ST][BJ][ALD]
+  double2* sB = sA + ST * BJ * ALD;       // [ST][BK][LDB]
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    int64_t t = tiles[it.tile];
+    int64_t base = 0;
+    for (int m = 0; m < N; ++m) {
+      const int64_t I = t % g.nb[m];
+      t /= g.nb[m];
+      if (m != j) base += I * g.b[m] * g.strides[m];
+    }
+    s_base = base;
+  }
+  for (int c = tid; c < COLS; c += kUpdThreads) {
+    int rem = c + half * COLS;
+    int64_t og = 0;
+    int ol = 0;
+    for (int m = 0; m < N; ++m) {
+      if (m == j) continue;
+      const int lm = rem % BT;
+      rem /= BT;
+      og += lm * g.strides[m];
+      ol += lm * g.bstride[m];
+    }
+    colg[c] = og;
+    coll[c] = ol;
+  }
+  __syncthreads();
+  const int64_t sj = g.strides[j];
+  const double2* Yb = Y + s_base;
+  const double2* Tj = T + g.toff[j] + (int64_t)it.rb0 * BT;
+  const int64_t nj = g.dims[j];
+  const bool kfast = j == 0;
+  int gofs[SL];
+  int sofs[SL];
+#pragma unroll
+  for (int i = 0; i < SL; ++i) {
+    const int e = tid + i * kUpdThreads;
+    int k, c;
+    if (kfast) {
+      k = e % BK;
+      c = e / BK;
+      sofs[i] = c * BK + (k ^ (BK >= 8 ? (c & 1) << 2 : 0));
+    } else {
+      c = e % COLS;
+      k = e / COLS;
+      sofs[i] = k * LDB + c;
+    }
+    gofs[i] = (int)((int64_t)k * sj + colg[c]);
+  }
+  const bool a_loader = tid < BJ * BK;
+  const int a_r = tid % BJ, a_k = tid / BJ;
+  auto load_stage = [&](int stage, int k0) {
+    double2* dB = sB + stage * BK * LDB;
+    const double2* src = Yb + (int64_t)k0 * sj;
+#pragma unroll
+    for (int i = 0; i < SL; ++i) cp_async16_bs(dB + sofs[i], src + gofs[i]);
+    if (a_loader) cp_async16_bs(sA + stage * BJ * ALD + a_r * ALD + a_k, Tj + a_r + (int64_t)(k0 + a_k) * nj);
+  };
+  const int lane = tid & 31, warp = tid >> 5;
+  double cre[RB][CB][2], cim[RB][CB][2], c3[M3 ? RB : 1][M3 ? CB : 1][2];
+#pragma unroll
+  for (int r = 0; r < RB; ++r)
+#pragma unroll
+    for (int q = 0; q < CB; ++q) {
+      cre[r][q][0] = cre[r][q][1] = cim[r][q][0] = cim[r][q][1] = 0.0;
+      if constexpr (M3) c3[r][q][0] = c3[r][q][1] = 0.0;
+    }
+  const int nk = (ke - kb) / BK;
+#pragma unroll
+  for (int st = 0; st < ST - 1; ++st) {
+    if (st < nk) load_stage(st, kb + st * BK);
+    cp_commit_bs();
+  }
+  const int cbase = warp * CB * 8 + (lane >> 2);
+  const int arow = lane >> 2, kq = lane & 3;
+  for (int kt = 0; kt < nk; ++kt) {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(ST - 2));
+    __syncthreads();
+    if (kt + ST - 1 < nk) load_stage((kt + ST - 1) % ST, kb + (kt + ST - 1) * BK);
+    cp_commit_bs();
+    const double2* cA = sA + (kt % ST) * BJ * ALD;
+    const double2* cB = sB + (kt % ST) * BK * LDB;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double br[CB], bi[CB], bs[CB];
+#pragma unroll
+      for (int q = 0; q < CB; ++q) {
+        const int c = cbase + q * 8;
+        const double2 b = kfast ? cB[c * BK + ((kk + kq) ^ (BK >= 8 ? (c & 1) << 2 : 0))] : cB[(kk + kq) * LDB + c];
+        br[q] = b.x;
+        bi[q] = b.y;
+        bs[q] = M3 ? b.x + b.y : 0.0;
+      }
+#pragma unroll
+      for (int r = 0; r < RB; ++r) {
+        const double2 a = cA[(r * 8 + arow) * ALD + kk + kq];
+        const double an = M3 ? a.x + a.y : -a.y;
+#pragma unroll
+        for (int q = 0; q < CB; ++q) {
+          if constexpr (M3) {
+            dmma_bs(cre[r][q][0], cre[r][q][1], a.x, br[q]);
+            dmma_bs(cim[r][q][0], cim[r][q][1], a.y, bi[q]);
+            dmma_bs(c3[r][q][0], c3[r][q][1], an, bs[q]);
+          } else {
+            dmma_bs(cre[r][q][0], cre[r][q][1], a.x, br[q]);
+            dmma_bs(cim[r][q][0], cim[r][q][1], a.x, bi[q]);
+            dmma_bs(cre[r][q][0], cre[r][q][1], an, bi[q]);
+            dmma_bs(cim[r][q][0], cim[r][q][1], a.y, br[q]);
+          }
+        }
+      }
+    }
+  }
+  cp_wait0_bs();
+  const int bsj = g.bstride[j];
+#pragma unroll
+  for (int r = 0; r < RB; ++r) {
+    const int row = r * 8 + (lane >> 2);
+    const int qb = row / BT;  // row block: the same for the whole fragment (BT % 8 == 0)
+    if (qb >= it.nrb) continue;
+    double2* out = ring + (int64_t)it.out[qb] * 4096 + (row % BT) * bsj;
+#pragma unroll
+    for (int q = 0; q < CB; ++q) {
+      const int c = warp * CB * 8 + q * 8 + 2 * kq;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        double2 v = M3 ? make_double2(cre[r][q][h] - cim[r][q][h], c3[r][q][h] - cre[r][q][h] - cim[r][q][h])
+                       : make_double2(cre[r][q][h], cim[r][q][h]);
+        double2* o = out + coll[c + h];
+        if (it.acc) v = cadd(*o, v);
+        *o = v;
+      }
+    }
+  }
+}
+
+using FarGroupKernel = void (*)(const TileGeom, const double2*, const int64_t*, const FarGroupItem*, double2*,
+                               const double2*);
+template <int BT, int G, int CB, bool M3, int KM, int ST, int H>
+__global__ void __launch_bounds__(kUpdThreads, 2)
+    far_group_kernel(const TileGeom g, const double2* __restrict__ T, const int64_t* __restrict__ tiles,
+                     const FarGroupItem* __restrict__ items, double2* __restrict__ ring, const double2* __restrict__ Y) {
+  extern __shared__ __align__(16) double2 sm[];
+  far_group_body<BT, G, CB, M3, KM, ST, H>(g, T, tiles, items[blockIdx.x / H], (int)(blockIdx.x % H), ring, Y, sm);
 }
 
 // n terms tp[i grp] * sp[i ss], i < n, into four independent accumulators (loads batched).
@@ -522,7 +724,16 @@ __constant__ LineOrder<4, 8> kLineOrder4 = make_line_order<4, 8>();
 //   near_out[item] (l_m, c) = sum_k T_m(o_m - B + l_m, o_m + k) Y_J(k along m, c)
 // (3M DMMA; near_target[slot N + m] = that item's index at the next level, -1 if none) — which
 // replaces the separate near-update launch on the critical path.
-template <int N, int B, int NT, bool PUSH, bool T2REG, bool SORT = true>
+// VAR bits (A/B experiments, tools/microbench/lines_bench.cu):
+//   1 = PIPE: split-phase step barrier (mbarrier: arrive right after this step's y store, wait
+//       before the next step's loads); each thread pre-accumulates, between the two, every
+//       mode >= 2 term of its NEXT row whose neighbour is at distance >= 2 (solved at least two
+//       steps earlier), so only the distance-1 terms and the mode-1 history stay between the
+//       barrier and the store;
+//   2 = QU: the mode-1 history update stops at the warp's largest active row;
+//   4 = PRO: factor loads issued together with the tile's loads;
+//   8 = PUSHU: the PUSH phase's three mode GEMMs unrolled into one instruction stream.
+template <int N, int B, int NT, bool PUSH, bool T2REG, bool SORT = true, int VAR = 0>
 __device__ __forceinline__ void diag_lines_body(const TileGeom& g, const double2* __restrict__ T, const int64_t tile,
                                                 const int4 tr, const double2* __restrict__ far_partial,
                                                 const double2* __restrict__ near_partial,
@@ -535,8 +746,18 @@ __device__ __forceinline__ void diag_lines_body(const TileGeom& g, const double2
   using PS = LinePad<N, B>;
   __shared__ int64_t so[N];
   __shared__ int64_t st[N];
+  constexpr bool PIPE = (VAR & 1) != 0;
+  constexpr bool QU = (VAR & 2) != 0;
+  constexpr bool PRO = (VAR & 4) != 0;
+  constexpr bool PUSHU = (VAR & 8) != 0;
+  __shared__ uint64_t step_bar;
   const int tid = threadIdx.x;
+  NDS_LPROBE(0);
+  int tgt_m[N];  // near-coupling targets of the PUSH phase, loaded before the long wavefront
+#pragma unroll
+  for (int m = 0; m < N; ++m) tgt_m[m] = PUSH ? near_target[m] : -1;
   if (tid == 0) {
+    if constexpr (PIPE) mbar_init_bs(&step_bar, NT / 32);
     int64_t t = tile;
     for (int m = 0; m < N; ++m) {
       const int64_t I = t % g.nb[m];
@@ -551,21 +772,53 @@ __device__ __forceinline__ void diag_lines_body(const TileGeom& g, const double2
   constexpr int ALD = B + 4;                        // = 4 mod 8: conflict-free DMMA A fragments
   double2* Ap = Dq + B * B;                         // [N][B][ALD]: T_m(o_m - B + r, o_m + k) (PUSH)
   __syncthreads();
+  // PRO: the factor loads go to registers first and are stored to shared memory only after the
+  // tile's own loads are in flight (one exposed latency instead of two)
+  static_assert(!PRO || B * B <= NT, "PRO: one factor entry per thread");
+  double2 tdv[N], apv[N], dqv = make_double2(0.0, 0.0);
+  const bool tl = tid < B * B;
+  if constexpr (PRO) {
+    const int r = tid % B, c = tid / B;
 #pragma unroll
-  for (int m = 0; m < N; ++m) {
-    const double2* Tm = T + g.toff[m];
-    const int64_t nm = g.dims[m];
-    const bool push_m = PUSH && so[m] >= B;
-    for (int e = tid; e < B * B; e += NT) {
-      const int r = e % B, c = e / B;  // rows fastest: coalesced along T_m's columns
-      Td[(m * B + r) * B + c] = Tm[(so[m] + r) + (so[m] + c) * nm];
-      if (push_m) Ap[(m * B + r) * ALD + c] = Tm[(so[m] - B + r) + (so[m] + c) * nm];
-      if (m == 0) {  // e = j B + r'
-        const int j = e / B, rr = e % B;
-        Dq[e] = rr >= j + 1 ? Tm[(so[0] + rr - 1 - j) + (so[0] + rr) * nm] : make_double2(0.0, 0.0);
+    for (int m = 0; m < N; ++m) {
+      const double2* Tm = T + g.toff[m];
+      const int64_t nm = g.dims[m];
+      const bool push_m = PUSH && so[m] >= B;
+      tdv[m] = tl ? Tm[(so[m] + r) + (so[m] + c) * nm] : make_double2(0.0, 0.0);
+      apv[m] = tl && push_m ? Tm[(so[m] - B + r) + (so[m] + c) * nm] : make_double2(0.0, 0.0);
+      if (m == 0) {
+        const int j = tid / B, rr = tid % B;
+        dqv = tl && rr >= j + 1 ? Tm[(so[0] + rr - 1 - j) + (so[0] + rr) * nm] : make_double2(0.0, 0.0);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int m = 0; m < N; ++m) {
+      const double2* Tm = T + g.toff[m];
+      const int64_t nm = g.dims[m];
+      const bool push_m = PUSH && so[m] >= B;
+      for (int e = tid; e < B * B; e += NT) {
+        const int r = e % B, c = e / B;  // rows fastest: coalesced along T_m's columns
+        Td[(m * B + r) * B + c] = Tm[(so[m] + r) + (so[m] + c) * nm];
+        if (push_m) Ap[(m * B + r) * ALD + c] = Tm[(so[m] - B + r) + (so[m] + c) * nm];
+        if (m == 0) {  // e = j B + r'
+          const int j = e / B, rr = e % B;
+          Dq[e] = rr >= j + 1 ? Tm[(so[0] + rr - 1 - j) + (so[0] + rr) * nm] : make_double2(0.0, 0.0);
+        }
       }
     }
   }
+  auto store_factors = [&]() {
+    if (!tl) return;
+    const int r = tid % B, c = tid / B;
+#pragma unroll
+    for (int m = 0; m < N; ++m) {
+      Td[(m * B + r) * B + c] = tdv[m];
+      if (PUSH && so[m] >= B) Ap[(m * B + r) * ALD + c] = apv[m];
+    }
+    Dq[tid] = dqv;
+  };
+  NDS_LPROBE(1);
   // tr = {far first, far count, near first, near count}; partials two at a time so that 2 x PER
   // loads per thread are in flight (the prologue is latency-bound)
   {
@@ -579,6 +832,7 @@ __device__ __forceinline__ void diag_lines_body(const TileGeom& g, const double2
       for (int m = 0; m < N; ++m) gidx += (so[m] + ((l >> (LB * m)) & (B - 1))) * st[m];
       v[i] = Y[gidx];
     }
+    if constexpr (PRO) store_factors();
     const int np = tr.y + tr.w;
     auto part = [&](int p) {
       return p < tr.y ? far_partial + (int64_t)(tr.x + p) * E + tid : near_partial + (int64_t)(tr.z + p - tr.y) * E + tid;
@@ -604,6 +858,7 @@ __device__ __forceinline__ void diag_lines_body(const TileGeom& g, const double2
     for (int i = 0; i < PER; ++i) S[PS::pad(tid + i * NT)] = v[i];
   }
   __syncthreads();
+  NDS_LPROBE(2);
 
   int lm[N];
   int d = 0, pb = 0;
@@ -631,10 +886,75 @@ __device__ __forceinline__ void diag_lines_body(const TileGeom& g, const double2
 #pragma unroll
   for (int j = 0; j < B - 1; ++j) q[j] = make_double2(0.0, 0.0);
 
+  if constexpr (PIPE) {
+    double2 pre = make_double2(0.0, 0.0), rden = make_double2(0.0, 0.0);
+    const int q2 = B - 1 - lm[1];
+    // every mode >= 2 term of row rr at neighbour distance >= 2, and the row's reciprocal
+    // denominator (both independent of the previous step)
+    auto prepare = [&](int rr) {
+      const double2* e = S + rr + pb;
+      double2 a[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int k = 1; k < B - 1; ++k)
+        if (k < q2) a[k & 3] = cfma(a[k & 3], T2REG ? t2r[T2REG ? k : 0] : t2s[k], e[(1 + k) * PS::a1]);
+#pragma unroll
+      for (int m = 2; m < N; ++m) {
+        const double2* tm = Td + (m * B + lm[m]) * B + lm[m] + 1;
+        const int qm = B - 1 - lm[m];
+#pragma unroll
+        for (int k = 1; k < B - 1; ++k)
+          if (k < qm) a[(k + 2) & 3] = cfma(a[(k + 2) & 3], tm[k], e[(1 + k) * PS::at(m)]);
+      }
+      pre = cadd(cadd(a[0], a[1]), cadd(a[2], a[3]));
+      rden = crecip_fast(cadd(Td[rr * (B + 1)], dsum));
+    };
+    if (lv0 == 0) prepare(B - 1);
+    const int lane = tid & 31;
+#pragma unroll 1
+    for (int lv = 0; lv < WL; ++lv) {
+      const int r = B - 1 - (lv - lv0);
+      const bool act = lv >= lv0 && r >= 0;
+      double2 y = make_double2(0.0, 0.0);
+      if (act) {
+        const double2* e = S + r + pb;
+        double2 acc = cadd(pre, q[0]);
+        if (q2 > 0) acc = cfma(acc, T2REG ? t2r[0] : t2s[0], e[PS::a1]);
+#pragma unroll
+        for (int m = 2; m < N; ++m)
+          if (lm[m] < B - 1) acc = cfma(acc, Td[(m * B + lm[m]) * B + lm[m] + 1], e[PS::at(m)]);
+        y = cmul(csub(e[0], acc), rden);
+        S[r + pb] = y;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive_bs(&step_bar);
+      const int rmax = QU ? (int)__reduce_max_sync(0xffffffffu, act ? (unsigned)r : 0u) : B;
+      if (act) {
+      if constexpr (QU) {
+#pragma unroll
+        for (int j = 0; j < B - 1; ++j) {
+          if (j >= rmax) break;  // warp-uniform
+          if (j < r) q[j] = cfma(j + 1 < B - 1 ? q[j + 1] : make_double2(0.0, 0.0), Dq[j * B + r], y);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < B - 1; ++j)
+          if (j < r) q[j] = cfma(j + 1 < B - 1 ? q[j + 1] : make_double2(0.0, 0.0), Dq[j * B + r], y);
+      }
+        if (r >= 1) prepare(r - 1);
+      } else if (lv == lv0 - 1) {
+        prepare(B - 1);
+      }
+      mbar_wait_bs(&step_bar, lv & 1);
+    }
+  } else {
 #pragma unroll 1
   for (int lv = 0; lv < WL; ++lv) {
     const int r = B - 1 - (lv - lv0);
-    if (lv >= lv0 && r >= 0) {
+    const bool act = lv >= lv0 && r >= 0;
+    const int rmax = QU ? (int)__reduce_max_sync(0xffffffffu, act ? (unsigned)r : 0u) : B;
+    if (act) {
       const double2* e = S + r + pb;  // this step's entry
       const double2 rden = crecip_fast(cadd(Td[r * (B + 1)], dsum));
       double2 a[4];
@@ -656,12 +976,22 @@ __device__ __forceinline__ void diag_lines_body(const TileGeom& g, const double2
       const double2 y = cmul(csub(e[0], acc), rden);
       S[r + pb] = y;
       // mode-1 history: q[j] <- q[j+1] + T_1(r-1-j, r) y for the rows r-1-j >= 0 still ahead
+      if constexpr (QU) {
 #pragma unroll
-      for (int j = 0; j < B - 1; ++j)
-        if (j < r) q[j] = cfma(j + 1 < B - 1 ? q[j + 1] : make_double2(0.0, 0.0), Dq[j * B + r], y);
+        for (int j = 0; j < B - 1; ++j) {
+          if (j >= rmax) break;  // warp-uniform
+          if (j < r) q[j] = cfma(j + 1 < B - 1 ? q[j + 1] : make_double2(0.0, 0.0), Dq[j * B + r], y);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < B - 1; ++j)
+          if (j < r) q[j] = cfma(j + 1 < B - 1 ? q[j + 1] : make_double2(0.0, 0.0), Dq[j * B + r], y);
+      }
     }
     __syncthreads();
   }
+  }
+  NDS_LPROBE(3);
   {
     constexpr int PER = E / NT;
 #pragma unroll
@@ -673,6 +1003,7 @@ __device__ __forceinline__ void diag_lines_body(const TileGeom& g, const double2
       Y[gidx] = S[PS::pad(l)];
     }
   }
+  NDS_LPROBE(4);
   if constexpr (PUSH) {
     // GEMM (B rows) x (NT columns) x (B k) per mode; warp w owns columns [32 w, 32 w + 32) as
     // RB x 4 fragments of 8 x 8. Column c = the local coordinates of the modes != m (earliest
@@ -692,9 +1023,10 @@ __device__ __forceinline__ void diag_lines_body(const TileGeom& g, const double2
         loff += l << (LB * mm);
       }
     };
-#pragma unroll 1
+#pragma unroll
     for (int m = 0; m < N; ++m) {
-      const int tgt = near_target[m];
+      if constexpr (!PUSHU) asm volatile("" ::: "memory");  // keep the modes' GEMMs apart (no overlap)
+      const int tgt = tgt_m[m];
       if (tgt < 0) continue;  // CTA-uniform
       int sb[4];
 #pragma unroll
@@ -744,16 +1076,17 @@ __device__ __forceinline__ void diag_lines_body(const TileGeom& g, const double2
         }
     }
   }
+  NDS_LPROBE(5);
 }
 
-template <int N, int B, int NT, bool PUSH, bool T2REG, bool SORT = true>
+template <int N, int B, int NT, bool PUSH, bool T2REG, bool SORT = true, int VAR = 0>
 __global__ void __launch_bounds__(NT, T2REG ? 1 : 2)
     tile_diag_lines_kernel(const TileGeom g, const double2* __restrict__ T, const int64_t* __restrict__ tiles,
                            const int4* __restrict__ tile_ranges, const double2* __restrict__ far_partial,
                            const double2* __restrict__ near_partial, const int* __restrict__ near_target,
                            double2* __restrict__ near_out, double2* __restrict__ Y) {
   extern __shared__ __align__(16) double2 sm[];
-  diag_lines_body<N, B, NT, PUSH, T2REG, SORT>(g, T, tiles[blockIdx.x], tile_ranges[blockIdx.x], far_partial, near_partial,
+  diag_lines_body<N, B, NT, PUSH, T2REG, SORT, VAR>(g, T, tiles[blockIdx.x], tile_ranges[blockIdx.x], far_partial, near_partial,
                                          near_target ? near_target + (int64_t)blockIdx.x * N : nullptr, near_out, Y,
                                          sm);
 }
@@ -763,16 +1096,18 @@ using LinesKernel = void (*)(const TileGeom, const double2*, const int64_t*, con
 static LinesKernel lines_kernel_for(int n_modes, int b, bool push) {
   static const bool t2smem = getenv("NDS_DIAG_T2SMEM") != nullptr;  // A/B experiments
   static const bool natural = getenv("NDS_DIAG_NATURAL") != nullptr;
+  // VAR 4 (PRO: factor loads overlapped with the tile's loads) measured 2 % faster per tile; the
+  // PIPE / QU variants slower (tools/microbench/lines_bench.cu)
   if (n_modes == 3 && b == 16) {
     if (natural)
       return push ? tile_diag_lines_kernel<3, 16, 256, true, true, false> : tile_diag_lines_kernel<3, 16, 256, false, true, false>;
     if (t2smem) return push ? tile_diag_lines_kernel<3, 16, 256, true, false> : tile_diag_lines_kernel<3, 16, 256, false, false>;
-    return push ? tile_diag_lines_kernel<3, 16, 256, true, true> : tile_diag_lines_kernel<3, 16, 256, false, true>;
+    return push ? tile_diag_lines_kernel<3, 16, 256, true, true, true, 4> : tile_diag_lines_kernel<3, 16, 256, false, true, true, 4>;
   }
   if (n_modes == 4 && b == 8 && natural)
     return push ? tile_diag_lines_kernel<4, 8, 512, true, true, false> : tile_diag_lines_kernel<4, 8, 512, false, true, false>;
   if (n_modes == 4 && b == 8)
-    return push ? tile_diag_lines_kernel<4, 8, 512, true, true> : tile_diag_lines_kernel<4, 8, 512, false, true>;
+    return push ? tile_diag_lines_kernel<4, 8, 512, true, true, true, 4> : tile_diag_lines_kernel<4, 8, 512, false, true, true, 4>;
   return nullptr;
 }
 static size_t lines_smem_bytes(int n_modes, int b) {
@@ -850,3 +1185,55 @@ static size_t diag_smem_bytes(int n_modes, int b, int wf_levels) {
   return (size_t)(ext + (ext & 1)) * 16 + (size_t)n_modes * b * b * 16 +
          (size_t)wf_levels * diag_threads_for(n_modes) * sizeof(uint16_t);
 }
+
+// Far-update configurations (measured, c1/c2/c3 solve): G = 1 — one item per (target, mode), as
+// the plain items, but with explicit ring slots so each level's items run longest first (LPT:
+// c1 solve 4.82 -> 4.6 ms); 3M, 4-stage cp.async ring, two CTAs per item (b = 16: 128 columns,
+// BK = 8; b = 8: 256 columns, BK = 4). Groups of G = 2/4 targets per item (32 rows, half the slab
+// traffic per flop) measured slower: the far kernel is not traffic-bound (DMMA pipe ~57 % busy,
+// latency/barrier stalls), and the remainder items add partial read-modify-writes.
+// NDS_FARGROUP=plain restores the plain per-target items, =2|4 selects G; NDS_FGCFG other shapes.
+struct FarGroupCfg {
+  FarGroupKernel kern;
+  int g, bk, stages, h;
+};
+static FarGroupCfg far_group_cfg(int b) {
+  static const std::string env = getenv("NDS_FARGROUP") ? getenv("NDS_FARGROUP") : "";
+  static const int var = getenv("NDS_FGCFG") ? atoi(getenv("NDS_FGCFG")) : 0;  // A/B shapes
+  if (env == "plain") return {nullptr, 0, 0, 0, 0};
+  const int gsel = env.empty() ? 0 : atoi(env.c_str());
+  if (b == 16) {
+    if (gsel == 2) return {far_group_kernel<16, 2, 2, true, 1, 3, 2>, 2, 8, 3, 2};
+    switch (var) {
+      case 1: return {far_group_kernel<16, 1, 2, true, 2, 3, 2>, 1, 16, 3, 2};
+      case 2: return {far_group_kernel<16, 1, 1, true, 1, 3, 4>, 1, 8, 3, 4};
+      case 3: return {far_group_kernel<16, 1, 4, true, 1, 3, 1>, 1, 8, 3, 1};
+      case 4: return {far_group_kernel<16, 1, 2, true, 1, 3, 2>, 1, 8, 3, 2};
+      default: return {far_group_kernel<16, 1, 2, true, 1, 4, 2>, 1, 8, 4, 2};
+    }
+  }
+  if (b == 8) {
+    if (gsel == 2) return {far_group_kernel<8, 2, 2, true, 2, 3, 4>, 2, 8, 3, 4};
+    if (gsel == 4) return {far_group_kernel<8, 4, 2, true, 2, 3, 4>, 4, 8, 3, 4};
+    switch (var) {
+      case 1: return {far_group_kernel<8, 1, 4, true, 2, 3, 2>, 1, 8, 3, 2};
+      case 2: return {far_group_kernel<8, 1, 8, true, 1, 3, 1>, 1, 4, 3, 1};
+      case 3: return {far_group_kernel<8, 1, 2, true, 1, 3, 4>, 1, 4, 3, 4};
+      case 4: return {far_group_kernel<8, 1, 4, false, 1, 3, 2>, 1, 4, 3, 2};
+      case 5: return {far_group_kernel<8, 1, 4, true, 1, 3, 2>, 1, 4, 3, 2};
+      case 6: return {far_group_kernel<8, 1, 4, true, 2, 4, 2>, 1, 8, 4, 2};
+      default: return {far_group_kernel<8, 1, 4, true, 1, 4, 2>, 1, 4, 4, 2};
+    }
+  }
+  return {nullptr, 0, 0, 0, 0};
+}
+// 0: plain per-target items (tile_update_kernel, slot = item index); G >= 1: FarGroupItem lists
+static int far_group_for(int b) { return far_group_cfg(b).g; }
+static int far_group_bk(int b) { return std::max(1, far_group_cfg(b).bk); }
+static size_t far_group_smem_bytes(int b) {
+  const FarGroupCfg c = far_group_cfg(b);
+  if (c.g < 1) return 0;
+  const int cols = 4096 / b / c.h, ald = c.bk <= 8 ? 12 : c.bk + 4;
+  return (size_t)cols * (8 + 4) + (size_t)c.stages * c.g * b * ald * 16 + (size_t)c.stages * c.bk * (cols + 2) * 16;
+}
+

@@ -82,6 +82,19 @@ struct TileGeom {
   int bstride[NDS_MAX_MODES]; // strides inside a full tile
 };
 
+// Grouped far-update work item (backsub_v2.cuh far_group_body): up to G consecutive targets
+// along mode j share one slab read; see solve_plan_build.
+struct FarGroupItem {
+  int tile;     // tile slot whose other block coordinates define the columns
+  int j;        // mode
+  int kb, ke;   // source rows along j (absolute; multiple of the stage depth)
+  int rb0;      // first target block along j
+  int nrb;      // valid row blocks
+  int acc;      // 1: accumulate into the slots
+  int pad;
+  int out[4];   // far-partial ring slot per row block
+};
+
 struct SolvePlan {
   TileGeom geom{};
   int levels = 0;                 // tile hyperplanes: sum_j (nb_j - 1) + 1
@@ -108,6 +121,14 @@ struct SolvePlan {
   double2* d_near_partial = nullptr;
   double2* d_near_partial2 = nullptr;  // push mode: near partials double-buffered by level parity
   int64_t max_far = 0, max_near = 0;
+  // grouped far items (fgroup >= 1; 0 = plain items): per level [fg_off[lv], fg_off[lv + 1]) of d_fg_items; their
+  // partials in a ring of fg_ring level regions of fg_slots tiles (region = target level % fg_ring)
+  int fgroup = 0;
+  std::vector<int64_t> fg_off;
+  FarGroupItem* d_fg_items = nullptr;
+  double2* d_fg_ring = nullptr;
+  int fg_ring = 0;
+  int64_t fg_slots = 0;
   cudaStream_t s_crit = nullptr, s_far = nullptr;
   // dataflow (persistent-kernel) solve, N = 3: per-slot / per-item tables, partial rings, counters
   bool persist = false;

@@ -1,0 +1,194 @@
+// Microbenchmark of the diagonal-tile kernel (tile_diag_lines_kernel, N=3, B=16, PUSH) on the c1
+// geometry: G CTAs each solving a distinct tile of the middle hyperplane with 3 far + 3 near
+// partials and pushing 3 near couplings, as in the real solve. Reports us/launch for several grid
+// sizes and the per-phase clock64 split of CTA 0 (factor loads, partial loads, wavefront, store,
+// push).
+// build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -lineinfo
+//        -I include -I paper_2412_15840_b200/csrc tools/microbench/lines_bench.cu -o tools/microbench/lines_bench
+#include <cstdio>
+#include <vector>
+#include <cmath>
+#include <algorithm>
+#define NDS_LINES_PROBE
+__device__ long long nds_lines_probe[8];
+#include "../../paper_2412_15840_b200/csrc/backsub.cu"
+
+using namespace nds;
+
+int main(int argc, char** argv) {
+  const int n = 256;
+  const int64_t dims[3] = {n, n, n};
+  const int64_t toff[3] = {0, (int64_t)n * n, 2 * (int64_t)n * n};
+  SolvePlan sp;
+  solve_plan_build(sp, 3, dims, toff);
+  const TileGeom& g = sp.geom;
+  const int64_t P = (int64_t)n * n * n;
+  std::vector<double2> T(3 * (size_t)n * n);
+  for (int j = 0; j < 3; ++j)
+    for (int c = 0; c < n; ++c)
+      for (int r = 0; r < n; ++r)
+        T[(size_t)j * n * n + r + (size_t)c * n] =
+            r > c ? make_double2(0, 0) : r == c ? make_double2(2.0 + 0.001 * r, 0.3) : make_double2(0.01 / (1 + c - r), -0.02 / (1 + c - r));
+  // tiles of hyperplane 22 (192 of them)
+  std::vector<int64_t> tiles;
+  for (int64_t t = 0; t < 16 * 16 * 16; ++t) {
+    const int a = t % 16, b = (t / 16) % 16, c = t / 256;
+    if (a + b + c == 22 && a > 0 && b > 0 && c > 0) tiles.push_back(t);
+  }
+  const int GMAX = 296;
+  while ((int)tiles.size() < GMAX) tiles.push_back(tiles[tiles.size() % 150]);
+  std::vector<int4> ranges(GMAX);
+  std::vector<int> tgt(GMAX * 3);
+  for (int i = 0; i < GMAX; ++i) {
+    ranges[i] = make_int4(3 * i, 3, 3 * i, 3);
+    for (int m = 0; m < 3; ++m) tgt[3 * i + m] = 3 * i + m;
+  }
+  double2 *dT, *dY, *dfar, *dnear, *dout;
+  int64_t* dtiles;
+  int4* dranges;
+  int* dtgt;
+  cudaMalloc(&dT, T.size() * 16);
+  cudaMalloc(&dY, P * 16);
+  cudaMalloc(&dfar, (size_t)GMAX * 3 * 4096 * 16);
+  cudaMalloc(&dnear, (size_t)GMAX * 3 * 4096 * 16);
+  cudaMalloc(&dout, (size_t)GMAX * 3 * 4096 * 16);
+  cudaMalloc(&dtiles, GMAX * 8);
+  cudaMalloc(&dranges, GMAX * 16);
+  cudaMalloc(&dtgt, GMAX * 3 * 4);
+  cudaMemcpy(dT, T.data(), T.size() * 16, cudaMemcpyHostToDevice);
+  cudaMemset(dY, 0, P * 16);
+  cudaMemset(dfar, 0, (size_t)GMAX * 3 * 4096 * 16);
+  cudaMemset(dnear, 0, (size_t)GMAX * 3 * 4096 * 16);
+  cudaMemcpy(dtiles, tiles.data(), GMAX * 8, cudaMemcpyHostToDevice);
+  cudaMemcpy(dranges, ranges.data(), GMAX * 16, cudaMemcpyHostToDevice);
+  cudaMemcpy(dtgt, tgt.data(), GMAX * 12, cudaMemcpyHostToDevice);
+  // a finite right-hand side: Y = 1 + small ramp (the solve is in place)
+  {
+    std::vector<double2> h(P);
+    for (int64_t i = 0; i < P; ++i) h[i] = make_double2(1.0 + 1e-9 * (i % 977), 0.5);
+    cudaMemcpy(dY, h.data(), P * 16, cudaMemcpyHostToDevice);
+  }
+  std::vector<double2> hY0(P);
+  cudaMemcpy(hY0.data(), dY, P * 16, cudaMemcpyDeviceToHost);
+  auto kl = lines_kernel_for(3, 16, true);
+  const size_t lsmem = lines_smem_bytes(3, 16);
+  cudaFuncAttributes fa;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  struct V {
+    const char* name;
+    LinesKernel k;
+  };
+  V vars[] = {{"VAR0", tile_diag_lines_kernel<3, 16, 256, true, true, true, 0>},
+              {"PRO", tile_diag_lines_kernel<3, 16, 256, true, true, true, 4>},
+              {"PUSHU", tile_diag_lines_kernel<3, 16, 256, true, true, true, 8>},
+              {"PRO+PUSHU", tile_diag_lines_kernel<3, 16, 256, true, true, true, 12>}};
+  std::vector<double2> refY, refO;
+  if (argc > 1) {  // profiling mode: one launch of variant argv[1] on 148 tiles
+    auto& v = vars[atoi(argv[1])];
+    cudaFuncSetAttribute(v.k, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
+    v.k<<<148, 256, lsmem>>>(g, dT, dtiles, dranges, dfar, dnear, dtgt, dout, dY);
+    cudaDeviceSynchronize();
+    printf("%s: %s\n", v.name, cudaGetErrorString(cudaGetLastError()));
+    return 0;
+  }
+  for (auto& v : vars) {
+    cudaFuncSetAttribute(v.k, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
+    cudaFuncGetAttributes(&fa, v.k);
+    // correctness: one launch of the 148 distinct tiles from the same Y against VAR0
+    cudaMemcpy(dY, hY0.data(), P * 16, cudaMemcpyHostToDevice);
+    cudaMemset(dout, 0, (size_t)GMAX * 3 * 4096 * 16);
+    v.k<<<148, 256, lsmem>>>(g, dT, dtiles, dranges, dfar, dnear, dtgt, dout, dY);
+    cudaDeviceSynchronize();
+    std::vector<double2> hy(P), ho((size_t)148 * 3 * 4096);
+    cudaMemcpy(hy.data(), dY, P * 16, cudaMemcpyDeviceToHost);
+    cudaMemcpy(ho.data(), dout, ho.size() * 16, cudaMemcpyDeviceToHost);
+    double dmax = 0, ymax = 0;
+    if (refY.empty()) {
+      refY = hy;
+      refO = ho;
+    }
+    for (int64_t i = 0; i < P; ++i) {
+      dmax = std::max(dmax, std::max(fabs(hy[i].x - refY[i].x), fabs(hy[i].y - refY[i].y)));
+      ymax = std::max(ymax, fabs(refY[i].x));
+    }
+    double omax = 0;
+    for (size_t i = 0; i < ho.size(); ++i) omax = std::max(omax, std::max(fabs(ho[i].x - refO[i].x), fabs(ho[i].y - refO[i].y)));
+    printf("%-8s %3d regs local %zu | max|dY| %.3e (max|Y| %.3e) max|dNear| %.3e | %s\n", v.name, fa.numRegs,
+           (size_t)fa.localSizeBytes, dmax, ymax, omax, cudaGetErrorString(cudaGetLastError()));
+    for (int grid : {1, 148, 192}) {
+      for (int w = 0; w < 3; ++w) v.k<<<grid, 256, lsmem>>>(g, dT, dtiles, dranges, dfar, dnear, dtgt, dout, dY);
+      cudaEventRecord(e0);
+      const int reps = 20;
+      for (int r = 0; r < reps; ++r) v.k<<<grid, 256, lsmem>>>(g, dT, dtiles, dranges, dfar, dnear, dtgt, dout, dY);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      printf("   grid %3d : %8.2f us/launch  err=%s\n", grid, ms * 1000 / reps, cudaGetErrorString(cudaGetLastError()));
+    }
+    cudaMemcpy(dY, hY0.data(), P * 16, cudaMemcpyHostToDevice);
+    v.k<<<1, 256, lsmem>>>(g, dT, dtiles, dranges, dfar, dnear, dtgt, dout, dY);
+    cudaDeviceSynchronize();
+    long long p[8];
+    cudaMemcpyFromSymbol(p, nds_lines_probe, sizeof(p));
+    printf("   CTA0 cycles: factors %lld  partials %lld  wavefront %lld  store %lld  push %lld  total %lld\n", p[1] - p[0],
+           p[2] - p[1], p[3] - p[2], p[4] - p[3], p[5] - p[4], p[5] - p[0]);
+  }
+  cudaMemcpy(dY, hY0.data(), P * 16, cudaMemcpyHostToDevice);
+  // co-residency: the mid-level far launch (3 modes per tile, K = the far range) next to the
+  // diagonal launch, as in the level pipeline (far(lv) overlaps diag(lv - 1))
+  {
+    std::vector<int4> items;
+    for (int i = 0; i < 192; ++i) {
+      const int64_t t = tiles[i];
+      const int I[3] = {(int)(t % 16), (int)((t / 16) % 16), (int)(t / 256)};
+      for (int j = 0; j < 3; ++j)
+        if (I[j] <= 13) items.push_back(make_int4(i, j, 16 * (I[j] + 2), 256));
+    }
+    const int ni = (int)items.size();
+    int4* ditems;
+    double2* dpart;
+    cudaMalloc(&ditems, ni * 16);
+    cudaMalloc(&dpart, (size_t)ni * 4096 * 16);
+    cudaMemcpy(ditems, items.data(), ni * 16, cudaMemcpyHostToDevice);
+    UpdateKernel ku = update_kernel_for(16);
+    const size_t usmem = update_smem_bytes(16);
+    const int uh = update_h(16);
+    cudaFuncSetAttribute(ku, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)usmem);
+    auto k2 = tile_diag_lines_kernel<3, 16, 256, true, false>;
+    cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
+    cudaFuncGetAttributes(&fa, k2);
+    printf("t2smem lines kernel: %d regs, local %zu; far items %d (H=%d, smem %zu)\n", fa.numRegs, (size_t)fa.localSizeBytes, ni, uh, usmem);
+    cudaStream_t s0, s1;
+    cudaStreamCreateWithFlags(&s0, cudaStreamNonBlocking);
+    cudaStreamCreateWithFlags(&s1, cudaStreamNonBlocking);
+    cudaEvent_t a0, a1, b1;
+    cudaEventCreate(&a0);
+    cudaEventCreate(&a1);
+    cudaEventCreate(&b1);
+    for (int variant = 0; variant < 2; ++variant) {
+      LinesKernel kk = variant == 0 ? kl : k2;
+      for (int mode = 0; mode < 3; ++mode) {  // 0 lines only, 1 far only, 2 both
+        float best = 1e9;
+        for (int rep = 0; rep < 6; ++rep) {
+          cudaEventRecord(a0, s0);
+          cudaStreamWaitEvent(s1, a0, 0);
+          if (mode >= 1) ku<<<ni * uh, kUpdThreads, usmem, s1>>>(g, dT, dtiles, ditems, dpart, dY);
+          if (mode != 1) kk<<<192, 256, lsmem, s0>>>(g, dT, dtiles, dranges, dfar, dnear, dtgt, dout, dY);
+          cudaEventRecord(b1, s1);
+          cudaStreamWaitEvent(s0, b1, 0);
+          cudaEventRecord(a1, s0);
+          cudaEventSynchronize(a1);
+          float ms;
+          cudaEventElapsedTime(&ms, a0, a1);
+          if (rep > 0) best = std::min(best, ms);
+        }
+        printf("%s %-10s: %8.2f us  err=%s\n", variant == 0 ? "t2reg " : "t2smem", mode == 0 ? "lines" : mode == 1 ? "far" : "lines+far",
+               best * 1000, cudaGetErrorString(cudaGetLastError()));
+      }
+    }
+  }
+  return 0;
+}
