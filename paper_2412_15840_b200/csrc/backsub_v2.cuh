@@ -1203,6 +1203,7 @@ static FarGroupCfg far_group_cfg(int b) {
   if (env == "plain") return {nullptr, 0, 0, 0, 0};
   const int gsel = env.empty() ? 0 : atoi(env.c_str());
   if (b == 16) {
+    if (gsel == 2 && var == 7) return {far_group_kernel<16, 2, 1, true, 1, 4, 4>, 2, 8, 4, 4};
     if (gsel == 2) return {far_group_kernel<16, 2, 2, true, 1, 3, 2>, 2, 8, 3, 2};
     switch (var) {
       case 1: return {far_group_kernel<16, 1, 2, true, 2, 3, 2>, 1, 16, 3, 2};
@@ -1213,6 +1214,8 @@ static FarGroupCfg far_group_cfg(int b) {
     }
   }
   if (b == 8) {
+    if (gsel == 2 && var == 7) return {far_group_kernel<8, 2, 1, true, 2, 4, 8>, 2, 8, 4, 8};
+    if (gsel == 4 && var == 7) return {far_group_kernel<8, 4, 1, true, 2, 4, 8>, 4, 8, 4, 8};
     if (gsel == 2) return {far_group_kernel<8, 2, 2, true, 2, 3, 4>, 2, 8, 3, 4};
     if (gsel == 4) return {far_group_kernel<8, 4, 2, true, 2, 3, 4>, 4, 8, 3, 4};
     switch (var) {
