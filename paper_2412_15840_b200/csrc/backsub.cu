@@ -336,7 +336,13 @@ void solve_plan_build(SolvePlan& sp, int n_modes, const int64_t* dims, const int
         }
       }
       int64_t kc = INT64_MAX;
-      if (natural > 0 && natural < 2 * 148) kc = std::max<int64_t>(32, ((rows + 295) / 296 + kq - 1) / kq * kq);
+      // k-split target: NDS_KSPLIT = CTA-items a small level is spread over (A/B). Default 0 = never
+      // split: every chunk is one more partial the diagonal CTA reads on the critical path (c1 tail
+      // levels: 3 items -> 21 chunks); unsplit, the small levels' far items still finish under the
+      // previous level's diagonal tiles (c1 solve 4.50 -> 4.41 ms)
+      static const int64_t ksplit = getenv("NDS_KSPLIT") ? atoll(getenv("NDS_KSPLIT")) : 0;
+      if (natural > 0 && natural < ksplit)
+        kc = std::max<int64_t>(32, ((rows + ksplit - 1) / ksplit + kq - 1) / kq * kq);
       static const int64_t kcap = getenv("NDS_KCAP") ? atoll(getenv("NDS_KCAP")) : 0;  // A/B: longest item
       if (kcap > 0) kc = std::min(kc, kcap);
       for (int64_t s2 = sp.level_off[lv]; s2 < sp.level_off[lv + 1]; ++s2) {
