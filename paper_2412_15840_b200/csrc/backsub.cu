@@ -592,6 +592,7 @@ void solve_plan_build(SolvePlan& sp, int n_modes, const int64_t* dims, const int
     NDS_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     NDS_CUDA(cudaStreamCreateWithPriority(&sp.s_crit, cudaStreamNonBlocking, hi));
     NDS_CUDA(cudaStreamCreateWithPriority(&sp.s_far, cudaStreamNonBlocking, lo));
+    NDS_CUDA(cudaStreamCreateWithPriority(&sp.s_far2, cudaStreamNonBlocking, lo));
     sp.ev.resize(2 * levels + 2);
     for (auto& e : sp.ev) NDS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
@@ -608,7 +609,8 @@ void solve_plan_free(SolvePlan& sp) {
   sp.ev.clear();
   if (sp.s_crit) cudaStreamDestroy(sp.s_crit);
   if (sp.s_far) cudaStreamDestroy(sp.s_far);
-  sp.s_crit = sp.s_far = nullptr;
+  if (sp.s_far2) cudaStreamDestroy(sp.s_far2);
+  sp.s_crit = sp.s_far = sp.s_far2 = nullptr;
 }
 
 // NDS_SOLVE=split|unified selects the dataflow (persistent-kernel) solve, an experimental A/B
@@ -772,8 +774,12 @@ int backsub_launch(const SolvePlan& sp, const double2* t_pool, double2* c, cudaS
   NDS_CUDA(cudaEventRecord(ev_start, stream));
   NDS_CUDA(cudaStreamWaitEvent(sp.s_crit, ev_start, 0));
   NDS_CUDA(cudaStreamWaitEvent(sp.s_far, ev_start, 0));
+  NDS_CUDA(cudaStreamWaitEvent(sp.s_far2, ev_start, 0));
   if (rec) rec->mark(stream, -1, 0);
   int head_waited = -1;
+  // far(lv) depends on diag(lv - 2) only: even and odd levels' far launches go to two streams so
+  // far(lv) may start while far(lv - 1)'s last CTAs drain (NDS_FAR2=0: one stream)
+  static const bool far2 = !(getenv("NDS_FAR2") && std::string(getenv("NDS_FAR2")) == "0");
   const bool grouped = sp.fgroup >= 1;
   const FarGroupCfg fgc = far_group_cfg(b);
   const size_t fg_smem = far_group_smem_bytes(b);
@@ -784,17 +790,18 @@ int backsub_launch(const SolvePlan& sp, const double2* t_pool, double2* c, cudaS
                                : sp.d_far_partial[lv & 1];
     if (nf > 0) {
       // far(lv) needs levels <= lv - 2; it overlaps diag(lv - 1) on the critical stream
-      if (lv >= 2) NDS_CUDA(cudaStreamWaitEvent(sp.s_far, ev_diag(lv - 2), 0));
-      tmark(sp.s_far, lv, 0);
+      cudaStream_t fs = far2 && (lv & 1) ? sp.s_far2 : sp.s_far;
+      if (lv >= 2) NDS_CUDA(cudaStreamWaitEvent(fs, ev_diag(lv - 2), 0));
+      tmark(fs, lv, 0);
       if (grouped)
-        fgc.kern<<<(unsigned)(nf * fgc.h), kUpdThreads, fg_smem, sp.s_far>>>(g, t_pool, sp.d_tiles,
-                                                                          sp.d_fg_items + sp.fg_off[lv], sp.d_fg_ring, c);
+        fgc.kern<<<(unsigned)(nf * fgc.h), kUpdThreads, fg_smem, fs>>>(g, t_pool, sp.d_tiles,
+                                                                    sp.d_fg_items + sp.fg_off[lv], sp.d_fg_ring, c);
       else
-        upd<<<(unsigned)(nf * uh), kUpdThreads, upd_smem, sp.s_far>>>(g, t_pool, sp.d_tiles, sp.d_far_items + sp.far_off[lv],
-                                                               far_buf, c);
+        upd<<<(unsigned)(nf * uh), kUpdThreads, upd_smem, fs>>>(g, t_pool, sp.d_tiles, sp.d_far_items + sp.far_off[lv],
+                                                         far_buf, c);
       NDS_LAUNCH_CHECK();
-      tmark(sp.s_far, lv, 1);
-      NDS_CUDA(cudaEventRecord(ev_far(lv), sp.s_far));
+      tmark(fs, lv, 1);
+      NDS_CUDA(cudaEventRecord(ev_far(lv), fs));
       ++launches;
     }
     double2* near_in = push ? (lv & 1 ? sp.d_near_partial2 : sp.d_near_partial) : sp.d_near_partial;

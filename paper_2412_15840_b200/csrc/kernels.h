@@ -129,7 +129,7 @@ struct SolvePlan {
   double2* d_fg_ring = nullptr;
   int fg_ring = 0;
   int64_t fg_slots = 0;
-  cudaStream_t s_crit = nullptr, s_far = nullptr;
+  cudaStream_t s_crit = nullptr, s_far = nullptr, s_far2 = nullptr;  // far: even / odd levels
   // dataflow (persistent-kernel) solve, N = 3: per-slot / per-item tables, partial rings, counters
   bool persist = false;
   int* d_level_of = nullptr;
