@@ -32,26 +32,6 @@ __device__ __forceinline__ void dmma_bs(double& c0, double& c1, double a, double
       : "d"(a), "d"(b));
 }
 
-__device__ __forceinline__ void mbar_init_bs(uint64_t* b, int count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"((unsigned)__cvta_generic_to_shared(b)), "r"(count)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_bs(uint64_t* b) {
-  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(
-                   (unsigned)__cvta_generic_to_shared(b))
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait_bs(uint64_t* b, int parity) {
-  const unsigned a = (unsigned)__cvta_generic_to_shared(b);
-  unsigned ok = 0;
-  do {
-    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-                 : "=r"(ok)
-                 : "r"(a), "r"(parity)
-                 : "memory");
-  } while (!ok);
-}
-
 // Off-tile coupling of one work item (tile I, mode j, rows [kb, ke) along mode j) as a small
 // complex GEMM on the FP64 tensor pipe:
 //   partial(l_j, c) = sum_{k in [kb, ke)} T_j(o_j + l_j, k) * Y(k along mode j, c),
@@ -724,15 +704,11 @@ __constant__ LineOrder<4, 8> kLineOrder4 = make_line_order<4, 8>();
 //   near_out[item] (l_m, c) = sum_k T_m(o_m - B + l_m, o_m + k) Y_J(k along m, c)
 // (3M DMMA; near_target[slot N + m] = that item's index at the next level, -1 if none) — which
 // replaces the separate near-update launch on the critical path.
-// VAR bits (A/B experiments, tools/microbench/lines_bench.cu):
-//   1 = PIPE: split-phase step barrier (mbarrier: arrive right after this step's y store, wait
-//       before the next step's loads); each thread pre-accumulates, between the two, every
-//       mode >= 2 term of its NEXT row whose neighbour is at distance >= 2 (solved at least two
-//       steps earlier), so only the distance-1 terms and the mode-1 history stay between the
-//       barrier and the store;
-//   2 = QU: the mode-1 history update stops at the warp's largest active row;
-//   4 = PRO: factor loads issued together with the tile's loads;
-//   8 = PUSHU: the PUSH phase's three mode GEMMs unrolled into one instruction stream.
+// VAR bits: 4 = PRO (factor loads issued together with the tile's loads). Measured and removed
+// (tools/microbench/lines_bench.cu): a split-phase (mbarrier) step barrier
+// with the next row's distance >= 2 terms pre-accumulated in between, a warp-uniform bound on
+// the history update, unrolling the PUSH modes, and a two-warps-per-32-lines form (512 threads,
+// 128 registers; wavefront 58 K -> 87 K cycles).
 template <int N, int B, int NT, bool PUSH, bool T2REG, bool SORT = true, int VAR = 0>
 __device__ __forceinline__ void diag_lines_body(const TileGeom& g, const double2* __restrict__ T, const int64_t tile,
                                                 const int4 tr, const double2* __restrict__ far_partial,
@@ -746,18 +722,13 @@ __device__ __forceinline__ void diag_lines_body(const TileGeom& g, const double2
   using PS = LinePad<N, B>;
   __shared__ int64_t so[N];
   __shared__ int64_t st[N];
-  constexpr bool PIPE = (VAR & 1) != 0;
-  constexpr bool QU = (VAR & 2) != 0;
   constexpr bool PRO = (VAR & 4) != 0;
-  constexpr bool PUSHU = (VAR & 8) != 0;
-  __shared__ uint64_t step_bar;
   const int tid = threadIdx.x;
   NDS_LPROBE(0);
   int tgt_m[N];  // near-coupling targets of the PUSH phase, loaded before the long wavefront
 #pragma unroll
   for (int m = 0; m < N; ++m) tgt_m[m] = PUSH ? near_target[m] : -1;
   if (tid == 0) {
-    if constexpr (PIPE) mbar_init_bs(&step_bar, NT / 32);
     int64_t t = tile;
     for (int m = 0; m < N; ++m) {
       const int64_t I = t % g.nb[m];
@@ -886,75 +857,10 @@ __device__ __forceinline__ void diag_lines_body(const TileGeom& g, const double2
 #pragma unroll
   for (int j = 0; j < B - 1; ++j) q[j] = make_double2(0.0, 0.0);
 
-  if constexpr (PIPE) {
-    double2 pre = make_double2(0.0, 0.0), rden = make_double2(0.0, 0.0);
-    const int q2 = B - 1 - lm[1];
-    // every mode >= 2 term of row rr at neighbour distance >= 2, and the row's reciprocal
-    // denominator (both independent of the previous step)
-    auto prepare = [&](int rr) {
-      const double2* e = S + rr + pb;
-      double2 a[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = make_double2(0.0, 0.0);
-#pragma unroll
-      for (int k = 1; k < B - 1; ++k)
-        if (k < q2) a[k & 3] = cfma(a[k & 3], T2REG ? t2r[T2REG ? k : 0] : t2s[k], e[(1 + k) * PS::a1]);
-#pragma unroll
-      for (int m = 2; m < N; ++m) {
-        const double2* tm = Td + (m * B + lm[m]) * B + lm[m] + 1;
-        const int qm = B - 1 - lm[m];
-#pragma unroll
-        for (int k = 1; k < B - 1; ++k)
-          if (k < qm) a[(k + 2) & 3] = cfma(a[(k + 2) & 3], tm[k], e[(1 + k) * PS::at(m)]);
-      }
-      pre = cadd(cadd(a[0], a[1]), cadd(a[2], a[3]));
-      rden = crecip_fast(cadd(Td[rr * (B + 1)], dsum));
-    };
-    if (lv0 == 0) prepare(B - 1);
-    const int lane = tid & 31;
-#pragma unroll 1
-    for (int lv = 0; lv < WL; ++lv) {
-      const int r = B - 1 - (lv - lv0);
-      const bool act = lv >= lv0 && r >= 0;
-      double2 y = make_double2(0.0, 0.0);
-      if (act) {
-        const double2* e = S + r + pb;
-        double2 acc = cadd(pre, q[0]);
-        if (q2 > 0) acc = cfma(acc, T2REG ? t2r[0] : t2s[0], e[PS::a1]);
-#pragma unroll
-        for (int m = 2; m < N; ++m)
-          if (lm[m] < B - 1) acc = cfma(acc, Td[(m * B + lm[m]) * B + lm[m] + 1], e[PS::at(m)]);
-        y = cmul(csub(e[0], acc), rden);
-        S[r + pb] = y;
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive_bs(&step_bar);
-      const int rmax = QU ? (int)__reduce_max_sync(0xffffffffu, act ? (unsigned)r : 0u) : B;
-      if (act) {
-      if constexpr (QU) {
-#pragma unroll
-        for (int j = 0; j < B - 1; ++j) {
-          if (j >= rmax) break;  // warp-uniform
-          if (j < r) q[j] = cfma(j + 1 < B - 1 ? q[j + 1] : make_double2(0.0, 0.0), Dq[j * B + r], y);
-        }
-      } else {
-#pragma unroll
-        for (int j = 0; j < B - 1; ++j)
-          if (j < r) q[j] = cfma(j + 1 < B - 1 ? q[j + 1] : make_double2(0.0, 0.0), Dq[j * B + r], y);
-      }
-        if (r >= 1) prepare(r - 1);
-      } else if (lv == lv0 - 1) {
-        prepare(B - 1);
-      }
-      mbar_wait_bs(&step_bar, lv & 1);
-    }
-  } else {
 #pragma unroll 1
   for (int lv = 0; lv < WL; ++lv) {
     const int r = B - 1 - (lv - lv0);
-    const bool act = lv >= lv0 && r >= 0;
-    const int rmax = QU ? (int)__reduce_max_sync(0xffffffffu, act ? (unsigned)r : 0u) : B;
-    if (act) {
+    if (lv >= lv0 && r >= 0) {
       const double2* e = S + r + pb;  // this step's entry
       const double2 rden = crecip_fast(cadd(Td[r * (B + 1)], dsum));
       double2 a[4];
@@ -976,20 +882,11 @@ __device__ __forceinline__ void diag_lines_body(const TileGeom& g, const double2
       const double2 y = cmul(csub(e[0], acc), rden);
       S[r + pb] = y;
       // mode-1 history: q[j] <- q[j+1] + T_1(r-1-j, r) y for the rows r-1-j >= 0 still ahead
-      if constexpr (QU) {
 #pragma unroll
-        for (int j = 0; j < B - 1; ++j) {
-          if (j >= rmax) break;  // warp-uniform
-          if (j < r) q[j] = cfma(j + 1 < B - 1 ? q[j + 1] : make_double2(0.0, 0.0), Dq[j * B + r], y);
-        }
-      } else {
-#pragma unroll
-        for (int j = 0; j < B - 1; ++j)
-          if (j < r) q[j] = cfma(j + 1 < B - 1 ? q[j + 1] : make_double2(0.0, 0.0), Dq[j * B + r], y);
-      }
+      for (int j = 0; j < B - 1; ++j)
+        if (j < r) q[j] = cfma(j + 1 < B - 1 ? q[j + 1] : make_double2(0.0, 0.0), Dq[j * B + r], y);
     }
     __syncthreads();
-  }
   }
   NDS_LPROBE(3);
   {
@@ -1023,9 +920,8 @@ __device__ __forceinline__ void diag_lines_body(const TileGeom& g, const double2
         loff += l << (LB * mm);
       }
     };
-#pragma unroll
+#pragma unroll 1
     for (int m = 0; m < N; ++m) {
-      if constexpr (!PUSHU) asm volatile("" ::: "memory");  // keep the modes' GEMMs apart (no overlap)
       const int tgt = tgt_m[m];
       if (tgt < 0) continue;  // CTA-uniform
       int sb[4];
@@ -1096,8 +992,7 @@ using LinesKernel = void (*)(const TileGeom, const double2*, const int64_t*, con
 static LinesKernel lines_kernel_for(int n_modes, int b, bool push) {
   static const bool t2smem = getenv("NDS_DIAG_T2SMEM") != nullptr;  // A/B experiments
   static const bool natural = getenv("NDS_DIAG_NATURAL") != nullptr;
-  // VAR 4 (PRO: factor loads overlapped with the tile's loads) measured 2 % faster per tile; the
-  // PIPE / QU variants slower (tools/microbench/lines_bench.cu)
+  // VAR 4 (PRO: factor loads overlapped with the tile's loads) measured 2 % faster per tile
   if (n_modes == 3 && b == 16) {
     if (natural)
       return push ? tile_diag_lines_kernel<3, 16, 256, true, true, false> : tile_diag_lines_kernel<3, 16, 256, false, true, false>;

@@ -81,9 +81,7 @@ int main(int argc, char** argv) {
     LinesKernel k;
   };
   V vars[] = {{"VAR0", tile_diag_lines_kernel<3, 16, 256, true, true, true, 0>},
-              {"PRO", tile_diag_lines_kernel<3, 16, 256, true, true, true, 4>},
-              {"PUSHU", tile_diag_lines_kernel<3, 16, 256, true, true, true, 8>},
-              {"PRO+PUSHU", tile_diag_lines_kernel<3, 16, 256, true, true, true, 12>}};
+              {"PRO", tile_diag_lines_kernel<3, 16, 256, true, true, true, 4>}};
   std::vector<double2> refY, refO;
   if (argc > 1) {  // profiling mode: one launch of variant argv[1] on 148 tiles
     auto& v = vars[atoi(argv[1])];
