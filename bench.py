@@ -17,7 +17,8 @@ with U_j). The host Schur factorisations are setup, computed once and timed sepa
           bounded slab sample of the same workload, rank 0 at N=1 only.
 
 --impl reference runs the reference's own CPU solver (oracle/_ref) the same way.
-Multi-GPU (torchrun): independent replicas of the workload, one per rank (weak scaling).
+Multi-GPU (torchrun): independent replicas of the workload, one per rank (weak scaling); with
+--sharded, ONE problem split across the ranks by the ShardedSolver (strong scaling).
 """
 from __future__ import annotations
 
@@ -180,6 +181,72 @@ def run_reference(args, world, rank):
     return 0
 
 
+def run_sharded(args, world, rank, local):
+    """--sharded: ONE problem of --config split across the ranks (strong scaling), through the
+    multi-GPU ShardedSolver (paper_2412_15840_b200/distributed.py): transforms local
+    in the L_N slab layout, NCCL all-to-all re-shards, triangular solve pipelined over (rank,
+    mode-N sub-block) with point-to-point block forwarding. value = P / (max-over-ranks device
+    time per solve). Schur is host setup on every rank (same seed, same factors)."""
+    import socket
+
+    import torch
+    import torch.distributed as dist
+    import paper_2412_15840_b200 as nds
+    from paper_2412_15840_b200 import configs
+    from paper_2412_15840_b200.distributed import CudaLocalOps, ShardedSolver, scatter_LN
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if not dist.is_initialized():  # one rank: a single-member NCCL group for the same code path
+        s = socket.socket()
+        s.bind(("127.0.0.1", 0))
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ["MASTER_PORT"] = str(s.getsockname()[1])
+        s.close()
+        dist.init_process_group("nccl", rank=0, world_size=1)
+    ctx = nds.Context(local)
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
+    a_list, b_host = configs.make_problem(args.config, seed=args.seed)
+    dims = tuple(b_host.shape)
+    P = int(np.prod(dims))
+    factors = [ctx.schur(a) for a in a_list]
+    us = [f[0] for f in factors]
+    ts = [f[1] for f in factors]
+    solver = ShardedSolver(dims, us, ts, CudaLocalOps(ctx))
+    b_local = torch.from_numpy(scatter_LN(b_host, world)[rank]).to(dev)
+    del b_host
+    for _ in range(args.warmup):
+        x_local = solver.solve(b_local)
+    torch.cuda.synchronize(dev)
+    dist.barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            x_local = solver.solve(b_local)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+    dist.barrier()
+    ms_step = max_over_ranks(world, e0.elapsed_time(e1), dev) / args.steps
+    verify = None
+    if args.verify:
+        verify = {"x_local_max": float(x_local.abs().max())}  # the residual needs the whole X
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": P / (ms_step * 1e-3), "unit": "unknowns/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "c128 (fp64 DMMA)",
+            "data": "synthetic (generator v1, seeded Gaussian)",
+            "config": {"workload": args.config, "dims": list(dims), "P": P, "parallelism": f"sharded x{world}",
+                       "description": configs.DESCRIPTIONS[args.config]},
+            "roofline": None, "cpu_baseline": None, "e2e": None, "gpu_launches": None,
+            "clocks": clk.summary(), "verify": verify}), flush=True)
+    dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -192,12 +259,17 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--verify", action="store_true", help="device residual check after timing")
+    ap.add_argument("--sharded", action="store_true",
+                    help="one problem split across the ranks (ShardedSolver, strong scaling) instead of replicas")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
 
     world, rank, local = dist_init()
     if args.impl == "reference":
         return run_reference(args, world, rank)
+
+    if args.sharded:
+        return run_sharded(args, world, rank, local)
 
     import torch
     import paper_2412_15840_b200 as nds

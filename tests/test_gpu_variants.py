@@ -56,3 +56,12 @@ def test_solve_variant_against_oracle(env):
     for case in json.loads(p.stdout.strip().splitlines()[-1]):
         assert case["err"] <= 1e-9, case
         assert case["res"] <= 1e-10, case
+
+
+def test_bench_sharded_mode_runs():
+    """bench.py --sharded: the multi-GPU ShardedSolver path (single-member NCCL group here)."""
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--sharded", "--config", "c0", "--steps", "2",
+                        "--warmup", "1"], capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert p.returncode == 0, p.stderr[-2000:]
+    line = json.loads(p.stdout.strip().splitlines()[-1])
+    assert line["scaling"] == "strong" and line["value"] > 0 and line["config"]["parallelism"] == "sharded x1"
