@@ -40,9 +40,9 @@ def test_full_config_residual(ctx, name):
 
 @pytest.mark.parametrize("name,dims", [("c1", (128, 96, 64)), ("c2", (32, 32, 32, 32)), ("c4", (2,) * 18)])
 def test_plan_graph_replay(ctx, name, dims):
-    """nds_plan_execute runs eagerly once, captures the second call into a CUDA graph and replays
-    it for later calls on the same buffers (re-capturing when they change): every call must
-    give the bitwise-same X (fixed summation orders), including after a buffer change."""
+    """nds_plan_execute (with NDS_GRAPH=1 in the environment: the graph-replay path; otherwise
+    the eager path) gives the bitwise-same X on every call (fixed summation orders), including
+    after a buffer change."""
     import torch
     a, b = configs.make_problem(name, seed=3, dims=dims)
     dims = b.shape  # the advection-diffusion generator (c2) uses one extent for every mode

@@ -44,6 +44,7 @@ VARIANTS = [
     {"NDS_DIAG": "wave"},
     {"NDS_NEAR": "kernel"},
     {"NDS_HEAD": "0"},
+    {"NDS_FAR2": "0"},
 ]
 
 
@@ -56,6 +57,14 @@ def test_solve_variant_against_oracle(env):
     for case in json.loads(p.stdout.strip().splitlines()[-1]):
         assert case["err"] <= 1e-9, case
         assert case["res"] <= 1e-10, case
+
+
+def test_plan_graph_replay_in_subprocess():
+    """The CUDA-graph replay path of nds_plan_execute (NDS_GRAPH=1) is bitwise-equal to eager."""
+    env = dict(os.environ, NDS_GRAPH="1")
+    p = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", os.path.join(ROOT, "tests", "test_gpu_fullsize.py"),
+                        "-k", "graph"], env=env, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert p.returncode == 0, p.stdout[-2000:] + p.stderr[-2000:]
 
 
 def test_bench_sharded_mode_runs():
