@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(WM* WN * 32, MINB) zgemm_dmma_kernel(const Gem
 }
 
 // Tile configurations. 3M kernels, 2 CTAs / SM, 8 warps, BK = 16, 3 stages:
-//   kWide: 64 x 32 per CTA (warps of 32 x 8);  kTall: 32 x 64 per CTA (warps of 32 x 8).
+//   kWide: 64 x 32 per CTA;  kTall: 32 x 64 per CTA; warps of 16 x 16.
 // The shape with the least padded output is chosen per GEMM (ties: kWide). NDS_GEMM=4m|3m64
 // force the 4-multiply 64 x 128 kernel / the 1-CTA 64 x 64 3M kernel (A/B experiments).
 // Algorithmic flops are counted as 8 per complex MAC in every roofline figure regardless.
@@ -289,12 +289,26 @@ static int forced_shape() {
   return v;
 }
 
+// Warp tiles of 16 x 16 (2 x 2 fragments): 4 operand sums and 4 fragment loads per 12 DMMAs
+// (32 x 8 warps: 5 and 5) — the 3M sums share the FP64 pipe with the DMMAs (c1 transforms
+// 4.74 -> 4.63 ms, c2 15.89 -> 15.36). NDS_GEMM_W82=1 restores the 32 x 8 warps (A/B).
+static bool w82() {
+  static const bool v = getenv("NDS_GEMM_W82") != nullptr;
+  return v;
+}
+
 static void launch_gemm(GemmShape shape, GemmArgs g, cudaStream_t stream) {
   switch (shape) {
-    case kTall: launch_gemm_t<32, 64, 16, 1, 8, 3, true, 2>(g, stream); break;
+    case kTall:
+      if (w82()) launch_gemm_t<32, 64, 16, 1, 8, 3, true, 2>(g, stream);
+      else launch_gemm_t<32, 64, 16, 2, 4, 3, true, 2>(g, stream);
+      break;
     case kForce4M: launch_gemm_t<64, 128, 16, 2, 4, 3, false>(g, stream); break;
     case kForce3M64: launch_gemm_t<64, 64, 16, 2, 4, 4, true>(g, stream); break;
-    default: launch_gemm_t<64, 32, 16, 2, 4, 3, true, 2>(g, stream); break;
+    default:
+      if (w82()) launch_gemm_t<64, 32, 16, 2, 4, 3, true, 2>(g, stream);
+      else launch_gemm_t<64, 32, 16, 4, 2, 3, true, 2>(g, stream);
+      break;
   }
 }
 
