@@ -343,8 +343,6 @@ void solve_plan_build(SolvePlan& sp, int n_modes, const int64_t* dims, const int
       static const int64_t ksplit = getenv("NDS_KSPLIT") ? atoll(getenv("NDS_KSPLIT")) : 0;
       if (natural > 0 && natural < ksplit)
         kc = std::max<int64_t>(32, ((rows + ksplit - 1) / ksplit + kq - 1) / kq * kq);
-      static const int64_t kcap = getenv("NDS_KCAP") ? atoll(getenv("NDS_KCAP")) : 0;  // A/B: longest item
-      if (kcap > 0) kc = std::min(kc, kcap);
       for (int64_t s2 = sp.level_off[lv]; s2 < sp.level_off[lv + 1]; ++s2) {
         int64_t r = tiles[s2];
         for (int j = 0; j < n_modes; ++j) {

@@ -1087,41 +1087,24 @@ static size_t diag_smem_bytes(int n_modes, int b, int wf_levels) {
 // BK = 8; b = 8: 256 columns, BK = 4). Groups of G = 2/4 targets per item (32 rows, half the slab
 // traffic per flop) measured slower: the far kernel is not traffic-bound (DMMA pipe ~57 % busy,
 // latency/barrier stalls), and the remainder items add partial read-modify-writes.
-// NDS_FARGROUP=plain restores the plain per-target items, =2|4 selects G; NDS_FGCFG other shapes.
+// NDS_FARGROUP=plain restores the plain per-target items, =2|4 selects G. Also measured for G = 1
+// and rejected: BK = 16 (1 CTA/SM by shared memory), one or four column CTAs per item, 4M.
 struct FarGroupCfg {
   FarGroupKernel kern;
   int g, bk, stages, h;
 };
 static FarGroupCfg far_group_cfg(int b) {
   static const std::string env = getenv("NDS_FARGROUP") ? getenv("NDS_FARGROUP") : "";
-  static const int var = getenv("NDS_FGCFG") ? atoi(getenv("NDS_FGCFG")) : 0;  // A/B shapes
   if (env == "plain") return {nullptr, 0, 0, 0, 0};
   const int gsel = env.empty() ? 0 : atoi(env.c_str());
   if (b == 16) {
-    if (gsel == 2 && var == 7) return {far_group_kernel<16, 2, 1, true, 1, 4, 4>, 2, 8, 4, 4};
     if (gsel == 2) return {far_group_kernel<16, 2, 2, true, 1, 3, 2>, 2, 8, 3, 2};
-    switch (var) {
-      case 1: return {far_group_kernel<16, 1, 2, true, 2, 3, 2>, 1, 16, 3, 2};
-      case 2: return {far_group_kernel<16, 1, 1, true, 1, 3, 4>, 1, 8, 3, 4};
-      case 3: return {far_group_kernel<16, 1, 4, true, 1, 3, 1>, 1, 8, 3, 1};
-      case 4: return {far_group_kernel<16, 1, 2, true, 1, 3, 2>, 1, 8, 3, 2};
-      default: return {far_group_kernel<16, 1, 2, true, 1, 4, 2>, 1, 8, 4, 2};
-    }
+    return {far_group_kernel<16, 1, 2, true, 1, 4, 2>, 1, 8, 4, 2};
   }
   if (b == 8) {
-    if (gsel == 2 && var == 7) return {far_group_kernel<8, 2, 1, true, 2, 4, 8>, 2, 8, 4, 8};
-    if (gsel == 4 && var == 7) return {far_group_kernel<8, 4, 1, true, 2, 4, 8>, 4, 8, 4, 8};
     if (gsel == 2) return {far_group_kernel<8, 2, 2, true, 2, 3, 4>, 2, 8, 3, 4};
     if (gsel == 4) return {far_group_kernel<8, 4, 2, true, 2, 3, 4>, 4, 8, 3, 4};
-    switch (var) {
-      case 1: return {far_group_kernel<8, 1, 4, true, 2, 3, 2>, 1, 8, 3, 2};
-      case 2: return {far_group_kernel<8, 1, 8, true, 1, 3, 1>, 1, 4, 3, 1};
-      case 3: return {far_group_kernel<8, 1, 2, true, 1, 3, 4>, 1, 4, 3, 4};
-      case 4: return {far_group_kernel<8, 1, 4, false, 1, 3, 2>, 1, 4, 3, 2};
-      case 5: return {far_group_kernel<8, 1, 4, true, 1, 3, 2>, 1, 4, 3, 2};
-      case 6: return {far_group_kernel<8, 1, 4, true, 2, 4, 2>, 1, 8, 4, 2};
-      default: return {far_group_kernel<8, 1, 4, true, 1, 4, 2>, 1, 4, 4, 2};
-    }
+    return {far_group_kernel<8, 1, 4, true, 1, 4, 2>, 1, 4, 4, 2};
   }
   return {nullptr, 0, 0, 0, 0};
 }

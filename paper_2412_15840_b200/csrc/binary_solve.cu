@@ -27,8 +27,7 @@ struct BinSolveGeom {
   const double2* t;   // per mode j: T_j (2x2 column-major) at t + 4 j
 };
 
-template <bool PIPE2>
-__global__ void __launch_bounds__(kBinSolveThreads, PIPE2 ? 2 : 3) binary_tile_solve_kernel(const BinSolveGeom g,
+__global__ void __launch_bounds__(kBinSolveThreads, 3) binary_tile_solve_kernel(const BinSolveGeom g,
                                                                               const int64_t* __restrict__ tiles,
                                                                               const int* __restrict__ wf,
                                                                               const int* __restrict__ wf_off,
@@ -67,8 +66,9 @@ __global__ void __launch_bounds__(kBinSolveThreads, PIPE2 ? 2 : 3) binary_tile_s
   const int64_t base = I << g.m;
   // 1. load + pull from neighbour slabs (outer modes with bit 0). The running sums live in shared
   //    memory (each thread owns the same entries l = tid + i * 256 throughout, so no barrier), so
-  //    registers hold only loads in flight: a whole slab (PIPE2: two slabs, software-pipelined)
-  //    per thread. Same per-entry order as the reference: own value, then q ascending.
+  //    registers hold only loads in flight: a whole slab per thread (two slabs, software-
+  //    pipelined, spill at 2 CTAs/SM and measured slower). Same per-entry order as the reference:
+  //    own value, then q ascending.
   constexpr int PER = 4096 / kBinSolveThreads;
 #pragma unroll
   for (int i = 0; i < PER; ++i) {
@@ -91,32 +91,11 @@ __global__ void __launch_bounds__(kBinSolveThreads, PIPE2 ? 2 : 3) binary_tile_s
       if (l < E) S[l] = cfms(S[l], c, v[i]);
     }
   };
-  if constexpr (PIPE2) {
-    int q = 0;
-    auto next = [&](int from) {
-      while (from < g.n_outer && ((I >> from) & 1)) ++from;
-      return from;
-    };
-    q = next(0);
-    double2 va[PER], vb[PER];
-    if (q < g.n_outer) load_slab(q, va);
-    while (q < g.n_outer) {
-      const int q2 = next(q + 1);
-      if (q2 < g.n_outer) load_slab(q2, vb);
-      apply(q, va);
-      if (q2 >= g.n_outer) break;
-      const int q3 = next(q2 + 1);
-      if (q3 < g.n_outer) load_slab(q3, va);
-      apply(q2, vb);
-      q = q3;
-    }
-  } else {
-    for (int q = 0; q < g.n_outer; ++q) {
-      if ((I >> q) & 1) continue;  // CTA-uniform
-      double2 v[PER];
-      load_slab(q, v);
-      apply(q, v);
-    }
+  for (int q = 0; q < g.n_outer; ++q) {
+    if ((I >> q) & 1) continue;  // CTA-uniform
+    double2 v[PER];
+    load_slab(q, v);
+    apply(q, v);
   }
   __syncthreads();
   // 2. local popcount wavefront, highest level first; inner-mode terms in mode order (loop fully
@@ -184,11 +163,9 @@ void binary_solve_plan_free(BinarySolvePlan& bp) {
 int binary_solve_launch(const BinarySolvePlan& bp, const double2* t_pool, double2* c, cudaStream_t stream,
                         Recorder* rec) {
   static bool attr_set = false;
-  static const int var = getenv("NDS_BSOLVE") ? atoi(getenv("NDS_BSOLVE")) : 0;  // A/B: 1 = two slabs in flight
-  auto kern = var == 1 ? binary_tile_solve_kernel<true> : binary_tile_solve_kernel<false>;
+  auto kern = binary_tile_solve_kernel;
   if (!attr_set) {
-    NDS_CUDA(cudaFuncSetAttribute(binary_tile_solve_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4096 * 16));
-    NDS_CUDA(cudaFuncSetAttribute(binary_tile_solve_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4096 * 16));
+    NDS_CUDA(cudaFuncSetAttribute(binary_tile_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 4096 * 16));
     attr_set = true;
   }
   BinSolveGeom g{bp.m, bp.n_outer, bp.m + 1, t_pool};
