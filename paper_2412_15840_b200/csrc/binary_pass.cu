@@ -27,10 +27,12 @@ struct BinPass {
   int nrb[3];      // group bits per round (<= 4)
   int rb[3][4];    // tile bit of each round bit
   int tb[3][12];   // tile bits carried by the thread index (and slot index) in each round
+  int rsw[3][16];  // swz(round bits of entry e): swz is linear over XOR, so swz(p0 | bits_e) =
+                   // swz(p0) ^ rsw[e] — one XOR per access instead of the full swizzle
   const double2* M[12];  // 2x2 column-major op(U_j) per group mode
 };
 
-__device__ __forceinline__ int swz(int p) { return p ^ (((p >> 3) ^ (p >> 6) ^ (p >> 9)) & 7); }
+__host__ __device__ __forceinline__ constexpr int swz(int p) { return p ^ (((p >> 3) ^ (p >> 6) ^ (p >> 9)) & 7); }
 
 // One round: each thread slot gathers the 2^NB entries spanning the round's NB group modes,
 // applies the NB 2x2 matrices as butterflies in registers, and scatters them back.
@@ -44,14 +46,12 @@ __device__ __forceinline__ void bin_round(const BinPass& bp, int rd, double2* S,
     int p0 = 0;
 #pragma unroll
     for (int i = 0; i < 12 - NB; ++i) p0 |= ((s >> i) & 1) << bp.tb[rd][i];
+    const int sp0 = swz(p0);
     int addr[V];
     double2 v[V];
 #pragma unroll
     for (int e = 0; e < V; ++e) {
-      int p = p0;
-#pragma unroll
-      for (int q = 0; q < NB; ++q) p |= ((e >> q) & 1) << rbit[q];
-      addr[e] = swz(p);
+      addr[e] = sp0 ^ bp.rsw[rd][e];
       v[e] = S[addr[e]];
     }
 #pragma unroll
@@ -83,17 +83,24 @@ __global__ void __launch_bounds__(kBinThreads, 2) binary_pass_kernel(const BinPa
   const int64_t o = tile / bp.n_runs;
   const int R = 1 << bp.logR;
   const int64_t base = run * R + bp.I * ((int64_t)1 << bp.k) * o;
-  // global -> shared (coalesced along runs of R entries): 8 loads of a thread in flight at a time
+  // global -> shared (coalesced along runs of R entries): 8 loads of a thread in flight at a time.
+  // p = tid + i * 256 with tid < 256: swz(p) = swz(tid) ^ swz(i * 256) (constant), and for
+  // R <= 256 the global offset is the thread's own plus i * I * (256 / R)
+  const int stid = swz(tid);
+  const bool small_r = bp.logR <= 8;
+  const int64_t gt = base + (tid & (R - 1)) + bp.I * (tid >> bp.logR);
+  const int64_t gstep = small_r ? bp.I * (kBinThreads >> bp.logR) : 0;
+  auto goff = [&](int i) {
+    const int p = tid + i * kBinThreads;
+    return small_r ? gt + i * gstep : base + (p & (R - 1)) + bp.I * (p >> bp.logR);
+  };
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     double2 v[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int p = tid + (h * 8 + i) * kBinThreads;
-      v[i] = x[base + (p & (R - 1)) + bp.I * (p >> bp.logR)];
-    }
+    for (int i = 0; i < 8; ++i) v[i] = x[goff(h * 8 + i)];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) S[swz(tid + (h * 8 + i) * kBinThreads)] = v[i];
+    for (int i = 0; i < 8; ++i) S[stid ^ swz((h * 8 + i) * kBinThreads)] = v[i];
   }
   __syncthreads();
   for (int rd = 0; rd < bp.rounds; ++rd) {
@@ -106,10 +113,7 @@ __global__ void __launch_bounds__(kBinThreads, 2) binary_pass_kernel(const BinPa
     __syncthreads();
   }
 #pragma unroll
-  for (int i = 0; i < 4096 / kBinThreads; ++i) {
-    const int p = tid + i * kBinThreads;
-    r[base + (p & (R - 1)) + bp.I * (p >> bp.logR)] = S[swz(p)];
-  }
+  for (int i = 0; i < 4096 / kBinThreads; ++i) r[goff(i)] = S[stid ^ swz(i * kBinThreads)];
 }
 
 // Plan the passes over [mode0, mode1) (1-based, all n_j = 2): greedily take as many binary modes
@@ -183,6 +187,11 @@ int binary_pass_launch(const FactorSet& f, const BinGroup& gr, bool adjoint, con
     for (int b : rest)
       if (b >= 0) order.push_back(b);
     for (size_t i = 0; i < order.size(); ++i) bp.tb[rd][i] = order[i];
+    for (int e = 0; e < (1 << nb); ++e) {
+      int bits = 0;
+      for (int q = 0; q < nb; ++q) bits |= ((e >> q) & 1) << bp.rb[rd][q];
+      bp.rsw[rd][e] = swz(bits);
+    }
   }
   static bool attr_set = false;
   if (!attr_set) {
