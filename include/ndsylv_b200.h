@@ -182,6 +182,10 @@ int nds_dev_mode_product(nds_ctx* ctx, int n_modes, const int64_t* dims, const n
  *   M a HOST rows_out x dims_x[mode-1] column-major matrix (negate it to subtract). Async. */
 int nds_dev_mode_update(nds_ctx* ctx, int n_modes, const int64_t* dims_x, int mode, int64_t rows_out,
                         const nds_z* m, const nds_z* d_x, nds_z* d_r);
+/* The same product without accumulation (r = M x_mode x; r need not be initialised): the
+ * sharded solver's local mode products. Async on the context stream. */
+int nds_dev_mode_apply(nds_ctx* ctx, int n_modes, const int64_t* dims_x, int mode, int64_t rows_out,
+                       const nds_z* m, const nds_z* d_x, nds_z* d_r);
 /* In-place triangular solve of a device tensor (back_substitute on device memory): T_j HOST
  * upper-triangular matrices. Synchronous; singular check and stats as nds_back_substitute. */
 int nds_dev_back_substitute(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z* const* t, nds_z* d_c,

@@ -51,7 +51,7 @@ EXPORTED = [
     "nds_plan_create", "nds_plan_destroy", "nds_plan_report", "nds_plan_total", "nds_plan_execute",
     "nds_plan_forward", "nds_plan_backsub", "nds_plan_inverse", "nds_plan_execute_host", "nds_plan_launches",
     "nds_plan_profile_begin", "nds_plan_profile_end",
-    "nds_dev_mode_product", "nds_dev_mode_update", "nds_dev_back_substitute", "nds_dev_residual",
+    "nds_dev_mode_product", "nds_dev_mode_update", "nds_dev_mode_apply", "nds_dev_back_substitute", "nds_dev_residual",
     "nds_triangular_exp", "nds_ode_create", "nds_ode_destroy", "nds_ode_at", "nds_ode_at_dev", "nds_propagate",
     "nds_rk4", "nds_tensor_file_info", "nds_read_tensor", "nds_write_tensor", "nds_read_tensor_dev",
     "nds_write_tensor_dev", "nds_random_problem", "nds_random_ode_system", "nds_randn",
@@ -172,6 +172,7 @@ def load_library(path: str = LIB_PATH):
                                        C.POINTER(C.c_float)]
     L.nds_dev_mode_product.argtypes = [_vp, C.c_int, _i64p, _vp, C.c_int, C.c_int, _vp, _vp, C.c_int]
     L.nds_dev_mode_update.argtypes = [_vp, C.c_int, _i64p, C.c_int, C.c_int64, _vp, _vp, _vp]
+    L.nds_dev_mode_apply.argtypes = [_vp, C.c_int, _i64p, C.c_int, C.c_int64, _vp, _vp, _vp]
     L.nds_dev_back_substitute.argtypes = [_vp, C.c_int, _i64p, _vp, _vp, C.c_double, C.POINTER(_Stats),
                                           C.POINTER(_Singular)]
     L.nds_dev_residual.argtypes = [_vp, C.c_int, _i64p, _vp, _vp, _vp, C.POINTER(C.c_double),
@@ -642,6 +643,12 @@ class Context:
         m = _f(m)
         self._check(self.lib.nds_dev_mode_update(self.h, len(dims_x), _dims(dims_x), int(mode), int(m.shape[0]),
                                                  m.ctypes.data, d_x, d_r))
+
+    def dev_mode_apply(self, dims_x, mode: int, m, d_x: int, d_r: int):
+        """r = m x_mode x on device tensors (no accumulation); m is a host (rows_out, n_mode) matrix."""
+        m = _f(m)
+        self._check(self.lib.nds_dev_mode_apply(self.h, len(dims_x), _dims(dims_x), int(mode), int(m.shape[0]),
+                                                m.ctypes.data, d_x, d_r))
 
     def dev_back_substitute(self, ts, dims, d_c: int, singular_tol=0.0) -> dict:
         """In-place triangular solve of a device tensor (back_substitute on device memory)."""

@@ -1525,8 +1525,21 @@ int nds_dev_mode_product(nds_ctx* ctx, int n_modes, const int64_t* dims, const n
   });
 }
 
+static int dev_mode_rect(nds_ctx* ctx, int n_modes, const int64_t* dims_x, int mode, int64_t rows_out,
+                         const nds_z* m, const nds_z* d_x, nds_z* d_r, bool accumulate);
+
 int nds_dev_mode_update(nds_ctx* ctx, int n_modes, const int64_t* dims_x, int mode, int64_t rows_out,
                         const nds_z* m, const nds_z* d_x, nds_z* d_r) {
+  return dev_mode_rect(ctx, n_modes, dims_x, mode, rows_out, m, d_x, d_r, true);
+}
+
+int nds_dev_mode_apply(nds_ctx* ctx, int n_modes, const int64_t* dims_x, int mode, int64_t rows_out,
+                       const nds_z* m, const nds_z* d_x, nds_z* d_r) {
+  return dev_mode_rect(ctx, n_modes, dims_x, mode, rows_out, m, d_x, d_r, false);
+}
+
+static int dev_mode_rect(nds_ctx* ctx, int n_modes, const int64_t* dims_x, int mode, int64_t rows_out,
+                         const nds_z* m, const nds_z* d_x, nds_z* d_r, bool accumulate) {
   if (!ctx) return NDS_ERR_INVALID;
   return guarded(ctx, [&] {
     checked_total(n_modes, dims_x, 1);
@@ -1546,9 +1559,10 @@ int nds_dev_mode_update(nds_ctx* ctx, int n_modes, const int64_t* dims_x, int mo
     NDS_CUDA(cudaMallocAsync(&dm, mm.size() * sizeof(double2), ctx->stream));
     NDS_CUDA(cudaMemcpyAsync(dm, mm.data(), mm.size() * sizeof(double2), cudaMemcpyHostToDevice, ctx->stream));
     nds::mode_product_matrix_launch(dm, dm + rows_out * n, nds::mode_view(n_modes, dims_x, mode), (const double2*)d_x,
-                                    (double2*)d_r, true, ctx->stream, rows_out);
+                                    (double2*)d_r, accumulate, ctx->stream, rows_out);
     NDS_CUDA(cudaFreeAsync(dm, ctx->stream));
-    NDS_CUDA(cudaStreamSynchronize(ctx->stream));  // mm must outlive the async copy
+    // no stream synchronisation: an async copy from pageable memory has staged mm before it
+    // returns, so the caller may queue further work (the sharded solver chains these)
   });
 }
 

@@ -53,8 +53,8 @@ class CudaLocalOps:
         return torch.zeros(count, dtype=torch.complex128, device=like.device)
 
     def mode_product(self, dims, m, mode, x):
-        out = self.zeros(int(np.prod(dims)), x)
-        self.ctx.dev_mode_update(dims, mode, m, x.data_ptr(), out.data_ptr())
+        out = torch.empty(int(np.prod(dims)), dtype=torch.complex128, device=x.device)
+        self.ctx.dev_mode_apply(dims, mode, m, x.data_ptr(), out.data_ptr())
         return out
 
     def mode_update(self, dims_x, mode, m, x, acc):
