@@ -42,11 +42,17 @@ __device__ __forceinline__ void bin_round(const BinPass& bp, int rd, double2* S,
   int rbit[NB];
 #pragma unroll
   for (int q = 0; q < NB; ++q) rbit[q] = bp.rb[rd][q];
-  for (int s = tid; s < (4096 >> NB); s += kBinThreads) {
-    int p0 = 0;
+  // slot s = tid + 256 j: its tile position p0(s) = p0(tid) ^ p0(256 j) (disjoint bits), and
+  // swz is linear, so swz(p0(s)) = swz(p0(tid)) ^ swz(p0(256 j)) — the thread part once per round
+  int p0t = 0;
 #pragma unroll
-    for (int i = 0; i < 12 - NB; ++i) p0 |= ((s >> i) & 1) << bp.tb[rd][i];
-    const int sp0 = swz(p0);
+  for (int i = 0; i < 8 && i < 12 - NB; ++i) p0t |= ((tid >> i) & 1) << bp.tb[rd][i];
+  const int spt = swz(p0t);
+  for (int s = tid; s < (4096 >> NB); s += kBinThreads) {
+    int p0j = 0;
+#pragma unroll
+    for (int i = 8; i < 12 - NB; ++i) p0j |= ((s >> i) & 1) << bp.tb[rd][i];
+    const int sp0 = spt ^ swz(p0j);
     int addr[V];
     double2 v[V];
 #pragma unroll
