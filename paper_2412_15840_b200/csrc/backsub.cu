@@ -701,7 +701,7 @@ static int persist_launch(const SolvePlan& sp, const double2* t_pool, double2* c
 }
 
 int backsub_launch(const SolvePlan& sp, const double2* t_pool, double2* c, cudaStream_t stream, Recorder* rec,
-                   const HeadSync* head) {
+                   const HeadSync* head, const TailHook* tail) {
   static bool attr_set = false;
   if (!attr_set) {
     NDS_CUDA(cudaFuncSetAttribute(tile_level_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -839,6 +839,7 @@ int backsub_launch(const SolvePlan& sp, const double2* t_pool, double2* c, cudaS
     tmark(sp.s_crit, lv, 5);
     NDS_CUDA(cudaEventRecord(ev_diag(lv), sp.s_crit));
     ++launches;
+    if (tail && tail->fn) tail->fn(tail->ctx, lv, sp.s_crit);
   }
   // join back into the caller's stream
   NDS_CUDA(cudaEventRecord(ev_end, sp.s_crit));

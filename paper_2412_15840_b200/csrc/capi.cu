@@ -36,6 +36,8 @@ struct nds_ctx {
   size_t io_stage_bytes = 0;
   cudaEvent_t io_ev[2] = {};
   cudaEvent_t hev[33] = {};
+  cudaStream_t tail = nullptr;   // tail overlap: first inverse pass per completed mode-N slab
+  cudaEvent_t tev[65] = {};
   std::map<std::vector<int64_t>, std::shared_ptr<nds::SolverCache>> solvers;  // by extents
 };
 
@@ -406,6 +408,52 @@ int execute(nds_plan* p, const double2* b, double2* x, double2* work, cudaEvent_
                     p->n_modes == 3 && passes.back().group < 0 && passes.back().mode == p->n_modes &&
                     lastv.outer == 1 && nds::gemm_rowm_ok(lastv);
   const int last_fwd = head ? N - 1 : N;
+  // Tail overlap (level-synchronous cubic-tile solve, first inverse pass a mode-1 pass that
+  // is not fused): the mode-1 product maps every mode-1 line independently, and the lines with
+  // mode-N index in tile block k are all final once tile (0, .., 0, k) is solved (level L-1-k).
+  // So the first inverse pass runs per mode-N block on a low-priority stream as soon as its level
+  // completes (highest block first) — no accumulation, each piece writes its own slab — and only
+  // the last block's piece remains after the solve. NDS_TAIL=0 disables.
+  static const bool tail_env = !(getenv("NDS_TAIL") && std::string(getenv("NDS_TAIL")) == "0");
+  const bool tail = tail_env && !p->fast_path && p->solver && !p->solver->binary && p->solver->sp.v2 &&
+                    !nds::backsub_is_dataflow(p->solver->sp) && passes.front().group < 0 &&
+                    passes.front().mode == 1 && p->n_modes >= 2 && p->solver->sp.geom.nb[p->n_modes - 1] <= 64;
+  struct TailState {
+    nds_plan* p;
+    XPass pass;
+    const double2* y;
+    double2* x;
+    int64_t nbN, levels, chunk;
+    int next, launches;
+  } ts{};
+  nds::TailHook tail_hook;
+  if (tail) {
+    const nds::TileGeom& tg = p->solver->sp.geom;
+    ts.p = p;
+    ts.pass = passes.front();
+    ts.y = dst_of(N);      // C, solved in place into Y
+    ts.x = dst_of(N + 1);  // first inverse pass output
+    ts.nbN = tg.nb[p->n_modes - 1];
+    ts.levels = p->solver->sp.levels;
+    ts.chunk = p->total / ts.nbN;
+    ts.next = (int)ts.nbN - 1;
+    tail_hook.ctx = &ts;
+    tail_hook.fn = [](void* vctx, int lv, cudaStream_t crit) {
+      TailState& t = *(TailState*)vctx;
+      while (t.next >= 0 && lv >= t.levels - 1 - t.next) {  // block `next` final after level L-1-next
+        nds_ctx* c = t.p->ctx;
+        NDS_CUDA(cudaEventRecord(c->tev[t.next], crit));
+        NDS_CUDA(cudaStreamWaitEvent(c->tail, c->tev[t.next], 0));
+        const int64_t off = (int64_t)t.next * t.chunk;
+        const nds::ModeView full = nds::mode_view(t.p->n_modes, t.p->dims, 1);
+        nds::ModeView v = full;
+        v.outer /= t.nbN;
+        nds::mode_product_launch(t.p->f, 1, false, v, t.y + off, t.x + off, false, c->tail);
+        ++t.launches;
+        --t.next;
+      }
+    };
+  }
   for (int j = 1; j <= last_fwd; ++j) {
     double2* dst = dst_of(j);
     const int kind = launch_pass(p, passes[j - 1], true, src, dst);
@@ -430,16 +478,31 @@ int execute(nds_plan* p, const double2* b, double2* x, double2* work, cudaEvent_
       NDS_CUDA(cudaEventRecord(p->ctx->hev[gq], p->ctx->side));
       ++launches;
     }
+    // the tail pieces write dst_of(N + 1), which the head groups read (pass N - 1's output)
+    if (tail) NDS_CUDA(cudaStreamWaitEvent(p->ctx->tail, p->ctx->hev[groups - 1], 0));
     nds::HeadSync hs;
     hs.per = per;
     hs.ev = p->ctx->hev;
-    launches += nds::backsub_launch(p->solver->sp, p->f.t_pool, c, s, rec, &hs);
+    launches += nds::backsub_launch(p->solver->sp, p->f.t_pool, c, s, rec, &hs, tail ? &tail_hook : nullptr);
+  } else if (tail) {
+    launches += nds::backsub_launch(p->solver->sp, p->f.t_pool, c, s, rec, nullptr, &tail_hook);
   } else {
     launches += backsub_run(p, c);
   }
-  if (ev) NDS_CUDA(cudaEventRecord(ev[2], s));
   src = c;
-  for (int j = 1; j <= N; ++j) {
+  int first_inv = 1;
+  if (tail) {
+    if (ts.next >= 0) throw Error(NDS_ERR_OTHER, "tail overlap: a mode-N block was never scheduled");
+    // join the first inverse pass (run per mode-N block on the tail stream)
+    NDS_CUDA(cudaEventRecord(p->ctx->tev[64], p->ctx->tail));
+    NDS_CUDA(cudaStreamWaitEvent(s, p->ctx->tev[64], 0));
+    launches += ts.launches;
+    if (rec) rec->mark(s, nds::kXformGemm, 1);
+    src = dst_of(N + 1);
+    first_inv = 2;
+  }
+  if (ev) NDS_CUDA(cudaEventRecord(ev[2], s));
+  for (int j = first_inv; j <= N; ++j) {
     double2* dst = dst_of(N + j);
     const int kind = launch_pass(p, passes[j - 1], false, src, dst);
     if (rec) rec->mark(s, kind, passes[j - 1].mode);
@@ -1079,6 +1142,12 @@ int nds_ctx_create(nds_ctx** out, int device) {
     NDS_CUDA(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
     NDS_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
     for (auto& e : c->hev) NDS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    {
+      int lo = 0, hi = 0;
+      NDS_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      NDS_CUDA(cudaStreamCreateWithPriority(&c->tail, cudaStreamNonBlocking, lo));
+    }
+    for (auto& e : c->tev) NDS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     // keep stream-ordered allocations (factor pools) cached instead of returning them at syncs
     cudaMemPool_t pool;
     NDS_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
@@ -1101,6 +1170,9 @@ void nds_ctx_destroy(nds_ctx* ctx) {
     if (e) cudaEventDestroy(e);
   for (auto& e : ctx->hev)
     if (e) cudaEventDestroy(e);
+  for (auto& e : ctx->tev)
+    if (e) cudaEventDestroy(e);
+  if (ctx->tail) cudaStreamDestroy(ctx->tail);
   if (ctx->copy) cudaStreamDestroy(ctx->copy);
   if (ctx->side) cudaStreamDestroy(ctx->side);
   if (ctx->stage) cudaFreeHost(ctx->stage);

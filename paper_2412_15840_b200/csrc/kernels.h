@@ -182,9 +182,15 @@ struct HeadSync {
   int per = 0;
   const cudaEvent_t* ev = nullptr;
 };
+// Tail overlap: after the diagonal launch of each level, fn(ctx, lv, critical stream) — used to
+// start the first inverse pass on the mode-N slabs of Y that this level completed.
+struct TailHook {
+  void (*fn)(void* ctx, int lv, cudaStream_t crit) = nullptr;
+  void* ctx = nullptr;
+};
 // In-place Y over C. Returns kernels launched.
 int backsub_launch(const SolvePlan& sp, const double2* t_pool, double2* c, cudaStream_t stream,
-                   Recorder* rec = nullptr, const HeadSync* head = nullptr);
+                   Recorder* rec = nullptr, const HeadSync* head = nullptr, const TailHook* tail = nullptr);
 // True when backsub_launch runs the dataflow (persistent-kernel) solve for this plan, which does
 // not honour HeadSync.
 bool backsub_is_dataflow(const SolvePlan& sp);

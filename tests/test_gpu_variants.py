@@ -45,6 +45,7 @@ VARIANTS = [
     {"NDS_NEAR": "kernel"},
     {"NDS_HEAD": "0"},
     {"NDS_FAR2": "0"},
+    {"NDS_TAIL": "0"},
 ]
 
 
