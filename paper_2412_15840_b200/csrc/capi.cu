@@ -497,7 +497,8 @@ int execute(nds_plan* p, const double2* b, double2* x, double2* work, cudaEvent_
     NDS_CUDA(cudaEventRecord(p->ctx->tev[64], p->ctx->tail));
     NDS_CUDA(cudaStreamWaitEvent(s, p->ctx->tev[64], 0));
     launches += ts.launches;
-    if (rec) rec->mark(s, nds::kXformGemm, 1);
+    // profiled with the solve (like the head pass): its pieces overlap the tail levels
+    if (rec) rec->mark(s, nds::kBacksubPersistent, 0);
     src = dst_of(N + 1);
     first_inv = 2;
   }
