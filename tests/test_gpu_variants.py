@@ -1,7 +1,8 @@
 """GPU parity of the solve paths that environment switches select (A/B experiments kept in the
 library): plain per-target far items, grouped far items (G = 2 / 4 targets per slab read, with
 remainder items that accumulate into their slot), k-split far items, the per-hyperplane diagonal
-kernel, the separate near-update launches and no head overlap. The switches are read once per
+kernel, the separate near-update launches, no head / tail overlap, one far stream and the
+dataflow (persistent-kernel) solve. The switches are read once per
 process, so each variant runs in a subprocess against the C oracle on cubic-tile shapes with
 several blocks per mode (far items, group remainders, truncated groups)."""
 import json
@@ -46,6 +47,8 @@ VARIANTS = [
     {"NDS_HEAD": "0"},
     {"NDS_FAR2": "0"},
     {"NDS_TAIL": "0"},
+    {"NDS_FARGROUP": "plain", "NDS_SOLVE": "split"},    # dataflow (persistent) solve, N = 3
+    {"NDS_FARGROUP": "plain", "NDS_SOLVE": "unified"},
 ]
 
 
