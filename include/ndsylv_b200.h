@@ -100,7 +100,8 @@ const char* nds_version(void);
 /* ---- context ------------------------------------------------------------------------- */
 int nds_ctx_create(nds_ctx** out, int device);
 void nds_ctx_destroy(nds_ctx* ctx);
-/* Use an external cudaStream_t (e.g. torch's current stream); NULL restores the own stream. */
+/* Use an external cudaStream_t (e.g. torch's current stream); NULL restores the own stream.
+ * To run on the legacy default stream pass cudaStreamLegacy ((void*)0x1), not NULL. */
 int nds_ctx_set_stream(nds_ctx* ctx, void* cuda_stream);
 void* nds_ctx_stream(nds_ctx* ctx);
 const char* nds_last_error(const nds_ctx* ctx);
@@ -164,6 +165,11 @@ int nds_plan_inverse(nds_plan* plan, const nds_z* d_in, nds_z* d_out, nds_z* d_w
 int nds_plan_execute_host(nds_plan* plan, const nds_z* h_b, nds_z* h_x, nds_report* rep);
 /* Kernel launches one nds_plan_execute issues. */
 int nds_plan_launches(const nds_plan* plan);
+/* Which triangular-solve route the plan takes: the fast-path divide,
+ * generic tiles (any shape), cubic 16^3 / 8^4 tiles with DMMA far updates (c0-c3), or the
+ * all-binary tiles (c4). -1 for a NULL plan. */
+enum { NDS_PATH_FAST = 0, NDS_PATH_GENERIC = 1, NDS_PATH_CUBIC = 2, NDS_PATH_BINARY = 3 };
+int nds_plan_solve_path(const nds_plan* plan);
 /* Per-launch device timing: after _begin, every launch of execute/forward/backsub/inverse records
  * a CUDA event on the context stream (up to max_launches). _end synchronises and returns the
  * number of launches written: kind (0 transform GEMM, 1 transform direct, 2 solve level,

@@ -263,6 +263,8 @@ class Ref:
         L.ref_write_tensor.argtypes = [C.c_char_p, C.c_int, _i64p, _dp]
         L.ref_read_tensor.argtypes = [C.c_char_p, C.POINTER(C.c_int), _i64p, _dp, C.c_int64]
         L.ref_random_ode_system.argtypes = [C.c_int, _i64p, C.c_uint64, _dpp, _dp, _dp]
+        L.ref_harness_randn.argtypes = [C.c_uint64, C.c_uint64, C.c_int64, _dp]
+        L.ref_solve_gen.argtypes = [C.c_int, _i64p, _dpp, _dp, C.c_uint64, _dp, C.POINTER(_ReportRef)]
 
     def _check(self, rc, bad=None, den=None):
         if rc:
@@ -392,6 +394,24 @@ class Ref:
         shape = tuple(dims[j] for j in range(n.value))
         out = np.empty(shape, dtype=np.complex128, order="F")
         self._check(self.lib.ref_read_tensor(path.encode(), C.byref(n), dims, _ptr(out), out.size))
+        return out
+
+    def solve_gen(self, a_list, dims, seed, b=None):
+        """ndsylv::solve with B = generator v1 (seed, stream 1000) built inside the library, or
+        a copy of `b`; returns (X, report)."""
+        ap, keep = _ptrs(a_list)
+        x = np.empty(tuple(dims), dtype=np.complex128, order="F")
+        bf = None if b is None else fortran(b)
+        bp = None if bf is None else _ptr(bf)
+        rep = _ReportRef()
+        self._check(self.lib.ref_solve_gen(len(dims), _dims(dims), ap, bp, int(seed), _ptr(x), C.byref(rep)))
+        return x, _as_dict(rep)
+
+    def randn(self, seed, stream, count):
+        """Harness generator v1 (same stream as the product's nds_randn) — inputs for the
+        reference arm and the X_ref fixtures without loading the product library."""
+        out = np.empty(int(count), dtype=np.float64)
+        self.lib.ref_harness_randn(seed & (2**64 - 1), stream & (2**64 - 1), int(count), _ptr(out))
         return out
 
     def random_ode_system(self, dims, seed):

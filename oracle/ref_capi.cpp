@@ -9,6 +9,7 @@
 // reference types (NDTensor / Matrix / SchurFactors, column-major complex<double>).
 #include <omp.h>
 
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -326,6 +327,68 @@ int ref_random_ode_system(int n_modes, const std::int64_t* dims, std::uint64_t s
 void ref_xoshiro_uniform(std::uint64_t seed, std::int64_t count, double* out) {
   Xoshiro256pp rng(seed);
   for (std::int64_t i = 0; i < count; ++i) out[i] = rng.uniform();
+}
+
+// Harness input generator v1 (NOT reference code): counter-based splitmix64 +
+// Box-Muller, the same stream as the product's nds_randn (csrc/randn.cpp), so that the reference
+// arm of bench.py and the X_ref fixture scripts build their inputs without loading the product
+// library. Value pair m of (seed, stream) uses counters 2m and 2m+1.
+void ref_harness_randn(std::uint64_t seed, std::uint64_t stream, std::int64_t count, double* out) {
+  auto mix = [](std::uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+  };
+  const std::uint64_t key = mix(mix(seed) ^ (stream * 0xd1342543de82ef95ULL + 0x632be59bd9b4e019ULL));
+  const std::int64_t pairs = (count + 1) / 2;
+  const double two_pi = 6.283185307179586476925286766559;
+#pragma omp parallel for schedule(static)
+  for (std::int64_t m = 0; m < pairs; ++m) {
+    const std::uint64_t b1 = mix(key + (2 * static_cast<std::uint64_t>(m) + 1) * 0x9e3779b97f4a7c15ULL);
+    const std::uint64_t b2 = mix(key + (2 * static_cast<std::uint64_t>(m) + 2) * 0x9e3779b97f4a7c15ULL);
+    const double u1 = static_cast<double>((b1 >> 11) + 1) * 0x1.0p-53;
+    const double u2 = static_cast<double>(b2 >> 11) * 0x1.0p-53;
+    const double r = std::sqrt(-2.0 * std::log(u1));
+    const double th = two_pi * u2;
+    out[2 * m] = r * std::cos(th);
+    if (2 * m + 1 < count) out[2 * m + 1] = r * std::sin(th);
+  }
+}
+
+// ndsylv::solve on a harness-generated right-hand side: B = ref_harness_randn(seed, 1000, 2P)
+// (generator v1) written straight into the reference's NDTensor, or copied from
+// `b` when it is non-null. Used by tests/golden/make_xref.py for the full-size X_ref fixtures of
+// c1-c4, where a separate host copy of an 8.6 GB B would not fit next to the solve.
+int ref_solve_gen(int n_modes, const std::int64_t* dims, const double* const* a, const double* b,
+                  std::uint64_t seed, double* x, ref_report* rep) {
+  return guarded([&] {
+    SylvesterProblem p;
+    for (int j = 0; j < n_modes; ++j) p.coefficients.push_back(matrix_from(static_cast<int>(dims[j]), a[j]));
+    if (b) {
+      p.rhs = tensor_from(n_modes, dims, b);
+    } else {
+      const auto d = dims_of(n_modes, dims);
+      const std::int64_t total = checked_total(d);
+      std::vector<cxd> v(static_cast<std::size_t>(total));
+      ref_harness_randn(seed, 1000, 2 * total, reinterpret_cast<double*>(v.data()));
+      p.rhs = NDTensor::make(d, std::move(v));
+    }
+    const SolveResult r = solve(p, SolveOptions{});
+    tensor_to(r.x, x);
+    if (rep) {
+      rep->min_abs_denominator = r.report.min_abs_denominator;
+      rep->used_normal_fast_path = r.report.used_normal_fast_path;
+      rep->flop_estimate = r.report.flop_estimate;
+      rep->schur_flop_estimate = r.report.schur_flop_estimate;
+      rep->backsub_entries = r.report.backsub_entries;
+      rep->backsub_multiplies = r.report.backsub_multiplies;
+      rep->schur_seconds = r.report.schur_seconds;
+      rep->transform_seconds = r.report.transform_seconds;
+      rep->backsub_seconds = r.report.backsub_seconds;
+      rep->inverse_seconds = r.report.inverse_seconds;
+      rep->total_seconds = r.report.total_seconds;
+    }
+  });
 }
 
 }  // extern "C"

@@ -49,7 +49,7 @@ EXPORTED = [
     "nds_ctx_trim", "nds_solve", "nds_solve_schur", "nds_schur", "nds_forward_transform", "nds_inverse_transform",
     "nds_back_substitute", "nds_mode_product", "nds_apply_operator", "nds_flop_estimate", "nds_schur_flop_estimate",
     "nds_plan_create", "nds_plan_destroy", "nds_plan_report", "nds_plan_total", "nds_plan_execute",
-    "nds_plan_forward", "nds_plan_backsub", "nds_plan_inverse", "nds_plan_execute_host", "nds_plan_launches",
+    "nds_plan_forward", "nds_plan_backsub", "nds_plan_inverse", "nds_plan_execute_host", "nds_plan_launches", "nds_plan_solve_path",
     "nds_plan_profile_begin", "nds_plan_profile_end",
     "nds_dev_mode_product", "nds_dev_mode_update", "nds_dev_mode_apply", "nds_dev_back_substitute", "nds_dev_residual",
     "nds_triangular_exp", "nds_ode_create", "nds_ode_destroy", "nds_ode_at", "nds_ode_at_dev", "nds_propagate",
@@ -167,6 +167,7 @@ def load_library(path: str = LIB_PATH):
     L.nds_plan_inverse.argtypes = [_vp, _vp, _vp, _vp]
     L.nds_plan_execute_host.argtypes = [_vp, _vp, _vp, C.POINTER(_Report)]
     L.nds_plan_launches.argtypes = [_vp]
+    L.nds_plan_solve_path.argtypes = [_vp]
     L.nds_plan_profile_begin.argtypes = [_vp, C.c_int]
     L.nds_plan_profile_end.argtypes = [_vp, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int),
                                        C.POINTER(C.c_float)]
@@ -425,6 +426,13 @@ class Plan:
     def launches(self) -> int:
         return self.ctx.lib.nds_plan_launches(self.h)
 
+    SOLVE_PATHS = {0: "fast", 1: "generic", 2: "cubic", 3: "binary"}
+
+    def solve_path(self) -> str:
+        """Triangular-solve route: 'fast', 'generic' (any shape), 'cubic' (16^3 / 8^4 DMMA tiles)
+        or 'binary' (all n_j = 2)."""
+        return self.SOLVE_PATHS[self.ctx.lib.nds_plan_solve_path(self.h)]
+
     def profile_begin(self, max_launches: int):
         self._check(self.ctx.lib.nds_plan_profile_begin(self.h, int(max_launches)))
 
@@ -470,8 +478,20 @@ class Context:
         if rc:
             _raise(rc, self.last_error(), sing)
 
+    # cudaStreamLegacy: the legacy default stream (torch's default stream reports handle 0)
+    LEGACY_STREAM = 0x1
+
     def set_stream(self, stream_handle: int | None):
-        self._check(self.lib.nds_ctx_set_stream(self.h, stream_handle or None))
+        """Run the context's device work on an external stream. None restores the context's own
+        stream; 0 (torch's default stream) means the legacy default stream, which orders with
+        every blocking stream of the process — NOT the context's own non-blocking stream."""
+        if stream_handle is None:
+            h = None
+        elif int(stream_handle) == 0:
+            h = self.LEGACY_STREAM
+        else:
+            h = int(stream_handle)
+        self._check(self.lib.nds_ctx_set_stream(self.h, h))
 
     def stream(self) -> int:
         return self.lib.nds_ctx_stream(self.h) or 0

@@ -15,8 +15,6 @@ import math
 
 import numpy as np
 
-from . import randn
-
 GENERATOR_VERSION = "v1"
 
 CONFIGS = {
@@ -36,7 +34,13 @@ DESCRIPTIONS = {
 }
 
 
-def gauss_coefficients(dims, seed, scaled=True):
+def _default_randn():
+    from . import randn
+    return randn
+
+
+def gauss_coefficients(dims, seed, scaled=True, randn=None):
+    randn = randn or _default_randn()
     out = []
     for j, n in enumerate(dims):
         g = randn(seed, 2 * j, n * n).reshape((n, n), order="F")
@@ -49,7 +53,8 @@ def gauss_coefficients(dims, seed, scaled=True):
     return out
 
 
-def gauss_rhs(dims, seed):
+def gauss_rhs(dims, seed, randn=None):
+    randn = randn or _default_randn()
     total = int(np.prod(dims))
     v = randn(seed, 1000, 2 * total).view(np.complex128)
     return v.reshape(dims, order="F")
@@ -80,11 +85,15 @@ def advdiff_rhs(n=96, n_modes=4):
     return np.asfortranarray(b.astype(np.complex128))
 
 
-def make_problem(name: str, seed: int = 0, dims=None):
-    """(coefficients, rhs) for a BASELINE config; `dims` overrides the shape (reduced sizes)."""
+def make_problem(name: str, seed: int = 0, dims=None, randn=None):
+    """(coefficients, rhs) for a BASELINE config; `dims` overrides the shape (reduced sizes).
+
+    `randn(seed, stream, count)` defaults to the product library's generator; the reference arm
+    of bench.py and the X_ref fixture scripts pass the bit-identical copy in oracle/_ref
+    (``oracle.Ref().randn``) so that they never load the product library."""
     cfg = CONFIGS[name]
     d = tuple(dims) if dims is not None else cfg["dims"]
     if cfg["kind"] == "advdiff":
         n = d[0]
         return advdiff_coefficients(n, len(d)), advdiff_rhs(n, len(d))
-    return gauss_coefficients(d, seed, cfg["scaled"]), gauss_rhs(d, seed)
+    return gauss_coefficients(d, seed, cfg["scaled"], randn), gauss_rhs(d, seed, randn)

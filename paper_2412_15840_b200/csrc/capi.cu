@@ -1320,6 +1320,14 @@ int nds_plan_execute_host(nds_plan* plan, const nds_z* h_b, nds_z* h_x, nds_repo
 
 int nds_plan_launches(const nds_plan* plan) { return plan ? plan->launches : -1; }
 
+int nds_plan_solve_path(const nds_plan* plan) {
+  if (!plan) return -1;
+  if (plan->fast_path) return NDS_PATH_FAST;
+  if (!plan->solver) return -1;
+  if (plan->solver->binary) return NDS_PATH_BINARY;
+  return plan->solver->sp.v2 ? NDS_PATH_CUBIC : NDS_PATH_GENERIC;
+}
+
 int nds_plan_profile_begin(nds_plan* plan, int max_launches) {
   if (!plan || max_launches < 2) return NDS_ERR_INVALID;
   return guarded(plan->ctx, [&] {

@@ -9,7 +9,8 @@ import pytest
 
 from paper_2412_15840_b200 import configs
 
-GOLDEN = sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", "*.npz")))
+GOLDEN = sorted(p for p in glob.glob(os.path.join(os.path.dirname(__file__), "golden", "*.npz"))
+                if not os.path.basename(p).startswith("xref_"))
 
 
 def load(path):
@@ -41,3 +42,20 @@ def test_generator_v1_pinned():
     assert np.array_equal(b, z["b"])
     for j in range(3):
         assert np.array_equal(a[j], z[f"a{j}"])
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4"])
+def test_xref_fixture_metadata(name):
+    """The full-size X_ref fixtures (tests/golden/make_xref.py, the reference's own solve) carry
+    the generator, seed, extents and enough samples for tests/test_gpu_fullsize.py."""
+    import json
+    from paper_2412_15840_b200 import configs
+    fx = np.load(os.path.join(os.path.dirname(__file__), "golden", f"xref_{name}.npz"))
+    assert tuple(fx["dims"]) == tuple(configs.CONFIGS[name]["dims"])
+    assert str(fx["generator"]) == configs.GENERATOR_VERSION and int(fx["seed"]) == 0
+    idx = fx["idx"]
+    assert idx.size >= 65536 and np.all(np.diff(idx) > 0) and idx[0] == 0 and idx[-1] == np.prod(fx["dims"]) - 1
+    assert np.all(np.isfinite(fx["x"])) and float(fx["xmax"]) >= np.abs(fx["x"]).max()
+    assert fx["sum_first"].shape == (fx["dims"][0],) and fx["sum_last"].shape == (fx["dims"][-1],)
+    meta = json.loads(str(fx["meta"]))
+    assert meta["config"] == name and meta["report"]["backsub_entries"] == np.prod(fx["dims"])

@@ -16,7 +16,8 @@ from conftest import rel_max
 
 pytestmark = pytest.mark.gpu
 
-GOLDEN = sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", "*.npz")))
+GOLDEN = sorted(p for p in glob.glob(os.path.join(os.path.dirname(__file__), "golden", "*.npz"))
+                if not os.path.basename(p).startswith("xref_"))
 
 
 def rand_c(rng, shape):
@@ -188,13 +189,50 @@ def test_c0_full_against_reference(ctx, ref):
     assert np.linalg.norm(res - b) / np.linalg.norm(b) <= 1e-10
 
 
-@pytest.mark.parametrize("name,dims", [("c1", (256, 256, 8)), ("c2", (32, 32, 32, 32)), ("c3", (128, 128, 8, 4)),
-                                       ("c4", (2,) * 16)])
-def test_configs_reduced_against_reference(ctx, ref, name, dims):
+# Reduced shapes chosen so that the solve runs the PRODUCTION route of each config (16^3 / 8^4
+# cubic tiles with >= 3 tile blocks per mode, i.e. DMMA far items, pushed near items and the
+# line-owner diagonal kernel; all-binary tiles for c4), with the default environment.
+REDUCED = [("c1", (128, 128, 64), "cubic"), ("c2", (32, 32, 32, 32), "cubic"), ("c3", (64, 64, 32, 32), "cubic"),
+           ("c3", (32, 32, 32, 32), "cubic"), ("c4", (2,) * 16, "binary"), ("c4", (2,) * 20, "binary")]
+
+
+@pytest.mark.parametrize("name,dims,path", REDUCED, ids=[f"{n}-{'x'.join(map(str, d))}" for n, d, _ in REDUCED])
+def test_configs_reduced_against_reference(ctx, ref, name, dims, path):
+    """sylvester.cpp:167-227 on the same inputs: the GPU X (host API and device plan) against the
+    reference's X at the north_star tolerance, on the route the full config takes."""
+    import torch
     a, b = configs.make_problem(name, seed=1, dims=dims)
-    x_ref, _ = ref.solve(a, b)
+    dims = b.shape
+    x_ref, rep = ref.solve(a, b)
     r = ctx.solve(a, b)
     assert rel_max(r.x, x_ref) <= 1e-9
+    assert r.report["backsub_multiplies"] == rep["backsub_multiplies"]
+    us, ts = zip(*[ctx.schur(m) for m in a])
+    plan = ctx.plan(list(us), list(ts))
+    assert plan.solve_path() == path
+    d_b = torch.from_numpy(np.ascontiguousarray(b.ravel(order="F"))).cuda()
+    d_x, d_w = torch.empty_like(d_b), torch.empty_like(d_b)
+    ctx.set_stream(torch.cuda.current_stream().cuda_stream)
+    plan.execute(d_b.data_ptr(), d_x.data_ptr(), d_w.data_ptr())
+    torch.cuda.synchronize()
+    ctx.set_stream(None)
+    x_plan = d_x.cpu().numpy().reshape(dims, order="F")
+    assert rel_max(x_plan, x_ref) <= 1e-9
+
+
+@pytest.mark.parametrize("dims", [(64, 64, 64), (48, 48, 48), (16, 32, 48, 64)],
+                         ids=["64x64x64", "48x48x48", "16x32x48x64"])
+def test_cubic_solve_stage_against_oracle(ctx, port, dims):
+    """The production cubic-tile back-substitution alone (default environment, far items on
+    every mode) against the oracle's back_substitute (sylvester.cpp:71-108) on the same C."""
+    rng = np.random.default_rng(23)
+    us, ts = rand_factors(rng, dims)
+    c = rand_c(rng, dims)
+    plan = ctx.plan(us, ts, allow_fast_path=False)
+    assert plan.solve_path() == "cubic"
+    y_gpu = ctx.back_substitute(ts, c)[0]
+    y_ref = port.back_substitute(ts, c)[0]
+    assert rel_max(y_gpu, y_ref) <= 1e-12
 
 
 @pytest.mark.parametrize("dims", [(2,) * 20, (48, 40, 64), (16, 16, 16, 32), (40, 3, 1024), (24, 20, 256),
