@@ -204,7 +204,8 @@ int nds_dev_residual(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z
 /* ---- ODE  dX/dt = sum_j A_j x_j X + B,  X(0) = X0  (reference ode.hpp) ------ */
 
 /* ndsylv::triangular_exp (schur.hpp:24, schur.cpp:203-228): f = exp(t T), T upper triangular
- * n x n column-major (Parlett recurrence, [6/6] Pade when the diagonal is not well separated).
+ * n x n column-major (Parlett recurrence; Taylor scaling and squaring when the diagonal is not
+ * well separated).
  * Host, like nds_schur. NDS_ERR_INVALID when T has a nonzero strict lower part. */
 int nds_triangular_exp(nds_ctx* ctx, int n, const nds_z* t_mat, double t, nds_z* f);
 

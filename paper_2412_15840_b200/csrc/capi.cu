@@ -858,19 +858,9 @@ void ode_create_impl(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z
     o->foff[j] = o->fsize;
     o->fsize += 2 * dims[j] * dims[j];
     o->t_host.emplace_back(t[j], t[j] + dims[j] * dims[j]);
-    // schur.cpp:164-174 diagonal_well_separated -> Parlett (device); otherwise Pade (host)
-    const int64_t n = dims[j];
-    double dmax = 0.0;
-    for (int64_t i = 0; i < n; ++i) dmax = std::max(dmax, std::hypot(t[j][i * (n + 1)].re, t[j][i * (n + 1)].im));
-    const double threshold = 1e-8 * (1.0 + dmax);
-    bool sep = true;
-    for (int64_t i = 0; i < n && sep; ++i)
-      for (int64_t k = i + 1; k < n; ++k)
-        if (std::hypot(t[j][i * (n + 1)].re - t[j][k * (n + 1)].re, t[j][i * (n + 1)].im - t[j][k * (n + 1)].im) <
-            threshold) {
-          sep = false;
-          break;
-        }
+    // well-separated diagonal -> Parlett recurrence on the device; otherwise host scaling and
+    // squaring (matfun.cpp)
+    const bool sep = nds::exp_diagonal_separated((int)dims[j], t[j]);
     o->parlett.push_back(sep ? 1 : 0);
   }
   NDS_CUDA(cudaMalloc(&o->d_c, bytes));
@@ -911,7 +901,8 @@ int ode_at_dev_impl(nds_ode* o, double time, double2* d_x, cudaEvent_t* ev) {
   const int N = p->n_modes;
   ensure_ws(ctx, p->total);
   // exp(time T_j) (schur.cpp:203-228): the Parlett recurrence on the device for modes with a
-  // well-separated diagonal; Pade on the host (staged once the previous upload drained) otherwise
+  // well-separated diagonal; scaling and squaring on the host (staged once the previous upload
+  // drained) otherwise
   if (ev) NDS_CUDA(cudaEventRecord(ev[0], s));
   int launches = 0;
   nds::ExpArgs ea{};
