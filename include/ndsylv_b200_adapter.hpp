@@ -4,6 +4,8 @@
 #include <chrono>
 #include <memory>
 #include <stdexcept>
+#include <string>
+#include <vector>
 #include "ndsylv/ode.hpp"
 #include "ndsylv/sylvester.hpp"
 #include "ndsylv_b200.h"
@@ -36,9 +38,25 @@ inline void rethrow(int rc, const nds_singular& s) {
   }
 }
 
+// The reference's shape checks (sylvester.cpp:17-27 validate_problem, ode.cpp:17-28) with its
+// messages, run before any Schur step or C-ABI call reads the coefficient storage.
+inline void validate_coefficients(const std::vector<Matrix>& coefficients, const std::vector<std::int64_t>& dims,
+                                  const char* what) {
+  const int n_modes = static_cast<int>(dims.size());
+  if (n_modes < 2) throw std::invalid_argument(std::string(what) + " order must be at least 2");
+  if (static_cast<int>(coefficients.size()) != n_modes)
+    throw std::invalid_argument("coefficient count does not match tensor order");
+  for (int j = 0; j < n_modes; ++j) {
+    const Matrix& a = coefficients[static_cast<std::size_t>(j)];
+    if (!a.square() || a.rows() != dims[static_cast<std::size_t>(j)])
+      throw std::invalid_argument("coefficient " + std::to_string(j + 1) + " does not match mode extent");
+  }
+}
+
 // Same contract as ndsylv::solve (sylvester.cpp:167-227): Schur on the host with the
 // reference's own ndsylv::schur, transforms + triangular solve on the GPU.
 inline SolveResult solve(const SylvesterProblem& p, const SolveOptions& o = {}) {
+  validate_coefficients(p.coefficients, p.rhs.dims, "problem");
   const int n = p.rhs.order();
   std::vector<SchurFactors> f;
   SolveResult r;
@@ -81,9 +99,7 @@ class OdePropagator {
   explicit OdePropagator(OdeSystem system, SolveOptions options = {})
       : system_(std::move(system)), options_(options) {
     const int n = system_.forcing.order();
-    if (n < 2) throw std::invalid_argument("system order must be at least 2");
-    if (static_cast<int>(system_.coefficients.size()) != n)
-      throw std::invalid_argument("coefficient count does not match tensor order");
+    validate_coefficients(system_.coefficients, system_.forcing.dims, "system");
     if (system_.initial.dims != system_.forcing.dims) throw std::invalid_argument("initial state shape mismatch");
     const auto t0 = std::chrono::steady_clock::now();
     for (const Matrix& a : system_.coefficients) factors_.push_back(schur(a));
@@ -137,6 +153,7 @@ inline SolveResult propagate(const OdeSystem& system, double t, const SolveOptio
 
 inline NDTensor rk4_reference(const OdeSystem& system, double t, double dt, std::int64_t max_steps = 50'000'000) {
   const int n = system.forcing.order();
+  validate_coefficients(system.coefficients, system.forcing.dims, "system");
   if (system.initial.dims != system.forcing.dims) throw std::invalid_argument("initial state shape mismatch");
   std::vector<const nds_z*> a;
   for (const Matrix& m : system.coefficients) a.push_back(reinterpret_cast<const nds_z*>(m.data()));

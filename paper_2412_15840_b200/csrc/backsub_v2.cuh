@@ -8,13 +8,6 @@
 #else
 #define NDS_LPROBE(k)
 #endif
-#ifdef NDS_DIAG_PROBES  // timing probes for tools/microbench/diag_bench.cu only
-#define NDS_PROBE(k, v) \
-  if (tid == 0 && blockIdx.x == 0) nds_diag_probe[lv * 4 + (k)] = clock64() + (long long)((v) * 0)
-#else
-#define NDS_PROBE(k, v)
-#endif
-
 constexpr int kUpdThreads = 256;
 
 
@@ -30,197 +23,6 @@ __device__ __forceinline__ void dmma_bs(double& c0, double& c1, double a, double
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
       : "+d"(c0), "+d"(c1)
       : "d"(a), "d"(b));
-}
-
-// Off-tile coupling of one work item (tile I, mode j, rows [kb, ke) along mode j) as a small
-// complex GEMM on the FP64 tensor pipe:
-//   partial(l_j, c) = sum_{k in [kb, ke)} T_j(o_j + l_j, k) * Y(k along mode j, c),
-// rows l_j (b_j = 8 RB), columns c = the other local coordinates of the tile (cols = 4096 / b_j),
-// K streamed from global through an ST-stage cp.async ring of BK = KM 2048 / cols rows (KM 32 KB).
-// Every thread owns 8 KM fixed (k, c) slots of each stage; their global / shared offsets are
-// computed once. Each warp owns RB x CB fragments (8x8) and reuses its A/B fragments across
-// them. The partial is written in tile-local column-major order for the diagonal kernel.
-template <int RB, int CB, bool M3, int KM, int ST, int H>
-__device__ __forceinline__ void update_body(const TileGeom& g, const double2* __restrict__ T,
-                                            const int64_t* __restrict__ tiles, const int4 it, const int half,
-                                            double2* __restrict__ out, const double2* __restrict__ Y,
-                                            double2* __restrict__ sm) {
-  constexpr int BJ = 8 * RB;
-  constexpr int TCOLS = 4096 / BJ;       // columns of the tile
-  constexpr int COLS = TCOLS / H;        // columns of this CTA (H CTAs per item)
-  constexpr int BK = KM * 2048 / TCOLS;
-  constexpr int LDB = COLS + 2;          // = 2 mod 8 -> conflict-free B fragments
-  constexpr int ALD = BK <= 8 ? 12 : BK + 4;  // = 4 mod 8 -> conflict-free A fragments
-  constexpr int SL = 8 * KM / H;         // load slots per thread and stage
-  static_assert(CB * 8 * (kUpdThreads / 32) == COLS && BK % 4 == 0 && BJ * BK <= kUpdThreads, "tile shape");
-  __shared__ int64_t so[NDS_MAX_MODES];
-  __shared__ int64_t s_base;
-  const int j = it.y, kb = it.z, ke = it.w;
-  const int N = g.n_modes;
-  int64_t* colg = (int64_t*)sm;  // global offset of column c
-  int* coll = (int*)(colg + COLS);
-  double2* sA = (double2*)(coll + COLS);  // [ST][BJ][ALD]
-  double2* sB = sA + ST * BJ * ALD;       // [ST][BK][LDB]
-  const int tid = threadIdx.x;
-  if (tid == 0) {
-    int64_t t = tiles[it.x];
-    int64_t base = 0;
-    for (int m = 0; m < N; ++m) {
-      const int64_t I = t % g.nb[m];
-      t /= g.nb[m];
-      so[m] = I * g.b[m];
-      if (m != j) base += so[m] * g.strides[m];
-    }
-    s_base = base;
-  }
-  for (int c = tid; c < COLS; c += kUpdThreads) {  // c: local coords of modes != j, earliest fastest
-    int rem = c + half * COLS;
-    int64_t og = 0;
-    int ol = 0;
-    for (int m = 0; m < N; ++m) {
-      if (m == j) continue;
-      const int lm = rem % BJ;
-      rem /= BJ;
-      og += lm * g.strides[m];
-      ol += lm * g.bstride[m];
-    }
-    colg[c] = og;
-    coll[c] = ol;
-  }
-  __syncthreads();
-  const int64_t sj = g.strides[j];
-  const double2* Yb = Y + s_base;
-  const double2* Tj = T + g.toff[j] + so[j];
-  const int64_t nj = g.dims[j];
-
-  // fixed per-thread load slots. Mode 1 (j == 0) is contiguous along k in global memory, so
-  // its lanes run along k and the stage is stored k-fastest ([c][8] with the k index XOR-swizzled
-  // by bit 0 of c: conflict-free for both the cp.async writes and the fragment reads); other
-  // modes run along c into the [k][LDB] layout.
-  const bool kfast = j == 0;
-  int gofs[SL];
-  int sofs[SL];
-#pragma unroll
-  for (int i = 0; i < SL; ++i) {
-    const int e = tid + i * kUpdThreads;
-    int k, c;
-    if (kfast) {
-      k = e % BK;
-      c = e / BK;
-      sofs[i] = c * BK + (k ^ (BK >= 8 ? (c & 1) << 2 : 0));
-    } else {
-      c = e % COLS;
-      k = e / COLS;
-      sofs[i] = k * LDB + c;
-    }
-    gofs[i] = (int)((int64_t)k * sj + colg[c]);
-  }
-  const bool a_loader = tid < BJ * BK;
-  const int a_r = tid % BJ, a_k = tid / BJ;  // rows fastest: coalesced along T_j's columns
-
-  auto load_stage = [&](int stage, int k0) {
-    double2* dB = sB + stage * BK * LDB;
-    const double2* src = Yb + (int64_t)k0 * sj;
-#pragma unroll
-    for (int i = 0; i < SL; ++i) cp_async16_bs(dB + sofs[i], src + gofs[i]);
-    if (a_loader) cp_async16_bs(sA + stage * BJ * ALD + a_r * ALD + a_k, Tj + a_r + (int64_t)(k0 + a_k) * nj);
-  };
-
-  const int lane = tid & 31, warp = tid >> 5;
-  // 4M: cre, cim; 3M: cre = Ar Br, cim = Ai Bi, c3 = (Ar + Ai)(Br + Bi) (see zgemm_dmma_kernel)
-  double cre[RB][CB][2], cim[RB][CB][2], c3[M3 ? RB : 1][M3 ? CB : 1][2];
-#pragma unroll
-  for (int r = 0; r < RB; ++r)
-#pragma unroll
-    for (int q = 0; q < CB; ++q) {
-      cre[r][q][0] = cre[r][q][1] = cim[r][q][0] = cim[r][q][1] = 0.0;
-      if constexpr (M3) c3[r][q][0] = c3[r][q][1] = 0.0;
-    }
-
-  const int nk = (ke - kb) / BK;  // host guarantees BK | (ke - kb)
-#pragma unroll
-  for (int st = 0; st < ST - 1; ++st) {
-    if (st < nk) load_stage(st, kb + st * BK);
-    cp_commit_bs();
-  }
-  const int cbase = warp * CB * 8 + (lane >> 2);
-  const int arow = lane >> 2, kq = lane & 3;
-  for (int kt = 0; kt < nk; ++kt) {
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(ST - 2));
-    __syncthreads();
-    if (kt + ST - 1 < nk) load_stage((kt + ST - 1) % ST, kb + (kt + ST - 1) * BK);
-    cp_commit_bs();
-    const double2* cA = sA + (kt % ST) * BJ * ALD;
-    const double2* cB = sB + (kt % ST) * BK * LDB;
-#pragma unroll
-    for (int kk = 0; kk < BK; kk += 4) {
-      double ar[RB], ai[RB], an[RB], br[CB], bi[CB];
-#pragma unroll
-      for (int r = 0; r < RB; ++r) {
-        const double2 a = cA[(r * 8 + arow) * ALD + kk + kq];
-        ar[r] = a.x;
-        ai[r] = a.y;
-        an[r] = M3 ? a.x + a.y : -a.y;
-      }
-#pragma unroll
-      for (int q = 0; q < CB; ++q) {
-        const int c = cbase + q * 8;
-        const double2 b = kfast ? cB[c * BK + ((kk + kq) ^ (BK >= 8 ? (c & 1) << 2 : 0))] : cB[(kk + kq) * LDB + c];
-        br[q] = b.x;
-        bi[q] = b.y;
-      }
-      if constexpr (M3) {
-        double bs[CB];
-#pragma unroll
-        for (int q = 0; q < CB; ++q) bs[q] = br[q] + bi[q];
-#pragma unroll
-        for (int r = 0; r < RB; ++r)
-#pragma unroll
-          for (int q = 0; q < CB; ++q) {
-            dmma_bs(cre[r][q][0], cre[r][q][1], ar[r], br[q]);
-            dmma_bs(cim[r][q][0], cim[r][q][1], ai[r], bi[q]);
-            dmma_bs(c3[r][q][0], c3[r][q][1], an[r], bs[q]);
-          }
-      } else {
-#pragma unroll
-        for (int r = 0; r < RB; ++r)
-#pragma unroll
-          for (int q = 0; q < CB; ++q) {
-            dmma_bs(cre[r][q][0], cre[r][q][1], ar[r], br[q]);
-            dmma_bs(cim[r][q][0], cim[r][q][1], ar[r], bi[q]);
-            dmma_bs(cre[r][q][0], cre[r][q][1], an[r], bi[q]);
-            dmma_bs(cim[r][q][0], cim[r][q][1], ai[r], br[q]);
-          }
-      }
-    }
-  }
-  cp_wait0_bs();
-  const int bsj = g.bstride[j];
-#pragma unroll
-  for (int r = 0; r < RB; ++r)
-#pragma unroll
-    for (int q = 0; q < CB; ++q) {
-      const int row = r * 8 + (lane >> 2);
-      const int c = warp * CB * 8 + q * 8 + 2 * kq;
-      if constexpr (M3) {
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-          out[row * bsj + coll[c + h]] =
-              make_double2(cre[r][q][h] - cim[r][q][h], c3[r][q][h] - cre[r][q][h] - cim[r][q][h]);
-      } else {
-        out[row * bsj + coll[c]] = make_double2(cre[r][q][0], cim[r][q][0]);
-        out[row * bsj + coll[c + 1]] = make_double2(cre[r][q][1], cim[r][q][1]);
-      }
-    }
-}
-
-template <int RB, int CB, bool M3, int KM, int ST, int H>
-__global__ void __launch_bounds__(kUpdThreads, (M3 && H == 1) ? 1 : 2)
-    tile_update_kernel(const TileGeom g, const double2* __restrict__ T, const int64_t* __restrict__ tiles,
-                       const int4* __restrict__ items, double2* __restrict__ partial, const double2* __restrict__ Y) {
-  extern __shared__ __align__(16) double2 sm[];
-  update_body<RB, CB, M3, KM, ST, H>(g, T, tiles, items[blockIdx.x / H], (int)(blockIdx.x % H),
-                                     partial + (int64_t)(blockIdx.x / H) * 4096, Y, sm);
 }
 
 // Grouped far update (SolvePlan::fgroup = G > 1). One item covers up to G target tiles that are
@@ -399,249 +201,6 @@ __global__ void __launch_bounds__(kUpdThreads, 2)
   far_group_body<BT, G, CB, M3, KM, ST, H>(g, T, tiles, items[blockIdx.x / H], (int)(blockIdx.x % H), ring, Y, sm);
 }
 
-// n terms tp[i grp] * sp[i ss], i < n, into four independent accumulators (loads batched).
-__device__ __forceinline__ void dot_run(const double2* tp, const double2* sp, int n, int grp, int ss,
-                                        double2 (&acc)[4]) {
-  int i = 0;
-  for (; i + 4 <= n; i += 4) {
-    const double2 t0 = tp[0], t1 = tp[grp], t2 = tp[2 * grp], t3 = tp[3 * grp];
-    const double2 s0 = sp[0], s1 = sp[ss], s2 = sp[2 * ss], s3 = sp[3 * ss];
-    acc[0] = cfma(acc[0], t0, s0);
-    acc[1] = cfma(acc[1], t1, s1);
-    acc[2] = cfma(acc[2], t2, s2);
-    acc[3] = cfma(acc[3], t3, s3);
-    tp += 4 * grp;
-    sp += 4 * ss;
-  }
-  for (; i < n; ++i) {
-    acc[0] = cfma(acc[0], tp[0], sp[0]);
-    tp += grp;
-    sp += ss;
-  }
-}
-
-// Padded local strides of the diagonal tile in shared memory, chosen so that the entries of a
-// local hyperplane (sorted by leading coordinates) fall into distinct 16-byte bank groups:
-// N=3, B=16: (1, 17, 274) -> address mod 8 = l1 + l2 + 2 l3; N=4, B=8: (1, 9, 74, 595).
-template <int N, int B>
-struct PadStrides {
-  static constexpr int s1 = B + 1;
-  static constexpr int s2 = N >= 3 ? s1 * B + 2 : 0;
-  static constexpr int s3 = N >= 4 ? s2 * B + 3 : 0;
-  __device__ static constexpr int at(int m) { return m == 0 ? 1 : m == 1 ? s1 : m == 2 ? s2 : s3; }
-  static constexpr int extent = 1 + (B - 1) * (1 + s1 + s2 + s3);
-  __device__ static int pad(int l) {
-    int a = 0;
-#pragma unroll
-    for (int m = 0; m < N; ++m) a += ((l >> ((B == 16 ? 4 : 3) * m)) & (B - 1)) * at(m);
-    return a;
-  }
-};
-
-
-// Diagonal tile (cubic, B^N = 4096 entries): S = C_I - sum(partials) (fixed order ->
-// deterministic), then the local anti-diagonal wavefront over sum_j l_j = t, highest first.
-// Hyperplane step lv (t = N (B - 1) - lv) is described by a host-built table: lvl[lv] =
-// lanes-per-entry grp | (busy warps << 8), and thr[lv][tid] = the local entry this thread works
-// on (0xffff: none); entries of a hyperplane are sorted by leading coordinates so lanes share
-// loop trip counts. An entry's grp lanes split its sum_j sum_{k > l_j} T_j(i_j, k) y(...) terms,
-// combine them with warp shuffles, and the leader scales by 1 / sum_j T_j(i_j, i_j). S uses
-// padded strides (PadStrides) so a hyperplane's entries sit in distinct shared-memory banks.
-template <int N, int B, int NT>
-__global__ void __launch_bounds__(NT, 2)
-    tile_diag_kernel(const TileGeom g, const double2* __restrict__ T, const int64_t* __restrict__ tiles,
-                     const int4* __restrict__ tile_ranges, const double2* __restrict__ far_partial,
-                     const double2* __restrict__ near_partial, const uint16_t* __restrict__ thr_g,
-                     const int* __restrict__ lvl_g, int wf_levels, double2* __restrict__ Y) {
-  constexpr int E = 4096;
-  constexpr int LB = B == 16 ? 4 : 3;
-  constexpr int WL = N * (B - 1) + 1;  // hyperplanes in a tile
-  static_assert((1 << (LB * N)) == E, "cubic 4096-entry tile");
-  using PS = PadStrides<N, B>;
-  extern __shared__ __align__(16) double2 sm[];
-  __shared__ int64_t so[N];
-  __shared__ int64_t st[N];
-  __shared__ int lvl[WL];
-  const int tid = threadIdx.x;
-  if (tid == 0) {
-    int64_t t = tiles[blockIdx.x];
-    for (int m = 0; m < N; ++m) {
-      const int64_t I = t % g.nb[m];
-      t /= g.nb[m];
-      so[m] = I * B;
-      st[m] = g.strides[m];
-    }
-  }
-  double2* S = sm;
-  double2* Td = S + PS::extent + (PS::extent & 1);  // [N][B][B] row-major: T_m(o_m + row, o_m + col)
-  uint16_t* thr = (uint16_t*)(Td + N * B * B);      // [WL][NT]
-  {
-    const uint4* src = (const uint4*)thr_g;
-    uint4* dst = (uint4*)thr;
-    for (int i = tid; i < WL * NT / 8; i += NT) dst[i] = src[i];
-  }
-  for (int i = tid; i < WL; i += NT) lvl[i] = lvl_g[i];
-  __syncthreads();
-#pragma unroll
-  for (int m = 0; m < N; ++m) {
-    const double2* Tm = T + g.toff[m];
-    const int64_t nm = g.dims[m];
-    for (int e = tid; e < B * B; e += NT) {
-      const int r = e / B, c = e % B;
-      Td[(m * B + r) * B + c] = Tm[(so[m] + r) + (so[m] + c) * nm];
-    }
-  }
-  const int4 tr = tile_ranges[blockIdx.x];  // {far first, far count, near first, near count}
-  {
-    constexpr int PER = E / NT;  // entries per thread, loads issued together
-    double2 v[PER];
-#pragma unroll
-    for (int i = 0; i < PER; ++i) {
-      const int l = tid + i * NT;
-      int64_t gidx = 0;
-#pragma unroll
-      for (int m = 0; m < N; ++m) gidx += (so[m] + ((l >> (LB * m)) & (B - 1))) * st[m];
-      v[i] = Y[gidx];
-    }
-    for (int p = 0; p < tr.y; ++p) {
-      const double2* pp = far_partial + (int64_t)(tr.x + p) * E + tid;
-#pragma unroll
-      for (int i = 0; i < PER; ++i) v[i] = csub(v[i], pp[i * NT]);
-    }
-    for (int p = 0; p < tr.w; ++p) {
-      const double2* pp = near_partial + (int64_t)(tr.z + p) * E + tid;
-#pragma unroll
-      for (int i = 0; i < PER; ++i) v[i] = csub(v[i], pp[i * NT]);
-    }
-#pragma unroll
-    for (int i = 0; i < PER; ++i) S[PS::pad(tid + i * NT)] = v[i];
-  }
-  __syncthreads();
-
-  const int warp = tid >> 5;
-#ifdef NDS_DIAG_CLOCK
-  if (tid == 0 && blockIdx.x == 0) nds_diag_clock_start = clock64();
-#endif
-#pragma unroll 1
-  for (int lv = 0; lv < wf_levels; ++lv) {
-    const int info = lvl[lv];
-    if (warp < (info >> 8)) {  // warp-uniform: this warp holds entries on hyperplane lv
-      const int grp = info & 0xff;
-      const int lraw = thr[lv * NT + tid];
-      NDS_PROBE(0, lraw);
-      const bool act = lraw != 0xffff;
-      const int l = act ? lraw : 0;
-      const int sub = tid & (grp - 1);
-      int lm[N];
-      int pl = 0;
-#pragma unroll
-      for (int m = 0; m < N; ++m) {
-        lm[m] = (l >> (LB * m)) & (B - 1);
-        pl += lm[m] * PS::at(m);
-      }
-      // denominator first: independent of S, its latency hides under the dot products
-      double2 den = make_double2(0.0, 0.0);
-#pragma unroll
-      for (int m = 0; m < N; ++m) den = cadd(den, Td[m * B * B + lm[m] * (B + 1)]);
-      const double2 rden = crecip_fast(den);  // issued before the dot products, off their chain
-      NDS_PROBE(1, rden.x);
-      double2 a0 = make_double2(0.0, 0.0), a1 = make_double2(0.0, 0.0);
-      double2 a2 = make_double2(0.0, 0.0), a3 = make_double2(0.0, 0.0);
-      // Flattened term loop: every entry of hyperplane lv has exactly lv terms (cubic tile), so
-      // the trip count is warp-uniform; term t maps to mode m (t >= qc[m]) and position k = t -
-      // qc[m] along it. Offsets are affine in t within a mode: S: sb[m] + t a_m, T: tb[m] + t.
-#if !defined(NDS_DIAG_FLAT) && !defined(NDS_DIAG_NODOT)
-      if (act) {
-#pragma unroll
-        for (int m = 0; m < N; ++m) {
-          const double2* tp = Td + m * B * B + lm[m] * (B + 1) + 1 + sub;
-          const double2* sp = S + pl + (1 + sub) * PS::at(m);
-          const int ss = grp * PS::at(m);
-          int q = B - 1 - lm[m] - sub;  // this lane's terms: ceil(q / grp)
-#pragma unroll 1
-          for (; q > 3 * grp; q -= 4 * grp) {  // 4 terms in flight
-            const double2 t0 = tp[0], t1 = tp[grp], t2 = tp[2 * grp], t3 = tp[3 * grp];
-            const double2 s0 = sp[0], s1 = sp[ss], s2 = sp[2 * ss], s3 = sp[3 * ss];
-            a0 = cfma(a0, t0, s0);
-            a1 = cfma(a1, t1, s1);
-            a2 = cfma(a2, t2, s2);
-            a3 = cfma(a3, t3, s3);
-            tp += 4 * grp;
-            sp += 4 * ss;
-          }
-          if (q > grp) {
-            const double2 t0 = tp[0], t1 = tp[grp], s0 = sp[0], s1 = sp[ss];
-            a0 = cfma(a0, t0, s0);
-            a1 = cfma(a1, t1, s1);
-            tp += 2 * grp;
-            sp += 2 * ss;
-            q -= 2 * grp;
-          }
-          if (q > 0) a2 = cfma(a2, tp[0], sp[0]);
-        }
-      }
-#elif !defined(NDS_DIAG_NODOT)
-      if (act) {
-        int qc[N], sb[N], tb[N];
-        int q = 0;
-#pragma unroll
-        for (int m = 0; m < N; ++m) {
-          qc[m] = q;
-          sb[m] = pl + (1 - q) * PS::at(m);
-          tb[m] = m * B * B + lm[m] * (B + 1) + 1 - q;
-          q += B - 1 - lm[m];
-        }
-        auto term = [&](int t, double2& a) {
-          int so = sb[0], sa = PS::at(0), to = tb[0];
-#pragma unroll
-          for (int m = 1; m < N; ++m)
-            if (t >= qc[m]) {
-              so = sb[m];
-              sa = PS::at(m);
-              to = tb[m];
-            }
-          a = cfma(a, Td[to + t], S[so + t * sa]);
-        };
-        int t = sub;
-#pragma unroll 1
-        for (; t + 3 * grp < lv; t += 4 * grp) {
-          term(t, a0);
-          term(t + grp, a1);
-          term(t + 2 * grp, a2);
-          term(t + 3 * grp, a3);
-        }
-        if (t < lv) term(t, a0);
-        if (t + grp < lv) term(t + grp, a1);
-        if (t + 2 * grp < lv) term(t + 2 * grp, a2);
-      }
-#endif
-      double2 acc = cadd(cadd(a0, a1), cadd(a2, a3));
-      NDS_PROBE(2, acc.x);
-      for (int o = 1; o < grp; o <<= 1) {
-        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
-        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
-      }
-      if (act && sub == 0) S[pl] = cmul(csub(S[pl], acc), rden);
-      NDS_PROBE(3, S[pl].x);
-    }
-    __syncthreads();
-#ifdef NDS_DIAG_CLOCK
-    if (tid == 0 && blockIdx.x == 0) nds_diag_clock[lv] = clock64();
-#endif
-  }
-  {
-    constexpr int PER = E / NT;
-#pragma unroll
-    for (int i = 0; i < PER; ++i) {
-      const int l = tid + i * NT;
-      int64_t gidx = 0;
-#pragma unroll
-      for (int m = 0; m < N; ++m) gidx += (so[m] + ((l >> (LB * m)) & (B - 1))) * st[m];
-      Y[gidx] = S[PS::pad(l)];
-    }
-  }
-}
-
 // Padded shared-memory strides of the line-owner kernel: thread t owns the mode-1 line
 // (l_2, l_3, ...) = digits of t, so a warp's lanes differ in l_2 (fastest) and a hyperplane puts
 // them at l_1 = s - l_2 - ...; a_2 - 1 odd spreads those lanes over all eight 16-byte bank groups.
@@ -704,12 +263,14 @@ __constant__ LineOrder<4, 8> kLineOrder4 = make_line_order<4, 8>();
 //   near_out[item] (l_m, c) = sum_k T_m(o_m - B + l_m, o_m + k) Y_J(k along m, c)
 // (3M DMMA; near_target[slot N + m] = that item's index at the next level, -1 if none) — which
 // replaces the separate near-update launch on the critical path.
-// VAR bits: 4 = PRO (factor loads issued together with the tile's loads). Measured and removed
+// The factor loads go to registers and are stored to shared memory after the tile's own loads are
+// in flight (one exposed latency instead of two; 2 % per tile). Measured and removed
 // (tools/microbench/lines_bench.cu): a split-phase (mbarrier) step barrier
 // with the next row's distance >= 2 terms pre-accumulated in between, a warp-uniform bound on
-// the history update, unrolling the PUSH modes, and a two-warps-per-32-lines form (512 threads,
-// 128 registers; wavefront 58 K -> 87 K cycles).
-template <int N, int B, int NT, bool PUSH, bool T2REG, bool SORT = true, int VAR = 0>
+// the history update, unrolling the PUSH modes, T_2 read from shared memory (128 registers, two
+// CTAs per SM, each 2.2x slower), natural line order, and a two-warps-per-32-lines form (512
+// threads, 128 registers; wavefront 58 K -> 87 K cycles).
+template <int N, int B, int NT>
 __device__ __forceinline__ void diag_lines_body(const TileGeom& g, const double2* __restrict__ T, const int64_t tile,
                                                 const int4 tr, const double2* __restrict__ far_partial,
                                                 const double2* __restrict__ near_partial,
@@ -722,7 +283,7 @@ __device__ __forceinline__ void diag_lines_body(const TileGeom& g, const double2
   using PS = LinePad<N, B>;
   __shared__ int64_t so[N];
   __shared__ int64_t st[N];
-  constexpr bool PRO = (VAR & 4) != 0;
+  constexpr bool PUSH = true, T2REG = true, SORT = true;
   const int tid = threadIdx.x;
   NDS_LPROBE(0);
   int tgt_m[N];  // near-coupling targets of the PUSH phase, loaded before the long wavefront
@@ -743,13 +304,11 @@ __device__ __forceinline__ void diag_lines_body(const TileGeom& g, const double2
   constexpr int ALD = B + 4;                        // = 4 mod 8: conflict-free DMMA A fragments
   double2* Ap = Dq + B * B;                         // [N][B][ALD]: T_m(o_m - B + r, o_m + k) (PUSH)
   __syncthreads();
-  // PRO: the factor loads go to registers first and are stored to shared memory only after the
-  // tile's own loads are in flight (one exposed latency instead of two)
-  static_assert(!PRO || B * B <= NT, "PRO: one factor entry per thread");
+  static_assert(B * B <= NT, "one factor entry per thread");
   double2 tdv[N], apv[N], dqv = make_double2(0.0, 0.0);
   const bool tl = tid < B * B;
-  if constexpr (PRO) {
-    const int r = tid % B, c = tid / B;
+  {
+    const int r = tid % B, c = tid / B;  // rows fastest: coalesced along T_m's columns
 #pragma unroll
     for (int m = 0; m < N; ++m) {
       const double2* Tm = T + g.toff[m];
@@ -760,22 +319,6 @@ __device__ __forceinline__ void diag_lines_body(const TileGeom& g, const double2
       if (m == 0) {
         const int j = tid / B, rr = tid % B;
         dqv = tl && rr >= j + 1 ? Tm[(so[0] + rr - 1 - j) + (so[0] + rr) * nm] : make_double2(0.0, 0.0);
-      }
-    }
-  } else {
-#pragma unroll
-    for (int m = 0; m < N; ++m) {
-      const double2* Tm = T + g.toff[m];
-      const int64_t nm = g.dims[m];
-      const bool push_m = PUSH && so[m] >= B;
-      for (int e = tid; e < B * B; e += NT) {
-        const int r = e % B, c = e / B;  // rows fastest: coalesced along T_m's columns
-        Td[(m * B + r) * B + c] = Tm[(so[m] + r) + (so[m] + c) * nm];
-        if (push_m) Ap[(m * B + r) * ALD + c] = Tm[(so[m] - B + r) + (so[m] + c) * nm];
-        if (m == 0) {  // e = j B + r'
-          const int j = e / B, rr = e % B;
-          Dq[e] = rr >= j + 1 ? Tm[(so[0] + rr - 1 - j) + (so[0] + rr) * nm] : make_double2(0.0, 0.0);
-        }
       }
     }
   }
@@ -803,7 +346,7 @@ __device__ __forceinline__ void diag_lines_body(const TileGeom& g, const double2
       for (int m = 0; m < N; ++m) gidx += (so[m] + ((l >> (LB * m)) & (B - 1))) * st[m];
       v[i] = Y[gidx];
     }
-    if constexpr (PRO) store_factors();
+    store_factors();
     const int np = tr.y + tr.w;
     auto part = [&](int p) {
       return p < tr.y ? far_partial + (int64_t)(tr.x + p) * E + tid : near_partial + (int64_t)(tr.z + p - tr.y) * E + tid;
@@ -975,146 +518,51 @@ __device__ __forceinline__ void diag_lines_body(const TileGeom& g, const double2
   NDS_LPROBE(5);
 }
 
-template <int N, int B, int NT, bool PUSH, bool T2REG, bool SORT = true, int VAR = 0>
-__global__ void __launch_bounds__(NT, T2REG ? 1 : 2)
+template <int N, int B, int NT>
+__global__ void __launch_bounds__(NT, 1)
     tile_diag_lines_kernel(const TileGeom g, const double2* __restrict__ T, const int64_t* __restrict__ tiles,
                            const int4* __restrict__ tile_ranges, const double2* __restrict__ far_partial,
                            const double2* __restrict__ near_partial, const int* __restrict__ near_target,
                            double2* __restrict__ near_out, double2* __restrict__ Y) {
   extern __shared__ __align__(16) double2 sm[];
-  diag_lines_body<N, B, NT, PUSH, T2REG, SORT, VAR>(g, T, tiles[blockIdx.x], tile_ranges[blockIdx.x], far_partial, near_partial,
+  diag_lines_body<N, B, NT>(g, T, tiles[blockIdx.x], tile_ranges[blockIdx.x], far_partial, near_partial,
                                          near_target ? near_target + (int64_t)blockIdx.x * N : nullptr, near_out, Y,
                                          sm);
 }
 
 using LinesKernel = void (*)(const TileGeom, const double2*, const int64_t*, const int4*, const double2*,
                              const double2*, const int*, double2*, double2*);
-static LinesKernel lines_kernel_for(int n_modes, int b, bool push) {
-  static const bool t2smem = getenv("NDS_DIAG_T2SMEM") != nullptr;  // A/B experiments
-  static const bool natural = getenv("NDS_DIAG_NATURAL") != nullptr;
-  // VAR 4 (PRO: factor loads overlapped with the tile's loads) measured 2 % faster per tile
-  if (n_modes == 3 && b == 16) {
-    if (natural)
-      return push ? tile_diag_lines_kernel<3, 16, 256, true, true, false> : tile_diag_lines_kernel<3, 16, 256, false, true, false>;
-    if (t2smem) return push ? tile_diag_lines_kernel<3, 16, 256, true, false> : tile_diag_lines_kernel<3, 16, 256, false, false>;
-    return push ? tile_diag_lines_kernel<3, 16, 256, true, true, true, 4> : tile_diag_lines_kernel<3, 16, 256, false, true, true, 4>;
-  }
-  if (n_modes == 4 && b == 8 && natural)
-    return push ? tile_diag_lines_kernel<4, 8, 512, true, true, false> : tile_diag_lines_kernel<4, 8, 512, false, true, false>;
-  if (n_modes == 4 && b == 8)
-    return push ? tile_diag_lines_kernel<4, 8, 512, true, true, true, 4> : tile_diag_lines_kernel<4, 8, 512, false, true, true, 4>;
+static LinesKernel lines_kernel_for(int n_modes, int b) {
+  if (n_modes == 3 && b == 16) return tile_diag_lines_kernel<3, 16, 256>;
+  if (n_modes == 4 && b == 8) return tile_diag_lines_kernel<4, 8, 512>;
   return nullptr;
 }
 static size_t lines_smem_bytes(int n_modes, int b) {
   const int ext = n_modes == 3 ? LinePad<3, 16>::extent : LinePad<4, 8>::extent;
   return (size_t)(ext + (ext & 1)) * 16 + (size_t)(n_modes + 1) * b * b * 16 + (size_t)n_modes * b * (b + 4) * 16;
 }
-
-using UpdateKernel = void (*)(const TileGeom, const double2*, const int64_t*, const int4*, double2*, const double2*);
-using DiagKernel = void (*)(const TileGeom, const double2*, const int64_t*, const int4*, const double2*,
-                            const double2*, const uint16_t*, const int*, int, double2*);
-
-// Update-kernel configurations (measured). b = 16: 3M, BK = 8, 3 stages, two CTAs per item
-// (128 columns each, 2 CTAs / SM): c1 solve 4.94 -> 4.36 ms vs one 256-column CTA (1 / SM).
-// b = 8: 4M, BK = 4, 3 stages, one CTA per item (2 / SM). NDS_UPD=3m|4m|k16|s4|h1|h2|h4 override
-// for A/B experiments.
-struct UpdCfg {
-  UpdateKernel kern;
-  int bk, stages, h;
-};
-static int update_override() {
-  static const int v = [] {
-    const char* e = getenv("NDS_UPD");
-    if (!e) return -1;
-    const std::string s(e);
-    return s == "3m" ? 1 : s == "4m" ? 0 : s == "k16" ? 2 : s == "s4" ? 3 : s == "h2" ? 4 : s == "h1" ? 5
-         : s == "h4" ? 6 : s == "h2s4" ? 7 : s == "h2s5" ? 8 : s == "h2k16s2" ? 9 : s == "h4k16" ? 10 : -1;
-  }();
-  return v;
-}
-static UpdCfg update_cfg_for(int b) {
-  const int o = update_override();
-  if (b == 8) {
-    if (o == 1) return {tile_update_kernel<1, 8, true, 1, 3, 1>, 4, 3, 1};
-    if (o == 4) return {tile_update_kernel<1, 4, true, 1, 3, 2>, 4, 3, 2};
-    if (o == 6) return {tile_update_kernel<1, 2, true, 1, 3, 4>, 4, 3, 4};
-    if (o == 7) return {tile_update_kernel<1, 8, false, 1, 4, 1>, 4, 4, 1};
-    if (o == 8) return {tile_update_kernel<1, 8, false, 1, 5, 1>, 4, 5, 1};
-    return {tile_update_kernel<1, 8, false, 1, 3, 1>, 4, 3, 1};
-  }
-  if (b == 16) {
-    if (o == 0) return {tile_update_kernel<2, 4, false, 1, 3, 1>, 8, 3, 1};
-    if (o == 2) return {tile_update_kernel<2, 4, true, 2, 3, 1>, 16, 3, 1};
-    if (o == 3) return {tile_update_kernel<2, 4, true, 1, 4, 1>, 8, 4, 1};
-    if (o == 5) return {tile_update_kernel<2, 4, true, 1, 3, 1>, 8, 3, 1};
-    if (o == 6) return {tile_update_kernel<2, 1, true, 1, 3, 4>, 8, 3, 4};
-    if (o == 7) return {tile_update_kernel<2, 2, true, 1, 4, 2>, 8, 4, 2};
-    if (o == 8) return {tile_update_kernel<2, 2, true, 1, 5, 2>, 8, 5, 2};
-    if (o == 9) return {tile_update_kernel<2, 2, true, 2, 2, 2>, 16, 2, 2};
-    if (o == 10) return {tile_update_kernel<2, 1, true, 2, 3, 4>, 16, 3, 4};
-    return {tile_update_kernel<2, 2, true, 1, 3, 2>, 8, 3, 2};
-  }
-  return {nullptr, 0, 0, 0};
-}
-static UpdateKernel update_kernel_for(int b) { return update_cfg_for(b).kern; }
-
-// Threads per diagonal-tile CTA: at least the widest local hyperplane (192 for 16^3, 480 for 8^4).
+// Threads per diagonal-tile CTA: one per mode-1 line (256 for 16^3, 512 for 8^4).
 static int diag_threads_for(int n_modes) { return n_modes == 3 ? 256 : 512; }
 
-static DiagKernel diag_kernel_for(int n_modes, int b) {
-  if (n_modes == 3 && b == 16) return tile_diag_kernel<3, 16, 256>;
-  if (n_modes == 4 && b == 8) return tile_diag_kernel<4, 8, 512>;
-  return nullptr;
-}
-static int update_bk(int b) { return update_cfg_for(b).bk; }
-static int update_h(int b) { return update_cfg_for(b).h; }
-
-static size_t update_smem_bytes(int b) {
-  const UpdCfg c = update_cfg_for(b);
-  const int cols = 4096 / b / c.h, ald = c.bk <= 8 ? 12 : c.bk + 4;
-  return (size_t)cols * (8 + 4) + (size_t)c.stages * b * ald * 16 + (size_t)c.stages * c.bk * (cols + 2) * 16;
-}
-
-static size_t diag_smem_bytes(int n_modes, int b, int wf_levels) {
-  const int ext = n_modes == 3 ? PadStrides<3, 16>::extent : PadStrides<4, 8>::extent;
-  return (size_t)(ext + (ext & 1)) * 16 + (size_t)n_modes * b * b * 16 +
-         (size_t)wf_levels * diag_threads_for(n_modes) * sizeof(uint16_t);
-}
-
-// Far-update configurations (measured, c1/c2/c3 solve): G = 1 — one item per (target, mode), as
-// the plain items, but with explicit ring slots so each level's items run longest first (LPT:
-// c1 solve 4.82 -> 4.6 ms); 3M, 4-stage cp.async ring, two CTAs per item (b = 16: 128 columns,
-// BK = 8; b = 8: 256 columns, BK = 4). Groups of G = 2/4 targets per item (32 rows, half the slab
-// traffic per flop) measured slower: the far kernel is not traffic-bound (DMMA pipe ~57 % busy,
-// latency/barrier stalls), and the remainder items add partial read-modify-writes.
-// NDS_FARGROUP=plain restores the plain per-target items, =2|4 selects G. Also measured for G = 1
-// and rejected: BK = 16 (1 CTA/SM by shared memory), one or four column CTAs per item, 4M.
+// Far-update configurations (measured, c1/c2/c3 solve): one item per
+// (target, mode) with an explicit ring slot so each level's items run longest first (LPT: c1
+// solve 4.82 -> 4.6 ms); 3M, 4-stage cp.async ring, two CTAs per item (b = 16: 128 columns,
+// BK = 8; b = 8: 256 columns, BK = 4). Measured and removed: groups of G = 2 / 4 targets per
+// slab read (slower on every config: the kernel is latency/barrier-bound, not traffic-bound, and
+// remainder items add partial read-modify-writes), k-split items, BK = 16, one or four column
+// CTAs per item, 4M.
 struct FarGroupCfg {
   FarGroupKernel kern;
   int g, bk, stages, h;
 };
 static FarGroupCfg far_group_cfg(int b) {
-  static const std::string env = getenv("NDS_FARGROUP") ? getenv("NDS_FARGROUP") : "";
-  if (env == "plain") return {nullptr, 0, 0, 0, 0};
-  const int gsel = env.empty() ? 0 : atoi(env.c_str());
-  if (b == 16) {
-    if (gsel == 2) return {far_group_kernel<16, 2, 2, true, 1, 3, 2>, 2, 8, 3, 2};
-    return {far_group_kernel<16, 1, 2, true, 1, 4, 2>, 1, 8, 4, 2};
-  }
-  if (b == 8) {
-    if (gsel == 2) return {far_group_kernel<8, 2, 2, true, 2, 3, 4>, 2, 8, 3, 4};
-    if (gsel == 4) return {far_group_kernel<8, 4, 2, true, 2, 3, 4>, 4, 8, 3, 4};
-    return {far_group_kernel<8, 1, 4, true, 1, 4, 2>, 1, 4, 4, 2};
-  }
+  if (b == 16) return {far_group_kernel<16, 1, 2, true, 1, 4, 2>, 1, 8, 4, 2};
+  if (b == 8) return {far_group_kernel<8, 1, 4, true, 1, 4, 2>, 1, 4, 4, 2};
   return {nullptr, 0, 0, 0, 0};
 }
-// 0: plain per-target items (tile_update_kernel, slot = item index); G >= 1: FarGroupItem lists
-static int far_group_for(int b) { return far_group_cfg(b).g; }
-static int far_group_bk(int b) { return std::max(1, far_group_cfg(b).bk); }
 static size_t far_group_smem_bytes(int b) {
   const FarGroupCfg c = far_group_cfg(b);
   if (c.g < 1) return 0;
   const int cols = 4096 / b / c.h, ald = c.bk <= 8 ? 12 : c.bk + 4;
   return (size_t)cols * (8 + 4) + (size_t)c.stages * c.g * b * ald * 16 + (size_t)c.stages * c.bk * (cols + 2) * 16;
 }
-

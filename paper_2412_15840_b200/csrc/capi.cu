@@ -39,6 +39,7 @@ struct nds_ctx {
   cudaStream_t tail = nullptr;   // tail overlap: first inverse pass per completed mode-N slab
   cudaEvent_t tev[65] = {};
   std::map<std::vector<int64_t>, std::shared_ptr<nds::SolverCache>> solvers;  // by extents
+  cudaMemPool_t pool = nullptr;  // private stream-ordered pool (factor sets, small matrices)
 };
 
 struct nds_plan {
@@ -61,14 +62,6 @@ struct nds_plan {
   std::vector<cudaEvent_t> pev;
   std::vector<int> pkind, pmode;
   nds::Recorder rec;
-  // nds_plan_execute replays a CUDA graph of the whole step (transforms + level-synchronous
-  // solve on the plan's fork/join streams) for repeated calls on the same device buffers
-  cudaGraphExec_t gexec = nullptr;
-  const void* gb = nullptr;
-  void* gx = nullptr;
-  void* gw = nullptr;
-  cudaStream_t gstream = nullptr;
-  int glaunches = 0, gcalls = 0;
 };
 
 namespace {
@@ -169,7 +162,8 @@ void upload_factors(nds_ctx* ctx, nds::FactorSet& f, int n_modes, const int64_t*
     NDS_CUDA(cudaHostAlloc(&ctx->stage, stage_bytes, cudaHostAllocDefault));
     ctx->stage_bytes = stage_bytes;
   }
-  NDS_CUDA(cudaMallocAsync(&f.pool, (size_t)(n_u + n_t + n_d + n_raw + 1) * sizeof(double2), ctx->stream));
+  NDS_CUDA(cudaMallocFromPoolAsync(&f.pool, (size_t)(n_u + n_t + n_d + n_raw + 1) * sizeof(double2), ctx->pool,
+                                   ctx->stream));
   f.stream = ctx->stream;
   double2* stage = (double2*)ctx->stage;
   nds::Geom& g = f.geom;
@@ -397,14 +391,12 @@ int execute(nds_plan* p, const double2* b, double2* x, double2* work, cudaEvent_
   if (rec) rec->mark(s, -1, 0);
   // Head overlap (cubic-tile solve, last pass a row-major GEMM): the last forward pass runs on a
   // side stream in row groups of mode-N tile blocks, highest first, while the solve's first levels
-  // (which need only the highest blocks) start; NDS_HEAD=0 disables. N = 3 only: there a group
+  // (which need only the highest blocks) start. N = 3 only: there a group
   // of two blocks (1/8 of the pass for c1) takes about as long as the two nearly empty levels
   // that wait for it (c1: -0.27 ms); with N = 4 the hyperplanes fill within a few levels and the
   // groups fall behind (c2: +2.2 ms), so it stays off.
   const ModeView lastv = nds::mode_view(p->n_modes, p->dims, passes.back().mode);
-  static const bool head_env = !(getenv("NDS_HEAD") && std::string(getenv("NDS_HEAD")) == "0");
-  const bool head = head_env && !p->fast_path && p->solver && !p->solver->binary && p->solver->sp.v2 &&
-                    !nds::backsub_is_dataflow(p->solver->sp) &&
+  const bool head = !p->fast_path && p->solver && !p->solver->binary && p->solver->sp.v2 &&
                     p->n_modes == 3 && passes.back().group < 0 && passes.back().mode == p->n_modes &&
                     lastv.outer == 1 && nds::gemm_rowm_ok(lastv);
   const int last_fwd = head ? N - 1 : N;
@@ -413,10 +405,9 @@ int execute(nds_plan* p, const double2* b, double2* x, double2* work, cudaEvent_
   // mode-N index in tile block k are all final once tile (0, .., 0, k) is solved (level L-1-k).
   // So the first inverse pass runs per mode-N block on a low-priority stream as soon as its level
   // completes (highest block first) — no accumulation, each piece writes its own slab — and only
-  // the last block's piece remains after the solve. NDS_TAIL=0 disables.
-  static const bool tail_env = !(getenv("NDS_TAIL") && std::string(getenv("NDS_TAIL")) == "0");
-  const bool tail = tail_env && !p->fast_path && p->solver && !p->solver->binary && p->solver->sp.v2 &&
-                    !nds::backsub_is_dataflow(p->solver->sp) && passes.front().group < 0 &&
+  // the last block's piece remains after the solve.
+  const bool tail = !p->fast_path && p->solver && !p->solver->binary && p->solver->sp.v2 &&
+                    passes.front().group < 0 &&
                     passes.front().mode == 1 && p->n_modes >= 2 && p->solver->sp.geom.nb[p->n_modes - 1] <= 64;
   struct TailState {
     nds_plan* p;
@@ -441,8 +432,7 @@ int execute(nds_plan* p, const double2* b, double2* x, double2* work, cudaEvent_
     tail_hook.fn = [](void* vctx, int lv, cudaStream_t crit) {
       TailState& t = *(TailState*)vctx;
       // two mode-N blocks per piece (c1 8.59 -> 8.52 ms against one; four: 8.75)
-      static const int grp_env = getenv("NDS_TAIL_GROUP") ? atoi(getenv("NDS_TAIL_GROUP")) : 2;
-      const int grp = std::max(1, grp_env);
+      const int grp = 2;
       while (t.next >= 0) {
         const int lo = std::max(0, t.next - grp + 1);  // piece = blocks [lo, next]
         if (lv < t.levels - 1 - lo) return;          // block lo final after level L-1-lo
@@ -567,7 +557,6 @@ void plan_create_impl(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_
 void plan_destroy_impl(nds_plan* p) {
   if (!p) return;
   cudaSetDevice(p->ctx->device);
-  if (p->gexec) cudaGraphExecDestroy(p->gexec);
   for (auto e : p->pev) cudaEventDestroy(e);
   free_factors(p->f);
   delete p;  // the shared solver structures stay cached in the context
@@ -1079,8 +1068,7 @@ void rk4_impl(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z* const
     const double h = direction * dt;
     const double remainder = span - (double)full_steps * dt;
     int64_t done = 0;
-    static const bool coop = !(getenv("NDS_RK4") && std::string(getenv("NDS_RK4")) == "graph");
-    if (fused && coop) {  // every step in one cooperative launch (grid barriers between stages)
+    if (fused) {  // every step in one cooperative launch (grid barriers between stages)
       nds::Rk4Buffers buf{X, {K1, K2, K3, K4}, {ST, ST2}, (unsigned int*)(flag + 32)};
       nds::rk4_persistent_launch(rs, buf, full_steps, h, remainder > 0.0 ? direction * remainder : 0.0, s);
       done = full_steps;
@@ -1090,7 +1078,7 @@ void rk4_impl(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z* const
       ++done;
     }
     constexpr int64_t kPerGraph = 8;
-    if (full_steps - done >= kPerGraph) {
+    if (full_steps - done >= kPerGraph && s != cudaStreamLegacy) {  // the legacy stream cannot be captured
       NDS_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
       for (int i = 0; i < kPerGraph; ++i) step(h);
       NDS_CUDA(cudaStreamEndCapture(s, &graph));
@@ -1098,7 +1086,7 @@ void rk4_impl(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z* const
       for (; full_steps - done >= kPerGraph; done += kPerGraph) NDS_CUDA(cudaGraphLaunch(exec, s));
     }
     for (; done < full_steps; ++done) step(h);
-    if (remainder > 0.0 && !(fused && coop)) step(direction * remainder);
+    if (remainder > 0.0 && !fused) step(direction * remainder);
     nds::nonfinite_launch(X, total, flag, s);
     int hflag = 0;
     NDS_CUDA(cudaMemcpyAsync(&hflag, flag, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -1145,11 +1133,16 @@ int nds_ctx_create(nds_ctx** out, int device) {
       NDS_CUDA(cudaStreamCreateWithPriority(&c->tail, cudaStreamNonBlocking, lo));
     }
     for (auto& e : c->tev) NDS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    // keep stream-ordered allocations (factor pools) cached instead of returning them at syncs
-    cudaMemPool_t pool;
-    NDS_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    // a private stream-ordered pool that keeps its blocks cached across syncs (the device's
+    // default pool, shared with torch / NCCL in the same process, is left untouched)
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.handleTypes = cudaMemHandleTypeNone;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = device;
+    NDS_CUDA(cudaMemPoolCreate(&c->pool, &props));
     uint64_t keep = UINT64_MAX;
-    NDS_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    NDS_CUDA(cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &keep));
     for (auto& e : c->cev) NDS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     *out = c.release();
   });
@@ -1177,6 +1170,7 @@ void nds_ctx_destroy(nds_ctx* ctx) {
   for (auto& e : ctx->io_ev)
     if (e) cudaEventDestroy(e);
   if (ctx->own) cudaStreamDestroy(ctx->own);
+  if (ctx->pool) cudaMemPoolDestroy(ctx->pool);
   delete ctx;
 }
 
@@ -1237,45 +1231,9 @@ int nds_plan_execute(nds_plan* plan, const nds_z* d_b, nds_z* d_x, nds_z* d_work
       w = plan->ctx->ws[1];
     }
     if (w == (double2*)d_x || w == (const double2*)d_b) throw Error(NDS_ERR_INVALID, "work must not alias b or x");
-    // CUDA graph replay (NDS_GRAPH=1 enables): the first call runs eagerly (lazy kernel
-    // attributes, solver caches), the second is captured, later calls on the same buffers and
-    // stream replay it — one launch instead of ~100 kernels + ~150 event operations. Off by
-    // default: measured 3 % slower on c1 (9.30 vs 8.99 ms), the captured kernel nodes lose the
-    // high / low stream priorities that keep the diagonal tiles ahead of the far items.
-    static const bool use_graph = getenv("NDS_GRAPH") && std::string(getenv("NDS_GRAPH")) == "1";
-    nds_ctx* c = plan->ctx;
-    const bool same = plan->gexec && plan->gb == d_b && plan->gx == d_x && plan->gw == w && plan->gstream == c->stream;
-    if (!use_graph || plan->profiling || plan->gcalls++ == 0) {
-      plan->launches = execute(plan, (const double2*)d_b, (double2*)d_x, w, nullptr);
-      return;
-    }
-    if (!same) {
-      if (plan->gexec) {
-        cudaGraphExecDestroy(plan->gexec);
-        plan->gexec = nullptr;
-      }
-      cudaGraph_t graph = nullptr;
-      NDS_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-      int n = 0;
-      try {
-        n = execute(plan, (const double2*)d_b, (double2*)d_x, w, nullptr);
-      } catch (...) {
-        cudaStreamEndCapture(c->stream, &graph);
-        if (graph) cudaGraphDestroy(graph);
-        throw;
-      }
-      NDS_CUDA(cudaStreamEndCapture(c->stream, &graph));
-      const cudaError_t e = cudaGraphInstantiate(&plan->gexec, graph, 0);
-      cudaGraphDestroy(graph);
-      NDS_CUDA(e);
-      plan->gb = d_b;
-      plan->gx = d_x;
-      plan->gw = w;
-      plan->gstream = c->stream;
-      plan->glaunches = n;
-    }
-    NDS_CUDA(cudaGraphLaunch(plan->gexec, c->stream));
-    plan->launches = plan->glaunches;
+    // (CUDA-graph replay of the whole step was measured 3 % slower on c1 — captured kernel nodes
+    // lose the stream priorities that keep the diagonal tiles ahead of the far items — and removed.)
+    plan->launches = execute(plan, (const double2*)d_b, (double2*)d_x, w, nullptr);
   });
 }
 
@@ -1633,13 +1591,15 @@ static int dev_mode_rect(nds_ctx* ctx, int n_modes, const int64_t* dims_x, int m
         mm[rows_out * n + i + k * rows_out] = make_double2(z.re, z.im);  // column-major
       }
     double2* dm = nullptr;
-    NDS_CUDA(cudaMallocAsync(&dm, mm.size() * sizeof(double2), ctx->stream));
-    NDS_CUDA(cudaMemcpyAsync(dm, mm.data(), mm.size() * sizeof(double2), cudaMemcpyHostToDevice, ctx->stream));
+    NDS_CUDA(cudaMallocFromPoolAsync(&dm, mm.size() * sizeof(double2), ctx->pool, ctx->stream));
+    // the host copy stays alive until the stream has consumed it (freed by a host callback), so
+    // the call returns without a stream synchronisation (the sharded solver chains these)
+    auto* hold = new std::vector<double2>(std::move(mm));
+    NDS_CUDA(cudaMemcpyAsync(dm, hold->data(), hold->size() * sizeof(double2), cudaMemcpyHostToDevice, ctx->stream));
+    NDS_CUDA(cudaLaunchHostFunc(ctx->stream, [](void* v) { delete (std::vector<double2>*)v; }, hold));
     nds::mode_product_matrix_launch(dm, dm + rows_out * n, nds::mode_view(n_modes, dims_x, mode), (const double2*)d_x,
                                     (double2*)d_r, accumulate, ctx->stream, rows_out);
     NDS_CUDA(cudaFreeAsync(dm, ctx->stream));
-    // no stream synchronisation: an async copy from pageable memory has staged mm before it
-    // returns, so the caller may queue further work (the sharded solver chains these)
   });
 }
 

@@ -82,15 +82,15 @@ struct TileGeom {
   int bstride[NDS_MAX_MODES]; // strides inside a full tile
 };
 
-// Grouped far-update work item (backsub_v2.cuh far_group_body): up to G consecutive targets
-// along mode j share one slab read; see solve_plan_build.
+// Far-update work item (backsub_v2.cuh far_group_body, G = 1): target tile slot, mode, source
+// rows [kb, ke) along the mode, and the far-partial ring slot it writes.
 struct FarGroupItem {
   int tile;     // tile slot whose other block coordinates define the columns
   int j;        // mode
   int kb, ke;   // source rows along j (absolute; multiple of the stage depth)
-  int rb0;      // first target block along j
-  int nrb;      // valid row blocks
-  int acc;      // 1: accumulate into the slots
+  int rb0;      // target block along j
+  int nrb;      // valid row blocks (1)
+  int acc;      // 1: accumulate into the slot (0 for G = 1)
   int pad;
   int out[4];   // far-partial ring slot per row block
 };
@@ -101,50 +101,26 @@ struct SolvePlan {
   std::vector<int64_t> level_off; // host copy, size levels + 1
   int64_t* d_tiles = nullptr;     // tile ids sorted by descending level
   int wf_levels = 0;              // hyperplanes inside a full tile
-  int* d_wf = nullptr;            // local entries sorted by descending local level
+  int* d_wf = nullptr;            // generic tiles: local entries sorted by descending local level
   int* d_wf_off = nullptr;
-  int* d_wf_group = nullptr;      // lanes per entry for each local hyperplane (v2)
-  uint16_t* d_thr = nullptr;      // v2: [wf_levels][diag threads] local entry per thread (0xffff none)
-  int* d_lvl = nullptr;           // v2: per local hyperplane: grp | (busy warps << 8)
-  int* d_near_target = nullptr;   // v2 lines kernel (push): [tile slot][mode] near item of slot - e_mode at the next level
+  int* d_near_target = nullptr;   // cubic: [tile slot][mode] near item of slot - e_mode at the next level
   void* pool = nullptr;
-  // v2 (GEMM regime: every b_j a power of two >= 8 dividing n_j): per level, DMMA update work
-  // items (tile, mode, k-range) writing partials, then one diagonal-tile kernel.
+  // Cubic regime (c0-c3: B^N = 4096-entry tiles, B in {8, 16} dividing every n_j): per level,
+  // far-update DMMA items (neighbours >= 2 blocks away, ready one level early, low-priority
+  // streams) into a ring of level regions, then one diagonal-tile launch that also pushes the
+  // near updates (adjacent block) of the next level.
   bool v2 = false;
-  // Items {tile slot (global), mode, k_begin, k_end}; far = neighbours >= 2 blocks away (ready
-  // one level early, low-priority stream), near = adjacent block (critical stream).
-  std::vector<int64_t> far_off, near_off;  // per level into the item lists, size levels + 1
-  int4* d_far_items = nullptr;
-  int4* d_near_items = nullptr;
+  std::vector<int64_t> near_off;  // per level: near items (computed by the previous level's diagonal CTAs)
   int4* d_tile_ranges = nullptr;  // per tile slot: {far first, far count, near first, near count} (level-relative)
-  double2* d_far_partial[2] = {nullptr, nullptr};  // double-buffered by level parity
-  double2* d_near_partial = nullptr;
-  double2* d_near_partial2 = nullptr;  // push mode: near partials double-buffered by level parity
-  int64_t max_far = 0, max_near = 0;
-  // grouped far items (fgroup >= 1; 0 = plain items): per level [fg_off[lv], fg_off[lv + 1]) of d_fg_items; their
-  // partials in a ring of fg_ring level regions of fg_slots tiles (region = target level % fg_ring)
-  int fgroup = 0;
-  std::vector<int64_t> fg_off;
+  double2* d_near_partial = nullptr;   // near partials double-buffered by level parity
+  double2* d_near_partial2 = nullptr;
+  int64_t max_near = 0;
+  std::vector<int64_t> fg_off;         // per level: [fg_off[lv], fg_off[lv + 1]) of d_fg_items
   FarGroupItem* d_fg_items = nullptr;
-  double2* d_fg_ring = nullptr;
+  double2* d_fg_ring = nullptr;        // far partials: fg_ring level regions of fg_slots tiles
   int fg_ring = 0;
   int64_t fg_slots = 0;
   cudaStream_t s_crit = nullptr, s_far = nullptr, s_far2 = nullptr;  // far: even / odd levels
-  // dataflow (persistent-kernel) solve, N = 3: per-slot / per-item tables, partial rings, counters
-  bool persist = false;
-  int* d_level_of = nullptr;
-  int* d_level_count = nullptr;
-  int* d_far_rel = nullptr;
-  int* d_far_dep = nullptr;
-  int* d_far_expected = nullptr;
-  int* d_push_slot = nullptr;
-  int* d_queue = nullptr;  // merged dataflow work order
-  int64_t n_far_items = 0, ctr_count = 0, n_queue = 0;
-  void* persist_pool = nullptr;
-  double2* d_far_ring = nullptr;
-  double2* d_near_ring = nullptr;
-  int* d_ctr = nullptr;
-  int* h_err = nullptr;  // pinned: watchdog flag of the last dataflow solve
   std::vector<cudaEvent_t> ev;  // diag(lv), far(lv), start, end
 };
 
@@ -191,9 +167,6 @@ struct TailHook {
 // In-place Y over C. Returns kernels launched.
 int backsub_launch(const SolvePlan& sp, const double2* t_pool, double2* c, cudaStream_t stream,
                    Recorder* rec = nullptr, const HeadSync* head = nullptr, const TailHook* tail = nullptr);
-// True when backsub_launch runs the dataflow (persistent-kernel) solve for this plan, which does
-// not honour HeadSync.
-bool backsub_is_dataflow(const SolvePlan& sp);
 
 // ---- matrix functions (ODE propagator) -----------------------------------------------------
 // exp(t T_m) by the Parlett recurrence, one CTA per listed mode: T_m at t_pool + toff[m]

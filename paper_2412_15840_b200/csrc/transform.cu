@@ -9,10 +9,11 @@
 //   * inner == 1  ("COLM", mode 1): C(b, i) = X(b, :) . M^T(:, i), rows of X contiguous in k;
 //   * otherwise (tiny inner, e.g. n_1 < 8): a direct kernel.
 // The GEMM runs on the FP64 tensor pipe (DMMA, mma.sync.m8n8k4.f64): measured 37.1 TF on B200
-// vs 34.1 TF for DFMA (tools/microbench/fp64_peaks.cu, profiles/). Complex products use four
-// real DMMAs per 8x8x4 block (re.re, -im.im, re.im, im.re) accumulated in registers; tiles are
-// staged global->shared with a multi-stage cp.async pipeline into bank-conflict-free padded
-// layouts (row strides = 4 resp. 2 mod 8 complex for the DMMA fragment pattern).
+// vs 34.1 TF for DFMA (tools/microbench/fp64_peaks.cu, profiles/). Complex products use the
+// 3-multiplication form: per 8x8x4 block three real DMMAs Ar Br, Ai Bi, (Ar + Ai)(Br + Bi), with
+// Re = p1 - p2 and Im = p3 - p1 - p2 (6 of the 8 real flops of a complex MAC); tiles are staged
+// global->shared with a multi-stage cp.async pipeline into bank-conflict-free padded layouts
+// (row strides = 4 resp. 2 mod 8 complex for the DMMA fragment pattern).
 #include <cstdlib>
 
 #include "common.cuh"
@@ -263,53 +264,20 @@ static void launch_gemm_t(GemmArgs g, cudaStream_t stream) {
   NDS_LAUNCH_CHECK();
 }
 
-enum GemmShape { kWide = 0, kTall = 1, kForce4M = 2, kForce3M64 = 3 };
+// Two CTA shapes (64 x 32 and 32 x 64, 8 warps of 16 x 16, 2 CTAs / SM, BK = 16, 3-stage ring);
+// per GEMM the one with the least padded output wins (n = 96 pads 64-row tiles by a third).
+// Warp tiles of 16 x 16 (2 x 2 fragments) need 4 operand sums and 4 fragment loads per 12 DMMAs
+// (32 x 8 warps: 5 and 5) — the 3M sums share the FP64 pipe with the DMMAs (c1 transforms
+// 4.74 -> 4.63 ms). Measured and removed: 4M 64 x 128, 3M 64 x 64 at 4 stages, 32 x 8 warps.
+enum GemmShape { kWide = 0, kTall = 1 };
 struct ShapeDims {
   int bm, bn;
 };
-static ShapeDims shape_dims(GemmShape s) {
-  switch (s) {
-    case kTall: return {32, 64};
-    case kForce4M: return {64, 128};
-    case kForce3M64: return {64, 64};
-    default: return {64, 32};
-  }
-}
-static int forced_shape() {
-  static const int v = [] {
-    const char* e = getenv("NDS_GEMM");
-    if (!e) return -1;
-    const std::string s(e);
-    if (s == "4m") return (int)kForce4M;
-    if (s == "3m64") return (int)kForce3M64;
-    if (s == "wide") return (int)kWide;
-    if (s == "tall") return (int)kTall;
-    return -1;
-  }();
-  return v;
-}
-
-// Warp tiles of 16 x 16 (2 x 2 fragments): 4 operand sums and 4 fragment loads per 12 DMMAs
-// (32 x 8 warps: 5 and 5) — the 3M sums share the FP64 pipe with the DMMAs (c1 transforms
-// 4.74 -> 4.63 ms, c2 15.89 -> 15.36). NDS_GEMM_W82=1 restores the 32 x 8 warps (A/B).
-static bool w82() {
-  static const bool v = getenv("NDS_GEMM_W82") != nullptr;
-  return v;
-}
+static ShapeDims shape_dims(GemmShape s) { return s == kTall ? ShapeDims{32, 64} : ShapeDims{64, 32}; }
 
 static void launch_gemm(GemmShape shape, GemmArgs g, cudaStream_t stream) {
-  switch (shape) {
-    case kTall:
-      if (w82()) launch_gemm_t<32, 64, 16, 1, 8, 3, true, 2>(g, stream);
-      else launch_gemm_t<32, 64, 16, 2, 4, 3, true, 2>(g, stream);
-      break;
-    case kForce4M: launch_gemm_t<64, 128, 16, 2, 4, 3, false>(g, stream); break;
-    case kForce3M64: launch_gemm_t<64, 64, 16, 2, 4, 4, true>(g, stream); break;
-    default:
-      if (w82()) launch_gemm_t<64, 32, 16, 2, 4, 3, true, 2>(g, stream);
-      else launch_gemm_t<64, 32, 16, 4, 2, 3, true, 2>(g, stream);
-      break;
-  }
+  if (shape == kTall) launch_gemm_t<32, 64, 16, 2, 4, 3, true, 2>(g, stream);
+  else launch_gemm_t<64, 32, 16, 4, 2, 3, true, 2>(g, stream);
 }
 
 // Column split for ROWM: power of two W in [8, bn] minimising padded columns (ties -> wider).
@@ -338,16 +306,10 @@ static double shape_cost(GemmArgs& g, bool colm, int64_t inner, GemmShape s) {
 }
 
 static void launch_gemm_auto(GemmArgs g, bool colm, int64_t inner, cudaStream_t stream) {
-  GemmShape best;
-  const int f = forced_shape();
-  if (f >= 0) {
-    best = (GemmShape)f;
-  } else {
-    GemmArgs gt = g;
-    const double cw = shape_cost(gt, colm, inner, kWide);
-    const double ct = shape_cost(gt, colm, inner, kTall);
-    best = ct < cw * (1.0 - 1e-9) ? kTall : kWide;
-  }
+  GemmArgs gt = g;
+  const double cw = shape_cost(gt, colm, inner, kWide);
+  const double ct = shape_cost(gt, colm, inner, kTall);
+  const GemmShape best = ct < cw * (1.0 - 1e-9) ? kTall : kWide;
   shape_cost(g, colm, inner, best);
   launch_gemm(best, g, stream);
 }

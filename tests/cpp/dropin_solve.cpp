@@ -35,6 +35,20 @@ int main() {
   } catch (const SingularOperatorError& e) {
     singular_ok = e.multi_index() == std::vector<std::int64_t>{2, 2};
   }
+  // validate_problem (sylvester.cpp:17-27): too few coefficients / wrong extent -> invalid_argument
+  int shape_ok = 0;
+  for (int variant = 0; variant < 2; ++variant) {
+    SylvesterProblem p;
+    p.rhs = NDTensor::zeros({3, 4});
+    p.coefficients = {Matrix::identity(3)};
+    if (variant == 1) p.coefficients.push_back(Matrix::identity(2));
+    try {
+      ndsylv::gpu::solve(p);
+    } catch (const std::invalid_argument&) {
+      ++shape_ok;
+    }
+  }
+  singular_ok = singular_ok && shape_ok == 2;
   std::printf("max_rel_diff %.3e singular_ok %d\n", worst, singular_ok);
 
   // ODE: the reference's own random systems (rng.hpp random_ode_system), CPU vs GPU

@@ -120,10 +120,10 @@ def test_full_config_residual(ctx, name):
 
 
 @pytest.mark.parametrize("name,dims", [("c1", (128, 96, 64)), ("c2", (32, 32, 32, 32)), ("c4", (2,) * 18)])
-def test_plan_graph_replay(ctx, name, dims):
-    """nds_plan_execute (with NDS_GRAPH=1 in the environment: the graph-replay path; otherwise
-    the eager path) gives the bitwise-same X on every call (fixed summation orders), including
-    after a buffer change."""
+def test_plan_repeatable(ctx, name, dims):
+    """nds_plan_execute gives the bitwise-same X on every call (fixed summation orders, no
+    floating-point atomics; test_sylvester.cpp:127-154 pins bitwise reruns), including after a
+    buffer change."""
     import torch
     a, b = configs.make_problem(name, seed=3, dims=dims)
     dims = b.shape  # the advection-diffusion generator (c2) uses one extent for every mode
@@ -133,7 +133,7 @@ def test_plan_graph_replay(ctx, name, dims):
     bufs = [(torch.empty_like(d_b), torch.empty_like(d_b)) for _ in range(2)]
     ctx.set_stream(torch.cuda.current_stream().cuda_stream)
     outs = []
-    for k in [0, 0, 0, 1, 1, 0]:  # eager, capture, replay, re-capture, replay, re-capture
+    for k in [0, 0, 0, 1, 1, 0]:
         d_x, d_w = bufs[k]
         d_x.zero_()
         d_w.fill_(float("nan"))

@@ -12,5 +12,5 @@ timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv pyth
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:far_group -s 20 -c 1 -o $O/far_c1_mid python tools/profile_step.py --config c1 --reps 1 > /dev/null 2>&1
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:tile_diag_lines -s 22 -c 1 -o $O/lines_c1_mid python tools/profile_step.py --config c1 --reps 1 > /dev/null 2>&1
 timeout 400 ncu --set full --clock-control none --import-source on -k regex:far_group -s 28 -c 1 -o $O/far_c3_mid python tools/profile_step.py --config c3 --reps 1 > /dev/null 2>&1
-NDS_HEAD=0 timeout 300 ncu --set full --clock-control none --import-source on -k regex:zgemm_dmma -s 2 -c 1 -o $O/zgemm_c1 python tools/profile_step.py --config c1 --reps 1 > /dev/null 2>&1
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:zgemm_dmma -s 2 -c 1 -o $O/zgemm_c1 python tools/profile_step.py --config c1 --reps 1 > /dev/null 2>&1
 echo done > $O/done
