@@ -201,6 +201,51 @@ int nds_dev_back_substitute(nds_ctx* ctx, int n_modes, const int64_t* dims, cons
 int nds_dev_residual(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z* const* a, const nds_z* d_x,
                      const nds_z* d_b, double* res_max, double* res_2, double* b_max, double* b_2);
 
+/* ---- multi-GPU sharded solve ---------------------
+ * One rank per GPU. B and X are sharded in layout L_N: rank r owns a contiguous range of the
+ * column-major tensor (nds_dist_slab) — a block of the last mode, or for all-binary problems one
+ * index of the last log2 P modes. Inside a solve the transforms re-shard once each way by an
+ * all-to-all and the triangular solve is pipelined over (rank, block of the last modes) with
+ * point-to-point forwarding of solved blocks; all exchanges are NCCL P2P on the rank's own
+ * communication stream, ordered against its compute stream by events (no host sync). */
+typedef struct nds_comm nds_comm;
+typedef struct nds_dist nds_dist;
+#define NDS_COMM_ID_BYTES 128
+typedef struct {
+  int32_t ranks, rank;
+  int32_t head_modes, tail_modes, pipe_modes, pipe_blocks;
+  int32_t local_solve_path;  /* NDS_PATH_* of the rank's local block solves */
+  int32_t launches;          /* kernels of the last solve (this rank) */
+  int64_t alltoall_bytes;    /* bytes this rank sends in the two all-to-alls of one solve */
+  int64_t pipeline_bytes;    /* bytes this rank forwards to lower ranks in one solve */
+  double min_abs_denominator;
+} nds_dist_info_t;
+/* NCCL unique id (rank 0 creates it, the caller broadcasts the NDS_COMM_ID_BYTES bytes). */
+int nds_comm_unique_id(void* id_out);
+/* NCCL communicator of rank `rank` of `world` on CUDA device `device` (NCCL is loaded at run
+ * time: libnccl.so.2, the copy already in the process if any). */
+int nds_comm_create_nccl(nds_comm** out, int device, int rank, int world, const void* id);
+/* In-process transport for `world` ranks sharing one device (one host thread per rank; tests):
+ * fills out[0..world-1]. */
+int nds_comm_create_loopback(int world, nds_comm** out);
+void nds_comm_destroy(nds_comm* comm);
+/* Rank state for the problem with Schur factors u, t (identical on every rank); comm NULL = one
+ * rank. Runs the singular check of the WHOLE operator first, so every rank fails alike
+ * (NDS_ERR_SINGULAR + sing with the global first offender) before any exchange. */
+int nds_dist_create(nds_ctx* ctx, nds_comm* comm, int n_modes, const int64_t* dims, const nds_z* const* u,
+                    const nds_z* const* t, double singular_tol, nds_dist** out, nds_singular* sing);
+void nds_dist_destroy(nds_dist* d);
+/* Rank r's L_N slab: flat offset and entry count within the full column-major tensor. */
+int nds_dist_slab(const nds_dist* d, int rank, int64_t* offset, int64_t* count);
+int nds_dist_info(const nds_dist* d, nds_dist_info_t* info);
+/* x = solve(b) on this rank's slabs (device pointers), asynchronous on the context stream; every
+ * rank of the communicator must call it. */
+int nds_dist_solve(nds_dist* d, const nds_z* d_b, nds_z* d_x);
+/* One process, n_devices GPUs: ndsylv::solve after its Schur step, sharded over the devices
+ * (one host thread, context and NCCL communicator per device), host buffers. */
+int nds_solve_multi(int n_devices, const int* devices, int n_modes, const int64_t* dims, const nds_z* const* u,
+                    const nds_z* const* t, const nds_z* b, nds_z* x, double singular_tol, nds_singular* sing);
+
 /* ---- ODE  dX/dt = sum_j A_j x_j X + B,  X(0) = X0  (reference ode.hpp) ------ */
 
 /* ndsylv::triangular_exp (schur.hpp:24, schur.cpp:203-228): f = exp(t T), T upper triangular

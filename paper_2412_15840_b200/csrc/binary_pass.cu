@@ -124,13 +124,14 @@ __global__ void __launch_bounds__(kBinThreads, 2) binary_pass_kernel(const BinPa
 
 // Plan the passes over [mode0, mode1) (1-based, all n_j = 2): greedily take as many binary modes
 // as fit a 4096-entry tile with runs of min(I, 8..4096) entries.
-std::vector<BinGroup> plan_binary_groups(int n_modes, const int64_t* dims) {
+std::vector<BinGroup> plan_binary_groups(int n_modes, const int64_t* dims, int lo, int hi) {
   std::vector<BinGroup> out;
+  if (hi < 0) hi = n_modes;
   int64_t inner = 1;
   int j = 0;
   while (j < n_modes) {
     int avail = 0;
-    while (j + avail < n_modes && dims[j + avail] == 2) ++avail;
+    while (j >= lo && j + avail < hi && dims[j + avail] == 2) ++avail;
     if (avail == 0) {
       inner *= dims[j];
       ++j;

@@ -1924,3 +1924,5 @@ int nds_random_ode_system(int n_modes, const int64_t* dims, uint64_t seed, nds_z
 void nds_randn(uint64_t seed, uint64_t stream, int64_t count, double* out) { nds::randn_host(seed, stream, count, out); }
 
 }  // extern "C"
+
+#include "sharded.cuh"

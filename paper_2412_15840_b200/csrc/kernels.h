@@ -57,7 +57,8 @@ struct BinGroup {
   int first = 0, count = 0, logR = 0;
   int64_t inner = 1, outer = 1;
 };
-std::vector<BinGroup> plan_binary_groups(int n_modes, const int64_t* dims);
+// Fused groups of runs of binary modes among modes [lo, hi) (0-based; hi < 0: all modes).
+std::vector<BinGroup> plan_binary_groups(int n_modes, const int64_t* dims, int lo = 0, int hi = -1);
 int binary_pass_launch(const FactorSet& f, const BinGroup& gr, bool adjoint, const double2* x, double2* r,
                        cudaStream_t stream);
 

@@ -242,8 +242,7 @@ __global__ void __launch_bounds__(WM* WN * 32, MINB) zgemm_dmma_kernel(const Gem
 
 // Tile configurations. 3M kernels, 2 CTAs / SM, 8 warps, BK = 16, 3 stages:
 //   kWide: 64 x 32 per CTA;  kTall: 32 x 64 per CTA; warps of 16 x 16.
-// The shape with the least padded output is chosen per GEMM (ties: kWide). NDS_GEMM=4m|3m64
-// force the 4-multiply 64 x 128 kernel / the 1-CTA 64 x 64 3M kernel (A/B experiments).
+// The shape with the least padded output is chosen per GEMM (ties: kWide).
 // Algorithmic flops are counted as 8 per complex MAC in every roofline figure regardless.
 template <int BM, int BN, int BK, int WM, int WN, int ST, bool M3, int MINB = 1>
 static void launch_gemm_t(GemmArgs g, cudaStream_t stream) {
@@ -325,7 +324,9 @@ int mode_product_matrix_launch(const double2* mrow, const double2* mcol, const M
                                double2* r, bool accumulate, cudaStream_t stream, int64_t rows_out, int64_t lda_row) {
   const int n = (int)v.n;
   const int64_t m = rows_out > 0 ? rows_out : v.n;  // rows of M (output extent along the mode)
-  const bool gemm = n >= 16 && (v.inner == 1 || v.inner >= 8);
+  // DMMA GEMM from 16 rows of K up (K is zero-padded to the 16-deep stage; rectangular updates
+  // with many output rows already pay from K = 8); tiny inner extents use the direct kernel
+  const bool gemm = (n >= 16 || (n >= 8 && m >= 32)) && (v.inner == 1 || v.inner >= 8);
   if (!gemm) {
     const int64_t total = v.inner * m * v.outer;
     const int threads = 256;
