@@ -17,8 +17,8 @@ with U_j). The host Schur factorisations are setup, computed once and timed sepa
           bounded slab sample of the same workload, rank 0 at N=1 only.
 
 --impl reference runs the reference's own CPU solver (oracle/_ref) the same way.
-Multi-GPU (torchrun): independent replicas of the workload, one per rank (weak scaling); with
---sharded, ONE problem split across the ranks by the ShardedSolver (strong scaling).
+Multi-GPU (torchrun, --gpus N > 1): ONE c3 problem sharded across the ranks by the C-ABI engine
+(nds_dist_*; strong scaling, NCCL); --replicas runs independent copies instead (weak scaling).
 """
 from __future__ import annotations
 
@@ -143,23 +143,32 @@ def bench_config(config, world, parallelism=None):
     return {"workload": config, "dims": list(dims), "P": int(np.prod(dims)),
             "description": configs.DESCRIPTIONS[config],
             "parallelism": parallelism or (f"replicas x{world}" if world > 1 else "1 GPU"),
-            "l2": "inputs larger than L2 (256 MiB per tensor vs 126 MB L2); no flush",
+            "l2": (f"inputs larger than L2 ({16 * int(np.prod(dims)) / 2**20:.0f} MiB per tensor vs 126 MB L2); no flush"
+                   if 16 * int(np.prod(dims)) > 126e6 else "inputs fit in L2; no flush (not a headline config)"),
             "schur": "host setup, excluded from the rate (BASELINE.md 2)"}
+
+
+# Bounded samples of the reference CPU solve for the configs whose full solve takes many minutes
+# (c3: ~12 min, c4: ~9 min, c2: ~2 min on 8 cores): the leading planes of the
+# workload (same extents in every other mode, same generator).
+REF_SAMPLE_DIMS = {"c2": (96, 96, 96, 8), "c3": (128, 128, 128, 2), "c4": (2,) * 23}
 
 
 class ReferenceStages:
     """The reference's own CPU solve stages (oracle/_ref: the unmodified ndsylv library built from
-    /root/reference/proj/src) on the FULL workload: forward_transform, back_substitute and
-    inverse_transform (sylvester.hpp:64-77) with the Schur factors from its own schur()
-    (setup, timed separately, like ndsylv::solve's SolveReport::schur_seconds). Inputs come from
-    the generator-v1 copy in the reference shim, so the product library is never loaded."""
+    /root/reference/proj/src): forward_transform, back_substitute and inverse_transform
+    (sylvester.hpp:64-77) with the Schur factors from its own schur() (setup, timed separately,
+    like ndsylv::solve's SolveReport::schur_seconds), on the FULL workload for c0 / c1 and on the
+    bounded sample REF_SAMPLE_DIMS otherwise. Inputs come from the generator-v1 copy in the
+    reference shim, so the product library is never loaded."""
 
     def __init__(self, config, seed, threads):
         import oracle
         from paper_2412_15840_b200 import configs
         self.ref = oracle.Ref()
         self.ref.set_threads(threads)
-        self.a, self.b = configs.make_problem(config, seed=seed, randn=self.ref.randn)
+        self.sample_dims = REF_SAMPLE_DIMS.get(config)
+        self.a, self.b = configs.make_problem(config, seed=seed, dims=self.sample_dims, randn=self.ref.randn)
         self.P = int(self.b.size)
         t0 = time.perf_counter()
         fac = [self.ref.schur(m) for m in self.a]
@@ -181,10 +190,13 @@ class ReferenceStages:
 
 
 def reference_sample_text(config, threads):
+    d = REF_SAMPLE_DIMS.get(config)
+    what = f"the full {config} workload" if d is None else \
+        f"a bounded sample of {config}: its leading planes {'x'.join(map(str, d))} (P = {int(np.prod(d))})"
     return (f"reference ndsylv stages (oracle/_ref, unmodified sources, g++ -O3 -fopenmp, no -march; "
             f"OpenMP over {threads} threads in the transforms, back_substitute serial by construction, "
-            f"sylvester.cpp:71-108) on the full {config} workload; rate = P / (forward + backsub + inverse "
-            f"wall seconds); Schur excluded (setup)")
+            f"sylvester.cpp:71-108) on {what}; rate = P / (forward + backsub + inverse wall seconds); "
+            f"Schur excluded (setup)")
 
 
 def verify_x(ctx, config, seed, a_list, dims, d_x, d_b):
@@ -208,6 +220,9 @@ def verify_x(ctx, config, seed, a_list, dims, d_x, d_b):
 def run_reference(args, world, rank):
     if rank != 0:
         return 0
+    sharded = world > 1 and not args.replicas
+    if sharded and "--config" not in sys.argv:
+        args.config = "c3"  # the same workload as our arm's sharded default
     threads = os.cpu_count() or 1
     rs = ReferenceStages(args.config, args.seed, threads)
     secs, stages = [], []
@@ -220,9 +235,11 @@ def run_reference(args, world, rank):
     value = rs.P / mean_s
     line = {"metric": METRIC, "value": value, "unit": "unknowns/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": mean_s * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic (generator v1, seeded Gaussian)",
+            "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "c128",
+            "data": "synthetic (generator v1, seeded Gaussian)",
             "impl": "reference",
-            "config": bench_config(args.config, 1),
+            "config": bench_config(args.config, world,
+                                   parallelism=f"sharded x{world} (nds_dist, NCCL)" if sharded else None),
             "cpu_baseline": {"value": value, "unit": "unknowns/s", "cores": threads, "kind": "reference",
                              "sample": reference_sample_text(args.config, threads)},
             "e2e": {"value": value, "unit": "unknowns/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -233,68 +250,106 @@ def run_reference(args, world, rank):
 
 
 def run_sharded(args, world, rank, local):
-    """--sharded: ONE problem of --config split across the ranks (strong scaling), through the
-    multi-GPU ShardedSolver (paper_2412_15840_b200/distributed.py): transforms local
-    in the L_N slab layout, NCCL all-to-all re-shards, triangular solve pipelined over (rank,
-    mode-N sub-block) with point-to-point block forwarding. value = P / (max-over-ranks device
-    time per solve). Schur is host setup on every rank (same seed, same factors)."""
-    import socket
-
+    """ONE problem split across the ranks (strong scaling) through the C-ABI sharded engine
+    (nds_dist_*, csrc/sharded.cuh): transforms local in L_N / L_1 with one NCCL
+    all-to-all each way, triangular solve pipelined over (rank, block of the last modes) with
+    point-to-point forwarding — all on the ranks' own streams, no host sync inside a solve.
+    value = P / (max-over-ranks device time per solve). The default for --gpus N > 1 (config c3);
+    rank 0 also times the single-GPU plan path on the same config for reference."""
     import torch
     import torch.distributed as dist
     import paper_2412_15840_b200 as nds
     from paper_2412_15840_b200 import configs
-    from paper_2412_15840_b200.distributed import CudaLocalOps, ShardedSolver, scatter_LN
+    from paper_2412_15840_b200.distributed import Comm, ShardedSolver, plan_layout
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if not dist.is_initialized():  # one rank: a single-member NCCL group for the same code path
-        s = socket.socket()
-        s.bind(("127.0.0.1", 0))
-        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        os.environ["MASTER_PORT"] = str(s.getsockname()[1])
-        s.close()
-        dist.init_process_group("nccl", rank=0, world_size=1)
     ctx = nds.Context(local)
     stream = torch.cuda.Stream(dev)
     torch.cuda.set_stream(stream)
+    ctx.set_stream(stream.cuda_stream)
     a_list, b_host = configs.make_problem(args.config, seed=args.seed)
     dims = tuple(b_host.shape)
     P = int(np.prod(dims))
+    t0 = time.perf_counter()
     factors = [ctx.schur(a) for a in a_list]
+    schur_s = time.perf_counter() - t0
     us = [f[0] for f in factors]
     ts = [f[1] for f in factors]
-    solver = ShardedSolver(dims, us, ts, CudaLocalOps(ctx))
-    b_local = torch.from_numpy(scatter_LN(b_host, world)[rank]).to(dev)
+    single = None
+    if rank == 0 and not args.no_single:  # the 1-GPU plan path on the same workload, for the scaling context
+        plan = ctx.plan(us, ts)
+        d_b = torch.from_numpy(np.ascontiguousarray(b_host.ravel(order="F"))).to(dev)
+        d_x, d_w = torch.empty_like(d_b), torch.empty_like(d_b)
+        for _ in range(2):
+            plan.execute(d_b.data_ptr(), d_x.data_ptr(), d_w.data_ptr())
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(3):
+            plan.execute(d_b.data_ptr(), d_x.data_ptr(), d_w.data_ptr())
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        ms1 = e0.elapsed_time(e1) / 3
+        single = {"ms_per_solve": ms1, "unknowns_per_s": P / (ms1 * 1e-3)}
+        del plan, d_b, d_x, d_w
+        torch.cuda.empty_cache()
+    comm = Comm.nccl(local) if world > 1 else None
+    solver = ShardedSolver(ctx, us, ts, comm)
+    off, cnt = solver.slab(rank)
+    flat = np.ascontiguousarray(b_host.reshape(-1, order="F")[off:off + cnt])
     del b_host
+    d_b = torch.from_numpy(flat).to(dev)
+    d_x = torch.empty_like(d_b)
     for _ in range(args.warmup):
-        x_local = solver.solve(b_local)
+        solver.solve(d_b, d_x)
     torch.cuda.synchronize(dev)
-    dist.barrier()
+    barrier(world)
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         e0.record(stream)
         for _ in range(args.steps):
-            x_local = solver.solve(b_local)
+            solver.solve(d_b, d_x)
         e1.record(stream)
         torch.cuda.synchronize(dev)
-    dist.barrier()
+    barrier(world)
     ms_step = max_over_ranks(world, e0.elapsed_time(e1), dev) / args.steps
+    info = solver.info()
+    L = plan_layout(dims, world)
     verify = None
-    if not args.no_verify:
-        verify = {"x_local_max": float(x_local.abs().max())}  # the residual needs the whole X
+    if not args.no_verify:  # X at the X_ref fixture's samples that fall in this rank's slab
+        path = os.path.join(ROOT, "tests", "golden", f"xref_{args.config}.npz")
+        if args.seed == 0 and os.path.exists(path):
+            fx = np.load(path)
+            sel = (fx["idx"] >= off) & (fx["idx"] < off + cnt)
+            x_s = d_x[torch.from_numpy(fx["idx"][sel] - off).to(dev)].cpu().numpy()
+            err = float(np.max(np.abs(x_s - fx["x"][sel]))) / float(fx["xmax"]) if sel.any() else 0.0
+            verify = {"xref_rel_max_sampled": max_over_ranks(world, err, dev), "ok": None}
+            verify["ok"] = verify["xref_rel_max_sampled"] <= 1e-9
     if rank == 0:
         print(json.dumps({
             "metric": METRIC, "value": P / (ms_step * 1e-3), "unit": "unknowns/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "c128 (fp64 DMMA)",
             "data": "synthetic (generator v1, seeded Gaussian)",
-            "config": {"workload": args.config, "dims": list(dims), "P": P, "parallelism": f"sharded x{world}",
-                       "description": configs.DESCRIPTIONS[args.config]},
-            "roofline": None, "cpu_baseline": None, "e2e": None, "gpu_launches": None,
+            "config": bench_config(args.config, world, parallelism=f"sharded x{world} (nds_dist, NCCL)"),
+            "schur_seconds_host": schur_s,
+            "sharding": {"head_modes": info["head_modes"], "tail_modes": info["tail_modes"],
+                         "pipe_modes": info["pipe_modes"], "pipe_blocks": info["pipe_blocks"],
+                         "local_solve_path": nds.Plan.SOLVE_PATHS.get(info["local_solve_path"]),
+                         "nvlink_bytes_per_solve_rank0": {"alltoall": L.alltoall_bytes(0),
+                                                          "pipeline": L.pipeline_bytes(0)},
+                         "nvlink_bytes_per_solve_max_rank": max(L.alltoall_bytes(r) + L.pipeline_bytes(r)
+                                                                for r in range(world))},
+            "single_gpu_plan_same_config": single,
+            "roofline": None, "cpu_baseline": None, "e2e": None,
+            "gpu_launches": info["launches"] * args.steps, "launches_per_step": info["launches"],
             "clocks": clk.summary(), "verify": verify}), flush=True)
-    dist.destroy_process_group()
+    solver.close()
+    if comm is not None:
+        comm.close()
+    if world > 1:
+        dist.destroy_process_group()
     return 0
 
 
@@ -312,7 +367,11 @@ def main():
     ap.add_argument("--no-verify", action="store_true",
                     help="skip the correctness stamp of the timed X (device residual + X_ref samples)")
     ap.add_argument("--sharded", action="store_true",
-                    help="one problem split across the ranks (ShardedSolver, strong scaling) instead of replicas")
+                    help="one problem split across the ranks (the default for --gpus N > 1; at N = 1 the same engine "
+                         "on one rank)")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N > 1: independent replicas of the workload, one per rank (weak scaling)")
+    ap.add_argument("--no-single", action="store_true", help="sharded mode: skip the 1-GPU plan reference timing")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
 
@@ -320,7 +379,9 @@ def main():
     if args.impl == "reference":
         return run_reference(args, world, rank)
 
-    if args.sharded:
+    if args.sharded or (world > 1 and not args.replicas):
+        if world > 1 and args.config == DEFAULT_CONFIG and "--config" not in sys.argv:
+            args.config = "c3"  # the sharded headline (BASELINE.json configs[3]: 1/2/4/8 B200)
         return run_sharded(args, world, rank, local)
 
     import torch

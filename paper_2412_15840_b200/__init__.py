@@ -55,6 +55,8 @@ EXPORTED = [
     "nds_triangular_exp", "nds_ode_create", "nds_ode_destroy", "nds_ode_at", "nds_ode_at_dev", "nds_propagate",
     "nds_rk4", "nds_tensor_file_info", "nds_read_tensor", "nds_write_tensor", "nds_read_tensor_dev",
     "nds_write_tensor_dev", "nds_random_problem", "nds_random_ode_system", "nds_randn",
+    "nds_comm_unique_id", "nds_comm_create_nccl", "nds_comm_create_loopback", "nds_comm_destroy", "nds_dist_create",
+    "nds_dist_destroy", "nds_dist_slab", "nds_dist_info", "nds_dist_solve", "nds_solve_multi",
 ]
 
 
@@ -115,6 +117,13 @@ class _Singular(C.Structure):
 
 class _Stats(C.Structure):
     _fields_ = [("entries", C.c_int64), ("multiplies", C.c_int64), ("min_abs_denominator", C.c_double)]
+
+
+class _DistInfo(C.Structure):
+    _fields_ = [("ranks", C.c_int32), ("rank", C.c_int32), ("head_modes", C.c_int32), ("tail_modes", C.c_int32),
+                ("pipe_modes", C.c_int32), ("pipe_blocks", C.c_int32), ("local_solve_path", C.c_int32),
+                ("launches", C.c_int32), ("alltoall_bytes", C.c_int64), ("pipeline_bytes", C.c_int64),
+                ("min_abs_denominator", C.c_double)]
 
 
 _vp = C.c_void_p
@@ -194,8 +203,40 @@ def load_library(path: str = LIB_PATH):
     L.nds_random_problem.argtypes = [_vp, C.c_int, _i64p, C.c_uint64, _vp, _vp, _vp]
     L.nds_random_ode_system.argtypes = [C.c_int, _i64p, C.c_uint64, _vp, _vp, _vp]
     L.nds_randn.argtypes = [C.c_uint64, C.c_uint64, C.c_int64, _vp]
+    L.nds_comm_unique_id.argtypes = [_vp]
+    L.nds_comm_create_nccl.argtypes = [C.POINTER(_vp), C.c_int, C.c_int, C.c_int, _vp]
+    L.nds_comm_create_loopback.argtypes = [C.c_int, C.POINTER(_vp)]
+    L.nds_comm_destroy.argtypes = [_vp]
+    L.nds_dist_create.argtypes = [_vp, _vp, C.c_int, _i64p, _vp, _vp, C.c_double, C.POINTER(_vp),
+                                  C.POINTER(_Singular)]
+    L.nds_dist_destroy.argtypes = [_vp]
+    L.nds_dist_slab.argtypes = [_vp, C.c_int, _i64p, _i64p]
+    L.nds_dist_info.argtypes = [_vp, C.POINTER(_DistInfo)]
+    L.nds_dist_solve.argtypes = [_vp, _vp, _vp]
+    L.nds_solve_multi.argtypes = [C.c_int, C.POINTER(C.c_int), C.c_int, _i64p, _vp, _vp, _vp, _vp, C.c_double,
+                                  C.POINTER(_Singular)]
     _lib = L
     return L
+
+
+def solve_multi(devices, us, ts, rhs, singular_tol=0.0) -> np.ndarray:
+    """nds_solve_multi: the solve after the Schur step, sharded over `devices` of this process
+    (one host thread + NCCL communicator per device; host buffers)."""
+    L = load_library()
+    b = _f(rhs)
+    x = np.empty_like(b, order="F")
+    up, ku = _ptr_array(us)
+    tp, kt = _ptr_array(ts)
+    devs = (C.c_int * len(devices))(*[int(d) for d in devices])
+    sing = _Singular()
+    rc = L.nds_solve_multi(len(devices), devs, b.ndim, _dims(b.shape), up, tp, b.ctypes.data, x.ctypes.data,
+                           float(singular_tol), C.byref(sing))
+    if rc == ERR_SINGULAR:
+        raise SingularOperatorError(L.nds_last_error(None).decode(), sing.multi_index[:sing.n_modes],
+                                    complex(sing.den_re, sing.den_im))
+    if rc:
+        raise NdsError(rc, L.nds_last_error(None).decode())
+    return x
 
 
 def version() -> str:

@@ -1,32 +1,30 @@
-"""Multi-GPU solve: one process per GPU, torch.distributed (NCCL over NVLink) for the exchanges.
+"""Multi-GPU sharded solve: one rank per GPU.
 
-SURVEY.md 8(e). The transforms shard naturally; the triangular solve does not.
+The product path is the C-ABI engine (`nds_dist_*`, csrc/sharded.cuh): per rank, the
+transforms in layout L_N / L_1 with one all-to-all each way, and the triangular solve pipelined
+over (rank, block of the last modes) with point-to-point forwarding of solved blocks — NCCL P2P
+on the rank's communication stream, stream-ordered against its compute stream (no host sync).
+`ShardedSolver` drives it from Python (torchrun: one process per GPU; the NCCL unique id is
+broadcast through the torch.distributed group).
 
-Layouts (every local tensor is column-major complex128, flattened):
-  L_N: rank r owns the slab of mode N  [sN_r, sN_r + mN_r)   -> local dims (n_1, ..., n_{N-1}, mN_r)
-  L_1: rank q owns the slab of mode 1  [s1_q, s1_q + m1_q)   -> local dims (m1_q, n_2, ..., n_N)
+`plan_layout` mirrors the engine's mode groups and partitions (checked against `nds_dist_info`
+by the GPU tests), and `HostShardedSolver` runs the SAME schedule with host tensors over any
+torch.distributed backend — the gloo tests (tests/test_distributed.py) cover the multi-rank
+orchestration on CPU with it.
 
-solve(B in L_N):
-  1. forward, modes 1..N-1: local (each mode product is independent across mode-N slabs);
-  2. all-to-all re-shard L_N -> L_1 (the only exchange of the transform);
-  3. forward, mode N: local in L_1;
-  4. triangular solve, pipelined over (rank, sub-block): each rank's L_1 slab is cut into K
-     contiguous sub-blocks along mode N (the slowest index). Block (q, k) needs
-       - the mode-1 couplings  C_q[k] -= T_1[q rows, q' cols] x_1 Y_q'[k]  from every q' > q
-         (T_1 is dense upper triangular, so rank q needs every higher rank, not only q + 1),
-         received point-to-point as soon as rank q' has solved its block k;
-       - the mode-N couplings from its own blocks k' > k, applied by rank q right after solving
-         k':  C_q[:s_k'] -= T_N[:s_k', k' cols] x_N Y_q[k']  (one rectangular update);
-     then the local solve with T_1 and T_N restricted to their diagonal blocks. Blocks form a
-     wavefront over (P-1-q) + (K-1-k): P + K - 1 waves instead of P serial slab solves;
-  5. inverse, modes 2..N: local in L_1;
-  6. all-to-all re-shard L_1 -> L_N;
-  7. inverse, mode 1: local in L_N.  X is returned in the input layout L_N.
-
-The per-rank compute goes through `LocalOps`; `CudaLocalOps` calls the C ABI kernels on the
-rank's GPU. Tests substitute a CPU implementation to exercise the orchestration with gloo.
+Layouts (column-major complex128 slabs):
+  L_N: rank r owns tail super-indices [sG_r, sG_r + mG_r) of the last g modes (g = 1: a block of
+       mode N; all-binary problems: g = log2 P modes, one index each) — a contiguous range of the
+       full tensor;
+  L_1: rank q owns head super-indices [sH_q, sH_q + mH_q) of the first h modes (h = g).
+Solve (B and X in L_N): forward modes outside the tail group (local) -> all-to-all L_N -> L_1 ->
+forward tail modes (local) -> pipelined triangular solve -> inverse modes outside the head group
+(local) -> all-to-all L_1 -> L_N -> inverse head modes (local).
 """
 from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
 
 import numpy as np
 import torch
@@ -41,171 +39,332 @@ def block_partition(n: int, parts: int):
     return starts, sizes
 
 
-class CudaLocalOps:
-    """Local compute on this rank's GPU through the ndsylv_b200 C ABI (device pointers)."""
+@dataclass
+class Layout:
+    """Mode groups and partitions of the sharded solve (mirror of choose_groups, sharded.cuh)."""
+    dims: tuple
+    P: int
+    h: int = 1
+    g: int = 1
+    gp: int = 1
+    sH: list = field(default_factory=list)
+    mH: list = field(default_factory=list)
+    sG: list = field(default_factory=list)
+    mG: list = field(default_factory=list)
+    sK: list = field(default_factory=list)
+    mK: list = field(default_factory=list)
 
-    def __init__(self, ctx):
-        self.ctx = ctx
-        # one stream for the C ABI kernels and torch/NCCL: received blocks are read in stream order
-        ctx.set_stream(torch.cuda.current_stream().cuda_stream)
+    @property
+    def N(self):
+        return len(self.dims)
 
-    def zeros(self, count, like):
-        return torch.zeros(count, dtype=torch.complex128, device=like.device)
+    def couples(self, lo, hi):
+        """Rank `lo` needs rank `hi`'s solved blocks (structural nonzero of T_H[lo, hi])."""
+        if hi <= lo:
+            return False
+        if self.h == 1:
+            return self.mH[lo] > 0 and self.mH[hi] > 0
+        a, b = self.sH[lo], self.sH[hi]
+        return bin(a ^ b).count("1") == 1 and (b & ~a) != 0
 
-    def mode_product(self, dims, m, mode, x):
-        out = torch.empty(int(np.prod(dims)), dtype=torch.complex128, device=x.device)
-        self.ctx.dev_mode_apply(dims, mode, m, x.data_ptr(), out.data_ptr())
-        return out
+    def ln_dims(self, r):
+        N = self.N
+        return tuple(self.dims[j] if j < N - self.g else (self.mG[r] if self.g == 1 else 1) for j in range(N))
 
-    def mode_update(self, dims_x, mode, m, x, acc):
-        """acc += m x_mode x (m rectangular, host)."""
-        self.ctx.dev_mode_update(dims_x, mode, m, x.data_ptr(), acc.data_ptr())
+    def l1_dims(self, q):
+        return tuple(self.dims[j] if j >= self.h else (self.mH[q] if self.h == 1 else 1) for j in range(self.N))
 
-    def back_substitute(self, ts, dims, c, tol):
-        self.ctx.dev_back_substitute(ts, dims, c.data_ptr(), tol)
+    def slab(self, r):
+        """(flat offset, count) of rank r's L_N slab in the full column-major tensor."""
+        head = int(np.prod(self.dims[:self.N - self.g]))
+        return self.sG[r] * head, self.mG[r] * head
 
-    def synchronize(self):
-        torch.cuda.synchronize()
+    def mid(self, hi):
+        return int(np.prod(self.dims[self.h:hi], dtype=np.int64)) if hi > self.h else 1
+
+    def alltoall_bytes(self, q):
+        Mg = self.mid(self.N - self.g)
+        return sum(16 * (self.mH[r] * Mg * self.mG[q] + self.mH[q] * Mg * self.mG[r]) for r in range(self.P) if r != q)
+
+    def pipeline_bytes(self, q):
+        Mp = self.mid(self.N - self.gp)
+        nK = int(np.prod(self.dims[self.N - self.gp:]))
+        return 16 * self.mH[q] * Mp * nK * sum(self.couples(qq, q) for qq in range(q))
 
 
-def _exchange(send_blocks, recv_sizes, group):
-    """Uneven all-to-all of complex128 blocks (sent as float64 pairs)."""
-    send = torch.cat([b.reshape(-1) for b in send_blocks]) if send_blocks else torch.empty(0, dtype=torch.complex128)
-    send_r = torch.view_as_real(send.contiguous()).reshape(-1)
-    recv_r = torch.empty(2 * sum(recv_sizes), dtype=torch.float64, device=send_r.device)
-    dist.all_to_all_single(recv_r, send_r, [2 * s for s in recv_sizes], [2 * b.numel() for b in send_blocks],
-                           group=group)
-    recv = torch.view_as_complex(recv_r.reshape(-1, 2))
-    out, off = [], 0
-    for s in recv_sizes:
-        out.append(recv[off:off + s])
-        off += s
+def plan_layout(dims, P) -> Layout:
+    dims = tuple(int(d) for d in dims)
+    N = len(dims)
+    L = Layout(dims, P)
+    binary = all(d == 2 for d in dims)
+    if P > 64:
+        raise ValueError("at most 64 ranks")
+    if P > 1 and binary:
+        k = P.bit_length() - 1
+        if 1 << k != P:
+            raise ValueError("all-binary problems shard over a power-of-two rank count")
+        if 2 * k > N - 1:
+            raise ValueError("too few binary modes for this rank count")
+        L.h = L.g = k
+        L.gp = max(1, min(k + 1, N - k - 1))
+    elif P > 1 and (dims[0] < P or dims[-1] < P):
+        raise ValueError("the first and last extents must be at least the number of ranks")
+    nH = int(np.prod(dims[:L.h]))
+    nG = int(np.prod(dims[N - L.g:]))
+    nK = int(np.prod(dims[N - L.gp:]))
+    L.sH, L.mH = block_partition(nH, P)
+    L.sG, L.mG = block_partition(nG, P)
+    K = 1
+    if P > 1:
+        if binary:
+            K = nK
+        else:
+            edge = 16 if N == 3 else 8
+            K = next((c for c in range(min(4 * P, nK), 0, -1) if nK % c == 0 and (nK // c) % edge == 0), 0)
+            if K == 0:
+                K = min(2 * P, nK)
+    L.sK, L.mK = block_partition(nK, K)
+    return L
+
+
+def kron_sum(ts, dims):
+    """Kronecker sum of the T_j of consecutive modes on their column-major super-index."""
+    n = int(np.prod(dims))
+    out = np.zeros((n, n), dtype=np.complex128)
+    acc = 1
+    for t, d in zip(ts, dims):
+        left = np.eye(acc)
+        right = np.eye(n // (acc * d))
+        out += np.kron(right, np.kron(t, left))  # column-major: earlier modes vary fastest
+        acc *= d
     return out
 
 
-class ShardedSolver:
-    """Distributed solve of sum_j A_j x_j X = B from host Schur factors (same on every rank)."""
+# ---- the C-ABI engine (product path on GPUs) ----------------------------------------------------
 
-    def __init__(self, dims, us, ts, ops, group=None, singular_tol=0.0, sub_blocks=None):
+class Comm:
+    """An nds_comm handle: NCCL (one rank per GPU) or the in-process loopback (tests)."""
+
+    def __init__(self, lib, handle):
+        self.lib, self.h = lib, handle
+
+    @staticmethod
+    def nccl(device: int, group=None):
+        """NCCL communicator over the ranks of a torch.distributed group (unique id broadcast)."""
+        from . import load_library
+        lib = load_library()
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        buf = (C.c_uint8 * 128)()
+        if rank == 0 and lib.nds_comm_unique_id(buf) != 0:
+            raise RuntimeError(lib.nds_last_error(None).decode())
+        obj = [bytes(buf)]
+        dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+        uid = (C.c_uint8 * 128).from_buffer_copy(obj[0])
+        h = C.c_void_p()
+        if lib.nds_comm_create_nccl(C.byref(h), int(device), rank, world, uid) != 0:
+            raise RuntimeError(lib.nds_last_error(None).decode())
+        return Comm(lib, h)
+
+    @staticmethod
+    def loopback(world: int):
+        from . import load_library
+        lib = load_library()
+        arr = (C.c_void_p * world)()
+        if lib.nds_comm_create_loopback(int(world), arr) != 0:
+            raise RuntimeError(lib.nds_last_error(None).decode())
+        return [Comm(lib, C.c_void_p(arr[r])) for r in range(world)]
+
+    def close(self):
+        if self.h:
+            self.lib.nds_comm_destroy(self.h)
+            self.h = None
+
+
+class ShardedSolver:
+    """One rank of the sharded solve on its GPU (nds_dist_*): `solve(d_b, d_x)` with this rank's
+    L_N slabs as device pointers (or torch tensors), asynchronous on the context stream."""
+
+    def __init__(self, ctx, us, ts, comm: Comm | None = None, singular_tol=0.0):
+        from . import _dims, _ptr_array, _Singular, SingularOperatorError, NdsError, ERR_SINGULAR
+        self.ctx = ctx
+        self.dims = tuple(int(u.shape[0]) for u in us)
+        up, self._ku = _ptr_array(us)
+        tp, self._kt = _ptr_array(ts)
+        self.comm = comm
+        h = C.c_void_p()
+        sing = _Singular()
+        rc = ctx.lib.nds_dist_create(ctx.h, comm.h if comm else None, len(self.dims), _dims(self.dims), up, tp,
+                                     float(singular_tol), C.byref(h), C.byref(sing))
+        if rc == ERR_SINGULAR:
+            raise SingularOperatorError(ctx.last_error(), sing.multi_index[:sing.n_modes],
+                                        complex(sing.den_re, sing.den_im))
+        if rc:
+            raise NdsError(rc, ctx.last_error())
+        self.h = h
+
+    def slab(self, rank: int):
+        off, cnt = C.c_int64(), C.c_int64()
+        self.ctx.lib.nds_dist_slab(self.h, int(rank), C.byref(off), C.byref(cnt))
+        return off.value, cnt.value
+
+    def info(self) -> dict:
+        from . import _DistInfo
+        i = _DistInfo()
+        self.ctx.lib.nds_dist_info(self.h, C.byref(i))
+        return {k: getattr(i, k) for k, _ in _DistInfo._fields_}
+
+    def solve(self, d_b, d_x):
+        from . import NdsError
+        pb = d_b.data_ptr() if hasattr(d_b, "data_ptr") else int(d_b)
+        px = d_x.data_ptr() if hasattr(d_x, "data_ptr") else int(d_x)
+        rc = self.ctx.lib.nds_dist_solve(self.h, pb, px)
+        if rc:
+            raise NdsError(rc, self.ctx.last_error())
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.ctx.lib.nds_dist_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# ---- host mirror of the engine's schedule (gloo tests) ------------------------------------------
+
+class HostShardedSolver:
+    """The engine's schedule (sharded.cuh dist_solve_impl) on host tensors over torch.distributed,
+    with the per-rank compute supplied by `ops` (mode_product(dims, m, mode, x),
+    back_substitute(ts, dims, c, tol)). Same layout, couplings, folding and block order."""
+
+    def __init__(self, dims, us, ts, ops, group=None, singular_tol=0.0):
         self.dims = tuple(int(d) for d in dims)
         self.N = len(self.dims)
         if self.N < 2:
             raise ValueError("problem order must be at least 2")
-        self.us = [np.asfortranarray(u, dtype=np.complex128) for u in us]
-        self.ts = [np.asfortranarray(t, dtype=np.complex128) for t in ts]
-        self.uhs = [np.asfortranarray(u.conj().T) for u in self.us]
-        self.ops = ops
-        self.group = group
+        self.us = [np.asarray(u, dtype=np.complex128) for u in us]
+        self.ts = [np.asarray(t, dtype=np.complex128) for t in ts]
+        self.uhs = [u.conj().T.copy() for u in self.us]
+        self.ops, self.group = ops, group
         self.P = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
-        n1, nN = self.dims[0], self.dims[-1]
-        if n1 < self.P or nN < self.P:
-            raise ValueError("n_1 and n_N must be >= the number of ranks")
-        self.s1, self.m1 = block_partition(n1, self.P)
-        self.sN, self.mN = block_partition(nN, self.P)
-        # pipeline depth along mode N (K sub-blocks per rank)
-        k = sub_blocks if sub_blocks is not None else 4 * self.P if self.P > 1 else 1
-        self.sK, self.mK = block_partition(nN, max(1, min(int(k), nN)))
-        # sylvester.cpp:29-33 — the tolerance of the WHOLE operator, not of a slab
+        self.L = plan_layout(self.dims, self.P)
         self.tol = singular_tol if singular_tol > 0 else np.finfo(float).eps * sum(np.linalg.norm(t) for t in self.ts)
+        L, N = self.L, self.N
+        self.TH = kron_sum(self.ts[:L.h], self.dims[:L.h])
+        self.TK = kron_sum(self.ts[N - L.gp:], self.dims[N - L.gp:])
 
-    # local dims
-    def dims_LN(self, r):
-        return self.dims[:-1] + (self.mN[r],)
-
-    def dims_L1(self, q):
-        return (self.m1[q],) + self.dims[1:]
-
-    def reshard_N_to_1(self, x):
-        """x: this rank's L_N slab -> this rank's L_1 slab."""
-        r, n1 = self.rank, self.dims[0]
-        rows = x.reshape(-1, n1)  # column-major: mode 1 fastest
-        send = [rows[:, self.s1[q]:self.s1[q] + self.m1[q]].contiguous() for q in range(self.P)]
-        rest = int(np.prod(self.dims[1:-1]))
-        recv_sizes = [self.m1[r] * rest * self.mN[src] for src in range(self.P)]
-        blocks = _exchange(send, recv_sizes, self.group)
-        return torch.cat(blocks)  # mode N is the slowest index: source slabs concatenate in order
-
-    def reshard_1_to_N(self, y):
-        """y: this rank's L_1 slab -> this rank's L_N slab."""
-        r, nN = self.rank, self.dims[-1]
-        planes = y.reshape(nN, -1)  # column-major: mode N slowest
-        send = [planes[self.sN[q]:self.sN[q] + self.mN[q]].contiguous() for q in range(self.P)]
-        rest = int(np.prod(self.dims[1:-1]))
-        recv_sizes = [self.m1[src] * rest * self.mN[r] for src in range(self.P)]
-        blocks = _exchange(send, recv_sizes, self.group)
-        n1 = self.dims[0]
-        out = torch.empty(n1 * rest * self.mN[r], dtype=y.dtype, device=y.device)
-        o_rows = out.reshape(-1, n1)
-        for src, blk in enumerate(blocks):
-            o_rows[:, self.s1[src]:self.s1[src] + self.m1[src]] = blk.reshape(-1, self.m1[src])
-        return out
-
-    def solve(self, b_local):
-        """b_local: this rank's L_N slab of B. Returns this rank's L_N slab of X."""
-        ops, r, N = self.ops, self.rank, self.N
-        # 1. forward, modes 1..N-1 (local in L_N)
-        x = b_local
-        for j in range(1, N):
-            x = ops.mode_product(self.dims_LN(r), self.uhs[j - 1], j, x)
-        # 2. re-shard, 3. mode N (local in L_1)
-        c = self.reshard_N_to_1(x)
-        c = ops.mode_product(self.dims_L1(r), self.uhs[N - 1], N, c)
-        # 4. triangular solve pipelined over (rank, mode-N sub-block)
-        self.pipelined_backsub(c)
-        # 5. inverse, modes 2..N (local in L_1), 6. re-shard, 7. mode 1 (local in L_N)
-        y = c
-        for j in range(2, N + 1):
-            y = ops.mode_product(self.dims_L1(r), self.us[j - 1], j, y)
-        x = self.reshard_1_to_N(y)
-        return ops.mode_product(self.dims_LN(r), self.us[0], 1, x)
-
-    def _global(self, q):
+    def _g(self, q):
         return q if self.group is None else dist.get_global_rank(self.group, q)
 
-    def pipelined_backsub(self, c):
-        """Step 4 in place on this rank's L_1 slab c (see the module docstring)."""
-        ops, r, N, P = self.ops, self.rank, self.N, self.P
-        t1, tN = self.ts[0], self.ts[-1]
-        s1, m1 = self.s1[r], self.m1[r]
-        mid = int(np.prod(self.dims[1:-1]))
-        plane = m1 * mid  # entries per mode-N index in this rank's slab
-        pending = []  # (work, tensor): sends stay alive until the end
-        for k in reversed(range(len(self.mK))):
-            sk, mk = self.sK[k], self.mK[k]
-            blk = c[sk * plane:(sk + mk) * plane]
-            # mode-1 couplings from every higher rank's block k
-            for q in range(P - 1, r, -1):
-                yq = torch.empty(self.m1[q] * mid * mk, dtype=c.dtype, device=c.device)
-                yr = torch.view_as_real(yq)
-                dist.recv(yr, src=self._global(q), group=self.group)
-                m = -np.asfortranarray(t1[s1:s1 + m1, self.s1[q]:self.s1[q] + self.m1[q]])
-                ops.mode_update((self.m1[q],) + self.dims[1:-1] + (mk,), 1, m, yq, blk)
-            # local solve: T_1 and T_N restricted to their diagonal blocks
-            ts_local = [np.asfortranarray(t1[s1:s1 + m1, s1:s1 + m1])] + self.ts[1:-1] + \
-                       [np.asfortranarray(tN[sk:sk + mk, sk:sk + mk])]
-            ops.back_substitute(ts_local, (m1,) + self.dims[1:-1] + (mk,), blk, self.tol)
-            # forward the solved block to every lower rank (point-to-point, non-blocking)
-            if r > 0:
-                ops.synchronize()
-                br = torch.view_as_real(blk)
-                for q in range(r - 1, -1, -1):
-                    pending.append((dist.isend(br, dst=self._global(q), group=self.group), br))
-            # mode-N couplings of this block into the lower sub-blocks of this rank
-            if sk > 0:
-                m = -np.asfortranarray(tN[:sk, sk:sk + mk])
-                ops.mode_update((m1,) + self.dims[1:-1] + (mk,), N, m, blk, c[:sk * plane])
-        for w, _ in pending:
+    def _apply(self, d, lo, hi, adjoint, x):
+        for j in range(lo, hi + 1):
+            x = self.ops.mode_product(d, self.uhs[j - 1] if adjoint else self.us[j - 1], j, x)
+        return x
+
+    def _exchange(self, send, recv):
+        """send/recv: per peer flat complex tensors (views into contiguous buffers)."""
+        ops = []
+        for r in range(self.P):
+            if r == self.rank:
+                continue
+            if send[r].numel():
+                ops.append(dist.P2POp(dist.isend, torch.view_as_real(send[r]).contiguous(), self._g(r), self.group))
+            if recv[r].numel():
+                ops.append(dist.P2POp(dist.irecv, recv[r], self._g(r), self.group))
+        bufs = [op.tensor for op in ops if op.op is dist.irecv]
+        for w in dist.batch_isend_irecv(ops) if ops else []:
             w.wait()
+        return bufs
+
+    def solve(self, b_local):
+        L, q, N, P = self.L, self.rank, self.N, self.P
+        lnd, l1d = L.ln_dims(q), L.l1_dims(q)
+        Mg, Mp = L.mid(N - L.g), L.mid(N - L.gp)
+        x = self._apply(lnd, 1, N - L.g, True, b_local)
+        # L_N -> L_1: pack rows [sH_r, sH_r + mH_r) of the head index for rank r
+        nH = int(np.prod(self.dims[:L.h]))
+        rows = x.reshape(-1, nH)
+        send = [rows[:, L.sH[r]:L.sH[r] + L.mH[r]].reshape(-1).contiguous() for r in range(P)]
+        l1 = torch.empty(int(np.prod(l1d)), dtype=torch.complex128)
+        plane_g = L.mH[q] * Mg
+        recv = [torch.empty(2 * L.mH[q] * Mg * L.mG[r], dtype=torch.float64) for r in range(P)]
+        self._exchange(send, recv)
+        for r in range(P):
+            piece = send[q] if r == q else torch.view_as_complex(recv[r].reshape(-1, 2))
+            l1[L.sG[r] * plane_g:(L.sG[r] + L.mG[r]) * plane_g] = piece
+        c = self._apply(l1d, N - L.g + 1, N, True, l1)
+        self._pipelined_backsub(c, Mp)
+        y = self._apply(l1d, L.h + 1, N, False, c)
+        # L_1 -> L_N
+        send = [y[L.sG[r] * plane_g:(L.sG[r] + L.mG[r]) * plane_g].contiguous() for r in range(P)]
+        recv = [torch.empty(2 * L.mH[r] * Mg * L.mG[q], dtype=torch.float64) for r in range(P)]
+        self._exchange(send, recv)
+        out = torch.empty(int(np.prod(lnd)), dtype=torch.complex128)
+        o_rows = out.reshape(-1, nH)
+        for r in range(P):
+            piece = send[q] if r == q else torch.view_as_complex(recv[r].reshape(-1, 2))
+            o_rows[:, L.sH[r]:L.sH[r] + L.mH[r]] = piece.reshape(-1, L.mH[r])
+        return self._apply(lnd, 1, L.h, False, out)
+
+    def _local_ts(self, k):
+        """T blocks of block k's local solve, extent-1 modes folded into the first other mode."""
+        L, q, N = self.L, self.rank, self.N
+        ext, tb = [], []
+        for j in range(N):
+            n, s0, m = self.dims[j], 0, self.dims[j]
+            if j < L.h:
+                s0, m = (L.sH[q], L.mH[q]) if L.h == 1 else ((L.sH[q] // int(np.prod(self.dims[:j]))) % n, 1)
+            elif j >= N - L.gp:
+                s0, m = (L.sK[k], L.mK[k]) if L.gp == 1 else \
+                    ((L.sK[k] // int(np.prod(self.dims[N - L.gp:j]))) % n, 1)
+            ext.append(m)
+            tb.append(self.ts[j][s0:s0 + m, s0:s0 + m])
+        keep = [j for j in range(N) if ext[j] > 1]
+        fold = sum(tb[j][0, 0] for j in range(N) if ext[j] == 1)
+        if not keep:
+            return (1,), [np.array([[fold]])]
+        lt = [np.array(tb[j], dtype=np.complex128) for j in keep]
+        lt[0] = lt[0] + fold * np.eye(ext[keep[0]])
+        return tuple(ext[j] for j in keep), lt
+
+    def _pipelined_backsub(self, c, Mp):
+        L, q, P = self.L, self.rank, self.P
+        plane = L.mH[q] * Mp
+        higher = [qp for qp in range(P - 1, q, -1) if L.couples(q, qp)]
+        lower = [qq for qq in range(q - 1, -1, -1) if L.couples(qq, q)]
+        K = len(L.sK)
+        for k in reversed(range(K)):
+            blk = c[L.sK[k] * plane:(L.sK[k] + L.mK[k]) * plane]
+            recv = []
+            for qp in higher:
+                t = torch.empty(2 * L.mH[qp] * Mp * L.mK[k], dtype=torch.float64)
+                recv.append(dist.P2POp(dist.irecv, t, self._g(qp), self.group))
+            for w in dist.batch_isend_irecv(recv) if recv else []:
+                w.wait()
+            for qp, op in zip(higher, recv):
+                y = torch.view_as_complex(op.tensor.reshape(-1, 2))
+                m = -self.TH[L.sH[q]:L.sH[q] + L.mH[q], L.sH[qp]:L.sH[qp] + L.mH[qp]]
+                blk += self.ops.mode_product((L.mH[qp], Mp * L.mK[k]), m, 1, y)
+            ldims, lts = self._local_ts(k)
+            self.ops.back_substitute(lts, ldims, blk, self.tol)
+            sends = [dist.P2POp(dist.isend, torch.view_as_real(blk).contiguous(), self._g(qq), self.group)
+                     for qq in lower]
+            for w in dist.batch_isend_irecv(sends) if sends else []:
+                w.wait()
+            if k > 0:  # pipe couplings into the lower blocks of this rank
+                m = -self.TK[:L.sK[k], L.sK[k]:L.sK[k] + L.mK[k]]
+                c[:L.sK[k] * plane] += self.ops.mode_product((plane, L.mK[k]), m, 2, blk)
 
 
 def scatter_LN(b, P):
     """Split a full column-major tensor (numpy, shape dims) into the L_N slabs (host helper)."""
-    nN = b.shape[-1]
-    s, m = block_partition(nN, P)
+    L = plan_layout(b.shape, P)
     flat = np.asfortranarray(b).reshape(-1, order="F")
-    plane = int(np.prod(b.shape[:-1]))
-    return [flat[s[r] * plane:(s[r] + m[r]) * plane].copy() for r in range(P)]
+    return [flat[o:o + n].copy() for o, n in (L.slab(r) for r in range(P))]
 
 
 def gather_LN(slabs, dims):
