@@ -299,6 +299,7 @@ struct nds_dist {
   std::vector<Mat> head_up;                // by source rank q' (> rank, nonzero coupling)
   std::vector<std::vector<std::pair<int64_t, Mat>>> pipe_up;  // by block k: (first target block or -1 = all lower, matrix)
   std::vector<std::unique_ptr<nds_plan>> local;  // by block k: T blocks of the local solve
+  std::unique_ptr<nds_plan> whole;                // one rank: the single-GPU plan path
   double2* mats = nullptr;
   double2 *ln = nullptr, *l1 = nullptr, *work = nullptr, *xbuf = nullptr, *pipe_buf[2] = {nullptr, nullptr};
   int64_t ln_size = 0, l1_size = 0, pipe_size = 0;
@@ -396,6 +397,7 @@ void dist_free(nds_dist* d) {
   if (d->cs) cudaStreamSynchronize(d->cs);
   for (auto& p : d->local) plan_destroy_impl(p.release());
   d->local.clear();
+  if (d->whole) plan_destroy_impl(d->whole.release());
   free_factors(d->f);
   for (double2* b : {d->mats, d->ln, d->l1, d->work, d->xbuf, d->pipe_buf[0]})
     if (b) cudaFree(b);
@@ -436,12 +438,12 @@ void choose_groups(nds_dist& d) {
       K = d.nK;
     } else {
       const int64_t edge = N == 3 ? 16 : 8;
-      for (int64_t c = std::min<int64_t>(4 * P, d.nK); c >= 1; --c)
+      for (int64_t c = std::min<int64_t>(4 * P, d.nK); c >= 2; --c)
         if (d.nK % c == 0 && (d.nK / c) % edge == 0) {
           K = c;
           break;
         }
-      if (K == 1) K = std::min<int64_t>(2 * P, d.nK);
+      if (K == 1) K = std::min<int64_t>(2 * P, d.nK);  // no whole-tile blocking: pipeline anyway
     }
   }
   block_partition(d.nK, (int)K, d.sK, d.mK);
@@ -472,6 +474,18 @@ void dist_create_impl(nds_dist* d, const nds_z* const* u, const nds_z* const* t,
   nds_ctx* ctx = d->ctx;
   const int N = d->N;
   choose_groups(*d);
+  if (d->P == 1) {  // one rank: the plan path (head / tail overlap, fused passes), no layouts
+    nds_plan* p = nullptr;
+    plan_create_impl(ctx, N, d->dims, u, t, singular_tol, 0u, &p, sing);
+    d->whole.reset(p);
+    d->tol = p->tol;
+    d->min_abs_den = p->min_abs_den;
+    int64_t total = 1;
+    for (int j = 0; j < N; ++j) total *= d->dims[j];
+    d->ln_size = d->l1_size = total;
+    NDS_CUDA(cudaMalloc(&d->work, (size_t)total * sizeof(double2)));
+    return;
+  }
   // the whole operator's factors; one singular check of the WHOLE operator on every rank
   // (sylvester.cpp:101-103), so all ranks raise the same first offender before any exchange
   d->tol = singular_tol > 0.0 ? singular_tol : default_tol(N, d->dims, t);
@@ -650,6 +664,10 @@ void dist_create_impl(nds_dist* d, const nds_z* const* u, const nds_z* const* t,
 
 int dist_solve_impl(nds_dist* d, const double2* b, double2* x) {
   nds_ctx* ctx = d->ctx;
+  if (d->whole) {
+    d->launches = execute(d->whole.get(), b, x, d->work, nullptr);
+    return d->launches;
+  }
   const int N = d->N, q = d->rank, P = d->P;
   const int K = (int)d->sK.size();
   cudaStream_t s = ctx->stream, cs = d->cs;
@@ -884,6 +902,7 @@ int nds_dist_info(const nds_dist* d, nds_dist_info_t* info) {
   info->pipe_blocks = (int)d->sK.size();
   info->local_solve_path = -1;
   if (!d->local.empty()) info->local_solve_path = nds_plan_solve_path(d->local[0].get());
+  if (d->whole) info->local_solve_path = nds_plan_solve_path(d->whole.get());
   info->alltoall_bytes = d->bytes_alltoall;
   int64_t Mp = 1;
   for (int j = d->h; j < d->N - d->gp; ++j) Mp *= d->dims[j];

@@ -120,8 +120,8 @@ def plan_layout(dims, P) -> Layout:
             K = nK
         else:
             edge = 16 if N == 3 else 8
-            K = next((c for c in range(min(4 * P, nK), 0, -1) if nK % c == 0 and (nK // c) % edge == 0), 0)
-            if K == 0:
+            K = next((c for c in range(min(4 * P, nK), 1, -1) if nK % c == 0 and (nK // c) % edge == 0), 1)
+            if K == 1:  # no whole-tile blocking: pipeline anyway
                 K = min(2 * P, nK)
     L.sK, L.mK = block_partition(nK, K)
     return L
