@@ -40,6 +40,23 @@ struct nds_ctx {
   cudaEvent_t tev[65] = {};
   std::map<std::vector<int64_t>, std::shared_ptr<nds::SolverCache>> solvers;  // by extents
   cudaMemPool_t pool = nullptr;  // private stream-ordered pool (factor sets, small matrices)
+  // pinned ring for PAGEABLE host tensors (std::vector storage): host copies into a slot overlap
+  // the DMA of the previous slot; deferred device->host copies drain slot by slot
+  char* ring = nullptr;
+  cudaEvent_t ring_ev[8] = {};
+  struct RingOut {
+    void* host = nullptr;
+    size_t bytes = 0;
+  } ring_out[8];
+  int ring_next = 0;
+  struct D2H {
+    void* host;
+    const void* dev;
+    size_t bytes;
+    cudaEvent_t ready;
+  };
+  std::vector<D2H> d2h_deferred;
+  cudaEvent_t d2h_ev[64] = {};
 };
 
 struct nds_plan {
@@ -134,6 +151,97 @@ void ensure_ws3(nds_ctx* ctx, int64_t total) {
   ctx->ws3_bytes = 0;
   NDS_CUDA(cudaMalloc(&ctx->ws[2], bytes));
   ctx->ws3_bytes = bytes;
+}
+
+// ---- host <-> device copies of pageable tensors (pinned staging ring) -----------------------
+constexpr size_t kRingSlot = 16u << 20;
+constexpr int kRingSlots = 8;
+
+bool host_pageable(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return a.type == cudaMemoryTypeUnregistered;
+}
+
+void par_memcpy(void* dst, const void* src, size_t bytes) {
+  constexpr size_t kPiece = 1u << 20;
+  const int64_t pieces = (int64_t)((bytes + kPiece - 1) / kPiece);
+#pragma omp parallel for schedule(static) if (pieces > 1)
+  for (int64_t i = 0; i < pieces; ++i) {
+    const size_t o = (size_t)i * kPiece;
+    std::memcpy((char*)dst + o, (const char*)src + o, std::min(kPiece, bytes - o));
+  }
+}
+
+void ensure_ring(nds_ctx* ctx) {
+  if (ctx->ring) return;
+  NDS_CUDA(cudaHostAlloc((void**)&ctx->ring, kRingSlot * kRingSlots, cudaHostAllocDefault));
+  for (auto& e : ctx->ring_ev) NDS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  for (auto& e : ctx->d2h_ev) NDS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+}
+
+// Take the next ring slot: wait for its last DMA and finish its pending copy-out.
+char* ring_slot(nds_ctx* ctx, int& slot) {
+  slot = ctx->ring_next++ % kRingSlots;
+  NDS_CUDA(cudaEventSynchronize(ctx->ring_ev[slot]));
+  auto& o = ctx->ring_out[slot];
+  if (o.host) {
+    par_memcpy(o.host, ctx->ring + (size_t)slot * kRingSlot, o.bytes);
+    o = {};
+  }
+  return ctx->ring + (size_t)slot * kRingSlot;
+}
+
+// Host -> device on stream s; pageable sources are staged (blocks the host for the copy-in).
+void copy_h2d(nds_ctx* ctx, void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  if (!host_pageable(src)) {
+    NDS_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+    return;
+  }
+  ensure_ring(ctx);
+  for (size_t o = 0; o < bytes; o += kRingSlot) {
+    const size_t n = std::min(kRingSlot, bytes - o);
+    int slot;
+    char* r = ring_slot(ctx, slot);
+    par_memcpy(r, (const char*)src + o, n);
+    NDS_CUDA(cudaMemcpyAsync((char*)dst + o, r, n, cudaMemcpyHostToDevice, s));
+    NDS_CUDA(cudaEventRecord(ctx->ring_ev[slot], s));
+  }
+}
+
+// Device -> host after `ready` (recorded on the producing stream): pinned destinations are
+// copied at once on stream s; pageable ones are deferred to d2h_drain, called after all device
+// work of the call is queued (the host then copies out slot by slot behind the DMAs).
+void copy_d2h(nds_ctx* ctx, void* dst, const void* src, size_t bytes, cudaStream_t s, cudaEvent_t ready) {
+  if (!host_pageable(dst)) {
+    if (ready) NDS_CUDA(cudaStreamWaitEvent(s, ready, 0));
+    NDS_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
+    return;
+  }
+  ensure_ring(ctx);
+  ctx->d2h_deferred.push_back({dst, src, bytes, ready});
+}
+
+void d2h_drain(nds_ctx* ctx, cudaStream_t s) {
+  for (const auto& r : ctx->d2h_deferred) {
+    if (r.ready) NDS_CUDA(cudaStreamWaitEvent(s, r.ready, 0));
+    for (size_t o = 0; o < r.bytes; o += kRingSlot) {
+      const size_t n = std::min(kRingSlot, r.bytes - o);
+      int slot;
+      char* buf = ring_slot(ctx, slot);
+      NDS_CUDA(cudaMemcpyAsync(buf, (const char*)r.dev + o, n, cudaMemcpyDeviceToHost, s));
+      NDS_CUDA(cudaEventRecord(ctx->ring_ev[slot], s));
+      ctx->ring_out[slot] = {(char*)r.host + o, n};
+    }
+  }
+  ctx->d2h_deferred.clear();
+  for (int i = 0; i < kRingSlots; ++i) {  // the remaining copy-outs, oldest first
+    int slot;
+    ring_slot(ctx, slot);
+  }
 }
 
 // Build the device factor set: U_j in four layouts, T_j, diag(T_j). u may be null (t-only) or
@@ -603,8 +711,7 @@ void prefetch_chunks(nds_ctx* ctx, const nds_z* hb, int64_t total, int K, int co
   NDS_CUDA(cudaEventRecord(ctx->ev[4], ctx->stream));
   NDS_CUDA(cudaStreamWaitEvent(ctx->copy, ctx->ev[4], 0));
   for (int k = 0; k < count; ++k) {
-    NDS_CUDA(cudaMemcpyAsync(ctx->ws[0] + k * chunk, hb + k * chunk, (size_t)chunk * sizeof(double2),
-                             cudaMemcpyHostToDevice, ctx->copy));
+    copy_h2d(ctx, ctx->ws[0] + k * chunk, hb + k * chunk, (size_t)chunk * sizeof(double2), ctx->copy);
     NDS_CUDA(cudaEventRecord(ctx->cev[k], ctx->copy));
   }
 }
@@ -624,9 +731,10 @@ void execute_host_impl(nds_plan* p, const nds_z* hb, nds_z* hx, nds_report* rep,
   int launches = 0;
   if (K == 1) {
     NDS_CUDA(cudaEventRecord(ctx->ev[4], s));
-    NDS_CUDA(cudaMemcpyAsync(X, hb, bytes, cudaMemcpyHostToDevice, s));
+    copy_h2d(ctx, X, hb, bytes, s);
     launches = execute(p, X, X, W, ctx->ev);
-    NDS_CUDA(cudaMemcpyAsync(hx, X, bytes, cudaMemcpyDeviceToHost, s));
+    copy_d2h(ctx, hx, X, bytes, s, nullptr);
+    d2h_drain(ctx, s);
     NDS_CUDA(cudaEventRecord(ctx->ev[5], s));
   } else {
     cudaStream_t cs = ctx->copy;
@@ -636,11 +744,19 @@ void execute_host_impl(nds_plan* p, const nds_z* hb, nds_z* hx, nds_report* rep,
       NDS_CUDA(cudaEventRecord(ctx->ev[4], s));
       NDS_CUDA(cudaStreamWaitEvent(cs, ctx->ev[4], 0));
     }
-    for (int k = prefetched; k < K; ++k) {
-      NDS_CUDA(cudaMemcpyAsync(X + k * chunk, hb + k * chunk, cbytes, cudaMemcpyHostToDevice, cs));
+    // pinned B: every chunk's H2D is queued up front; pageable B: each chunk is staged through the
+    // pinned ring just before its passes are queued, so the host copy-in of chunk k + 1 overlaps
+    // the DMA and the passes of chunk k
+    const bool staged_in = host_pageable(hb);
+    auto land = [&](int k) {
+      if (k < prefetched) return;
+      copy_h2d(ctx, X + k * chunk, hb + k * chunk, cbytes, cs);
       NDS_CUDA(cudaEventRecord(ctx->cev[k], cs));
-    }
-    NDS_CUDA(cudaEventRecord(ctx->ev[6], cs));
+      if (k == K - 1) NDS_CUDA(cudaEventRecord(ctx->ev[6], cs));
+    };
+    if (!staged_in)
+      for (int k = 0; k < K; ++k) land(k);
+    if (prefetched >= K) NDS_CUDA(cudaEventRecord(ctx->ev[6], cs));
     // Last pass per chunk too when it is a row-major GEMM whose chunk slab is >= 16 wide:
     // forward as C += U^H[:, slab_k] x_N X_k (K-split, chunks accumulate in order into a third
     // buffer), inverse as X_k = U[slab_k, :] x_N Y (row block). Then only one chunk's worth of
@@ -656,6 +772,7 @@ void execute_host_impl(nds_plan* p, const nds_z* hb, nds_z* hx, nds_report* rep,
       const int n = (int)lv.n;
       auto chunk_buf = [&](int pass) { return (pass % 2 == 1) ? S3 : X; };  // per-chunk ping-pong
       for (int k = 0; k < K; ++k) {  // forward: passes 1 .. np-1, then the slab's share of pass np
+        if (staged_in) land(k);
         NDS_CUDA(cudaStreamWaitEvent(s, ctx->cev[k], 0));
         const double2* src = X + k * chunk;
         for (int j = 1; j < np; ++j) {
@@ -689,12 +806,12 @@ void execute_host_impl(nds_plan* p, const nds_z* hb, nds_z* hx, nds_report* rep,
         }
         if (p->flags & NDS_REAL_OUTPUT) launches += nds::real_part_launch(X + k * chunk, chunk, s);
         NDS_CUDA(cudaEventRecord(ctx->cev[8 + k], s));
-        NDS_CUDA(cudaStreamWaitEvent(cs, ctx->cev[8 + k], 0));
-        NDS_CUDA(cudaMemcpyAsync(hx + k * chunk, X + k * chunk, cbytes, cudaMemcpyDeviceToHost, cs));
+        copy_d2h(ctx, hx + k * chunk, X + k * chunk, cbytes, cs, ctx->cev[8 + k]);
       }
     } else {
       auto dst_of = [&](int pass) { return (pass % 2 == 1) ? W : X; };  // pass 1..2 np; input in X
       for (int k = 0; k < K; ++k) {  // forward: passes 1 .. np-1 per chunk as it lands
+        if (staged_in) land(k);
         NDS_CUDA(cudaStreamWaitEvent(s, ctx->cev[k], 0));
         const double2* src = X + k * chunk;
         for (int j = 1; j < np; ++j) {
@@ -723,11 +840,11 @@ void execute_host_impl(nds_plan* p, const nds_z* hb, nds_z* hx, nds_report* rep,
         }
         if (p->flags & NDS_REAL_OUTPUT) launches += nds::real_part_launch(X + k * chunk, chunk, s);
         NDS_CUDA(cudaEventRecord(ctx->cev[8 + k], s));
-        NDS_CUDA(cudaStreamWaitEvent(cs, ctx->cev[8 + k], 0));
-        NDS_CUDA(cudaMemcpyAsync(hx + k * chunk, X + k * chunk, cbytes, cudaMemcpyDeviceToHost, cs));
+        copy_d2h(ctx, hx + k * chunk, X + k * chunk, cbytes, cs, ctx->cev[8 + k]);
       }
     }
     NDS_CUDA(cudaEventRecord(ctx->ev[3], s));
+    d2h_drain(ctx, cs);
     NDS_CUDA(cudaEventRecord(ctx->ev[5], cs));
     NDS_CUDA(cudaStreamWaitEvent(s, ctx->ev[5], 0));
   }
@@ -1171,6 +1288,11 @@ void nds_ctx_destroy(nds_ctx* ctx) {
     if (e) cudaEventDestroy(e);
   if (ctx->own) cudaStreamDestroy(ctx->own);
   if (ctx->pool) cudaMemPoolDestroy(ctx->pool);
+  if (ctx->ring) cudaFreeHost(ctx->ring);
+  for (auto& e : ctx->ring_ev)
+    if (e) cudaEventDestroy(e);
+  for (auto& e : ctx->d2h_ev)
+    if (e) cudaEventDestroy(e);
   delete ctx;
 }
 

@@ -251,3 +251,35 @@ def test_host_path_with_copy_overlap(ctx, port, dims):
     assert rel_max(r.x, x_ref) <= 1e-11
     r2 = ctx.solve_schur(us, ts, b, allow_fast_path=False, real_output=True)
     assert np.all(r2.x.imag == 0) and rel_max(r2.x.real, x_ref.real) <= 1e-11
+
+
+@pytest.mark.parametrize("dims", [(48, 40, 64), (40, 3, 1024), (2,) * 20, (24, 20, 16)],
+                         ids=["48x40x64", "40x3x1024", "bin20", "24x20x16"])
+def test_host_path_pageable_equals_pinned(ctx, dims):
+    """nds_solve_schur from PAGEABLE host buffers (the reference's std::vector storage, staged
+    through the library's pinned ring) and from pinned buffers: bitwise the same X."""
+    import ctypes as C
+    import torch
+    rng = np.random.default_rng(29)
+    us, ts = rand_factors(rng, dims)
+    b = np.asfortranarray(rand_c(rng, dims))
+    flat = np.ascontiguousarray(b.reshape(-1, order="F"))
+    outs = []
+    for pinned in (False, True):
+        if pinned:
+            hb = torch.from_numpy(flat.copy()).pin_memory()
+            hx = torch.empty_like(hb).pin_memory()
+            pb, px = hb.data_ptr(), hx.data_ptr()
+        else:
+            hb, hx = flat.copy(), np.empty_like(flat)
+            pb, px = hb.ctypes.data, hx.ctypes.data
+        up, ku = nds._ptr_array(us)
+        tp, kt = nds._ptr_array(ts)
+        rep, sing = nds._Report(), nds._Singular()
+        rc = ctx.lib.nds_solve_schur(ctx.h, len(dims), nds._dims(dims), up, tp, pb, px, 0.0, 0, C.byref(rep),
+                                     C.byref(sing))
+        assert rc == 0, ctx.last_error()
+        outs.append(hx.numpy().copy() if pinned else hx.copy())
+    assert np.array_equal(outs[0], outs[1])
+    x_ref, _ = oracle.Port().solve_schur(us, ts, b, flags=0)
+    assert rel_max(outs[0].reshape(dims, order="F"), x_ref) <= 1e-11
