@@ -261,6 +261,9 @@ void upload_factors(nds_ctx* ctx, nds::FactorSet& f, int n_modes, const int64_t*
   const int64_t n_t = t ? sq : 0;
   const int64_t n_d = t ? diag : 0;
   const int64_t n_raw = u ? sq : 0;
+  int64_t n_blk = 0;
+  if (u)
+    for (int j = 0; j < n_modes; ++j) n_blk += nds::blocked_entries(dims[j]);
   const size_t stage_bytes = (size_t)(n_raw + n_t + n_d) * sizeof(double2);
   NDS_CUDA(cudaStreamSynchronize(ctx->stream));  // the staging buffer may still feed a previous copy
   if (ctx->stage_bytes < stage_bytes) {
@@ -270,8 +273,8 @@ void upload_factors(nds_ctx* ctx, nds::FactorSet& f, int n_modes, const int64_t*
     NDS_CUDA(cudaHostAlloc(&ctx->stage, stage_bytes, cudaHostAllocDefault));
     ctx->stage_bytes = stage_bytes;
   }
-  NDS_CUDA(cudaMallocFromPoolAsync(&f.pool, (size_t)(n_u + n_t + n_d + n_raw + 1) * sizeof(double2), ctx->pool,
-                                   ctx->stream));
+  NDS_CUDA(cudaMallocFromPoolAsync(&f.pool, (size_t)(n_u + n_t + n_d + n_raw + n_blk + 1) * sizeof(double2),
+                                   ctx->pool, ctx->stream));
   f.stream = ctx->stream;
   double2* stage = (double2*)ctx->stage;
   nds::Geom& g = f.geom;
@@ -330,6 +333,7 @@ void upload_factors(nds_ctx* ctx, nds::FactorSet& f, int n_modes, const int64_t*
   if (u) {
     NDS_CUDA(cudaMemcpyAsync(raw, stage, (size_t)sq * sizeof(double2), cudaMemcpyHostToDevice, ctx->stream));
     nds::factor_layouts_launch(f, raw, ctx->stream);
+    if (n_blk) nds::blocked_layouts_launch(f, raw + n_raw, ctx->stream);
   }
 }
 

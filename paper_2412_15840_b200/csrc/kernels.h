@@ -20,6 +20,13 @@ struct FactorSet {
   double2* u_col[NDS_MAX_MODES] = {};
   double2* uh_row[NDS_MAX_MODES] = {};
   double2* uh_col[NDS_MAX_MODES] = {};
+  // Stage-blocked copies for the bulk-copy (TMA) fed transform GEMM, modes with n_j a multiple of
+  // 16: per op (0: U, 1: U^H) and CTA shape (0: 64 x 32, 1: 32 x 64), the A operand of the
+  // row-major GEMM as [row tile][k tile][BM rows][BK + 4] and the B operand of the mode-1 GEMM
+  // as [column tile][k tile][BK][BN + 2] — the padded shared-memory stage images, so one
+  // cp.async.bulk moves a whole operand stage (transform.cu).
+  double2* ablk[NDS_MAX_MODES][2][2] = {};
+  double2* bblk[NDS_MAX_MODES][2][2] = {};
   double2* pool = nullptr;  // one allocation backing all of the above + T + diag
   cudaStream_t stream = nullptr;  // stream the pool was allocated on (stream-ordered free)
   double2* t_pool = nullptr;     // T_j column-major, concatenated (offsets in geom.toff)
@@ -66,9 +73,10 @@ int binary_pass_launch(const FactorSet& f, const BinGroup& gr, bool adjoint, con
 // rows_out > 0: rectangular M (rows_out x n), r has extent rows_out along the mode.
 // lda_row > 0: m_row is a column block of a wider row-major matrix (row stride lda_row); only
 // valid on the GEMM path with inner >= 8 (the caller checks gemm_rowm_ok).
+// blk: the two stage-blocked images of M for the bulk-copy GEMM (FactorSet::ablk / bblk), or null.
 int mode_product_matrix_launch(const double2* m_row, const double2* m_col, const ModeView& v, const double2* x,
                                double2* r, bool accumulate, cudaStream_t stream, int64_t rows_out = -1,
-                               int64_t lda_row = -1);
+                               int64_t lda_row = -1, const double2* const* blk = nullptr);
 inline bool gemm_rowm_ok(const ModeView& v) { return v.n >= 16 && v.inner >= 8; }
 
 // ---- triangular solve --------------------------------------------------------------------
@@ -187,6 +195,10 @@ int parlett_launch(const ExpArgs& a, int count, cudaStream_t stream);
 // ---- elementwise / reductions ------------------------------------------------------------
 // Build u_row / u_col / uh_row / uh_col of every mode from the raw column-major U_j (concatenated).
 void factor_layouts_launch(const FactorSet& f, const double2* raw, cudaStream_t stream);
+// Entries of the stage-blocked operand images of one n x n factor (0 when n is not a multiple
+// of 16), and their construction from u_row / u_col / uh_row / uh_col (transform.cu).
+int64_t blocked_entries(int64_t n);
+void blocked_layouts_launch(FactorSet& f, double2* base, cudaStream_t stream);
 // min |den| over all entries and the largest flat index with |den| <= tol (-1 if none).
 void den_scan(const Geom& g, const double2* diag, double tol, double* min_abs, int64_t* max_bad, cudaStream_t stream,
               void* scratch /* >= 16 bytes device */);

@@ -59,6 +59,11 @@ struct GemmArgs {
   int64_t alim, blim;
   int64_t ntile_rows, ntile_a;
   int accumulate;
+  // bulk-copy (TMA) path: stage-blocked image of the constant operand (ROWM: A, COLM: B) for the
+  // chosen CTA shape, or null; colm = the mode-1 form (A = the tensor, B = M^T)
+  const double2* blk;
+  const double2* blk_shape[2];
+  int colm;
 };
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
@@ -240,6 +245,185 @@ __global__ void __launch_bounds__(WM* WN * 32, MINB) zgemm_dmma_kernel(const Gem
   }
 }
 
+// ------------------------------------------------------------------------------------------
+// The same GEMM fed by bulk asynchronous copies (TMA engine, cp.async.bulk) into an mbarrier
+// ring: per stage ONE copy of the constant operand's stage image (FactorSet::ablk / bblk: the
+// padded, bank-conflict-free layout precomputed per factor) plus one copy per contiguous run of
+// the tensor operand (ROWM: BK rows of W entries per column group; COLM: BM rows of BK entries).
+// Warp 0 is also the producer: at the top of k-tile kt its lanes refill the stage k-tile kt - 1
+// used (after every warp released it on the stage's empty barrier), so each stage is in flight
+// for STAGES - 1 k-tiles; consumers wait on the stage's full barrier (expect-tx byte count) —
+// no per-thread cp.async address work and no CTA-wide barrier per stage. Needs K % BK == 0 and
+// whole column groups (inner % W == 0); other GEMMs take zgemm_dmma_kernel.
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  unsigned done = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, int MINB>
+__global__ void __launch_bounds__(WM* WN * 32, MINB) zgemm_tma_kernel(const GemmArgs g, int colm) {
+  using Cfg = GemmCfg<BM, BN, BK, WM, WN, STAGES>;
+  constexpr int NW = WM * WN;
+  constexpr int MI = Cfg::MI, NI = Cfg::NI;
+  extern __shared__ __align__(16) double2 smem[];
+  double2* sA = smem;
+  double2* sB = smem + STAGES * Cfg::kStageA;
+  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int wy = warp / WN, wx = warp % WN;
+  const int64_t tile = blockIdx.x;
+  const int64_t row_tile = tile % g.ntile_rows;
+  const int64_t col_tile = tile / g.ntile_rows;
+  const int64_t row0 = row_tile * BM;
+  const int64_t a0 = (col_tile % g.ntile_a) << g.wshift;
+  const int64_t b0 = (col_tile / g.ntile_a) * (BN >> g.wshift);
+  const int W = 1 << g.wshift;
+  const int groups = BN >> g.wshift;
+  const int nk = g.K / BK;
+  // valid rows (COLM A) / column groups (ROWM B) of this tile; the rest stays zero in every stage
+  const int vrows = colm ? (int)(g.rows - row0 < BM ? g.rows - row0 : BM) : BM;
+  const int vgroups = colm ? groups : (int)(g.blim - b0 < groups ? g.blim - b0 : groups);
+  if (colm) {
+    for (int e = tid; e < STAGES * (BM - vrows) * Cfg::kLdA; e += blockDim.x) {
+      const int st = e / ((BM - vrows) * Cfg::kLdA), rem = e % ((BM - vrows) * Cfg::kLdA);
+      sA[st * Cfg::kStageA + vrows * Cfg::kLdA + rem] = make_double2(0.0, 0.0);
+    }
+  } else if (vgroups < groups) {
+    for (int e = tid; e < STAGES * BK * BN; e += blockDim.x) {
+      const int st = e / (BK * BN), k = (e / BN) % BK, c = e % BN;
+      if ((c >> g.wshift) >= vgroups) sB[st * Cfg::kStageB + k * Cfg::kLdB + c] = make_double2(0.0, 0.0);
+    }
+  }
+  if (tid == 0) {
+    for (int s2 = 0; s2 < STAGES; ++s2) {
+      mbar_init(&full[s2], 1);
+      mbar_init(&empty[s2], NW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  const unsigned stage_bytes =
+      colm ? (unsigned)(vrows * BK * 16 + Cfg::kStageB * 16) : (unsigned)(Cfg::kStageA * 16 + vgroups * BK * W * 16);
+  const int64_t ct = col_tile % g.ntile_a;  // COLM: column tile of B
+  // warp 0: fill stage st with k-tile kt (lane 0 arms the barrier, the lanes issue the copies)
+  auto produce = [&](int st, int kt) {
+    if (lane == 0) mbar_expect_tx(&full[st], stage_bytes);
+    __syncwarp();
+    double2* dA = sA + st * Cfg::kStageA;
+    double2* dB = sB + st * Cfg::kStageB;
+    const int k0 = kt * BK;
+    if (colm) {
+      if (lane == 0) bulk_g2s(dB, g.blk + ((ct * nk + kt) * BK) * Cfg::kLdB, Cfg::kStageB * 16, &full[st]);
+      for (int r = lane; r < vrows; r += 32)
+        bulk_g2s(dA + r * Cfg::kLdA, g.A + (row0 + r) * g.lda + k0, BK * 16, &full[st]);
+    } else {
+      if (lane == 0) bulk_g2s(dA, g.blk + ((row_tile * nk + kt) * BM) * Cfg::kLdA, Cfg::kStageA * 16, &full[st]);
+      for (int e = lane; e < BK * vgroups; e += 32) {
+        const int k = e / vgroups, q = e % vgroups;
+        bulk_g2s(dB + k * Cfg::kLdB + q * W, g.B + (int64_t)(k0 + k) * g.ldbk + a0 + (b0 + q) * g.ldbb, W * 16,
+                 &full[st]);
+      }
+    }
+  };
+  if (warp == 0)
+    for (int s2 = 0; s2 < STAGES && s2 < nk; ++s2) produce(s2, s2);
+
+  double cre[MI][NI][2], cim[MI][NI][2], c3[MI][NI][2];
+#pragma unroll
+  for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < NI; ++ni)
+      cre[mi][ni][0] = cre[mi][ni][1] = cim[mi][ni][0] = cim[mi][ni][1] = c3[mi][ni][0] = c3[mi][ni][1] = 0.0;
+  const int arow = wy * (BM / WM) + (lane >> 2);
+  const int bcol = wx * (BN / WN) + (lane >> 2);
+  const int kq = lane & 3;
+  for (int kt = 0; kt < nk; ++kt) {
+    if (warp == 0 && kt >= 1 && kt - 1 + STAGES < nk) {  // refill the stage k-tile kt - 1 used
+      const int st = (kt - 1) % STAGES;
+      if (lane == 0) mbar_wait(&empty[st], ((kt - 1) / STAGES) & 1);
+      __syncwarp();
+      produce(st, kt - 1 + STAGES);
+    }
+    const int st = kt % STAGES;
+    mbar_wait(&full[st], (kt / STAGES) & 1);
+    const double2* cA = sA + st * Cfg::kStageA;
+    const double2* cB = sB + st * Cfg::kStageB;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double ar[MI], ai[MI], an[MI], br[NI], bi[NI], bs[NI];
+#pragma unroll
+      for (int mi = 0; mi < MI; ++mi) {
+        const double2 v = cA[(arow + mi * 8) * Cfg::kLdA + kk + kq];
+        ar[mi] = v.x;
+        ai[mi] = v.y;
+        an[mi] = v.x + v.y;
+      }
+#pragma unroll
+      for (int ni = 0; ni < NI; ++ni) {
+        const double2 v = cB[(kk + kq) * Cfg::kLdB + bcol + ni * 8];
+        br[ni] = v.x;
+        bi[ni] = v.y;
+        bs[ni] = v.x + v.y;
+      }
+#pragma unroll
+      for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < NI; ++ni) {
+          dmma(cre[mi][ni][0], cre[mi][ni][1], ar[mi], br[ni]);
+          dmma(cim[mi][ni][0], cim[mi][ni][1], ai[mi], bi[ni]);
+          dmma(c3[mi][ni][0], c3[mi][ni][1], an[mi], bs[ni]);
+        }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+  }
+
+#pragma unroll
+  for (int mi = 0; mi < MI; ++mi) {
+    const int64_t r = row0 + wy * (BM / WM) + mi * 8 + (lane >> 2);
+    if (r >= g.rows) continue;
+#pragma unroll
+    for (int ni = 0; ni < NI; ++ni) {
+      const int c = wx * (BN / WN) + ni * 8 + 2 * kq;
+      const int64_t ga = a0 + (c & (W - 1));
+      const int64_t gb = b0 + (c >> g.wshift);
+      if (gb >= g.blim) continue;
+      double2* dst = g.C + r * g.ldcr + ga + gb * g.ldcb;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (ga + h < g.alim) {
+          double2 v = make_double2(cre[mi][ni][h] - cim[mi][ni][h], c3[mi][ni][h] - cre[mi][ni][h] - cim[mi][ni][h]);
+          if (g.accumulate) v = cadd(dst[h], v);
+          dst[h] = v;
+        }
+      }
+    }
+  }
+}
+
 // Tile configurations. 3M kernels, 2 CTAs / SM, 8 warps, BK = 16, 3 stages:
 //   kWide: 64 x 32 per CTA;  kTall: 32 x 64 per CTA; warps of 16 x 16.
 // The shape with the least padded output is chosen per GEMM (ties: kWide).
@@ -249,17 +433,24 @@ static void launch_gemm_t(GemmArgs g, cudaStream_t stream) {
   using Cfg = GemmCfg<BM, BN, BK, WM, WN, ST>;
   static bool attr_set = false;
   auto kern = zgemm_dmma_kernel<BM, BN, BK, WM, WN, ST, M3, MINB>;
+  auto tkern = zgemm_tma_kernel<BM, BN, BK, WM, WN, ST, MINB>;
   if (!attr_set) {
     NDS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem));
+    NDS_CUDA(cudaFuncSetAttribute(tkern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem));
     attr_set = true;
   }
+  const bool colm = g.colm != 0;
   g.ntile_rows = (g.rows + BM - 1) / BM;
   const int64_t W = 1ll << g.wshift;
   g.ntile_a = (g.alim + W - 1) / W;
   const int64_t bb = BN / W;
   const int64_t ntile_b = (g.blim + bb - 1) / bb;
   const int64_t tiles = g.ntile_rows * g.ntile_a * ntile_b;
-  kern<<<(unsigned)tiles, Cfg::kThreads, Cfg::kSmem, stream>>>(g);
+  const bool tma = M3 && g.blk && g.K % BK == 0 && (colm || g.alim % W == 0);
+  if (tma)
+    tkern<<<(unsigned)tiles, Cfg::kThreads, Cfg::kSmem, stream>>>(g, colm ? 1 : 0);
+  else
+    kern<<<(unsigned)tiles, Cfg::kThreads, Cfg::kSmem, stream>>>(g);
   NDS_LAUNCH_CHECK();
 }
 
@@ -310,18 +501,87 @@ static void launch_gemm_auto(GemmArgs g, bool colm, int64_t inner, cudaStream_t 
   const double ct = shape_cost(gt, colm, inner, kTall);
   const GemmShape best = ct < cw * (1.0 - 1e-9) ? kTall : kWide;
   shape_cost(g, colm, inner, best);
+  g.blk = g.blk_shape[best];
   launch_gemm(best, g, stream);
+}
+
+// ---- stage-blocked operand images for the bulk-copy GEMM (FactorSet::ablk / bblk) ---------------
+// shape 0 = kWide (BM 64, BN 32), 1 = kTall (BM 32, BN 64); BK = 16, row pads BK + 4 / BN + 2.
+static int64_t ablk_entries(int64_t n, int bm) { return (n + bm - 1) / bm * bm * (n / 16) * 20; }
+static int64_t bblk_entries(int64_t n, int bn) { return (n + bn - 1) / bn * (n / 16) * 16 * (bn + 2); }
+
+int64_t blocked_entries(int64_t n) {
+  if (n < 16 || n % 16) return 0;
+  return 2 * (ablk_entries(n, 64) + ablk_entries(n, 32) + bblk_entries(n, 32) + bblk_entries(n, 64));
+}
+
+// A image: [row tile][k tile][BM][20]: (row, k) of M row-major, zero beyond n rows / 16 k.
+__global__ void ablk_kernel(const double2* __restrict__ mrow, int n, int bm, double2* __restrict__ out, int64_t total) {
+  const int nkt = n / 16;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(e % 20);
+    const int64_t q = e / 20;
+    const int r = (int)(q % bm);
+    const int64_t q2 = q / bm;
+    const int kt = (int)(q2 % nkt);
+    const int64_t rt = q2 / nkt;
+    const int64_t row = rt * bm + r;
+    out[e] = (row < n && c < 16) ? mrow[row * n + kt * 16 + c] : make_double2(0.0, 0.0);
+  }
+}
+// B image of the mode-1 GEMM: [col tile][k tile][16][BN + 2]: B(k, i) = mcol[i + k n].
+__global__ void bblk_kernel(const double2* __restrict__ mcol, int n, int bn, double2* __restrict__ out, int64_t total) {
+  const int nkt = n / 16, ld = bn + 2;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(e % ld);
+    const int64_t q = e / ld;
+    const int k = (int)(q % 16);
+    const int64_t q2 = q / 16;
+    const int kt = (int)(q2 % nkt);
+    const int64_t ct = q2 / nkt;
+    const int64_t col = ct * bn + c;
+    out[e] = (col < n && c < bn) ? mcol[col + (int64_t)(kt * 16 + k) * n] : make_double2(0.0, 0.0);
+  }
+}
+
+void blocked_layouts_launch(FactorSet& f, double2* base, cudaStream_t stream) {
+  double2* p = base;
+  for (int j = 0; j < f.n_modes; ++j) {
+    const int n = (int)f.dims[j];
+    if (!blocked_entries(n)) continue;
+    for (int op = 0; op < 2; ++op) {
+      const double2* mrow = op ? f.uh_row[j] : f.u_row[j];
+      const double2* mcol = op ? f.uh_col[j] : f.u_col[j];
+      for (int sh = 0; sh < 2; ++sh) {
+        const int bm = sh ? 32 : 64, bn = sh ? 64 : 32;
+        const int64_t na = ablk_entries(n, bm), nb = bblk_entries(n, bn);
+        f.ablk[j][op][sh] = p;
+        ablk_kernel<<<(unsigned)std::min<int64_t>((na + 255) / 256, 1024), 256, 0, stream>>>(mrow, n, bm, p, na);
+        NDS_LAUNCH_CHECK();
+        p += na;
+        f.bblk[j][op][sh] = p;
+        bblk_kernel<<<(unsigned)std::min<int64_t>((nb + 255) / 256, 1024), 256, 0, stream>>>(mcol, n, bn, p, nb);
+        NDS_LAUNCH_CHECK();
+        p += nb;
+      }
+    }
+  }
 }
 
 int mode_product_launch(const FactorSet& f, int mode, bool adjoint, const ModeView& v, const double2* x, double2* r,
                         bool accumulate, cudaStream_t stream) {
   const double2* mrow = adjoint ? f.uh_row[mode - 1] : f.u_row[mode - 1];
   const double2* mcol = adjoint ? f.uh_col[mode - 1] : f.u_col[mode - 1];
-  return mode_product_matrix_launch(mrow, mcol, v, x, r, accumulate, stream);
+  const int op = adjoint ? 1 : 0;
+  const bool colm = v.inner == 1;
+  const double2* blk[2] = {colm ? f.bblk[mode - 1][op][0] : f.ablk[mode - 1][op][0],
+                           colm ? f.bblk[mode - 1][op][1] : f.ablk[mode - 1][op][1]};
+  return mode_product_matrix_launch(mrow, mcol, v, x, r, accumulate, stream, -1, -1, blk);
 }
 
 int mode_product_matrix_launch(const double2* mrow, const double2* mcol, const ModeView& v, const double2* x,
-                               double2* r, bool accumulate, cudaStream_t stream, int64_t rows_out, int64_t lda_row) {
+                               double2* r, bool accumulate, cudaStream_t stream, int64_t rows_out, int64_t lda_row,
+                               const double2* const* blk) {
   const int n = (int)v.n;
   const int64_t m = rows_out > 0 ? rows_out : v.n;  // rows of M (output extent along the mode)
   // DMMA GEMM from 16 rows of K up (K is zero-padded to the 16-deep stage; rectangular updates
@@ -339,6 +599,11 @@ int mode_product_matrix_launch(const double2* mrow, const double2* mcol, const M
   GemmArgs g{};
   g.K = n;
   g.accumulate = accumulate ? 1 : 0;
+  g.colm = v.inner == 1 ? 1 : 0;
+  if (blk && rows_out <= 0 && lda_row <= 0) {
+    g.blk_shape[0] = blk[0];
+    g.blk_shape[1] = blk[1];
+  }
   if (v.inner == 1) {  // COLM: C(b, i) = X(b, :) . M^T(:, i)
     g.A = x;
     g.lda = n;
