@@ -27,39 +27,16 @@ struct BinSolveGeom {
   const double2* t;   // per mode j: T_j (2x2 column-major) at t + 4 j
 };
 
-__device__ __forceinline__ unsigned bs_smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void bs_mbar_wait(uint64_t* bar, unsigned parity) {
-  unsigned done = 0;
-  do {
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(done)
-        : "r"(bs_smem_u32(bar)), "r"(parity)
-        : "memory");
-  } while (!done);
-}
-
-// Per tile (one CTA, 256 threads, 3 CTAs / SM):
-//   1. pull — the tile's own slab and its neighbour slabs (outer modes with bit 0, ascending) are
-//      streamed through a ring of four 16 KB slots by bulk asynchronous copies (cp.async.bulk,
-//      TMA engine) completing on per-slot mbarriers; thread t accumulates its 16 entries
-//      l = t + 256 i in registers (own value, then q ascending: the reference's per-entry order);
-//      the producer (thread 0) refills a slot as soon as all eight warps released it, so up to
-//      four 16 KB pieces per CTA (192 KB per SM) are in flight;
-//   2. the ring's 64 KB becomes the tile S; local popcount wavefront, highest level first;
-//   3. store the slab.
 __global__ void __launch_bounds__(kBinSolveThreads, 3) binary_tile_solve_kernel(const BinSolveGeom g,
                                                                               const int64_t* __restrict__ tiles,
                                                                               const int* __restrict__ wf,
                                                                               const int* __restrict__ wf_off,
                                                                               double2* __restrict__ Y) {
-  extern __shared__ __align__(128) double2 S[];  // 2^m entries; first the pull ring (4 x 1024)
+  extern __shared__ __align__(16) double2 S[];  // 2^m entries
   __shared__ double2 t01[64], t00[64], t11[64];
   __shared__ double2 dlo[64], dhi[64];  // den(l) = dlo[l & 63] + dhi[l >> 6] (outer part in dhi)
   __shared__ double2 dout;
-  __shared__ __align__(8) uint64_t full[4], empty[4];
-  constexpr int kSlot = 1024;  // entries per ring slot (16 KB)
-  const int tid = threadIdx.x, lane = tid & 31;
+  const int tid = threadIdx.x;
   const int N = g.m + g.n_outer;
   const int E = 1 << g.m;
   const int mlo = g.m < 6 ? g.m : 6, mhi = g.m - mlo;
@@ -69,47 +46,7 @@ __global__ void __launch_bounds__(kBinSolveThreads, 3) binary_tile_solve_kernel(
     t01[j] = g.t[4 * j + 2];
     t11[j] = g.t[4 * j + 3];
   }
-  const int64_t base = I << g.m;
-  // pieces: the own slab, then each neighbour slab (q ascending), E / kSlot pieces per slab
-  const int ppb = E >= kSlot ? E / kSlot : 1;        // pieces per slab
-  const int pbytes = (E >= kSlot ? kSlot : E) * 16;  // bytes per piece
-  int nsrc = 1;
-  for (int q = 0; q < g.n_outer; ++q) nsrc += ((I >> q) & 1) ? 0 : 1;
-  const int npieces = nsrc * ppb;
-  auto piece_src = [&](int i) {  // global address of piece i
-    const int src = i / ppb, p = i % ppb;
-    int64_t off = base;
-    if (src > 0) {  // the src-th zero bit of I
-      int seen = 0;
-      for (int q = 0; q < g.n_outer; ++q)
-        if (!((I >> q) & 1) && ++seen == src) {
-          off = base + ((int64_t)1 << (g.m + q));
-          break;
-        }
-    }
-    return Y + off + (int64_t)p * kSlot;
-  };
-  auto issue = [&](int i) {
-    const int slot = i & 3;
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bs_smem_u32(&full[slot])),
-                 "r"(pbytes)
-                 : "memory");
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-                     bs_smem_u32(S + slot * kSlot)),
-                 "l"(piece_src(i)), "r"(pbytes), "r"(bs_smem_u32(&full[slot]))
-                 : "memory");
-  };
-  if (tid == 0) {
-    for (int s2 = 0; s2 < 4; ++s2) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bs_smem_u32(&full[s2])), "r"(1));
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bs_smem_u32(&empty[s2])),
-                   "r"(kBinSolveThreads / 32));
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
   __syncthreads();
-  if (tid == 0)
-    for (int i = 0; i < 4 && i < npieces; ++i) issue(i);
   if (tid == 0) {
     double2 d = make_double2(0.0, 0.0);
     for (int q = 0; q < g.n_outer; ++q) d = cadd(d, ((I >> q) & 1) ? t11[g.m + q] : t00[g.m + q]);
@@ -126,49 +63,39 @@ __global__ void __launch_bounds__(kBinSolveThreads, 3) binary_tile_solve_kernel(
     for (int j = 0; j < mhi; ++j) d = cadd(d, ((x >> j) & 1) ? t11[mlo + j] : t00[mlo + j]);
     dhi[x] = cadd(d, dout);
   }
-  // 1. pull: acc[i] holds entry tid + 256 i; piece p of a slab holds entries [1024 p, 1024 p + 1024)
+  const int64_t base = I << g.m;
+  // 1. load + pull from neighbour slabs (outer modes with bit 0). The running sums live in shared
+  //    memory (each thread owns the same entries l = tid + i * 256 throughout, so no barrier), so
+  //    registers hold only loads in flight: a whole slab per thread (two slabs, software-
+  //    pipelined, spill at 2 CTAs/SM and measured slower). Same per-entry order as the reference:
+  //    own value, then q ascending.
   constexpr int PER = 4096 / kBinSolveThreads;
-  double2 acc[PER];
-#pragma unroll
-  for (int i = 0; i < PER; ++i) acc[i] = make_double2(0.0, 0.0);
-  int piece = 0, q = -1;
-  for (int src = 0; src < nsrc; ++src) {
-    double2 c = make_double2(0.0, 0.0);
-    if (src > 0) {
-      do {
-        ++q;
-      } while ((I >> q) & 1);
-      c = t01[g.m + q];
-    }
-#pragma unroll
-    for (int p = 0; p < 4; ++p) {
-      if (p < ppb) {
-        const int slot = piece & 3;
-        if (tid == 0 && piece >= 1 && piece + 3 < npieces) {  // refill the slot piece - 1 used
-          bs_mbar_wait(&empty[(piece - 1) & 3], ((piece - 1) >> 2) & 1);
-          issue(piece + 3);
-        }
-        bs_mbar_wait(&full[slot], (piece >> 2) & 1);
-        const double2* v = S + slot * kSlot;
-#pragma unroll
-        for (int i2 = 0; i2 < 4; ++i2) {
-          const int li = tid + i2 * kBinSolveThreads;  // entry within the piece
-          if (li < (pbytes >> 4)) {
-            const double2 x = v[li];
-            acc[p * 4 + i2] = src == 0 ? x : cfms(acc[p * 4 + i2], c, x);
-          }
-        }
-        __syncwarp();
-        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bs_smem_u32(&empty[slot])) : "memory");
-        ++piece;
-      }
-    }
-  }
-  __syncthreads();  // every piece consumed: the ring becomes the tile
 #pragma unroll
   for (int i = 0; i < PER; ++i) {
     const int l = tid + i * kBinSolveThreads;
-    if (l < E) S[l] = acc[i];
+    if (l < E) S[l] = Y[base + l];
+  }
+  auto load_slab = [&](int q, double2 (&v)[PER]) {
+    const double2* nb = Y + base + ((int64_t)1 << (g.m + q));
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const int l = tid + i * kBinSolveThreads;
+      v[i] = l < E ? __ldcg(nb + l) : make_double2(0.0, 0.0);
+    }
+  };
+  auto apply = [&](int q, const double2 (&v)[PER]) {
+    const double2 c = t01[g.m + q];
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const int l = tid + i * kBinSolveThreads;
+      if (l < E) S[l] = cfms(S[l], c, v[i]);
+    }
+  };
+  for (int q = 0; q < g.n_outer; ++q) {
+    if ((I >> q) & 1) continue;  // CTA-uniform
+    double2 v[PER];
+    load_slab(q, v);
+    apply(q, v);
   }
   __syncthreads();
   // 2. local popcount wavefront, highest level first; inner-mode terms in mode order (loop fully
@@ -242,7 +169,7 @@ int binary_solve_launch(const BinarySolvePlan& bp, const double2* t_pool, double
     attr_set = true;
   }
   BinSolveGeom g{bp.m, bp.n_outer, bp.m + 1, t_pool};
-  const size_t smem = std::max<size_t>(((size_t)1 << bp.m) * sizeof(double2), 4 * 1024 * sizeof(double2));
+  const size_t smem = ((size_t)1 << bp.m) * sizeof(double2);
   int launches = 0;
   for (int lv = 0; lv < bp.levels; ++lv) {
     const int64_t n = bp.level_off[lv + 1] - bp.level_off[lv];
