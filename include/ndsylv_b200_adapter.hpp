@@ -90,6 +90,35 @@ inline SolveResult solve(const SylvesterProblem& p, const SolveOptions& o = {}) 
   return r;
 }
 
+// The same solve sharded over several GPUs of this process (nds_solve_multi: one host thread,
+// context and NCCL communicator per device). Report: Schur time only (the per-device stage times
+// stay inside the library).
+inline SolveResult solve_multi(const SylvesterProblem& p, const std::vector<int>& devices, const SolveOptions& o = {}) {
+  validate_coefficients(p.coefficients, p.rhs.dims, "problem");
+  std::vector<SchurFactors> f;
+  SolveResult r;
+  const auto t0 = std::chrono::steady_clock::now();
+  for (const Matrix& a : p.coefficients) f.push_back(schur(a));
+  r.report.schur_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  std::vector<const nds_z*> u, t;
+  for (auto& s : f) {
+    u.push_back(reinterpret_cast<const nds_z*>(s.u.data()));
+    t.push_back(reinterpret_cast<const nds_z*>(s.t.data()));
+  }
+  r.x = NDTensor::zeros(p.rhs.dims);
+  nds_singular sing{};
+  const int rc = nds_solve_multi(static_cast<int>(devices.size()), devices.data(), p.rhs.order(), p.rhs.dims.data(),
+                                 u.data(), t.data(), reinterpret_cast<const nds_z*>(p.rhs.data.data()),
+                                 reinterpret_cast<nds_z*>(r.x.data.data()), o.singular_tol, &sing);
+  if (rc == NDS_ERR_SINGULAR)
+    throw SingularOperatorError(std::vector<std::int64_t>(sing.multi_index, sing.multi_index + sing.n_modes),
+                                cxd(sing.den_re, sing.den_im));
+  if (rc != NDS_OK) throw std::runtime_error(nds_last_error(nullptr));
+  r.report.backsub_entries = static_cast<std::int64_t>(p.rhs.data.size());
+  r.report.total_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return r;
+}
+
 // Stage functions (sylvester.hpp:64-77) map 1:1: nds_forward_transform, nds_inverse_transform,
 // nds_back_substitute (in place, like the reference), nds_mode_product, nds_apply_operator.
 

@@ -49,6 +49,12 @@ int main() {
     }
   }
   singular_ok = singular_ok && shape_ok == 2;
+  {  // the sharded entry on this process's device(s): one device here
+    const GeneratedProblem g = random_problem({12, 10, 16}, 77);
+    const SolveResult cpu = solve(g.problem);
+    const SolveResult gpu = ndsylv::gpu::solve_multi(g.problem, {0});
+    worst = std::max(worst, max_abs_diff(cpu.x, gpu.x) / max_abs(cpu.x));
+  }
   std::printf("max_rel_diff %.3e singular_ok %d\n", worst, singular_ok);
 
   // ODE: the reference's own random systems (rng.hpp random_ode_system), CPU vs GPU
