@@ -51,6 +51,15 @@ def fp64_peak():
         return 37.2, "nominal 148 SM x 64 FMA/clk x 2 x 1.965 GHz (no measured file)"
 
 
+def hbm_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (driver-measured copy bandwidth)"
+    except Exception:
+        return 6507.2, "B200_PROFILING.md fallback (no MEASURED_PEAKS.json)"
+
+
 def ncu_traffic(config):
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
@@ -446,6 +455,7 @@ def main():
     for kind, mode, ms in recs:
         by_kind.setdefault(kind, []).append((mode, ms))
     gemm = by_kind.get("transform_gemm", [])
+    passes = by_kind.get("transform_direct", [])
     peak_tf, peak_src = fp64_peak()
     roofline = None
     if gemm:
@@ -453,7 +463,8 @@ def main():
         avg_ms = sum(ms for _, ms in gemm) / len(gemm)
         achieved = sum(flops) / sum(ms for _, ms in gemm) / 1e9  # TFLOP/s (flop/ms / 1e9)
         traffic = ncu_traffic(args.config)
-        roofline = {"bound": "tensor", "pipe": "FP64 DMMA (mma.sync.m8n8k4.f64)", "kernel": "zgemm_dmma_kernel",
+        roofline = {"bound": "tensor", "pipe": "FP64 DMMA (mma.sync.m8n8k4.f64)",
+                    "kernel": "zgemm_tma_kernel (modes >= 2, bulk-copy fed) / zgemm_dmma_kernel (mode 1)",
                     "achieved": round(achieved, 3), "peak": peak_tf, "unit": "TFLOP/s",
                     "frac": round(achieved / peak_tf, 4), "traffic": traffic,
                     "flops_per_launch": flops[0], "avg_launch_ms": avg_ms,
@@ -462,6 +473,14 @@ def main():
                     # the kernel multiplies complex numbers with 3 real products (3M), so it executes
                     # 6 of the 8 algorithmic flops per CMAC: the tensor pipe itself runs at pipe_frac
                     "pipe_frac": round(achieved * 0.75 / peak_tf, 4)}
+    elif passes:  # all-binary (c4): the fused binary passes are HBM-bound
+        hbm, hbm_src = hbm_peak()
+        avg_ms = sum(ms for _, ms in passes) / len(passes)
+        achieved = 2.0 * 16 * P / (avg_ms * 1e-3) / 1e9  # GB/s
+        roofline = {"bound": "hbm", "kernel": "binary_pass_kernel (fused runs of up to 12 binary modes)",
+                    "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s", "frac": round(achieved / hbm, 4),
+                    "traffic": ncu_traffic(args.config), "bytes_per_launch": 2.0 * 16 * P, "avg_launch_ms": avg_ms,
+                    "peak_source": hbm_src, "algorithmic": "2 x 16 P bytes per fused pass (read + write once)"}
     step_ms_prof = sum(ms for _, _, ms in recs) / args.steps
     stage_ms = {k: sum(ms for _, ms in v) / args.steps for k, v in by_kind.items()}
     solve_flops = 8.0 * P * (sum(dims) - len(dims)) / 2 + 8.0 * P
