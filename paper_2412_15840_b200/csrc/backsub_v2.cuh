@@ -123,18 +123,50 @@ __device__ __forceinline__ void far_group_body(const TileGeom& g, const double2*
       if constexpr (M3) c3[r][q][0] = c3[r][q][1] = 0.0;
     }
   const int nk = (ke - kb) / BK;
-#pragma unroll
-  for (int st = 0; st < ST - 1; ++st) {
-    if (st < nk) load_stage(st, kb + st * BK);
-    cp_commit_bs();
+  // mbarrier pipeline instead of a CTA barrier per stage: every thread's cp.async of a stage
+  // complete on the stage's full barrier (cp.async.mbarrier.arrive.noinc, one arrival per
+  // thread), warps release a stage on its empty barrier, and a stage is refilled one k-tile
+  // after it was consumed (so a warp waits only for the slowest warp of the previous k-tile,
+  // not of the current one). All ST stages are filled up front.
+  __shared__ __align__(8) uint64_t fullb[ST], emptyb[ST];
+  auto bar_addr = [](uint64_t* b) { return (unsigned)__cvta_generic_to_shared(b); };
+  auto mb_wait = [&](uint64_t* b, unsigned parity) {
+    unsigned done = 0;
+    do {
+      asm volatile(
+          "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+          : "=r"(done)
+          : "r"(bar_addr(b)), "r"(parity)
+          : "memory");
+    } while (!done);
+  };
+  auto arrive_full = [&](int st) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(bar_addr(&fullb[st])) : "memory");
+  };
+  if (tid == 0) {
+    for (int st = 0; st < ST; ++st) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar_addr(&fullb[st])), "r"(kUpdThreads));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar_addr(&emptyb[st])), "r"(kUpdThreads / 32));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
+  __syncthreads();
+#pragma unroll
+  for (int st = 0; st < ST; ++st)
+    if (st < nk) {
+      load_stage(st, kb + st * BK);
+      arrive_full(st);
+    }
   const int cbase = warp * CB * 8 + (lane >> 2);
   const int arow = lane >> 2, kq = lane & 3;
   for (int kt = 0; kt < nk; ++kt) {
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(ST - 2));
-    __syncthreads();
-    if (kt + ST - 1 < nk) load_stage((kt + ST - 1) % ST, kb + (kt + ST - 1) * BK);
-    cp_commit_bs();
+    if (kt >= 1 && kt - 1 + ST < nk) {  // refill the stage k-tile kt - 1 used
+      const int st = (kt - 1) % ST;
+      mb_wait(&emptyb[st], ((kt - 1) / ST) & 1);
+      load_stage(st, kb + (kt - 1 + ST) * BK);
+      arrive_full(st);
+    }
+    mb_wait(&fullb[kt % ST], (kt / ST) & 1);
     const double2* cA = sA + (kt % ST) * BJ * ALD;
     const double2* cB = sB + (kt % ST) * BK * LDB;
 #pragma unroll
@@ -167,8 +199,9 @@ __device__ __forceinline__ void far_group_body(const TileGeom& g, const double2*
         }
       }
     }
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar_addr(&emptyb[kt % ST])) : "memory");
   }
-  cp_wait0_bs();
   const int bsj = g.bstride[j];
 #pragma unroll
   for (int r = 0; r < RB; ++r) {

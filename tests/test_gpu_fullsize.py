@@ -145,3 +145,32 @@ def test_plan_repeatable(ctx, name, dims):
         assert np.array_equal(o, outs[0])
     res = ctx.apply_operator(a, np.asfortranarray(outs[0].reshape(dims, order="F")))
     assert np.linalg.norm(res - b) / np.linalg.norm(b) <= 1e-10
+
+
+def test_plan_on_torch_default_stream(ctx):
+    """ctx.set_stream(<torch's default stream, handle 0>) runs the library on the LEGACY default
+    stream, so torch work queued right after it (no synchronisation) sees the finished X, and a
+    buffer torch frees and reuses is not still being written (ADVICE: a handle of 0 used to fall
+    back to the context's own non-blocking stream)."""
+    import torch
+    a, b = configs.make_problem("c1", seed=4, dims=(128, 128, 128))
+    us, ts = zip(*[ctx.schur(m) for m in a])
+    plan = ctx.plan(list(us), list(ts))
+    d_b = torch.from_numpy(np.ascontiguousarray(b.ravel(order="F"))).cuda()
+    ref_x = None
+    with torch.cuda.stream(torch.cuda.default_stream()):
+        ctx.set_stream(torch.cuda.current_stream().cuda_stream)  # handle 0 -> legacy stream
+        assert torch.cuda.current_stream().cuda_stream == 0
+        for rep in range(3):
+            d_x, d_w = torch.empty_like(d_b), torch.empty_like(d_b)
+            d_x.fill_(float("nan"))
+            plan.execute(d_b.data_ptr(), d_x.data_ptr(), d_w.data_ptr())
+            x_host = d_x.cpu().numpy()  # torch reads on its default stream right away
+            del d_x, d_w                # the allocator may hand these to the next iteration
+            assert np.all(np.isfinite(x_host))
+            if ref_x is None:
+                ref_x = x_host
+            assert np.array_equal(x_host, ref_x)
+        ctx.set_stream(None)
+    res = ctx.apply_operator(a, ref_x.reshape(b.shape, order="F"))
+    assert np.linalg.norm(res - b) / np.linalg.norm(b) <= 1e-10
