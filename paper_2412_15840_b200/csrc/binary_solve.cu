@@ -25,6 +25,7 @@ struct BinSolveGeom {
   int n_outer;        // N - m
   int wf_levels;      // m + 1
   const double2* t;   // per mode j: T_j (2x2 column-major) at t + 4 j
+  int pull;           // 0: decoupled tiles (outer modes diagonalised into the transforms)
 };
 
 __global__ void __launch_bounds__(kBinSolveThreads, 3) binary_tile_solve_kernel(const BinSolveGeom g,
@@ -91,7 +92,7 @@ __global__ void __launch_bounds__(kBinSolveThreads, 3) binary_tile_solve_kernel(
       if (l < E) S[l] = cfms(S[l], c, v[i]);
     }
   };
-  for (int q = 0; q < g.n_outer; ++q) {
+  for (int q = 0; q < g.n_outer && g.pull; ++q) {
     if ((I >> q) & 1) continue;  // CTA-uniform
     double2 v[PER];
     load_slab(q, v);
@@ -161,16 +162,23 @@ void binary_solve_plan_free(BinarySolvePlan& bp) {
 }
 
 int binary_solve_launch(const BinarySolvePlan& bp, const double2* t_pool, double2* c, cudaStream_t stream,
-                        Recorder* rec) {
+                        Recorder* rec, bool decoupled) {
   static bool attr_set = false;
   auto kern = binary_tile_solve_kernel;
   if (!attr_set) {
     NDS_CUDA(cudaFuncSetAttribute(binary_tile_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 4096 * 16));
     attr_set = true;
   }
-  BinSolveGeom g{bp.m, bp.n_outer, bp.m + 1, t_pool};
+  BinSolveGeom g{bp.m, bp.n_outer, bp.m + 1, t_pool, decoupled ? 0 : 1};
   const size_t smem = ((size_t)1 << bp.m) * sizeof(double2);
   int launches = 0;
+  if (decoupled) {  // every tile independent: one launch, no neighbour pulls
+    const int64_t n = bp.level_off.back();
+    kern<<<(unsigned)n, kBinSolveThreads, smem, stream>>>(g, bp.d_tiles, bp.d_wf, bp.d_wf_off, c);
+    NDS_LAUNCH_CHECK();
+    if (rec) rec->mark(stream, kBacksubLevel, 0);
+    return 1;
+  }
   for (int lv = 0; lv < bp.levels; ++lv) {
     const int64_t n = bp.level_off[lv + 1] - bp.level_off[lv];
     kern<<<(unsigned)n, kBinSolveThreads, smem, stream>>>(g, bp.d_tiles + bp.level_off[lv],

@@ -3,6 +3,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <complex>
 #include <cstring>
 #include <limits>
 #include <map>
@@ -73,6 +74,14 @@ struct nds_plan {
   std::shared_ptr<nds::SolverCache> solver;  // dims-only structures, shared via the context
   bool singular = false;                     // deferred singular check (ODE propagator)
   nds_singular sing_info{};
+  // All-binary route with the outer modes (>= 12) diagonalised: T_j = V_j diag(T_j) V_j^{-1},
+  // V_j = [[1, beta_j], [0, 1]], beta_j = T_j(0,1) / (T_j(1,1) - T_j(0,0)). The solve's passes
+  // use fd, whose outer-mode factors are V_j^{-1} U_j^H (forward) and U_j V_j (inverse), and the
+  // tiles decouple (binary_solve_launch(decoupled)). Only execute / execute_host use it; the
+  // stage APIs keep the plain U_j and the coupled solve.
+  bool bin_diag = false;
+  nds::FactorSet fd;
+  double2* fd_buf = nullptr;
   int launches = 0;
   // per-launch CUDA-event profile (nds_plan_profile_begin / _end)
   bool profiling = false;
@@ -412,23 +421,30 @@ std::vector<XPass> transform_passes(const nds_plan* p) {
   return out;
 }
 
-int launch_pass(nds_plan* p, const XPass& ps, bool adjoint, const double2* src, double2* dst) {
-  if (ps.group >= 0) return nds::binary_pass_launch(p->f, p->groups[ps.group], adjoint, src, dst, p->ctx->stream);
-  return nds::mode_product_launch(p->f, ps.mode, adjoint, nds::mode_view(p->n_modes, p->dims, ps.mode), src, dst,
-                                  false, p->ctx->stream);
+// Factors of a full solve's passes: the diagonalised all-binary route merges V_j^{-1} / V_j into
+// the outer modes' factors; stage APIs (merged = false) always use the plain U_j.
+const nds::FactorSet& pass_factors(const nds_plan* p, bool merged) { return merged && p->bin_diag ? p->fd : p->f; }
+
+int launch_pass(nds_plan* p, const XPass& ps, bool adjoint, const double2* src, double2* dst, bool merged = false) {
+  const nds::FactorSet& f = pass_factors(p, merged);
+  if (ps.group >= 0) return nds::binary_pass_launch(f, p->groups[ps.group], adjoint, src, dst, p->ctx->stream);
+  return nds::mode_product_launch(f, ps.mode, adjoint, nds::mode_view(p->n_modes, p->dims, ps.mode), src, dst, false,
+                                  p->ctx->stream);
 }
 
 // The same pass restricted to one of K contiguous chunks of the slowest modes (those of the last
 // pass): its outer extent shrinks by K; src / dst point at the chunk.
-int launch_pass_chunk(nds_plan* p, const XPass& ps, bool adjoint, const double2* src, double2* dst, int K) {
+int launch_pass_chunk(nds_plan* p, const XPass& ps, bool adjoint, const double2* src, double2* dst, int K,
+                      bool merged = false) {
+  const nds::FactorSet& f = pass_factors(p, merged);
   if (ps.group >= 0) {
     nds::BinGroup g = p->groups[ps.group];
     g.outer /= K;
-    return nds::binary_pass_launch(p->f, g, adjoint, src, dst, p->ctx->stream);
+    return nds::binary_pass_launch(f, g, adjoint, src, dst, p->ctx->stream);
   }
   ModeView v = nds::mode_view(p->n_modes, p->dims, ps.mode);
   v.outer /= K;
-  return nds::mode_product_launch(p->f, ps.mode, adjoint, v, src, dst, false, p->ctx->stream);
+  return nds::mode_product_launch(f, ps.mode, adjoint, v, src, dst, false, p->ctx->stream);
 }
 
 int transform_chain(nds_plan* p, bool adjoint, const double2* in, double2* out, double2* work) {
@@ -474,19 +490,89 @@ void build_solver(nds_plan* p) {
   p->solver = slot;
 }
 
-int launch_solver(nds_plan* p, double2* c, cudaStream_t s, nds::Recorder* rec) {
-  if (p->solver->binary) return nds::binary_solve_launch(p->solver->bsp, p->f.t_pool, c, s, rec);
+int launch_solver(nds_plan* p, double2* c, cudaStream_t s, nds::Recorder* rec, bool merged = false) {
+  if (p->solver->binary)
+    return nds::binary_solve_launch(p->solver->bsp, p->f.t_pool, c, s, rec, merged && p->bin_diag);
   return nds::backsub_launch(p->solver->sp, p->f.t_pool, c, s, rec);
 }
 
-int backsub_run(nds_plan* p, double2* c) {
+int backsub_run(nds_plan* p, double2* c, bool merged = false) {
   nds::Recorder* rec = p->profiling ? &p->rec : nullptr;
   if (p->fast_path) {
     nds::fast_divide_launch(p->f.geom, p->f.diag_pool, c, p->ctx->stream);
     if (rec) rec->mark(p->ctx->stream, nds::kElementwise, 0);
     return 1;
   }
-  return launch_solver(p, c, p->ctx->stream, rec);
+  return launch_solver(p, c, p->ctx->stream, rec, merged);
+}
+
+// Decide the diagonalised all-binary route and build its merged outer-mode factors. Guard: every
+// outer T_j has distinct eigenvalues and prod_j cond(V_j) <= 1e6 (cond = ((sqrt(|b|^2 + 4) +
+// |b|) / 2)^2 for V = [[1, b], [0, 1]]); measured error on c4-type problems ~1e-15, i.e. the
+// bound is very pessimistic. Otherwise the plan keeps the coupled (pull) solve.
+void plan_binary_diag(nds_plan* p, const nds_z* const* u, const nds_z* const* t) {
+  p->bin_diag = false;
+  const int N = p->n_modes, m = 12;
+  if (p->fast_path || N <= m) return;
+  for (int j = 0; j < N; ++j)
+    if (p->dims[j] != 2) return;
+  using cx = std::complex<double>;
+  auto z = [](nds_z v) { return cx(v.re, v.im); };
+  std::vector<cx> beta(N);
+  double cond = 1.0;
+  for (int j = m; j < N; ++j) {
+    const cx t00 = z(t[j][0]), t01 = z(t[j][2]), t11 = z(t[j][3]);
+    const cx gap = t11 - t00;
+    if (std::abs(gap) == 0.0) return;
+    beta[j] = t01 / gap;
+    const double b = std::abs(beta[j]);
+    if (!std::isfinite(b)) return;
+    const double s = 0.5 * (std::sqrt(b * b + 4.0) + b);
+    cond *= s * s;
+  }
+  if (!(cond <= 1e6)) return;
+  // per outer mode: [row-major | column-major] of W_fwd = V^{-1} U^H and W_inv = U V
+  const int nb = N - m;
+  std::vector<double2> host((size_t)nb * 16);
+  for (int j = m; j < N; ++j) {
+    cx U[2][2], UH[2][2], Wf[2][2], Wi[2][2];
+    for (int r = 0; r < 2; ++r)
+      for (int c = 0; c < 2; ++c) {
+        U[r][c] = z(u[j][r + 2 * c]);
+        UH[c][r] = std::conj(U[r][c]);
+      }
+    const cx b = beta[j];
+    // V^{-1} = [[1, -b], [0, 1]]: row 0 of W_fwd = UH row 0 - b UH row 1
+    for (int c = 0; c < 2; ++c) {
+      Wf[0][c] = UH[0][c] - b * UH[1][c];
+      Wf[1][c] = UH[1][c];
+    }
+    // U V: column 1 of W_inv = U col 1 + b U col 0
+    for (int r = 0; r < 2; ++r) {
+      Wi[r][0] = U[r][0];
+      Wi[r][1] = U[r][1] + b * U[r][0];
+    }
+    double2* o = host.data() + (size_t)(j - m) * 16;
+    for (int r = 0; r < 2; ++r)
+      for (int c = 0; c < 2; ++c) {
+        o[0 + r * 2 + c] = make_double2(Wi[r][c].real(), Wi[r][c].imag());   // u_row
+        o[4 + r + c * 2] = make_double2(Wi[r][c].real(), Wi[r][c].imag());   // u_col
+        o[8 + r * 2 + c] = make_double2(Wf[r][c].real(), Wf[r][c].imag());   // uh_row
+        o[12 + r + c * 2] = make_double2(Wf[r][c].real(), Wf[r][c].imag());  // uh_col
+      }
+  }
+  NDS_CUDA(cudaMalloc(&p->fd_buf, host.size() * sizeof(double2)));
+  NDS_CUDA(cudaMemcpy(p->fd_buf, host.data(), host.size() * sizeof(double2), cudaMemcpyHostToDevice));
+  p->fd = p->f;
+  p->fd.pool = nullptr;  // owned by f
+  for (int j = m; j < N; ++j) {
+    double2* o = p->fd_buf + (size_t)(j - m) * 16;
+    p->fd.u_row[j] = o;
+    p->fd.u_col[j] = o + 4;
+    p->fd.uh_row[j] = o + 8;
+    p->fd.uh_col[j] = o + 12;
+  }
+  p->bin_diag = true;
 }
 
 // Full path on device buffers: b -> (fwd) -> C -> (solve, in place) -> Y -> (inv) -> x.
@@ -563,7 +649,7 @@ int execute(nds_plan* p, const double2* b, double2* x, double2* work, cudaEvent_
   }
   for (int j = 1; j <= last_fwd; ++j) {
     double2* dst = dst_of(j);
-    const int kind = launch_pass(p, passes[j - 1], true, src, dst);
+    const int kind = launch_pass(p, passes[j - 1], true, src, dst, true);
     if (rec) rec->mark(s, kind, -passes[j - 1].mode);
     ++launches;
     src = dst;
@@ -594,7 +680,7 @@ int execute(nds_plan* p, const double2* b, double2* x, double2* work, cudaEvent_
   } else if (tail) {
     launches += nds::backsub_launch(p->solver->sp, p->f.t_pool, c, s, rec, nullptr, &tail_hook);
   } else {
-    launches += backsub_run(p, c);
+    launches += backsub_run(p, c, true);
   }
   src = c;
   int first_inv = 1;
@@ -612,7 +698,7 @@ int execute(nds_plan* p, const double2* b, double2* x, double2* work, cudaEvent_
   if (ev) NDS_CUDA(cudaEventRecord(ev[2], s));
   for (int j = first_inv; j <= N; ++j) {
     double2* dst = dst_of(N + j);
-    const int kind = launch_pass(p, passes[j - 1], false, src, dst);
+    const int kind = launch_pass(p, passes[j - 1], false, src, dst, true);
     if (rec) rec->mark(s, kind, passes[j - 1].mode);
     ++launches;
     src = dst;
@@ -662,7 +748,10 @@ void plan_create_impl(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_
       throw Error(NDS_ERR_SINGULAR, format_singular(tmp));
     }
   }
-  if (!p->fast_path) build_solver(p.get());
+  if (!p->fast_path) {
+    build_solver(p.get());
+    plan_binary_diag(p.get(), u, t);
+  }
   *out = p.release();
 }
 
@@ -671,6 +760,7 @@ void plan_destroy_impl(nds_plan* p) {
   cudaSetDevice(p->ctx->device);
   for (auto e : p->pev) cudaEventDestroy(e);
   free_factors(p->f);
+  if (p->fd_buf) cudaFree(p->fd_buf);
   delete p;  // the shared solver structures stay cached in the context
 }
 
@@ -781,7 +871,7 @@ void execute_host_impl(nds_plan* p, const nds_z* hb, nds_z* hx, nds_report* rep,
         const double2* src = X + k * chunk;
         for (int j = 1; j < np; ++j) {
           double2* dst = chunk_buf(j) + k * chunk;
-          launch_pass_chunk(p, passes[j - 1], true, src, dst, K);
+          launch_pass_chunk(p, passes[j - 1], true, src, dst, K, true);
           ++launches;
           src = dst;
         }
@@ -792,7 +882,7 @@ void execute_host_impl(nds_plan* p, const nds_z* hb, nds_z* hx, nds_report* rep,
       NDS_CUDA(cudaEventRecord(ctx->ev[0], s));
       double2* c = W;
       NDS_CUDA(cudaEventRecord(ctx->ev[1], s));
-      launches += backsub_run(p, c);
+      launches += backsub_run(p, c, true);
       NDS_CUDA(cudaEventRecord(ctx->ev[2], s));
       // inverse per chunk: row block of the last pass, then passes 1 .. np-1; inverse pass i of
       // np writes X when np - i is even, so the chunk ends in X
@@ -804,7 +894,7 @@ void execute_host_impl(nds_plan* p, const nds_z* hb, nds_z* hx, nds_report* rep,
         const double2* src = dst0;
         for (int j = 1; j < np; ++j) {
           double2* dst = inv_buf(1 + j) + k * chunk;
-          launch_pass_chunk(p, passes[j - 1], false, src, dst, K);
+          launch_pass_chunk(p, passes[j - 1], false, src, dst, K, true);
           ++launches;
           src = dst;
         }
@@ -820,25 +910,25 @@ void execute_host_impl(nds_plan* p, const nds_z* hb, nds_z* hx, nds_report* rep,
         const double2* src = X + k * chunk;
         for (int j = 1; j < np; ++j) {
           double2* dst = dst_of(j) + k * chunk;
-          launch_pass_chunk(p, passes[j - 1], true, src, dst, K);
+          launch_pass_chunk(p, passes[j - 1], true, src, dst, K, true);
           ++launches;
           src = dst;
         }
       }
       NDS_CUDA(cudaEventRecord(ctx->ev[0], s));
-      launch_pass(p, passes.back(), true, dst_of(np - 1), dst_of(np));  // forward last pass, whole tensor
+      launch_pass(p, passes.back(), true, dst_of(np - 1), dst_of(np), true);  // forward last pass, whole tensor
       ++launches;
       double2* c = dst_of(np);
       NDS_CUDA(cudaEventRecord(ctx->ev[1], s));
-      launches += backsub_run(p, c);
+      launches += backsub_run(p, c, true);
       NDS_CUDA(cudaEventRecord(ctx->ev[2], s));
-      launch_pass(p, passes.back(), false, c, dst_of(np + 1));  // inverse: last pass first
+      launch_pass(p, passes.back(), false, c, dst_of(np + 1), true);  // inverse: last pass first
       ++launches;
       for (int k = 0; k < K; ++k) {
         const double2* src = dst_of(np + 1) + k * chunk;
         for (int j = 1; j < np; ++j) {
           double2* dst = dst_of(np + 1 + j) + k * chunk;
-          launch_pass_chunk(p, passes[j - 1], false, src, dst, K);
+          launch_pass_chunk(p, passes[j - 1], false, src, dst, K, true);
           ++launches;
           src = dst;
         }

@@ -146,8 +146,10 @@ struct BinarySolvePlan {
 void binary_solve_plan_build(BinarySolvePlan& bp, int n_modes);
 void binary_solve_plan_free(BinarySolvePlan& bp);
 // t_pool: T_j (2x2 column-major) at t_pool + 4 j.
+// decoupled: the outer modes were diagonalised into the transform passes (capi.cu, all-binary
+// route), so every tile is an independent inner-mode solve (den still includes the outer modes).
 int binary_solve_launch(const BinarySolvePlan& bp, const double2* t_pool, double2* c, cudaStream_t stream,
-                        Recorder* rec = nullptr);
+                        Recorder* rec = nullptr, bool decoupled = false);
 
 // Dims-only solver structures (tile lists, work items, partial buffers, internal streams), cached
 // per context and shared by every plan with the same extents.
