@@ -122,6 +122,98 @@ __global__ void __launch_bounds__(kBinThreads, 2) binary_pass_kernel(const BinPa
   for (int i = 0; i < 4096 / kBinThreads; ++i) r[goff(i)] = S[stid ^ swz(i * kBinThreads)];
 }
 
+// ---- fused pass: forward modes 1-12, decoupled tile solve, inverse modes 1-12 -------------------
+// The all-binary route with diagonalised outer modes (capi.cu plan_binary_diag) leaves 2^(N-12)
+// independent 12-mode tile solves, and a tile is exactly the 4096-entry contiguous tile of the
+// modes-1-12 pass. Modes commute, so a full solve applies the outer modes' passes first; then
+// ONE kernel loads each tile, applies U_j^H of modes 1-12 (butterfly rounds), solves the tile
+// (popcount wavefront; den = sum over all N modes of T_j(i_j, i_j), the outer part from the
+// tile's outer index), applies U_j of modes 1-12 and stores — two passes and the separate solve
+// pass fused into one read and one write of the tensor.
+struct BinTileSolve {
+  const double2* t;    // T_j (2x2 column-major) at t + 4 j, all N modes
+  int n_outer;         // N - 12
+  const int* wf;       // the 4096 tile entries by popcount, highest first
+  const int* wf_off;   // 14 offsets
+};
+
+__global__ void __launch_bounds__(kBinThreads, 2)
+    binary_fused_solve_kernel(const BinPass fw, const BinPass iv, const BinTileSolve ts, const double2* __restrict__ x,
+                              double2* __restrict__ r) {
+  extern __shared__ __align__(16) double2 S[];  // 4096 entries, swizzled (swz)
+  __shared__ double2 Mq[12][4];
+  __shared__ double2 t01[12], dlo[64], dhi[64];
+  __shared__ double2 dout;
+  const int tid = threadIdx.x;
+  const int64_t tile = blockIdx.x;  // outer index (modes 13..N)
+  const int64_t base = tile << 12;
+  if (tid < 48) Mq[tid >> 2][tid & 3] = fw.M[tid >> 2][tid & 3];
+  if (tid < 12) t01[tid] = ts.t[4 * tid + 2];
+  if (tid == 0) {
+    double2 d = make_double2(0.0, 0.0);
+    for (int q = 0; q < ts.n_outer; ++q) d = cadd(d, ts.t[4 * (12 + q) + (((tile >> q) & 1) ? 3 : 0)]);
+    dout = d;
+  }
+  const int stid = swz(tid);
+  // tile load: contiguous 4096 entries (run R = 4096 / ... : pass geometry inner = 1)
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    double2 v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = x[base + tid + (h * 8 + i) * kBinThreads];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) S[stid ^ swz((h * 8 + i) * kBinThreads)] = v[i];
+  }
+  __syncthreads();
+  for (int rd = 0; rd < fw.rounds; ++rd) {
+    switch (fw.nrb[rd]) {
+      case 4: bin_round<4>(fw, rd, S, Mq, tid); break;
+      case 3: bin_round<3>(fw, rd, S, Mq, tid); break;
+      case 2: bin_round<2>(fw, rd, S, Mq, tid); break;
+      default: bin_round<1>(fw, rd, S, Mq, tid); break;
+    }
+    __syncthreads();
+  }
+  // den tables (modes 1-6 | modes 7-12 + the outer part), then the inverse factors
+  if (tid < 64) {
+    double2 d = make_double2(0.0, 0.0);
+    for (int j = 0; j < 6; ++j) d = cadd(d, ts.t[4 * j + (((tid >> j) & 1) ? 3 : 0)]);
+    dlo[tid] = d;
+  } else if (tid < 128) {
+    const int xh = tid - 64;
+    double2 d = make_double2(0.0, 0.0);
+    for (int j = 0; j < 6; ++j) d = cadd(d, ts.t[4 * (6 + j) + (((xh >> j) & 1) ? 3 : 0)]);
+    dhi[xh] = cadd(d, dout);
+  } else if (tid < 128 + 48) {
+    const int e = tid - 128;
+    Mq[e >> 2][e & 3] = iv.M[e >> 2][e & 3];
+  }
+  __syncthreads();
+  for (int lv = 0; lv < 13; ++lv) {
+    const int p1 = ts.wf_off[lv + 1];
+    for (int p = ts.wf_off[lv] + tid; p < p1; p += kBinThreads) {
+      const int l = ts.wf[p];
+      double2 num = S[swz(l)];
+#pragma unroll
+      for (int j = 0; j < 12; ++j)
+        if (!((l >> j) & 1)) num = cfms(num, t01[j], S[swz(l | (1 << j))]);
+      S[swz(l)] = cmul(num, crecip_fast(cadd(dlo[l & 63], dhi[l >> 6])));
+    }
+    __syncthreads();
+  }
+  for (int rd = 0; rd < iv.rounds; ++rd) {
+    switch (iv.nrb[rd]) {
+      case 4: bin_round<4>(iv, rd, S, Mq, tid); break;
+      case 3: bin_round<3>(iv, rd, S, Mq, tid); break;
+      case 2: bin_round<2>(iv, rd, S, Mq, tid); break;
+      default: bin_round<1>(iv, rd, S, Mq, tid); break;
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4096 / kBinThreads; ++i) r[base + tid + i * kBinThreads] = S[stid ^ swz(i * kBinThreads)];
+}
+
 // Plan the passes over [mode0, mode1) (1-based, all n_j = 2): greedily take as many binary modes
 // as fit a 4096-entry tile with runs of min(I, 8..4096) entries.
 std::vector<BinGroup> plan_binary_groups(int n_modes, const int64_t* dims, int lo, int hi) {
@@ -160,8 +252,7 @@ std::vector<BinGroup> plan_binary_groups(int n_modes, const int64_t* dims, int l
   return out;
 }
 
-int binary_pass_launch(const FactorSet& f, const BinGroup& gr, bool adjoint, const double2* x, double2* r,
-                       cudaStream_t stream) {
+static BinPass make_bin_pass(const FactorSet& f, const BinGroup& gr, bool adjoint) {
   BinPass bp{};
   bp.I = gr.inner;
   bp.O = gr.outer;
@@ -200,6 +291,12 @@ int binary_pass_launch(const FactorSet& f, const BinGroup& gr, bool adjoint, con
       bp.rsw[rd][e] = swz(bits);
     }
   }
+  return bp;
+}
+
+int binary_pass_launch(const FactorSet& f, const BinGroup& gr, bool adjoint, const double2* x, double2* r,
+                       cudaStream_t stream) {
+  const BinPass bp = make_bin_pass(f, gr, adjoint);
   static bool attr_set = false;
   if (!attr_set) {
     NDS_CUDA(cudaFuncSetAttribute(binary_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 4096 * 16));
@@ -209,6 +306,23 @@ int binary_pass_launch(const FactorSet& f, const BinGroup& gr, bool adjoint, con
   binary_pass_kernel<<<(unsigned)tiles, kBinThreads, 4096 * 16, stream>>>(bp, x, r);
   NDS_LAUNCH_CHECK();
   return kXformDirect;
+}
+
+int binary_fused_solve_launch(const FactorSet& fwd, const FactorSet& inv, const BinGroup& gr, const double2* t_pool,
+                              int n_outer, const int* wf, const int* wf_off, const double2* x, double2* r,
+                              cudaStream_t stream) {
+  if (gr.first != 1 || gr.count != 12 || gr.logR != 0 || gr.inner != 1) throw Error(NDS_ERR_OTHER, "fused pass: not a modes-1-12 tile pass");
+  const BinPass fw = make_bin_pass(fwd, gr, true);
+  const BinPass iv = make_bin_pass(inv, gr, false);
+  static bool attr_set = false;
+  if (!attr_set) {
+    NDS_CUDA(cudaFuncSetAttribute(binary_fused_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 4096 * 16));
+    attr_set = true;
+  }
+  BinTileSolve ts{t_pool, n_outer, wf, wf_off};
+  binary_fused_solve_kernel<<<(unsigned)gr.outer, kBinThreads, 4096 * 16, stream>>>(fw, iv, ts, x, r);
+  NDS_LAUNCH_CHECK();
+  return kBacksubLevel;
 }
 
 }  // namespace nds

@@ -577,8 +577,63 @@ void plan_binary_diag(nds_plan* p, const nds_z* const* u, const nds_z* const* t)
 
 // Full path on device buffers: b -> (fwd) -> C -> (solve, in place) -> Y -> (inv) -> x.
 // Destinations alternate W/X from the first pass so the 2N-th pass lands in x and b is only read.
+// The diagonalised all-binary route with a modes-1-12 first pass: the outer modes' passes
+// (merged V^{-1} U^H), then ONE fused kernel per tile (forward modes 1-12, the decoupled tile
+// solve, inverse modes 1-12), then the outer modes' inverse passes (merged U V). Modes commute,
+// so only the rounding order changes. Returns -1 when the plan does not qualify.
+bool fused_binary_ok(const nds_plan* p, const std::vector<XPass>& passes) {
+  if (!p->bin_diag || passes.empty() || passes.front().group < 0) return false;
+  const nds::BinGroup& g = p->groups[passes.front().group];
+  return g.first == 1 && g.count == 12 && g.logR == 0 && g.inner == 1 && p->solver && p->solver->binary &&
+         p->solver->bsp.m == 12;
+}
+
+int execute_fused_binary(nds_plan* p, const std::vector<XPass>& passes, const double2* b, double2* x, double2* work,
+                         cudaEvent_t* ev) {
+  cudaStream_t s = p->ctx->stream;
+  nds::Recorder* rec = p->profiling ? &p->rec : nullptr;
+  const int np = (int)passes.size(), total = 2 * np - 1;
+  auto dst_of = [&](int k) { return ((total - k) % 2 == 0) ? x : work; };  // pass k = 1..total lands in x last
+  if (ev) NDS_CUDA(cudaEventRecord(ev[0], s));
+  if (rec) rec->mark(s, -1, 0);
+  const double2* src = b;
+  int k = 0, launches = 0;
+  for (int j = 2; j <= np; ++j) {
+    double2* dst = dst_of(++k);
+    const int kind = launch_pass(p, passes[j - 1], true, src, dst, true);
+    if (rec) rec->mark(s, kind, -passes[j - 1].mode);
+    ++launches;
+    src = dst;
+  }
+  if (ev) NDS_CUDA(cudaEventRecord(ev[1], s));
+  {
+    double2* dst = dst_of(++k);
+    const nds::BinarySolvePlan& bp = p->solver->bsp;
+    const int kind = nds::binary_fused_solve_launch(p->fd, p->fd, p->groups[passes.front().group], p->f.t_pool,
+                                                    bp.n_outer, bp.d_wf, bp.d_wf_off, src, dst, s);
+    if (rec) rec->mark(s, kind, 0);
+    ++launches;
+    src = dst;
+  }
+  if (ev) NDS_CUDA(cudaEventRecord(ev[2], s));
+  for (int j = np; j >= 2; --j) {
+    double2* dst = dst_of(++k);
+    const int kind = launch_pass(p, passes[j - 1], false, src, dst, true);
+    if (rec) rec->mark(s, kind, passes[j - 1].mode);
+    ++launches;
+    src = dst;
+  }
+  if (p->flags & NDS_REAL_OUTPUT) {
+    launches += nds::real_part_launch(x, p->total, s);
+    if (rec) rec->mark(s, nds::kElementwise, 0);
+  }
+  if (ev) NDS_CUDA(cudaEventRecord(ev[3], s));
+  return launches;
+}
+
 int execute(nds_plan* p, const double2* b, double2* x, double2* work, cudaEvent_t* ev) {
   const std::vector<XPass> passes = transform_passes(p);
+  if (fused_binary_ok(p, passes)) return execute_fused_binary(p, passes, b, x, work, ev);
   const int N = (int)passes.size();
   cudaStream_t s = p->ctx->stream;
   nds::Recorder* rec = p->profiling ? &p->rec : nullptr;

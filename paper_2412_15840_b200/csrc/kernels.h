@@ -68,6 +68,12 @@ struct BinGroup {
 std::vector<BinGroup> plan_binary_groups(int n_modes, const int64_t* dims, int lo = 0, int hi = -1);
 int binary_pass_launch(const FactorSet& f, const BinGroup& gr, bool adjoint, const double2* x, double2* r,
                        cudaStream_t stream);
+// Modes 1-12 forward (fwd's U^H), the decoupled 12-mode tile solve (den over all modes; the
+// outer modes' coupling diagonalised away), modes 1-12 inverse (inv's U) — one kernel, one read
+// and one write of the tensor; gr is the modes-1-12 pass (first 1, count 12, inner 1).
+int binary_fused_solve_launch(const FactorSet& fwd, const FactorSet& inv, const BinGroup& gr, const double2* t_pool,
+                              int n_outer, const int* wf, const int* wf_off, const double2* x, double2* r,
+                              cudaStream_t stream);
 
 // Plain matrix variant (apply_operator / residual): m_row, m_col are the two layouts of M.
 // rows_out > 0: rectangular M (rows_out x n), r has extent rows_out along the mode.
