@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(kBinThreads, 2) binary_pass_kernel(const BinPa
 struct BinTileSolve {
   const double2* t;    // T_j (2x2 column-major) at t + 4 j, all N modes
   int n_outer;         // N - 12
-  const int* wf;       // the 4096 tile entries by popcount, highest first
+  const uint16_t* wf;  // the 4096 tile entries by popcount, highest first (bank-interleaved)
   const int* wf_off;   // 14 offsets
 };
 
@@ -189,15 +189,20 @@ __global__ void __launch_bounds__(kBinThreads, 2)
     Mq[e >> 2][e & 3] = iv.M[e >> 2][e & 3];
   }
   __syncthreads();
+  // popcount wavefront on the swizzled tile: swz is XOR-linear, so the slot of l | e_j (bit j of
+  // l clear) is swz(l) ^ swz(e_j); terms split over two accumulators (even / odd modes)
   for (int lv = 0; lv < 13; ++lv) {
     const int p1 = ts.wf_off[lv + 1];
     for (int p = ts.wf_off[lv] + tid; p < p1; p += kBinThreads) {
       const int l = ts.wf[p];
-      double2 num = S[swz(l)];
+      const int sl = swz(l);
+      double2 n0 = S[sl], n1 = make_double2(0.0, 0.0);
 #pragma unroll
-      for (int j = 0; j < 12; ++j)
-        if (!((l >> j) & 1)) num = cfms(num, t01[j], S[swz(l | (1 << j))]);
-      S[swz(l)] = cmul(num, crecip_fast(cadd(dlo[l & 63], dhi[l >> 6])));
+      for (int j = 0; j < 12; j += 2) {
+        if (!((l >> j) & 1)) n0 = cfms(n0, t01[j], S[sl ^ swz(1 << j)]);
+        if (!((l >> (j + 1)) & 1)) n1 = cfms(n1, t01[j + 1], S[sl ^ swz(2 << j)]);
+      }
+      S[sl] = cmul(cadd(n0, n1), crecip_fast(cadd(dlo[l & 63], dhi[l >> 6])));
     }
     __syncthreads();
   }
@@ -309,7 +314,7 @@ int binary_pass_launch(const FactorSet& f, const BinGroup& gr, bool adjoint, con
 }
 
 int binary_fused_solve_launch(const FactorSet& fwd, const FactorSet& inv, const BinGroup& gr, const double2* t_pool,
-                              int n_outer, const int* wf, const int* wf_off, const double2* x, double2* r,
+                              int n_outer, const uint16_t* wf, const int* wf_off, const double2* x, double2* r,
                               cudaStream_t stream) {
   if (gr.first != 1 || gr.count != 12 || gr.logR != 0 || gr.inner != 1) throw Error(NDS_ERR_OTHER, "fused pass: not a modes-1-12 tile pass");
   const BinPass fw = make_bin_pass(fwd, gr, true);

@@ -146,11 +146,29 @@ void binary_solve_plan_build(BinarySolvePlan& bp, int n_modes) {
     std::vector<int> pos(wf_off.begin(), wf_off.end() - 1);
     for (int l = E - 1; l >= 0; --l) wf[pos[m - __builtin_popcount(l)]++] = l;
   }
-  const size_t bytes = ntiles * sizeof(int64_t) + (E + m + 2) * sizeof(int);
+  // the fused kernel's order (binary_pass.cu, swizzled tile): within a level, entries
+  // round-robin over the 16-byte bank group of their swizzled slot, so the lanes of an 8-lane
+  // shared-memory phase hit distinct groups (the term loads XOR the slot with a constant, which
+  // keeps them distinct)
+  std::vector<uint16_t> wfs(E);
+  {
+    auto swz = [](int q) { return q ^ (((q >> 3) ^ (q >> 6) ^ (q >> 9)) & 7); };
+    for (int lv = 0; lv <= m; ++lv) {
+      std::vector<std::vector<int>> bucket(8);
+      for (int i = wf_off[lv]; i < wf_off[lv + 1]; ++i) bucket[swz(wf[i]) & 7].push_back(wf[i]);
+      int o = wf_off[lv];
+      for (size_t r = 0; o < wf_off[lv + 1]; ++r)
+        for (int b = 0; b < 8; ++b)
+          if (r < bucket[b].size()) wfs[o++] = (uint16_t)bucket[b][r];
+    }
+  }
+  const size_t bytes = ntiles * sizeof(int64_t) + (E + m + 2) * sizeof(int) + E * sizeof(uint16_t) + 16;
   NDS_CUDA(cudaMalloc(&bp.pool, bytes));
   bp.d_tiles = (int64_t*)bp.pool;
   bp.d_wf = (int*)(bp.d_tiles + ntiles);
   bp.d_wf_off = bp.d_wf + E;
+  bp.d_wf_swz = (uint16_t*)(bp.d_wf_off + m + 2);
+  NDS_CUDA(cudaMemcpy(bp.d_wf_swz, wfs.data(), E * sizeof(uint16_t), cudaMemcpyHostToDevice));
   NDS_CUDA(cudaMemcpy(bp.d_tiles, tiles.data(), ntiles * sizeof(int64_t), cudaMemcpyHostToDevice));
   NDS_CUDA(cudaMemcpy(bp.d_wf, wf.data(), E * sizeof(int), cudaMemcpyHostToDevice));
   NDS_CUDA(cudaMemcpy(bp.d_wf_off, wf_off.data(), (m + 2) * sizeof(int), cudaMemcpyHostToDevice));

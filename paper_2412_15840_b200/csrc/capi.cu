@@ -610,7 +610,7 @@ int execute_fused_binary(nds_plan* p, const std::vector<XPass>& passes, const do
     double2* dst = dst_of(++k);
     const nds::BinarySolvePlan& bp = p->solver->bsp;
     const int kind = nds::binary_fused_solve_launch(p->fd, p->fd, p->groups[passes.front().group], p->f.t_pool,
-                                                    bp.n_outer, bp.d_wf, bp.d_wf_off, src, dst, s);
+                                                    bp.n_outer, bp.d_wf_swz, bp.d_wf_off, src, dst, s);
     if (rec) rec->mark(s, kind, 0);
     ++launches;
     src = dst;

@@ -72,7 +72,7 @@ int binary_pass_launch(const FactorSet& f, const BinGroup& gr, bool adjoint, con
 // outer modes' coupling diagonalised away), modes 1-12 inverse (inv's U) — one kernel, one read
 // and one write of the tensor; gr is the modes-1-12 pass (first 1, count 12, inner 1).
 int binary_fused_solve_launch(const FactorSet& fwd, const FactorSet& inv, const BinGroup& gr, const double2* t_pool,
-                              int n_outer, const int* wf, const int* wf_off, const double2* x, double2* r,
+                              int n_outer, const uint16_t* wf, const int* wf_off, const double2* x, double2* r,
                               cudaStream_t stream);
 
 // Plain matrix variant (apply_operator / residual): m_row, m_col are the two layouts of M.
@@ -147,6 +147,7 @@ struct BinarySolvePlan {
   int64_t* d_tiles = nullptr;
   int* d_wf = nullptr;
   int* d_wf_off = nullptr;
+  uint16_t* d_wf_swz = nullptr;  // the same levels, bank-group interleaved for the swizzled tile
   void* pool = nullptr;
 };
 void binary_solve_plan_build(BinarySolvePlan& bp, int n_modes);
