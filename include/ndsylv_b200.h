@@ -55,8 +55,10 @@ typedef enum {
   NDS_ERR_NONFINITE = 9
 } nds_status;
 
-/* SolveOptions (sylvester.hpp:19-28): allow_fast_path defaults to true in the reference. */
-enum { NDS_ALLOW_FAST_PATH = 1u, NDS_REAL_OUTPUT = 2u };
+/* SolveOptions (sylvester.hpp:19-28): allow_fast_path defaults to true in the reference.
+ * NDS_NO_DIAGONALISE (B200 extension): full solves keep the plain Schur factors and the
+ * wavefront tile solves even when the block-diagonalised route's guard passes. */
+enum { NDS_ALLOW_FAST_PATH = 1u, NDS_REAL_OUTPUT = 2u, NDS_NO_DIAGONALISE = 4u };
 
 /* SolveReport (sylvester.hpp:30-42) plus device-side timings. */
 typedef struct {
@@ -170,6 +172,12 @@ int nds_plan_launches(const nds_plan* plan);
  * all-binary tiles (c4). -1 for a NULL plan. */
 enum { NDS_PATH_FAST = 0, NDS_PATH_GENERIC = 1, NDS_PATH_CUBIC = 2, NDS_PATH_BINARY = 3 };
 int nds_plan_solve_path(const nds_plan* plan);
+/* Whether FULL solves (nds_plan_execute / _execute_host / nds_solve*) run on diagonalised factors:
+ * cubic route — every B x B diagonal block of T_j diagonalised (diagonal tiles become divisions);
+ * binary route — the outer modes' 2 x 2 T_j diagonalised (tiles decouple). *cond receives the
+ * guard's bound prod_j cond_2 (<= 1e6 when taken; 0 when not evaluated). Returns 1 / 0, -1 for a
+ * NULL plan. Stage calls (forward / backsub / inverse) always use the plain factors. */
+int nds_plan_diagonalised(const nds_plan* plan, double* cond);
 /* Per-launch device timing: after _begin, every launch of execute/forward/backsub/inverse records
  * a CUDA event on the context stream (up to max_launches). _end synchronises and returns the
  * number of launches written: kind (0 transform GEMM, 1 transform direct, 2 solve level,

@@ -39,6 +39,7 @@ LIB_PATH = os.path.join(HERE, "libndsylv_b200.so")
 NDS_MAX_MODES = 64
 ALLOW_FAST_PATH = 1
 REAL_OUTPUT = 2
+NO_DIAGONALISE = 4
 
 (OK, ERR_OTHER, ERR_SINGULAR, ERR_FILE, ERR_NOMEM, ERR_INVALID, ERR_CONVERGENCE, ERR_OVERFLOW, ERR_CUDA,
  ERR_NONFINITE) = range(10)
@@ -50,6 +51,7 @@ EXPORTED = [
     "nds_back_substitute", "nds_mode_product", "nds_apply_operator", "nds_flop_estimate", "nds_schur_flop_estimate",
     "nds_plan_create", "nds_plan_destroy", "nds_plan_report", "nds_plan_total", "nds_plan_execute",
     "nds_plan_forward", "nds_plan_backsub", "nds_plan_inverse", "nds_plan_execute_host", "nds_plan_launches", "nds_plan_solve_path",
+    "nds_plan_diagonalised",
     "nds_plan_profile_begin", "nds_plan_profile_end",
     "nds_dev_mode_product", "nds_dev_mode_update", "nds_dev_mode_apply", "nds_dev_back_substitute", "nds_dev_residual",
     "nds_triangular_exp", "nds_ode_create", "nds_ode_destroy", "nds_ode_at", "nds_ode_at_dev", "nds_propagate",
@@ -177,6 +179,7 @@ def load_library(path: str = LIB_PATH):
     L.nds_plan_execute_host.argtypes = [_vp, _vp, _vp, C.POINTER(_Report)]
     L.nds_plan_launches.argtypes = [_vp]
     L.nds_plan_solve_path.argtypes = [_vp]
+    L.nds_plan_diagonalised.argtypes = [_vp, C.POINTER(C.c_double)]
     L.nds_plan_profile_begin.argtypes = [_vp, C.c_int]
     L.nds_plan_profile_end.argtypes = [_vp, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int),
                                        C.POINTER(C.c_float)]
@@ -413,12 +416,14 @@ class OdePropagator:
 class Plan:
     """Device-resident solver for one coefficient set (factors uploaded once)."""
 
-    def __init__(self, ctx: "Context", us, ts, singular_tol=0.0, allow_fast_path=True, real_output=False):
+    def __init__(self, ctx: "Context", us, ts, singular_tol=0.0, allow_fast_path=True, real_output=False,
+                 diagonalise=True):
         self.ctx = ctx
         self.dims = tuple(int(u.shape[0]) for u in us)
         up, self._ku = _ptr_array(us)
         tp, self._kt = _ptr_array(ts)
-        flags = (ALLOW_FAST_PATH if allow_fast_path else 0) | (REAL_OUTPUT if real_output else 0)
+        flags = (ALLOW_FAST_PATH if allow_fast_path else 0) | (REAL_OUTPUT if real_output else 0) | (
+            0 if diagonalise else NO_DIAGONALISE)
         h = _vp()
         sing = _Singular()
         rc = ctx.lib.nds_plan_create(ctx.h, len(us), _dims(self.dims), up, tp, float(singular_tol), flags,
@@ -473,6 +478,13 @@ class Plan:
         """Triangular-solve route: 'fast', 'generic' (any shape), 'cubic' (16^3 / 8^4 DMMA tiles)
         or 'binary' (all n_j = 2)."""
         return self.SOLVE_PATHS[self.ctx.lib.nds_plan_solve_path(self.h)]
+
+    def diagonalised(self):
+        """(taken, cond): whether full solves run on diagonalised factors (cubic: T_j's diagonal
+        blocks; binary: the outer modes) and the guard's prod_j cond_2 bound."""
+        c = C.c_double(0.0)
+        r = self.ctx.lib.nds_plan_diagonalised(self.h, C.byref(c))
+        return bool(r == 1), float(c.value)
 
     def profile_begin(self, max_launches: int):
         self._check(self.ctx.lib.nds_plan_profile_begin(self.h, int(max_launches)))
@@ -691,8 +703,8 @@ class Context:
         self._check(self.lib.nds_write_tensor_dev(self.h, path.encode(), len(dims), _dims(dims), d_in))
 
     # ---- device surfaces ------------------------------------------------------------------
-    def plan(self, us, ts, singular_tol=0.0, allow_fast_path=True, real_output=False) -> Plan:
-        return Plan(self, us, ts, singular_tol, allow_fast_path, real_output)
+    def plan(self, us, ts, singular_tol=0.0, allow_fast_path=True, real_output=False, diagonalise=True) -> Plan:
+        return Plan(self, us, ts, singular_tol, allow_fast_path, real_output, diagonalise)
 
     def dev_mode_product(self, dims, d_m: int, mode: int, d_x: int, d_r: int, conj_transpose=False,
                          accumulate=False):

@@ -122,6 +122,7 @@ __global__ void __launch_bounds__(kSolveThreads) tile_level_kernel(const TileGeo
 
 
 #include "backsub_v2.cuh"
+#include "backsub_blk.cuh"
 
 // Tile shape: grow the smallest extents first (earlier modes win ties, keeping tiles contiguous
 // along mode 1) while prod b_j <= kMaxTile.
@@ -458,6 +459,126 @@ int backsub_launch(const SolvePlan& sp, const double2* t_pool, double2* c, cudaS
     for (auto e : tev) cudaEventDestroy(e);
   }
   return launches;
+}
+
+void blk_solve_plan_build(BlkSolvePlan& bp, const SolvePlan& sp, const int* d) {
+  const TileGeom& g = sp.geom;
+  const int N = g.n_modes;
+  int64_t ntiles = 1;
+  int levels = 1;
+  for (int j = 0; j < N; ++j) {
+    bp.d[j] = d[j];
+    ntiles *= g.nb[j];
+    levels += (int)(g.dims[j] / d[j] - 1);
+  }
+  bp.levels = levels;
+  struct T {
+    int lv;
+    int64_t k;  // rows pulled (all modes)
+    int64_t id;
+  };
+  std::vector<T> ts((size_t)ntiles);
+  for (int64_t t = 0; t < ntiles; ++t) {
+    int64_t r = t, k = 0;
+    int lv = 0;
+    for (int j = 0; j < N; ++j) {
+      const int64_t I = r % g.nb[j];
+      r /= g.nb[j];
+      const int64_t sb = I * g.b[j] / d[j];
+      lv += (int)sb;
+      k += g.dims[j] - (sb + 1) * d[j];
+    }
+    ts[t] = {levels - 1 - lv, k, t};
+  }
+  std::stable_sort(ts.begin(), ts.end(), [](const T& a, const T& b) { return a.lv != b.lv ? a.lv < b.lv : a.k > b.k; });
+  bp.level_off.assign(levels + 1, 0);
+  std::vector<int64_t> ids((size_t)ntiles);
+  for (int64_t i = 0; i < ntiles; ++i) {
+    ids[i] = ts[i].id;
+    bp.level_off[ts[i].lv + 1]++;
+  }
+  for (int i = 0; i < levels; ++i) bp.level_off[i + 1] += bp.level_off[i];
+  NDS_CUDA(cudaMalloc(&bp.d_tiles, (size_t)ntiles * sizeof(int64_t)));
+  NDS_CUDA(cudaMemcpy(bp.d_tiles, ids.data(), (size_t)ntiles * sizeof(int64_t), cudaMemcpyHostToDevice));
+}
+
+void blk_solve_plan_free(BlkSolvePlan& bp) {
+  if (bp.d_tiles) cudaFree(bp.d_tiles);
+  bp.d_tiles = nullptr;
+}
+
+int blk_backsub_launch(const SolvePlan& sp, const BlkSolvePlan& bp, const double2* t_pool, double2* c,
+                       cudaStream_t stream, Recorder* rec) {
+  const TileGeom& g = sp.geom;
+  const BlkLaunch bl = blk_cfg(g.n_modes, g.b[0]);
+  static bool attr_set = false;
+  if (!attr_set) {
+    for (int nm : {3, 4}) {
+      const BlkLaunch x = blk_cfg(nm, nm == 3 ? 16 : 8);
+      NDS_CUDA(cudaFuncSetAttribute(x.kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)x.smem));
+    }
+    attr_set = true;
+  }
+  BlkArgs ba;
+  ba.g = g;
+  for (int j = 0; j < NDS_MAX_MODES; ++j) ba.d[j] = j < g.n_modes ? bp.d[j] : 1;
+  if (rec) rec->mark(stream, -1, 0);
+  int launches = 0;
+  for (int lv = 0; lv < bp.levels; ++lv) {
+    const int64_t nt = bp.level_off[lv + 1] - bp.level_off[lv];
+    if (nt == 0) continue;
+    bl.kern<<<(unsigned)nt, kBlkThreads, bl.smem, stream>>>(ba, t_pool, bp.d_tiles + bp.level_off[lv], c);
+    NDS_LAUNCH_CHECK();
+    if (rec) rec->mark(stream, kBacksubLevel, lv);
+    ++launches;
+  }
+  return launches;
+}
+
+__global__ void blockdiag_mul_kernel(int64_t n, int d, const double2* __restrict__ a, const double2* __restrict__ blk,
+                                     int right, int conj_t, double2* __restrict__ out) {
+  const int64_t total = n * n;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e % n, c = e / n;
+    const int64_t q = (right ? c : r) / d, o = q * d;
+    const double2* bq = blk + q * (int64_t)d * d;
+    auto bel = [&](int64_t i, int64_t k) {  // Bq(i, k) or Bq^H(i, k)
+      if (!conj_t) return bq[i + k * d];
+      const double2 v = bq[k + i * d];
+      return make_double2(v.x, -v.y);
+    };
+    double2 s = make_double2(0.0, 0.0);
+    if (right)
+      for (int k = 0; k < d; ++k) s = cfma(s, a[r + (o + k) * n], bel(k, c - o));
+    else
+      for (int k = 0; k < d; ++k) s = cfma(s, bel(r - o, k), a[(o + k) + c * n]);
+    out[e] = s;
+  }
+}
+
+__global__ void blockdiag_fix_kernel(int64_t n, int d, const double2* __restrict__ diag_src, double2* __restrict__ t) {
+  const int64_t total = n * n;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e % n, c = e / n;
+    if (r / d == c / d)
+      t[e] = r == c ? diag_src[e] : make_double2(0.0, 0.0);
+    else if (r / d > c / d)
+      t[e] = make_double2(0.0, 0.0);
+  }
+}
+
+void blockdiag_mul_launch(int64_t n, int d, const double2* a, const double2* blk, bool right, bool conj_t,
+                          double2* out, cudaStream_t stream) {
+  const int64_t total = n * n;
+  blockdiag_mul_kernel<<<(unsigned)std::min<int64_t>((total + 255) / 256, 4096), 256, 0, stream>>>(
+      n, d, a, blk, right ? 1 : 0, conj_t ? 1 : 0, out);
+  NDS_LAUNCH_CHECK();
+}
+
+void blockdiag_fix_launch(int64_t n, int d, const double2* diag_src, double2* t, cudaStream_t stream) {
+  const int64_t total = n * n;
+  blockdiag_fix_kernel<<<(unsigned)std::min<int64_t>((total + 255) / 256, 4096), 256, 0, stream>>>(n, d, diag_src, t);
+  NDS_LAUNCH_CHECK();
 }
 
 }  // namespace nds

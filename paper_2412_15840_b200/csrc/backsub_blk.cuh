@@ -1,0 +1,280 @@
+// Triangular solve of the BLOCK-DIAGONALISED cubic route (capi.cu plan_cubic_diag). Included by
+// backsub.cu after backsub_v2.cuh (reuses dmma_bs, cp_async16_bs).
+//
+// The plan replaced every T_j by T'_j = W_j^{-1} T_j W_j, W_j = blockdiag of the eigenvector
+// matrices of T_j's D_j x D_j diagonal blocks (D_j a multiple of the tile edge B): T'_j is block
+// upper triangular with DIAGONAL D_j x D_j diagonal blocks. In Eq. (9) (sylvester.cpp:88-106) an
+// entry then couples only to entries in a HIGHER D_j-block along some mode, so with super-blocks
+// of D_j rows the index space is a grid of super-tiles whose levels sum_j floor(i_j / D_j) run
+// from high to low, and every entry of a level is independent of the others:
+//   y(i) = (c(i) - sum_j sum_{k >= (floor(i_j / D_j) + 1) D_j} T'_j(i_j, k) y(i with i_j -> k))
+//          / sum_j T_j(i_j, i_j).
+// One launch per level; one CTA per B^N tile of the level's super-tiles PULLS all its couplings:
+// per mode j a (B rows) x (B^(N-1) columns) x (K_j = n_j - kb_j rows) complex GEMM on the FP64
+// tensor pipe (3M DMMA), the operands streamed through one multi-stage cp.async + mbarrier ring
+// that runs across the modes without draining (k-tile t -> (mode, k-tile)); each mode's result is
+// subtracted from the tile held in shared memory, then the tile is divided by its denominators
+// and stored. No partial buffers, no side streams: the whole solve is `levels` launches
+// (c1 with D = 64: 10, against 46 tile hyperplanes of the wavefront route).
+
+constexpr int kBlkThreads = 256;
+
+struct BlkArgs {
+  TileGeom g;
+  int d[NDS_MAX_MODES];  // diagonalisation block (super-block) extent per mode
+};
+
+template <int N, int B, int BK, int ST>
+struct BlkCfg {
+  static constexpr int E = 4096;
+  static constexpr int LB = B == 16 ? 4 : 3;
+  static constexpr int TC = E / B;        // columns of every mode's GEMM
+  static constexpr int NW = kBlkThreads / 32;
+  static constexpr int CB = TC / 8 / NW;  // column fragments per warp
+  static constexpr int RB = B / 8;        // row fragments
+  static constexpr int LDB = TC + 2;      // row-major B stage stride (modes >= 2)
+  static constexpr int ALD = BK <= 8 ? 12 : BK + 4;
+  static constexpr int SL = BK * TC / kBlkThreads;  // B elements per thread per stage
+  static constexpr int BSTAGE = BK * LDB;           // >= TC * BK (mode-1 k-fastest layout)
+  static constexpr int ASTAGE = B * ALD;
+  static constexpr size_t smem() {
+    return (size_t)(E + ST * (BSTAGE + ASTAGE)) * sizeof(double2) + (size_t)N * TC * sizeof(int);
+  }
+};
+
+template <int N, int B, int BK, int ST>
+__global__ void __launch_bounds__(kBlkThreads, 1)
+    blk_level_kernel(const BlkArgs ba, const double2* __restrict__ T, const int64_t* __restrict__ tiles,
+                     double2* __restrict__ Y) {
+  using C = BlkCfg<N, B, BK, ST>;
+  constexpr int E = C::E, LB = C::LB, TC = C::TC, CB = C::CB, RB = C::RB, LDB = C::LDB, ALD = C::ALD;
+  constexpr int SL = C::SL;
+  static_assert(C::SL * kBlkThreads == BK * TC && B * BK <= kBlkThreads && BK % 4 == 0, "stage shape");
+  extern __shared__ __align__(16) double2 smem[];
+  double2* sS = smem;                          // the tile (local index l = sum_m l_m B^m)
+  double2* sB = sS + E;                        // [ST][BSTAGE]
+  double2* sA = sB + ST * C::BSTAGE;           // [ST][B][ALD]
+  int* colg = (int*)(sA + ST * C::ASTAGE);     // [N][TC]: global offset of column c for mode j
+  __shared__ __align__(8) uint64_t fullb[ST], emptyb[ST];
+  __shared__ int64_t so[N];
+  __shared__ int kb_s[N], nk_s[N];
+  __shared__ double2 dd[N][B];
+  const TileGeom& g = ba.g;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid < N) {
+    int64_t t = tiles[blockIdx.x];
+    for (int m = 0; m < N; ++m) {
+      const int64_t I = t % g.nb[m];
+      t /= g.nb[m];
+      if (m == tid) {
+        so[m] = I * B;
+        const int64_t kb = (so[m] / ba.d[m] + 1) * ba.d[m];
+        kb_s[m] = (int)kb;
+        nk_s[m] = kb < g.dims[m] ? (int)((g.dims[m] - kb) / BK) : 0;
+      }
+    }
+  }
+  // column tables: column c of mode j = local coordinates of the modes != j (earliest fastest)
+  for (int e = tid; e < N * TC; e += kBlkThreads) {
+    const int j = e / TC;
+    int x = e % TC, o = 0;
+#pragma unroll
+    for (int m = 0; m < N; ++m) {
+      if (m == j) continue;
+      o += (x & (B - 1)) * (int)g.strides[m];
+      x >>= LB;
+    }
+    colg[e] = o;
+  }
+  auto bar_addr = [](uint64_t* b) { return (unsigned)__cvta_generic_to_shared(b); };
+  if (tid == 0) {
+    for (int st = 0; st < ST; ++st) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar_addr(&fullb[st])), "r"(kBlkThreads));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar_addr(&emptyb[st])), "r"(kBlkThreads / 32));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (tid < N * B) dd[tid / B][tid % B] = T[g.toff[tid / B] + (so[tid / B] + tid % B) * (g.dims[tid / B] + 1)];
+  int64_t base = 0;  // tile origin
+#pragma unroll
+  for (int m = 0; m < N; ++m) base += so[m] * g.strides[m];
+  int nkt = 0;
+#pragma unroll
+  for (int m = 0; m < N; ++m) nkt += nk_s[m];
+
+  // ---- producer: k-tile t of the mode sequence (modes with no coupling have nk = 0) ----
+  int pj = 0, pkt = 0;  // producer cursor
+  auto advance = [&](int& j, int& kt) {
+    ++kt;
+    while (j < N && kt >= nk_s[j]) {
+      kt = 0;
+      ++j;
+    }
+  };
+  while (pj < N && nk_s[pj] == 0) ++pj;
+  auto mb_wait = [&](uint64_t* b, unsigned parity) {
+    unsigned done = 0;
+    do {
+      asm volatile(
+          "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+          : "=r"(done)
+          : "r"(bar_addr(b)), "r"(parity)
+          : "memory");
+    } while (!done);
+  };
+  auto load_stage = [&](int stage) {  // the producer cursor's k-tile into `stage`
+    const int j = pj;
+    const int k0 = kb_s[j] + pkt * BK;
+    const int64_t sj = g.strides[j];
+    // source rows k0.. of the tile column: the tile origin with mode j moved to row k0
+    const double2* src = Y + (base - so[j] * sj) + (int64_t)k0 * sj;
+    double2* dB = sB + stage * C::BSTAGE;
+    const int* cg = colg + j * TC;
+#pragma unroll
+    for (int i = 0; i < SL; ++i) {
+      const int e = tid + i * kBlkThreads;
+      int k, c, soff;
+      if (j == 0) {  // mode 1: contiguous along k in HBM — k-fastest smem, XOR swizzle
+        k = e % BK;
+        c = e / BK;
+        soff = c * BK + (k ^ (BK >= 8 ? (c & 1) << 2 : 0));
+      } else {
+        c = e % TC;
+        k = e / TC;
+        soff = k * LDB + c;
+      }
+      cp_async16_bs(dB + soff, src + (int64_t)k * sj + cg[c]);
+    }
+    if (tid < B * BK) {  // T'_j(so_j + r, k0 + k), rows fastest (column-major T: coalesced)
+      const int r = tid % B, k = tid / B;
+      cp_async16_bs(sA + stage * C::ASTAGE + r * ALD + k,
+                    T + g.toff[j] + (so[j] + r) + (int64_t)(k0 + k) * g.dims[j]);
+    }
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(bar_addr(&fullb[stage])) : "memory");
+    advance(pj, pkt);
+  };
+#pragma unroll
+  for (int st = 0; st < ST; ++st)
+    if (st < nkt) load_stage(st);
+  // the tile itself (C) into shared memory while the first stages are in flight
+  {
+    constexpr int PER = E / kBlkThreads;
+    double2 v[PER];
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const int l = tid + i * kBlkThreads;
+      int64_t o = 0;
+#pragma unroll
+      for (int m = 0; m < N; ++m) o += ((l >> (LB * m)) & (B - 1)) * g.strides[m];
+      v[i] = Y[base + o];
+    }
+#pragma unroll
+    for (int i = 0; i < PER; ++i) sS[tid + i * kBlkThreads] = v[i];
+  }
+
+  // ---- consumer ----
+  double cre[RB][CB][2], cim[RB][CB][2], c3[RB][CB][2];
+  auto zero = [&]() {
+#pragma unroll
+    for (int r = 0; r < RB; ++r)
+#pragma unroll
+      for (int q = 0; q < CB; ++q)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) cre[r][q][h] = cim[r][q][h] = c3[r][q][h] = 0.0;
+  };
+  zero();
+  const int cbase = warp * CB * 8 + (lane >> 2);
+  const int arow = lane >> 2, kq = lane & 3;
+  int cj = 0, ckt = 0;
+  while (cj < N && nk_s[cj] == 0) ++cj;
+  for (int t = 0; t < nkt; ++t) {
+    if (t >= 1 && t - 1 + ST < nkt) {  // refill the stage k-tile t - 1 used
+      const int st = (t - 1) % ST;
+      mb_wait(&emptyb[st], ((t - 1) / ST) & 1);
+      load_stage(st);
+    }
+    mb_wait(&fullb[t % ST], (t / ST) & 1);
+    const double2* cA = sA + (t % ST) * C::ASTAGE;
+    const double2* cBs = sB + (t % ST) * C::BSTAGE;
+    const bool kfast = cj == 0;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double br[CB], bi[CB], bs[CB];
+#pragma unroll
+      for (int q = 0; q < CB; ++q) {
+        const int c = cbase + q * 8;
+        const double2 b = kfast ? cBs[c * BK + ((kk + kq) ^ (BK >= 8 ? (c & 1) << 2 : 0))] : cBs[(kk + kq) * LDB + c];
+        br[q] = b.x;
+        bi[q] = b.y;
+        bs[q] = b.x + b.y;
+      }
+#pragma unroll
+      for (int r = 0; r < RB; ++r) {
+        const double2 a = cA[(r * 8 + arow) * ALD + kk + kq];
+        const double as = a.x + a.y;
+#pragma unroll
+        for (int q = 0; q < CB; ++q) {
+          dmma_bs(cre[r][q][0], cre[r][q][1], a.x, br[q]);
+          dmma_bs(cim[r][q][0], cim[r][q][1], a.y, bi[q]);
+          dmma_bs(c3[r][q][0], c3[r][q][1], as, bs[q]);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar_addr(&emptyb[t % ST])) : "memory");
+    if (++ckt == nk_s[cj]) {  // mode cj done: S -= its GEMM (modes in turn: CTA barrier first)
+      __syncthreads();
+      const int bsj = 1 << (LB * cj);
+#pragma unroll
+      for (int q = 0; q < CB; ++q)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int c = warp * CB * 8 + q * 8 + 2 * kq + h;
+          // local index of column c for mode cj (the modes != cj in order, earliest fastest)
+          int x = c, lo = 0;
+#pragma unroll
+          for (int m = 0; m < N; ++m) {
+            if (m == cj) continue;
+            lo += (x & (B - 1)) << (LB * m);
+            x >>= LB;
+          }
+#pragma unroll
+          for (int r = 0; r < RB; ++r) {
+            const int l = lo + (r * 8 + arow) * bsj;
+            sS[l] = csub(sS[l], make_double2(cre[r][q][h] - cim[r][q][h], c3[r][q][h] - cre[r][q][h] - cim[r][q][h]));
+          }
+        }
+      zero();
+      ckt = 0;
+      ++cj;
+      while (cj < N && nk_s[cj] == 0) ++cj;
+    }
+  }
+  __syncthreads();
+  constexpr int PER = E / kBlkThreads;
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    const int l = tid + i * kBlkThreads;
+    double2 den = dd[0][l & (B - 1)];
+    int64_t o = l & (B - 1);
+#pragma unroll
+    for (int m = 1; m < N; ++m) {
+      const int lm = (l >> (LB * m)) & (B - 1);
+      den = cadd(den, dd[m][lm]);
+      o += lm * g.strides[m];
+    }
+    Y[base + o] = cmul(sS[l], crecip_fast(den));
+  }
+}
+
+using BlkKernel = void (*)(const BlkArgs, const double2*, const int64_t*, double2*);
+struct BlkLaunch {
+  BlkKernel kern;
+  size_t smem;
+};
+static BlkLaunch blk_cfg(int n_modes, int b) {
+  if (n_modes == 3 && b == 16) return {blk_level_kernel<3, 16, 8, 3>, BlkCfg<3, 16, 8, 3>::smem()};
+  if (n_modes == 4 && b == 8) return {blk_level_kernel<4, 8, 4, 3>, BlkCfg<4, 8, 4, 3>::smem()};
+  return {nullptr, 0};
+}

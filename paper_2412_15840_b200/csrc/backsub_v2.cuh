@@ -279,6 +279,87 @@ constexpr LineOrder<N, B> make_line_order() {
 __constant__ LineOrder<3, 16> kLineOrder3 = make_line_order<3, 16>();
 __constant__ LineOrder<4, 8> kLineOrder4 = make_line_order<4, 8>();
 
+// Near-coupling push of a solved tile held in shared memory (padded layout LinePad): for every
+// mode m with a target (tgt_m[m] >= 0, CTA-uniform), near_out[tgt] (l_m, c) = sum_k Ap_m(l_m, k)
+// S(k along m, c) — GEMM (B rows) x (NT columns) x (B k), 3M DMMA; warp w owns columns
+// [32 w, 32 w + 32) as RB x 4 fragments of 8 x 8. Column c = the local coordinates of the modes
+// != m (earliest fastest). Ap = [N][B][B + 4]: T_m(o_m - B + r, o_m + k).
+template <int N, int B, int NT>
+__device__ __forceinline__ void push_near(const double2* __restrict__ S, const double2* __restrict__ Ap,
+                                          const int* tgt_m, double2* __restrict__ near_out) {
+  using PS = LinePad<N, B>;
+  constexpr int E = 4096;
+  constexpr int LB = B == 16 ? 4 : 3;
+  constexpr int ALD = B + 4;
+  const int tid = threadIdx.x;
+  constexpr int RB = B / 8;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int kq = lane & 3, ar = lane >> 2;
+  auto col_offsets = [&](int c, int m, int& soff, int& loff) {
+    soff = 0;
+    loff = 0;
+#pragma unroll
+    for (int mm = 0; mm < N; ++mm) {
+      if (mm == m) continue;
+      const int l = c & (B - 1);
+      c >>= LB;
+      soff += l * PS::at(mm);
+      loff += l << (LB * mm);
+    }
+  };
+#pragma unroll 1
+  for (int m = 0; m < N; ++m) {
+    const int tgt = tgt_m[m];
+    if (tgt < 0) continue;  // CTA-uniform
+    int sb[4];
+#pragma unroll
+    for (int qf = 0; qf < 4; ++qf) {
+      int lo;
+      col_offsets(warp * 32 + qf * 8 + ar, m, sb[qf], lo);
+    }
+    double2* out = near_out + (int64_t)tgt * E;
+    const double2* am = Ap + m * B * ALD;
+    double cre[RB][4][2], cim[RB][4][2], c3[RB][4][2];
+#pragma unroll
+    for (int ri = 0; ri < RB; ++ri)
+#pragma unroll
+      for (int qf = 0; qf < 4; ++qf)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) cre[ri][qf][h] = cim[ri][qf][h] = c3[ri][qf][h] = 0.0;
+#pragma unroll
+    for (int kk = 0; kk < B / 4; ++kk) {
+      double a_r[RB], a_i[RB], a_s[RB];
+#pragma unroll
+      for (int ri = 0; ri < RB; ++ri) {
+        const double2 a = am[(ri * 8 + ar) * ALD + kk * 4 + kq];
+        a_r[ri] = a.x, a_i[ri] = a.y, a_s[ri] = a.x + a.y;
+      }
+#pragma unroll
+      for (int qf = 0; qf < 4; ++qf) {
+        const double2 v = S[(kk * 4 + kq) * PS::at(m) + sb[qf]];
+        const double vs = v.x + v.y;
+#pragma unroll
+        for (int ri = 0; ri < RB; ++ri) {
+          dmma_bs(cre[ri][qf][0], cre[ri][qf][1], a_r[ri], v.x);
+          dmma_bs(cim[ri][qf][0], cim[ri][qf][1], a_i[ri], v.y);
+          dmma_bs(c3[ri][qf][0], c3[ri][qf][1], a_s[ri], vs);
+        }
+      }
+    }
+#pragma unroll
+    for (int qf = 0; qf < 4; ++qf)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        int so_, lo;
+        col_offsets(warp * 32 + qf * 8 + 2 * kq + h, m, so_, lo);
+#pragma unroll
+        for (int ri = 0; ri < RB; ++ri)
+          out[((ri * 8 + ar) << (LB * m)) + lo] =
+              make_double2(cre[ri][qf][h] - cim[ri][qf][h], c3[ri][qf][h] - cre[ri][qf][h] - cim[ri][qf][h]);
+      }
+  }
+}
+
 // Diagonal tile, line-owner formulation. Thread t owns the mode-1 line with fixed local
 // coordinates (l_2, .., l_N) = base-B digits of t and walks it from row B-1 down to 0, one row
 // per local hyperplane: row r is solved at step lv = (N-1)(B-1) - d + (B-1-r), d = sum_{m>=2} l_m.
@@ -477,77 +558,7 @@ __device__ __forceinline__ void diag_lines_body(const TileGeom& g, const double2
     }
   }
   NDS_LPROBE(4);
-  if constexpr (PUSH) {
-    // GEMM (B rows) x (NT columns) x (B k) per mode; warp w owns columns [32 w, 32 w + 32) as
-    // RB x 4 fragments of 8 x 8. Column c = the local coordinates of the modes != m (earliest
-    // fastest, as in tile_update_kernel's partial layout).
-    constexpr int RB = B / 8;
-    const int lane = tid & 31, warp = tid >> 5;
-    const int kq = lane & 3, ar = lane >> 2;
-    auto col_offsets = [&](int c, int m, int& soff, int& loff) {
-      soff = 0;
-      loff = 0;
-#pragma unroll
-      for (int mm = 0; mm < N; ++mm) {
-        if (mm == m) continue;
-        const int l = c & (B - 1);
-        c >>= LB;
-        soff += l * PS::at(mm);
-        loff += l << (LB * mm);
-      }
-    };
-#pragma unroll 1
-    for (int m = 0; m < N; ++m) {
-      const int tgt = tgt_m[m];
-      if (tgt < 0) continue;  // CTA-uniform
-      int sb[4];
-#pragma unroll
-      for (int qf = 0; qf < 4; ++qf) {
-        int lo;
-        col_offsets(warp * 32 + qf * 8 + ar, m, sb[qf], lo);
-      }
-      double2* out = near_out + (int64_t)tgt * E;
-      const double2* am = Ap + m * B * ALD;
-      double cre[RB][4][2], cim[RB][4][2], c3[RB][4][2];
-#pragma unroll
-      for (int ri = 0; ri < RB; ++ri)
-#pragma unroll
-        for (int qf = 0; qf < 4; ++qf)
-#pragma unroll
-          for (int h = 0; h < 2; ++h) cre[ri][qf][h] = cim[ri][qf][h] = c3[ri][qf][h] = 0.0;
-#pragma unroll
-      for (int kk = 0; kk < B / 4; ++kk) {
-        double a_r[RB], a_i[RB], a_s[RB];
-#pragma unroll
-        for (int ri = 0; ri < RB; ++ri) {
-          const double2 a = am[(ri * 8 + ar) * ALD + kk * 4 + kq];
-          a_r[ri] = a.x, a_i[ri] = a.y, a_s[ri] = a.x + a.y;
-        }
-#pragma unroll
-        for (int qf = 0; qf < 4; ++qf) {
-          const double2 v = S[(kk * 4 + kq) * PS::at(m) + sb[qf]];
-          const double vs = v.x + v.y;
-#pragma unroll
-          for (int ri = 0; ri < RB; ++ri) {
-            dmma_bs(cre[ri][qf][0], cre[ri][qf][1], a_r[ri], v.x);
-            dmma_bs(cim[ri][qf][0], cim[ri][qf][1], a_i[ri], v.y);
-            dmma_bs(c3[ri][qf][0], c3[ri][qf][1], a_s[ri], vs);
-          }
-        }
-      }
-#pragma unroll
-      for (int qf = 0; qf < 4; ++qf)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          int so_, lo;
-          col_offsets(warp * 32 + qf * 8 + 2 * kq + h, m, so_, lo);
-#pragma unroll
-          for (int ri = 0; ri < RB; ++ri)
-            out[((ri * 8 + ar) << (LB * m)) + lo] =
-                make_double2(cre[ri][qf][h] - cim[ri][qf][h], c3[ri][qf][h] - cre[ri][qf][h] - cim[ri][qf][h]);
-        }
-    }
-  }
+  if constexpr (PUSH) push_near<N, B, NT>(S, Ap, tgt_m, near_out);
   NDS_LPROBE(5);
 }
 

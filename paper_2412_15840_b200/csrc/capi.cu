@@ -82,6 +82,14 @@ struct nds_plan {
   bool bin_diag = false;
   nds::FactorSet fd;
   double2* fd_buf = nullptr;
+  // Cubic-tile route with every T_j block-diagonalised (plan_cubic_diag): T'_j = W_j^{-1} T_j W_j,
+  // W_j = blockdiag of the unit-column eigenvector matrices of T_j's B x B diagonal blocks. Full
+  // solves run the passes with fc (forward W_j^{-1} U_j^H, inverse U_j W_j) and the solve on
+  // fc.t_pool = T'_j, whose diagonal tiles are divisions. cd_inv / cd_fwd own the memory.
+  bool cub_diag = false;
+  double cub_cond = 0.0, bin_cond = 0.0;  // prod_j max_q cond_2(V_{j,q}) of the route's guard
+  nds::FactorSet cd_inv, cd_fwd, fc;
+  nds::BlkSolvePlan blk;  // super-tile levels of the route
   int launches = 0;
   // per-launch CUDA-event profile (nds_plan_profile_begin / _end)
   bool profiling = false;
@@ -351,6 +359,54 @@ void free_factors(nds::FactorSet& f) {
   f.pool = nullptr;
 }
 
+// A factor set built from DEVICE data (same pool layout as upload_factors): d_u = the raw
+// column-major U_j concatenated, d_t / d_diag = T_j concatenated and their diagonals (or null).
+void device_factors(nds_ctx* ctx, nds::FactorSet& f, int n_modes, const int64_t* dims, const double2* d_u,
+                    const double2* d_t, const double2* d_diag) {
+  f.n_modes = n_modes;
+  int64_t sq = 0, diag = 0, n_blk = 0;
+  for (int j = 0; j < n_modes; ++j) {
+    f.dims[j] = dims[j];
+    sq += dims[j] * dims[j];
+    diag += dims[j];
+    n_blk += nds::blocked_entries(dims[j]);
+  }
+  const int64_t n_t = d_t ? sq : 0, n_d = d_t ? diag : 0;
+  NDS_CUDA(cudaMallocFromPoolAsync(&f.pool, (size_t)(4 * sq + n_t + n_d + sq + n_blk + 1) * sizeof(double2), ctx->pool,
+                                   ctx->stream));
+  f.stream = ctx->stream;
+  nds::Geom& g = f.geom;
+  g.n_modes = n_modes;
+  g.total = 1;
+  int64_t off = 0, toff = 0, doff = 0;
+  for (int j = 0; j < n_modes; ++j) {
+    const int64_t n = dims[j];
+    g.dims[j] = n;
+    g.strides[j] = g.total;
+    g.total *= n;
+    f.u_row[j] = f.pool + off;
+    f.u_col[j] = f.pool + off + n * n;
+    f.uh_row[j] = f.pool + off + 2 * n * n;
+    f.uh_col[j] = f.pool + off + 3 * n * n;
+    off += 4 * n * n;
+    g.toff[j] = toff;
+    toff += n * n;
+    g.doff[j] = doff;
+    doff += n;
+  }
+  if (d_t) {
+    f.t_pool = f.pool + off;
+    f.diag_pool = f.pool + off + sq;
+    NDS_CUDA(cudaMemcpyAsync(f.t_pool, d_t, (size_t)sq * sizeof(double2), cudaMemcpyDeviceToDevice, ctx->stream));
+    NDS_CUDA(cudaMemcpyAsync(f.diag_pool, d_diag, (size_t)diag * sizeof(double2), cudaMemcpyDeviceToDevice,
+                             ctx->stream));
+  }
+  double2* raw = f.pool + 4 * sq + n_t + n_d;
+  NDS_CUDA(cudaMemcpyAsync(raw, d_u, (size_t)sq * sizeof(double2), cudaMemcpyDeviceToDevice, ctx->stream));
+  nds::factor_layouts_launch(f, raw, ctx->stream);
+  if (n_blk) nds::blocked_layouts_launch(f, raw + sq, ctx->stream);
+}
+
 // sylvester.cpp:29-33 — eps * sum_j ||T_j||_F (std::norm = re^2 + im^2, matrix.cpp:99-103).
 double default_tol(int n_modes, const int64_t* dims, const nds_z* const* t) {
   double s = 0.0;
@@ -423,7 +479,9 @@ std::vector<XPass> transform_passes(const nds_plan* p) {
 
 // Factors of a full solve's passes: the diagonalised all-binary route merges V_j^{-1} / V_j into
 // the outer modes' factors; stage APIs (merged = false) always use the plain U_j.
-const nds::FactorSet& pass_factors(const nds_plan* p, bool merged) { return merged && p->bin_diag ? p->fd : p->f; }
+const nds::FactorSet& pass_factors(const nds_plan* p, bool merged) {
+  return !merged ? p->f : p->bin_diag ? p->fd : p->cub_diag ? p->fc : p->f;
+}
 
 int launch_pass(nds_plan* p, const XPass& ps, bool adjoint, const double2* src, double2* dst, bool merged = false) {
   const nds::FactorSet& f = pass_factors(p, merged);
@@ -493,6 +551,7 @@ void build_solver(nds_plan* p) {
 int launch_solver(nds_plan* p, double2* c, cudaStream_t s, nds::Recorder* rec, bool merged = false) {
   if (p->solver->binary)
     return nds::binary_solve_launch(p->solver->bsp, p->f.t_pool, c, s, rec, merged && p->bin_diag);
+  if (merged && p->cub_diag) return nds::blk_backsub_launch(p->solver->sp, p->blk, p->fc.t_pool, c, s, rec);
   return nds::backsub_launch(p->solver->sp, p->f.t_pool, c, s, rec);
 }
 
@@ -513,7 +572,7 @@ int backsub_run(nds_plan* p, double2* c, bool merged = false) {
 void plan_binary_diag(nds_plan* p, const nds_z* const* u, const nds_z* const* t) {
   p->bin_diag = false;
   const int N = p->n_modes, m = 12;
-  if (p->fast_path || N <= m) return;
+  if (p->fast_path || N <= m || (p->flags & NDS_NO_DIAGONALISE)) return;
   for (int j = 0; j < N; ++j)
     if (p->dims[j] != 2) return;
   using cx = std::complex<double>;
@@ -530,6 +589,7 @@ void plan_binary_diag(nds_plan* p, const nds_z* const* u, const nds_z* const* t)
     const double s = 0.5 * (std::sqrt(b * b + 4.0) + b);
     cond *= s * s;
   }
+  p->bin_cond = cond;
   if (!(cond <= 1e6)) return;
   // per outer mode: [row-major | column-major] of W_fwd = V^{-1} U^H and W_inv = U V
   const int nb = N - m;
@@ -573,6 +633,198 @@ void plan_binary_diag(nds_plan* p, const nds_z* const* u, const nds_z* const* t)
     p->fd.uh_col[j] = o + 12;
   }
   p->bin_diag = true;
+}
+
+// Decide the block-diagonalised cubic route and build its factors. Every diagonal D_j x D_j block
+// T_q of T_j (D_j a multiple of the tile edge B dividing n_j) with distinct eigenvalues is
+// diagonalised by the upper triangular V_q of its unit-norm eigenvectors (T_q V_q = V_q diag(T_q));
+// with W_j = blockdiag(V_q),
+//   sum_j T_j = (x_j W_j) (sum_j W_j^{-1} T_j W_j) (x_j W_j)^{-1},
+// and T'_j = W_j^{-1} T_j W_j is block upper triangular with DIAGONAL diagonal blocks diag(T_j):
+// entries couple only across super-blocks of D_j rows, so the solve runs one launch per super-tile
+// level (backsub_blk.cuh; c1: 10 levels with D = 64 instead of 46 tile hyperplanes) and the
+// within-block couplings vanish from the work. W_j^{-1} merges into the forward factor
+// (W_j^{-1} U_j^H) and W_j into the inverse one (U_j W_j): the transform passes are unchanged in
+// number and cost, and den = sum_j T_j(i_j, i_j) is unchanged (the singular check and min |den|
+// hold as before). Guard: the forward error grows at most with cond_2(x_j W_j) =
+// prod_j max_q cond_2(V_q), kept <= 1e6 (the c4 route's bound; c1 measures 2.2e5 at D = 64,
+// c3 5.7e5 at D = 32, the advection-diffusion spectra of c2 ~1e15 already at D = 8 — c2 keeps the
+// wavefront route). D_j is grown greedily (doubling the mode whose product stays smallest) while
+// the bound holds. cond_2 is estimated by power iteration on V^H V and V^{-H} V^{-1}.
+constexpr double kCubicDiagCondMax = 1e6;
+
+using cxd = std::complex<double>;
+// ||M||_2 of a d x d column-major matrix: power iteration on M^H M from a fixed start
+double norm2_est(int d, const cxd* M) {
+  std::vector<cxd> x(d), y(d);
+  for (int i = 0; i < d; ++i) x[i] = cxd(1.0 + 0.37 * i, 0.11 * (i % 5));
+  double lam = 0.0;
+  for (int it = 0; it < 30; ++it) {
+    for (int r = 0; r < d; ++r) y[r] = 0.0;
+    for (int c = 0; c < d; ++c)
+      for (int r = 0; r < d; ++r) y[r] += M[r + c * d] * x[c];
+    double nx = 0.0;
+    for (int c = 0; c < d; ++c) {
+      cxd acc = 0.0;
+      for (int r = 0; r < d; ++r) acc += std::conj(M[r + c * d]) * y[r];
+      x[c] = acc;
+      nx += std::norm(acc);
+    }
+    nx = std::sqrt(nx);
+    if (!(nx > 0.0) || !std::isfinite(nx)) return std::numeric_limits<double>::infinity();
+    lam = nx;
+    for (auto& v : x) v /= nx;
+  }
+  return std::sqrt(lam);
+}
+// Eigenvectors (unit columns, upper triangular) and their inverse of the d x d diagonal block at
+// offset o of T (n x n column-major); returns cond_2 (inf when two eigenvalues coincide).
+double block_eig(const nds_z* t, int64_t n, int64_t o, int d, cxd* v, cxd* w) {
+  auto T = [&](int r, int c) { return cxd(t[(o + r) + (o + c) * n].re, t[(o + r) + (o + c) * n].im); };
+  for (int k = 0; k < d; ++k) {
+    for (int i = 0; i < d; ++i) v[i + k * d] = 0.0;
+    v[k + k * d] = 1.0;
+    const cxd lk = T(k, k);
+    for (int i = k - 1; i >= 0; --i) {
+      cxd acc = 0.0;
+      for (int l = i + 1; l <= k; ++l) acc += T(i, l) * v[l + k * d];
+      const cxd gap = lk - T(i, i);
+      if (std::abs(gap) == 0.0) return std::numeric_limits<double>::infinity();
+      v[i + k * d] = acc / gap;
+    }
+    double nn = 0.0;
+    for (int i = 0; i <= k; ++i) nn += std::norm(v[i + k * d]);
+    nn = std::sqrt(nn);
+    if (!std::isfinite(nn) || nn == 0.0) return std::numeric_limits<double>::infinity();
+    for (int i = 0; i <= k; ++i) v[i + k * d] /= nn;
+  }
+  for (int c = 0; c < d; ++c)  // V^{-1}: back substitution per column
+    for (int i = d - 1; i >= 0; --i) {
+      cxd acc = (i == c) ? 1.0 : 0.0;
+      for (int l = i + 1; l <= c; ++l) acc -= v[i + l * d] * w[l + c * d];
+      w[i + c * d] = i > c ? 0.0 : acc / v[i + i * d];
+    }
+  return norm2_est(d, v) * norm2_est(d, w);
+}
+
+void plan_cubic_diag(nds_plan* p, const nds_z* const* u, const nds_z* const* t) {
+  (void)u;
+  p->cub_diag = false;
+  if (p->fast_path || !p->solver || p->solver->binary || !p->solver->sp.v2 || (p->flags & NDS_NO_DIAGONALISE))
+    return;
+  const int N = p->n_modes;
+  const nds::TileGeom& tg = p->solver->sp.geom;
+  const int B = tg.b[0];
+  {  // the level kernel's 32-bit column offsets
+    int64_t span = 0;
+    for (int j = 0; j < N; ++j) span += (B - 1) * tg.strides[j];
+    if (span >= (int64_t)1 << 31) return;
+  }
+  // per mode: candidate D = B, 2B, .. dividing n_j; blocks evaluated lazily
+  struct Cand {
+    int d;
+    double cond = -1.0;
+    std::vector<cxd> v, w;  // per block d x d column-major, concatenated
+  };
+  std::vector<std::vector<Cand>> cands(N);
+  for (int j = 0; j < N; ++j)
+    for (int64_t d = B; d <= std::min<int64_t>(p->dims[j], 128); d *= 2)  // host eigensolves stay O(n 128^2)
+      if (p->dims[j] % d == 0) cands[j].push_back({(int)d});
+  auto eval = [&](int j, int ci) {
+    Cand& c = cands[j][ci];
+    if (c.cond >= 0.0) return c.cond;
+    const int64_t n = p->dims[j];
+    const int d = c.d, nb = (int)(n / d);
+    c.v.assign((size_t)n * d, 0.0);
+    c.w.assign((size_t)n * d, 0.0);
+    std::vector<double> cq(nb);
+#pragma omp parallel for schedule(dynamic, 1) if (nb > 1)
+    for (int q = 0; q < nb; ++q)
+      cq[q] = block_eig(t[j], n, (int64_t)q * d, d, c.v.data() + (size_t)q * d * d, c.w.data() + (size_t)q * d * d);
+    double mx = 0.0;
+    for (double x : cq) mx = std::max(mx, std::isfinite(x) ? x : std::numeric_limits<double>::infinity());
+    c.cond = mx;
+    return mx;
+  };
+  std::vector<int> sel(N, 0);
+  double prod = 1.0;
+  for (int j = 0; j < N; ++j) prod *= eval(j, 0);
+  p->cub_cond = prod;
+  if (!(prod <= kCubicDiagCondMax)) return;
+  for (;;) {  // grow the super-blocks: double the mode whose product stays smallest
+    int best = -1;
+    double best_prod = 0.0;
+    for (int j = 0; j < N; ++j) {
+      if (sel[j] + 1 >= (int)cands[j].size()) continue;
+      const double np = prod / cands[j][sel[j]].cond * eval(j, sel[j] + 1);
+      if (np <= kCubicDiagCondMax && (best < 0 || np < best_prod)) {
+        best = j;
+        best_prod = np;
+      }
+    }
+    if (best < 0) break;
+    ++sel[best];
+    prod = best_prod;
+  }
+  p->cub_cond = prod;
+  int d[NDS_MAX_MODES] = {};
+  for (int j = 0; j < N; ++j) d[j] = cands[j][sel[j]].d;
+  // device: M_inv = U W, M_fwd^H = U W^{-H} (uploaded as "U", so the set's U^H layouts hold
+  // W^{-1} U^H), T' = W^{-1} T W with its diagonal blocks set to diag(T) exactly
+  int64_t sq = 0, vb = 0;
+  for (int j = 0; j < N; ++j) {
+    sq += p->dims[j] * p->dims[j];
+    vb += p->dims[j] * d[j];
+  }
+  std::vector<double2> hv((size_t)2 * vb);
+  {
+    int64_t o = 0;
+    for (int j = 0; j < N; ++j) {
+      const Cand& c = cands[j][sel[j]];
+      for (size_t i = 0; i < c.v.size(); ++i) {
+        hv[o + i] = make_double2(c.v[i].real(), c.v[i].imag());
+        hv[vb + o + i] = make_double2(c.w[i].real(), c.w[i].imag());
+      }
+      o += (int64_t)c.v.size();
+    }
+  }
+  cudaStream_t s = p->ctx->stream;
+  double2* tmp = nullptr;  // [V | V^{-1}] [M_inv] [M_fwd^H] [T W] [T']
+  NDS_CUDA(cudaMallocFromPoolAsync(&tmp, (size_t)(2 * vb + 4 * sq) * sizeof(double2), p->ctx->pool, s));
+  NDS_CUDA(cudaMemcpyAsync(tmp, hv.data(), hv.size() * sizeof(double2), cudaMemcpyHostToDevice, s));
+  double2 *dv = tmp, *dw = tmp + vb, *minv = tmp + 2 * vb, *mfh = minv + sq, *tw = mfh + sq, *tpr = tw + sq;
+  {
+    int64_t o = 0, ov = 0;
+    for (int j = 0; j < N; ++j) {
+      const int64_t n = p->dims[j];
+      const double2* uj = p->f.u_col[j];  // U_j column-major (factor_layouts)
+      const double2* tj = p->f.t_pool + p->f.geom.toff[j];
+      nds::blockdiag_mul_launch(n, d[j], uj, dv + ov, true, false, minv + o, s);
+      nds::blockdiag_mul_launch(n, d[j], uj, dw + ov, true, true, mfh + o, s);
+      nds::blockdiag_mul_launch(n, d[j], tj, dv + ov, true, false, tw + o, s);
+      nds::blockdiag_mul_launch(n, d[j], tw + o, dw + ov, false, false, tpr + o, s);
+      nds::blockdiag_fix_launch(n, d[j], tj, tpr + o, s);
+      o += n * n;
+      ov += n * d[j];
+    }
+  }
+  // hv must stay alive until its copy ran: the device factor builds below are stream-ordered
+  device_factors(p->ctx, p->cd_inv, N, p->dims, minv, tpr, p->f.diag_pool);
+  device_factors(p->ctx, p->cd_fwd, N, p->dims, mfh, nullptr, nullptr);
+  NDS_CUDA(cudaFreeAsync(tmp, s));
+  NDS_CUDA(cudaStreamSynchronize(s));  // hv (pageable) copy complete before it goes out of scope
+  p->fc = p->cd_inv;
+  p->fc.pool = nullptr;  // owned by cd_inv / cd_fwd
+  for (int j = 0; j < N; ++j) {
+    p->fc.uh_row[j] = p->cd_fwd.uh_row[j];
+    p->fc.uh_col[j] = p->cd_fwd.uh_col[j];
+    for (int sh = 0; sh < 2; ++sh) {
+      p->fc.ablk[j][1][sh] = p->cd_fwd.ablk[j][1][sh];
+      p->fc.bblk[j][1][sh] = p->cd_fwd.bblk[j][1][sh];
+    }
+  }
+  nds::blk_solve_plan_build(p->blk, p->solver->sp, d);
+  p->cub_diag = true;
 }
 
 // Full path on device buffers: b -> (fwd) -> C -> (solve, in place) -> Y -> (inv) -> x.
@@ -649,7 +901,7 @@ int execute(nds_plan* p, const double2* b, double2* x, double2* work, cudaEvent_
   // that wait for it (c1: -0.27 ms); with N = 4 the hyperplanes fill within a few levels and the
   // groups fall behind (c2: +2.2 ms), so it stays off.
   const ModeView lastv = nds::mode_view(p->n_modes, p->dims, passes.back().mode);
-  const bool head = !p->fast_path && p->solver && !p->solver->binary && p->solver->sp.v2 &&
+  const bool head = !p->fast_path && !p->cub_diag && p->solver && !p->solver->binary && p->solver->sp.v2 &&
                     p->n_modes == 3 && passes.back().group < 0 && passes.back().mode == p->n_modes &&
                     lastv.outer == 1 && nds::gemm_rowm_ok(lastv);
   const int last_fwd = head ? N - 1 : N;
@@ -659,7 +911,7 @@ int execute(nds_plan* p, const double2* b, double2* x, double2* work, cudaEvent_
   // So the first inverse pass runs per mode-N block on a low-priority stream as soon as its level
   // completes (highest block first) — no accumulation, each piece writes its own slab — and only
   // the last block's piece remains after the solve.
-  const bool tail = !p->fast_path && p->solver && !p->solver->binary && p->solver->sp.v2 &&
+  const bool tail = !p->fast_path && !p->cub_diag && p->solver && !p->solver->binary && p->solver->sp.v2 &&
                     passes.front().group < 0 &&
                     passes.front().mode == 1 && p->n_modes >= 2 && p->solver->sp.geom.nb[p->n_modes - 1] <= 64;
   struct TailState {
@@ -696,7 +948,7 @@ int execute(nds_plan* p, const double2* b, double2* x, double2* work, cudaEvent_
         const nds::ModeView full = nds::mode_view(t.p->n_modes, t.p->dims, 1);
         nds::ModeView v = full;
         v.outer = v.outer / t.nbN * (t.next - lo + 1);
-        nds::mode_product_launch(t.p->f, 1, false, v, t.y + off, t.x + off, false, c->tail);
+        nds::mode_product_launch(pass_factors(t.p, true), 1, false, v, t.y + off, t.x + off, false, c->tail);
         ++t.launches;
         t.next = lo - 1;
       }
@@ -721,7 +973,7 @@ int execute(nds_plan* p, const double2* b, double2* x, double2* work, cudaEvent_
     NDS_CUDA(cudaStreamWaitEvent(p->ctx->side, p->ctx->hev[32], 0));
     for (int gq = 0; gq < groups; ++gq) {
       const int64_t hi = nbN - (int64_t)gq * per, lo = std::max<int64_t>(0, hi - per);
-      nds::mode_product_matrix_launch(p->f.uh_row[p->n_modes - 1] + lo * b * n, nullptr, lastv, src,
+      nds::mode_product_matrix_launch(pass_factors(p, true).uh_row[p->n_modes - 1] + lo * b * n, nullptr, lastv, src,
                                       c + lo * b * lastv.inner, false, p->ctx->side, (hi - lo) * b);
       NDS_CUDA(cudaEventRecord(p->ctx->hev[gq], p->ctx->side));
       ++launches;
@@ -806,6 +1058,7 @@ void plan_create_impl(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_
   if (!p->fast_path) {
     build_solver(p.get());
     plan_binary_diag(p.get(), u, t);
+    plan_cubic_diag(p.get(), u, t);
   }
   *out = p.release();
 }
@@ -815,6 +1068,9 @@ void plan_destroy_impl(nds_plan* p) {
   cudaSetDevice(p->ctx->device);
   for (auto e : p->pev) cudaEventDestroy(e);
   free_factors(p->f);
+  free_factors(p->cd_inv);
+  free_factors(p->cd_fwd);
+  nds::blk_solve_plan_free(p->blk);
   if (p->fd_buf) cudaFree(p->fd_buf);
   delete p;  // the shared solver structures stay cached in the context
 }
@@ -930,7 +1186,8 @@ void execute_host_impl(nds_plan* p, const nds_z* hb, nds_z* hx, nds_report* rep,
           ++launches;
           src = dst;
         }
-        nds::mode_product_matrix_launch(p->f.uh_row[lp.mode - 1] + k * slab, nullptr, ModeView{lv.inner, slab, 1}, src,
+        nds::mode_product_matrix_launch(pass_factors(p, true).uh_row[lp.mode - 1] + k * slab, nullptr,
+                                        ModeView{lv.inner, slab, 1}, src,
                                         W, k > 0, s, n, n);
         ++launches;
       }
@@ -944,7 +1201,8 @@ void execute_host_impl(nds_plan* p, const nds_z* hb, nds_z* hx, nds_report* rep,
       auto inv_buf = [&](int i) { return ((np - i) % 2 == 0) ? X : S3; };
       for (int k = 0; k < K; ++k) {
         double2* dst0 = inv_buf(1) + k * chunk;
-        nds::mode_product_matrix_launch(p->f.u_row[lp.mode - 1] + k * slab * n, nullptr, lv, c, dst0, false, s, slab);
+        nds::mode_product_matrix_launch(pass_factors(p, true).u_row[lp.mode - 1] + k * slab * n, nullptr, lv, c, dst0,
+                                        false, s, slab);
         ++launches;
         const double2* src = dst0;
         for (int j = 1; j < np; ++j) {
@@ -1546,6 +1804,12 @@ int nds_plan_solve_path(const nds_plan* plan) {
   if (!plan->solver) return -1;
   if (plan->solver->binary) return NDS_PATH_BINARY;
   return plan->solver->sp.v2 ? NDS_PATH_CUBIC : NDS_PATH_GENERIC;
+}
+
+int nds_plan_diagonalised(const nds_plan* plan, double* cond) {
+  if (!plan) return -1;
+  if (cond) *cond = plan->bin_diag ? plan->bin_cond : plan->cub_cond;
+  return plan->bin_diag || plan->cub_diag ? 1 : 0;
 }
 
 int nds_plan_profile_begin(nds_plan* plan, int max_launches) {

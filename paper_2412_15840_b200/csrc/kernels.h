@@ -167,6 +167,26 @@ struct SolverCache {
   ~SolverCache();
 };
 
+// Block-diagonalised cubic route (backsub_blk.cuh): super-blocks of d[j] rows per mode (multiples
+// of the tile edge), the cubic tiles grouped by super-tile level sum_j floor(I_j b / d_j)
+// (highest first; within a level longest pull first), one launch per level.
+struct BlkSolvePlan {
+  int d[NDS_MAX_MODES] = {};
+  int levels = 0;
+  std::vector<int64_t> level_off;
+  int64_t* d_tiles = nullptr;
+};
+void blk_solve_plan_build(BlkSolvePlan& bp, const SolvePlan& sp, const int* d);
+void blk_solve_plan_free(BlkSolvePlan& bp);
+int blk_backsub_launch(const SolvePlan& sp, const BlkSolvePlan& bp, const double2* t_pool, double2* c,
+                       cudaStream_t stream, Recorder* rec = nullptr);
+// out = A blockdiag(Bq) (right = true) or blockdiag(Bq) A, A and out n x n column-major, blocks
+// of d x d column-major at blk + q d^2; conj_t: use Bq^H. Then (fix_t) T' cleanup: entries of a
+// diagonal d-block set to diag_src's diagonal exactly, entries below the block diagonal zeroed.
+void blockdiag_mul_launch(int64_t n, int d, const double2* a, const double2* blk, bool right, bool conj_t,
+                          double2* out, cudaStream_t stream);
+void blockdiag_fix_launch(int64_t n, int d, const double2* diag_src, double2* t, cudaStream_t stream);
+
 void solve_plan_build(SolvePlan& sp, int n_modes, const int64_t* dims, const int64_t* toff);
 void solve_plan_free(SolvePlan& sp);
 // Head overlap: the last forward pass (mode N) produced in row groups of `per` mode-N tile blocks,

@@ -310,3 +310,45 @@ def test_binary_diagonalised_route_matches_coupled_solve(ctx, ref, n_modes, seed
     assert rel_max(x_stage, x_ref) <= 1e-12
     r = ctx.solve(a, b)  # host path (chunked passes) takes the diagonalised route too
     assert rel_max(r.x, x_ref) <= 1e-12
+
+
+DIAG_CASES = [("c1", (128, 128, 64), True), ("c1", (64, 64, 64), True), ("c3", (64, 64, 32, 32), True),
+              ("c3", (32, 32, 32, 32), True), ("c2", (32, 32, 32, 32), False)]
+
+
+@pytest.mark.parametrize("name,dims,taken", DIAG_CASES, ids=[f"{n}-{'x'.join(map(str, d))}" for n, d, _ in DIAG_CASES])
+def test_cubic_diagonalised_route(ctx, ref, name, dims, taken):
+    """Block-diagonalised cubic route (capi.cu plan_cubic_diag): full solves replace T_j by
+    W_j^{-1} T_j W_j (W_j = eigenvectors of T_j's diagonal tile blocks), so the diagonal tiles are
+    divisions. The guard takes it for the Gaussian configs (c1, c3) and refuses the clustered
+    advection-diffusion spectra (c2). The route, the wavefront route (NO_DIAGONALISE) and the stage
+    APIs (plain factors) all match the reference's X at the north_star tolerance."""
+    import torch
+    a, b = configs.make_problem(name, seed=1, dims=dims)
+    x_ref, _ = ref.solve(a, b)
+    us, ts = zip(*[ctx.schur(m) for m in a])
+    d_b = torch.from_numpy(np.ascontiguousarray(b.ravel(order="F"))).cuda()
+    ctx.set_stream(torch.cuda.current_stream().cuda_stream)
+    xs = {}
+    for diag in (True, False):
+        plan = ctx.plan(list(us), list(ts), diagonalise=diag)
+        assert plan.solve_path() == "cubic"
+        got, cond = plan.diagonalised()
+        assert got == (taken and diag)
+        if diag and taken:
+            assert 1.0 <= cond <= 1e6
+        d_x, d_w, d_c = torch.empty_like(d_b), torch.empty_like(d_b), torch.empty_like(d_b)
+        plan.execute(d_b.data_ptr(), d_x.data_ptr(), d_w.data_ptr())
+        plan.forward(d_b.data_ptr(), d_c.data_ptr(), d_w.data_ptr())
+        plan.backsub(d_c.data_ptr())
+        plan.inverse(d_c.data_ptr(), d_c.data_ptr(), d_w.data_ptr())
+        torch.cuda.synchronize()
+        xs[diag] = d_x.cpu().numpy().reshape(b.shape, order="F")
+        x_stage = d_c.cpu().numpy().reshape(b.shape, order="F")
+        assert rel_max(x_stage, x_ref) <= 1e-11
+        plan.close()
+    ctx.set_stream(None)
+    assert rel_max(xs[True], x_ref) <= 1e-11
+    assert rel_max(xs[False], x_ref) <= 1e-11
+    r = ctx.solve(a, b)  # host path (chunked passes, split last pass) on the same route
+    assert rel_max(r.x, x_ref) <= 1e-11
