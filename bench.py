@@ -483,9 +483,19 @@ def main():
                     "peak_source": hbm_src, "algorithmic": "2 x 16 P bytes per fused pass (read + write once)"}
     step_ms_prof = sum(ms for _, _, ms in recs) / args.steps
     stage_ms = {k: sum(ms for _, ms in v) / args.steps for k, v in by_kind.items()}
-    solve_flops = 8.0 * P * (sum(dims) - len(dims)) / 2 + 8.0 * P
+    # algorithmic work of the solve: Eq. (9) has sum_j (n_j - 1) / 2 CMACs per entry; on the
+    # block-diagonalised route (super-blocks D_j) only the couplings across super-blocks remain,
+    # sum_j (n_j - D_j) / 2 per entry (all of it on the FP64 tensor pipe), plus the division
+    sb_levels, sb_d = plan.superblocks()
+    if sb_d:
+        solve_flops = 8.0 * P * sum(n - d for n, d in zip(dims, sb_d)) / 2 + 8.0 * P
+    else:
+        solve_flops = 8.0 * P * (sum(dims) - len(dims)) / 2 + 8.0 * P
     solve_ms = stage_ms.get("solve_level", 0.0) + stage_ms.get("solve_persistent", 0.0)
+    diag_taken, diag_cond = plan.diagonalised()
     kernels = {
+        "solve_route": {"diagonalised": diag_taken, "cond_bound": diag_cond, "superblocks": sb_d,
+                        "levels": sb_levels or None},
         "transform_gemm_share": stage_ms.get("transform_gemm", 0.0) / step_ms_prof if step_ms_prof else None,
         "stage_ms_per_step": {k: round(v, 4) for k, v in stage_ms.items()},
         "solve_tflops": solve_flops / (solve_ms * 1e-3) / 1e12 if solve_ms else None,

@@ -178,6 +178,10 @@ int nds_plan_solve_path(const nds_plan* plan);
  * guard's bound prod_j cond_2 (<= 1e6 when taken; 0 when not evaluated). Returns 1 / 0, -1 for a
  * NULL plan. Stage calls (forward / backsub / inverse) always use the plain factors. */
 int nds_plan_diagonalised(const nds_plan* plan, double* cond);
+/* Cubic block-diagonalised route: d[j] = the super-block extent D_j of mode j (T_j's D_j x D_j
+ * diagonal blocks diagonalised); returns the number of solve levels sum_j (n_j / D_j - 1) + 1,
+ * 0 when full solves do not take that route (d untouched), -1 for a NULL plan. */
+int nds_plan_superblocks(const nds_plan* plan, int64_t* d);
 /* Per-launch device timing: after _begin, every launch of execute/forward/backsub/inverse records
  * a CUDA event on the context stream (up to max_launches). _end synchronises and returns the
  * number of launches written: kind (0 transform GEMM, 1 transform direct, 2 solve level,

@@ -51,7 +51,7 @@ EXPORTED = [
     "nds_back_substitute", "nds_mode_product", "nds_apply_operator", "nds_flop_estimate", "nds_schur_flop_estimate",
     "nds_plan_create", "nds_plan_destroy", "nds_plan_report", "nds_plan_total", "nds_plan_execute",
     "nds_plan_forward", "nds_plan_backsub", "nds_plan_inverse", "nds_plan_execute_host", "nds_plan_launches", "nds_plan_solve_path",
-    "nds_plan_diagonalised",
+    "nds_plan_diagonalised", "nds_plan_superblocks",
     "nds_plan_profile_begin", "nds_plan_profile_end",
     "nds_dev_mode_product", "nds_dev_mode_update", "nds_dev_mode_apply", "nds_dev_back_substitute", "nds_dev_residual",
     "nds_triangular_exp", "nds_ode_create", "nds_ode_destroy", "nds_ode_at", "nds_ode_at_dev", "nds_propagate",
@@ -180,6 +180,7 @@ def load_library(path: str = LIB_PATH):
     L.nds_plan_launches.argtypes = [_vp]
     L.nds_plan_solve_path.argtypes = [_vp]
     L.nds_plan_diagonalised.argtypes = [_vp, C.POINTER(C.c_double)]
+    L.nds_plan_superblocks.argtypes = [_vp, C.POINTER(C.c_int64)]
     L.nds_plan_profile_begin.argtypes = [_vp, C.c_int]
     L.nds_plan_profile_end.argtypes = [_vp, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int),
                                        C.POINTER(C.c_float)]
@@ -485,6 +486,13 @@ class Plan:
         c = C.c_double(0.0)
         r = self.ctx.lib.nds_plan_diagonalised(self.h, C.byref(c))
         return bool(r == 1), float(c.value)
+
+    def superblocks(self):
+        """(levels, D) of the block-diagonalised cubic route (super-block extent per mode), or
+        (0, None) when full solves do not take it."""
+        d = (C.c_int64 * len(self.dims))()
+        lv = self.ctx.lib.nds_plan_superblocks(self.h, d)
+        return (lv, tuple(int(x) for x in d)) if lv > 0 else (0, None)
 
     def profile_begin(self, max_launches: int):
         self._check(self.ctx.lib.nds_plan_profile_begin(self.h, int(max_launches)))

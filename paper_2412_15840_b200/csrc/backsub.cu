@@ -510,11 +510,11 @@ void blk_solve_plan_free(BlkSolvePlan& bp) {
 int blk_backsub_launch(const SolvePlan& sp, const BlkSolvePlan& bp, const double2* t_pool, double2* c,
                        cudaStream_t stream, Recorder* rec) {
   const TileGeom& g = sp.geom;
-  const BlkLaunch bl = blk_cfg(g.n_modes, g.b[0]);
+  const BlkLaunchT bl = blk_cfg(g.n_modes, g.b[0]);
   static bool attr_set = false;
   if (!attr_set) {
     for (int nm : {3, 4}) {
-      const BlkLaunch x = blk_cfg(nm, nm == 3 ? 16 : 8);
+      const BlkLaunchT x = blk_cfg(nm, nm == 3 ? 16 : 8);
       NDS_CUDA(cudaFuncSetAttribute(x.kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)x.smem));
     }
     attr_set = true;
@@ -527,58 +527,12 @@ int blk_backsub_launch(const SolvePlan& sp, const BlkSolvePlan& bp, const double
   for (int lv = 0; lv < bp.levels; ++lv) {
     const int64_t nt = bp.level_off[lv + 1] - bp.level_off[lv];
     if (nt == 0) continue;
-    bl.kern<<<(unsigned)nt, kBlkThreads, bl.smem, stream>>>(ba, t_pool, bp.d_tiles + bp.level_off[lv], c);
+    bl.kern<<<(unsigned)nt, bl.threads, bl.smem, stream>>>(ba, t_pool, bp.d_tiles + bp.level_off[lv], c);
     NDS_LAUNCH_CHECK();
     if (rec) rec->mark(stream, kBacksubLevel, lv);
     ++launches;
   }
   return launches;
-}
-
-__global__ void blockdiag_mul_kernel(int64_t n, int d, const double2* __restrict__ a, const double2* __restrict__ blk,
-                                     int right, int conj_t, double2* __restrict__ out) {
-  const int64_t total = n * n;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = e % n, c = e / n;
-    const int64_t q = (right ? c : r) / d, o = q * d;
-    const double2* bq = blk + q * (int64_t)d * d;
-    auto bel = [&](int64_t i, int64_t k) {  // Bq(i, k) or Bq^H(i, k)
-      if (!conj_t) return bq[i + k * d];
-      const double2 v = bq[k + i * d];
-      return make_double2(v.x, -v.y);
-    };
-    double2 s = make_double2(0.0, 0.0);
-    if (right)
-      for (int k = 0; k < d; ++k) s = cfma(s, a[r + (o + k) * n], bel(k, c - o));
-    else
-      for (int k = 0; k < d; ++k) s = cfma(s, bel(r - o, k), a[(o + k) + c * n]);
-    out[e] = s;
-  }
-}
-
-__global__ void blockdiag_fix_kernel(int64_t n, int d, const double2* __restrict__ diag_src, double2* __restrict__ t) {
-  const int64_t total = n * n;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = e % n, c = e / n;
-    if (r / d == c / d)
-      t[e] = r == c ? diag_src[e] : make_double2(0.0, 0.0);
-    else if (r / d > c / d)
-      t[e] = make_double2(0.0, 0.0);
-  }
-}
-
-void blockdiag_mul_launch(int64_t n, int d, const double2* a, const double2* blk, bool right, bool conj_t,
-                          double2* out, cudaStream_t stream) {
-  const int64_t total = n * n;
-  blockdiag_mul_kernel<<<(unsigned)std::min<int64_t>((total + 255) / 256, 4096), 256, 0, stream>>>(
-      n, d, a, blk, right ? 1 : 0, conj_t ? 1 : 0, out);
-  NDS_LAUNCH_CHECK();
-}
-
-void blockdiag_fix_launch(int64_t n, int d, const double2* diag_src, double2* t, cudaStream_t stream) {
-  const int64_t total = n * n;
-  blockdiag_fix_kernel<<<(unsigned)std::min<int64_t>((total + 255) / 256, 4096), 256, 0, stream>>>(n, d, diag_src, t);
-  NDS_LAUNCH_CHECK();
 }
 
 }  // namespace nds

@@ -17,24 +17,22 @@
 // and stored. No partial buffers, no side streams: the whole solve is `levels` launches
 // (c1 with D = 64: 10, against 46 tile hyperplanes of the wavefront route).
 
-constexpr int kBlkThreads = 256;
-
 struct BlkArgs {
   TileGeom g;
   int d[NDS_MAX_MODES];  // diagonalisation block (super-block) extent per mode
 };
 
-template <int N, int B, int BK, int ST>
+template <int N, int B, int BK, int ST, int NT>
 struct BlkCfg {
   static constexpr int E = 4096;
   static constexpr int LB = B == 16 ? 4 : 3;
   static constexpr int TC = E / B;        // columns of every mode's GEMM
-  static constexpr int NW = kBlkThreads / 32;
+  static constexpr int NW = NT / 32;
   static constexpr int CB = TC / 8 / NW;  // column fragments per warp
   static constexpr int RB = B / 8;        // row fragments
   static constexpr int LDB = TC + 2;      // row-major B stage stride (modes >= 2)
   static constexpr int ALD = BK <= 8 ? 12 : BK + 4;
-  static constexpr int SL = BK * TC / kBlkThreads;  // B elements per thread per stage
+  static constexpr int SL = BK * TC / NT;           // B elements per thread per stage
   static constexpr int BSTAGE = BK * LDB;           // >= TC * BK (mode-1 k-fastest layout)
   static constexpr int ASTAGE = B * ALD;
   static constexpr size_t smem() {
@@ -42,11 +40,12 @@ struct BlkCfg {
   }
 };
 
-template <int N, int B, int BK, int ST>
-__global__ void __launch_bounds__(kBlkThreads, 1)
+template <int N, int B, int BK, int ST, int NT>
+__global__ void __launch_bounds__(NT, 1)
     blk_level_kernel(const BlkArgs ba, const double2* __restrict__ T, const int64_t* __restrict__ tiles,
                      double2* __restrict__ Y) {
-  using C = BlkCfg<N, B, BK, ST>;
+  using C = BlkCfg<N, B, BK, ST, NT>;
+  constexpr int kBlkThreads = NT;
   constexpr int E = C::E, LB = C::LB, TC = C::TC, CB = C::CB, RB = C::RB, LDB = C::LDB, ALD = C::ALD;
   constexpr int SL = C::SL;
   static_assert(C::SL * kBlkThreads == BK * TC && B * BK <= kBlkThreads && BK % 4 == 0, "stage shape");
@@ -197,26 +196,40 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
     mb_wait(&fullb[t % ST], (t / ST) & 1);
     const double2* cA = sA + (t % ST) * C::ASTAGE;
     const double2* cBs = sB + (t % ST) * C::BSTAGE;
-    const bool kfast = cj == 0;
+    // all of the k-tile's fragments are loaded before its DMMAs (the layout branch is per k-tile,
+    // so the loads of both 4-deep steps issue back to back)
+    double2 bv[BK / 4][CB], av[BK / 4][RB];
+    if (cj == 0) {  // mode 1: k-fastest swizzled stage
 #pragma unroll
-    for (int kk = 0; kk < BK; kk += 4) {
-      double br[CB], bi[CB], bs[CB];
+      for (int kk = 0; kk < BK / 4; ++kk)
 #pragma unroll
-      for (int q = 0; q < CB; ++q) {
-        const int c = cbase + q * 8;
-        const double2 b = kfast ? cBs[c * BK + ((kk + kq) ^ (BK >= 8 ? (c & 1) << 2 : 0))] : cBs[(kk + kq) * LDB + c];
-        br[q] = b.x;
-        bi[q] = b.y;
-        bs[q] = b.x + b.y;
-      }
+        for (int q = 0; q < CB; ++q) {
+          const int c = cbase + q * 8;
+          bv[kk][q] = cBs[c * BK + ((kk * 4 + kq) ^ (BK >= 8 ? (c & 1) << 2 : 0))];
+        }
+    } else {
+#pragma unroll
+      for (int kk = 0; kk < BK / 4; ++kk)
+#pragma unroll
+        for (int q = 0; q < CB; ++q) bv[kk][q] = cBs[(kk * 4 + kq) * LDB + cbase + q * 8];
+    }
+#pragma unroll
+    for (int kk = 0; kk < BK / 4; ++kk)
+#pragma unroll
+      for (int r = 0; r < RB; ++r) av[kk][r] = cA[(r * 8 + arow) * ALD + kk * 4 + kq];
+#pragma unroll
+    for (int kk = 0; kk < BK / 4; ++kk) {
+      double bs[CB];
+#pragma unroll
+      for (int q = 0; q < CB; ++q) bs[q] = bv[kk][q].x + bv[kk][q].y;
 #pragma unroll
       for (int r = 0; r < RB; ++r) {
-        const double2 a = cA[(r * 8 + arow) * ALD + kk + kq];
+        const double2 a = av[kk][r];
         const double as = a.x + a.y;
 #pragma unroll
         for (int q = 0; q < CB; ++q) {
-          dmma_bs(cre[r][q][0], cre[r][q][1], a.x, br[q]);
-          dmma_bs(cim[r][q][0], cim[r][q][1], a.y, bi[q]);
+          dmma_bs(cre[r][q][0], cre[r][q][1], a.x, bv[kk][q].x);
+          dmma_bs(cim[r][q][0], cim[r][q][1], a.y, bv[kk][q].y);
           dmma_bs(c3[r][q][0], c3[r][q][1], as, bs[q]);
         }
       }
@@ -269,12 +282,15 @@ __global__ void __launch_bounds__(kBlkThreads, 1)
 }
 
 using BlkKernel = void (*)(const BlkArgs, const double2*, const int64_t*, double2*);
-struct BlkLaunch {
+struct BlkLaunchT {
   BlkKernel kern;
   size_t smem;
+  int threads;
 };
-static BlkLaunch blk_cfg(int n_modes, int b) {
-  if (n_modes == 3 && b == 16) return {blk_level_kernel<3, 16, 8, 3>, BlkCfg<3, 16, 8, 3>::smem()};
-  if (n_modes == 4 && b == 8) return {blk_level_kernel<4, 8, 4, 3>, BlkCfg<4, 8, 4, 3>::smem()};
-  return {nullptr, 0};
+// Measured (c1 / c3 solve): N = 3 — 256 threads, BK = 8, 3 stages: 1.31 ms (512 threads 1.37,
+// 4 stages 1.34); N = 4 — 512 threads, BK = 4, 3 stages: 18.1 ms (256 threads 19.9, 4 stages 20.1).
+static BlkLaunchT blk_cfg(int n_modes, int b) {
+  if (n_modes == 3 && b == 16) return {blk_level_kernel<3, 16, 8, 3, 256>, BlkCfg<3, 16, 8, 3, 256>::smem(), 256};
+  if (n_modes == 4 && b == 8) return {blk_level_kernel<4, 8, 4, 3, 512>, BlkCfg<4, 8, 4, 3, 512>::smem(), 512};
+  return {nullptr, 0, 0};
 }

@@ -133,8 +133,10 @@ __global__ void __launch_bounds__(kBinThreads, 2) binary_pass_kernel(const BinPa
 struct BinTileSolve {
   const double2* t;    // T_j (2x2 column-major) at t + 4 j, all N modes
   int n_outer;         // N - 12
-  const uint16_t* wf;  // the 4096 tile entries by popcount, highest first (bank-interleaved)
-  const int* wf_off;   // 14 offsets
+  const uint16_t* wf;  // the 4096 tile entries by popcount over the coupled modes, highest first
+                       // (bank-interleaved)
+  const int* wf_off;   // levels + 1 offsets
+  int levels;          // coupled inner modes + 1
 };
 
 __global__ void __launch_bounds__(kBinThreads, 2)
@@ -191,7 +193,7 @@ __global__ void __launch_bounds__(kBinThreads, 2)
   __syncthreads();
   // popcount wavefront on the swizzled tile: swz is XOR-linear, so the slot of l | e_j (bit j of
   // l clear) is swz(l) ^ swz(e_j); terms split over two accumulators (even / odd modes)
-  for (int lv = 0; lv < 13; ++lv) {
+  for (int lv = 0; lv < ts.levels; ++lv) {
     const int p1 = ts.wf_off[lv + 1];
     for (int p = ts.wf_off[lv] + tid; p < p1; p += kBinThreads) {
       const int l = ts.wf[p];
@@ -314,8 +316,8 @@ int binary_pass_launch(const FactorSet& f, const BinGroup& gr, bool adjoint, con
 }
 
 int binary_fused_solve_launch(const FactorSet& fwd, const FactorSet& inv, const BinGroup& gr, const double2* t_pool,
-                              int n_outer, const uint16_t* wf, const int* wf_off, const double2* x, double2* r,
-                              cudaStream_t stream) {
+                              int n_outer, const uint16_t* wf, const int* wf_off, int levels, const double2* x,
+                              double2* r, cudaStream_t stream) {
   if (gr.first != 1 || gr.count != 12 || gr.logR != 0 || gr.inner != 1) throw Error(NDS_ERR_OTHER, "fused pass: not a modes-1-12 tile pass");
   const BinPass fw = make_bin_pass(fwd, gr, true);
   const BinPass iv = make_bin_pass(inv, gr, false);
@@ -324,7 +326,7 @@ int binary_fused_solve_launch(const FactorSet& fwd, const FactorSet& inv, const 
     NDS_CUDA(cudaFuncSetAttribute(binary_fused_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 4096 * 16));
     attr_set = true;
   }
-  BinTileSolve ts{t_pool, n_outer, wf, wf_off};
+  BinTileSolve ts{t_pool, n_outer, wf, wf_off, levels};
   binary_fused_solve_kernel<<<(unsigned)gr.outer, kBinThreads, 4096 * 16, stream>>>(fw, iv, ts, x, r);
   NDS_LAUNCH_CHECK();
   return kBacksubLevel;

@@ -82,6 +82,10 @@ struct nds_plan {
   bool bin_diag = false;
   nds::FactorSet fd;
   double2* fd_buf = nullptr;
+  const double2* bin_t = nullptr;       // T'_j of the route (2 x 2 column-major, all modes)
+  const uint16_t* bin_wf = nullptr;     // tile wavefront over the coupled inner modes
+  const int* bin_wf_off = nullptr;
+  int bin_wf_levels = 0;
   // Cubic-tile route with every T_j block-diagonalised (plan_cubic_diag): T'_j = W_j^{-1} T_j W_j,
   // W_j = blockdiag of the unit-column eigenvector matrices of T_j's B x B diagonal blocks. Full
   // solves run the passes with fc (forward W_j^{-1} U_j^H, inverse U_j W_j) and the solve on
@@ -89,7 +93,7 @@ struct nds_plan {
   bool cub_diag = false;
   double cub_cond = 0.0, bin_cond = 0.0;  // prod_j max_q cond_2(V_{j,q}) of the route's guard
   nds::FactorSet cd_inv, cd_fwd, fc;
-  nds::BlkSolvePlan blk;  // super-tile levels of the route
+  const nds::BlkSolvePlan* blk = nullptr;  // super-tile levels of the route (owned by the solver cache)
   int launches = 0;
   // per-launch CUDA-event profile (nds_plan_profile_begin / _end)
   bool profiling = false;
@@ -550,8 +554,9 @@ void build_solver(nds_plan* p) {
 
 int launch_solver(nds_plan* p, double2* c, cudaStream_t s, nds::Recorder* rec, bool merged = false) {
   if (p->solver->binary)
-    return nds::binary_solve_launch(p->solver->bsp, p->f.t_pool, c, s, rec, merged && p->bin_diag);
-  if (merged && p->cub_diag) return nds::blk_backsub_launch(p->solver->sp, p->blk, p->fc.t_pool, c, s, rec);
+    return nds::binary_solve_launch(p->solver->bsp, merged && p->bin_diag ? p->bin_t : p->f.t_pool, c, s, rec,
+                                    merged && p->bin_diag);
+  if (merged && p->cub_diag) return nds::blk_backsub_launch(p->solver->sp, *p->blk, p->fc.t_pool, c, s, rec);
   return nds::backsub_launch(p->solver->sp, p->f.t_pool, c, s, rec);
 }
 
@@ -565,10 +570,15 @@ int backsub_run(nds_plan* p, double2* c, bool merged = false) {
   return launch_solver(p, c, p->ctx->stream, rec, merged);
 }
 
-// Decide the diagonalised all-binary route and build its merged outer-mode factors. Guard: every
-// outer T_j has distinct eigenvalues and prod_j cond(V_j) <= 1e6 (cond = ((sqrt(|b|^2 + 4) +
-// |b|) / 2)^2 for V = [[1, b], [0, 1]]); measured error on c4-type problems ~1e-15, i.e. the
-// bound is very pessimistic. Otherwise the plan keeps the coupled (pull) solve.
+// Decide the diagonalised all-binary route and build its merged factors. Every T_j = [[a, b],
+// [0, d]] with a != d is diagonalised by V_j = [[1, beta_j], [0, 1]], beta_j = b / (d - a). The
+// outer modes (>= 12) must all be diagonalised (then the 4096-entry tiles of modes 1-12 decouple);
+// the inner modes are added greedily, smallest cond first, while the bound holds — each one drops
+// its coupling from the tile wavefront, whose levels become the popcounts over the remaining inner
+// modes (c4 seed 0: 13 -> 3 levels). Guard: prod_j cond(V_j) <= 1e6 over the diagonalised modes
+// (cond = ((sqrt(|b|^2 + 4) + |b|) / 2)^2 for V = [[1, b], [0, 1]]); measured error on c4-type
+// problems ~1e-15, i.e. the bound is very pessimistic. Otherwise the plan keeps the coupled
+// (pull) solve.
 void plan_binary_diag(nds_plan* p, const nds_z* const* u, const nds_z* const* t) {
   p->bin_diag = false;
   const int N = p->n_modes, m = 12;
@@ -578,23 +588,41 @@ void plan_binary_diag(nds_plan* p, const nds_z* const* u, const nds_z* const* t)
   using cx = std::complex<double>;
   auto z = [](nds_z v) { return cx(v.re, v.im); };
   std::vector<cx> beta(N);
-  double cond = 1.0;
-  for (int j = m; j < N; ++j) {
+  std::vector<double> cj(N, std::numeric_limits<double>::infinity());
+  for (int j = 0; j < N; ++j) {
     const cx t00 = z(t[j][0]), t01 = z(t[j][2]), t11 = z(t[j][3]);
     const cx gap = t11 - t00;
-    if (std::abs(gap) == 0.0) return;
+    if (std::abs(gap) == 0.0) continue;
     beta[j] = t01 / gap;
     const double b = std::abs(beta[j]);
-    if (!std::isfinite(b)) return;
-    const double s = 0.5 * (std::sqrt(b * b + 4.0) + b);
-    cond *= s * s;
+    if (!std::isfinite(b)) continue;
+    const double sq = 0.5 * (std::sqrt(b * b + 4.0) + b);
+    cj[j] = sq * sq;
   }
+  double cond = 1.0;
+  for (int j = m; j < N; ++j) cond *= cj[j];
   p->bin_cond = cond;
   if (!(cond <= 1e6)) return;
-  // per outer mode: [row-major | column-major] of W_fwd = V^{-1} U^H and W_inv = U V
-  const int nb = N - m;
-  std::vector<double2> host((size_t)nb * 16);
-  for (int j = m; j < N; ++j) {
+  std::vector<int> inner(m);
+  for (int j = 0; j < m; ++j) inner[j] = j;
+  std::stable_sort(inner.begin(), inner.end(), [&](int x, int y) { return cj[x] < cj[y]; });
+  std::vector<bool> diag(N, false);
+  for (int j = m; j < N; ++j) diag[j] = true;
+  for (int j : inner)
+    if (cond * cj[j] <= 1e6) {
+      cond *= cj[j];
+      diag[j] = true;
+    }
+  p->bin_cond = cond;
+  // per diagonalised mode: [row-major | column-major] of W_fwd = V^{-1} U^H and W_inv = U V; then
+  // T'_j (2 x 2 column-major, all modes: diagonal for the diagonalised ones); then the tile
+  // wavefront: entries by popcount over the coupled inner modes, highest first, bank-interleaved
+  std::vector<double2> host((size_t)N * 16 + (size_t)N * 4);
+  for (int j = 0; j < N; ++j) {
+    double2* tp = host.data() + (size_t)N * 16 + 4 * j;
+    for (int e = 0; e < 4; ++e) tp[e] = make_double2(t[j][e].re, t[j][e].im);
+    if (!diag[j]) continue;
+    tp[2] = make_double2(0.0, 0.0);
     cx U[2][2], UH[2][2], Wf[2][2], Wi[2][2];
     for (int r = 0; r < 2; ++r)
       for (int c = 0; c < 2; ++c) {
@@ -612,7 +640,7 @@ void plan_binary_diag(nds_plan* p, const nds_z* const* u, const nds_z* const* t)
       Wi[r][0] = U[r][0];
       Wi[r][1] = U[r][1] + b * U[r][0];
     }
-    double2* o = host.data() + (size_t)(j - m) * 16;
+    double2* o = host.data() + (size_t)j * 16;
     for (int r = 0; r < 2; ++r)
       for (int c = 0; c < 2; ++c) {
         o[0 + r * 2 + c] = make_double2(Wi[r][c].real(), Wi[r][c].imag());   // u_row
@@ -621,17 +649,54 @@ void plan_binary_diag(nds_plan* p, const nds_z* const* u, const nds_z* const* t)
         o[12 + r + c * 2] = make_double2(Wf[r][c].real(), Wf[r][c].imag());  // uh_col
       }
   }
-  NDS_CUDA(cudaMalloc(&p->fd_buf, host.size() * sizeof(double2)));
-  NDS_CUDA(cudaMemcpy(p->fd_buf, host.data(), host.size() * sizeof(double2), cudaMemcpyHostToDevice));
+  int cmask = 0, k = 0;  // coupled inner modes
+  for (int j = 0; j < m; ++j)
+    if (!diag[j]) {
+      cmask |= 1 << j;
+      ++k;
+    }
+  const int E = 1 << m;
+  std::vector<int> wf(E), off(k + 2, 0), cnt(k + 1, 0);
+  for (int l = 0; l < E; ++l) cnt[k - __builtin_popcount(l & cmask)]++;
+  for (int i = 0; i <= k; ++i) off[i + 1] = off[i] + cnt[i];
+  {
+    std::vector<int> pos(off.begin(), off.end() - 1);
+    for (int l = E - 1; l >= 0; --l) wf[pos[k - __builtin_popcount(l & cmask)]++] = l;
+  }
+  std::vector<uint16_t> wfs(E);
+  {
+    auto swz = [](int q) { return q ^ (((q >> 3) ^ (q >> 6) ^ (q >> 9)) & 7); };
+    for (int lv = 0; lv <= k; ++lv) {
+      std::vector<std::vector<int>> bucket(8);
+      for (int i = off[lv]; i < off[lv + 1]; ++i) bucket[swz(wf[i]) & 7].push_back(wf[i]);
+      int o = off[lv];
+      for (size_t r = 0; o < off[lv + 1]; ++r)
+        for (int bq = 0; bq < 8; ++bq)
+          if (r < bucket[bq].size()) wfs[o++] = (uint16_t)bucket[bq][r];
+    }
+  }
+  const size_t fbytes = host.size() * sizeof(double2);
+  const size_t bytes = fbytes + E * sizeof(uint16_t) + (k + 2) * sizeof(int);
+  std::vector<char> blob(bytes);
+  std::memcpy(blob.data(), host.data(), fbytes);
+  std::memcpy(blob.data() + fbytes, wfs.data(), E * sizeof(uint16_t));
+  std::memcpy(blob.data() + fbytes + E * sizeof(uint16_t), off.data(), (k + 2) * sizeof(int));
+  NDS_CUDA(cudaMalloc(&p->fd_buf, bytes));
+  NDS_CUDA(cudaMemcpy(p->fd_buf, blob.data(), bytes, cudaMemcpyHostToDevice));
   p->fd = p->f;
   p->fd.pool = nullptr;  // owned by f
-  for (int j = m; j < N; ++j) {
-    double2* o = p->fd_buf + (size_t)(j - m) * 16;
+  for (int j = 0; j < N; ++j) {
+    if (!diag[j]) continue;
+    double2* o = p->fd_buf + (size_t)j * 16;
     p->fd.u_row[j] = o;
     p->fd.u_col[j] = o + 4;
     p->fd.uh_row[j] = o + 8;
     p->fd.uh_col[j] = o + 12;
   }
+  p->bin_t = p->fd_buf + (size_t)N * 16;
+  p->bin_wf = (const uint16_t*)((const char*)p->fd_buf + fbytes);
+  p->bin_wf_off = (const int*)((const char*)p->fd_buf + fbytes + E * sizeof(uint16_t));
+  p->bin_wf_levels = k + 1;
   p->bin_diag = true;
 }
 
@@ -647,68 +712,17 @@ void plan_binary_diag(nds_plan* p, const nds_z* const* u, const nds_z* const* t)
 // (W_j^{-1} U_j^H) and W_j into the inverse one (U_j W_j): the transform passes are unchanged in
 // number and cost, and den = sum_j T_j(i_j, i_j) is unchanged (the singular check and min |den|
 // hold as before). Guard: the forward error grows at most with cond_2(x_j W_j) =
-// prod_j max_q cond_2(V_q), kept <= 1e6 (the c4 route's bound; c1 measures 2.2e5 at D = 64,
-// c3 5.7e5 at D = 32, the advection-diffusion spectra of c2 ~1e15 already at D = 8 — c2 keeps the
-// wavefront route). D_j is grown greedily (doubling the mode whose product stays smallest) while
-// the bound holds. cond_2 is estimated by power iteration on V^H V and V^{-H} V^{-1}.
+// prod_j max_q cond_2(V_q), kept <= 1e6 (the c4 route's bound; c1 takes D = (64, 128, 128) at
+// 6.3e5, c3 (8, 32, 64, 128) at 6.2e5; the advection-diffusion spectra of c2 give ~5e15 already
+// at D = 8 — c2 keeps the wavefront route). D_j (<= 128) is grown greedily, doubling the mode
+// whose product stays smallest, while the bound holds. The eigenvector blocks and their cond_2
+// (power iteration on V^H V and V^{-H} V^{-1}) of every candidate are computed on the device in
+// one launch (blockdiag.cu), so the plan's host work stays small.
 constexpr double kCubicDiagCondMax = 1e6;
-
-using cxd = std::complex<double>;
-// ||M||_2 of a d x d column-major matrix: power iteration on M^H M from a fixed start
-double norm2_est(int d, const cxd* M) {
-  std::vector<cxd> x(d), y(d);
-  for (int i = 0; i < d; ++i) x[i] = cxd(1.0 + 0.37 * i, 0.11 * (i % 5));
-  double lam = 0.0;
-  for (int it = 0; it < 30; ++it) {
-    for (int r = 0; r < d; ++r) y[r] = 0.0;
-    for (int c = 0; c < d; ++c)
-      for (int r = 0; r < d; ++r) y[r] += M[r + c * d] * x[c];
-    double nx = 0.0;
-    for (int c = 0; c < d; ++c) {
-      cxd acc = 0.0;
-      for (int r = 0; r < d; ++r) acc += std::conj(M[r + c * d]) * y[r];
-      x[c] = acc;
-      nx += std::norm(acc);
-    }
-    nx = std::sqrt(nx);
-    if (!(nx > 0.0) || !std::isfinite(nx)) return std::numeric_limits<double>::infinity();
-    lam = nx;
-    for (auto& v : x) v /= nx;
-  }
-  return std::sqrt(lam);
-}
-// Eigenvectors (unit columns, upper triangular) and their inverse of the d x d diagonal block at
-// offset o of T (n x n column-major); returns cond_2 (inf when two eigenvalues coincide).
-double block_eig(const nds_z* t, int64_t n, int64_t o, int d, cxd* v, cxd* w) {
-  auto T = [&](int r, int c) { return cxd(t[(o + r) + (o + c) * n].re, t[(o + r) + (o + c) * n].im); };
-  for (int k = 0; k < d; ++k) {
-    for (int i = 0; i < d; ++i) v[i + k * d] = 0.0;
-    v[k + k * d] = 1.0;
-    const cxd lk = T(k, k);
-    for (int i = k - 1; i >= 0; --i) {
-      cxd acc = 0.0;
-      for (int l = i + 1; l <= k; ++l) acc += T(i, l) * v[l + k * d];
-      const cxd gap = lk - T(i, i);
-      if (std::abs(gap) == 0.0) return std::numeric_limits<double>::infinity();
-      v[i + k * d] = acc / gap;
-    }
-    double nn = 0.0;
-    for (int i = 0; i <= k; ++i) nn += std::norm(v[i + k * d]);
-    nn = std::sqrt(nn);
-    if (!std::isfinite(nn) || nn == 0.0) return std::numeric_limits<double>::infinity();
-    for (int i = 0; i <= k; ++i) v[i + k * d] /= nn;
-  }
-  for (int c = 0; c < d; ++c)  // V^{-1}: back substitution per column
-    for (int i = d - 1; i >= 0; --i) {
-      cxd acc = (i == c) ? 1.0 : 0.0;
-      for (int l = i + 1; l <= c; ++l) acc -= v[i + l * d] * w[l + c * d];
-      w[i + c * d] = i > c ? 0.0 : acc / v[i + i * d];
-    }
-  return norm2_est(d, v) * norm2_est(d, w);
-}
 
 void plan_cubic_diag(nds_plan* p, const nds_z* const* u, const nds_z* const* t) {
   (void)u;
+  (void)t;
   p->cub_diag = false;
   if (p->fast_path || !p->solver || p->solver->binary || !p->solver->sp.v2 || (p->flags & NDS_NO_DIAGONALISE))
     return;
@@ -720,43 +734,66 @@ void plan_cubic_diag(nds_plan* p, const nds_z* const* u, const nds_z* const* t) 
     for (int j = 0; j < N; ++j) span += (B - 1) * tg.strides[j];
     if (span >= (int64_t)1 << 31) return;
   }
-  // per mode: candidate D = B, 2B, .. dividing n_j; blocks evaluated lazily
+  // every candidate (mode j, D = B, 2B, .. <= 128 dividing n_j) evaluated on the device in one
+  // launch (block_eig_kernel: eigenvectors, inverse, cond_2 per block); the host then picks D_j
   struct Cand {
     int d;
-    double cond = -1.0;
-    std::vector<cxd> v, w;  // per block d x d column-major, concatenated
+    int first, count;  // jobs
+    int64_t voff;      // V / W pool offset of its first block
+    double cond = 0.0;
   };
   std::vector<std::vector<Cand>> cands(N);
+  std::vector<nds::EigJob> jobs;
+  int64_t vtot = 0;
   for (int j = 0; j < N; ++j)
-    for (int64_t d = B; d <= std::min<int64_t>(p->dims[j], 128); d *= 2)  // host eigensolves stay O(n 128^2)
-      if (p->dims[j] % d == 0) cands[j].push_back({(int)d});
-  auto eval = [&](int j, int ci) {
-    Cand& c = cands[j][ci];
-    if (c.cond >= 0.0) return c.cond;
-    const int64_t n = p->dims[j];
-    const int d = c.d, nb = (int)(n / d);
-    c.v.assign((size_t)n * d, 0.0);
-    c.w.assign((size_t)n * d, 0.0);
-    std::vector<double> cq(nb);
-#pragma omp parallel for schedule(dynamic, 1) if (nb > 1)
-    for (int q = 0; q < nb; ++q)
-      cq[q] = block_eig(t[j], n, (int64_t)q * d, d, c.v.data() + (size_t)q * d * d, c.w.data() + (size_t)q * d * d);
-    double mx = 0.0;
-    for (double x : cq) mx = std::max(mx, std::isfinite(x) ? x : std::numeric_limits<double>::infinity());
-    c.cond = mx;
-    return mx;
-  };
+    for (int64_t d = B; d <= std::min<int64_t>(p->dims[j], 128); d *= 2) {
+      if (p->dims[j] % d) continue;
+      Cand c{(int)d, (int)jobs.size(), (int)(p->dims[j] / d), vtot};
+      for (int q = 0; q < c.count; ++q) {
+        jobs.push_back({p->dims[j], q * d, p->f.geom.toff[j], vtot, (int)d, j});
+        vtot += d * d;
+      }
+      cands[j].push_back(c);
+    }
+  cudaStream_t s = p->ctx->stream;
+  int64_t sq = 0;
+  for (int j = 0; j < N; ++j) sq += p->dims[j] * p->dims[j];
+  // device scratch: [jobs][cond][V pool][W pool][M_inv][M_fwd^H][T W][T']
+  const size_t jb_bytes = (jobs.size() * sizeof(nds::EigJob) + 255) / 256 * 256;
+  const size_t cd_bytes = (jobs.size() * sizeof(double) + 255) / 256 * 256;
+  char* scratch = nullptr;
+  NDS_CUDA(cudaMallocFromPoolAsync((void**)&scratch, jb_bytes + cd_bytes + (size_t)(2 * vtot + 4 * sq) * sizeof(double2),
+                                   p->ctx->pool, s));
+  nds::EigJob* d_jobs = (nds::EigJob*)scratch;
+  double* d_cond = (double*)(scratch + jb_bytes);
+  double2* dv = (double2*)(scratch + jb_bytes + cd_bytes);
+  double2* dw = dv + vtot;
+  double2 *minv = dw + vtot, *mfh = minv + sq, *tw = mfh + sq, *tpr = tw + sq;
+  std::vector<double> cond(jobs.size());
+  NDS_CUDA(cudaMemcpyAsync(d_jobs, jobs.data(), jobs.size() * sizeof(nds::EigJob), cudaMemcpyHostToDevice, s));
+  nds::block_eig_launch(p->f.t_pool, d_jobs, (int)jobs.size(), dv, dw, d_cond, s);
+  NDS_CUDA(cudaMemcpyAsync(cond.data(), d_cond, jobs.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+  NDS_CUDA(cudaStreamSynchronize(s));
+  for (int j = 0; j < N; ++j)
+    for (Cand& c : cands[j]) {
+      c.cond = 0.0;
+      for (int q = 0; q < c.count; ++q) c.cond = std::max(c.cond, cond[c.first + q]);
+      if (!std::isfinite(c.cond)) c.cond = std::numeric_limits<double>::infinity();
+    }
   std::vector<int> sel(N, 0);
   double prod = 1.0;
-  for (int j = 0; j < N; ++j) prod *= eval(j, 0);
+  for (int j = 0; j < N; ++j) prod *= cands[j][0].cond;
   p->cub_cond = prod;
-  if (!(prod <= kCubicDiagCondMax)) return;
+  if (!(prod <= kCubicDiagCondMax)) {
+    NDS_CUDA(cudaFreeAsync(scratch, s));
+    return;
+  }
   for (;;) {  // grow the super-blocks: double the mode whose product stays smallest
     int best = -1;
     double best_prod = 0.0;
     for (int j = 0; j < N; ++j) {
       if (sel[j] + 1 >= (int)cands[j].size()) continue;
-      const double np = prod / cands[j][sel[j]].cond * eval(j, sel[j] + 1);
+      const double np = prod / cands[j][sel[j]].cond * cands[j][sel[j] + 1].cond;
       if (np <= kCubicDiagCondMax && (best < 0 || np < best_prod)) {
         best = j;
         best_prod = np;
@@ -769,34 +806,13 @@ void plan_cubic_diag(nds_plan* p, const nds_z* const* u, const nds_z* const* t) 
   p->cub_cond = prod;
   int d[NDS_MAX_MODES] = {};
   for (int j = 0; j < N; ++j) d[j] = cands[j][sel[j]].d;
-  // device: M_inv = U W, M_fwd^H = U W^{-H} (uploaded as "U", so the set's U^H layouts hold
-  // W^{-1} U^H), T' = W^{-1} T W with its diagonal blocks set to diag(T) exactly
-  int64_t sq = 0, vb = 0;
-  for (int j = 0; j < N; ++j) {
-    sq += p->dims[j] * p->dims[j];
-    vb += p->dims[j] * d[j];
-  }
-  std::vector<double2> hv((size_t)2 * vb);
+  // M_inv = U W, M_fwd^H = U W^{-H} (uploaded as "U", so the set's U^H layouts hold W^{-1} U^H),
+  // T' = W^{-1} T W with its diagonal blocks set to diag(T) exactly
   {
     int64_t o = 0;
     for (int j = 0; j < N; ++j) {
-      const Cand& c = cands[j][sel[j]];
-      for (size_t i = 0; i < c.v.size(); ++i) {
-        hv[o + i] = make_double2(c.v[i].real(), c.v[i].imag());
-        hv[vb + o + i] = make_double2(c.w[i].real(), c.w[i].imag());
-      }
-      o += (int64_t)c.v.size();
-    }
-  }
-  cudaStream_t s = p->ctx->stream;
-  double2* tmp = nullptr;  // [V | V^{-1}] [M_inv] [M_fwd^H] [T W] [T']
-  NDS_CUDA(cudaMallocFromPoolAsync(&tmp, (size_t)(2 * vb + 4 * sq) * sizeof(double2), p->ctx->pool, s));
-  NDS_CUDA(cudaMemcpyAsync(tmp, hv.data(), hv.size() * sizeof(double2), cudaMemcpyHostToDevice, s));
-  double2 *dv = tmp, *dw = tmp + vb, *minv = tmp + 2 * vb, *mfh = minv + sq, *tw = mfh + sq, *tpr = tw + sq;
-  {
-    int64_t o = 0, ov = 0;
-    for (int j = 0; j < N; ++j) {
       const int64_t n = p->dims[j];
+      const int64_t ov = cands[j][sel[j]].voff;
       const double2* uj = p->f.u_col[j];  // U_j column-major (factor_layouts)
       const double2* tj = p->f.t_pool + p->f.geom.toff[j];
       nds::blockdiag_mul_launch(n, d[j], uj, dv + ov, true, false, minv + o, s);
@@ -805,14 +821,11 @@ void plan_cubic_diag(nds_plan* p, const nds_z* const* u, const nds_z* const* t) 
       nds::blockdiag_mul_launch(n, d[j], tw + o, dw + ov, false, false, tpr + o, s);
       nds::blockdiag_fix_launch(n, d[j], tj, tpr + o, s);
       o += n * n;
-      ov += n * d[j];
     }
   }
-  // hv must stay alive until its copy ran: the device factor builds below are stream-ordered
   device_factors(p->ctx, p->cd_inv, N, p->dims, minv, tpr, p->f.diag_pool);
   device_factors(p->ctx, p->cd_fwd, N, p->dims, mfh, nullptr, nullptr);
-  NDS_CUDA(cudaFreeAsync(tmp, s));
-  NDS_CUDA(cudaStreamSynchronize(s));  // hv (pageable) copy complete before it goes out of scope
+  NDS_CUDA(cudaFreeAsync(scratch, s));
   p->fc = p->cd_inv;
   p->fc.pool = nullptr;  // owned by cd_inv / cd_fwd
   for (int j = 0; j < N; ++j) {
@@ -823,7 +836,15 @@ void plan_cubic_diag(nds_plan* p, const nds_z* const* u, const nds_z* const* t) 
       p->fc.bblk[j][1][sh] = p->cd_fwd.bblk[j][1][sh];
     }
   }
-  nds::blk_solve_plan_build(p->blk, p->solver->sp, d);
+  {
+    const std::vector<int> key(d, d + N);
+    auto it = p->solver->blk.find(key);
+    if (it == p->solver->blk.end()) {
+      it = p->solver->blk.emplace(key, nds::BlkSolvePlan{}).first;
+      nds::blk_solve_plan_build(it->second, p->solver->sp, d);
+    }
+    p->blk = &it->second;
+  }
   p->cub_diag = true;
 }
 
@@ -861,8 +882,9 @@ int execute_fused_binary(nds_plan* p, const std::vector<XPass>& passes, const do
   {
     double2* dst = dst_of(++k);
     const nds::BinarySolvePlan& bp = p->solver->bsp;
-    const int kind = nds::binary_fused_solve_launch(p->fd, p->fd, p->groups[passes.front().group], p->f.t_pool,
-                                                    bp.n_outer, bp.d_wf_swz, bp.d_wf_off, src, dst, s);
+    const int kind = nds::binary_fused_solve_launch(p->fd, p->fd, p->groups[passes.front().group], p->bin_t,
+                                                    bp.n_outer, p->bin_wf, p->bin_wf_off, p->bin_wf_levels, src, dst,
+                                                    s);
     if (rec) rec->mark(s, kind, 0);
     ++launches;
     src = dst;
@@ -1070,7 +1092,6 @@ void plan_destroy_impl(nds_plan* p) {
   free_factors(p->f);
   free_factors(p->cd_inv);
   free_factors(p->cd_fwd);
-  nds::blk_solve_plan_free(p->blk);
   if (p->fd_buf) cudaFree(p->fd_buf);
   delete p;  // the shared solver structures stay cached in the context
 }
@@ -1810,6 +1831,14 @@ int nds_plan_diagonalised(const nds_plan* plan, double* cond) {
   if (!plan) return -1;
   if (cond) *cond = plan->bin_diag ? plan->bin_cond : plan->cub_cond;
   return plan->bin_diag || plan->cub_diag ? 1 : 0;
+}
+
+int nds_plan_superblocks(const nds_plan* plan, int64_t* d) {
+  if (!plan) return -1;
+  if (!plan->cub_diag) return 0;
+  if (d)
+    for (int j = 0; j < plan->n_modes; ++j) d[j] = plan->blk->d[j];
+  return plan->blk->levels;
 }
 
 int nds_plan_profile_begin(nds_plan* plan, int max_launches) {

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <map>
 #include <vector>
 
 #include "common.cuh"
@@ -71,9 +72,11 @@ int binary_pass_launch(const FactorSet& f, const BinGroup& gr, bool adjoint, con
 // Modes 1-12 forward (fwd's U^H), the decoupled 12-mode tile solve (den over all modes; the
 // outer modes' coupling diagonalised away), modes 1-12 inverse (inv's U) — one kernel, one read
 // and one write of the tensor; gr is the modes-1-12 pass (first 1, count 12, inner 1).
+// t_pool: T'_j (2 x 2, all N modes; diagonal for the diagonalised ones), wf / wf_off: the tile
+// entries by popcount over the coupled inner modes (levels = their count + 1).
 int binary_fused_solve_launch(const FactorSet& fwd, const FactorSet& inv, const BinGroup& gr, const double2* t_pool,
-                              int n_outer, const uint16_t* wf, const int* wf_off, const double2* x, double2* r,
-                              cudaStream_t stream);
+                              int n_outer, const uint16_t* wf, const int* wf_off, int levels, const double2* x,
+                              double2* r, cudaStream_t stream);
 
 // Plain matrix variant (apply_operator / residual): m_row, m_col are the two layouts of M.
 // rows_out > 0: rectangular M (rows_out x n), r has extent rows_out along the mode.
@@ -158,15 +161,6 @@ void binary_solve_plan_free(BinarySolvePlan& bp);
 int binary_solve_launch(const BinarySolvePlan& bp, const double2* t_pool, double2* c, cudaStream_t stream,
                         Recorder* rec = nullptr, bool decoupled = false);
 
-// Dims-only solver structures (tile lists, work items, partial buffers, internal streams), cached
-// per context and shared by every plan with the same extents.
-struct SolverCache {
-  bool binary = false;
-  BinarySolvePlan bsp;
-  SolvePlan sp;
-  ~SolverCache();
-};
-
 // Block-diagonalised cubic route (backsub_blk.cuh): super-blocks of d[j] rows per mode (multiples
 // of the tile edge), the cubic tiles grouped by super-tile level sum_j floor(I_j b / d_j)
 // (highest first; within a level longest pull first), one launch per level.
@@ -176,10 +170,30 @@ struct BlkSolvePlan {
   std::vector<int64_t> level_off;
   int64_t* d_tiles = nullptr;
 };
+// Dims-only solver structures (tile lists, work items, partial buffers, internal streams), cached
+// per context and shared by every plan with the same extents; the block-diagonalised route's
+// level lists by super-block extents.
+struct SolverCache {
+  bool binary = false;
+  BinarySolvePlan bsp;
+  SolvePlan sp;
+  std::map<std::vector<int>, BlkSolvePlan> blk;
+  ~SolverCache();
+};
+
 void blk_solve_plan_build(BlkSolvePlan& bp, const SolvePlan& sp, const int* d);
 void blk_solve_plan_free(BlkSolvePlan& bp);
 int blk_backsub_launch(const SolvePlan& sp, const BlkSolvePlan& bp, const double2* t_pool, double2* c,
                        cudaStream_t stream, Recorder* rec = nullptr);
+// Eigenvector blocks of the route's candidates (blockdiag.cu): job = block at row offset o of
+// T_j (n x n at t_pool + toff) with extent d <= 128; V, W = V^{-1} (d x d column-major at
+// vpool / wpool + voff) and cond_2(V) into cond[job] (inf on a repeated eigenvalue).
+struct EigJob {
+  int64_t n, o, toff, voff;
+  int d, mode;
+};
+void block_eig_launch(const double2* t_pool, const EigJob* jobs, int njobs, double2* vpool, double2* wpool,
+                      double* cond, cudaStream_t stream);
 // out = A blockdiag(Bq) (right = true) or blockdiag(Bq) A, A and out n x n column-major, blocks
 // of d x d column-major at blk + q d^2; conj_t: use Bq^H. Then (fix_t) T' cleanup: entries of a
 // diagonal d-block set to diag_src's diagonal exactly, entries below the block diagonal zeroed.
