@@ -288,7 +288,8 @@ struct BlkLaunchT {
   int threads;
 };
 // Measured (c1 / c3 solve): N = 3 — 256 threads, BK = 8, 3 stages: 1.31 ms (512 threads 1.37,
-// 4 stages 1.34); N = 4 — 512 threads, BK = 4, 3 stages: 18.1 ms (256 threads 19.9, 4 stages 20.1).
+// 4 stages 1.34, BK = 16 x 2 stages 1.46 / 1.49 with 512 threads); N = 4 — 512 threads, BK = 4,
+// 3 stages: 18.1 ms (256 threads 19.9, 4 stages 20.1, BK = 8 x 2 stages 18.9 / 19.3).
 static BlkLaunchT blk_cfg(int n_modes, int b) {
   if (n_modes == 3 && b == 16) return {blk_level_kernel<3, 16, 8, 3, 256>, BlkCfg<3, 16, 8, 3, 256>::smem(), 256};
   if (n_modes == 4 && b == 8) return {blk_level_kernel<4, 8, 4, 3, 512>, BlkCfg<4, 8, 4, 3, 512>::smem(), 512};

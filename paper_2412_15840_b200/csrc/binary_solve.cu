@@ -213,6 +213,7 @@ int binary_solve_launch(const BinarySolvePlan& bp, const double2* t_pool, double
 namespace nds {
 SolverCache::~SolverCache() {
   for (auto& kv : blk) blk_solve_plan_free(kv.second);
+  for (auto& kv : bin_wf) cudaFree(kv.second);
   if (binary)
     binary_solve_plan_free(bsp);
   else

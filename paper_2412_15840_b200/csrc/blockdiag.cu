@@ -9,149 +9,266 @@
 
 namespace nds {
 
-// One CTA per job (block q of mode j at candidate extent d, d <= blockDim.x), thread k <-> column k.
-//  1. V(:, k): the eigenvector of the upper triangular block T_q for T_q(k, k), V(k, k) = 1,
-//     V(i, k) = sum_{l = i+1..k} T(i, l) V(l, k) / (T(k, k) - T(i, i)), then unit 2-norm;
-//  2. W = V^{-1} (upper triangular): column c by back substitution;
+// One CTA (128 threads) per job: block q of a candidate (mode j, extent d <= 128). Both
+// triangular recurrences run ROW by row (row i from the bottom up, all columns k > i at once,
+// thread k <-> column k), so every step's operands are shared-memory reads: the unknown matrix
+// is kept packed (upper triangle, row i holding columns i..d-1 at i d - i (i - 1) / 2; 132 KB at
+// d = 128) and the known row streams in from global memory one step ahead.
+//  1. V: T V = V diag(T), V(k, k) = 1, V(i, k) = sum_{l = i+1..k} T(i, l) V(l, k) / (T(k, k) -
+//     T(i, i)); then every column scaled to unit 2-norm;
+//  2. W = V^{-1}: W(c, c) = 1 / V(c, c), W(i, c) = -sum_{l = i+1..c} V(i, l) W(l, c) / V(i, i);
 //  3. cond_2(V) = ||V||_2 ||W||_2, both by 12 power iterations on M^H M (shared vectors).
 // A zero eigenvalue gap (repeated eigenvalue) or a non-finite entry makes cond infinite.
-__global__ void __launch_bounds__(128) block_eig_kernel(const double2* __restrict__ t_pool,
-                                                        const EigJob* __restrict__ jobs, double2* __restrict__ vpool,
-                                                        double2* __restrict__ wpool, double* __restrict__ cond) {
-  const EigJob jb = jobs[blockIdx.x];
-  const int d = jb.d, k = threadIdx.x;
-  const int64_t n = jb.n, o = jb.o;
-  const double2* T = t_pool + jb.toff;
-  auto Tq = [&](int r, int c) { return T[(o + r) + (o + c) * n]; };
-  double2* V = vpool + jb.voff;  // column-major d x d
-  double2* W = wpool + jb.voff;
+constexpr int kEigThreads = 128;
+__host__ __device__ constexpr int tri_off(int i, int d) { return i * d - i * (i - 1) / 2; }
+size_t block_eig_smem(int dmax) { return (size_t)tri_off(dmax, dmax) * sizeof(double2); }
+// sum_{l = l0..k} r[l] * U(l, k) for the packed upper triangle U in shared memory (row l at
+// tri_off(l, d)): consecutive rows of column k are d - l - 1 apart; four independent accumulators
+__device__ __forceinline__ double2 tri_dot_impl(const double2* __restrict__ r, const double2* __restrict__ tri, int l0,
+                                                int k, int d) {
+  double2 a[4] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0), make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+  int p = tri_off(l0, d) + (k - l0);
+  int l = l0;
+  for (; l + 3 <= k; l += 4) {
+    const int p1 = p + (d - l - 1), p2 = p1 + (d - l - 2), p3 = p2 + (d - l - 3);
+    a[0] = cfma(a[0], r[l], tri[p]);
+    a[1] = cfma(a[1], r[l + 1], tri[p1]);
+    a[2] = cfma(a[2], r[l + 2], tri[p2]);
+    a[3] = cfma(a[3], r[l + 3], tri[p3]);
+    p = p3 + (d - l - 4);
+  }
+  for (; l <= k; ++l) {
+    a[0] = cfma(a[0], r[l], tri[p]);
+    p += d - l - 1;
+  }
+  return cadd(cadd(a[0], a[1]), cadd(a[2], a[3]));
+}
+
+__global__ void __launch_bounds__(kEigThreads) block_eig_kernel(const double2* __restrict__ t_pool, const EigCands cs,
+                                                               double2* __restrict__ vpool, double2* __restrict__ wpool,
+                                                               double* __restrict__ cond) {
+  extern __shared__ __align__(16) double2 tri[];  // the packed unknown upper triangle (V, then W)
+  int ci = 0;
+  while (ci + 1 < cs.count && (int)blockIdx.x >= cs.first[ci + 1]) ++ci;
+  const int q = blockIdx.x - cs.first[ci];
+  const int d = cs.d[ci];
+  const int k = threadIdx.x, lane = k & 31, warp = k >> 5;
+  const int64_t n = cs.n[ci], o = (int64_t)q * d;
+  const double2* T = t_pool + cs.toff[ci];
+  double2* V = vpool + cs.voff[ci] + (int64_t)q * d * d;  // column-major d x d
+  double2* W = wpool + cs.voff[ci] + (int64_t)q * d * d;
+  auto P = [d](int r, int c) { return tri_off(r, d) + (c - r); };
+  auto tri_dot = [&](const double2* r, int l0, int kk, int dd) { return tri_dot_impl(r, tri, l0, kk, dd); };
   __shared__ int bad;
+  __shared__ double2 row[2][128];  // the known row of this step (double-buffered)
   __shared__ double2 x[128], y[128];
   __shared__ double red[4];
   if (k == 0) bad = 0;
+  // ---- 1. V, rows d-1 .. 0 ----
+  if (k < d) row[(d - 1) & 1][k] = T[(o + d - 1) + (o + k) * n];
+  double2 lk = k < d ? T[(o + k) + (o + k) * n] : make_double2(0.0, 0.0);
   __syncthreads();
-  if (k < d) {
-    double2* vk = V + (int64_t)k * d;
-    for (int i = k + 1; i < d; ++i) vk[i] = make_double2(0.0, 0.0);
-    vk[k] = make_double2(1.0, 0.0);
-    const double2 lk = Tq(k, k);
-    double nn = 1.0;
-    for (int i = k - 1; i >= 0; --i) {
-      double2 acc = make_double2(0.0, 0.0);
-      for (int l = i + 1; l <= k; ++l) acc = cfma(acc, Tq(i, l), vk[l]);
-      const double2 gap = csub(lk, Tq(i, i));
+  for (int i = d - 1; i >= 0; --i) {
+    const double2* ti = row[i & 1];  // ti[c] = T(i, c)
+    if (i > 0 && k < d) row[(i - 1) & 1][k] = T[(o + i - 1) + (o + k) * n];  // next row, one step ahead
+    if (k == i) tri[P(i, i)] = make_double2(1.0, 0.0);
+    else if (k > i && k < d) {
+      const double2 acc = tri_dot(ti, i + 1, k, d);
+      const double2 gap = csub(lk, ti[i]);
       if (gap.x == 0.0 && gap.y == 0.0) {
         bad = 1;
-        break;
+        tri[P(i, k)] = make_double2(0.0, 0.0);
+      } else {
+        tri[P(i, k)] = cdiv(acc, gap);
       }
-      const double2 vi = cdiv(acc, gap);
-      vk[i] = vi;
-      nn += vi.x * vi.x + vi.y * vi.y;
     }
-    nn = sqrt(nn);
-    if (!isfinite(nn)) bad = 1;
-    const double s = 1.0 / nn;
-    for (int i = 0; i <= k; ++i) vk[i] = make_double2(vk[i].x * s, vk[i].y * s);
+    __syncthreads();
   }
-  __syncthreads();
-  if (k < d) {  // W(:, c), c = k: W(c, c) = 1 / V(c, c); W(i, c) = -sum_{l=i+1..c} V(i, l) W(l, c) / V(i, i)
-    double2* wc = W + (int64_t)k * d;
-    for (int i = k + 1; i < d; ++i) wc[i] = make_double2(0.0, 0.0);
-    for (int i = k; i >= 0; --i) {
-      double2 acc = make_double2(i == k ? 1.0 : 0.0, 0.0);
-      for (int l = i + 1; l <= k; ++l) acc = csub(acc, cmul(V[i + (int64_t)l * d], wc[l]));
-      wc[i] = cdiv(acc, V[i + (int64_t)i * d]);
-    }
-  }
-  __syncthreads();
-  double nrm[2];
-  for (int which = 0; which < 2; ++which) {
-    const double2* M = which ? W : V;
+  // ||M||_2 of the packed upper triangle in shared memory: 12 power iterations on M^H M
+  auto norm2 = [&]() {
     if (k < d) x[k] = make_double2(1.0 + 0.37 * k, 0.11 * (k % 5));
     __syncthreads();
     double lam = 0.0;
     for (int it = 0; it < 12; ++it) {
       if (k < d) {  // y = M x (row k)
-        double2 s = make_double2(0.0, 0.0);
-        for (int c = k; c < d; ++c) s = cfma(s, M[k + (int64_t)c * d], x[c]);
-        y[k] = s;
+        double2 s0 = make_double2(0.0, 0.0), s1 = make_double2(0.0, 0.0);
+        const double2* mk = tri + tri_off(k, d) - k;
+        int c = k;
+        for (; c + 1 < d; c += 2) {
+          s0 = cfma(s0, mk[c], x[c]);
+          s1 = cfma(s1, mk[c + 1], x[c + 1]);
+        }
+        if (c < d) s0 = cfma(s0, mk[c], x[c]);
+        y[k] = cadd(s0, s1);
       }
       __syncthreads();
       double part = 0.0;
       double2 xn = make_double2(0.0, 0.0);
       if (k < d) {  // x = M^H y (column k)
-        for (int r = 0; r <= k; ++r) {
-          const double2 m = M[r + (int64_t)k * d];
-          xn = cfma(xn, make_double2(m.x, -m.y), y[r]);
+        double2 x1 = make_double2(0.0, 0.0);
+        int p = k, r = 0;  // P(r, k) = p, rows r -> r + 1 step by d - r - 1
+        for (; r + 1 <= k; r += 2) {
+          const double2 m0 = tri[p], m1 = tri[p + (d - r - 1)];
+          xn = cfma(xn, make_double2(m0.x, -m0.y), y[r]);
+          x1 = cfma(x1, make_double2(m1.x, -m1.y), y[r + 1]);
+          p += (d - r - 1) + (d - r - 2);
         }
+        if (r <= k) xn = cfma(xn, make_double2(tri[p].x, -tri[p].y), y[r]);
+        xn = cadd(xn, x1);
         part = xn.x * xn.x + xn.y * xn.y;
       }
       for (int sh = 16; sh > 0; sh >>= 1) part += __shfl_xor_sync(0xffffffffu, part, sh);
-      if ((k & 31) == 0) red[k >> 5] = part;
+      if (lane == 0) red[warp] = part;
       __syncthreads();
       const double tot = sqrt(red[0] + red[1] + red[2] + red[3]);
       lam = tot;
       if (k < d) x[k] = make_double2(xn.x / tot, xn.y / tot);
       __syncthreads();
     }
-    nrm[which] = sqrt(lam);
+    return sqrt(lam);
+  };
+  if (k < d) {  // unit columns (in place), stored column-major
+    double nn = 0.0;
+    for (int i = 0; i <= k; ++i) {
+      const double2 v = tri[P(i, k)];
+      nn += v.x * v.x + v.y * v.y;
+    }
+    nn = sqrt(nn);
+    if (!isfinite(nn) || nn == 0.0) {
+      bad = 1;
+      nn = 1.0;
+    }
+    const double sc = 1.0 / nn;
+    for (int i = 0; i < d; ++i) {
+      double2 v = make_double2(0.0, 0.0);
+      if (i <= k) {
+        v = tri[P(i, k)];
+        v = make_double2(v.x * sc, v.y * sc);
+        tri[P(i, k)] = v;
+      }
+      V[i + (int64_t)k * d] = v;
+    }
   }
+  __syncthreads();
+  const double nv = norm2();
+  // ---- 2. W = V^{-1}, rows d-1 .. 0 (V rows from global, just written) ----
+  if (k < d) row[(d - 1) & 1][k] = V[(d - 1) + (int64_t)k * d];
+  __syncthreads();
+  for (int i = d - 1; i >= 0; --i) {
+    const double2* vi = row[i & 1];  // vi[c] = V(i, c)
+    if (i > 0 && k < d) row[(i - 1) & 1][k] = V[(i - 1) + (int64_t)k * d];
+    if (k == i) tri[P(i, i)] = cdiv(make_double2(1.0, 0.0), vi[i]);
+    else if (k > i && k < d) {
+      const double2 acc = tri_dot(vi, i + 1, k, d);
+      tri[P(i, k)] = cdiv(make_double2(-acc.x, -acc.y), vi[i]);
+    }
+    __syncthreads();
+  }
+  if (k < d)
+    for (int i = 0; i < d; ++i) W[i + (int64_t)k * d] = i <= k ? tri[P(i, k)] : make_double2(0.0, 0.0);
+  const double nw = norm2();
   if (k == 0) {
-    const double c = nrm[0] * nrm[1];
+    const double c = nv * nw;
     cond[blockIdx.x] = (bad || !isfinite(c)) ? INFINITY : c;
   }
 }
 
-void block_eig_launch(const double2* t_pool, const EigJob* jobs, int njobs, double2* vpool, double2* wpool,
-                      double* cond, cudaStream_t stream) {
+void block_eig_launch(const double2* t_pool, const EigCands& cands, double2* vpool, double2* wpool, double* cond,
+                      cudaStream_t stream) {
+  const int njobs = cands.count > 0 ? cands.first[cands.count] : 0;
   if (njobs <= 0) return;
-  block_eig_kernel<<<(unsigned)njobs, 128, 0, stream>>>(t_pool, jobs, vpool, wpool, cond);
+  int dmax = 0;
+  for (int c = 0; c < cands.count; ++c) dmax = std::max(dmax, cands.d[c]);
+  const size_t smem = block_eig_smem(dmax);
+  static size_t attr = 0;
+  if (smem > attr) {
+    NDS_CUDA(cudaFuncSetAttribute(block_eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = smem;
+  }
+  block_eig_kernel<<<(unsigned)njobs, kEigThreads, smem, stream>>>(t_pool, cands, vpool, wpool, cond);
   NDS_LAUNCH_CHECK();
 }
 
-__global__ void blockdiag_mul_kernel(int64_t n, int d, const double2* __restrict__ a, const double2* __restrict__ blk,
-                                     int right, int conj_t, double2* __restrict__ out) {
+__global__ void param_blob_kernel(const ParamBlob b, double2* __restrict__ dst) {
+  for (int i = threadIdx.x; i < b.count; i += blockDim.x) dst[i] = b.v[i];
+}
+
+void param_blob_launch(const ParamBlob& blob, double2* dst, cudaStream_t stream) {
+  if (blob.count <= 0) return;
+  param_blob_kernel<<<1, 256, 0, stream>>>(blob, dst);
+  NDS_LAUNCH_CHECK();
+}
+
+// out_y = A_y blockdiag(B_y) for y = blockIdx.y (up to three products of one mode per launch):
+// out(r, c) = sum_{k in block(c)} A(r, o + k) B_q(k, c - o), B_q or B_q^H (conj).
+struct BdRight {
+  int count;
+  const double2* a[3];
+  const double2* blk[3];
+  int conj[3];
+  double2* out[3];
+};
+__global__ void blockdiag_right_kernel(int64_t n, int d, const BdRight j) {
+  const int y = blockIdx.y;
+  const double2* __restrict__ a = j.a[y];
+  const double2* __restrict__ blk = j.blk[y];
+  const bool conj_t = j.conj[y] != 0;
+  double2* __restrict__ out = j.out[y];
   const int64_t total = n * n;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = e % n, c = e / n;
-    const int64_t q = (right ? c : r) / d, o = q * d;
+    const int64_t q = c / d, o = q * d, cc = c - o;
     const double2* bq = blk + q * (int64_t)d * d;
-    auto bel = [&](int64_t i, int64_t k) {  // Bq(i, k) or Bq^H(i, k)
-      if (!conj_t) return bq[i + k * d];
-      const double2 v = bq[k + i * d];
-      return make_double2(v.x, -v.y);
-    };
-    double2 s = make_double2(0.0, 0.0);
-    if (right)
-      for (int k = 0; k < d; ++k) s = cfma(s, a[r + (o + k) * n], bel(k, c - o));
-    else
-      for (int k = 0; k < d; ++k) s = cfma(s, bel(r - o, k), a[(o + k) + c * n]);
-    out[e] = s;
+    double2 s0 = make_double2(0.0, 0.0), s1 = make_double2(0.0, 0.0);
+    for (int k = 0; k < d; k += 2) {  // d even
+      double2 b0 = conj_t ? bq[cc + k * d] : bq[k + cc * d];
+      double2 b1 = conj_t ? bq[cc + (k + 1) * d] : bq[k + 1 + cc * d];
+      if (conj_t) {
+        b0.y = -b0.y;
+        b1.y = -b1.y;
+      }
+      s0 = cfma(s0, a[r + (o + k) * n], b0);
+      s1 = cfma(s1, a[r + (o + k + 1) * n], b1);
+    }
+    out[e] = cadd(s0, s1);
   }
 }
 
-__global__ void blockdiag_fix_kernel(int64_t n, int d, const double2* __restrict__ diag_src, double2* __restrict__ t) {
+// T' = blockdiag(W_q) TV with the route's structure imposed: entries of a diagonal d-block are
+// diag(T) exactly (off-diagonal 0), entries below the block diagonal 0.
+__global__ void blockdiag_left_fix_kernel(int64_t n, int d, const double2* __restrict__ w, const double2* __restrict__ tv,
+                                          const double2* __restrict__ t, double2* __restrict__ out) {
   const int64_t total = n * n;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = e % n, c = e / n;
-    if (r / d == c / d)
-      t[e] = r == c ? diag_src[e] : make_double2(0.0, 0.0);
-    else if (r / d > c / d)
-      t[e] = make_double2(0.0, 0.0);
+    const int64_t qr = r / d, qc = c / d;
+    if (qr == qc) {
+      out[e] = r == c ? t[e] : make_double2(0.0, 0.0);
+      continue;
+    }
+    if (qr > qc) {
+      out[e] = make_double2(0.0, 0.0);
+      continue;
+    }
+    const int64_t o = qr * d;
+    const double2* wq = w + qr * (int64_t)d * d;
+    double2 s0 = make_double2(0.0, 0.0), s1 = make_double2(0.0, 0.0);
+    for (int k = (int)(r - o); k < d; k += 2) {  // W_q upper triangular: columns k >= r - o
+      s0 = cfma(s0, wq[(r - o) + k * d], tv[(o + k) + c * n]);
+      if (k + 1 < d) s1 = cfma(s1, wq[(r - o) + (k + 1) * d], tv[(o + k + 1) + c * n]);
+    }
+    out[e] = cadd(s0, s1);
   }
 }
 
-void blockdiag_mul_launch(int64_t n, int d, const double2* a, const double2* blk, bool right, bool conj_t,
-                          double2* out, cudaStream_t stream) {
+void blockdiag_factors_launch(int64_t n, int d, const double2* u, const double2* t, const double2* v, const double2* w,
+                              double2* minv, double2* mfh, double2* tv, double2* tprime, cudaStream_t stream) {
   const int64_t total = n * n;
-  blockdiag_mul_kernel<<<(unsigned)std::min<int64_t>((total + 255) / 256, 4096), 256, 0, stream>>>(
-      n, d, a, blk, right ? 1 : 0, conj_t ? 1 : 0, out);
+  const unsigned gx = (unsigned)std::min<int64_t>((total + 255) / 256, 2048);
+  BdRight j{3, {u, u, t}, {v, w, v}, {0, 1, 0}, {minv, mfh, tv}};
+  blockdiag_right_kernel<<<dim3(gx, 3), 256, 0, stream>>>(n, d, j);
   NDS_LAUNCH_CHECK();
-}
-
-void blockdiag_fix_launch(int64_t n, int d, const double2* diag_src, double2* t, cudaStream_t stream) {
-  const int64_t total = n * n;
-  blockdiag_fix_kernel<<<(unsigned)std::min<int64_t>((total + 255) / 256, 4096), 256, 0, stream>>>(n, d, diag_src, t);
+  blockdiag_left_fix_kernel<<<gx, 256, 0, stream>>>(n, d, w, tv, t, tprime);
   NDS_LAUNCH_CHECK();
 }
 

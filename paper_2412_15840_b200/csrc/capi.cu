@@ -5,6 +5,7 @@
 #include <cmath>
 #include <complex>
 #include <cstring>
+#include <functional>
 #include <limits>
 #include <map>
 #include <memory>
@@ -366,7 +367,7 @@ void free_factors(nds::FactorSet& f) {
 // A factor set built from DEVICE data (same pool layout as upload_factors): d_u = the raw
 // column-major U_j concatenated, d_t / d_diag = T_j concatenated and their diagonals (or null).
 void device_factors(nds_ctx* ctx, nds::FactorSet& f, int n_modes, const int64_t* dims, const double2* d_u,
-                    const double2* d_t, const double2* d_diag) {
+                    const double2* d_t, const double2* d_diag, int op_mask = 3) {
   f.n_modes = n_modes;
   int64_t sq = 0, diag = 0, n_blk = 0;
   for (int j = 0; j < n_modes; ++j) {
@@ -408,7 +409,7 @@ void device_factors(nds_ctx* ctx, nds::FactorSet& f, int n_modes, const int64_t*
   double2* raw = f.pool + 4 * sq + n_t + n_d;
   NDS_CUDA(cudaMemcpyAsync(raw, d_u, (size_t)sq * sizeof(double2), cudaMemcpyDeviceToDevice, ctx->stream));
   nds::factor_layouts_launch(f, raw, ctx->stream);
-  if (n_blk) nds::blocked_layouts_launch(f, raw + sq, ctx->stream);
+  if (n_blk) nds::blocked_layouts_launch(f, raw + sq, ctx->stream, op_mask);
 }
 
 // sylvester.cpp:29-33 — eps * sum_j ||T_j||_F (std::norm = re^2 + im^2, matrix.cpp:99-103).
@@ -656,33 +657,40 @@ void plan_binary_diag(nds_plan* p, const nds_z* const* u, const nds_z* const* t)
       ++k;
     }
   const int E = 1 << m;
-  std::vector<int> wf(E), off(k + 2, 0), cnt(k + 1, 0);
-  for (int l = 0; l < E; ++l) cnt[k - __builtin_popcount(l & cmask)]++;
-  for (int i = 0; i <= k; ++i) off[i + 1] = off[i] + cnt[i];
-  {
-    std::vector<int> pos(off.begin(), off.end() - 1);
-    for (int l = E - 1; l >= 0; --l) wf[pos[k - __builtin_popcount(l & cmask)]++] = l;
-  }
-  std::vector<uint16_t> wfs(E);
-  {
-    auto swz = [](int q) { return q ^ (((q >> 3) ^ (q >> 6) ^ (q >> 9)) & 7); };
-    for (int lv = 0; lv <= k; ++lv) {
-      std::vector<std::vector<int>> bucket(8);
-      for (int i = off[lv]; i < off[lv + 1]; ++i) bucket[swz(wf[i]) & 7].push_back(wf[i]);
-      int o = off[lv];
-      for (size_t r = 0; o < off[lv + 1]; ++r)
-        for (int bq = 0; bq < 8; ++bq)
-          if (r < bucket[bq].size()) wfs[o++] = (uint16_t)bucket[bq][r];
+  void*& wbuf = p->solver->bin_wf[cmask];
+  if (!wbuf) {  // once per coupled-mode mask (cached with the dims-only solver structures)
+    std::vector<int> wf(E), off(k + 2, 0), cnt(k + 1, 0);
+    for (int l = 0; l < E; ++l) cnt[k - __builtin_popcount(l & cmask)]++;
+    for (int i = 0; i <= k; ++i) off[i + 1] = off[i] + cnt[i];
+    {
+      std::vector<int> pos(off.begin(), off.end() - 1);
+      for (int l = E - 1; l >= 0; --l) wf[pos[k - __builtin_popcount(l & cmask)]++] = l;
     }
+    std::vector<uint16_t> wfs(E);
+    {
+      auto swz = [](int q) { return q ^ (((q >> 3) ^ (q >> 6) ^ (q >> 9)) & 7); };
+      for (int lv = 0; lv <= k; ++lv) {
+        std::vector<std::vector<int>> bucket(8);
+        for (int i = off[lv]; i < off[lv + 1]; ++i) bucket[swz(wf[i]) & 7].push_back(wf[i]);
+        int o = off[lv];
+        for (size_t r = 0; o < off[lv + 1]; ++r)
+          for (int bq = 0; bq < 8; ++bq)
+            if (r < bucket[bq].size()) wfs[o++] = (uint16_t)bucket[bq][r];
+      }
+    }
+    const size_t bytes = E * sizeof(uint16_t) + (k + 2) * sizeof(int);
+    std::vector<char> blob(bytes);
+    std::memcpy(blob.data(), wfs.data(), E * sizeof(uint16_t));
+    std::memcpy(blob.data() + E * sizeof(uint16_t), off.data(), (k + 2) * sizeof(int));
+    NDS_CUDA(cudaMalloc(&wbuf, bytes));
+    NDS_CUDA(cudaMemcpy(wbuf, blob.data(), bytes, cudaMemcpyHostToDevice));
   }
-  const size_t fbytes = host.size() * sizeof(double2);
-  const size_t bytes = fbytes + E * sizeof(uint16_t) + (k + 2) * sizeof(int);
-  std::vector<char> blob(bytes);
-  std::memcpy(blob.data(), host.data(), fbytes);
-  std::memcpy(blob.data() + fbytes, wfs.data(), E * sizeof(uint16_t));
-  std::memcpy(blob.data() + fbytes + E * sizeof(uint16_t), off.data(), (k + 2) * sizeof(int));
-  NDS_CUDA(cudaMalloc(&p->fd_buf, bytes));
-  NDS_CUDA(cudaMemcpy(p->fd_buf, blob.data(), bytes, cudaMemcpyHostToDevice));
+  // the merged factors and T' go through a kernel parameter (no copy behind a streaming tensor)
+  nds::ParamBlob pb;
+  pb.count = (int)host.size();
+  std::memcpy(pb.v, host.data(), host.size() * sizeof(double2));
+  NDS_CUDA(cudaMallocFromPoolAsync((void**)&p->fd_buf, host.size() * sizeof(double2), p->ctx->pool, p->ctx->stream));
+  nds::param_blob_launch(pb, p->fd_buf, p->ctx->stream);
   p->fd = p->f;
   p->fd.pool = nullptr;  // owned by f
   for (int j = 0; j < N; ++j) {
@@ -694,8 +702,8 @@ void plan_binary_diag(nds_plan* p, const nds_z* const* u, const nds_z* const* t)
     p->fd.uh_col[j] = o + 12;
   }
   p->bin_t = p->fd_buf + (size_t)N * 16;
-  p->bin_wf = (const uint16_t*)((const char*)p->fd_buf + fbytes);
-  p->bin_wf_off = (const int*)((const char*)p->fd_buf + fbytes + E * sizeof(uint16_t));
+  p->bin_wf = (const uint16_t*)wbuf;
+  p->bin_wf_off = (const int*)((const char*)wbuf + E * sizeof(uint16_t));
   p->bin_wf_levels = k + 1;
   p->bin_diag = true;
 }
@@ -743,36 +751,41 @@ void plan_cubic_diag(nds_plan* p, const nds_z* const* u, const nds_z* const* t) 
     double cond = 0.0;
   };
   std::vector<std::vector<Cand>> cands(N);
-  std::vector<nds::EigJob> jobs;
+  nds::EigCands ec{};
+  int njobs = 0;
   int64_t vtot = 0;
   for (int j = 0; j < N; ++j)
     for (int64_t d = B; d <= std::min<int64_t>(p->dims[j], 128); d *= 2) {
-      if (p->dims[j] % d) continue;
-      Cand c{(int)d, (int)jobs.size(), (int)(p->dims[j] / d), vtot};
-      for (int q = 0; q < c.count; ++q) {
-        jobs.push_back({p->dims[j], q * d, p->f.geom.toff[j], vtot, (int)d, j});
-        vtot += d * d;
-      }
+      if (p->dims[j] % d || ec.count >= nds::kMaxEigCands) continue;
+      Cand c{(int)d, njobs, (int)(p->dims[j] / d), vtot};
+      ec.d[ec.count] = (int)d;
+      ec.first[ec.count] = njobs;
+      ec.n[ec.count] = p->dims[j];
+      ec.toff[ec.count] = p->f.geom.toff[j];
+      ec.voff[ec.count] = vtot;
+      ++ec.count;
+      njobs += c.count;
+      vtot += p->dims[j] * d;
       cands[j].push_back(c);
     }
+  ec.first[ec.count] = njobs;
+  for (int j = 0; j < N; ++j)
+    if (cands[j].empty()) return;
   cudaStream_t s = p->ctx->stream;
   int64_t sq = 0;
   for (int j = 0; j < N; ++j) sq += p->dims[j] * p->dims[j];
-  // device scratch: [jobs][cond][V pool][W pool][M_inv][M_fwd^H][T W][T']
-  const size_t jb_bytes = (jobs.size() * sizeof(nds::EigJob) + 255) / 256 * 256;
-  const size_t cd_bytes = (jobs.size() * sizeof(double) + 255) / 256 * 256;
+  // device scratch: [cond][V pool][W pool][M_inv][M_fwd^H][T W][T']
+  const size_t cd_bytes = ((size_t)njobs * sizeof(double) + 255) / 256 * 256;
   char* scratch = nullptr;
-  NDS_CUDA(cudaMallocFromPoolAsync((void**)&scratch, jb_bytes + cd_bytes + (size_t)(2 * vtot + 4 * sq) * sizeof(double2),
+  NDS_CUDA(cudaMallocFromPoolAsync((void**)&scratch, cd_bytes + (size_t)(2 * vtot + 4 * sq) * sizeof(double2),
                                    p->ctx->pool, s));
-  nds::EigJob* d_jobs = (nds::EigJob*)scratch;
-  double* d_cond = (double*)(scratch + jb_bytes);
-  double2* dv = (double2*)(scratch + jb_bytes + cd_bytes);
+  double* d_cond = (double*)scratch;
+  double2* dv = (double2*)(scratch + cd_bytes);
   double2* dw = dv + vtot;
   double2 *minv = dw + vtot, *mfh = minv + sq, *tw = mfh + sq, *tpr = tw + sq;
-  std::vector<double> cond(jobs.size());
-  NDS_CUDA(cudaMemcpyAsync(d_jobs, jobs.data(), jobs.size() * sizeof(nds::EigJob), cudaMemcpyHostToDevice, s));
-  nds::block_eig_launch(p->f.t_pool, d_jobs, (int)jobs.size(), dv, dw, d_cond, s);
-  NDS_CUDA(cudaMemcpyAsync(cond.data(), d_cond, jobs.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+  std::vector<double> cond(njobs);
+  nds::block_eig_launch(p->f.t_pool, ec, dv, dw, d_cond, s);
+  NDS_CUDA(cudaMemcpyAsync(cond.data(), d_cond, njobs * sizeof(double), cudaMemcpyDeviceToHost, s));
   NDS_CUDA(cudaStreamSynchronize(s));
   for (int j = 0; j < N; ++j)
     for (Cand& c : cands[j]) {
@@ -815,16 +828,12 @@ void plan_cubic_diag(nds_plan* p, const nds_z* const* u, const nds_z* const* t) 
       const int64_t ov = cands[j][sel[j]].voff;
       const double2* uj = p->f.u_col[j];  // U_j column-major (factor_layouts)
       const double2* tj = p->f.t_pool + p->f.geom.toff[j];
-      nds::blockdiag_mul_launch(n, d[j], uj, dv + ov, true, false, minv + o, s);
-      nds::blockdiag_mul_launch(n, d[j], uj, dw + ov, true, true, mfh + o, s);
-      nds::blockdiag_mul_launch(n, d[j], tj, dv + ov, true, false, tw + o, s);
-      nds::blockdiag_mul_launch(n, d[j], tw + o, dw + ov, false, false, tpr + o, s);
-      nds::blockdiag_fix_launch(n, d[j], tj, tpr + o, s);
+      nds::blockdiag_factors_launch(n, d[j], uj, tj, dv + ov, dw + ov, minv + o, mfh + o, tw + o, tpr + o, s);
       o += n * n;
     }
   }
-  device_factors(p->ctx, p->cd_inv, N, p->dims, minv, tpr, p->f.diag_pool);
-  device_factors(p->ctx, p->cd_fwd, N, p->dims, mfh, nullptr, nullptr);
+  device_factors(p->ctx, p->cd_inv, N, p->dims, minv, tpr, p->f.diag_pool, 1);  // U W: op U only
+  device_factors(p->ctx, p->cd_fwd, N, p->dims, mfh, nullptr, nullptr, 2);      // W^{-1} U^H: op U^H only
   NDS_CUDA(cudaFreeAsync(scratch, s));
   p->fc = p->cd_inv;
   p->fc.pool = nullptr;  // owned by cd_inv / cd_fwd
@@ -1040,9 +1049,11 @@ int execute(nds_plan* p, const double2* b, double2* x, double2* work, cudaEvent_
   return launches;
 }
 
+// after_upload: called once the factor upload is queued (nds_solve_schur streams B in from there,
+// so the small factor copy is not queued behind the tensor).
 void plan_create_impl(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z* const* u, const nds_z* const* t,
                       double singular_tol, unsigned flags, nds_plan** out, nds_singular* sing,
-                      bool defer_singular = false) {
+                      bool defer_singular = false, const std::function<void()>& after_upload = {}) {
   if (!out) throw Error(NDS_ERR_INVALID, "out is null");
   *out = nullptr;
   const int64_t total = checked_total(n_modes, dims, 2);
@@ -1060,6 +1071,7 @@ void plan_create_impl(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_
   for (int j = 0; diag_route && j < n_modes; ++j) diag_route = numerically_diagonal(dims[j], t[j]);
   p->fast_path = diag_route;
   upload_factors(ctx, p->f, n_modes, dims, u, t);
+  if (after_upload) after_upload();
   p->groups = nds::plan_binary_groups(n_modes, dims);
   // Singular check over all entries (sylvester.cpp:101-103 / :137): the first offender in the
   // reference's descending visiting order is the one with the largest flat index.
@@ -1092,7 +1104,7 @@ void plan_destroy_impl(nds_plan* p) {
   free_factors(p->f);
   free_factors(p->cd_inv);
   free_factors(p->cd_fwd);
-  if (p->fd_buf) cudaFree(p->fd_buf);
+  if (p->fd_buf) cudaFreeAsync(p->fd_buf, p->ctx->stream);
   delete p;  // the shared solver structures stay cached in the context
 }
 
@@ -1886,19 +1898,25 @@ int nds_solve_schur(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z*
     const int64_t total = checked_total(n_modes, dims, 2);
     if (!b || !x) throw Error(NDS_ERR_INVALID, "null tensor pointer");
     ensure_device(ctx);
-    // chunks of B start streaming in while the host sets the plan up (factor staging, singular
-    // scan); only the first one, so the factor upload does not queue behind the whole tensor
+    // chunks of B stream in while the host and the device set the plan up (singular scan,
+    // diagonalisation): pinned B — every chunk, queued right after the factor upload (so that
+    // small copy goes first and the link never idles); pageable B (staged through the pinned
+    // ring by host copies) — the first chunk, before the plan
     nds_plan probe;
     probe.n_modes = n_modes;
     std::memcpy(probe.dims, dims, n_modes * sizeof(int64_t));
     probe.total = total;
     probe.groups = nds::plan_binary_groups(n_modes, dims);
     const int K = chunk_count(&probe);
-    const int pre = K > 1 && (const void*)b != (const void*)x ? 1 : 0;
-    if (pre) prefetch_chunks(ctx, b, total, K, pre);
+    const bool can = K > 1 && (const void*)b != (const void*)x;
+    const bool pinned_b = can && !host_pageable(b);
+    const int pre = !can ? 0 : pinned_b ? K : 1;
+    if (can && !pinned_b) prefetch_chunks(ctx, b, total, K, pre);
+    std::function<void()> after;
+    if (pinned_b) after = [&] { prefetch_chunks(ctx, b, total, K, pre); };
     nds_plan* p = nullptr;
     try {
-      plan_create_impl(ctx, n_modes, dims, u, t, singular_tol, flags, &p, sing);
+      plan_create_impl(ctx, n_modes, dims, u, t, singular_tol, flags, &p, sing, false, after);
     } catch (...) {
       if (pre) cudaStreamSynchronize(ctx->copy);  // b must not be read after we return
       throw;

@@ -178,6 +178,7 @@ struct SolverCache {
   BinarySolvePlan bsp;
   SolvePlan sp;
   std::map<std::vector<int>, BlkSolvePlan> blk;
+  std::map<int, void*> bin_wf;  // all-binary diagonalised route: tile wavefront by coupled-mode mask
   ~SolverCache();
 };
 
@@ -185,21 +186,33 @@ void blk_solve_plan_build(BlkSolvePlan& bp, const SolvePlan& sp, const int* d);
 void blk_solve_plan_free(BlkSolvePlan& bp);
 int blk_backsub_launch(const SolvePlan& sp, const BlkSolvePlan& bp, const double2* t_pool, double2* c,
                        cudaStream_t stream, Recorder* rec = nullptr);
+// Small plan data written by a kernel from its by-value parameter (no copy-engine traffic, so it
+// does not queue behind a tensor streaming in): dst[0, count) = blob.v.
+constexpr int kParamBlobMax = 20 * NDS_MAX_MODES;
+struct ParamBlob {
+  int count;
+  double2 v[kParamBlobMax];
+};
+void param_blob_launch(const ParamBlob& blob, double2* dst, cudaStream_t stream);
 // Eigenvector blocks of the route's candidates (blockdiag.cu): job = block at row offset o of
 // T_j (n x n at t_pool + toff) with extent d <= 128; V, W = V^{-1} (d x d column-major at
 // vpool / wpool + voff) and cond_2(V) into cond[job] (inf on a repeated eigenvalue).
-struct EigJob {
-  int64_t n, o, toff, voff;
-  int d, mode;
+// Candidates are passed by value (no host->device copy in the plan, which runs while the tensor
+// streams in): candidate c covers jobs [first[c], first[c + 1]), blocks q = job - first[c].
+constexpr int kMaxEigCands = 5 * NDS_MAX_MODES;
+struct EigCands {
+  int count;
+  int d[kMaxEigCands];
+  int first[kMaxEigCands + 1];
+  int64_t n[kMaxEigCands], toff[kMaxEigCands], voff[kMaxEigCands];
 };
-void block_eig_launch(const double2* t_pool, const EigJob* jobs, int njobs, double2* vpool, double2* wpool,
-                      double* cond, cudaStream_t stream);
-// out = A blockdiag(Bq) (right = true) or blockdiag(Bq) A, A and out n x n column-major, blocks
-// of d x d column-major at blk + q d^2; conj_t: use Bq^H. Then (fix_t) T' cleanup: entries of a
-// diagonal d-block set to diag_src's diagonal exactly, entries below the block diagonal zeroed.
-void blockdiag_mul_launch(int64_t n, int d, const double2* a, const double2* blk, bool right, bool conj_t,
-                          double2* out, cudaStream_t stream);
-void blockdiag_fix_launch(int64_t n, int d, const double2* diag_src, double2* t, cudaStream_t stream);
+void block_eig_launch(const double2* t_pool, const EigCands& cands, double2* vpool, double2* wpool, double* cond,
+                      cudaStream_t stream);
+// The route's factors of one mode (n x n column-major; V, W = V^{-1}: n / d blocks of d x d):
+// minv = U blockdiag(V), mfh = U blockdiag(W)^H, tv = T blockdiag(V) (scratch),
+// tprime = blockdiag(W) T blockdiag(V) with diagonal d-blocks = diag(T) exactly, zero below.
+void blockdiag_factors_launch(int64_t n, int d, const double2* u, const double2* t, const double2* v, const double2* w,
+                              double2* minv, double2* mfh, double2* tv, double2* tprime, cudaStream_t stream);
 
 void solve_plan_build(SolvePlan& sp, int n_modes, const int64_t* dims, const int64_t* toff);
 void solve_plan_free(SolvePlan& sp);
@@ -241,7 +254,8 @@ void factor_layouts_launch(const FactorSet& f, const double2* raw, cudaStream_t 
 // Entries of the stage-blocked operand images of one n x n factor (0 when n is not a multiple
 // of 16), and their construction from u_row / u_col / uh_row / uh_col (transform.cu).
 int64_t blocked_entries(int64_t n);
-void blocked_layouts_launch(FactorSet& f, double2* base, cudaStream_t stream);
+// op_mask: bit 0 builds the images of U, bit 1 those of U^H (sets that use one op only).
+void blocked_layouts_launch(FactorSet& f, double2* base, cudaStream_t stream, int op_mask = 3);
 // min |den| over all entries and the largest flat index with |den| <= tol (-1 if none).
 void den_scan(const Geom& g, const double2* diag, double tol, double* min_abs, int64_t* max_bad, cudaStream_t stream,
               void* scratch /* >= 16 bytes device */);

@@ -546,12 +546,16 @@ __global__ void bblk_kernel(const double2* __restrict__ mcol, int n, int bn, dou
   }
 }
 
-void blocked_layouts_launch(FactorSet& f, double2* base, cudaStream_t stream) {
+void blocked_layouts_launch(FactorSet& f, double2* base, cudaStream_t stream, int op_mask) {
   double2* p = base;
   for (int j = 0; j < f.n_modes; ++j) {
     const int n = (int)f.dims[j];
     if (!blocked_entries(n)) continue;
     for (int op = 0; op < 2; ++op) {
+      if (!((op_mask >> op) & 1)) {  // not needed: keep the slot layout, skip the build
+        for (int sh = 0; sh < 2; ++sh) p += ablk_entries(n, sh ? 32 : 64) + bblk_entries(n, sh ? 64 : 32);
+        continue;
+      }
       const double2* mrow = op ? f.uh_row[j] : f.u_row[j];
       const double2* mcol = op ? f.uh_col[j] : f.u_col[j];
       for (int sh = 0; sh < 2; ++sh) {
