@@ -122,29 +122,42 @@ __global__ void __launch_bounds__(NT, 1)
           : "memory");
     } while (!done);
   };
-  auto load_stage = [&](int stage) {  // the producer cursor's k-tile into `stage`
-    const int j = pj;
-    const int k0 = kb_s[j] + pkt * BK;
-    const int64_t sj = g.strides[j];
-    // source rows k0.. of the tile column: the tile origin with mode j moved to row k0
-    const double2* src = Y + (base - so[j] * sj) + (int64_t)k0 * sj;
-    double2* dB = sB + stage * C::BSTAGE;
+  // producer per-thread state of its current mode: the SL elements' offsets inside a stage (the
+  // same for every k-tile of the mode), rebuilt only when the producer moves to another mode
+  int p_mode = -1;
+  int64_t p_gofs[SL];
+  int p_soff[SL];
+  const double2* p_src = nullptr;  // row 0 of mode p_mode through the tile's other coordinates
+  int64_t p_sj = 0;
+  auto producer_mode = [&](int j) {
+    p_mode = j;
+    p_sj = g.strides[j];
+    p_src = Y + (base - so[j] * p_sj);
     const int* cg = colg + j * TC;
 #pragma unroll
     for (int i = 0; i < SL; ++i) {
       const int e = tid + i * kBlkThreads;
-      int k, c, soff;
+      int k, c;
       if (j == 0) {  // mode 1: contiguous along k in HBM — k-fastest smem, XOR swizzle
         k = e % BK;
         c = e / BK;
-        soff = c * BK + (k ^ (BK >= 8 ? (c & 1) << 2 : 0));
+        p_soff[i] = c * BK + (k ^ (BK >= 8 ? (c & 1) << 2 : 0));
       } else {
         c = e % TC;
         k = e / TC;
-        soff = k * LDB + c;
+        p_soff[i] = k * LDB + c;
       }
-      cp_async16_bs(dB + soff, src + (int64_t)k * sj + cg[c]);
+      p_gofs[i] = (int64_t)k * p_sj + cg[c];
     }
+  };
+  auto load_stage = [&](int stage) {  // the producer cursor's k-tile into `stage`
+    const int j = pj;
+    if (j != p_mode) producer_mode(j);
+    const int k0 = kb_s[j] + pkt * BK;
+    const double2* src = p_src + (int64_t)k0 * p_sj;
+    double2* dB = sB + stage * C::BSTAGE;
+#pragma unroll
+    for (int i = 0; i < SL; ++i) cp_async16_bs(dB + p_soff[i], src + p_gofs[i]);
     if (tid < B * BK) {  // T'_j(so_j + r, k0 + k), rows fastest (column-major T: coalesced)
       const int r = tid % B, k = tid / B;
       cp_async16_bs(sA + stage * C::ASTAGE + r * ALD + k,
