@@ -40,8 +40,8 @@ struct BlkCfg {
   }
 };
 
-template <int N, int B, int BK, int ST, int NT>
-__global__ void __launch_bounds__(NT, 1)
+template <int N, int B, int BK, int ST, int NT, int MINB = 1>
+__global__ void __launch_bounds__(NT, MINB)
     blk_level_kernel(const BlkArgs ba, const double2* __restrict__ T, const int64_t* __restrict__ tiles,
                      double2* __restrict__ Y) {
   using C = BlkCfg<N, B, BK, ST, NT>;
@@ -302,7 +302,9 @@ struct BlkLaunchT {
 };
 // Measured (c1 / c3 solve): N = 3 — 256 threads, BK = 8, 3 stages: 1.31 ms (512 threads 1.37,
 // 4 stages 1.34, BK = 16 x 2 stages 1.46 / 1.49 with 512 threads); N = 4 — 512 threads, BK = 4,
-// 3 stages: 18.1 ms (256 threads 19.9, 4 stages 20.1, BK = 8 x 2 stages 18.9 / 19.3).
+// 3 stages: 18.1 ms (256 threads 19.9, 4 stages 20.1, BK = 8 x 2 stages 18.9 / 19.3). After the
+// producer-offset change (c1 1.195 ms): N = 3 with BK = 4 x 2 stages at 2 CTAs / SM (128
+// registers, spills) 1.169, BK = 4 x 3 stages 1.34.
 static BlkLaunchT blk_cfg(int n_modes, int b) {
   if (n_modes == 3 && b == 16) return {blk_level_kernel<3, 16, 8, 3, 256>, BlkCfg<3, 16, 8, 3, 256>::smem(), 256};
   if (n_modes == 4 && b == 8) return {blk_level_kernel<4, 8, 4, 3, 512>, BlkCfg<4, 8, 4, 3, 512>::smem(), 512};
