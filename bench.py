@@ -447,7 +447,7 @@ def main():
     value = world * P / (ms_step * 1e-3)
 
     # --- per-launch profile of the same workload (separate pass, CUDA events per launch) -----
-    plan.profile_begin(launches_per_step * args.steps + 8)
+    plan.profile_begin(2 * (launches_per_step + 4) * args.steps + 8)  # launches + the library's stage markers
     for _ in range(args.steps):
         plan.execute(d_b.data_ptr(), d_x.data_ptr(), d_w.data_ptr())
     recs = plan.profile_end()
@@ -501,6 +501,40 @@ def main():
         "solve_tflops": solve_flops / (solve_ms * 1e-3) / 1e12 if solve_ms else None,
         "solve_frac_fp64": (solve_flops / (solve_ms * 1e-3) / 1e12) / peak_tf if solve_ms else None,
     }
+    # every kernel class of the step against its roofline (north_star: "each kernel's achieved
+    # HBM GB/s or FP64 FLOP/s as a fraction of B200 peak"), from the per-launch CUDA events
+    hbm, hbm_src = hbm_peak()
+    per_kernel = []
+    if gemm:
+        g_ms = sum(ms for _, ms in gemm) / args.steps
+        g_fl = sum(8.0 * P * dims[abs(m) - 1] for m, _ in gemm) / args.steps
+        per_kernel.append({"kernel": "transform GEMM (zgemm_tma / zgemm_dmma)", "launches_per_step": len(gemm) // args.steps,
+                           "ms_per_step": round(g_ms, 4), "achieved": round(g_fl / (g_ms * 1e-3) / 1e12, 3),
+                           "unit": "TFLOP/s", "peak": peak_tf, "frac": round(g_fl / (g_ms * 1e-3) / 1e12 / peak_tf, 4),
+                           "bound": "FP64 tensor (DMMA)"})
+    if passes:
+        p_ms = sum(ms for _, ms in passes) / args.steps
+        p_by = 32.0 * P * (len(passes) // args.steps)
+        per_kernel.append({"kernel": "binary_pass_kernel (fused binary modes)", "launches_per_step": len(passes) // args.steps,
+                           "ms_per_step": round(p_ms, 4), "achieved": round(p_by / (p_ms * 1e-3) / 1e9, 1),
+                           "unit": "GB/s", "peak": hbm, "frac": round(p_by / (p_ms * 1e-3) / 1e9 / hbm, 4),
+                           "bound": "HBM"})
+    levels = by_kind.get("solve_level", [])
+    if levels and all(n == 2 for n in dims):  # the fused all-binary tile kernel: one read + one write
+        f_ms = sum(ms for _, ms in levels) / args.steps
+        per_kernel.append({"kernel": "binary_fused_solve_kernel (modes 1-12 fwd + tile solve + inv)",
+                           "launches_per_step": len(levels) // args.steps, "ms_per_step": round(f_ms, 4),
+                           "achieved": round(32.0 * P / (f_ms * 1e-3) / 1e9, 1), "unit": "GB/s", "peak": hbm,
+                           "frac": round(32.0 * P / (f_ms * 1e-3) / 1e9 / hbm, 4), "bound": "HBM / FP64 issue"})
+    elif solve_ms:
+        per_kernel.append({"kernel": "blk_level_kernel (block-diagonalised solve)" if sb_d else
+                           "solve (wavefront route: tile_diag_lines + far_group)",
+                           "launches_per_step": (len(levels) // args.steps) if levels else None,
+                           "ms_per_step": round(solve_ms, 4), "achieved": round(solve_flops / (solve_ms * 1e-3) / 1e12, 3),
+                           "unit": "TFLOP/s", "peak": peak_tf,
+                           "frac": round(solve_flops / (solve_ms * 1e-3) / 1e12 / peak_tf, 4),
+                           "bound": "FP64 tensor (DMMA)"})
+    kernels["per_kernel"] = per_kernel
 
     # --- end to end through the C-ABI host-buffer call -----------------------------------------
     e2e = None

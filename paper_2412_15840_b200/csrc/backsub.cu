@@ -522,7 +522,6 @@ int blk_backsub_launch(const SolvePlan& sp, const BlkSolvePlan& bp, const double
   BlkArgs ba;
   ba.g = g;
   for (int j = 0; j < NDS_MAX_MODES; ++j) ba.d[j] = j < g.n_modes ? bp.d[j] : 1;
-  if (rec) rec->mark(stream, -1, 0);
   int launches = 0;
   for (int lv = 0; lv < bp.levels; ++lv) {
     const int64_t nt = bp.level_off[lv + 1] - bp.level_off[lv];

@@ -352,3 +352,60 @@ def test_cubic_diagonalised_route(ctx, ref, name, dims, taken):
     assert rel_max(xs[False], x_ref) <= 1e-11
     r = ctx.solve(a, b)  # host path (chunked passes, split last pass) on the same route
     assert rel_max(r.x, x_ref) <= 1e-11
+
+
+def test_cubic_diagonalised_superblocks_and_guard(ctx, port):
+    """Super-block choice of the block-diagonalised route: every D_j is a multiple of the tile
+    edge dividing n_j, the level count is sum_j (n_j / D_j - 1) + 1, and the guard's bound holds.
+    A repeated eigenvalue inside a tile block (no eigenvector basis) makes the guard refuse the
+    route; both plans match the oracle's full solve."""
+    import torch
+    rng = np.random.default_rng(41)
+    dims = (64, 64, 64)
+    us, ts = rand_factors(rng, dims)
+    b = rand_c(rng, dims)
+    x_ref, _ = port.solve_schur(us, ts, b, flags=0)
+    ts_rep = [t.copy() for t in ts]
+    ts_rep[1][6, 6] = ts_rep[1][5, 5]  # same 16-row block of mode 2
+    x_rep, _ = port.solve_schur(us, ts_rep, b, flags=0)
+    d_b = torch.from_numpy(np.ascontiguousarray(b.ravel(order="F"))).cuda()
+    ctx.set_stream(torch.cuda.current_stream().cuda_stream)
+    for t_list, x_want, taken in ((ts, x_ref, True), (ts_rep, x_rep, False)):
+        plan = ctx.plan(us, t_list, allow_fast_path=False)
+        got, cond = plan.diagonalised()
+        assert got == taken
+        levels, d = plan.superblocks()
+        if taken:
+            assert cond <= 1e6
+            assert all(dj % 16 == 0 and n % dj == 0 for n, dj in zip(dims, d))
+            assert levels == sum(n // dj - 1 for n, dj in zip(dims, d)) + 1
+        else:
+            assert levels == 0 and d is None
+        d_x, d_w = torch.empty_like(d_b), torch.empty_like(d_b)
+        plan.execute(d_b.data_ptr(), d_x.data_ptr(), d_w.data_ptr())
+        torch.cuda.synchronize()
+        x = d_x.cpu().numpy().reshape(dims, order="F")
+        assert rel_max(x, x_want) <= 1e-11
+        plan.close()
+    ctx.set_stream(None)
+
+
+@pytest.mark.parametrize("n_modes,seed", [(16, 5), (24, 6)])
+def test_binary_diagonalised_inner_modes(ctx, ref, n_modes, seed):
+    """All-binary route: besides the outer modes, inner modes are diagonalised within the guard
+    (the fused kernel's tile wavefront shrinks to the coupled inner modes); the full solve through
+    the fused kernel (modes 1-12 pass first) matches the reference."""
+    import torch
+    a, b = configs.make_problem("c4", seed=seed, dims=(2,) * n_modes)
+    x_ref, _ = ref.solve(a, b)
+    us, ts = zip(*[ctx.schur(m) for m in a])
+    plan = ctx.plan(list(us), list(ts))
+    got, cond = plan.diagonalised()
+    assert got and cond <= 1e6
+    d_b = torch.from_numpy(np.ascontiguousarray(b.ravel(order="F"))).cuda()
+    d_x, d_w = torch.empty_like(d_b), torch.empty_like(d_b)
+    ctx.set_stream(torch.cuda.current_stream().cuda_stream)
+    plan.execute(d_b.data_ptr(), d_x.data_ptr(), d_w.data_ptr())
+    torch.cuda.synchronize()
+    ctx.set_stream(None)
+    assert rel_max(d_x.cpu().numpy().reshape(b.shape, order="F"), x_ref) <= 1e-12
