@@ -424,6 +424,161 @@ __global__ void __launch_bounds__(WM* WN * 32, MINB) zgemm_tma_kernel(const Gemm
   }
 }
 
+// Stage geometry of the short-K bulk-copy GEMM: the constant operand's stage image is UNPADDED
+// (BM x BK, 16-byte chunks XOR-swizzled by row parity: entry (r, k) at r BK + (k ^ 4 (r & 1)),
+// the same banks as the padded rows), which leaves room for a 4-stage ring at 2 CTAs / SM.
+// Measured (per pass): n = 128 (c3) 7.26 ms vs 7.36 with zgemm_tma_kernel's padded 3-stage ring;
+// n = 256 (c1) 0.917 vs 0.886 — so factors with n >= 256 keep the padded images and that kernel.
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool PAD = false>
+struct TmaCfg {
+  static constexpr int kThreads = WM * WN * 32;
+  static constexpr int kLdA = PAD ? BK + 4 : BK;
+  static constexpr int kLdB = BN + 2;  // complex; = 2 mod 8 -> conflict-free B fragments
+  static constexpr int kStageA = BM * kLdA;
+  static constexpr int kStageB = BK * kLdB;
+  static constexpr size_t kSmem = (size_t)STAGES * (kStageA + kStageB) * sizeof(double2);
+  static constexpr int MI = BM / WM / 8;
+  static constexpr int NI = BN / WN / 8;
+};
+__host__ __device__ __forceinline__ int ablk_swz(int r, int k) { return k ^ ((r & 1) << 2); }
+// Operand images of an n x n factor: padded rows for long K (n >= 256: 16 or more k-tiles, where
+// the 3-stage padded ring is faster) and for extents that take the 32 x 64 CTA shape (n = 96, c2:
+// 13.30 vs 13.10 ms with the deeper ring), swizzled unpadded rows with a 4-stage ring otherwise.
+__host__ __device__ __forceinline__ bool tma_padded(int64_t n) { return n >= 256 || n % 64 != 0; }
+
+// The short-K variant of zgemm_tma_kernel (row-major form only): unpadded, swizzled constant-
+// operand stages and a deeper ring.
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, int MINB>
+__global__ void __launch_bounds__(WM* WN * 32, MINB) zgemm_tma_swz_kernel(const GemmArgs g) {
+  constexpr bool PAD = false;
+  using Cfg = TmaCfg<BM, BN, BK, WM, WN, STAGES, PAD>;
+  constexpr int NW = WM * WN;
+  constexpr int MI = Cfg::MI, NI = Cfg::NI;
+  static_assert(BK == 16, "the stage images are 16 deep");
+  extern __shared__ __align__(16) double2 smem[];
+  double2* sA = smem;
+  double2* sB = smem + STAGES * Cfg::kStageA;
+  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int wy = warp / WN, wx = warp % WN;
+  const int64_t tile = blockIdx.x;
+  const int64_t row_tile = tile % g.ntile_rows;
+  const int64_t col_tile = tile / g.ntile_rows;
+  const int64_t row0 = row_tile * BM;
+  const int64_t a0 = (col_tile % g.ntile_a) << g.wshift;
+  const int64_t b0 = (col_tile / g.ntile_a) * (BN >> g.wshift);
+  const int W = 1 << g.wshift;
+  const int groups = BN >> g.wshift;
+  const int nk = g.K / BK;
+  // valid column groups of this tile; the rest of B stays zero in every stage
+  const int vgroups = (int)(g.blim - b0 < groups ? g.blim - b0 : groups);
+  if (vgroups < groups) {
+    for (int e = tid; e < STAGES * BK * BN; e += blockDim.x) {
+      const int st = e / (BK * BN), k = (e / BN) % BK, c = e % BN;
+      if ((c >> g.wshift) >= vgroups) sB[st * Cfg::kStageB + k * Cfg::kLdB + c] = make_double2(0.0, 0.0);
+    }
+  }
+  if (tid == 0) {
+    for (int s2 = 0; s2 < STAGES; ++s2) {
+      mbar_init(&full[s2], 1);
+      mbar_init(&empty[s2], NW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  const unsigned stage_bytes = (unsigned)(Cfg::kStageA * 16 + vgroups * BK * W * 16);
+  // warp 0: fill stage st with k-tile kt (lane 0 arms the barrier, the lanes issue the copies)
+  auto produce = [&](int st, int kt) {
+    if (lane == 0) mbar_expect_tx(&full[st], stage_bytes);
+    __syncwarp();
+    double2* dA = sA + st * Cfg::kStageA;
+    double2* dB = sB + st * Cfg::kStageB;
+    const int k0 = kt * BK;
+    if (lane == 0) bulk_g2s(dA, g.blk + ((row_tile * nk + kt) * BM) * Cfg::kLdA, Cfg::kStageA * 16, &full[st]);
+    for (int e = lane; e < BK * vgroups; e += 32) {
+      const int k = e / vgroups, q = e % vgroups;
+      bulk_g2s(dB + k * Cfg::kLdB + q * W, g.B + (int64_t)(k0 + k) * g.ldbk + a0 + (b0 + q) * g.ldbb, W * 16,
+               &full[st]);
+    }
+  };
+  if (warp == 0)
+    for (int s2 = 0; s2 < STAGES && s2 < nk; ++s2) produce(s2, s2);
+
+  double cre[MI][NI][2], cim[MI][NI][2], c3[MI][NI][2];
+#pragma unroll
+  for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < NI; ++ni)
+      cre[mi][ni][0] = cre[mi][ni][1] = cim[mi][ni][0] = cim[mi][ni][1] = c3[mi][ni][0] = c3[mi][ni][1] = 0.0;
+  const int arow = wy * (BM / WM) + (lane >> 2);
+  const int bcol = wx * (BN / WN) + (lane >> 2);
+  const int kq = lane & 3;
+  const int asw = PAD ? 0 : (arow & 1) << 2;  // rows arow + 8 mi share the parity
+  for (int kt = 0; kt < nk; ++kt) {
+    if (warp == 0 && kt >= 1 && kt - 1 + STAGES < nk) {  // refill the stage k-tile kt - 1 used
+      const int st = (kt - 1) % STAGES;
+      if (lane == 0) mbar_wait(&empty[st], ((kt - 1) / STAGES) & 1);
+      __syncwarp();
+      produce(st, kt - 1 + STAGES);
+    }
+    const int st = kt % STAGES;
+    mbar_wait(&full[st], (kt / STAGES) & 1);
+    const double2* cA = sA + st * Cfg::kStageA;
+    const double2* cB = sB + st * Cfg::kStageB;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double ar[MI], ai[MI], an[MI], br[NI], bi[NI], bs[NI];
+#pragma unroll
+      for (int mi = 0; mi < MI; ++mi) {
+        const double2 v = cA[(arow + mi * 8) * Cfg::kLdA + ((kk + kq) ^ asw)];
+        ar[mi] = v.x;
+        ai[mi] = v.y;
+        an[mi] = v.x + v.y;
+      }
+#pragma unroll
+      for (int ni = 0; ni < NI; ++ni) {
+        const double2 v = cB[(kk + kq) * Cfg::kLdB + bcol + ni * 8];
+        br[ni] = v.x;
+        bi[ni] = v.y;
+        bs[ni] = v.x + v.y;
+      }
+#pragma unroll
+      for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < NI; ++ni) {
+          dmma(cre[mi][ni][0], cre[mi][ni][1], ar[mi], br[ni]);
+          dmma(cim[mi][ni][0], cim[mi][ni][1], ai[mi], bi[ni]);
+          dmma(c3[mi][ni][0], c3[mi][ni][1], an[mi], bs[ni]);
+        }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+  }
+
+#pragma unroll
+  for (int mi = 0; mi < MI; ++mi) {
+    const int64_t r = row0 + wy * (BM / WM) + mi * 8 + (lane >> 2);
+    if (r >= g.rows) continue;
+#pragma unroll
+    for (int ni = 0; ni < NI; ++ni) {
+      const int c = wx * (BN / WN) + ni * 8 + 2 * kq;
+      const int64_t ga = a0 + (c & (W - 1));
+      const int64_t gb = b0 + (c >> g.wshift);
+      if (gb >= g.blim) continue;
+      double2* dst = g.C + r * g.ldcr + ga + gb * g.ldcb;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (ga + h < g.alim) {
+          double2 v = make_double2(cre[mi][ni][h] - cim[mi][ni][h], c3[mi][ni][h] - cre[mi][ni][h] - cim[mi][ni][h]);
+          if (g.accumulate) v = cadd(dst[h], v);
+          dst[h] = v;
+        }
+      }
+    }
+  }
+}
+
 // Tile configurations. 3M kernels, 2 CTAs / SM, 8 warps, BK = 16, 3 stages:
 //   kWide: 64 x 32 per CTA;  kTall: 32 x 64 per CTA; warps of 16 x 16.
 // The shape with the least padded output is chosen per GEMM (ties: kWide).
@@ -431,12 +586,15 @@ __global__ void __launch_bounds__(WM* WN * 32, MINB) zgemm_tma_kernel(const Gemm
 template <int BM, int BN, int BK, int WM, int WN, int ST, bool M3, int MINB = 1>
 static void launch_gemm_t(GemmArgs g, cudaStream_t stream) {
   using Cfg = GemmCfg<BM, BN, BK, WM, WN, ST>;
+  using SCfg = TmaCfg<BM, BN, BK, WM, WN, 4>;
   static bool attr_set = false;
   auto kern = zgemm_dmma_kernel<BM, BN, BK, WM, WN, ST, M3, MINB>;
   auto tkern = zgemm_tma_kernel<BM, BN, BK, WM, WN, ST, MINB>;
+  auto skern = zgemm_tma_swz_kernel<BM, BN, BK, WM, WN, 4, MINB>;
   if (!attr_set) {
     NDS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem));
     NDS_CUDA(cudaFuncSetAttribute(tkern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem));
+    NDS_CUDA(cudaFuncSetAttribute(skern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SCfg::kSmem));
     attr_set = true;
   }
   const bool colm = g.colm != 0;
@@ -449,7 +607,9 @@ static void launch_gemm_t(GemmArgs g, cudaStream_t stream) {
   // bulk-copy feed for the row-major form only: the mode-1 form would need one copy per 256-byte
   // row of the tensor operand (64 per stage) and measured 1.32 ms per c1 pass vs 0.94 with cp.async
   const bool tma = M3 && g.blk && !colm && g.K % BK == 0 && g.alim % W == 0;
-  if (tma)
+  if (tma && !tma_padded(g.K))  // short K: the swizzled images of that factor, 4-stage ring
+    skern<<<(unsigned)tiles, SCfg::kThreads, SCfg::kSmem, stream>>>(g);
+  else if (tma)
     tkern<<<(unsigned)tiles, Cfg::kThreads, Cfg::kSmem, stream>>>(g, colm ? 1 : 0);
   else
     kern<<<(unsigned)tiles, Cfg::kThreads, Cfg::kSmem, stream>>>(g);
@@ -509,7 +669,7 @@ static void launch_gemm_auto(GemmArgs g, bool colm, int64_t inner, cudaStream_t 
 
 // ---- stage-blocked operand images for the bulk-copy GEMM (FactorSet::ablk / bblk) ---------------
 // shape 0 = kWide (BM 64, BN 32), 1 = kTall (BM 32, BN 64); BK = 16, row pads BK + 4 / BN + 2.
-static int64_t ablk_entries(int64_t n, int bm) { return (n + bm - 1) / bm * bm * (n / 16) * 20; }
+static int64_t ablk_entries(int64_t n, int bm) { return (n + bm - 1) / bm * bm * (n / 16) * (tma_padded(n) ? 20 : 16); }
 static int64_t bblk_entries(int64_t n, int bn) { return (n + bn - 1) / bn * (n / 16) * 16 * (bn + 2); }
 
 int64_t blocked_entries(int64_t n) {
@@ -517,17 +677,21 @@ int64_t blocked_entries(int64_t n) {
   return 2 * (ablk_entries(n, 64) + ablk_entries(n, 32) + bblk_entries(n, 32) + bblk_entries(n, 64));
 }
 
-// A image: [row tile][k tile][BM][20]: (row, k) of M row-major, zero beyond n rows / 16 k.
+// A image: [row tile][k tile][BM][ld]: (row, k) of M row-major, zero beyond n rows; ld = 20
+// (padded, k at slot k, zero pad) when tma_padded(n), else 16 with k at slot ablk_swz(r, k).
 __global__ void ablk_kernel(const double2* __restrict__ mrow, int n, int bm, double2* __restrict__ out, int64_t total) {
   const int nkt = n / 16;
+  const bool pad = tma_padded(n);
+  const int ld = pad ? 20 : 16;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int c = (int)(e % 20);
-    const int64_t q = e / 20;
+    const int slot = (int)(e % ld);
+    const int64_t q = e / ld;
     const int r = (int)(q % bm);
     const int64_t q2 = q / bm;
     const int kt = (int)(q2 % nkt);
     const int64_t rt = q2 / nkt;
     const int64_t row = rt * bm + r;
+    const int c = pad ? slot : ablk_swz(r, slot);  // the swizzle is an involution
     out[e] = (row < n && c < 16) ? mrow[row * n + kt * 16 + c] : make_double2(0.0, 0.0);
   }
 }
@@ -565,9 +729,9 @@ void blocked_layouts_launch(FactorSet& f, double2* base, cudaStream_t stream, in
         ablk_kernel<<<(unsigned)std::min<int64_t>((na + 255) / 256, 1024), 256, 0, stream>>>(mrow, n, bm, p, na);
         NDS_LAUNCH_CHECK();
         p += na;
-        f.bblk[j][op][sh] = p;
-        bblk_kernel<<<(unsigned)std::min<int64_t>((nb + 255) / 256, 1024), 256, 0, stream>>>(mcol, n, bn, p, nb);
-        NDS_LAUNCH_CHECK();
+        // the mode-1 (column-major) form keeps the cp.async kernel, so its B images are not built
+        f.bblk[j][op][sh] = nullptr;
+        (void)mcol;
         p += nb;
       }
     }
