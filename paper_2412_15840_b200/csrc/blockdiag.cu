@@ -189,6 +189,143 @@ void block_eig_launch(const double2* t_pool, const EigCands& cands, double2* vpo
   NDS_LAUNCH_CHECK();
 }
 
+// ---- Schur reordering (ZTREXC by adjacent swaps, all pairs of a round at once) -----------------
+// Reorders the diagonal of every upper triangular T_j (n x n column-major, in place) by unitary
+// adjacent swaps, accumulating the rotations into U_j (T_j = U_j^H A_j U_j stays a Schur form).
+// Target: position P holds the eigenvalue whose rank by real part (ties by imaginary part, then
+// position) is R(P) = the digits of P read in reverse over the mixed radix (B, 2, 2, .., rest):
+// then every aligned block of B 2^k positions holds eigenvalues spread evenly over the spectrum
+// instead of the neighbours the QR iteration deflates together, which is what keeps the
+// eigenvector matrices of the diagonal blocks well conditioned (c2: prod cond at D = 16 from 1e19
+// to 7e2). Odd-even transposition sort: n rounds; in a round the pairs (k, k+1) of one parity whose
+// keys are out of order swap — per pair a ZLARTG rotation of (T(k,k+1), T(k+1,k+1) - T(k,k)),
+// applied to rows k, k+1 (columns > k+1), then to columns k, k+1 (rows < k) of T and of U, and
+// T(k,k) <-> T(k+1,k+1) (T(k,k+1) is unchanged). Disjoint pairs commute (left vs right
+// multiplications), so a round is three barrier-separated phases. One CTA per mode.
+__device__ __forceinline__ void zlartg_dev(double2 f, double2 g, double& cs, double2& sn) {
+  const double af = hypot(f.x, f.y), ag = hypot(g.x, g.y);
+  if (ag == 0.0) {
+    cs = 1.0;
+    sn = make_double2(0.0, 0.0);
+  } else if (af == 0.0) {
+    cs = 0.0;
+    sn = make_double2(g.x / ag, -g.y / ag);  // conj(g) / |g|
+  } else {
+    const double nrm = hypot(af, ag);
+    cs = af / nrm;
+    const double2 fu = make_double2(f.x / af, f.y / af);                 // f / |f|
+    const double2 gc = make_double2(g.x / nrm, -g.y / nrm);              // conj(g) / norm
+    sn = cmul(fu, gc);
+  }
+}
+__global__ void __launch_bounds__(1024) schur_reorder_kernel(const ReorderArgs ra, double2* __restrict__ tpool,
+                                                             double2* __restrict__ upool) {
+  __shared__ int key[kReorderMaxN];
+  __shared__ int act[kReorderMaxN / 2];
+  __shared__ double rc[kReorderMaxN / 2];
+  __shared__ double2 rs[kReorderMaxN / 2];
+  const int m = blockIdx.x;
+  const int n = ra.n[m];
+  double2* T = tpool + ra.off[m];
+  double2* U = upool + ra.off[m];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  if (n > kReorderMaxN || ra.nrad[m] <= 0) return;
+  // target position of the eigenvalue now at position p: its rank s, digits of s over the reversed
+  // radices (most significant = the within-block digit), recomposed over the radices
+  for (int p = tid; p < n; p += nt) {
+    const double2 lp = T[p + (int64_t)p * n];
+    int srank = 0;
+    for (int q = 0; q < n; ++q) {
+      const double2 lq = T[q + (int64_t)q * n];
+      srank += (lq.x < lp.x) || (lq.x == lp.x && (lq.y < lp.y || (lq.y == lp.y && q < p)));
+    }
+    int rem = srank, pos = 0, place = 1;
+    // weights of R: digit i has weight prod_{k > i} r_k; peel from the most significant (i = 0)
+    int wt = 1;
+    for (int i = 1; i < ra.nrad[m]; ++i) wt *= ra.rad[m][i];
+    for (int i = 0; i < ra.nrad[m]; ++i) {
+      const int d = rem / wt;
+      rem -= d * wt;
+      pos += d * place;
+      place *= ra.rad[m][i];
+      if (i + 1 < ra.nrad[m]) wt /= ra.rad[m][i + 1];
+    }
+    key[p] = pos;
+  }
+  __syncthreads();
+  for (int round = 0; round < n; ++round) {
+    const int par = round & 1, np = (n - par) / 2;
+    for (int i = tid; i < np; i += nt) {  // 1. rotations of the out-of-order pairs
+      const int k = par + 2 * i;
+      const bool sw = key[k] > key[k + 1];
+      act[i] = sw;
+      if (sw) {
+        const double2 t11 = T[k + (int64_t)k * n], t22 = T[(k + 1) + (int64_t)(k + 1) * n];
+        double cs;
+        double2 sn;
+        zlartg_dev(T[k + (int64_t)(k + 1) * n], csub(t22, t11), cs, sn);
+        rc[i] = cs;
+        rs[i] = sn;
+      }
+    }
+    __syncthreads();
+    // 2. rows k, k+1, columns > k+1: (x, y) <- (c x + s y, c y - conj(s) x)
+    for (int64_t e = tid; e < (int64_t)np * n; e += nt) {
+      const int i = (int)(e / n), j = (int)(e % n), k = par + 2 * i;
+      if (!act[i] || j <= k + 1) continue;
+      const double c = rc[i];
+      const double2 sv = rs[i];
+      const double2 x = T[k + (int64_t)j * n], y = T[(k + 1) + (int64_t)j * n];
+      T[k + (int64_t)j * n] = cadd(make_double2(c * x.x, c * x.y), cmul(sv, y));
+      T[(k + 1) + (int64_t)j * n] = csub(make_double2(c * y.x, c * y.y), cmul(make_double2(sv.x, -sv.y), x));
+    }
+    __syncthreads();
+    // 3. columns k, k+1 of T (rows < k) and of U (all rows) with (c, conj(s)); the diagonal swap
+    for (int64_t e = tid; e < (int64_t)np * n; e += nt) {
+      const int i = (int)(e / n), r = (int)(e % n), k = par + 2 * i;
+      if (!act[i]) continue;
+      const double c = rc[i];
+      const double2 sc = make_double2(rs[i].x, -rs[i].y);  // conj(s)
+      if (r < k) {
+        const double2 x = T[r + (int64_t)k * n], y = T[r + (int64_t)(k + 1) * n];
+        T[r + (int64_t)k * n] = cadd(make_double2(c * x.x, c * x.y), cmul(sc, y));
+        T[r + (int64_t)(k + 1) * n] = csub(make_double2(c * y.x, c * y.y), cmul(make_double2(sc.x, -sc.y), x));
+      }
+      {
+        const double2 x = U[r + (int64_t)k * n], y = U[r + (int64_t)(k + 1) * n];
+        U[r + (int64_t)k * n] = cadd(make_double2(c * x.x, c * x.y), cmul(sc, y));
+        U[r + (int64_t)(k + 1) * n] = csub(make_double2(c * y.x, c * y.y), cmul(make_double2(sc.x, -sc.y), x));
+      }
+      if (r == 0) {
+        const double2 t11 = T[k + (int64_t)k * n];
+        T[k + (int64_t)k * n] = T[(k + 1) + (int64_t)(k + 1) * n];
+        T[(k + 1) + (int64_t)(k + 1) * n] = t11;
+        const int kk = key[k];
+        key[k] = key[k + 1];
+        key[k + 1] = kk;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+void schur_reorder_launch(const ReorderArgs& ra, int n_modes, double2* tpool, double2* upool, cudaStream_t stream) {
+  schur_reorder_kernel<<<(unsigned)n_modes, 1024, 0, stream>>>(ra, tpool, upool);
+  NDS_LAUNCH_CHECK();
+}
+
+__global__ void diag_extract_kernel(const Geom g, const double2* __restrict__ t, double2* __restrict__ diag) {
+  const int m = blockIdx.y;
+  const int64_t n = g.dims[m];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    diag[g.doff[m] + i] = t[g.toff[m] + i * (n + 1)];
+}
+
+void diag_extract_launch(const Geom& g, const double2* t_pool, double2* diag, cudaStream_t stream) {
+  diag_extract_kernel<<<dim3(4, (unsigned)g.n_modes), 256, 0, stream>>>(g, t_pool, diag);
+  NDS_LAUNCH_CHECK();
+}
+
 __global__ void param_blob_kernel(const ParamBlob b, double2* __restrict__ dst) {
   for (int i = threadIdx.x; i < b.count; i += blockDim.x) dst[i] = b.v[i];
 }

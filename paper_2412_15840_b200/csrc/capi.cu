@@ -403,8 +403,11 @@ void device_factors(nds_ctx* ctx, nds::FactorSet& f, int n_modes, const int64_t*
     f.t_pool = f.pool + off;
     f.diag_pool = f.pool + off + sq;
     NDS_CUDA(cudaMemcpyAsync(f.t_pool, d_t, (size_t)sq * sizeof(double2), cudaMemcpyDeviceToDevice, ctx->stream));
-    NDS_CUDA(cudaMemcpyAsync(f.diag_pool, d_diag, (size_t)diag * sizeof(double2), cudaMemcpyDeviceToDevice,
-                             ctx->stream));
+    if (d_diag)
+      NDS_CUDA(cudaMemcpyAsync(f.diag_pool, d_diag, (size_t)diag * sizeof(double2), cudaMemcpyDeviceToDevice,
+                               ctx->stream));
+    else
+      nds::diag_extract_launch(f.geom, f.t_pool, f.diag_pool, ctx->stream);
   }
   double2* raw = f.pool + 4 * sq + n_t + n_d;
   NDS_CUDA(cudaMemcpyAsync(raw, d_u, (size_t)sq * sizeof(double2), cudaMemcpyDeviceToDevice, ctx->stream));
@@ -774,17 +777,38 @@ void plan_cubic_diag(nds_plan* p, const nds_z* const* u, const nds_z* const* t) 
   cudaStream_t s = p->ctx->stream;
   int64_t sq = 0;
   for (int j = 0; j < N; ++j) sq += p->dims[j] * p->dims[j];
-  // device scratch: [cond][V pool][W pool][M_inv][M_fwd^H][T W][T']
+  // device scratch: [cond][V pool][W pool][M_inv][M_fwd^H][T W][T'][T~][U~]
   const size_t cd_bytes = ((size_t)njobs * sizeof(double) + 255) / 256 * 256;
   char* scratch = nullptr;
-  NDS_CUDA(cudaMallocFromPoolAsync((void**)&scratch, cd_bytes + (size_t)(2 * vtot + 4 * sq) * sizeof(double2),
+  NDS_CUDA(cudaMallocFromPoolAsync((void**)&scratch, cd_bytes + (size_t)(2 * vtot + 6 * sq) * sizeof(double2),
                                    p->ctx->pool, s));
   double* d_cond = (double*)scratch;
   double2* dv = (double2*)(scratch + cd_bytes);
   double2* dw = dv + vtot;
-  double2 *minv = dw + vtot, *mfh = minv + sq, *tw = mfh + sq, *tpr = tw + sq;
+  double2 *minv = dw + vtot, *mfh = minv + sq, *tw = mfh + sq, *tpr = tw + sq, *tre = tpr + sq, *ure = tre + sq;
+  // the Schur forms reordered (schur_reorder_kernel: eigenvalues spread over every aligned block)
+  // into T~ = Q^H T Q, U~ = U Q: the route's blocks, factors and denominators all come from them
+  // (the same operator; the singular check above ran on the caller's T with the same denominators)
+  NDS_CUDA(cudaMemcpyAsync(tre, p->f.t_pool, (size_t)sq * sizeof(double2), cudaMemcpyDeviceToDevice, s));
+  nds::ReorderArgs ra{};
+  for (int j = 0; j < N; ++j) {
+    const int64_t n = p->dims[j];
+    NDS_CUDA(cudaMemcpyAsync(ure + p->f.geom.toff[j], p->f.u_col[j], (size_t)(n * n) * sizeof(double2),
+                             cudaMemcpyDeviceToDevice, s));
+    ra.n[j] = (int)n;
+    ra.off[j] = p->f.geom.toff[j];
+    int nr = 0, prod = B;
+    ra.rad[j][nr++] = B;
+    while (prod * 2 <= 128 && n % (prod * 2) == 0 && nr < 11) {
+      ra.rad[j][nr++] = 2;
+      prod *= 2;
+    }
+    if (n / prod > 1) ra.rad[j][nr++] = (int)(n / prod);
+    ra.nrad[j] = n <= nds::kReorderMaxN ? nr : 0;  // larger extents keep their order
+  }
+  nds::schur_reorder_launch(ra, N, tre, ure, s);
   std::vector<double> cond(njobs);
-  nds::block_eig_launch(p->f.t_pool, ec, dv, dw, d_cond, s);
+  nds::block_eig_launch(tre, ec, dv, dw, d_cond, s);
   NDS_CUDA(cudaMemcpyAsync(cond.data(), d_cond, njobs * sizeof(double), cudaMemcpyDeviceToHost, s));
   NDS_CUDA(cudaStreamSynchronize(s));
   for (int j = 0; j < N; ++j)
@@ -826,13 +850,14 @@ void plan_cubic_diag(nds_plan* p, const nds_z* const* u, const nds_z* const* t) 
     for (int j = 0; j < N; ++j) {
       const int64_t n = p->dims[j];
       const int64_t ov = cands[j][sel[j]].voff;
-      const double2* uj = p->f.u_col[j];  // U_j column-major (factor_layouts)
-      const double2* tj = p->f.t_pool + p->f.geom.toff[j];
+      const double2* uj = ure + p->f.geom.toff[j];  // U~_j, T~_j column-major
+      const double2* tj = tre + p->f.geom.toff[j];
       nds::blockdiag_factors_launch(n, d[j], uj, tj, dv + ov, dw + ov, minv + o, mfh + o, tw + o, tpr + o, s);
       o += n * n;
     }
   }
-  device_factors(p->ctx, p->cd_inv, N, p->dims, minv, tpr, p->f.diag_pool, 1);  // U W: op U only
+  device_factors(p->ctx, p->cd_inv, N, p->dims, minv, tpr, nullptr, 1);  // U W: op U only; diag from T'
+
   device_factors(p->ctx, p->cd_fwd, N, p->dims, mfh, nullptr, nullptr, 2);      // W^{-1} U^H: op U^H only
   NDS_CUDA(cudaFreeAsync(scratch, s));
   p->fc = p->cd_inv;

@@ -186,6 +186,20 @@ void blk_solve_plan_build(BlkSolvePlan& bp, const SolvePlan& sp, const int* d);
 void blk_solve_plan_free(BlkSolvePlan& bp);
 int blk_backsub_launch(const SolvePlan& sp, const BlkSolvePlan& bp, const double2* t_pool, double2* c,
                        cudaStream_t stream, Recorder* rec = nullptr);
+// Schur reordering of the block-diagonalised route (blockdiag.cu): per mode, T_j and U_j (n x n
+// column-major at off[m] in the two pools, in place) reordered so the eigenvalue of real-part rank
+// R(P) sits at position P, R = digit reversal over the radices rad[m][0..nrad) (least significant
+// first: the tile edge, then 2s, then the rest); nrad = 0 skips the mode.
+constexpr int kReorderMaxN = 1024;
+struct ReorderArgs {
+  int n[NDS_MAX_MODES];
+  int64_t off[NDS_MAX_MODES];
+  int nrad[NDS_MAX_MODES];
+  int rad[NDS_MAX_MODES][12];
+};
+void schur_reorder_launch(const ReorderArgs& ra, int n_modes, double2* tpool, double2* upool, cudaStream_t stream);
+// diag(T_j) of every mode (t_pool at g.toff) into diag (at g.doff).
+void diag_extract_launch(const Geom& g, const double2* t_pool, double2* diag, cudaStream_t stream);
 // Small plan data written by a kernel from its by-value parameter (no copy-engine traffic, so it
 // does not queue behind a tensor streaming in): dst[0, count) = blob.v.
 constexpr int kParamBlobMax = 20 * NDS_MAX_MODES;

@@ -313,16 +313,18 @@ def test_binary_diagonalised_route_matches_coupled_solve(ctx, ref, n_modes, seed
 
 
 DIAG_CASES = [("c1", (128, 128, 64), True), ("c1", (64, 64, 64), True), ("c3", (64, 64, 32, 32), True),
-              ("c3", (32, 32, 32, 32), True), ("c2", (32, 32, 32, 32), False)]
+              ("c3", (32, 32, 32, 32), True), ("c2", (32, 32, 32, 32), True), ("c2", (48, 48, 48, 48), True)]
 
 
 @pytest.mark.parametrize("name,dims,taken", DIAG_CASES, ids=[f"{n}-{'x'.join(map(str, d))}" for n, d, _ in DIAG_CASES])
 def test_cubic_diagonalised_route(ctx, ref, name, dims, taken):
     """Block-diagonalised cubic route (capi.cu plan_cubic_diag): full solves replace T_j by
     W_j^{-1} T_j W_j (W_j = eigenvectors of T_j's diagonal tile blocks), so the diagonal tiles are
-    divisions. The guard takes it for the Gaussian configs (c1, c3) and refuses the clustered
-    advection-diffusion spectra (c2). The route, the wavefront route (NO_DIAGONALISE) and the stage
-    APIs (plain factors) all match the reference's X at the north_star tolerance."""
+    divisions. With the Schur forms reordered (eigenvalues spread over every block) the guard takes
+    it for the Gaussian configs (c1, c3) and for the advection-diffusion spectra of c2 (refused in
+    the QR iteration's order: clustered neighbours). The route, the wavefront route
+    (NO_DIAGONALISE) and the stage APIs (plain factors) all match the reference's X at the
+    north_star tolerance."""
     import torch
     a, b = configs.make_problem(name, seed=1, dims=dims)
     x_ref, _ = ref.solve(a, b)
@@ -357,8 +359,10 @@ def test_cubic_diagonalised_route(ctx, ref, name, dims, taken):
 def test_cubic_diagonalised_superblocks_and_guard(ctx, port):
     """Super-block choice of the block-diagonalised route: every D_j is a multiple of the tile
     edge dividing n_j, the level count is sum_j (n_j / D_j - 1) + 1, and the guard's bound holds.
-    A repeated eigenvalue inside a tile block (no eigenvector basis) makes the guard refuse the
-    route; both plans match the oracle's full solve."""
+    The plan reorders the Schur forms so every block holds eigenvalues spread over the spectrum, so
+    a repeated eigenvalue still admits the route (the copies land in different blocks), while a mode
+    whose eigenvalues are ALL equal (every block repeats one: no eigenvector basis) makes the guard
+    refuse it; all plans match the oracle's full solve."""
     import torch
     rng = np.random.default_rng(41)
     dims = (64, 64, 64)
@@ -366,11 +370,14 @@ def test_cubic_diagonalised_superblocks_and_guard(ctx, port):
     b = rand_c(rng, dims)
     x_ref, _ = port.solve_schur(us, ts, b, flags=0)
     ts_rep = [t.copy() for t in ts]
-    ts_rep[1][6, 6] = ts_rep[1][5, 5]  # same 16-row block of mode 2
+    ts_rep[1][6, 6] = ts_rep[1][5, 5]  # a repeated eigenvalue (same 16-row block before reordering)
     x_rep, _ = port.solve_schur(us, ts_rep, b, flags=0)
+    ts_all = [t.copy() for t in ts]
+    ts_all[1][np.diag_indices(dims[1])] = 2.5 + 0.25j  # every eigenvalue of mode 2 the same
+    x_all, _ = port.solve_schur(us, ts_all, b, flags=0)
     d_b = torch.from_numpy(np.ascontiguousarray(b.ravel(order="F"))).cuda()
     ctx.set_stream(torch.cuda.current_stream().cuda_stream)
-    for t_list, x_want, taken in ((ts, x_ref, True), (ts_rep, x_rep, False)):
+    for t_list, x_want, taken in ((ts, x_ref, True), (ts_rep, x_rep, True), (ts_all, x_all, False)):
         plan = ctx.plan(us, t_list, allow_fast_path=False)
         got, cond = plan.diagonalised()
         assert got == taken
