@@ -52,6 +52,7 @@ __global__ void __launch_bounds__(kEigThreads) block_eig_kernel(const double2* _
   while (ci + 1 < cs.count && (int)blockIdx.x >= cs.first[ci + 1]) ++ci;
   const int q = blockIdx.x - cs.first[ci];
   const int d = cs.d[ci];
+  if (d > 128) return;  // block_eig_big_kernel's job
   const int k = threadIdx.x, lane = k & 31, warp = k >> 5;
   const int64_t n = cs.n[ci], o = (int64_t)q * d;
   const double2* T = t_pool + cs.toff[ci];
@@ -173,12 +174,157 @@ __global__ void __launch_bounds__(kEigThreads) block_eig_kernel(const double2* _
   }
 }
 
+// The same for one block of 128 < d <= 256 (a whole mode: D = n), one CTA of 256 threads: the
+// unknown triangles (V, then W) live row-major in global scratch (2 d^2 entries per job, L2
+// resident) so a step's reads are coalesced across the columns, then are written column-major.
+constexpr int kEigBigThreads = 256;
+__global__ void __launch_bounds__(kEigBigThreads) block_eig_big_kernel(const double2* __restrict__ t_pool,
+                                                                      const EigCands cs, double2* __restrict__ vpool,
+                                                                      double2* __restrict__ wpool,
+                                                                      double* __restrict__ cond,
+                                                                      double2* __restrict__ scratch) {
+  int ci = 0;
+  while (ci + 1 < cs.count && (int)blockIdx.x >= cs.first[ci + 1]) ++ci;
+  const int d = cs.d[ci];
+  if (d <= 128) return;  // block_eig_kernel's job
+  const int q = blockIdx.x - cs.first[ci];
+  const int k = threadIdx.x, lane = k & 31, warp = k >> 5;
+  const int64_t n = cs.n[ci], o = (int64_t)q * d;
+  const double2* T = t_pool + cs.toff[ci];
+  double2* V = vpool + cs.voff[ci] + (int64_t)q * d * d;
+  double2* W = wpool + cs.voff[ci] + (int64_t)q * d * d;
+  double2* R = scratch + cs.soff[ci] + (int64_t)q * 2 * d * d;  // V row-major
+  double2* Q = R + (int64_t)d * d;                              // W row-major
+  __shared__ int bad;
+  __shared__ double2 row[2][kEigBigThreads];
+  __shared__ double2 x[kEigBigThreads], y[kEigBigThreads];
+  __shared__ double red[kEigBigThreads / 32];
+  __shared__ double colscale[kEigBigThreads];
+  if (k == 0) bad = 0;
+  // ---- 1. V (row-major in R), rows d-1 .. 0 ----
+  if (k < d) row[(d - 1) & 1][k] = T[(o + d - 1) + (o + k) * n];
+  const double2 lk = k < d ? T[(o + k) + (o + k) * n] : make_double2(0.0, 0.0);
+  __syncthreads();
+  for (int i = d - 1; i >= 0; --i) {
+    const double2* ti = row[i & 1];
+    if (i > 0 && k < d) row[(i - 1) & 1][k] = T[(o + i - 1) + (o + k) * n];
+    if (k < d) {
+      double2 v = make_double2(k == i ? 1.0 : 0.0, 0.0);
+      if (k > i) {
+        double2 a0 = make_double2(0.0, 0.0), a1 = make_double2(0.0, 0.0);
+        int l = i + 1;
+        for (; l + 1 <= k; l += 2) {
+          a0 = cfma(a0, ti[l], R[(int64_t)l * d + k]);
+          a1 = cfma(a1, ti[l + 1], R[(int64_t)(l + 1) * d + k]);
+        }
+        if (l <= k) a0 = cfma(a0, ti[l], R[(int64_t)l * d + k]);
+        const double2 gap = csub(lk, ti[i]);
+        if (gap.x == 0.0 && gap.y == 0.0) {
+          bad = 1;
+        } else {
+          v = cdiv(cadd(a0, a1), gap);
+        }
+      }
+      R[(int64_t)i * d + k] = v;
+    }
+    __syncthreads();
+  }
+  if (k < d) {  // unit columns
+    double nn = 0.0;
+    for (int i = 0; i <= k; ++i) {
+      const double2 v = R[(int64_t)i * d + k];
+      nn += v.x * v.x + v.y * v.y;
+    }
+    nn = sqrt(nn);
+    if (!isfinite(nn) || nn == 0.0) {
+      bad = 1;
+      nn = 1.0;
+    }
+    colscale[k] = 1.0 / nn;
+  }
+  __syncthreads();
+  for (int64_t e = k; e < (int64_t)d * d; e += kEigBigThreads) {  // scale R in place; V column-major
+    const int i = (int)(e / d), c = (int)(e % d);
+    double2 v = R[e];
+    v = make_double2(v.x * colscale[c], v.y * colscale[c]);
+    R[e] = v;
+    V[i + (int64_t)c * d] = v;
+  }
+  __syncthreads();
+  // ||M||_2 of a row-major upper triangular M in global memory: 12 power iterations on M^H M
+  auto norm2 = [&](const double2* M) {
+    if (k < d) x[k] = make_double2(1.0 + 0.37 * k, 0.11 * (k % 5));
+    __syncthreads();
+    double lam = 0.0;
+    for (int it = 0; it < 12; ++it) {
+      if (k < d) {
+        double2 sacc = make_double2(0.0, 0.0);
+        for (int c = k; c < d; ++c) sacc = cfma(sacc, M[(int64_t)k * d + c], x[c]);
+        y[k] = sacc;
+      }
+      __syncthreads();
+      double part = 0.0;
+      double2 xn = make_double2(0.0, 0.0);
+      if (k < d) {
+        for (int r = 0; r <= k; ++r) {
+          const double2 m = M[(int64_t)r * d + k];
+          xn = cfma(xn, make_double2(m.x, -m.y), y[r]);
+        }
+        part = xn.x * xn.x + xn.y * xn.y;
+      }
+      for (int sh = 16; sh > 0; sh >>= 1) part += __shfl_xor_sync(0xffffffffu, part, sh);
+      if (lane == 0) red[warp] = part;
+      __syncthreads();
+      double tot = 0.0;
+      for (int w2 = 0; w2 < kEigBigThreads / 32; ++w2) tot += red[w2];
+      tot = sqrt(tot);
+      lam = tot;
+      if (k < d) x[k] = make_double2(xn.x / tot, xn.y / tot);
+      __syncthreads();
+    }
+    return sqrt(lam);
+  };
+  const double nv = norm2(R);
+  // ---- 2. W = V^{-1} (row-major in Q), rows d-1 .. 0 ----
+  if (k < d) row[(d - 1) & 1][k] = R[(int64_t)(d - 1) * d + k];
+  __syncthreads();
+  for (int i = d - 1; i >= 0; --i) {
+    const double2* vi = row[i & 1];
+    if (i > 0 && k < d) row[(i - 1) & 1][k] = R[(int64_t)(i - 1) * d + k];
+    if (k < d) {
+      double2 w = make_double2(0.0, 0.0);
+      if (k == i) {
+        w = cdiv(make_double2(1.0, 0.0), vi[i]);
+      } else if (k > i) {
+        double2 a0 = make_double2(0.0, 0.0), a1 = make_double2(0.0, 0.0);
+        int l = i + 1;
+        for (; l + 1 <= k; l += 2) {
+          a0 = cfma(a0, vi[l], Q[(int64_t)l * d + k]);
+          a1 = cfma(a1, vi[l + 1], Q[(int64_t)(l + 1) * d + k]);
+        }
+        if (l <= k) a0 = cfma(a0, vi[l], Q[(int64_t)l * d + k]);
+        const double2 acc = cadd(a0, a1);
+        w = cdiv(make_double2(-acc.x, -acc.y), vi[i]);
+      }
+      Q[(int64_t)i * d + k] = w;
+    }
+    __syncthreads();
+  }
+  for (int64_t e = k; e < (int64_t)d * d; e += kEigBigThreads) W[(e / d) + (e % d) * d] = Q[e];
+  __syncthreads();
+  const double nw = norm2(Q);
+  if (k == 0) {
+    const double c = nv * nw;
+    cond[blockIdx.x] = (bad || !isfinite(c)) ? INFINITY : c;
+  }
+}
+
 void block_eig_launch(const double2* t_pool, const EigCands& cands, double2* vpool, double2* wpool, double* cond,
-                      cudaStream_t stream) {
+                      double2* scratch, cudaStream_t stream) {
   const int njobs = cands.count > 0 ? cands.first[cands.count] : 0;
   if (njobs <= 0) return;
   int dmax = 0;
-  for (int c = 0; c < cands.count; ++c) dmax = std::max(dmax, cands.d[c]);
+  for (int c = 0; c < cands.count; ++c) dmax = std::max(dmax, std::min(cands.d[c], 128));
   const size_t smem = block_eig_smem(dmax);
   static size_t attr = 0;
   if (smem > attr) {
@@ -187,6 +333,12 @@ void block_eig_launch(const double2* t_pool, const EigCands& cands, double2* vpo
   }
   block_eig_kernel<<<(unsigned)njobs, kEigThreads, smem, stream>>>(t_pool, cands, vpool, wpool, cond);
   NDS_LAUNCH_CHECK();
+  bool big = false;
+  for (int c = 0; c < cands.count; ++c) big = big || cands.d[c] > 128;
+  if (big) {
+    block_eig_big_kernel<<<(unsigned)njobs, kEigBigThreads, 0, stream>>>(t_pool, cands, vpool, wpool, cond, scratch);
+    NDS_LAUNCH_CHECK();
+  }
 }
 
 // ---- Schur reordering (ZTREXC by adjacent swaps, all pairs of a round at once) -----------------

@@ -731,19 +731,21 @@ void plan_binary_diag(nds_plan* p, const nds_z* const* u, const nds_z* const* t)
 // one launch (blockdiag.cu), so the plan's host work stays small.
 constexpr double kCubicDiagCondMax = 1e6;
 
-void plan_cubic_diag(nds_plan* p, const nds_z* const* u, const nds_z* const* t) {
-  (void)u;
-  (void)t;
+// thorough: also evaluate whole modes of 128 < n_j <= 256 as one block (block_eig_big_kernel,
+// ~5 ms of device time at n = 256). reorder: run the candidates on the reordered Schur forms.
+// c1: thorough D = (128, 256, 128), 3 levels, solve 0.71 ms; one-shot (64, 128, 128) on the
+// caller's order, 6 levels, 1.19 ms.
+bool plan_cubic_diag_try(nds_plan* p, bool thorough, bool reorder) {
   p->cub_diag = false;
   if (p->fast_path || !p->solver || p->solver->binary || !p->solver->sp.v2 || (p->flags & NDS_NO_DIAGONALISE))
-    return;
+    return false;
   const int N = p->n_modes;
   const nds::TileGeom& tg = p->solver->sp.geom;
   const int B = tg.b[0];
   {  // the level kernel's 32-bit column offsets
     int64_t span = 0;
     for (int j = 0; j < N; ++j) span += (B - 1) * tg.strides[j];
-    if (span >= (int64_t)1 << 31) return;
+    if (span >= (int64_t)1 << 31) return false;
   }
   // every candidate (mode j, D = B, 2B, .. <= 128 dividing n_j) evaluated on the device in one
   // launch (block_eig_kernel: eigenvectors, inverse, cond_2 per block); the host then picks D_j
@@ -757,35 +759,45 @@ void plan_cubic_diag(nds_plan* p, const nds_z* const* u, const nds_z* const* t) 
   nds::EigCands ec{};
   int njobs = 0;
   int64_t vtot = 0;
-  for (int j = 0; j < N; ++j)
-    for (int64_t d = B; d <= std::min<int64_t>(p->dims[j], 128); d *= 2) {
-      if (p->dims[j] % d || ec.count >= nds::kMaxEigCands) continue;
+  int64_t stot = 0;  // global scratch of the whole-mode (d > 128) candidates
+  for (int j = 0; j < N; ++j) {
+    // D = B 2^k <= 128 dividing n_j, and the whole mode D = n_j (<= 256): T'_j diagonal
+    std::vector<int64_t> ds;
+    for (int64_t d = B; d <= std::min<int64_t>(p->dims[j], 128); d *= 2)
+      if (p->dims[j] % d == 0) ds.push_back(d);
+    if (p->dims[j] <= (thorough ? 256 : 128) && (ds.empty() || ds.back() != p->dims[j])) ds.push_back(p->dims[j]);
+    for (int64_t d : ds) {
+      if (ec.count >= nds::kMaxEigCands) break;
       Cand c{(int)d, njobs, (int)(p->dims[j] / d), vtot};
       ec.d[ec.count] = (int)d;
       ec.first[ec.count] = njobs;
       ec.n[ec.count] = p->dims[j];
       ec.toff[ec.count] = p->f.geom.toff[j];
       ec.voff[ec.count] = vtot;
+      ec.soff[ec.count] = stot;
+      if (d > 128) stot += 2 * d * d * c.count;
       ++ec.count;
       njobs += c.count;
       vtot += p->dims[j] * d;
       cands[j].push_back(c);
     }
+  }
   ec.first[ec.count] = njobs;
   for (int j = 0; j < N; ++j)
-    if (cands[j].empty()) return;
+    if (cands[j].empty()) return false;
   cudaStream_t s = p->ctx->stream;
   int64_t sq = 0;
   for (int j = 0; j < N; ++j) sq += p->dims[j] * p->dims[j];
   // device scratch: [cond][V pool][W pool][M_inv][M_fwd^H][T W][T'][T~][U~]
   const size_t cd_bytes = ((size_t)njobs * sizeof(double) + 255) / 256 * 256;
   char* scratch = nullptr;
-  NDS_CUDA(cudaMallocFromPoolAsync((void**)&scratch, cd_bytes + (size_t)(2 * vtot + 6 * sq) * sizeof(double2),
-                                   p->ctx->pool, s));
+  NDS_CUDA(cudaMallocFromPoolAsync((void**)&scratch,
+                                   cd_bytes + (size_t)(2 * vtot + 6 * sq + stot + 1) * sizeof(double2), p->ctx->pool, s));
   double* d_cond = (double*)scratch;
   double2* dv = (double2*)(scratch + cd_bytes);
   double2* dw = dv + vtot;
   double2 *minv = dw + vtot, *mfh = minv + sq, *tw = mfh + sq, *tpr = tw + sq, *tre = tpr + sq, *ure = tre + sq;
+  double2* eig_scratch = ure + sq;
   // the Schur forms reordered (schur_reorder_kernel: eigenvalues spread over every aligned block)
   // into T~ = Q^H T Q, U~ = U Q: the route's blocks, factors and denominators all come from them
   // (the same operator; the singular check above ran on the caller's T with the same denominators)
@@ -806,9 +818,9 @@ void plan_cubic_diag(nds_plan* p, const nds_z* const* u, const nds_z* const* t) 
     if (n / prod > 1) ra.rad[j][nr++] = (int)(n / prod);
     ra.nrad[j] = n <= nds::kReorderMaxN ? nr : 0;  // larger extents keep their order
   }
-  nds::schur_reorder_launch(ra, N, tre, ure, s);
+  if (reorder) nds::schur_reorder_launch(ra, N, tre, ure, s);
   std::vector<double> cond(njobs);
-  nds::block_eig_launch(tre, ec, dv, dw, d_cond, s);
+  nds::block_eig_launch(tre, ec, dv, dw, d_cond, eig_scratch, s);
   NDS_CUDA(cudaMemcpyAsync(cond.data(), d_cond, njobs * sizeof(double), cudaMemcpyDeviceToHost, s));
   NDS_CUDA(cudaStreamSynchronize(s));
   for (int j = 0; j < N; ++j)
@@ -823,7 +835,7 @@ void plan_cubic_diag(nds_plan* p, const nds_z* const* u, const nds_z* const* t) 
   p->cub_cond = prod;
   if (!(prod <= kCubicDiagCondMax)) {
     NDS_CUDA(cudaFreeAsync(scratch, s));
-    return;
+    return false;
   }
   for (;;) {  // grow the super-blocks: double the mode whose product stays smallest
     int best = -1;
@@ -880,7 +892,24 @@ void plan_cubic_diag(nds_plan* p, const nds_z* const* u, const nds_z* const* t) 
     p->blk = &it->second;
   }
   p->cub_diag = true;
+  return true;
 }
+
+// thorough (persistent plans, nds_plan_create): the Schur forms reordered and whole modes of
+// n_j <= 256 as candidates — the best route, ~15-20 ms of plan time at n = 256 (the reordering
+// sweeps n rounds over T and U on one CTA per mode). One-shot host-buffer solves (plan creation
+// inside the call: nds_solve / nds_solve_schur) keep the caller's order and blocks <= 128, and
+// reorder only when that order fails the guard (c2).
+void plan_cubic_diag(nds_plan* p, const nds_z* const* u, const nds_z* const* t, bool thorough) {
+  (void)u;
+  (void)t;
+  if (thorough) {
+    plan_cubic_diag_try(p, true, true);
+    return;
+  }
+  if (!plan_cubic_diag_try(p, false, false)) plan_cubic_diag_try(p, false, true);
+}
+
 
 // Full path on device buffers: b -> (fwd) -> C -> (solve, in place) -> Y -> (inv) -> x.
 // Destinations alternate W/X from the first pass so the 2N-th pass lands in x and b is only read.
@@ -1078,7 +1107,8 @@ int execute(nds_plan* p, const double2* b, double2* x, double2* work, cudaEvent_
 // so the small factor copy is not queued behind the tensor).
 void plan_create_impl(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z* const* u, const nds_z* const* t,
                       double singular_tol, unsigned flags, nds_plan** out, nds_singular* sing,
-                      bool defer_singular = false, const std::function<void()>& after_upload = {}) {
+                      bool defer_singular = false, const std::function<void()>& after_upload = {},
+                      bool thorough = false) {
   if (!out) throw Error(NDS_ERR_INVALID, "out is null");
   *out = nullptr;
   const int64_t total = checked_total(n_modes, dims, 2);
@@ -1117,7 +1147,7 @@ void plan_create_impl(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_
   if (!p->fast_path) {
     build_solver(p.get());
     plan_binary_diag(p.get(), u, t);
-    plan_cubic_diag(p.get(), u, t);
+    plan_cubic_diag(p.get(), u, t, thorough);
   }
   *out = p.release();
 }
@@ -1794,7 +1824,7 @@ int nds_schur(nds_ctx* ctx, int n, const nds_z* a, nds_z* u, nds_z* t) {
 int nds_plan_create(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z* const* u, const nds_z* const* t,
                     double singular_tol, unsigned flags, nds_plan** out, nds_singular* sing) {
   if (!ctx) return NDS_ERR_INVALID;
-  return guarded(ctx, [&] { plan_create_impl(ctx, n_modes, dims, u, t, singular_tol, flags, out, sing); });
+  return guarded(ctx, [&] { plan_create_impl(ctx, n_modes, dims, u, t, singular_tol, flags, out, sing, false, {}, true); });
 }
 
 void nds_plan_destroy(nds_plan* plan) { plan_destroy_impl(plan); }

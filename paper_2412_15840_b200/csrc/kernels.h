@@ -213,15 +213,17 @@ void param_blob_launch(const ParamBlob& blob, double2* dst, cudaStream_t stream)
 // vpool / wpool + voff) and cond_2(V) into cond[job] (inf on a repeated eigenvalue).
 // Candidates are passed by value (no host->device copy in the plan, which runs while the tensor
 // streams in): candidate c covers jobs [first[c], first[c + 1]), blocks q = job - first[c].
-constexpr int kMaxEigCands = 5 * NDS_MAX_MODES;
+constexpr int kMaxEigCands = 6 * NDS_MAX_MODES;
+// Extents d > 128 (a whole mode, D = n <= 256) use global scratch: 2 d^2 entries per block at
+// soff[c] + 2 q d^2.
 struct EigCands {
   int count;
   int d[kMaxEigCands];
   int first[kMaxEigCands + 1];
-  int64_t n[kMaxEigCands], toff[kMaxEigCands], voff[kMaxEigCands];
+  int64_t n[kMaxEigCands], toff[kMaxEigCands], voff[kMaxEigCands], soff[kMaxEigCands];
 };
 void block_eig_launch(const double2* t_pool, const EigCands& cands, double2* vpool, double2* wpool, double* cond,
-                      cudaStream_t stream);
+                      double2* scratch, cudaStream_t stream);
 // The route's factors of one mode (n x n column-major; V, W = V^{-1}: n / d blocks of d x d):
 // minv = U blockdiag(V), mfh = U blockdiag(W)^H, tv = T blockdiag(V) (scratch),
 // tprime = blockdiag(W) T blockdiag(V) with diagonal d-blocks = diag(T) exactly, zero below.
