@@ -18,14 +18,21 @@
 // (c1 with D = 64: 10, against 46 tile hyperplanes of the wavefront route).
 
 struct BlkArgs {
-  TileGeom g;
-  int d[NDS_MAX_MODES];  // diagonalisation block (super-block) extent per mode
+  TileGeom g;            // the COUPLED modes' geometry (modes with D_j < n_j)
+  int d[NDS_MAX_MODES];  // diagonalisation block (super-block) extent per coupled mode
+  // Uncoupled modes (D_j = n_j: T'_j diagonal) are a batch: tile id = coupled tile + ntc * batch
+  // index; the batch index adds boff[b] to the tile origin and bden[b] (their diagonal terms) to
+  // every denominator. boff = null: no batch.
+  const int64_t* boff;
+  const double2* bden;
+  int64_t ntc;
 };
+constexpr int ilog2c(int x) { return x <= 1 ? 0 : 1 + ilog2c(x / 2); }
 
 template <int N, int B, int BK, int ST, int NT>
 struct BlkCfg {
   static constexpr int E = 4096;
-  static constexpr int LB = B == 16 ? 4 : 3;
+  static constexpr int LB = ilog2c(B);
   static constexpr int TC = E / B;        // columns of every mode's GEMM
   static constexpr int NW = NT / 32;
   static constexpr int CB = TC / 8 / NW;  // column fragments per warp
@@ -48,7 +55,7 @@ __global__ void __launch_bounds__(NT, MINB)
   constexpr int kBlkThreads = NT;
   constexpr int E = C::E, LB = C::LB, TC = C::TC, CB = C::CB, RB = C::RB, LDB = C::LDB, ALD = C::ALD;
   constexpr int SL = C::SL;
-  static_assert(C::SL * kBlkThreads == BK * TC && B * BK <= kBlkThreads && BK % 4 == 0, "stage shape");
+  static_assert(C::SL * kBlkThreads == BK * TC && BK % 4 == 0 && (1 << (LB * N)) == E, "stage shape");
   extern __shared__ __align__(16) double2 smem[];
   double2* sS = smem;                          // the tile (local index l = sum_m l_m B^m)
   double2* sB = sS + E;                        // [ST][BSTAGE]
@@ -60,8 +67,13 @@ __global__ void __launch_bounds__(NT, MINB)
   __shared__ double2 dd[N][B];
   const TileGeom& g = ba.g;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int64_t tile_id = tiles[blockIdx.x], tb = 0;
+  if (ba.boff) {
+    tb = tile_id / ba.ntc;
+    tile_id -= tb * ba.ntc;
+  }
   if (tid < N) {
-    int64_t t = tiles[blockIdx.x];
+    int64_t t = tile_id;
     for (int m = 0; m < N; ++m) {
       const int64_t I = t % g.nb[m];
       t /= g.nb[m];
@@ -95,7 +107,8 @@ __global__ void __launch_bounds__(NT, MINB)
   }
   __syncthreads();
   if (tid < N * B) dd[tid / B][tid % B] = T[g.toff[tid / B] + (so[tid / B] + tid % B) * (g.dims[tid / B] + 1)];
-  int64_t base = 0;  // tile origin
+  int64_t base = ba.boff ? ba.boff[tb] : 0;  // tile origin
+  const double2 dext = ba.boff ? ba.bden[tb] : make_double2(0.0, 0.0);
 #pragma unroll
   for (int m = 0; m < N; ++m) base += so[m] * g.strides[m];
   int nkt = 0;
@@ -158,8 +171,8 @@ __global__ void __launch_bounds__(NT, MINB)
     double2* dB = sB + stage * C::BSTAGE;
 #pragma unroll
     for (int i = 0; i < SL; ++i) cp_async16_bs(dB + p_soff[i], src + p_gofs[i]);
-    if (tid < B * BK) {  // T'_j(so_j + r, k0 + k), rows fastest (column-major T: coalesced)
-      const int r = tid % B, k = tid / B;
+    for (int e = tid; e < B * BK; e += kBlkThreads) {  // T'_j(so_j + r, k0 + k), rows fastest (coalesced)
+      const int r = e % B, k = e / B;
       cp_async16_bs(sA + stage * C::ASTAGE + r * ALD + k,
                     T + g.toff[j] + (so[j] + r) + (int64_t)(k0 + k) * g.dims[j]);
     }
@@ -282,7 +295,7 @@ __global__ void __launch_bounds__(NT, MINB)
 #pragma unroll
   for (int i = 0; i < PER; ++i) {
     const int l = tid + i * kBlkThreads;
-    double2 den = dd[0][l & (B - 1)];
+    double2 den = cadd(dext, dd[0][l & (B - 1)]);
     int64_t o = l & (B - 1);
 #pragma unroll
     for (int m = 1; m < N; ++m) {

@@ -95,6 +95,7 @@ struct nds_plan {
   double cub_cond = 0.0, bin_cond = 0.0;  // prod_j max_q cond_2(V_{j,q}) of the route's guard
   nds::FactorSet cd_inv, cd_fwd, fc;
   const nds::BlkSolvePlan* blk = nullptr;  // super-tile levels of the route (owned by the solver cache)
+  double2* blk_bden = nullptr;             // its batch denominators (uncoupled modes), per plan
   int launches = 0;
   // per-launch CUDA-event profile (nds_plan_profile_begin / _end)
   bool profiling = false;
@@ -560,7 +561,7 @@ int launch_solver(nds_plan* p, double2* c, cudaStream_t s, nds::Recorder* rec, b
   if (p->solver->binary)
     return nds::binary_solve_launch(p->solver->bsp, merged && p->bin_diag ? p->bin_t : p->f.t_pool, c, s, rec,
                                     merged && p->bin_diag);
-  if (merged && p->cub_diag) return nds::blk_backsub_launch(p->solver->sp, *p->blk, p->fc.t_pool, c, s, rec);
+  if (merged && p->cub_diag) return nds::blk_backsub_launch(*p->blk, p->fc.t_pool, p->blk_bden, c, s, rec);
   return nds::backsub_launch(p->solver->sp, p->f.t_pool, c, s, rec);
 }
 
@@ -887,9 +888,14 @@ bool plan_cubic_diag_try(nds_plan* p, bool thorough, bool reorder) {
     auto it = p->solver->blk.find(key);
     if (it == p->solver->blk.end()) {
       it = p->solver->blk.emplace(key, nds::BlkSolvePlan{}).first;
-      nds::blk_solve_plan_build(it->second, p->solver->sp, d);
+      nds::blk_solve_plan_build(it->second, N, p->dims, p->f.geom.toff, d, B);
     }
     p->blk = &it->second;
+    if (p->blk->nbatch > 1) {  // this plan's batch denominators (the diagonal of its T')
+      NDS_CUDA(cudaMallocFromPoolAsync((void**)&p->blk_bden, (size_t)p->blk->nbatch * sizeof(double2), p->ctx->pool,
+                                       p->ctx->stream));
+      nds::blk_batch_den_launch(*p->blk, p->fc.geom, p->fc.diag_pool, p->blk_bden, p->ctx->stream);
+    }
   }
   p->cub_diag = true;
   return true;
@@ -1159,6 +1165,7 @@ void plan_destroy_impl(nds_plan* p) {
   free_factors(p->f);
   free_factors(p->cd_inv);
   free_factors(p->cd_fwd);
+  if (p->blk_bden) cudaFreeAsync(p->blk_bden, p->ctx->stream);
   if (p->fd_buf) cudaFreeAsync(p->fd_buf, p->ctx->stream);
   delete p;  // the shared solver structures stay cached in the context
 }
@@ -1904,7 +1911,7 @@ int nds_plan_superblocks(const nds_plan* plan, int64_t* d) {
   if (!plan) return -1;
   if (!plan->cub_diag) return 0;
   if (d)
-    for (int j = 0; j < plan->n_modes; ++j) d[j] = plan->blk->d[j];
+    for (int j = 0; j < plan->n_modes; ++j) d[j] = plan->blk->dmode[j];
   return plan->blk->levels;
 }
 

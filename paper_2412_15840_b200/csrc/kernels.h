@@ -162,13 +162,24 @@ int binary_solve_launch(const BinarySolvePlan& bp, const double2* t_pool, double
                         Recorder* rec = nullptr, bool decoupled = false);
 
 // Block-diagonalised cubic route (backsub_blk.cuh): super-blocks of d[j] rows per mode (multiples
-// of the tile edge), the cubic tiles grouped by super-tile level sum_j floor(I_j b / d_j)
-// (highest first; within a level longest pull first), one launch per level.
+// of the tile edge); the coupled modes (d < n) tiled 64^2 / 16^3 / 8^4 by their count, the
+// uncoupled ones a batch (or every mode tiled when no kernel fits); tiles grouped by super-tile
+// level sum_j floor(I_j b / d_j) (highest first; within a level longest pull first), one launch
+// per level.
 struct BlkSolvePlan {
-  int d[NDS_MAX_MODES] = {};
+  int d[NDS_MAX_MODES] = {};      // per tiled mode
+  int dmode[NDS_MAX_MODES] = {};  // per mode of the problem
+  TileGeom g{};               // the tiled modes: the coupled ones (the rest a batch), or all
   int levels = 0;
+  int64_t ntc = 1, nbatch = 1;
+  std::vector<int> uncoupled;  // batch modes (empty: none folded)
   std::vector<int64_t> level_off;
   int64_t* d_tiles = nullptr;
+  int64_t* d_boff = nullptr;  // batch origin offsets (inside d_tiles' allocation), or null
+};
+struct BlkBatchModes {
+  int count;
+  int mode[NDS_MAX_MODES];
 };
 // Dims-only solver structures (tile lists, work items, partial buffers, internal streams), cached
 // per context and shared by every plan with the same extents; the block-diagonalised route's
@@ -182,9 +193,13 @@ struct SolverCache {
   ~SolverCache();
 };
 
-void blk_solve_plan_build(BlkSolvePlan& bp, const SolvePlan& sp, const int* d);
+void blk_solve_plan_build(BlkSolvePlan& bp, int n_modes, const int64_t* dims, const int64_t* toff, const int* d,
+                          int b);
+// Per plan: the batch denominators sum_{uncoupled j} T'_j(i_j, i_j) (diag of the route's T').
+void blk_batch_den_launch(const BlkSolvePlan& bp, const Geom& g, const double2* diag, double2* out,
+                          cudaStream_t stream);
 void blk_solve_plan_free(BlkSolvePlan& bp);
-int blk_backsub_launch(const SolvePlan& sp, const BlkSolvePlan& bp, const double2* t_pool, double2* c,
+int blk_backsub_launch(const BlkSolvePlan& bp, const double2* t_pool, const double2* bden, double2* c,
                        cudaStream_t stream, Recorder* rec = nullptr);
 // Schur reordering of the block-diagonalised route (blockdiag.cu): per mode, T_j and U_j (n x n
 // column-major at off[m] in the two pools, in place) reordered so the eigenvalue of real-part rank
