@@ -416,3 +416,61 @@ def test_binary_diagonalised_inner_modes(ctx, ref, n_modes, seed):
     torch.cuda.synchronize()
     ctx.set_stream(None)
     assert rel_max(d_x.cpu().numpy().reshape(b.shape, order="F"), x_ref) <= 1e-12
+
+
+def _spectrum_factors(rng, dims, kind):
+    """Unitary U and upper-triangular T whose eigenvalues (the diagonal) follow `kind`:
+    'spread' (disk of radius 1 around 2), 'clustered' (most of them within 1e-3 of each other),
+    'real' (real, graded like a discretised diffusion operator), with O(1/sqrt(n)) coupling."""
+    us, ts = [], []
+    for n in dims:
+        q, _ = np.linalg.qr(rand_c(rng, (n, n)))
+        t = np.triu(rand_c(rng, (n, n))) / np.sqrt(n)
+        if kind == "spread":
+            lam = 2.0 + rng.uniform(0, 1, n) ** 0.5 * np.exp(2j * np.pi * rng.uniform(0, 1, n))
+        elif kind == "clustered":
+            lam = 2.0 + 1e-3 * (rng.standard_normal(n) + 1j * rng.standard_normal(n))
+            lam[: n // 4] += rng.uniform(0.5, 1.5, n // 4)
+        else:
+            lam = 0.25 + np.sort(rng.uniform(0, 1, n)) ** 2 + 0j
+        t[np.diag_indices(n)] = lam
+        us.append(np.asfortranarray(q))
+        ts.append(np.asfortranarray(t))
+    return us, ts
+
+
+ROUTE_CASES = [((48, 48, 48), "spread"), ((64, 32, 48), "spread"), ((32, 32, 32, 32), "spread"),
+               ((48, 48, 48), "clustered"), ((32, 32, 32, 32), "clustered"), ((64, 64, 64), "real"),
+               ((32, 48, 32, 16), "real"), ((96, 32, 32), "spread")]
+
+
+@pytest.mark.parametrize("dims,kind", ROUTE_CASES, ids=[f"{k}-{'x'.join(map(str, d))}" for d, k in ROUTE_CASES])
+def test_diagonalised_route_guard_random_spectra(ctx, port, dims, kind):
+    """The guard on random spectra: whenever the plan takes the block-diagonalised route its bound
+    is <= 1e6 and X matches the oracle at the north_star tolerance; clustered spectra (no
+    well-conditioned eigenvector basis for the blocks) must either be refused (wavefront route)
+    or still land within tolerance. Both routes of the same plan are checked."""
+    import torch
+    import zlib
+    rng = np.random.default_rng(zlib.crc32(f"{kind}{dims}".encode()))
+    us, ts = _spectrum_factors(rng, dims, kind)
+    b = rand_c(rng, dims)
+    x_ref, _ = port.solve_schur(us, ts, b, flags=0)
+    d_b = torch.from_numpy(np.ascontiguousarray(b.ravel(order="F"))).cuda()
+    ctx.set_stream(torch.cuda.current_stream().cuda_stream)
+    for diag in (True, False):
+        plan = ctx.plan(us, ts, allow_fast_path=False, diagonalise=diag)
+        taken, cond = plan.diagonalised()
+        d_x, d_w = torch.empty_like(d_b), torch.empty_like(d_b)
+        plan.execute(d_b.data_ptr(), d_x.data_ptr(), d_w.data_ptr())
+        torch.cuda.synchronize()
+        err = rel_max(d_x.cpu().numpy().reshape(dims, order="F"), x_ref)
+        if taken:
+            assert cond <= 1e6
+            assert err <= 1e-9, (kind, dims, cond, err)
+        else:
+            assert err <= 1e-11, (kind, dims, err)
+        plan.close()
+    ctx.set_stream(None)
+    r = ctx.solve_schur(us, ts, b, allow_fast_path=False)  # one-shot route choice
+    assert rel_max(r.x, x_ref) <= 1e-9

@@ -20,12 +20,13 @@ NCU="ncu --set full --clock-control none --import-source on"
 P="python tools/profile_step.py --reps 1"
 timeout 400 $NCU -k regex:zgemm_tma -s 1 -c 1 -o $O/zgemm_tma_c1 $P --config c1 > /dev/null 2>&1
 timeout 400 $NCU -k regex:zgemm_dmma -s 0 -c 1 -o $O/zgemm_dmma_c1 $P --config c1 > /dev/null 2>&1
-# blk_level_kernel: c1 has 6 levels per solve (2 warm-up solves + 1): -s 15 = level 3 of the last
-timeout 400 $NCU -k regex:blk_level -s 15 -c 1 -o $O/blk_c1_l3 $P --config c1 > /dev/null 2>&1
-# c3: 20 levels per solve: level 10 of the last solve
-timeout 600 $NCU -k regex:blk_level -s 50 -c 1 -o $O/blk_c3_l10 $P --config c3 > /dev/null 2>&1
+# blk_level_kernel: c1 has 3 levels per solve (2 warm-up solves + 1): -s 7 = level 1 of the last
+timeout 400 $NCU -k regex:blk_level -s 7 -c 1 -o $O/blk_c1_l1 $P --config c1 > /dev/null 2>&1
+# c3: 4 levels per solve: level 1 of the last solve; c2: 12 levels: level 5 of the last
+timeout 600 $NCU -k regex:blk_level -s 9 -c 1 -o $O/blk_c3_l1 $P --config c3 > /dev/null 2>&1
+timeout 600 $NCU -k regex:blk_level -s 29 -c 1 -o $O/blk_c2_l5 $P --config c2 > /dev/null 2>&1
+timeout 400 $NCU -k regex:schur_reorder -c 1 -o $O/schur_reorder_c1 python tools/gpu/plan_timing.py c1 > /dev/null 2>&1
 timeout 400 $NCU -k regex:block_eig -c 1 -o $O/block_eig_c1 python tools/gpu/plan_timing.py c1 > /dev/null 2>&1
 timeout 600 $NCU -k regex:binary_pass -s 1 -c 1 -o $O/binary_pass_c4 $P --config c4 > /dev/null 2>&1
 timeout 600 $NCU -k regex:binary_fused -s 1 -c 1 -o $O/binary_fused_c4 $P --config c4 > /dev/null 2>&1
-timeout 600 $NCU -k regex:tile_diag_lines -s 22 -c 1 -o $O/lines_c2_mid $P --config c2 > /dev/null 2>&1
 echo done > $O/done
