@@ -342,17 +342,10 @@ void solve_plan_free(SolvePlan& sp) {
 
 int backsub_launch(const SolvePlan& sp, const double2* t_pool, double2* c, cudaStream_t stream, Recorder* rec,
                    const HeadSync* head, const TailHook* tail) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    NDS_CUDA(cudaFuncSetAttribute(tile_level_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)(kMaxTile * sizeof(double2))));
-    for (int b : {8, 16})
-      NDS_CUDA(cudaFuncSetAttribute(far_group_cfg(b).kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)far_group_smem_bytes(b)));
-    NDS_CUDA(cudaFuncSetAttribute(lines_kernel_for(3, 16), cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024));
-    NDS_CUDA(cudaFuncSetAttribute(lines_kernel_for(4, 8), cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024));
-    attr_set = true;
-  }
+  smem_optin(tile_level_kernel, kMaxTile * sizeof(double2));
+  for (int b : {8, 16}) smem_optin(far_group_cfg(b).kern, far_group_smem_bytes(b));
+  smem_optin(lines_kernel_for(3, 16), 112 * 1024);
+  smem_optin(lines_kernel_for(4, 8), 112 * 1024);
   const TileGeom& g = sp.geom;
   int launches = 0;
   if (!sp.v2) {
@@ -604,14 +597,7 @@ int blk_backsub_launch(const BlkSolvePlan& bp, const double2* t_pool, const doub
   const TileGeom& g = bp.g;
   const BlkLaunchT bl = blk_cfg(g.n_modes, g.b[0]);
   if (!bl.kern) throw Error(NDS_ERR_OTHER, "block-diagonalised solve: no level kernel for this tile geometry");
-  static bool attr_set = false;
-  if (!attr_set) {
-    for (int nm : {3, 4}) {
-      const BlkLaunchT x = blk_cfg(nm, nm == 3 ? 16 : 8);
-      NDS_CUDA(cudaFuncSetAttribute(x.kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)x.smem));
-    }
-    attr_set = true;
-  }
+  smem_optin(bl.kern, bl.smem);
   BlkArgs ba;
   ba.g = g;
   for (int j = 0; j < NDS_MAX_MODES; ++j) ba.d[j] = j < g.n_modes ? bp.d[j] : 1;

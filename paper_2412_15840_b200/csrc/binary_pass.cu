@@ -304,11 +304,7 @@ static BinPass make_bin_pass(const FactorSet& f, const BinGroup& gr, bool adjoin
 int binary_pass_launch(const FactorSet& f, const BinGroup& gr, bool adjoint, const double2* x, double2* r,
                        cudaStream_t stream) {
   const BinPass bp = make_bin_pass(f, gr, adjoint);
-  static bool attr_set = false;
-  if (!attr_set) {
-    NDS_CUDA(cudaFuncSetAttribute(binary_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 4096 * 16));
-    attr_set = true;
-  }
+  smem_optin(binary_pass_kernel, 4096 * 16);
   const int64_t tiles = bp.n_runs * bp.O;
   binary_pass_kernel<<<(unsigned)tiles, kBinThreads, 4096 * 16, stream>>>(bp, x, r);
   NDS_LAUNCH_CHECK();
@@ -321,11 +317,7 @@ int binary_fused_solve_launch(const FactorSet& fwd, const FactorSet& inv, const 
   if (gr.first != 1 || gr.count != 12 || gr.logR != 0 || gr.inner != 1) throw Error(NDS_ERR_OTHER, "fused pass: not a modes-1-12 tile pass");
   const BinPass fw = make_bin_pass(fwd, gr, true);
   const BinPass iv = make_bin_pass(inv, gr, false);
-  static bool attr_set = false;
-  if (!attr_set) {
-    NDS_CUDA(cudaFuncSetAttribute(binary_fused_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 4096 * 16));
-    attr_set = true;
-  }
+  smem_optin(binary_fused_solve_kernel, 4096 * 16);
   BinTileSolve ts{t_pool, n_outer, wf, wf_off, levels};
   binary_fused_solve_kernel<<<(unsigned)gr.outer, kBinThreads, 4096 * 16, stream>>>(fw, iv, ts, x, r);
   NDS_LAUNCH_CHECK();

@@ -181,12 +181,8 @@ void binary_solve_plan_free(BinarySolvePlan& bp) {
 
 int binary_solve_launch(const BinarySolvePlan& bp, const double2* t_pool, double2* c, cudaStream_t stream,
                         Recorder* rec, bool decoupled) {
-  static bool attr_set = false;
   auto kern = binary_tile_solve_kernel;
-  if (!attr_set) {
-    NDS_CUDA(cudaFuncSetAttribute(binary_tile_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 4096 * 16));
-    attr_set = true;
-  }
+  smem_optin(binary_tile_solve_kernel, 4096 * 16);
   BinSolveGeom g{bp.m, bp.n_outer, bp.m + 1, t_pool, decoupled ? 0 : 1};
   const size_t smem = ((size_t)1 << bp.m) * sizeof(double2);
   int launches = 0;

@@ -326,11 +326,7 @@ void block_eig_launch(const double2* t_pool, const EigCands& cands, double2* vpo
   int dmax = 0;
   for (int c = 0; c < cands.count; ++c) dmax = std::max(dmax, std::min(cands.d[c], 128));
   const size_t smem = block_eig_smem(dmax);
-  static size_t attr = 0;
-  if (smem > attr) {
-    NDS_CUDA(cudaFuncSetAttribute(block_eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = smem;
-  }
+  smem_optin(block_eig_kernel, smem);
   block_eig_kernel<<<(unsigned)njobs, kEigThreads, smem, stream>>>(t_pool, cands, vpool, wpool, cond);
   NDS_LAUNCH_CHECK();
   bool big = false;

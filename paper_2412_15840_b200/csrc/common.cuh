@@ -4,8 +4,11 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <map>
+#include <mutex>
 #include <stdexcept>
 #include <string>
+#include <utility>
 
 #include "error.h"
 #include "ndsylv_b200.h"
@@ -21,6 +24,27 @@ namespace nds {
   } while (0)
 
 #define NDS_LAUNCH_CHECK() NDS_CUDA(cudaGetLastError())
+
+// Dynamic shared-memory opt-in of a kernel before its launch. Function attributes belong to the
+// device's context, so the (device, kernel) pairs already raised are remembered — with the
+// largest size set — rather than one process-wide flag (several devices in one process:
+// nds_solve_multi, one host thread per device in the loopback engine).
+inline void smem_optin(const void* fn, size_t bytes) {
+  if (bytes <= 48 * 1024) return;
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> done;
+  int dev = 0;
+  NDS_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& cur = done[{dev, fn}];
+  if (cur >= bytes) return;
+  NDS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  cur = bytes;
+}
+template <class K>
+inline void smem_optin(K* kern, size_t bytes) {
+  smem_optin((const void*)kern, bytes);
+}
 
 // Mode-j view of a column-major tensor (reference kernels.cpp:9-21): (inner, n, outer).
 struct ModeView {

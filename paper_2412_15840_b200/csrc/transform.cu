@@ -587,16 +587,12 @@ template <int BM, int BN, int BK, int WM, int WN, int ST, bool M3, int MINB = 1>
 static void launch_gemm_t(GemmArgs g, cudaStream_t stream) {
   using Cfg = GemmCfg<BM, BN, BK, WM, WN, ST>;
   using SCfg = TmaCfg<BM, BN, BK, WM, WN, 4>;
-  static bool attr_set = false;
   auto kern = zgemm_dmma_kernel<BM, BN, BK, WM, WN, ST, M3, MINB>;
   auto tkern = zgemm_tma_kernel<BM, BN, BK, WM, WN, ST, MINB>;
   auto skern = zgemm_tma_swz_kernel<BM, BN, BK, WM, WN, 4, MINB>;
-  if (!attr_set) {
-    NDS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem));
-    NDS_CUDA(cudaFuncSetAttribute(tkern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem));
-    NDS_CUDA(cudaFuncSetAttribute(skern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SCfg::kSmem));
-    attr_set = true;
-  }
+  smem_optin(kern, Cfg::kSmem);
+  smem_optin(tkern, Cfg::kSmem);
+  smem_optin(skern, SCfg::kSmem);
   const bool colm = g.colm != 0;
   g.ntile_rows = (g.rows + BM - 1) / BM;
   const int64_t W = 1ll << g.wshift;
