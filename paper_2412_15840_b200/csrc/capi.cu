@@ -794,6 +794,13 @@ bool plan_cubic_diag_try(nds_plan* p, bool thorough, bool reorder) {
   char* scratch = nullptr;
   NDS_CUDA(cudaMallocFromPoolAsync((void**)&scratch,
                                    cd_bytes + (size_t)(2 * vtot + 6 * sq + stot + 1) * sizeof(double2), p->ctx->pool, s));
+  struct ScratchGuard {  // stream-ordered release on every exit (route refused, errors)
+    char* ptr;
+    cudaStream_t st;
+    ~ScratchGuard() {
+      if (ptr) cudaFreeAsync(ptr, st);
+    }
+  } scratch_guard{scratch, s};
   double* d_cond = (double*)scratch;
   double2* dv = (double2*)(scratch + cd_bytes);
   double2* dw = dv + vtot;
@@ -834,10 +841,7 @@ bool plan_cubic_diag_try(nds_plan* p, bool thorough, bool reorder) {
   double prod = 1.0;
   for (int j = 0; j < N; ++j) prod *= cands[j][0].cond;
   p->cub_cond = prod;
-  if (!(prod <= kCubicDiagCondMax)) {
-    NDS_CUDA(cudaFreeAsync(scratch, s));
-    return false;
-  }
+  if (!(prod <= kCubicDiagCondMax)) return false;
   for (;;) {  // grow the super-blocks: double the mode whose product stays smallest
     int best = -1;
     double best_prod = 0.0;
@@ -872,7 +876,6 @@ bool plan_cubic_diag_try(nds_plan* p, bool thorough, bool reorder) {
   device_factors(p->ctx, p->cd_inv, N, p->dims, minv, tpr, nullptr, 1);  // U W: op U only; diag from T'
 
   device_factors(p->ctx, p->cd_fwd, N, p->dims, mfh, nullptr, nullptr, 2);      // W^{-1} U^H: op U^H only
-  NDS_CUDA(cudaFreeAsync(scratch, s));
   p->fc = p->cd_inv;
   p->fc.pool = nullptr;  // owned by cd_inv / cd_fwd
   for (int j = 0; j < N; ++j) {
@@ -1109,6 +1112,8 @@ int execute(nds_plan* p, const double2* b, double2* x, double2* work, cudaEvent_
   return launches;
 }
 
+void plan_destroy_impl(nds_plan* p);
+
 // after_upload: called once the factor upload is queued (nds_solve_schur streams B in from there,
 // so the small factor copy is not queued behind the tensor).
 void plan_create_impl(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z* const* u, const nds_z* const* t,
@@ -1151,9 +1156,14 @@ void plan_create_impl(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_
     }
   }
   if (!p->fast_path) {
-    build_solver(p.get());
-    plan_binary_diag(p.get(), u, t);
-    plan_cubic_diag(p.get(), u, t, thorough);
+    try {
+      build_solver(p.get());
+      plan_binary_diag(p.get(), u, t);
+      plan_cubic_diag(p.get(), u, t, thorough);
+    } catch (...) {  // release what the plan holds so far (factor sets, route buffers), then report
+      plan_destroy_impl(p.release());
+      throw;
+    }
   }
   *out = p.release();
 }
