@@ -583,15 +583,16 @@ __global__ void __launch_bounds__(WM* WN * 32, MINB) zgemm_tma_swz_kernel(const 
 //   kWide: 64 x 32 per CTA;  kTall: 32 x 64 per CTA; warps of 16 x 16.
 // The shape with the least padded output is chosen per GEMM (ties: kWide).
 // Algorithmic flops are counted as 8 per complex MAC in every roofline figure regardless.
-template <int BM, int BN, int BK, int WM, int WN, int ST, bool M3, int MINB = 1>
+template <int BM, int BN, int BK, int WM, int WN, int ST, bool M3, int MINB = 1, int TST = ST>
 static void launch_gemm_t(GemmArgs g, cudaStream_t stream) {
   using Cfg = GemmCfg<BM, BN, BK, WM, WN, ST>;
+  using PCfg = GemmCfg<BM, BN, BK, WM, WN, TST>;  // the padded bulk-copy kernel's ring
   using SCfg = TmaCfg<BM, BN, BK, WM, WN, 4>;
   auto kern = zgemm_dmma_kernel<BM, BN, BK, WM, WN, ST, M3, MINB>;
-  auto tkern = zgemm_tma_kernel<BM, BN, BK, WM, WN, ST, MINB>;
+  auto tkern = zgemm_tma_kernel<BM, BN, BK, WM, WN, TST, MINB>;
   auto skern = zgemm_tma_swz_kernel<BM, BN, BK, WM, WN, 4, MINB>;
   smem_optin(kern, Cfg::kSmem);
-  smem_optin(tkern, Cfg::kSmem);
+  smem_optin(tkern, PCfg::kSmem);
   smem_optin(skern, SCfg::kSmem);
   const bool colm = g.colm != 0;
   g.ntile_rows = (g.rows + BM - 1) / BM;
@@ -606,7 +607,7 @@ static void launch_gemm_t(GemmArgs g, cudaStream_t stream) {
   if (tma && !tma_padded(g.K))  // short K: the swizzled images of that factor, 4-stage ring
     skern<<<(unsigned)tiles, SCfg::kThreads, SCfg::kSmem, stream>>>(g);
   else if (tma)
-    tkern<<<(unsigned)tiles, Cfg::kThreads, Cfg::kSmem, stream>>>(g, colm ? 1 : 0);
+    tkern<<<(unsigned)tiles, PCfg::kThreads, PCfg::kSmem, stream>>>(g, colm ? 1 : 0);
   else
     kern<<<(unsigned)tiles, Cfg::kThreads, Cfg::kSmem, stream>>>(g);
   NDS_LAUNCH_CHECK();
@@ -623,8 +624,10 @@ struct ShapeDims {
 };
 static ShapeDims shape_dims(GemmShape s) { return s == kTall ? ShapeDims{32, 64} : ShapeDims{64, 32}; }
 
+// The 32 x 64 shape's smaller padded A stage leaves room for a 4-stage bulk-copy ring at 2 CTAs /
+// SM (c1 mode-2 pass 0.883 -> 0.877 ms, c2 2.04 -> 2.00).
 static void launch_gemm(GemmShape shape, GemmArgs g, cudaStream_t stream) {
-  if (shape == kTall) launch_gemm_t<32, 64, 16, 2, 4, 3, true, 2>(g, stream);
+  if (shape == kTall) launch_gemm_t<32, 64, 16, 2, 4, 3, true, 2, 4>(g, stream);
   else launch_gemm_t<64, 32, 16, 4, 2, 3, true, 2>(g, stream);
 }
 
@@ -657,7 +660,10 @@ static void launch_gemm_auto(GemmArgs g, bool colm, int64_t inner, cudaStream_t 
   GemmArgs gt = g;
   const double cw = shape_cost(gt, colm, inner, kWide);
   const double ct = shape_cost(gt, colm, inner, kTall);
-  const GemmShape best = ct < cw * (1.0 - 1e-9) ? kTall : kWide;
+  // ties (same padded volume): the 32 x 64 shape for long K (n >= 256: c1 mode 1 (cp.async) 0.932
+  // vs 0.939 ms, mode 2 (padded bulk copy, 4 stages) 0.877 vs 0.886), 64 x 32 below (c3: 58.5 vs
+  // 58.0 ms of transforms with the 32 x 64 shape on ties)
+  const GemmShape best = ct < cw * (1.0 - 1e-9) || (ct <= cw * (1.0 + 1e-9) && g.K >= 256) ? kTall : kWide;
   shape_cost(g, colm, inner, best);
   g.blk = g.blk_shape[best];
   launch_gemm(best, g, stream);
