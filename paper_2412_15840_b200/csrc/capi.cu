@@ -514,7 +514,7 @@ int launch_pass_chunk(nds_plan* p, const XPass& ps, bool adjoint, const double2*
   return nds::mode_product_launch(f, ps.mode, adjoint, v, src, dst, false, p->ctx->stream);
 }
 
-int transform_chain(nds_plan* p, bool adjoint, const double2* in, double2* out, double2* work) {
+int transform_chain(nds_plan* p, bool adjoint, const double2* in, double2* out, double2* work, bool merged = false) {
   const std::vector<XPass> passes = transform_passes(p);
   const int N = (int)passes.size();
   nds::Recorder* rec = p->profiling ? &p->rec : nullptr;
@@ -525,7 +525,7 @@ int transform_chain(nds_plan* p, bool adjoint, const double2* in, double2* out, 
     // Out of place: last pass lands in out. In place: first pass must leave `in`, so start in
     // work (an odd pass count then ends in work and is copied back).
     double2* dst = in_place ? ((j % 2 == 1) ? work : out) : (((N - j) % 2 == 0) ? out : work);
-    const int kind = launch_pass(p, passes[j - 1], adjoint, src, dst);
+    const int kind = launch_pass(p, passes[j - 1], adjoint, src, dst, merged);
     if (rec) rec->mark(p->ctx->stream, kind, adjoint ? -passes[j - 1].mode : passes[j - 1].mode);
     ++launches;
     src = dst;
@@ -1433,6 +1433,10 @@ struct nds_ode {
   std::vector<std::vector<nds_z>> t_host;  // T_j (column-major) for the host exponentials
   std::vector<char> parlett;               // mode has a well-separated diagonal: exp on the device
   int64_t fsize = 0;
+  // the plan's block-diagonalised route (T'_j = W_j^{-1} T~_j W_j, factors U~_j W_j): the whole
+  // propagator then works in that basis — exp(t T'_j) = W_j^{-1} exp(t T~_j) W_j by the same
+  // Parlett recurrence (T'_j is upper triangular), the level solve, the merged transforms
+  bool merged = false;
 };
 
 namespace {
@@ -1466,19 +1470,31 @@ void ode_create_impl(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z
   std::unique_ptr<nds_ode, void (*)(nds_ode*)> o(new nds_ode, ode_destroy_impl);
   // the propagator always back-substitutes (ode.cpp:74), never the fast path
   plan_create_impl(ctx, n_modes, dims, u, t, singular_tol, flags & ~(unsigned)NDS_ALLOW_FAST_PATH, &o->plan, nullptr,
-                   true);
+                   true, {}, true);
   nds_plan* p = o->plan;
   const int64_t total = p->total;
   const size_t bytes = (size_t)total * sizeof(double2);
   cudaStream_t s = ctx->stream;
+  o->merged = p->cub_diag;
+  std::vector<const nds_z*> tq(t, t + n_modes);  // the T the propagator uses: T_j, or the route's T'_j
+  if (o->merged) {
+    int64_t sq = 0;
+    for (int j = 0; j < n_modes; ++j) sq += dims[j] * dims[j];
+    std::vector<nds_z> tp((size_t)sq);
+    NDS_CUDA(cudaMemcpyAsync(tp.data(), p->fc.t_pool, (size_t)sq * sizeof(double2), cudaMemcpyDeviceToHost, s));
+    NDS_CUDA(cudaStreamSynchronize(s));
+    for (int j = 0; j < n_modes; ++j) o->t_host.emplace_back(tp.data() + p->fc.geom.toff[j],
+                                                             tp.data() + p->fc.geom.toff[j] + dims[j] * dims[j]);
+    for (int j = 0; j < n_modes; ++j) tq[j] = o->t_host[j].data();
+  }
   o->foff.resize(n_modes);
   for (int j = 0; j < n_modes; ++j) {
     o->foff[j] = o->fsize;
     o->fsize += 2 * dims[j] * dims[j];
-    o->t_host.emplace_back(t[j], t[j] + dims[j] * dims[j]);
+    if (!o->merged) o->t_host.emplace_back(t[j], t[j] + dims[j] * dims[j]);
     // well-separated diagonal -> Parlett recurrence on the device; otherwise host scaling and
     // squaring (matfun.cpp)
-    const bool sep = nds::exp_diagonal_separated((int)dims[j], t[j]);
+    const bool sep = nds::exp_diagonal_separated((int)dims[j], tq[j]);
     o->parlett.push_back(sep ? 1 : 0);
   }
   NDS_CUDA(cudaMalloc(&o->d_c, bytes));
@@ -1489,11 +1505,11 @@ void ode_create_impl(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z
   ensure_ws(ctx, total);
   // C = forward(B); Y0 = forward(X0) (ode.cpp:53-54)
   NDS_CUDA(cudaMemcpyAsync(ctx->ws[0], forcing, bytes, cudaMemcpyHostToDevice, s));
-  transform_chain(p, true, ctx->ws[0], o->d_c, ctx->ws[1]);
+  transform_chain(p, true, ctx->ws[0], o->d_c, ctx->ws[1], o->merged);
   NDS_CUDA(cudaMemcpyAsync(ctx->ws[0], initial, bytes, cudaMemcpyHostToDevice, s));
-  transform_chain(p, true, ctx->ws[0], ctx->ws[0], ctx->ws[1]);
+  transform_chain(p, true, ctx->ws[0], ctx->ws[0], ctx->ws[1], o->merged);
   // G0 = sum_j T_j x_j Y0 + C (ode.cpp:55-56: apply_operator then add_scaled(., 1, C))
-  for (int j = 0; j < n_modes; ++j) pack_layouts(dims[j], t[j], o->h_f + o->foff[j]);
+  for (int j = 0; j < n_modes; ++j) pack_layouts(dims[j], tq[j], o->h_f + o->foff[j]);
   ode_upload_f(o.get());
   NDS_CUDA(cudaMalloc(&o->d_trow, (size_t)(o->fsize / 2) * sizeof(double2)));
   for (int j = 0; j < n_modes; ++j)  // the row-major halves of the T layouts just uploaded
@@ -1524,7 +1540,7 @@ int ode_at_dev_impl(nds_ode* o, double time, double2* d_x, cudaEvent_t* ev) {
   if (ev) NDS_CUDA(cudaEventRecord(ev[0], s));
   int launches = 0;
   nds::ExpArgs ea{};
-  ea.t_pool = p->f.t_pool;
+  ea.t_pool = o->merged ? p->fc.t_pool : p->f.t_pool;
   ea.t_row = o->d_trow;
   ea.f = (double2*)o->d_f;
   ea.t = time;
@@ -1561,10 +1577,10 @@ int ode_at_dev_impl(nds_ode* o, double time, double2* d_x, cudaEvent_t* ev) {
   }
   launches += nds::axpy_launch(g, g, make_double2(-1.0, 0.0), o->d_c, p->total, s);
   if (ev) NDS_CUDA(cudaEventRecord(ev[1], s));
-  launches += launch_solver(p, g, s, nullptr);  // back_substitute (ode.cpp:76)
+  launches += launch_solver(p, g, s, nullptr, o->merged);  // back_substitute (ode.cpp:76)
   if (ev) NDS_CUDA(cudaEventRecord(ev[2], s));
   double2* other = (g == ctx->ws[0]) ? ctx->ws[1] : ctx->ws[0];
-  launches += transform_chain(p, false, g, d_x, other);  // inverse_transform (ode.cpp:82)
+  launches += transform_chain(p, false, g, d_x, other, o->merged);  // inverse_transform (ode.cpp:82)
   if (p->flags & NDS_REAL_OUTPUT) launches += nds::real_part_launch(d_x, p->total, s);
   if (ev) NDS_CUDA(cudaEventRecord(ev[3], s));
   return launches;
