@@ -29,4 +29,6 @@ timeout 400 $NCU -k regex:schur_reorder -c 1 -o $O/schur_reorder_c1 python tools
 timeout 400 $NCU -k regex:block_eig -c 1 -o $O/block_eig_c1 python tools/gpu/plan_timing.py c1 > /dev/null 2>&1
 timeout 600 $NCU -k regex:binary_pass -s 1 -c 1 -o $O/binary_pass_c4 $P --config c4 > /dev/null 2>&1
 timeout 600 $NCU -k regex:binary_fused -s 1 -c 1 -o $O/binary_fused_c4 $P --config c4 > /dev/null 2>&1
+timeout 600 python tools/bench_ode.py > $O/ode_bench.json 2> $O/ode_bench.err
+timeout 300 python tools/gpu/route_survey.py > $O/route_survey.txt 2>&1
 echo done > $O/done
