@@ -789,8 +789,8 @@ bool plan_cubic_diag_try(nds_plan* p, bool thorough, bool reorder) {
   cudaStream_t s = p->ctx->stream;
   int64_t sq = 0;
   for (int j = 0; j < N; ++j) sq += p->dims[j] * p->dims[j];
-  // device scratch: [cond][V pool][W pool][M_inv][M_fwd^H][T W][T'][T~][U~]
-  const size_t cd_bytes = ((size_t)njobs * sizeof(double) + 255) / 256 * 256;
+  // device scratch: [cond, reorder barrier word][V pool][W pool][M_inv][M_fwd^H][T W][T'][T~][U~]
+  const size_t cd_bytes = ((size_t)njobs * sizeof(double) + sizeof(unsigned int) + 255) / 256 * 256;
   char* scratch = nullptr;
   NDS_CUDA(cudaMallocFromPoolAsync((void**)&scratch,
                                    cd_bytes + (size_t)(2 * vtot + 6 * sq + stot + 1) * sizeof(double2), p->ctx->pool, s));
@@ -826,7 +826,7 @@ bool plan_cubic_diag_try(nds_plan* p, bool thorough, bool reorder) {
     if (n / prod > 1) ra.rad[j][nr++] = (int)(n / prod);
     ra.nrad[j] = n <= nds::kReorderMaxN ? nr : 0;  // larger extents keep their order
   }
-  if (reorder) nds::schur_reorder_launch(ra, N, tre, ure, s);
+  if (reorder) nds::schur_reorder_launch(ra, N, tre, ure, (unsigned int*)(d_cond + njobs), s);
   std::vector<double> cond(njobs);
   nds::block_eig_launch(tre, ec, dv, dw, d_cond, eig_scratch, s);
   NDS_CUDA(cudaMemcpyAsync(cond.data(), d_cond, njobs * sizeof(double), cudaMemcpyDeviceToHost, s));

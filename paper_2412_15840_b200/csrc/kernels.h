@@ -212,7 +212,9 @@ struct ReorderArgs {
   int nrad[NDS_MAX_MODES];
   int rad[NDS_MAX_MODES][12];
 };
-void schur_reorder_launch(const ReorderArgs& ra, int n_modes, double2* tpool, double2* upool, cudaStream_t stream);
+// bar: a device word for the grid barrier (zeroed here).
+void schur_reorder_launch(const ReorderArgs& ra, int n_modes, double2* tpool, double2* upool, unsigned int* bar,
+                          cudaStream_t stream);
 // diag(T_j) of every mode (t_pool at g.toff) into diag (at g.doff).
 void diag_extract_launch(const Geom& g, const double2* t_pool, double2* diag, cudaStream_t stream);
 // Small plan data written by a kernel from its by-value parameter (no copy-engine traffic, so it
