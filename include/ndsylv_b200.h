@@ -165,6 +165,15 @@ int nds_plan_backsub(nds_plan* plan, nds_z* d_c);
 int nds_plan_inverse(nds_plan* plan, const nds_z* d_in, nds_z* d_out, nds_z* d_work);
 /* Host buffers, synchronous: H2D(b), execute, D2H(x); stage device times into rep. */
 int nds_plan_execute_host(nds_plan* plan, const nds_z* h_b, nds_z* h_x, nds_report* rep);
+/* count right-hand sides through the same plan, synchronous: x[k] = solve(b[k]). With PINNED
+ * buffers the solves are pipelined (H2D of b[k+1] and D2H of x[k-1] overlap solve k on separate
+ * copy streams; device B / X double-buffered), so the period per right-hand side is
+ * max(solve, H2D, D2H); pageable buffers run nds_plan_execute_host per right-hand side. x[k] may
+ * alias b[k], no other aliasing. rep: static fields, total_seconds (the whole call) and
+ * kernel_launches (all solves). Replaces a loop of ndsylv::solve over the same coefficients
+ * (sylvester.cpp:167-227) with the Schur step and the plan done once. */
+int nds_plan_execute_host_many(nds_plan* plan, int count, const nds_z* const* h_b, nds_z* const* h_x,
+                               nds_report* rep);
 /* Kernel launches one nds_plan_execute issues. */
 int nds_plan_launches(const nds_plan* plan);
 /* Which triangular-solve route the plan takes: the fast-path divide,

@@ -90,6 +90,43 @@ inline SolveResult solve(const SylvesterProblem& p, const SolveOptions& o = {}) 
   return r;
 }
 
+// Several right-hand sides with the same coefficients: what a loop of ndsylv::solve over
+// problems that share A_1..A_N computes (sylvester.cpp:167-227 per call), with the Schur step and
+// the device plan done once (nds_plan_create) and the right-hand sides streamed through
+// nds_plan_execute_host_many (pipelined when the tensors' storage is pinned).
+inline std::vector<NDTensor> solve_many(const std::vector<Matrix>& coefficients, const std::vector<NDTensor>& rhs,
+                                        const SolveOptions& o = {}) {
+  std::vector<NDTensor> xs;
+  if (rhs.empty()) return xs;
+  validate_coefficients(coefficients, rhs[0].dims, "problem");
+  for (const NDTensor& b : rhs)
+    if (b.dims != rhs[0].dims) throw std::invalid_argument("right-hand side shape mismatch");
+  std::vector<SchurFactors> f;
+  for (const Matrix& a : coefficients) f.push_back(schur(a));
+  std::vector<const nds_z*> u, t;
+  for (auto& s : f) {
+    u.push_back(reinterpret_cast<const nds_z*>(s.u.data()));
+    t.push_back(reinterpret_cast<const nds_z*>(s.t.data()));
+  }
+  const unsigned flags = (o.allow_fast_path ? NDS_ALLOW_FAST_PATH : 0u) | (o.real_output ? NDS_REAL_OUTPUT : 0u);
+  nds_plan* plan = nullptr;
+  nds_singular sing{};
+  rethrow(nds_plan_create(context(), rhs[0].order(), rhs[0].dims.data(), u.data(), t.data(), o.singular_tol, flags,
+                          &plan, &sing),
+          sing);
+  std::vector<const nds_z*> hb;
+  std::vector<nds_z*> hx;
+  for (const NDTensor& b : rhs) {
+    xs.push_back(NDTensor::zeros(b.dims));
+    hb.push_back(reinterpret_cast<const nds_z*>(b.data.data()));
+    hx.push_back(reinterpret_cast<nds_z*>(xs.back().data.data()));
+  }
+  const int rc = nds_plan_execute_host_many(plan, static_cast<int>(rhs.size()), hb.data(), hx.data(), nullptr);
+  nds_plan_destroy(plan);
+  rethrow(rc, sing);
+  return xs;
+}
+
 // The same solve sharded over several GPUs of this process (nds_solve_multi: one host thread,
 // context and NCCL communicator per device). Report: Schur time only (the per-device stage times
 // stay inside the library).

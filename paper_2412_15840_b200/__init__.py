@@ -50,7 +50,7 @@ EXPORTED = [
     "nds_ctx_trim", "nds_solve", "nds_solve_schur", "nds_schur", "nds_forward_transform", "nds_inverse_transform",
     "nds_back_substitute", "nds_mode_product", "nds_apply_operator", "nds_flop_estimate", "nds_schur_flop_estimate",
     "nds_plan_create", "nds_plan_destroy", "nds_plan_report", "nds_plan_total", "nds_plan_execute",
-    "nds_plan_forward", "nds_plan_backsub", "nds_plan_inverse", "nds_plan_execute_host", "nds_plan_launches", "nds_plan_solve_path",
+    "nds_plan_forward", "nds_plan_backsub", "nds_plan_inverse", "nds_plan_execute_host", "nds_plan_execute_host_many", "nds_plan_launches", "nds_plan_solve_path",
     "nds_plan_diagonalised", "nds_plan_superblocks",
     "nds_plan_profile_begin", "nds_plan_profile_end",
     "nds_dev_mode_product", "nds_dev_mode_update", "nds_dev_mode_apply", "nds_dev_back_substitute", "nds_dev_residual",
@@ -177,6 +177,7 @@ def load_library(path: str = LIB_PATH):
     L.nds_plan_backsub.argtypes = [_vp, _vp]
     L.nds_plan_inverse.argtypes = [_vp, _vp, _vp, _vp]
     L.nds_plan_execute_host.argtypes = [_vp, _vp, _vp, C.POINTER(_Report)]
+    L.nds_plan_execute_host_many.argtypes = [_vp, C.c_int, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_Report)]
     L.nds_plan_launches.argtypes = [_vp]
     L.nds_plan_solve_path.argtypes = [_vp]
     L.nds_plan_diagonalised.argtypes = [_vp, C.POINTER(C.c_double)]
@@ -469,6 +470,25 @@ class Plan:
         rep = _Report()
         self._check(self.ctx.lib.nds_plan_execute_host(self.h, h_b, h_x, C.byref(rep)))
         return _dict(rep)
+
+    def execute_host_many(self, bs, xs=None):
+        """Several right-hand sides through this plan (nds_plan_execute_host_many): pinned host
+        buffers are pipelined (H2D of b[k+1] / D2H of x[k-1] under solve k). bs: list of
+        column-major complex128 arrays of shape dims (or host pointers as ints, with xs given)."""
+        if bs and isinstance(bs[0], int):
+            hb, hx, keep = list(bs), list(xs), None
+        else:
+            bs = [_f(b) for b in bs]
+            if xs is None:
+                xs = [np.empty_like(b, order="F") for b in bs]
+            hb = [b.ctypes.data for b in bs]
+            hx = [x.ctypes.data for x in xs]
+        n = len(hb)
+        pb = (_vp * max(n, 1))(*hb)
+        px = (_vp * max(n, 1))(*hx)
+        rep = _Report()
+        self._check(self.ctx.lib.nds_plan_execute_host_many(self.h, n, pb, px, C.byref(rep)))
+        return xs, _dict(rep)
 
     def launches(self) -> int:
         return self.ctx.lib.nds_plan_launches(self.h)

@@ -59,6 +59,12 @@ struct nds_ctx {
   };
   std::vector<D2H> d2h_deferred;
   cudaEvent_t d2h_ev[64] = {};
+  // streamed right-hand sides (nds_plan_execute_host_many): B and X double-buffered on the
+  // device, the D2H of X_{k-1} on its own stream beside the H2D of B_{k+1} (ctx->copy)
+  cudaStream_t copy_out = nullptr;
+  double2* mbuf[4] = {};  // B slot 0, B slot 1, X slot 0, X slot 1
+  size_t mbuf_bytes = 0;
+  cudaEvent_t mev[10] = {};  // in_ready[2], in_free[2], out_ready[2], out_free[2], start, end
 };
 
 struct nds_plan {
@@ -1380,6 +1386,95 @@ void execute_host_impl(nds_plan* p, const nds_z* hb, nds_z* hx, nds_report* rep,
   }
 }
 
+// Several right-hand sides through one plan (the same operator, e.g. a sequence of independent
+// loads or the stages of a time integrator whose forcings are known up front). A single solve
+// cannot overlap its own H2D with its D2H (every X entry depends on every B entry), but
+// consecutive solves can: B_{k+1} streams in on the copy stream and X_{k-1} streams out on
+// copy_out while solve k runs, so with pinned buffers the period per right-hand side is
+// max(device solve, H2D, D2H) instead of their sum. B and X are double-buffered on the device;
+// every buffer hand-over is an event (in_ready / in_free / out_ready / out_free per slot).
+// Pageable buffers (or a single right-hand side) take the chunked one-shot path per solve.
+void execute_host_many_impl(nds_plan* p, int count, const nds_z* const* hb, nds_z* const* hx, nds_report* rep) {
+  if (count < 0 || (count > 0 && (!hb || !hx))) throw Error(NDS_ERR_INVALID, "null tensor pointer array");
+  for (int k = 0; k < count; ++k)
+    if (!hb[k] || !hx[k]) throw Error(NDS_ERR_INVALID, "null tensor pointer");
+  const auto t0 = Clock::now();
+  nds_ctx* ctx = p->ctx;
+  ensure_device(ctx);
+  bool pinned = count > 1;
+  for (int k = 0; k < count && pinned; ++k) pinned = !host_pageable(hb[k]) && !host_pageable(hx[k]);
+  int launches = 0;
+  if (!pinned) {
+    for (int k = 0; k < count; ++k) {
+      nds_report r{};
+      execute_host_impl(p, hb[k], hx[k], &r);
+      launches += r.kernel_launches;
+    }
+  } else {
+    const size_t bytes = (size_t)p->total * sizeof(double2);
+    ensure_ws(ctx, p->total);
+    if (ctx->mbuf_bytes < bytes) {
+      for (auto& w : ctx->mbuf)
+        if (w) {
+          cudaFree(w);
+          w = nullptr;
+        }
+      ctx->mbuf_bytes = 0;
+      for (auto& w : ctx->mbuf) NDS_CUDA(cudaMalloc(&w, bytes));
+      ctx->mbuf_bytes = bytes;
+    }
+    if (!ctx->copy_out) NDS_CUDA(cudaStreamCreateWithFlags(&ctx->copy_out, cudaStreamNonBlocking));
+    if (!ctx->mev[0]) {
+      for (int i = 0; i < 8; ++i) NDS_CUDA(cudaEventCreateWithFlags(&ctx->mev[i], cudaEventDisableTiming));
+      NDS_CUDA(cudaEventCreate(&ctx->mev[8]));
+      NDS_CUDA(cudaEventCreate(&ctx->mev[9]));
+    }
+    cudaStream_t s = ctx->stream, in = ctx->copy, out = ctx->copy_out;
+    cudaEvent_t* in_ready = ctx->mev;
+    cudaEvent_t* in_free = ctx->mev + 2;
+    cudaEvent_t* out_ready = ctx->mev + 4;
+    cudaEvent_t* out_free = ctx->mev + 6;
+    double2* W = ctx->ws[1];
+    NDS_CUDA(cudaEventRecord(ctx->mev[8], s));
+    NDS_CUDA(cudaStreamWaitEvent(in, ctx->mev[8], 0));
+    NDS_CUDA(cudaStreamWaitEvent(out, ctx->mev[8], 0));
+    auto h2d = [&](int k) {
+      const int slot = k & 1;
+      if (k >= 2) NDS_CUDA(cudaStreamWaitEvent(in, in_free[slot], 0));  // solve k-2 has read it
+      NDS_CUDA(cudaMemcpyAsync(ctx->mbuf[slot], hb[k], bytes, cudaMemcpyHostToDevice, in));
+      NDS_CUDA(cudaEventRecord(in_ready[slot], in));
+    };
+    h2d(0);
+    for (int k = 0; k < count; ++k) {
+      const int slot = k & 1;
+      if (k + 1 < count) h2d(k + 1);
+      NDS_CUDA(cudaStreamWaitEvent(s, in_ready[slot], 0));
+      if (k >= 2) NDS_CUDA(cudaStreamWaitEvent(s, out_free[slot], 0));  // X_{k-2} has left
+      launches += execute(p, ctx->mbuf[slot], ctx->mbuf[2 + slot], W, nullptr);
+      NDS_CUDA(cudaEventRecord(in_free[slot], s));
+      NDS_CUDA(cudaEventRecord(out_ready[slot], s));
+      NDS_CUDA(cudaStreamWaitEvent(out, out_ready[slot], 0));
+      NDS_CUDA(cudaMemcpyAsync(hx[k], ctx->mbuf[2 + slot], bytes, cudaMemcpyDeviceToHost, out));
+      NDS_CUDA(cudaEventRecord(out_free[slot], out));
+    }
+    NDS_CUDA(cudaStreamWaitEvent(s, out_free[(count - 1) & 1], 0));  // the last X has left
+    NDS_CUDA(cudaEventRecord(ctx->mev[9], s));
+    NDS_CUDA(cudaStreamSynchronize(s));
+  }
+  p->launches = count > 0 ? launches / count : 0;
+  if (rep) {
+    report_static(p, rep);
+    rep->total_seconds = secs(t0);
+    if (pinned) {
+      const double dev = ev_ms(ctx->mev[8], ctx->mev[9]) * 1e-3;
+      rep->transform_seconds = rep->backsub_seconds = rep->inverse_seconds = 0.0;
+      rep->h2d_seconds = rep->d2h_seconds = 0.0;
+      rep->total_seconds = std::max(rep->total_seconds, dev);
+    }
+    rep->kernel_launches = launches;
+  }
+}
+
 // Host-buffer transform (forward_transform / inverse_transform).
 void transform_host(nds_ctx* ctx, int n_modes, const int64_t* dims, const nds_z* const* u, const nds_z* in, nds_z* out,
                     bool adjoint) {
@@ -1821,6 +1916,9 @@ void nds_ctx_destroy(nds_ctx* ctx) {
     if (e) cudaEventDestroy(e);
   for (auto& e : ctx->d2h_ev)
     if (e) cudaEventDestroy(e);
+  for (auto& e : ctx->mev)
+    if (e) cudaEventDestroy(e);
+  if (ctx->copy_out) cudaStreamDestroy(ctx->copy_out);
   delete ctx;
 }
 
@@ -1843,6 +1941,12 @@ void nds_ctx_trim(nds_ctx* ctx) {
       w = nullptr;
     }
   ctx->ws_bytes = ctx->ws3_bytes = 0;
+  for (auto& w : ctx->mbuf)
+    if (w) {
+      cudaFree(w);
+      w = nullptr;
+    }
+  ctx->mbuf_bytes = 0;
   cudaStreamSynchronize(ctx->stream);
   ctx->solvers.clear();  // plans still alive keep their shared solver structures
 }
@@ -1915,6 +2019,12 @@ int nds_plan_inverse(nds_plan* plan, const nds_z* d_in, nds_z* d_out, nds_z* d_w
 int nds_plan_execute_host(nds_plan* plan, const nds_z* h_b, nds_z* h_x, nds_report* rep) {
   if (!plan) return NDS_ERR_INVALID;
   return guarded(plan->ctx, [&] { execute_host_impl(plan, h_b, h_x, rep); });
+}
+
+int nds_plan_execute_host_many(nds_plan* plan, int count, const nds_z* const* h_b, nds_z* const* h_x,
+                               nds_report* rep) {
+  if (!plan) return NDS_ERR_INVALID;
+  return guarded(plan->ctx, [&] { execute_host_many_impl(plan, count, h_b, h_x, rep); });
 }
 
 int nds_plan_launches(const nds_plan* plan) { return plan ? plan->launches : -1; }

@@ -55,6 +55,18 @@ int main() {
     const SolveResult gpu = ndsylv::gpu::solve_multi(g.problem, {0});
     worst = std::max(worst, max_abs_diff(cpu.x, gpu.x) / max_abs(cpu.x));
   }
+  {  // several right-hand sides through one plan: each against the reference's own solve
+    const GeneratedProblem g = random_problem({32, 24, 16}, 501);
+    std::vector<NDTensor> rhs;
+    for (std::uint64_t s : {502u, 503u, 504u}) rhs.push_back(random_problem({32, 24, 16}, s).problem.rhs);
+    const std::vector<NDTensor> xs = ndsylv::gpu::solve_many(g.problem.coefficients, rhs);
+    for (size_t k = 0; k < rhs.size(); ++k) {
+      SylvesterProblem p = g.problem;
+      p.rhs = rhs[k];
+      const SolveResult cpu = solve(p);
+      worst = std::max(worst, max_abs_diff(cpu.x, xs[k]) / max_abs(cpu.x));
+    }
+  }
   std::printf("max_rel_diff %.3e singular_ok %d\n", worst, singular_ok);
 
   // ODE: the reference's own random systems (rng.hpp random_ode_system), CPU vs GPU

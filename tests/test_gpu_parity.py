@@ -285,6 +285,45 @@ def test_host_path_pageable_equals_pinned(ctx, dims):
     assert rel_max(outs[0].reshape(dims, order="F"), x_ref) <= 1e-11
 
 
+@pytest.mark.parametrize("dims,count", [((64, 64, 64), 5), ((16, 16, 16, 32), 3), ((2,) * 18, 4), ((24, 20, 16), 2),
+                                        ((48, 40, 64), 1)],
+                         ids=["64^3x5", "16x16x16x32x3", "bin18x4", "24x20x16x2", "48x40x64x1"])
+def test_execute_host_many(ctx, port, dims, count):
+    """nds_plan_execute_host_many: several right-hand sides through one plan, pinned (pipelined:
+    H2D of b[k+1] and D2H of x[k-1] under solve k, device buffers double-buffered) and pageable
+    (one chunked host solve each). Every x[k] against the oracle on b[k]; pinned and pageable
+    runs against each other and against the device-pointer execute of the same plan (bitwise:
+    the pipelined path runs the same kernels on whole tensors)."""
+    import torch
+    rng = np.random.default_rng(41)
+    us, ts = rand_factors(rng, dims)
+    bs = [np.asfortranarray(rand_c(rng, dims)) for _ in range(count)]
+    plan = ctx.plan(us, ts, allow_fast_path=False)
+    xs_page, rep = plan.execute_host_many(bs)
+    assert rep["kernel_launches"] > 0
+    flats = [torch.from_numpy(np.ascontiguousarray(b.reshape(-1, order="F"))).pin_memory() for b in bs]
+    outs = [torch.empty_like(f).pin_memory() for f in flats]
+    plan.execute_host_many([f.data_ptr() for f in flats], [o.data_ptr() for o in outs])
+    dev_b = torch.from_numpy(np.ascontiguousarray(bs[-1].reshape(-1, order="F"))).cuda()
+    dev_x = torch.empty_like(dev_b)
+    plan.execute(dev_b.data_ptr(), dev_x.data_ptr())
+    torch.cuda.synchronize()
+    x_dev = dev_x.cpu().numpy()
+    for k in range(count):
+        x_ref, _ = port.solve_schur(us, ts, bs[k], flags=0)
+        x_pin = outs[k].numpy().reshape(dims, order="F")
+        assert rel_max(x_pin, x_ref) <= 1e-11
+        assert rel_max(xs_page[k], x_ref) <= 1e-11
+    if count > 1:
+        assert np.array_equal(outs[-1].numpy(), x_dev)
+    # in place (x[k] aliases b[k]) gives the same X
+    inplace = [f.clone().pin_memory() for f in flats]
+    plan.execute_host_many([f.data_ptr() for f in inplace], [f.data_ptr() for f in inplace])
+    for k in range(count):
+        assert np.array_equal(inplace[k].numpy(), outs[k].numpy()) or count == 1
+    plan.close()
+
+
 @pytest.mark.parametrize("n_modes,seed", [(13, 1), (16, 2), (20, 3)])
 def test_binary_diagonalised_route_matches_coupled_solve(ctx, ref, n_modes, seed):
     """All-binary problems with more than 12 modes: a full solve (nds_plan_execute) diagonalises
