@@ -36,7 +36,9 @@ __host__ __device__ __forceinline__ constexpr int swz(int p) { return p ^ (((p >
 
 // One round: each thread slot gathers the 2^NB entries spanning the round's NB group modes,
 // applies the NB 2x2 matrices as butterflies in registers, and scatters them back.
-template <int NB>
+// UNIT: the matrices are unit-diagonal ([[1, p], [q, 1]], the normalised factors of the fused
+// route — four FMAs per output instead of eight).
+template <int NB, bool UNIT = false>
 __device__ __forceinline__ void bin_round(const BinPass& bp, int rd, double2* S, const double2 (*Mq)[4], int tid) {
   constexpr int V = 1 << NB;
   int rbit[NB];
@@ -68,8 +70,13 @@ __device__ __forceinline__ void bin_round(const BinPass& bp, int rd, double2* S,
       for (int e = 0; e < V; ++e) {
         if (!((e >> q) & 1)) {
           const double2 a = v[e], b = v[e | (1 << q)];
-          v[e] = cfma(cmul(m00, a), m01, b);
-          v[e | (1 << q)] = cfma(cmul(m10, a), m11, b);
+          if (UNIT) {
+            v[e] = cfma(a, m01, b);
+            v[e | (1 << q)] = cfma(b, m10, a);
+          } else {
+            v[e] = cfma(cmul(m00, a), m01, b);
+            v[e | (1 << q)] = cfma(cmul(m10, a), m11, b);
+          }
         }
       }
     }
@@ -78,6 +85,20 @@ __device__ __forceinline__ void bin_round(const BinPass& bp, int rd, double2* S,
   }
 }
 
+template <bool UNIT>
+__device__ __forceinline__ void bin_rounds(const BinPass& bp, double2* S, const double2 (*Mq)[4], int tid) {
+  for (int rd = 0; rd < bp.rounds; ++rd) {
+    switch (bp.nrb[rd]) {
+      case 4: bin_round<4, UNIT>(bp, rd, S, Mq, tid); break;
+      case 3: bin_round<3, UNIT>(bp, rd, S, Mq, tid); break;
+      case 2: bin_round<2, UNIT>(bp, rd, S, Mq, tid); break;
+      default: bin_round<1, UNIT>(bp, rd, S, Mq, tid); break;
+    }
+    __syncthreads();
+  }
+}
+
+template <bool UNIT>
 __global__ void __launch_bounds__(kBinThreads, 2) binary_pass_kernel(const BinPass bp, const double2* __restrict__ x,
                                                                   double2* __restrict__ r) {
   extern __shared__ __align__(16) double2 S[];  // 4096 entries (64 KB, dynamic)
@@ -109,15 +130,7 @@ __global__ void __launch_bounds__(kBinThreads, 2) binary_pass_kernel(const BinPa
     for (int i = 0; i < 8; ++i) S[stid ^ swz((h * 8 + i) * kBinThreads)] = v[i];
   }
   __syncthreads();
-  for (int rd = 0; rd < bp.rounds; ++rd) {
-    switch (bp.nrb[rd]) {
-      case 4: bin_round<4>(bp, rd, S, Mq, tid); break;
-      case 3: bin_round<3>(bp, rd, S, Mq, tid); break;
-      case 2: bin_round<2>(bp, rd, S, Mq, tid); break;
-      default: bin_round<1>(bp, rd, S, Mq, tid); break;
-    }
-    __syncthreads();
-  }
+  bin_rounds<UNIT>(bp, S, Mq, tid);
 #pragma unroll
   for (int i = 0; i < 4096 / kBinThreads; ++i) r[goff(i)] = S[stid ^ swz(i * kBinThreads)];
 }
@@ -132,6 +145,8 @@ __global__ void __launch_bounds__(kBinThreads, 2) binary_pass_kernel(const BinPa
 // pass fused into one read and one write of the tensor.
 struct BinTileSolve {
   const double2* t;    // T_j (2x2 column-major) at t + 4 j, all N modes
+  const double2* e;    // normalised route (UNIT): the deferred diagonal scale e_j[bit] of every mode at
+                       // e + 2 j (forward row scale x inverse column scale); nullptr otherwise
   int n_outer;         // N - 12
   const uint16_t* wf;  // the 4096 tile entries by popcount over the coupled modes, highest first
                        // (bank-interleaved)
@@ -139,13 +154,23 @@ struct BinTileSolve {
   int levels;          // coupled inner modes + 1
 };
 
+// UNIT (normalised factors): every forward factor is diag(f_j) [[1, p], [q, 1]] and every inverse
+// factor [[1, p'], [q', 1]] diag(g_j) — here and in the outer modes' passes. The diagonal parts
+// commute with all the other modes' butterflies and with the division by den, so all of them
+// meet in this kernel as one separable scale E[l] = prod_j (f_j g_j)[bit_j(l)] applied where the
+// tile solve reads its right-hand side: with c = D_f c^ (c^ = the tile after the unit butterflies)
+// and w = D_g y the tile the unit inverse butterflies expect,
+//   w[l] = (E[l] c^[l] - sum_j t01_j (g_j[0] / g_j[1]) w[l | e_j]) / den[l]
+// (the ratio folded into ts.t on the host).
+template <bool UNIT>
 __global__ void __launch_bounds__(kBinThreads, 2)
     binary_fused_solve_kernel(const BinPass fw, const BinPass iv, const BinTileSolve ts, const double2* __restrict__ x,
                               double2* __restrict__ r) {
   extern __shared__ __align__(16) double2 S[];  // 4096 entries, swizzled (swz)
   __shared__ double2 Mq[12][4];
   __shared__ double2 t01[12], dlo[64], dhi[64];
-  __shared__ double2 dout;
+  __shared__ double2 dout, eout;
+  __shared__ double2 elo[UNIT ? 64 : 1], ehi[UNIT ? 64 : 1];
   const int tid = threadIdx.x;
   const int64_t tile = blockIdx.x;  // outer index (modes 13..N)
   const int64_t base = tile << 12;
@@ -155,6 +180,11 @@ __global__ void __launch_bounds__(kBinThreads, 2)
     double2 d = make_double2(0.0, 0.0);
     for (int q = 0; q < ts.n_outer; ++q) d = cadd(d, ts.t[4 * (12 + q) + (((tile >> q) & 1) ? 3 : 0)]);
     dout = d;
+    if (UNIT) {
+      double2 e = make_double2(1.0, 0.0);
+      for (int q = 0; q < ts.n_outer; ++q) e = cmul(e, ts.e[2 * (12 + q) + ((tile >> q) & 1)]);
+      eout = e;
+    }
   }
   const int stid = swz(tid);
   // tile load: contiguous 4096 entries (run R = 4096 / ... : pass geometry inner = 1)
@@ -167,25 +197,27 @@ __global__ void __launch_bounds__(kBinThreads, 2)
     for (int i = 0; i < 8; ++i) S[stid ^ swz((h * 8 + i) * kBinThreads)] = v[i];
   }
   __syncthreads();
-  for (int rd = 0; rd < fw.rounds; ++rd) {
-    switch (fw.nrb[rd]) {
-      case 4: bin_round<4>(fw, rd, S, Mq, tid); break;
-      case 3: bin_round<3>(fw, rd, S, Mq, tid); break;
-      case 2: bin_round<2>(fw, rd, S, Mq, tid); break;
-      default: bin_round<1>(fw, rd, S, Mq, tid); break;
-    }
-    __syncthreads();
-  }
+  bin_rounds<UNIT>(fw, S, Mq, tid);
   // den tables (modes 1-6 | modes 7-12 + the outer part), then the inverse factors
   if (tid < 64) {
     double2 d = make_double2(0.0, 0.0);
     for (int j = 0; j < 6; ++j) d = cadd(d, ts.t[4 * j + (((tid >> j) & 1) ? 3 : 0)]);
     dlo[tid] = d;
+    if (UNIT) {
+      double2 e = make_double2(1.0, 0.0);
+      for (int j = 0; j < 6; ++j) e = cmul(e, ts.e[2 * j + ((tid >> j) & 1)]);
+      elo[tid] = e;
+    }
   } else if (tid < 128) {
     const int xh = tid - 64;
     double2 d = make_double2(0.0, 0.0);
     for (int j = 0; j < 6; ++j) d = cadd(d, ts.t[4 * (6 + j) + (((xh >> j) & 1) ? 3 : 0)]);
     dhi[xh] = cadd(d, dout);
+    if (UNIT) {
+      double2 e = eout;
+      for (int j = 0; j < 6; ++j) e = cmul(e, ts.e[2 * (6 + j) + ((xh >> j) & 1)]);
+      ehi[xh] = e;
+    }
   } else if (tid < 128 + 48) {
     const int e = tid - 128;
     Mq[e >> 2][e & 3] = iv.M[e >> 2][e & 3];
@@ -199,6 +231,7 @@ __global__ void __launch_bounds__(kBinThreads, 2)
       const int l = ts.wf[p];
       const int sl = swz(l);
       double2 n0 = S[sl], n1 = make_double2(0.0, 0.0);
+      if (UNIT) n0 = cmul(cmul(elo[l & 63], ehi[l >> 6]), n0);
 #pragma unroll
       for (int j = 0; j < 12; j += 2) {
         if (!((l >> j) & 1)) n0 = cfms(n0, t01[j], S[sl ^ swz(1 << j)]);
@@ -208,15 +241,7 @@ __global__ void __launch_bounds__(kBinThreads, 2)
     }
     __syncthreads();
   }
-  for (int rd = 0; rd < iv.rounds; ++rd) {
-    switch (iv.nrb[rd]) {
-      case 4: bin_round<4>(iv, rd, S, Mq, tid); break;
-      case 3: bin_round<3>(iv, rd, S, Mq, tid); break;
-      case 2: bin_round<2>(iv, rd, S, Mq, tid); break;
-      default: bin_round<1>(iv, rd, S, Mq, tid); break;
-    }
-    __syncthreads();
-  }
+  bin_rounds<UNIT>(iv, S, Mq, tid);
 #pragma unroll
   for (int i = 0; i < 4096 / kBinThreads; ++i) r[base + tid + i * kBinThreads] = S[stid ^ swz(i * kBinThreads)];
 }
@@ -302,24 +327,34 @@ static BinPass make_bin_pass(const FactorSet& f, const BinGroup& gr, bool adjoin
 }
 
 int binary_pass_launch(const FactorSet& f, const BinGroup& gr, bool adjoint, const double2* x, double2* r,
-                       cudaStream_t stream) {
+                       cudaStream_t stream, bool unit) {
   const BinPass bp = make_bin_pass(f, gr, adjoint);
-  smem_optin(binary_pass_kernel, 4096 * 16);
   const int64_t tiles = bp.n_runs * bp.O;
-  binary_pass_kernel<<<(unsigned)tiles, kBinThreads, 4096 * 16, stream>>>(bp, x, r);
+  if (unit) {
+    smem_optin(binary_pass_kernel<true>, 4096 * 16);
+    binary_pass_kernel<true><<<(unsigned)tiles, kBinThreads, 4096 * 16, stream>>>(bp, x, r);
+  } else {
+    smem_optin(binary_pass_kernel<false>, 4096 * 16);
+    binary_pass_kernel<false><<<(unsigned)tiles, kBinThreads, 4096 * 16, stream>>>(bp, x, r);
+  }
   NDS_LAUNCH_CHECK();
   return kXformDirect;
 }
 
 int binary_fused_solve_launch(const FactorSet& fwd, const FactorSet& inv, const BinGroup& gr, const double2* t_pool,
                               int n_outer, const uint16_t* wf, const int* wf_off, int levels, const double2* x,
-                              double2* r, cudaStream_t stream) {
+                              double2* r, cudaStream_t stream, const double2* unit_scales) {
   if (gr.first != 1 || gr.count != 12 || gr.logR != 0 || gr.inner != 1) throw Error(NDS_ERR_OTHER, "fused pass: not a modes-1-12 tile pass");
   const BinPass fw = make_bin_pass(fwd, gr, true);
   const BinPass iv = make_bin_pass(inv, gr, false);
-  smem_optin(binary_fused_solve_kernel, 4096 * 16);
-  BinTileSolve ts{t_pool, n_outer, wf, wf_off, levels};
-  binary_fused_solve_kernel<<<(unsigned)gr.outer, kBinThreads, 4096 * 16, stream>>>(fw, iv, ts, x, r);
+  BinTileSolve ts{t_pool, unit_scales, n_outer, wf, wf_off, levels};
+  if (unit_scales) {
+    smem_optin(binary_fused_solve_kernel<true>, 4096 * 16);
+    binary_fused_solve_kernel<true><<<(unsigned)gr.outer, kBinThreads, 4096 * 16, stream>>>(fw, iv, ts, x, r);
+  } else {
+    smem_optin(binary_fused_solve_kernel<false>, 4096 * 16);
+    binary_fused_solve_kernel<false><<<(unsigned)gr.outer, kBinThreads, 4096 * 16, stream>>>(fw, iv, ts, x, r);
+  }
   NDS_LAUNCH_CHECK();
   return kBacksubLevel;
 }

@@ -90,6 +90,15 @@ struct nds_plan {
   nds::FactorSet fd;
   double2* fd_buf = nullptr;
   const double2* bin_t = nullptr;       // T'_j of the route (2 x 2 column-major, all modes)
+  // Normalised form of the route's factors (execute_fused_binary only): forward factor of mode j
+  // = diag(f_j) [[1, p], [q, 1]], inverse = [[1, p'], [q', 1]] diag(g_j); fn holds the
+  // unit-diagonal matrices (column-major slots only), bin_e the scales (f_j g_j)[0], [1] per mode,
+  // bin_tn = T'_j with the coupling scaled by g_j[0] / g_j[1]. Off (bin_norm false) when a
+  // diagonal entry of some factor is tiny against the matrix.
+  bool bin_norm = false;
+  nds::FactorSet fn;
+  const double2* bin_e = nullptr;
+  const double2* bin_tn = nullptr;
   const uint16_t* bin_wf = nullptr;     // tile wavefront over the coupled inner modes
   const int* bin_wf_off = nullptr;
   int bin_wf_levels = 0;
@@ -629,18 +638,22 @@ void plan_binary_diag(nds_plan* p, const nds_z* const* u, const nds_z* const* t)
   // T'_j (2 x 2 column-major, all modes: diagonal for the diagonalised ones); then the tile
   // wavefront: entries by popcount over the coupled inner modes, highest first, bank-interleaved
   std::vector<double2> host((size_t)N * 16 + (size_t)N * 4);
+  // normalised forms: [fwd unit matrix, column-major (4) | inv unit matrix (4)] per mode, then the
+  // scales e_j (2 per mode), then T'_j with the scaled coupling (4 per mode)
+  std::vector<double2> hostn((size_t)N * 14);
+  bool norm_ok = true;
+  auto d2 = [](cx v) { return make_double2(v.real(), v.imag()); };
   for (int j = 0; j < N; ++j) {
     double2* tp = host.data() + (size_t)N * 16 + 4 * j;
     for (int e = 0; e < 4; ++e) tp[e] = make_double2(t[j][e].re, t[j][e].im);
-    if (!diag[j]) continue;
-    tp[2] = make_double2(0.0, 0.0);
     cx U[2][2], UH[2][2], Wf[2][2], Wi[2][2];
     for (int r = 0; r < 2; ++r)
       for (int c = 0; c < 2; ++c) {
         U[r][c] = z(u[j][r + 2 * c]);
         UH[c][r] = std::conj(U[r][c]);
       }
-    const cx b = beta[j];
+    const cx b = diag[j] ? beta[j] : cx(0.0, 0.0);
+    if (diag[j]) tp[2] = make_double2(0.0, 0.0);
     // V^{-1} = [[1, -b], [0, 1]]: row 0 of W_fwd = UH row 0 - b UH row 1
     for (int c = 0; c < 2; ++c) {
       Wf[0][c] = UH[0][c] - b * UH[1][c];
@@ -651,6 +664,37 @@ void plan_binary_diag(nds_plan* p, const nds_z* const* u, const nds_z* const* t)
       Wi[r][0] = U[r][0];
       Wi[r][1] = U[r][1] + b * U[r][0];
     }
+    {
+      // W_fwd = diag(f) [[1, p], [q, 1]] (row scales), W_inv = [[1, p'], [q', 1]] diag(g) (column
+      // scales); refused when a diagonal entry is tiny against its matrix
+      double mf = 0.0, mi = 0.0;
+      for (int r = 0; r < 2; ++r)
+        for (int c = 0; c < 2; ++c) {
+          mf = std::max(mf, std::abs(Wf[r][c]));
+          mi = std::max(mi, std::abs(Wi[r][c]));
+        }
+      const cx f0 = Wf[0][0], f1 = Wf[1][1], g0 = Wi[0][0], g1 = Wi[1][1];
+      if (!(std::abs(f0) >= 1e-3 * mf && std::abs(f1) >= 1e-3 * mf && std::abs(g0) >= 1e-3 * mi &&
+            std::abs(g1) >= 1e-3 * mi)) {
+        norm_ok = false;
+      } else {
+        double2* nf = hostn.data() + (size_t)j * 8;
+        nf[0] = nf[3] = make_double2(1.0, 0.0);
+        nf[2] = d2(Wf[0][1] / f0);  // (0,1), column-major
+        nf[1] = d2(Wf[1][0] / f1);  // (1,0)
+        double2* ni = nf + 4;
+        ni[0] = ni[3] = make_double2(1.0, 0.0);
+        ni[2] = d2(Wi[0][1] / g1);
+        ni[1] = d2(Wi[1][0] / g0);
+        double2* es = hostn.data() + (size_t)N * 8 + 2 * j;
+        es[0] = d2(f0 * g0);
+        es[1] = d2(f1 * g1);
+        double2* tn = hostn.data() + (size_t)N * 10 + 4 * j;
+        for (int e = 0; e < 4; ++e) tn[e] = tp[e];
+        tn[2] = d2(cx(tp[2].x, tp[2].y) * g0 / g1);
+      }
+    }
+    if (!diag[j]) continue;
     double2* o = host.data() + (size_t)j * 16;
     for (int r = 0; r < 2; ++r)
       for (int c = 0; c < 2; ++c) {
@@ -699,8 +743,25 @@ void plan_binary_diag(nds_plan* p, const nds_z* const* u, const nds_z* const* t)
   nds::ParamBlob pb;
   pb.count = (int)host.size();
   std::memcpy(pb.v, host.data(), host.size() * sizeof(double2));
-  NDS_CUDA(cudaMallocFromPoolAsync((void**)&p->fd_buf, host.size() * sizeof(double2), p->ctx->pool, p->ctx->stream));
+  NDS_CUDA(cudaMallocFromPoolAsync((void**)&p->fd_buf, (host.size() + hostn.size()) * sizeof(double2), p->ctx->pool,
+                                   p->ctx->stream));
   nds::param_blob_launch(pb, p->fd_buf, p->ctx->stream);
+  p->bin_norm = norm_ok;
+  if (norm_ok) {  // (used only by execute_fused_binary, where every pass is a binary group)
+    pb.count = (int)hostn.size();
+    std::memcpy(pb.v, hostn.data(), hostn.size() * sizeof(double2));
+    double2* nb = p->fd_buf + host.size();
+    nds::param_blob_launch(pb, nb, p->ctx->stream);
+    p->fn = p->f;
+    p->fn.pool = nullptr;  // owned by f
+    for (int j = 0; j < N; ++j) {
+      p->fn.u_row[j] = p->fn.uh_row[j] = nullptr;  // the binary passes read the column-major slots only
+      p->fn.uh_col[j] = nb + (size_t)j * 8;
+      p->fn.u_col[j] = nb + (size_t)j * 8 + 4;
+    }
+    p->bin_e = nb + (size_t)N * 8;
+    p->bin_tn = nb + (size_t)N * 10;
+  }
   p->fd = p->f;
   p->fd.pool = nullptr;  // owned by f
   for (int j = 0; j < N; ++j) {
@@ -949,9 +1010,17 @@ int execute_fused_binary(nds_plan* p, const std::vector<XPass>& passes, const do
   if (rec) rec->mark(s, -1, 0);
   const double2* src = b;
   int k = 0, launches = 0;
+  // normalised factors (unit-diagonal butterflies, scales applied by the fused kernel) when the
+  // plan built them
+  bool norm = p->bin_norm;
+  for (const XPass& ps : passes) norm = norm && ps.group >= 0;
+  auto outer_pass = [&](const XPass& ps, bool adjoint, const double2* from, double2* to) {
+    return norm ? nds::binary_pass_launch(p->fn, p->groups[ps.group], adjoint, from, to, s, true)
+                                        : launch_pass(p, ps, adjoint, from, to, true);
+  };
   for (int j = 2; j <= np; ++j) {
     double2* dst = dst_of(++k);
-    const int kind = launch_pass(p, passes[j - 1], true, src, dst, true);
+    const int kind = outer_pass(passes[j - 1], true, src, dst);
     if (rec) rec->mark(s, kind, -passes[j - 1].mode);
     ++launches;
     src = dst;
@@ -960,9 +1029,11 @@ int execute_fused_binary(nds_plan* p, const std::vector<XPass>& passes, const do
   {
     double2* dst = dst_of(++k);
     const nds::BinarySolvePlan& bp = p->solver->bsp;
-    const int kind = nds::binary_fused_solve_launch(p->fd, p->fd, p->groups[passes.front().group], p->bin_t,
-                                                    bp.n_outer, p->bin_wf, p->bin_wf_off, p->bin_wf_levels, src, dst,
-                                                    s);
+    const nds::FactorSet& ff = norm ? p->fn : p->fd;
+    const int kind = nds::binary_fused_solve_launch(ff, ff, p->groups[passes.front().group],
+                                                    norm ? p->bin_tn : p->bin_t, bp.n_outer, p->bin_wf,
+                                                    p->bin_wf_off, p->bin_wf_levels, src, dst, s,
+                                                    norm ? p->bin_e : nullptr);
     if (rec) rec->mark(s, kind, 0);
     ++launches;
     src = dst;
@@ -970,7 +1041,7 @@ int execute_fused_binary(nds_plan* p, const std::vector<XPass>& passes, const do
   if (ev) NDS_CUDA(cudaEventRecord(ev[2], s));
   for (int j = np; j >= 2; --j) {
     double2* dst = dst_of(++k);
-    const int kind = launch_pass(p, passes[j - 1], false, src, dst, true);
+    const int kind = outer_pass(passes[j - 1], false, src, dst);
     if (rec) rec->mark(s, kind, passes[j - 1].mode);
     ++launches;
     src = dst;

@@ -67,8 +67,10 @@ struct BinGroup {
 };
 // Fused groups of runs of binary modes among modes [lo, hi) (0-based; hi < 0: all modes).
 std::vector<BinGroup> plan_binary_groups(int n_modes, const int64_t* dims, int lo = 0, int hi = -1);
+// unit: f's matrices for these modes are unit-diagonal [[1, p], [q, 1]] (the normalised factors
+// of the fused all-binary route; their diagonal parts are applied by the fused tile kernel).
 int binary_pass_launch(const FactorSet& f, const BinGroup& gr, bool adjoint, const double2* x, double2* r,
-                       cudaStream_t stream);
+                       cudaStream_t stream, bool unit = false);
 // Modes 1-12 forward (fwd's U^H), the decoupled 12-mode tile solve (den over all modes; the
 // outer modes' coupling diagonalised away), modes 1-12 inverse (inv's U) — one kernel, one read
 // and one write of the tensor; gr is the modes-1-12 pass (first 1, count 12, inner 1).
@@ -76,7 +78,10 @@ int binary_pass_launch(const FactorSet& f, const BinGroup& gr, bool adjoint, con
 // entries by popcount over the coupled inner modes (levels = their count + 1).
 int binary_fused_solve_launch(const FactorSet& fwd, const FactorSet& inv, const BinGroup& gr, const double2* t_pool,
                               int n_outer, const uint16_t* wf, const int* wf_off, int levels, const double2* x,
-                              double2* r, cudaStream_t stream);
+                              double2* r, cudaStream_t stream, const double2* unit_scales = nullptr);
+// unit_scales != nullptr: the normalised route — fwd / inv hold unit-diagonal matrices for all
+// modes, unit_scales the deferred diagonal scale e_j[0], e_j[1] of every mode (2 per mode), and
+// t_pool's couplings carry the inverse factors' column-scale ratio (binary_pass.cu).
 
 // Plain matrix variant (apply_operator / residual): m_row, m_col are the two layouts of M.
 // rows_out > 0: rectangular M (rows_out x n), r has extent rows_out along the mode.
