@@ -11,6 +11,9 @@
 // modes: each thread gathers the 2^4 entries spanning the round's modes into registers, applies
 // the 2x2 matrices as butterflies, and scatters back. Modes commute (test_kernels.cpp:91-99), so
 // the grouping changes rounding only.
+#include <algorithm>
+#include <vector>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -29,17 +32,49 @@ struct BinPass {
   int tb[3][12];   // tile bits carried by the thread index (and slot index) in each round
   int rsw[3][16];  // swz(round bits of entry e): swz is linear over XOR, so swz(p0 | bits_e) =
                    // swz(p0) ^ rsw[e] — one XOR per access instead of the full swizzle
+  int64_t gbit[12];      // global offset of tile bit b (run bits: 2^b; group bit q: I 2^q)
   const double2* M[12];  // 2x2 column-major op(U_j) per group mode
 };
 
 __host__ __device__ __forceinline__ constexpr int swz(int p) { return p ^ (((p >> 3) ^ (p >> 6) ^ (p >> 9)) & 7); }
 
+// Where a round reads / writes the tile: the first round of a pass gathers straight from global
+// memory (its thread bits are the lowest tile bits, so a warp reads whole 128-byte runs) and the
+// last one scatters straight to it — the tile crosses shared memory only between rounds.
+enum : int { kIoShared = 0, kSrcGlobal = 1, kDstGlobal = 2 };
+
+template <int NB, bool UNIT>
+__device__ __forceinline__ void bin_butterflies(const int (&rbit)[NB], int logR, const double2 (*Mq)[4],
+                                                double2 (&v)[1 << NB]) {
+  constexpr int V = 1 << NB;
+#pragma unroll
+  for (int q = 0; q < NB; ++q) {
+    const int mode = rbit[q] - logR;
+    const double2 m00 = Mq[mode][0], m10 = Mq[mode][1], m01 = Mq[mode][2], m11 = Mq[mode][3];
+#pragma unroll
+    for (int e = 0; e < V; ++e) {
+      if (!((e >> q) & 1)) {
+        const double2 a = v[e], b = v[e | (1 << q)];
+        if (UNIT) {
+          v[e] = cfma(a, m01, b);
+          v[e | (1 << q)] = cfma(b, m10, a);
+        } else {
+          v[e] = cfma(cmul(m00, a), m01, b);
+          v[e | (1 << q)] = cfma(cmul(m10, a), m11, b);
+        }
+      }
+    }
+  }
+}
+
 // One round: each thread slot gathers the 2^NB entries spanning the round's NB group modes,
 // applies the NB 2x2 matrices as butterflies in registers, and scatters them back.
 // UNIT: the matrices are unit-diagonal ([[1, p], [q, 1]], the normalised factors of the fused
-// route — four FMAs per output instead of eight).
-template <int NB, bool UNIT = false>
-__device__ __forceinline__ void bin_round(const BinPass& bp, int rd, double2* S, const double2 (*Mq)[4], int tid) {
+// route — four FMAs per output instead of eight). SYNC: a CTA barrier between the first slot's
+// loads and its butterflies (publishes Mq written just before the call).
+template <int NB, bool UNIT, int IO, bool SYNC = false>
+__device__ __forceinline__ void bin_round(const BinPass& bp, int rd, double2* S, const double2 (*Mq)[4], int tid,
+                                          const double2* __restrict__ gin = nullptr, double2* __restrict__ gout = nullptr) {
   constexpr int V = 1 << NB;
   int rbit[NB];
 #pragma unroll
@@ -47,57 +82,72 @@ __device__ __forceinline__ void bin_round(const BinPass& bp, int rd, double2* S,
   // slot s = tid + 256 j: its tile position p0(s) = p0(tid) ^ p0(256 j) (disjoint bits), and
   // swz is linear, so swz(p0(s)) = swz(p0(tid)) ^ swz(p0(256 j)) — the thread part once per round
   int p0t = 0;
+  int64_t g0t = 0;
 #pragma unroll
-  for (int i = 0; i < 8 && i < 12 - NB; ++i) p0t |= ((tid >> i) & 1) << bp.tb[rd][i];
+  for (int i = 0; i < 8 && i < 12 - NB; ++i) {
+    const int bit = (tid >> i) & 1;
+    p0t |= bit << bp.tb[rd][i];
+    if (IO != kIoShared && bit) g0t += bp.gbit[bp.tb[rd][i]];
+  }
   const int spt = swz(p0t);
-  for (int s = tid; s < (4096 >> NB); s += kBinThreads) {
-    int p0j = 0;
-#pragma unroll
-    for (int i = 8; i < 12 - NB; ++i) p0j |= ((s >> i) & 1) << bp.tb[rd][i];
-    const int sp0 = spt ^ swz(p0j);
-    int addr[V];
-    double2 v[V];
+  int64_t ge[V];
+  if (IO != kIoShared) {
 #pragma unroll
     for (int e = 0; e < V; ++e) {
-      addr[e] = sp0 ^ bp.rsw[rd][e];
-      v[e] = S[addr[e]];
+      ge[e] = 0;
+#pragma unroll
+      for (int q = 0; q < NB; ++q)
+        if ((e >> q) & 1) ge[e] += bp.gbit[rbit[q]];
     }
+  }
+  for (int s = tid; s < (4096 >> NB); s += kBinThreads) {
+    int p0j = 0;
+    int64_t g0 = g0t;
 #pragma unroll
-    for (int q = 0; q < NB; ++q) {
-      const int mode = rbit[q] - bp.logR;
-      const double2 m00 = Mq[mode][0], m10 = Mq[mode][1], m01 = Mq[mode][2], m11 = Mq[mode][3];
-#pragma unroll
-      for (int e = 0; e < V; ++e) {
-        if (!((e >> q) & 1)) {
-          const double2 a = v[e], b = v[e | (1 << q)];
-          if (UNIT) {
-            v[e] = cfma(a, m01, b);
-            v[e | (1 << q)] = cfma(b, m10, a);
-          } else {
-            v[e] = cfma(cmul(m00, a), m01, b);
-            v[e | (1 << q)] = cfma(cmul(m10, a), m11, b);
-          }
-        }
-      }
+    for (int i = 8; i < 12 - NB; ++i) {
+      const int bit = (s >> i) & 1;
+      p0j |= bit << bp.tb[rd][i];
+      if (IO != kIoShared && bit) g0 += bp.gbit[bp.tb[rd][i]];
     }
+    const int sp0 = spt ^ swz(p0j);
+    double2 v[V];
 #pragma unroll
-    for (int e = 0; e < V; ++e) S[addr[e]] = v[e];
+    for (int e = 0; e < V; ++e) v[e] = (IO & kSrcGlobal) ? gin[g0 + ge[e]] : S[sp0 ^ bp.rsw[rd][e]];
+    if (SYNC && s == tid) __syncthreads();
+    bin_butterflies<NB, UNIT>(rbit, bp.logR, Mq, v);
+#pragma unroll
+    for (int e = 0; e < V; ++e) {
+      if (IO & kDstGlobal)
+        gout[g0 + ge[e]] = v[e];
+      else
+        S[sp0 ^ bp.rsw[rd][e]] = v[e];
+    }
   }
 }
 
+template <bool UNIT, int IO, bool SYNC = false>
+__device__ __forceinline__ void bin_round_any(const BinPass& bp, int rd, double2* S, const double2 (*Mq)[4], int tid,
+                                              const double2* __restrict__ gin = nullptr,
+                                              double2* __restrict__ gout = nullptr) {
+  switch (bp.nrb[rd]) {
+    case 4: bin_round<4, UNIT, IO, SYNC>(bp, rd, S, Mq, tid, gin, gout); break;
+    case 3: bin_round<3, UNIT, IO, SYNC>(bp, rd, S, Mq, tid, gin, gout); break;
+    case 2: bin_round<2, UNIT, IO, SYNC>(bp, rd, S, Mq, tid, gin, gout); break;
+    default: bin_round<1, UNIT, IO, SYNC>(bp, rd, S, Mq, tid, gin, gout); break;
+  }
+}
+
+// All rounds of a tile staged in shared memory (the coupled fused kernel below).
 template <bool UNIT>
 __device__ __forceinline__ void bin_rounds(const BinPass& bp, double2* S, const double2 (*Mq)[4], int tid) {
   for (int rd = 0; rd < bp.rounds; ++rd) {
-    switch (bp.nrb[rd]) {
-      case 4: bin_round<4, UNIT>(bp, rd, S, Mq, tid); break;
-      case 3: bin_round<3, UNIT>(bp, rd, S, Mq, tid); break;
-      case 2: bin_round<2, UNIT>(bp, rd, S, Mq, tid); break;
-      default: bin_round<1, UNIT>(bp, rd, S, Mq, tid); break;
-    }
+    bin_round_any<UNIT, kIoShared>(bp, rd, S, Mq, tid);
     __syncthreads();
   }
 }
 
+// A pass: round 0 global -> shared, middle rounds in shared memory, the last one shared -> global
+// (a single round: global -> global, no shared memory at all).
 template <bool UNIT>
 __global__ void __launch_bounds__(kBinThreads, 2) binary_pass_kernel(const BinPass bp, const double2* __restrict__ x,
                                                                   double2* __restrict__ r) {
@@ -108,31 +158,18 @@ __global__ void __launch_bounds__(kBinThreads, 2) binary_pass_kernel(const BinPa
   const int64_t tile = blockIdx.x;
   const int64_t run = tile % bp.n_runs;
   const int64_t o = tile / bp.n_runs;
-  const int R = 1 << bp.logR;
-  const int64_t base = run * R + bp.I * ((int64_t)1 << bp.k) * o;
-  // global -> shared (coalesced along runs of R entries): 8 loads of a thread in flight at a time.
-  // p = tid + i * 256 with tid < 256: swz(p) = swz(tid) ^ swz(i * 256) (constant), and for
-  // R <= 256 the global offset is the thread's own plus i * I * (256 / R)
-  const int stid = swz(tid);
-  const bool small_r = bp.logR <= 8;
-  const int64_t gt = base + (tid & (R - 1)) + bp.I * (tid >> bp.logR);
-  const int64_t gstep = small_r ? bp.I * (kBinThreads >> bp.logR) : 0;
-  auto goff = [&](int i) {
-    const int p = tid + i * kBinThreads;
-    return small_r ? gt + i * gstep : base + (p & (R - 1)) + bp.I * (p >> bp.logR);
-  };
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    double2 v[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) v[i] = x[goff(h * 8 + i)];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) S[stid ^ swz((h * 8 + i) * kBinThreads)] = v[i];
+  const int64_t base = (run << bp.logR) + bp.I * ((int64_t)1 << bp.k) * o;
+  if (bp.rounds == 1) {
+    bin_round_any<UNIT, kSrcGlobal | kDstGlobal, true>(bp, 0, S, Mq, tid, x + base, r + base);
+    return;
   }
+  bin_round_any<UNIT, kSrcGlobal, true>(bp, 0, S, Mq, tid, x + base, nullptr);
   __syncthreads();
-  bin_rounds<UNIT>(bp, S, Mq, tid);
-#pragma unroll
-  for (int i = 0; i < 4096 / kBinThreads; ++i) r[goff(i)] = S[stid ^ swz(i * kBinThreads)];
+  for (int rd = 1; rd + 1 < bp.rounds; ++rd) {
+    bin_round_any<UNIT, kIoShared>(bp, rd, S, Mq, tid);
+    __syncthreads();
+  }
+  bin_round_any<UNIT, kDstGlobal>(bp, bp.rounds - 1, S, Mq, tid, nullptr, r + base);
 }
 
 // ---- fused pass: forward modes 1-12, decoupled tile solve, inverse modes 1-12 -------------------
@@ -246,6 +283,101 @@ __global__ void __launch_bounds__(kBinThreads, 2)
   for (int i = 0; i < 4096 / kBinThreads; ++i) r[base + tid + i * kBinThreads] = S[stid ^ swz(i * kBinThreads)];
 }
 
+// ---- the same with at most four coupled inner modes: the tile solve is a round -----------------
+// When the modes left coupled fit one round (<= 4: c4 keeps 2), the round that holds them (C)
+// does forward butterflies, the triangular solve of its 16 entries (descending, all couplings
+// are inside the thread's registers) and the inverse butterflies in one visit; round A (the
+// highest remaining bits) gathers from / scatters to global memory, so the tile crosses shared
+// memory four times in all (A -> B -> C -> B -> A) instead of once per round and once per
+// wavefront level. Rounds: 0 = A, 1 = B, 2 = C in fw and iv (same bits, different matrices).
+struct BinRoundSolve {
+  const double2* t;  // T'_j (2 x 2 column-major) at t + 4 j, all N modes (couplings pre-scaled if UNIT)
+  const double2* e;  // UNIT: the deferred scales e_j[0], e_j[1] at e + 2 j
+  int n_outer;       // N - 12
+  int cpl;           // bit q: round-C bit q is a coupled mode
+};
+
+template <bool UNIT>
+__global__ void __launch_bounds__(kBinThreads, 2)
+    binary_fused_round_kernel(const BinPass fw, const BinPass iv, const BinRoundSolve ts, const double2* __restrict__ x,
+                              double2* __restrict__ r) {
+  extern __shared__ __align__(16) double2 S[];  // 4096 entries, swizzled (swz)
+  __shared__ double2 Mqf[12][4], Mqi[12][4];
+  __shared__ double2 t01[4], dround[16], eround[16];
+  __shared__ double2 dout, eout;
+  const int tid = threadIdx.x;
+  const int64_t tile = blockIdx.x;  // outer index (modes 13..N)
+  const int64_t base = tile << 12;
+  if (tid < 48) {
+    Mqf[tid >> 2][tid & 3] = fw.M[tid >> 2][tid & 3];
+  } else if (tid < 96) {
+    const int e = tid - 48;
+    Mqi[e >> 2][e & 3] = iv.M[e >> 2][e & 3];
+  } else if (tid < 100) {
+    t01[tid - 96] = ts.t[4 * fw.rb[2][tid - 96] + 2];
+  } else if (tid < 116) {
+    const int e = tid - 100;
+    double2 d = make_double2(0.0, 0.0), sc = make_double2(1.0, 0.0);
+    for (int q = 0; q < 4; ++q) {
+      const int j = fw.rb[2][q], bit = (e >> q) & 1;
+      d = cadd(d, ts.t[4 * j + (bit ? 3 : 0)]);
+      if (UNIT) sc = cmul(sc, ts.e[2 * j + bit]);
+    }
+    dround[e] = d;
+    eround[e] = sc;
+  } else if (tid == 128) {
+    double2 d = make_double2(0.0, 0.0), sc = make_double2(1.0, 0.0);
+    for (int q = 0; q < ts.n_outer; ++q) {
+      const int bit = (int)((tile >> q) & 1);
+      d = cadd(d, ts.t[4 * (12 + q) + (bit ? 3 : 0)]);
+      if (UNIT) sc = cmul(sc, ts.e[2 * (12 + q) + bit]);
+    }
+    dout = d;
+    eout = sc;
+  }
+  bin_round<4, UNIT, kSrcGlobal, true>(fw, 0, S, Mqf, tid, x + base, nullptr);
+  __syncthreads();
+  bin_round<4, UNIT, kIoShared>(fw, 1, S, Mqf, tid);
+  // the thread's part of den and of the scale: the 8 tile bits outside round C + the outer modes
+  double2 dfix = dout, efix = eout;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int j = fw.tb[2][i], bit = (tid >> i) & 1;
+    dfix = cadd(dfix, ts.t[4 * j + (bit ? 3 : 0)]);
+    if (UNIT) efix = cmul(efix, ts.e[2 * j + bit]);
+  }
+  __syncthreads();
+  {
+    int rbit[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) rbit[q] = fw.rb[2][q];
+    int p0 = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) p0 |= ((tid >> i) & 1) << fw.tb[2][i];
+    const int sp0 = swz(p0);
+    double2 v[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) v[e] = S[sp0 ^ fw.rsw[2][e]];
+    bin_butterflies<4, UNIT>(rbit, 0, Mqf, v);
+#pragma unroll
+    for (int e = 15; e >= 0; --e) {
+      double2 n = v[e];
+      if (UNIT) n = cmul(cmul(efix, eround[e]), n);
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (!((e >> q) & 1) && ((ts.cpl >> q) & 1)) n = cfms(n, t01[q], v[e | (1 << q)]);
+      v[e] = cmul(n, crecip_fast(cadd(dfix, dround[e])));
+    }
+    bin_butterflies<4, UNIT>(rbit, 0, Mqi, v);
+#pragma unroll
+    for (int e = 0; e < 16; ++e) S[sp0 ^ fw.rsw[2][e]] = v[e];
+  }
+  __syncthreads();
+  bin_round<4, UNIT, kIoShared>(iv, 1, S, Mqi, tid);
+  __syncthreads();
+  bin_round<4, UNIT, kDstGlobal>(iv, 0, S, Mqi, tid, nullptr, r + base);
+}
+
 // Plan the passes over [mode0, mode1) (1-based, all n_j = 2): greedily take as many binary modes
 // as fit a 4096-entry tile with runs of min(I, 8..4096) entries.
 std::vector<BinGroup> plan_binary_groups(int n_modes, const int64_t* dims, int lo, int hi) {
@@ -284,7 +416,12 @@ std::vector<BinGroup> plan_binary_groups(int n_modes, const int64_t* dims, int l
   return out;
 }
 
-static BinPass make_bin_pass(const FactorSet& f, const BinGroup& gr, bool adjoint) {
+// rounds: the tile bits of each round (<= 4 each, all group bits exactly once); ascending[rd]:
+// thread bits in ascending tile-bit order (rounds that touch global memory: a warp covers the
+// lowest tile bits, i.e. whole runs), otherwise the first three with distinct residues mod 3
+// where possible (conflict-free shared-memory phases under swz).
+static BinPass make_bin_pass(const FactorSet& f, const BinGroup& gr, bool adjoint,
+                             const std::vector<std::vector<int>>& rounds, const std::vector<bool>& ascending) {
   BinPass bp{};
   bp.I = gr.inner;
   bp.O = gr.outer;
@@ -292,28 +429,28 @@ static BinPass make_bin_pass(const FactorSet& f, const BinGroup& gr, bool adjoin
   bp.k = gr.count;
   bp.n_runs = gr.inner >> gr.logR;
   for (int q = 0; q < gr.count; ++q) bp.M[q] = adjoint ? f.uh_col[gr.first - 1 + q] : f.u_col[gr.first - 1 + q];
-  // rounds of <= 4 group bits; thread bits: the remaining tile bits, first three with distinct
-  // residues mod 3 where possible (conflict-free shared-memory phases under swz)
-  bp.rounds = (gr.count + 3) / 4;
+  for (int b = 0; b < 12; ++b) bp.gbit[b] = b < gr.logR ? (int64_t)1 << b : gr.inner << (b - gr.logR);
+  bp.rounds = (int)rounds.size();
   for (int rd = 0; rd < bp.rounds; ++rd) {
-    const int nb = std::min(4, gr.count - 4 * rd);
+    const int nb = (int)rounds[rd].size();
     bp.nrb[rd] = nb;
     bool used[12] = {};
     for (int q = 0; q < nb; ++q) {
-      bp.rb[rd][q] = gr.logR + 4 * rd + q;
+      bp.rb[rd][q] = rounds[rd][q];
       used[bp.rb[rd][q]] = true;
     }
     std::vector<int> rest;
     for (int b = 0; b < 12; ++b)
       if (!used[b]) rest.push_back(b);
     std::vector<int> order;
-    for (int want = 0; want < 3; ++want)
-      for (size_t i = 0; i < rest.size(); ++i)
-        if (rest[i] >= 0 && rest[i] % 3 == want) {
-          order.push_back(rest[i]);
-          rest[i] = -1;
-          break;
-        }
+    if (!ascending[rd])
+      for (int want = 0; want < 3; ++want)
+        for (size_t i = 0; i < rest.size(); ++i)
+          if (rest[i] >= 0 && rest[i] % 3 == want) {
+            order.push_back(rest[i]);
+            rest[i] = -1;
+            break;
+          }
     for (int b : rest)
       if (b >= 0) order.push_back(b);
     for (size_t i = 0; i < order.size(); ++i) bp.tb[rd][i] = order[i];
@@ -326,9 +463,43 @@ static BinPass make_bin_pass(const FactorSet& f, const BinGroup& gr, bool adjoin
   return bp;
 }
 
+// Rounds of consecutive group bits, all staged in shared memory.
+static BinPass make_bin_pass_staged(const FactorSet& f, const BinGroup& gr, bool adjoint) {
+  std::vector<std::vector<int>> rounds;
+  for (int b = 0; b < gr.count; b += 4) {
+    rounds.emplace_back();
+    for (int q = b; q < std::min(b + 4, gr.count); ++q) rounds.back().push_back(gr.logR + q);
+  }
+  return make_bin_pass(f, gr, adjoint, rounds, std::vector<bool>(rounds.size(), false));
+}
+
+// A pass of its own: the first round (global -> shared) takes the highest group bits, the last
+// (shared -> global) the lowest, a middle one the rest.
+static BinPass make_bin_pass_streamed(const FactorSet& f, const BinGroup& gr, bool adjoint) {
+  const int k = gr.count, lo = gr.logR;
+  std::vector<std::vector<int>> rounds;
+  auto range = [&](int a, int b) {  // group bits [a, b)
+    rounds.emplace_back();
+    for (int q = a; q < b; ++q) rounds.back().push_back(lo + q);
+  };
+  if (k <= 4) {
+    range(0, k);
+  } else if (k <= 8) {
+    range(k - 4, k);
+    range(0, k - 4);
+  } else {
+    range(k - 4, k);
+    range(4, k - 4);
+    range(0, 4);
+  }
+  std::vector<bool> asc(rounds.size(), false);
+  asc.front() = asc.back() = true;
+  return make_bin_pass(f, gr, adjoint, rounds, asc);
+}
+
 int binary_pass_launch(const FactorSet& f, const BinGroup& gr, bool adjoint, const double2* x, double2* r,
                        cudaStream_t stream, bool unit) {
-  const BinPass bp = make_bin_pass(f, gr, adjoint);
+  const BinPass bp = make_bin_pass_streamed(f, gr, adjoint);
   const int64_t tiles = bp.n_runs * bp.O;
   if (unit) {
     smem_optin(binary_pass_kernel<true>, 4096 * 16);
@@ -342,11 +513,42 @@ int binary_pass_launch(const FactorSet& f, const BinGroup& gr, bool adjoint, con
 }
 
 int binary_fused_solve_launch(const FactorSet& fwd, const FactorSet& inv, const BinGroup& gr, const double2* t_pool,
-                              int n_outer, const uint16_t* wf, const int* wf_off, int levels, const double2* x,
-                              double2* r, cudaStream_t stream, const double2* unit_scales) {
+                              int n_outer, const uint16_t* wf, const int* wf_off, int levels, int cmask,
+                              const double2* x, double2* r, cudaStream_t stream, const double2* unit_scales) {
   if (gr.first != 1 || gr.count != 12 || gr.logR != 0 || gr.inner != 1) throw Error(NDS_ERR_OTHER, "fused pass: not a modes-1-12 tile pass");
-  const BinPass fw = make_bin_pass(fwd, gr, true);
-  const BinPass iv = make_bin_pass(inv, gr, false);
+  if (__builtin_popcount(cmask) <= 4) {
+    // round C = the coupled bits, filled up with the lowest other bits; A = the highest four of
+    // the rest (global side), B = the other four
+    std::vector<int> c, rest;
+    for (int b = 0; b < 12; ++b)
+      if ((cmask >> b) & 1) c.push_back(b);
+    for (int b = 0; b < 12 && c.size() < 4; ++b)
+      if (!((cmask >> b) & 1)) c.push_back(b);
+    std::sort(c.begin(), c.end());
+    for (int b = 0; b < 12; ++b)
+      if (std::find(c.begin(), c.end(), b) == c.end()) rest.push_back(b);
+    const std::vector<std::vector<int>> rounds = {{rest[4], rest[5], rest[6], rest[7]},
+                                                  {rest[0], rest[1], rest[2], rest[3]},
+                                                  c};
+    const std::vector<bool> asc = {true, false, false};
+    const BinPass fw = make_bin_pass(fwd, gr, true, rounds, asc);
+    const BinPass iv = make_bin_pass(inv, gr, false, rounds, asc);
+    int cpl = 0;
+    for (int q = 0; q < 4; ++q)
+      if ((cmask >> c[q]) & 1) cpl |= 1 << q;
+    BinRoundSolve ts{t_pool, unit_scales, n_outer, cpl};
+    if (unit_scales) {
+      smem_optin(binary_fused_round_kernel<true>, 4096 * 16);
+      binary_fused_round_kernel<true><<<(unsigned)gr.outer, kBinThreads, 4096 * 16, stream>>>(fw, iv, ts, x, r);
+    } else {
+      smem_optin(binary_fused_round_kernel<false>, 4096 * 16);
+      binary_fused_round_kernel<false><<<(unsigned)gr.outer, kBinThreads, 4096 * 16, stream>>>(fw, iv, ts, x, r);
+    }
+    NDS_LAUNCH_CHECK();
+    return kBacksubLevel;
+  }
+  const BinPass fw = make_bin_pass_staged(fwd, gr, true);
+  const BinPass iv = make_bin_pass_staged(inv, gr, false);
   BinTileSolve ts{t_pool, unit_scales, n_outer, wf, wf_off, levels};
   if (unit_scales) {
     smem_optin(binary_fused_solve_kernel<true>, 4096 * 16);

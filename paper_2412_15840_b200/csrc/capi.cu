@@ -102,6 +102,7 @@ struct nds_plan {
   const uint16_t* bin_wf = nullptr;     // tile wavefront over the coupled inner modes
   const int* bin_wf_off = nullptr;
   int bin_wf_levels = 0;
+  int bin_cmask = 0;  // inner modes left coupled
   // Cubic-tile route with every T_j block-diagonalised (plan_cubic_diag): T'_j = W_j^{-1} T_j W_j,
   // W_j = blockdiag of the unit-column eigenvector matrices of T_j's B x B diagonal blocks. Full
   // solves run the passes with fc (forward W_j^{-1} U_j^H, inverse U_j W_j) and the solve on
@@ -776,6 +777,7 @@ void plan_binary_diag(nds_plan* p, const nds_z* const* u, const nds_z* const* t)
   p->bin_wf = (const uint16_t*)wbuf;
   p->bin_wf_off = (const int*)((const char*)wbuf + E * sizeof(uint16_t));
   p->bin_wf_levels = k + 1;
+  p->bin_cmask = cmask;
   p->bin_diag = true;
 }
 
@@ -1032,7 +1034,7 @@ int execute_fused_binary(nds_plan* p, const std::vector<XPass>& passes, const do
     const nds::FactorSet& ff = norm ? p->fn : p->fd;
     const int kind = nds::binary_fused_solve_launch(ff, ff, p->groups[passes.front().group],
                                                     norm ? p->bin_tn : p->bin_t, bp.n_outer, p->bin_wf,
-                                                    p->bin_wf_off, p->bin_wf_levels, src, dst, s,
+                                                    p->bin_wf_off, p->bin_wf_levels, p->bin_cmask, src, dst, s,
                                                     norm ? p->bin_e : nullptr);
     if (rec) rec->mark(s, kind, 0);
     ++launches;

@@ -77,8 +77,12 @@ int binary_pass_launch(const FactorSet& f, const BinGroup& gr, bool adjoint, con
 // t_pool: T'_j (2 x 2, all N modes; diagonal for the diagonalised ones), wf / wf_off: the tile
 // entries by popcount over the coupled inner modes (levels = their count + 1).
 int binary_fused_solve_launch(const FactorSet& fwd, const FactorSet& inv, const BinGroup& gr, const double2* t_pool,
-                              int n_outer, const uint16_t* wf, const int* wf_off, int levels, const double2* x,
-                              double2* r, cudaStream_t stream, const double2* unit_scales = nullptr);
+                              int n_outer, const uint16_t* wf, const int* wf_off, int levels, int cmask,
+                              const double2* x, double2* r, cudaStream_t stream,
+                              const double2* unit_scales = nullptr);
+// cmask: the inner modes left coupled (bit j = mode j + 1). Up to four: the tile solve is one
+// round of the butterfly network (binary_fused_round_kernel; wf unused); more: the popcount
+// wavefront kernel.
 // unit_scales != nullptr: the normalised route — fwd / inv hold unit-diagonal matrices for all
 // modes, unit_scales the deferred diagonal scale e_j[0], e_j[1] of every mode (2 per mode), and
 // t_pool's couplings carry the inverse factors' column-scale ratio (binary_pass.cu).
