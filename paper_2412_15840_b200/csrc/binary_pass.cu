@@ -72,10 +72,11 @@ __device__ __forceinline__ void bin_butterflies(const int (&rbit)[NB], int logR,
 // UNIT: the matrices are unit-diagonal ([[1, p], [q, 1]], the normalised factors of the fused
 // route — four FMAs per output instead of eight). SYNC: a CTA barrier between the first slot's
 // loads and its butterflies (publishes Mq written just before the call).
-template <int NB, bool UNIT, int IO, bool SYNC = false>
+template <int NB, bool UNIT, int IO, bool SYNC = false, int LOGT = 8>
 __device__ __forceinline__ void bin_round(const BinPass& bp, int rd, double2* S, const double2 (*Mq)[4], int tid,
                                           const double2* __restrict__ gin = nullptr, double2* __restrict__ gout = nullptr) {
   constexpr int V = 1 << NB;
+  constexpr int T = 1 << LOGT;  // threads of the CTA
   int rbit[NB];
 #pragma unroll
   for (int q = 0; q < NB; ++q) rbit[q] = bp.rb[rd][q];
@@ -84,7 +85,7 @@ __device__ __forceinline__ void bin_round(const BinPass& bp, int rd, double2* S,
   int p0t = 0;
   int64_t g0t = 0;
 #pragma unroll
-  for (int i = 0; i < 8 && i < 12 - NB; ++i) {
+  for (int i = 0; i < LOGT && i < 12 - NB; ++i) {
     const int bit = (tid >> i) & 1;
     p0t |= bit << bp.tb[rd][i];
     if (IO != kIoShared && bit) g0t += bp.gbit[bp.tb[rd][i]];
@@ -100,11 +101,11 @@ __device__ __forceinline__ void bin_round(const BinPass& bp, int rd, double2* S,
         if ((e >> q) & 1) ge[e] += bp.gbit[rbit[q]];
     }
   }
-  for (int s = tid; s < (4096 >> NB); s += kBinThreads) {
+  for (int s = tid; s < (4096 >> NB); s += T) {
     int p0j = 0;
     int64_t g0 = g0t;
 #pragma unroll
-    for (int i = 8; i < 12 - NB; ++i) {
+    for (int i = LOGT; i < 12 - NB; ++i) {
       const int bit = (s >> i) & 1;
       p0j |= bit << bp.tb[rd][i];
       if (IO != kIoShared && bit) g0 += bp.gbit[bp.tb[rd][i]];
@@ -297,17 +298,55 @@ struct BinRoundSolve {
   int cpl;           // bit q: round-C bit q is a coupled mode
 };
 
+// One round of the persistent kernel below on a contiguous tile: the thread's slot (one per
+// thread: 256 threads x 16 entries) is fixed per round for the whole launch, so its swizzled
+// position sp0 and tile offset p0 come precomputed.
+template <bool UNIT, int IO>
+__device__ __forceinline__ void fused_round(const BinPass& bp, int rd, double2* S, const double2 (*Mq)[4], int p0,
+                                            const double2* __restrict__ gin, double2* __restrict__ gout) {
+  const int sp0 = swz(p0);
+  int rbit[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) rbit[q] = bp.rb[rd][q];
+  double2 v[16];
+#pragma unroll
+  for (int e = 0; e < 16; ++e) {
+    if (IO & kSrcGlobal) {
+      int eb = 0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) eb |= ((e >> q) & 1) << rbit[q];
+      v[e] = gin[p0 | eb];
+    } else {
+      v[e] = S[sp0 ^ bp.rsw[rd][e]];
+    }
+  }
+  bin_butterflies<4, UNIT>(rbit, 0, Mq, v);
+#pragma unroll
+  for (int e = 0; e < 16; ++e) {
+    if (IO & kDstGlobal) {
+      int eb = 0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) eb |= ((e >> q) & 1) << rbit[q];
+      gout[p0 | eb] = v[e];
+    } else {
+      S[sp0 ^ bp.rsw[rd][e]] = v[e];
+    }
+  }
+}
+
+// Persistent: a CTA walks tiles blockIdx.x, + gridDim.x, ... (two CTAs per SM), so the factor
+// tables, the per-thread slot positions and the thread's tile-independent part of den / scale are
+// set up once per CTA; per tile only the outer modes' part (one warp, lanes over modes, shuffle
+// tree) is new.
 template <bool UNIT>
 __global__ void __launch_bounds__(kBinThreads, 2)
-    binary_fused_round_kernel(const BinPass fw, const BinPass iv, const BinRoundSolve ts, const double2* __restrict__ x,
-                              double2* __restrict__ r) {
+    binary_fused_round_kernel(const BinPass fw, const BinPass iv, const BinRoundSolve ts, int64_t n_tiles,
+                              const double2* __restrict__ x, double2* __restrict__ r) {
   extern __shared__ __align__(16) double2 S[];  // 4096 entries, swizzled (swz)
   __shared__ double2 Mqf[12][4], Mqi[12][4];
   __shared__ double2 t01[4], dround[16], eround[16];
   __shared__ double2 dout, eout;
   const int tid = threadIdx.x;
-  const int64_t tile = blockIdx.x;  // outer index (modes 13..N)
-  const int64_t base = tile << 12;
   if (tid < 48) {
     Mqf[tid >> 2][tid & 3] = fw.M[tid >> 2][tid & 3];
   } else if (tid < 96) {
@@ -325,57 +364,89 @@ __global__ void __launch_bounds__(kBinThreads, 2)
     }
     dround[e] = d;
     eround[e] = sc;
-  } else if (tid == 128) {
-    double2 d = make_double2(0.0, 0.0), sc = make_double2(1.0, 0.0);
-    for (int q = 0; q < ts.n_outer; ++q) {
-      const int bit = (int)((tile >> q) & 1);
-      d = cadd(d, ts.t[4 * (12 + q) + (bit ? 3 : 0)]);
-      if (UNIT) sc = cmul(sc, ts.e[2 * (12 + q) + bit]);
-    }
-    dout = d;
-    eout = sc;
   }
-  bin_round<4, UNIT, kSrcGlobal, true>(fw, 0, S, Mqf, tid, x + base, nullptr);
-  __syncthreads();
-  bin_round<4, UNIT, kIoShared>(fw, 1, S, Mqf, tid);
-  // the thread's part of den and of the scale: the 8 tile bits outside round C + the outer modes
-  double2 dfix = dout, efix = eout;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int j = fw.tb[2][i], bit = (tid >> i) & 1;
-    dfix = cadd(dfix, ts.t[4 * j + (bit ? 3 : 0)]);
-    if (UNIT) efix = cmul(efix, ts.e[2 * j + bit]);
-  }
-  __syncthreads();
+  // slot positions per round (A, B, C) and the tile-independent part of den / scale (the 8 tile
+  // bits outside round C): per-thread constants of the launch, parked in shared memory
+  __shared__ int slot_p0[3][kBinThreads];
+  __shared__ double2 slot_d[kBinThreads], slot_e[kBinThreads];
   {
-    int rbit[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) rbit[q] = fw.rb[2][q];
-    int p0 = 0;
+    for (int rd = 0; rd < 3; ++rd) {
+      int p = 0;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) p0 |= ((tid >> i) & 1) << fw.tb[2][i];
-    const int sp0 = swz(p0);
-    double2 v[16];
-#pragma unroll
-    for (int e = 0; e < 16; ++e) v[e] = S[sp0 ^ fw.rsw[2][e]];
-    bin_butterflies<4, UNIT>(rbit, 0, Mqf, v);
-#pragma unroll
-    for (int e = 15; e >= 0; --e) {
-      double2 n = v[e];
-      if (UNIT) n = cmul(cmul(efix, eround[e]), n);
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (!((e >> q) & 1) && ((ts.cpl >> q) & 1)) n = cfms(n, t01[q], v[e | (1 << q)]);
-      v[e] = cmul(n, crecip_fast(cadd(dfix, dround[e])));
+      for (int i = 0; i < 8; ++i) p |= ((tid >> i) & 1) << fw.tb[rd][i];
+      slot_p0[rd][tid] = p;
     }
-    bin_butterflies<4, UNIT>(rbit, 0, Mqi, v);
+    double2 d = make_double2(0.0, 0.0), sc = make_double2(1.0, 0.0);
 #pragma unroll
-    for (int e = 0; e < 16; ++e) S[sp0 ^ fw.rsw[2][e]] = v[e];
+    for (int i = 0; i < 8; ++i) {
+      const int j = fw.tb[2][i], bit = (tid >> i) & 1;
+      d = cadd(d, ts.t[4 * j + (bit ? 3 : 0)]);
+      if (UNIT) sc = cmul(sc, ts.e[2 * j + bit]);
+    }
+    slot_d[tid] = d;
+    slot_e[tid] = sc;
   }
+  int rbit[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) rbit[q] = fw.rb[2][q];
   __syncthreads();
-  bin_round<4, UNIT, kIoShared>(iv, 1, S, Mqi, tid);
-  __syncthreads();
-  bin_round<4, UNIT, kDstGlobal>(iv, 0, S, Mqi, tid, nullptr, r + base);
+  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {  // tile = outer index (modes 13..N)
+    const double2* xt = x + (tile << 12);
+    double2* rt = r + (tile << 12);
+    if (tid < 32) {
+      // the outer modes' part of den and of the scale: lane q takes modes 12 + q, 12 + q + 32
+      double2 d = make_double2(0.0, 0.0), sc = make_double2(1.0, 0.0);
+      for (int q = tid; q < ts.n_outer; q += 32) {
+        const int bit = (int)((tile >> q) & 1);
+        d = cadd(d, ts.t[4 * (12 + q) + (bit ? 3 : 0)]);
+        if (UNIT) sc = cmul(sc, ts.e[2 * (12 + q) + bit]);
+      }
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) {
+        d.x += __shfl_xor_sync(0xffffffffu, d.x, o);
+        d.y += __shfl_xor_sync(0xffffffffu, d.y, o);
+        if (UNIT) {
+          const double2 w = make_double2(__shfl_xor_sync(0xffffffffu, sc.x, o), __shfl_xor_sync(0xffffffffu, sc.y, o));
+          sc = cmul(sc, w);
+        }
+      }
+      if (tid == 0) {
+        dout = d;
+        eout = sc;
+      }
+    }
+    fused_round<UNIT, kSrcGlobal>(fw, 0, S, Mqf, slot_p0[0][tid], xt, nullptr);
+    __syncthreads();
+    fused_round<UNIT, kIoShared>(fw, 1, S, Mqf, slot_p0[1][tid], nullptr, nullptr);
+    __syncthreads();
+    {
+      const double2 dfix = cadd(slot_d[tid], dout);
+      const double2 efix = UNIT ? cmul(slot_e[tid], eout) : make_double2(1.0, 0.0);
+      const int sp0c = swz(slot_p0[2][tid]);
+      double2 v[16];
+#pragma unroll
+      for (int e = 0; e < 16; ++e) v[e] = S[sp0c ^ fw.rsw[2][e]];
+      bin_butterflies<4, UNIT>(rbit, 0, Mqf, v);
+#pragma unroll
+      for (int e = 15; e >= 0; --e) {
+        double2 n = v[e];
+        if (UNIT) n = cmul(cmul(efix, eround[e]), n);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (!((e >> q) & 1) && ((ts.cpl >> q) & 1)) n = cfms(n, t01[q], v[e | (1 << q)]);
+        v[e] = cmul(n, crecip_fast(cadd(dfix, dround[e])));
+      }
+      bin_butterflies<4, UNIT>(rbit, 0, Mqi, v);
+#pragma unroll
+      for (int e = 0; e < 16; ++e) S[sp0c ^ fw.rsw[2][e]] = v[e];
+    }
+    __syncthreads();
+    fused_round<UNIT, kIoShared>(iv, 1, S, Mqi, slot_p0[1][tid], nullptr, nullptr);
+    __syncthreads();
+    fused_round<UNIT, kDstGlobal>(iv, 0, S, Mqi, slot_p0[0][tid], nullptr, rt);
+    __syncthreads();  // the tile buffer and dout / eout are reused
+  }
 }
 
 // Plan the passes over [mode0, mode1) (1-based, all n_j = 2): greedily take as many binary modes
@@ -537,13 +608,24 @@ int binary_fused_solve_launch(const FactorSet& fwd, const FactorSet& inv, const 
     for (int q = 0; q < 4; ++q)
       if ((cmask >> c[q]) & 1) cpl |= 1 << q;
     BinRoundSolve ts{t_pool, unit_scales, n_outer, cpl};
+    // persistent: the resident CTAs (two per SM) walk the tiles
+    int dev = 0, sms = 0, per_sm = 0;
+    NDS_CUDA(cudaGetDevice(&dev));
+    NDS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     if (unit_scales) {
       smem_optin(binary_fused_round_kernel<true>, 4096 * 16);
-      binary_fused_round_kernel<true><<<(unsigned)gr.outer, kBinThreads, 4096 * 16, stream>>>(fw, iv, ts, x, r);
+      NDS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, binary_fused_round_kernel<true>, kBinThreads,
+                                                             4096 * 16));
     } else {
       smem_optin(binary_fused_round_kernel<false>, 4096 * 16);
-      binary_fused_round_kernel<false><<<(unsigned)gr.outer, kBinThreads, 4096 * 16, stream>>>(fw, iv, ts, x, r);
+      NDS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, binary_fused_round_kernel<false>, kBinThreads,
+                                                             4096 * 16));
     }
+    const unsigned grid = (unsigned)std::min<int64_t>(gr.outer, (int64_t)sms * std::max(per_sm, 1));
+    if (unit_scales)
+      binary_fused_round_kernel<true><<<grid, kBinThreads, 4096 * 16, stream>>>(fw, iv, ts, gr.outer, x, r);
+    else
+      binary_fused_round_kernel<false><<<grid, kBinThreads, 4096 * 16, stream>>>(fw, iv, ts, gr.outer, x, r);
     NDS_LAUNCH_CHECK();
     return kBacksubLevel;
   }
