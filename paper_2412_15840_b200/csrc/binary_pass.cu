@@ -72,11 +72,10 @@ __device__ __forceinline__ void bin_butterflies(const int (&rbit)[NB], int logR,
 // UNIT: the matrices are unit-diagonal ([[1, p], [q, 1]], the normalised factors of the fused
 // route — four FMAs per output instead of eight). SYNC: a CTA barrier between the first slot's
 // loads and its butterflies (publishes Mq written just before the call).
-template <int NB, bool UNIT, int IO, bool SYNC = false, int LOGT = 8>
+template <int NB, bool UNIT, int IO, bool SYNC = false>
 __device__ __forceinline__ void bin_round(const BinPass& bp, int rd, double2* S, const double2 (*Mq)[4], int tid,
                                           const double2* __restrict__ gin = nullptr, double2* __restrict__ gout = nullptr) {
   constexpr int V = 1 << NB;
-  constexpr int T = 1 << LOGT;  // threads of the CTA
   int rbit[NB];
 #pragma unroll
   for (int q = 0; q < NB; ++q) rbit[q] = bp.rb[rd][q];
@@ -85,7 +84,7 @@ __device__ __forceinline__ void bin_round(const BinPass& bp, int rd, double2* S,
   int p0t = 0;
   int64_t g0t = 0;
 #pragma unroll
-  for (int i = 0; i < LOGT && i < 12 - NB; ++i) {
+  for (int i = 0; i < 8 && i < 12 - NB; ++i) {
     const int bit = (tid >> i) & 1;
     p0t |= bit << bp.tb[rd][i];
     if (IO != kIoShared && bit) g0t += bp.gbit[bp.tb[rd][i]];
@@ -101,11 +100,11 @@ __device__ __forceinline__ void bin_round(const BinPass& bp, int rd, double2* S,
         if ((e >> q) & 1) ge[e] += bp.gbit[rbit[q]];
     }
   }
-  for (int s = tid; s < (4096 >> NB); s += T) {
+  for (int s = tid; s < (4096 >> NB); s += kBinThreads) {
     int p0j = 0;
     int64_t g0 = g0t;
 #pragma unroll
-    for (int i = LOGT; i < 12 - NB; ++i) {
+    for (int i = 8; i < 12 - NB; ++i) {
       const int bit = (s >> i) & 1;
       p0j |= bit << bp.tb[rd][i];
       if (IO != kIoShared && bit) g0 += bp.gbit[bp.tb[rd][i]];
