@@ -457,6 +457,52 @@ def test_binary_diagonalised_inner_modes(ctx, ref, n_modes, seed):
     assert rel_max(d_x.cpu().numpy().reshape(b.shape, order="F"), x_ref) <= 1e-12
 
 
+def _binary_factors(rng, n_modes, coupled=(), antidiagonal=()):
+    """2 x 2 Schur pairs: random unitary U_j and T_j = [[a, b], [0, d]] with separated eigenvalues;
+    modes in `coupled` get a repeated eigenvalue (a = d: not diagonalisable, so the route must
+    keep their coupling); modes in `antidiagonal` get U_j = [[0, 1], [1, 0]] (zero diagonal: the
+    unit-diagonal normalisation of the factors is refused)."""
+    us, ts = [], []
+    for j in range(n_modes):
+        q, _ = np.linalg.qr(rand_c(rng, (2, 2)))
+        if j in antidiagonal:
+            q = np.array([[0, 1], [1, 0]], dtype=np.complex128)
+        a = 2.0 + 0.3 * (rng.standard_normal() + 1j * rng.standard_normal())
+        d = a if j in coupled else a + 1.0 + 0.2j * rng.standard_normal()
+        t = np.array([[a, 0.5 * (rng.standard_normal() + 1j * rng.standard_normal())], [0, d]], dtype=np.complex128)
+        us.append(np.asfortranarray(q))
+        ts.append(np.asfortranarray(t))
+    return us, ts
+
+
+@pytest.mark.parametrize("coupled,antidiagonal", [((), ()), ((0, 5, 11), ()), ((1, 2, 3, 4), ()), ((0, 2, 4, 6, 8, 10), ()),
+                                                  ((3,), (7,)), ((), (0, 13)), ((0, 1, 2, 3, 4), (12,))])
+def test_binary_fused_kernel_variants(ctx, coupled, antidiagonal):
+    """The fused all-binary route on hand-built Schur factors, against the C oracle on the same
+    factors: up to four coupled inner modes at any tile bits (the solve inside a butterfly round),
+    more than four (the popcount-wavefront kernel), and factors with a zero diagonal entry (plain
+    instead of unit-diagonal butterflies)."""
+    import oracle
+    import torch
+    rng = np.random.default_rng(1234 + 17 * len(coupled) + len(antidiagonal))
+    n_modes = 15
+    us, ts = _binary_factors(rng, n_modes, coupled, antidiagonal)
+    b = rand_c(rng, (2,) * n_modes)
+    b = np.asfortranarray(b)
+    x_ref, _ = oracle.Port().solve_schur(us, ts, b)
+    plan = ctx.plan(us, ts)
+    got, cond = plan.diagonalised()
+    assert got and cond <= 1e6
+    d_b = torch.from_numpy(np.ascontiguousarray(b.ravel(order="F"))).cuda()
+    d_x, d_w = torch.empty_like(d_b), torch.empty_like(d_b)
+    ctx.set_stream(torch.cuda.current_stream().cuda_stream)
+    plan.execute(d_b.data_ptr(), d_x.data_ptr(), d_w.data_ptr())
+    torch.cuda.synchronize()
+    ctx.set_stream(None)
+    plan.close()
+    assert rel_max(d_x.cpu().numpy().reshape(b.shape, order="F"), x_ref) <= 1e-12
+
+
 def _spectrum_factors(rng, dims, kind):
     """Unitary U and upper-triangular T whose eigenvalues (the diagonal) follow `kind`:
     'spread' (disk of radius 1 around 2), 'clustered' (most of them within 1e-3 of each other),
