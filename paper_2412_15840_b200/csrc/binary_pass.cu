@@ -12,6 +12,7 @@
 // the 2x2 matrices as butterflies, and scatters back. Modes commute (test_kernels.cpp:91-99), so
 // the grouping changes rounding only.
 #include <algorithm>
+#include <complex>
 #include <vector>
 
 #include "common.cuh"
@@ -295,37 +296,60 @@ struct BinRoundSolve {
   const double2* e;  // UNIT: the deferred scales e_j[0], e_j[1] at e + 2 j
   int n_outer;       // N - 12
   int cpl;           // bit q: round-C bit q is a coupled mode
+  // By value, so every coefficient is a constant-bank operand of its DFMA (no shared-memory
+  // table reads in the inner loops): the 2 x 2 matrices by [round][round bit] (column-major:
+  // m00, m10, m01, m11), forward and inverse; round C's coupling t01 per bit and its part of den
+  // and of the scale per entry e.
+  double2 mf[3][4][4], mi[3][4][4];
+  double2 t01[4], dround[16], eround[16];
 };
 
+template <bool UNIT>
+__device__ __forceinline__ void const_butterflies(const double2 (&m)[4][4], double2 (&v)[16]) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      if (!((e >> q) & 1)) {
+        const double2 a = v[e], b = v[e | (1 << q)];
+        if (UNIT) {
+          v[e] = cfma(a, m[q][2], b);
+          v[e | (1 << q)] = cfma(b, m[q][1], a);
+        } else {
+          v[e] = cfma(cmul(m[q][0], a), m[q][2], b);
+          v[e | (1 << q)] = cfma(cmul(m[q][1], a), m[q][3], b);
+        }
+      }
+    }
+  }
+}
+
 // One round of the persistent kernel below on a contiguous tile: the thread's slot (one per
-// thread: 256 threads x 16 entries) is fixed per round for the whole launch, so its swizzled
-// position sp0 and tile offset p0 come precomputed.
+// thread: 256 threads x 16 entries) is fixed per round for the whole launch, so its tile offset
+// p0 comes precomputed.
 template <bool UNIT, int IO>
-__device__ __forceinline__ void fused_round(const BinPass& bp, int rd, double2* S, const double2 (*Mq)[4], int p0,
+__device__ __forceinline__ void fused_round(const BinPass& bp, int rd, const double2 (&m)[4][4], double2* S, int p0,
                                             const double2* __restrict__ gin, double2* __restrict__ gout) {
   const int sp0 = swz(p0);
-  int rbit[4];
-#pragma unroll
-  for (int q = 0; q < 4; ++q) rbit[q] = bp.rb[rd][q];
   double2 v[16];
 #pragma unroll
   for (int e = 0; e < 16; ++e) {
     if (IO & kSrcGlobal) {
       int eb = 0;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) eb |= ((e >> q) & 1) << rbit[q];
+      for (int q = 0; q < 4; ++q) eb |= ((e >> q) & 1) << bp.rb[rd][q];
       v[e] = gin[p0 | eb];
     } else {
       v[e] = S[sp0 ^ bp.rsw[rd][e]];
     }
   }
-  bin_butterflies<4, UNIT>(rbit, 0, Mq, v);
+  const_butterflies<UNIT>(m, v);
 #pragma unroll
   for (int e = 0; e < 16; ++e) {
     if (IO & kDstGlobal) {
       int eb = 0;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) eb |= ((e >> q) & 1) << rbit[q];
+      for (int q = 0; q < 4; ++q) eb |= ((e >> q) & 1) << bp.rb[rd][q];
       gout[p0 | eb] = v[e];
     } else {
       S[sp0 ^ bp.rsw[rd][e]] = v[e];
@@ -333,37 +357,16 @@ __device__ __forceinline__ void fused_round(const BinPass& bp, int rd, double2* 
   }
 }
 
-// Persistent: a CTA walks tiles blockIdx.x, + gridDim.x, ... (two CTAs per SM), so the factor
-// tables, the per-thread slot positions and the thread's tile-independent part of den / scale are
-// set up once per CTA; per tile only the outer modes' part (one warp, lanes over modes, shuffle
-// tree) is new.
+// Persistent: a CTA walks tiles blockIdx.x, + gridDim.x, ... (two CTAs per SM), so the per-thread
+// slot positions and the thread's tile-independent part of den / scale are set up once per CTA;
+// per tile only the outer modes' part (one warp, lanes over modes, shuffle tree) is new.
 template <bool UNIT>
 __global__ void __launch_bounds__(kBinThreads, 2)
-    binary_fused_round_kernel(const BinPass fw, const BinPass iv, const BinRoundSolve ts, int64_t n_tiles,
-                              const double2* __restrict__ x, double2* __restrict__ r) {
+    binary_fused_round_kernel(const __grid_constant__ BinPass fw, const __grid_constant__ BinRoundSolve ts,
+                              int64_t n_tiles, const double2* __restrict__ x, double2* __restrict__ r) {
   extern __shared__ __align__(16) double2 S[];  // 4096 entries, swizzled (swz)
-  __shared__ double2 Mqf[12][4], Mqi[12][4];
-  __shared__ double2 t01[4], dround[16], eround[16];
   __shared__ double2 dout, eout;
   const int tid = threadIdx.x;
-  if (tid < 48) {
-    Mqf[tid >> 2][tid & 3] = fw.M[tid >> 2][tid & 3];
-  } else if (tid < 96) {
-    const int e = tid - 48;
-    Mqi[e >> 2][e & 3] = iv.M[e >> 2][e & 3];
-  } else if (tid < 100) {
-    t01[tid - 96] = ts.t[4 * fw.rb[2][tid - 96] + 2];
-  } else if (tid < 116) {
-    const int e = tid - 100;
-    double2 d = make_double2(0.0, 0.0), sc = make_double2(1.0, 0.0);
-    for (int q = 0; q < 4; ++q) {
-      const int j = fw.rb[2][q], bit = (e >> q) & 1;
-      d = cadd(d, ts.t[4 * j + (bit ? 3 : 0)]);
-      if (UNIT) sc = cmul(sc, ts.e[2 * j + bit]);
-    }
-    dround[e] = d;
-    eround[e] = sc;
-  }
   // slot positions per round (A, B, C) and the tile-independent part of den / scale (the 8 tile
   // bits outside round C): per-thread constants of the launch, parked in shared memory
   __shared__ int slot_p0[3][kBinThreads];
@@ -386,9 +389,6 @@ __global__ void __launch_bounds__(kBinThreads, 2)
     slot_d[tid] = d;
     slot_e[tid] = sc;
   }
-  int rbit[4];
-#pragma unroll
-  for (int q = 0; q < 4; ++q) rbit[q] = fw.rb[2][q];
   __syncthreads();
   for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {  // tile = outer index (modes 13..N)
     const double2* xt = x + (tile << 12);
@@ -415,9 +415,9 @@ __global__ void __launch_bounds__(kBinThreads, 2)
         eout = sc;
       }
     }
-    fused_round<UNIT, kSrcGlobal>(fw, 0, S, Mqf, slot_p0[0][tid], xt, nullptr);
+    fused_round<UNIT, kSrcGlobal>(fw, 0, ts.mf[0], S, slot_p0[0][tid], xt, nullptr);
     __syncthreads();
-    fused_round<UNIT, kIoShared>(fw, 1, S, Mqf, slot_p0[1][tid], nullptr, nullptr);
+    fused_round<UNIT, kIoShared>(fw, 1, ts.mf[1], S, slot_p0[1][tid], nullptr, nullptr);
     __syncthreads();
     {
       const double2 dfix = cadd(slot_d[tid], dout);
@@ -426,24 +426,24 @@ __global__ void __launch_bounds__(kBinThreads, 2)
       double2 v[16];
 #pragma unroll
       for (int e = 0; e < 16; ++e) v[e] = S[sp0c ^ fw.rsw[2][e]];
-      bin_butterflies<4, UNIT>(rbit, 0, Mqf, v);
+      const_butterflies<UNIT>(ts.mf[2], v);
 #pragma unroll
       for (int e = 15; e >= 0; --e) {
         double2 n = v[e];
-        if (UNIT) n = cmul(cmul(efix, eround[e]), n);
+        if (UNIT) n = cmul(cmul(efix, ts.eround[e]), n);
 #pragma unroll
         for (int q = 0; q < 4; ++q)
-          if (!((e >> q) & 1) && ((ts.cpl >> q) & 1)) n = cfms(n, t01[q], v[e | (1 << q)]);
-        v[e] = cmul(n, crecip_fast(cadd(dfix, dround[e])));
+          if (!((e >> q) & 1) && ((ts.cpl >> q) & 1)) n = cfms(n, ts.t01[q], v[e | (1 << q)]);
+        v[e] = cmul(n, crecip_fast(cadd(dfix, ts.dround[e])));
       }
-      bin_butterflies<4, UNIT>(rbit, 0, Mqi, v);
+      const_butterflies<UNIT>(ts.mi[2], v);
 #pragma unroll
       for (int e = 0; e < 16; ++e) S[sp0c ^ fw.rsw[2][e]] = v[e];
     }
     __syncthreads();
-    fused_round<UNIT, kIoShared>(iv, 1, S, Mqi, slot_p0[1][tid], nullptr, nullptr);
+    fused_round<UNIT, kIoShared>(fw, 1, ts.mi[1], S, slot_p0[1][tid], nullptr, nullptr);
     __syncthreads();
-    fused_round<UNIT, kDstGlobal>(iv, 0, S, Mqi, slot_p0[0][tid], nullptr, rt);
+    fused_round<UNIT, kDstGlobal>(fw, 0, ts.mi[0], S, slot_p0[0][tid], nullptr, rt);
     __syncthreads();  // the tile buffer and dout / eout are reused
   }
 }
@@ -584,9 +584,10 @@ int binary_pass_launch(const FactorSet& f, const BinGroup& gr, bool adjoint, con
 
 int binary_fused_solve_launch(const FactorSet& fwd, const FactorSet& inv, const BinGroup& gr, const double2* t_pool,
                               int n_outer, const uint16_t* wf, const int* wf_off, int levels, int cmask,
-                              const double2* x, double2* r, cudaStream_t stream, const double2* unit_scales) {
+                              const BinHostFactors& host, const double2* x, double2* r, cudaStream_t stream,
+                              const double2* unit_scales) {
   if (gr.first != 1 || gr.count != 12 || gr.logR != 0 || gr.inner != 1) throw Error(NDS_ERR_OTHER, "fused pass: not a modes-1-12 tile pass");
-  if (__builtin_popcount(cmask) <= 4) {
+  if (__builtin_popcount(cmask) <= 4 && host.fwd) {
     // round C = the coupled bits, filled up with the lowest other bits; A = the highest four of
     // the rest (global side), B = the other four
     std::vector<int> c, rest;
@@ -602,11 +603,33 @@ int binary_fused_solve_launch(const FactorSet& fwd, const FactorSet& inv, const 
                                                   c};
     const std::vector<bool> asc = {true, false, false};
     const BinPass fw = make_bin_pass(fwd, gr, true, rounds, asc);
-    const BinPass iv = make_bin_pass(inv, gr, false, rounds, asc);
     int cpl = 0;
     for (int q = 0; q < 4; ++q)
       if ((cmask >> c[q]) & 1) cpl |= 1 << q;
-    BinRoundSolve ts{t_pool, unit_scales, n_outer, cpl};
+    BinRoundSolve ts{};
+    ts.t = t_pool;
+    ts.e = unit_scales;
+    ts.n_outer = n_outer;
+    ts.cpl = cpl;
+    auto cx = [](double2 a) { return std::complex<double>(a.x, a.y); };
+    auto d2 = [](std::complex<double> a) { return make_double2(a.real(), a.imag()); };
+    for (int rd = 0; rd < 3; ++rd)
+      for (int q = 0; q < 4; ++q)
+        for (int e = 0; e < 4; ++e) {
+          ts.mf[rd][q][e] = host.fwd[4 * rounds[rd][q] + e];
+          ts.mi[rd][q][e] = host.inv[4 * rounds[rd][q] + e];
+        }
+    for (int q = 0; q < 4; ++q) ts.t01[q] = host.t[4 * c[q] + 2];
+    for (int e = 0; e < 16; ++e) {
+      std::complex<double> d(0.0, 0.0), sc(1.0, 0.0);
+      for (int q = 0; q < 4; ++q) {
+        const int bit = (e >> q) & 1;
+        d += cx(host.t[4 * c[q] + (bit ? 3 : 0)]);
+        if (host.e) sc *= cx(host.e[2 * c[q] + bit]);
+      }
+      ts.dround[e] = d2(d);
+      ts.eround[e] = d2(sc);
+    }
     // persistent: the resident CTAs (two per SM) walk the tiles
     int dev = 0, sms = 0, per_sm = 0;
     NDS_CUDA(cudaGetDevice(&dev));
@@ -622,9 +645,9 @@ int binary_fused_solve_launch(const FactorSet& fwd, const FactorSet& inv, const 
     }
     const unsigned grid = (unsigned)std::min<int64_t>(gr.outer, (int64_t)sms * std::max(per_sm, 1));
     if (unit_scales)
-      binary_fused_round_kernel<true><<<grid, kBinThreads, 4096 * 16, stream>>>(fw, iv, ts, gr.outer, x, r);
+      binary_fused_round_kernel<true><<<grid, kBinThreads, 4096 * 16, stream>>>(fw, ts, gr.outer, x, r);
     else
-      binary_fused_round_kernel<false><<<grid, kBinThreads, 4096 * 16, stream>>>(fw, iv, ts, gr.outer, x, r);
+      binary_fused_round_kernel<false><<<grid, kBinThreads, 4096 * 16, stream>>>(fw, ts, gr.outer, x, r);
     NDS_LAUNCH_CHECK();
     return kBacksubLevel;
   }

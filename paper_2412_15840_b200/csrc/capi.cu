@@ -103,6 +103,9 @@ struct nds_plan {
   const int* bin_wf_off = nullptr;
   int bin_wf_levels = 0;
   int bin_cmask = 0;  // inner modes left coupled
+  // host copies for the round kernel's by-value coefficients: [fwd 4N | inv 4N | T' 4N | e 2N],
+  // plain factors (e unused) and normalised ones
+  std::vector<double2> bin_host_plain, bin_host_norm;
   // Cubic-tile route with every T_j block-diagonalised (plan_cubic_diag): T'_j = W_j^{-1} T_j W_j,
   // W_j = blockdiag of the unit-column eigenvector matrices of T_j's B x B diagonal blocks. Full
   // solves run the passes with fc (forward W_j^{-1} U_j^H, inverse U_j W_j) and the solve on
@@ -642,6 +645,7 @@ void plan_binary_diag(nds_plan* p, const nds_z* const* u, const nds_z* const* t)
   // normalised forms: [fwd unit matrix, column-major (4) | inv unit matrix (4)] per mode, then the
   // scales e_j (2 per mode), then T'_j with the scaled coupling (4 per mode)
   std::vector<double2> hostn((size_t)N * 14);
+  std::vector<double2> hplain((size_t)N * 14);
   bool norm_ok = true;
   auto d2 = [](cx v) { return make_double2(v.real(), v.imag()); };
   for (int j = 0; j < N; ++j) {
@@ -665,6 +669,12 @@ void plan_binary_diag(nds_plan* p, const nds_z* const* u, const nds_z* const* t)
       Wi[r][0] = U[r][0];
       Wi[r][1] = U[r][1] + b * U[r][0];
     }
+    for (int r = 0; r < 2; ++r)
+      for (int c = 0; c < 2; ++c) {
+        hplain[(size_t)4 * j + r + 2 * c] = d2(Wf[r][c]);
+        hplain[(size_t)4 * N + 4 * j + r + 2 * c] = d2(Wi[r][c]);
+      }
+    for (int e = 0; e < 4; ++e) hplain[(size_t)8 * N + 4 * j + e] = tp[e];
     {
       // W_fwd = diag(f) [[1, p], [q, 1]] (row scales), W_inv = [[1, p'], [q', 1]] diag(g) (column
       // scales); refused when a diagonal entry is tiny against its matrix
@@ -747,8 +757,20 @@ void plan_binary_diag(nds_plan* p, const nds_z* const* u, const nds_z* const* t)
   NDS_CUDA(cudaMallocFromPoolAsync((void**)&p->fd_buf, (host.size() + hostn.size()) * sizeof(double2), p->ctx->pool,
                                    p->ctx->stream));
   nds::param_blob_launch(pb, p->fd_buf, p->ctx->stream);
+  p->bin_host_plain = std::move(hplain);
+  p->bin_host_norm.clear();
   p->bin_norm = norm_ok;
   if (norm_ok) {  // (used only by execute_fused_binary, where every pass is a binary group)
+    p->bin_host_norm.resize((size_t)N * 14);
+    for (int j = 0; j < N; ++j) {
+      for (int e = 0; e < 4; ++e) {
+        p->bin_host_norm[(size_t)4 * j + e] = hostn[(size_t)8 * j + e];
+        p->bin_host_norm[(size_t)4 * N + 4 * j + e] = hostn[(size_t)8 * j + 4 + e];
+        p->bin_host_norm[(size_t)8 * N + 4 * j + e] = hostn[(size_t)10 * N + 4 * j + e];
+      }
+      p->bin_host_norm[(size_t)12 * N + 2 * j] = hostn[(size_t)8 * N + 2 * j];
+      p->bin_host_norm[(size_t)12 * N + 2 * j + 1] = hostn[(size_t)8 * N + 2 * j + 1];
+    }
     pb.count = (int)hostn.size();
     std::memcpy(pb.v, hostn.data(), hostn.size() * sizeof(double2));
     double2* nb = p->fd_buf + host.size();
@@ -1032,9 +1054,16 @@ int execute_fused_binary(nds_plan* p, const std::vector<XPass>& passes, const do
     double2* dst = dst_of(++k);
     const nds::BinarySolvePlan& bp = p->solver->bsp;
     const nds::FactorSet& ff = norm ? p->fn : p->fd;
+    const std::vector<double2>& hv = norm ? p->bin_host_norm : p->bin_host_plain;
+    const size_t nm = (size_t)p->n_modes;
+    nds::BinHostFactors hf;
+    hf.fwd = hv.data();
+    hf.inv = hv.data() + 4 * nm;
+    hf.t = hv.data() + 8 * nm;
+    hf.e = norm ? hv.data() + 12 * nm : nullptr;
     const int kind = nds::binary_fused_solve_launch(ff, ff, p->groups[passes.front().group],
                                                     norm ? p->bin_tn : p->bin_t, bp.n_outer, p->bin_wf,
-                                                    p->bin_wf_off, p->bin_wf_levels, p->bin_cmask, src, dst, s,
+                                                    p->bin_wf_off, p->bin_wf_levels, p->bin_cmask, hf, src, dst, s,
                                                     norm ? p->bin_e : nullptr);
     if (rec) rec->mark(s, kind, 0);
     ++launches;

@@ -76,9 +76,18 @@ int binary_pass_launch(const FactorSet& f, const BinGroup& gr, bool adjoint, con
 // and one write of the tensor; gr is the modes-1-12 pass (first 1, count 12, inner 1).
 // t_pool: T'_j (2 x 2, all N modes; diagonal for the diagonalised ones), wf / wf_off: the tile
 // entries by popcount over the coupled inner modes (levels = their count + 1).
+// Host copies of what the device pointers hold (all N modes): the forward / inverse 2 x 2
+// matrices (column-major, 4 per mode), T'_j (4 per mode) and, on the normalised route, the scales
+// (2 per mode; else nullptr). The round kernel takes its coefficients by value from them.
+struct BinHostFactors {
+  const double2* fwd = nullptr;
+  const double2* inv = nullptr;
+  const double2* t = nullptr;
+  const double2* e = nullptr;
+};
 int binary_fused_solve_launch(const FactorSet& fwd, const FactorSet& inv, const BinGroup& gr, const double2* t_pool,
                               int n_outer, const uint16_t* wf, const int* wf_off, int levels, int cmask,
-                              const double2* x, double2* r, cudaStream_t stream,
+                              const BinHostFactors& host, const double2* x, double2* r, cudaStream_t stream,
                               const double2* unit_scales = nullptr);
 // cmask: the inner modes left coupled (bit j = mode j + 1). Up to four: the tile solve is one
 // round of the butterfly network (binary_fused_round_kernel; wf unused); more: the popcount
