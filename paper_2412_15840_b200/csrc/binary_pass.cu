@@ -33,6 +33,8 @@ struct BinPass {
   int tb[3][12];   // tile bits carried by the thread index (and slot index) in each round
   int rsw[3][16];  // swz(round bits of entry e): swz is linear over XOR, so swz(p0 | bits_e) =
                    // swz(p0) ^ rsw[e] — one XOR per access instead of the full swizzle
+  int lane_mode;   // >= 0: round 0 also applies this group mode across lanes l, l ^ 16 by shuffles (its
+                   // tile bit is thread bit 4 of round 0), so 9 modes take two rounds
   int64_t gbit[12];      // global offset of tile bit b (run bits: 2^b; group bit q: I 2^q)
   const double2* M[12];  // 2x2 column-major op(U_j) per group mode
 };
@@ -73,7 +75,7 @@ __device__ __forceinline__ void bin_butterflies(const int (&rbit)[NB], int logR,
 // UNIT: the matrices are unit-diagonal ([[1, p], [q, 1]], the normalised factors of the fused
 // route — four FMAs per output instead of eight). SYNC: a CTA barrier between the first slot's
 // loads and its butterflies (publishes Mq written just before the call).
-template <int NB, bool UNIT, int IO, bool SYNC = false>
+template <int NB, bool UNIT, int IO, bool SYNC = false, bool LANE = false>
 __device__ __forceinline__ void bin_round(const BinPass& bp, int rd, double2* S, const double2 (*Mq)[4], int tid,
                                           const double2* __restrict__ gin = nullptr, double2* __restrict__ gout = nullptr) {
   constexpr int V = 1 << NB;
@@ -116,6 +118,16 @@ __device__ __forceinline__ void bin_round(const BinPass& bp, int rd, double2* S,
     for (int e = 0; e < V; ++e) v[e] = (IO & kSrcGlobal) ? gin[g0 + ge[e]] : S[sp0 ^ bp.rsw[rd][e]];
     if (SYNC && s == tid) __syncthreads();
     bin_butterflies<NB, UNIT>(rbit, bp.logR, Mq, v);
+    if (LANE) {
+      // one more mode across the lane pair (l, l ^ 16): every lane computes its own output
+      const bool hi = (tid & 16) != 0;
+      const double2 cs = Mq[bp.lane_mode][hi ? 3 : 0], co = Mq[bp.lane_mode][hi ? 1 : 2];
+#pragma unroll
+      for (int e = 0; e < V; ++e) {
+        const double2 o = make_double2(__shfl_xor_sync(0xffffffffu, v[e].x, 16), __shfl_xor_sync(0xffffffffu, v[e].y, 16));
+        v[e] = UNIT ? cfma(v[e], co, o) : cfma(cmul(cs, v[e]), co, o);
+      }
+    }
 #pragma unroll
     for (int e = 0; e < V; ++e) {
       if (IO & kDstGlobal)
@@ -130,6 +142,10 @@ template <bool UNIT, int IO, bool SYNC = false>
 __device__ __forceinline__ void bin_round_any(const BinPass& bp, int rd, double2* S, const double2 (*Mq)[4], int tid,
                                               const double2* __restrict__ gin = nullptr,
                                               double2* __restrict__ gout = nullptr) {
+  if (IO == kSrcGlobal && bp.lane_mode >= 0) {  // (a four-bit first round by construction)
+    bin_round<4, UNIT, IO, SYNC, true>(bp, rd, S, Mq, tid, gin, gout);
+    return;
+  }
   switch (bp.nrb[rd]) {
     case 4: bin_round<4, UNIT, IO, SYNC>(bp, rd, S, Mq, tid, gin, gout); break;
     case 3: bin_round<3, UNIT, IO, SYNC>(bp, rd, S, Mq, tid, gin, gout); break;
@@ -491,8 +507,10 @@ std::vector<BinGroup> plan_binary_groups(int n_modes, const int64_t* dims, int l
 // lowest tile bits, i.e. whole runs), otherwise the first three with distinct residues mod 3
 // where possible (conflict-free shared-memory phases under swz).
 static BinPass make_bin_pass(const FactorSet& f, const BinGroup& gr, bool adjoint,
-                             const std::vector<std::vector<int>>& rounds, const std::vector<bool>& ascending) {
+                             const std::vector<std::vector<int>>& rounds, const std::vector<bool>& ascending,
+                             int lane_bit = -1) {
   BinPass bp{};
+  bp.lane_mode = lane_bit >= 0 ? lane_bit - gr.logR : -1;
   bp.I = gr.inner;
   bp.O = gr.outer;
   bp.logR = gr.logR;
@@ -523,6 +541,10 @@ static BinPass make_bin_pass(const FactorSet& f, const BinGroup& gr, bool adjoin
           }
     for (int b : rest)
       if (b >= 0) order.push_back(b);
+    if (rd == 0 && lane_bit >= 0) {  // the lane-pair mode's tile bit becomes thread bit 4
+      order.erase(std::find(order.begin(), order.end(), lane_bit));
+      order.insert(order.begin() + 4, lane_bit);
+    }
     for (size_t i = 0; i < order.size(); ++i) bp.tb[rd][i] = order[i];
     for (int e = 0; e < (1 << nb); ++e) {
       int bits = 0;
@@ -557,6 +579,10 @@ static BinPass make_bin_pass_streamed(const FactorSet& f, const BinGroup& gr, bo
   } else if (k <= 8) {
     range(k - 4, k);
     range(0, k - 4);
+  } else if (k == 9) {  // 4 register bits + 1 lane bit in the first round, 4 in the last
+    range(5, 9);
+    range(0, 4);
+    return make_bin_pass(f, gr, adjoint, rounds, {true, true}, lo + 4);
   } else {
     range(k - 4, k);
     range(4, k - 4);
