@@ -320,6 +320,6 @@ struct BlkLaunchT {
 // registers, spills) 1.169, BK = 4 x 3 stages 1.34.
 static BlkLaunchT blk_cfg(int n_modes, int b) {
   if (n_modes == 3 && b == 16) return {blk_level_kernel<3, 16, 8, 3, 256>, BlkCfg<3, 16, 8, 3, 256>::smem(), 256};
-  if (n_modes == 4 && b == 8) return {blk_level_kernel<4, 8, 4, 3, 512>, BlkCfg<4, 8, 4, 3, 512>::smem(), 512};
+  if (n_modes == 4 && b == 8) return {blk_level_kernel<4, 8, 4, 4, 512>, BlkCfg<4, 8, 4, 4, 512>::smem(), 512};
   return {nullptr, 0, 0};
 }
