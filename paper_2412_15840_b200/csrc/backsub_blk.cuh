@@ -319,7 +319,8 @@ struct BlkLaunchT {
 // producer-offset change (c1 1.195 ms): N = 3 with BK = 4 x 2 stages at 2 CTAs / SM (128
 // registers, spills) 1.169, BK = 4 x 3 stages 1.34.
 // End of round 2 (c2 is the only BASELINE config left on 8^4 tiles: D = (32, 32, 32, 16), twelve
-// short levels): 8^4 with a 4-stage ring 5.11 ms against 5.51 with three; 16^3 with four stages
+// short levels): 8^4 with a 4-stage ring 5.11 ms against 5.51 with three (four stages and 256
+// threads 5.52, 1024 threads 5.82, BK = 8 x 2 stages 5.26); 16^3 with four stages
 // 0.768 (c1) / 10.25 ms (c3) against 0.716 / 9.46 with three.
 static BlkLaunchT blk_cfg(int n_modes, int b) {
   if (n_modes == 3 && b == 16) return {blk_level_kernel<3, 16, 8, 3, 256>, BlkCfg<3, 16, 8, 3, 256>::smem(), 256};
