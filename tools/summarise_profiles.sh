@@ -11,7 +11,7 @@ for c in c1 c2 c3 c4; do
 done
 for c in c3 c4; do tail -n 1 $I/bench_sharded1_$c.json > profiles/${R}_bench_sharded1_$c.json; done
 tail -n 1 $I/reference_c1.json > profiles/${R}_reference_c1.json
-tail -n 1 $I/ode_bench.json > profiles/${R}_ode_bench.json
+cp $I/ode_bench.json profiles/${R}_ode_bench.json  # two lines: OdePropagator::at on c1, RK4 on c0
 cp $I/plan_timing.txt profiles/${R}_plan_timing.txt
 cp $I/route_survey.txt profiles/${R}_route_survey.txt
 cp $I/gpu.txt profiles/${R}_gpu.txt
