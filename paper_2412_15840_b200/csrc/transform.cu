@@ -16,6 +16,8 @@
 // (row strides = 4 resp. 2 mod 8 complex for the DMMA fragment pattern).
 #include <cstdlib>
 
+#include <cuda.h>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -424,6 +426,156 @@ __global__ void __launch_bounds__(WM* WN * 32, MINB) zgemm_tma_kernel(const Gemm
   }
 }
 
+// ---- mode-1 form fed by tensor-map TMA ---------------------------------------------------------
+// The mode-1 product (inner = 1) is C(b, i) = sum_k X(b, k) M^T(k, i): the tensor is the A operand,
+// one contiguous n-entry fibre per row b. A 2-D tensor map over (k as doubles, b) lets ONE
+// cp.async.bulk.tensor per group of four k's fetch the BM x 4 box of a stage (64 bytes per row,
+// rows n * 16 bytes apart) straight from the tensor's own strides — the per-row bulk copies of the
+// plain bulk-copy form (BM of them per stage) were slower than cp.async. The box lands as
+// [row][4 k], so a stage is [k group][row][4]: the A fragment of a quarter-warp (2 rows x 4 k) is
+// 128 contiguous bytes, conflict-free without padding. Rows beyond the tensor are zero-filled by
+// the copy engine. B = the factor's stage-blocked image (FactorSet::bblk), one bulk copy per stage.
+static bool encode_colm_tmap(CUtensorMap* out, const double2* a, int64_t rows, int64_t lda, int K, int bm) {
+  typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                               const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                               CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static EncodeFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return (EncodeFn)f;
+  }();
+  if (!fn || ((uintptr_t)a & 15) || rows > 0x7fffffffll) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)2 * K, (cuuint64_t)rows};  // doubles along k, fibres
+  const cuuint64_t strides[1] = {(cuuint64_t)lda * 16};
+  const cuuint32_t box[2] = {8, (cuuint32_t)bm};
+  const cuuint32_t estr[2] = {1, 1};
+  return fn(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)a, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
+}
+__device__ __forceinline__ void tmap_g2s_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, int MINB>
+__global__ void __launch_bounds__(WM* WN * 32, MINB)
+    zgemm_tmap_colm_kernel(const GemmArgs g, const __grid_constant__ CUtensorMap amap) {
+  using Cfg = GemmCfg<BM, BN, BK, WM, WN, STAGES>;
+  constexpr int NW = WM * WN;
+  constexpr int MI = Cfg::MI, NI = Cfg::NI;
+  constexpr int kStageA = BM * BK;  // [BK / 4][BM][4], unpadded
+  extern __shared__ __align__(16) double2 smem[];
+  // the tensor copies need 128-byte aligned destinations: align the stage area by hand (the launch
+  // allocates 128 spare bytes)
+  double2* sA = smem + ((128u - (smem_u32(smem) & 127u)) & 127u) / 16;
+  double2* sB = sA + STAGES * kStageA;
+  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int wy = warp / WN, wx = warp % WN;
+  const int64_t tile = blockIdx.x;
+  const int64_t row_tile = tile % g.ntile_rows;
+  const int64_t ct = tile / g.ntile_rows;  // column tile of M^T (blim = 1)
+  const int64_t row0 = row_tile * BM;
+  const int64_t a0 = ct * BN;
+  const int nk = g.K / BK;
+  if (tid == 0) {
+    for (int s2 = 0; s2 < STAGES; ++s2) {
+      mbar_init(&full[s2], 1);
+      mbar_init(&empty[s2], NW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  constexpr unsigned stage_bytes = (unsigned)((kStageA + Cfg::kStageB) * 16);
+  auto produce = [&](int st, int kt) {  // one lane: the B image and BK / 4 boxes of the tensor
+    mbar_expect_tx(&full[st], stage_bytes);
+    bulk_g2s(sB + st * Cfg::kStageB, g.blk + ((ct * nk + kt) * BK) * Cfg::kLdB, Cfg::kStageB * 16, &full[st]);
+#pragma unroll
+    for (int kg = 0; kg < BK / 4; ++kg)
+      tmap_g2s_2d(sA + st * kStageA + kg * BM * 4, &amap, 2 * (kt * BK + kg * 4), (int)row0, &full[st]);
+  };
+  if (tid == 0)
+    for (int s2 = 0; s2 < STAGES && s2 < nk; ++s2) produce(s2, s2);
+
+  double cre[MI][NI][2], cim[MI][NI][2], c3[MI][NI][2];
+#pragma unroll
+  for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < NI; ++ni)
+      cre[mi][ni][0] = cre[mi][ni][1] = cim[mi][ni][0] = cim[mi][ni][1] = c3[mi][ni][0] = c3[mi][ni][1] = 0.0;
+  const int arow = wy * (BM / WM) + (lane >> 2);
+  const int bcol = wx * (BN / WN) + (lane >> 2);
+  const int kq = lane & 3;
+  for (int kt = 0; kt < nk; ++kt) {
+    if (warp == 0 && kt >= 1 && kt - 1 + STAGES < nk) {  // refill the stage k-tile kt - 1 used
+      const int st = (kt - 1) % STAGES;
+      if (lane == 0) {
+        mbar_wait(&empty[st], ((kt - 1) / STAGES) & 1);
+        produce(st, kt - 1 + STAGES);
+      }
+      __syncwarp();
+    }
+    const int st = kt % STAGES;
+    mbar_wait(&full[st], (kt / STAGES) & 1);
+    const double2* cA = sA + st * kStageA;
+    const double2* cB = sB + st * Cfg::kStageB;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double ar[MI], ai[MI], an[MI], br[NI], bi[NI], bs[NI];
+#pragma unroll
+      for (int mi = 0; mi < MI; ++mi) {
+        const double2 v = cA[((kk >> 2) * BM + arow + mi * 8) * 4 + kq];
+        ar[mi] = v.x;
+        ai[mi] = v.y;
+        an[mi] = v.x + v.y;
+      }
+#pragma unroll
+      for (int ni = 0; ni < NI; ++ni) {
+        const double2 v = cB[(kk + kq) * Cfg::kLdB + bcol + ni * 8];
+        br[ni] = v.x;
+        bi[ni] = v.y;
+        bs[ni] = v.x + v.y;
+      }
+#pragma unroll
+      for (int mi = 0; mi < MI; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < NI; ++ni) {
+          dmma(cre[mi][ni][0], cre[mi][ni][1], ar[mi], br[ni]);
+          dmma(cim[mi][ni][0], cim[mi][ni][1], ai[mi], bi[ni]);
+          dmma(c3[mi][ni][0], c3[mi][ni][1], an[mi], bs[ni]);
+        }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+  }
+#pragma unroll
+  for (int mi = 0; mi < MI; ++mi) {
+    const int64_t r = row0 + wy * (BM / WM) + mi * 8 + (lane >> 2);
+    if (r >= g.rows) continue;
+#pragma unroll
+    for (int ni = 0; ni < NI; ++ni) {
+      const int64_t ga = a0 + wx * (BN / WN) + ni * 8 + 2 * kq;
+      double2* dst = g.C + r * g.ldcr + ga;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (ga + h < g.alim) {
+          double2 v = make_double2(cre[mi][ni][h] - cim[mi][ni][h], c3[mi][ni][h] - cre[mi][ni][h] - cim[mi][ni][h]);
+          if (g.accumulate) v = cadd(dst[h], v);
+          dst[h] = v;
+        }
+      }
+    }
+  }
+}
+
 // Stage geometry of the short-K bulk-copy GEMM: the constant operand's stage image is UNPADDED
 // (BM x BK, 16-byte chunks XOR-swizzled by row parity: entry (r, k) at r BK + (k ^ 4 (r & 1)),
 // the same banks as the padded rows), which leaves room for a 4-stage ring at 2 CTAs / SM.
@@ -604,6 +756,19 @@ static void launch_gemm_t(GemmArgs g, cudaStream_t stream) {
   // bulk-copy feed for the row-major form only: the mode-1 form would need one copy per 256-byte
   // row of the tensor operand (64 per stage) and measured 1.32 ms per c1 pass vs 0.94 with cp.async
   const bool tma = M3 && g.blk && !colm && g.K % BK == 0 && g.alim % W == 0;
+  if (M3 && g.blk && colm && g.K % BK == 0 && g.ldbb == 0 && g.blim == 1 && g.wshift == __builtin_ctz(BN)) {
+    // mode-1 form: the tensor through a 2-D tensor map (falls through to cp.async if the driver
+    // cannot encode one)
+    CUtensorMap amap;
+    if (encode_colm_tmap(&amap, g.A, g.rows, g.lda, g.K, BM)) {
+      auto ckern = zgemm_tmap_colm_kernel<BM, BN, BK, WM, WN, TST, MINB>;
+      constexpr size_t csmem = (size_t)TST * (BM * BK + PCfg::kStageB) * sizeof(double2) + 128;
+      smem_optin(ckern, csmem);
+      ckern<<<(unsigned)tiles, PCfg::kThreads, csmem, stream>>>(g, amap);
+      NDS_LAUNCH_CHECK();
+      return;
+    }
+  }
   if (tma && !tma_padded(g.K))  // short K: the swizzled images of that factor, 4-stage ring
     skern<<<(unsigned)tiles, SCfg::kThreads, SCfg::kSmem, stream>>>(g);
   else if (tma)
@@ -731,9 +896,13 @@ void blocked_layouts_launch(FactorSet& f, double2* base, cudaStream_t stream, in
         ablk_kernel<<<(unsigned)std::min<int64_t>((na + 255) / 256, 1024), 256, 0, stream>>>(mrow, n, bm, p, na);
         NDS_LAUNCH_CHECK();
         p += na;
-        // the mode-1 (column-major) form keeps the cp.async kernel, so its B images are not built
+        // the mode-1 (column-major) form exists for the first mode only
         f.bblk[j][op][sh] = nullptr;
-        (void)mcol;
+        if (j == 0) {
+          f.bblk[j][op][sh] = p;
+          bblk_kernel<<<(unsigned)std::min<int64_t>((nb + 255) / 256, 1024), 256, 0, stream>>>(mcol, n, bn, p, nb);
+          NDS_LAUNCH_CHECK();
+        }
         p += nb;
       }
     }
