@@ -464,7 +464,7 @@ def main():
         achieved = sum(flops) / sum(ms for _, ms in gemm) / 1e9  # TFLOP/s (flop/ms / 1e9)
         traffic = ncu_traffic(args.config)
         roofline = {"bound": "tensor", "pipe": "FP64 DMMA (mma.sync.m8n8k4.f64)",
-                    "kernel": "zgemm_tma_kernel (modes >= 2, bulk-copy fed) / zgemm_dmma_kernel (mode 1)",
+                    "kernel": "zgemm_tma_kernel (modes >= 2, bulk-copy fed) / zgemm_tmap_colm_kernel (mode 1, tensor-map TMA)",
                     "achieved": round(achieved, 3), "peak": peak_tf, "unit": "TFLOP/s",
                     "frac": round(achieved / peak_tf, 4), "traffic": traffic,
                     "flops_per_launch": flops[0], "avg_launch_ms": avg_ms,
@@ -508,7 +508,7 @@ def main():
     if gemm:
         g_ms = sum(ms for _, ms in gemm) / args.steps
         g_fl = sum(8.0 * P * dims[abs(m) - 1] for m, _ in gemm) / args.steps
-        per_kernel.append({"kernel": "transform GEMM (zgemm_tma / zgemm_dmma)", "launches_per_step": len(gemm) // args.steps,
+        per_kernel.append({"kernel": "transform GEMM (zgemm_tma / zgemm_tmap_colm)", "launches_per_step": len(gemm) // args.steps,
                            "ms_per_step": round(g_ms, 4), "achieved": round(g_fl / (g_ms * 1e-3) / 1e12, 3),
                            "unit": "TFLOP/s", "peak": peak_tf, "frac": round(g_fl / (g_ms * 1e-3) / 1e12 / peak_tf, 4),
                            "bound": "FP64 tensor (DMMA)"})
