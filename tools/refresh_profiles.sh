@@ -18,7 +18,7 @@ timeout 300 python tools/gpu/plan_timing.py c1 c2 c3 c4 > $O/plan_timing.txt 2>&
 timeout 400 ncu --metrics gpu__time_duration.sum --clock-control none --csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-verify > $O/launches_c1.csv 2> $O/launches_c1.err
 NCU="ncu --set full --clock-control none --import-source on"
 P="python tools/profile_step.py --reps 1"
-timeout 400 $NCU -k regex:zgemm_tma -s 1 -c 1 -o $O/zgemm_tma_c1 $P --config c1 > /dev/null 2>&1
+timeout 400 $NCU -k regex:zgemm_tma_kernel -s 1 -c 1 -o $O/zgemm_tma_c1 $P --config c1 > /dev/null 2>&1
 timeout 400 $NCU -k regex:zgemm_tmap_colm -s 0 -c 1 -o $O/zgemm_tmap_colm_c1 $P --config c1 > /dev/null 2>&1
 # blk_level_kernel: c1 has 3 levels per solve (2 warm-up solves + 1): -s 7 = level 1 of the last
 timeout 400 $NCU -k regex:blk_level -s 7 -c 1 -o $O/blk_c1_l1 $P --config c1 > /dev/null 2>&1
