@@ -493,8 +493,9 @@ __global__ void __launch_bounds__(WM* WN * 32, MINB)
   const int lane = tid & 31, warp = tid >> 5;
   const int wy = warp / WN, wx = warp % WN;
   const int64_t tile = blockIdx.x;
-  const int64_t row_tile = tile % g.ntile_rows;
-  const int64_t ct = tile / g.ntile_rows;  // column tile of M^T (blim = 1)
+  // column tiles fastest: the CTAs sharing a row tile of the tensor run together (tensor read once)
+  const int64_t row_tile = tile / g.ntile_a;
+  const int64_t ct = tile % g.ntile_a;  // column tile of M^T (blim = 1)
   const int64_t row0 = row_tile * BM;
   const int64_t a0 = ct * BN;
   const int nk = g.K / BK;
